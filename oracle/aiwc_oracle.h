@@ -1,0 +1,32 @@
+/* aiwc_oracle.h -- TEST INFRASTRUCTURE ONLY (see aiwc_oracle.c). */
+#ifndef AIWC_ORACLE_H
+#define AIWC_ORACLE_H
+#include <stdint.h>
+
+typedef struct {
+  uint32_t n_opcodes;    /* opcode dictionary size */
+  uint32_t history_len;  /* branch history bits, 0 -> 16 (entropy.py:16) */
+  uint64_t entry_cap;    /* TraceTooLarge cap (metrics.py:54-57); 0 = unlimited */
+} oracle_params;
+
+typedef struct {
+  uint64_t n, min, max, sum, mid_lo, mid_hi; /* mid_lo/hi: ranks (n-1)/2 and n/2 */
+} oracle_dist;
+
+typedef struct {
+  int status;               /* 0 ok, 1 TraceTooLarge, 2 malformed columnar input */
+  uint64_t entries_at_fail;
+  uint64_t total_instructions, work_items, barriers, opcode_cov;
+  oracle_dist itb, ipt;
+  uint64_t n_widths;        /* width Counter in insertion order */
+  uint64_t *width_vals, *width_counts;
+  uint64_t footprint, footprint90, unique_reads, unique_writes, total_reads, total_writes;
+  double gmae, lmae[10];
+  uint64_t n_sites, branch90, executions, excluded, observations;
+  double yokota, linear;
+} oracle_result;
+
+int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
+               const oracle_params *p, oracle_result *r);
+void oracle_free(oracle_result *r);
+#endif
