@@ -1,0 +1,318 @@
+"""Benchmark: trace events/s for the full AIWC metric vector (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2]
+
+One step = one pass of the hot path (aiwc_reset + aiwc_ingest + aiwc_finalize:
+every report field) over one synthetic trace resident in HBM.  The N=1
+workload is BASELINE configs[1] (C2, 256 M-event kmeans-like streaming trace,
+2^23 work-items, local 256).  `value` is events/s with the trace already on
+the device; `e2e` is the same metric through the public Python API
+(`consume` + `finalize`) from pinned HOST columns, H2D and the result D2H
+inside the timed region.  The trace (2.4 GB) is larger than L2, so no L2 flush
+is needed between steps.
+
+`--impl reference` times the reference algorithm's CPU restatement
+(oracle/aiwc_oracle.c; the Python reference cannot travel to the GPU box) on a
+bounded prefix of the same trace, on rank 0 only.
+
+Under torchrun (N>1) every rank processes its own work-group shard of an
+N-times larger trace (weak scaling) and the per-rank reductions are combined
+over NCCL (paper_1805_04207_b200/dist.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace events/sec (full AIWC metric vector)"
+UNIT = "events/s"
+ALG_BYTES_PER_EVENT = 9  # one kind byte + one payload u64
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fp:
+            return json.load(fp)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) == 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def _dist_env():
+    return int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the C restatement of the reference path on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args) -> None:
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1805_04207_b200 import synth
+
+    oracle.build()
+    cfg = args.config
+    w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
+    # bounded sample: the first whole work-groups of the same trace (a valid trace)
+    sample_wi = min(w, args.ref_sample_wi)
+    tr = synth.python_trace(cfg, sample_wi) if args.ref_python_gen else None
+    if tr is None:
+        import torch
+
+        torch.cuda.set_device(0)
+        tr = synth.device_trace(cfg, sample_wi).to_numpy()
+    kind, payload = tr.kind, tr.payload.view(np.uint64)
+    n = int(kind.shape[0])
+    for _ in range(args.warmup):
+        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+        times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    v = n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
+        "config": {"workload": f"C{cfg} {synth.NAMES[cfg]} prefix of {sample_wi} work-items ({n} events)",
+                   "full_workload_work_items": w},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"first {sample_wi} work-items of C{cfg} ({n} events), oracle/aiwc_oracle.c, "
+                                   "single-threaded restatement of consume+finalize"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    from paper_1805_04207_b200 import _native, consume, finalize, synth
+    from paper_1805_04207_b200.metrics import trace_info
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = args.config
+    w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
+    # weak scaling: rank r owns work-groups [r*G, (r+1)*G) of a world*w work-item trace
+    tr = synth.device_trace(cfg, w)
+    n = tr.n_events
+    stream = torch.cuda.current_stream(dev)
+    ctx = _native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING)
+    lib = ctx.lib
+    info = trace_info(tr)
+    kptr = ctypes.c_void_p(tr.kind.data_ptr())
+    pptr = ctypes.c_void_p(tr.payload.data_ptr())
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    res = _native.Result()
+
+    def step():
+        ctx.check(lib.aiwc_reset(ctx.h))
+        ctx.check(lib.aiwc_ingest(ctx.h, kptr, pptr, ctypes.byref(info), sptr))
+        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), sptr))
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = {p: [] for p in _native.PHASES}
+    kernels = 0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record(stream)
+        for _ in range(args.steps):
+            step()
+            for i, p in enumerate(_native.PHASES):
+                phases[p].append(res.phase_ms[i])
+            kernels += res.kernels_launched
+        end.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = n * world / (ms_step / 1e3)
+
+    # ---- e2e: public API from pinned host columns ----
+    hk = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    hp = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    hk.copy_(tr.kind)
+    hp.copy_(tr.payload)
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    host_tr = ColumnarTrace(hk, hp, tr.kernel_name, 0, tr.global_size, tr.local_size, tr.opcodes, [], tr.addr_stats)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        finalize(consume(host_tr, max_entries=1 << 62, device=local))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    for _ in range(e2e_steps):
+        rep = finalize(consume(host_tr, max_entries=1 << 62, device=local))
+    e_end.record()
+    torch.cuda.synchronize()
+    e2e_ms = max(e_start.elapsed_time(e_end), (time.perf_counter() - t0) * 1e3) / e2e_steps
+    d2h = res.d2h_bytes
+    e2e_value = n * world / (e2e_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (the ingest pass) ----
+    peaks = measured_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    ingest_ms = statistics.median(phases["ingest"])
+    achieved = ALG_BYTES_PER_EVENT * n / (ingest_ms / 1e3) / 1e9
+    step_alg = ALG_BYTES_PER_EVENT * n / (ms_step / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, w, args)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
+            "config": {"workload": f"C{cfg} {synth.NAMES[cfg]}: {w} work-items x {world} ranks, "
+                                   f"{n} events per rank, local 256" if cfg != 1 else f"C1 sweep4 {w} work-items",
+                       "events_per_rank": n, "l2": "trace (9 B/event) larger than L2; no flush needed",
+                       "parallelism": f"work-group shards x{world}"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * n, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms, "path": "consume(ColumnarTrace on pinned host)+finalize"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None, "kernel": "aiwc::ingest_kernel<true>",
+                         "peak_source": peak_src, "alg_bytes_per_event": ALG_BYTES_PER_EVENT,
+                         "step_alg_gbs": step_alg, "step_frac": step_alg / peak},
+            "phases_ms": {p: statistics.median(v) for p, v in phases.items()},
+            "gpu_launches": kernels,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "report_check": {"total_memory_footprint": rep.total_memory_footprint, "gmae": rep.gmae,
+                             "footprint_90": rep.footprint_90},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def cpu_baseline(cfg, w, args):
+    """Oracle (C restatement of the reference path) on a bounded prefix, rank 0 only."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_1805_04207_b200 import synth
+
+    try:
+        oracle.build()
+        sample_wi = min(w, args.ref_sample_wi)
+        tr = synth.device_trace(cfg, sample_wi).to_numpy()
+        kind, payload = tr.kind, tr.payload.view(np.uint64)
+        t0 = time.perf_counter()
+        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+        dt = time.perf_counter() - t0
+        return {"value": kind.shape[0] / dt, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"first {sample_wi} work-items of C{cfg} ({kind.shape[0]} events), oracle/aiwc_oracle.c"}
+    except Exception as exc:  # pragma: no cover
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--work-items", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-sample-wi", type=int, default=1 << 21)
+    ap.add_argument("--ref-python-gen", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

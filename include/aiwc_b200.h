@@ -1,0 +1,161 @@
+/*
+ * aiwc_b200.h -- C ABI of the B200-native AIWC metric engine.
+ *
+ * Replaces the reference's metric hot path (pure Python):
+ *   aiwc.metrics.consume   pkg/src/aiwc/metrics.py:98-196   -> aiwc_reset + aiwc_ingest
+ *   aiwc.metrics.finalize  pkg/src/aiwc/metrics.py:273-386  -> aiwc_finalize
+ *   aiwc.entropy.*         pkg/src/aiwc/entropy.py:20-133   (inside aiwc_finalize)
+ *   aiwc.errors.InvalidStream / TraceTooLarge / AiwcError    -> AIWC_ERR_* codes + aiwc_last_error
+ * The Python mirror (paper_1805_04207_b200.metrics) binds these with ctypes;
+ * INTEGRATION.md shows the binding a maintainer of the reference would add.
+ *
+ * Plain C types only.  Device pointers are CUDA global-memory addresses on the
+ * ctx's device; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  One ctx per trace stream: a ctx is not thread-safe,
+ * distinct ctxs are.  The ctx owns all scratch memory; the caller owns the
+ * trace buffers until the call that received them returns.
+ */
+#ifndef AIWC_B200_H
+#define AIWC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AIWC_ABI_VERSION 1
+
+/* ---- columnar trace layout: one kind byte + one payload u64 per event ----
+ * bit0 instr, bit1 read, bit2 write, bit3 branch, bit4 work-item boundary,
+ * bit5 segment open (with bit4), bit6 work-group, bit7 variant.            */
+enum {
+  AIWC_K_PAD = 0x00,          /* no event (padding); never produced by encoders */
+  AIWC_K_INSTR = 0x01,        /* payload = opcode_id << 32 | width             */
+  AIWC_K_LOAD = 0x02,         /* payload = address                             */
+  AIWC_K_ATOMIC_LOAD = 0x82,
+  AIWC_K_STORE = 0x04,
+  AIWC_K_ATOMIC_STORE = 0x84,
+  AIWC_K_BRANCH = 0x08,       /* payload = site << 1 | taken, site < 2^32       */
+  AIWC_K_WI_END = 0x10,       /* payload = local linear id                     */
+  AIWC_K_BARRIER = 0x90,
+  AIWC_K_WI_BEGIN = 0x30,     /* payload = local linear id                     */
+  AIWC_K_WI_RESUME = 0xB0,    /* payload = local linear id                     */
+  AIWC_K_WG_BEGIN = 0x40,     /* payload = group key (< 2^31, injective)       */
+  AIWC_K_WG_END = 0xC0,
+  AIWC_K_KERNEL_BEGIN = 0x20,
+  AIWC_K_KERNEL_END = 0xA0
+};
+
+/* ---- return codes (0 = success) ---- */
+enum {
+  AIWC_OK = 0,
+  AIWC_ERR_INVALID_STREAM = 1, /* aiwc.errors.InvalidStream  (errors.py:70-79)  */
+  AIWC_ERR_TOO_LARGE = 2,      /* aiwc.errors.TraceTooLarge  (errors.py:82-89)  */
+  AIWC_ERR_INCONSISTENT = 3,   /* aiwc.errors.AiwcError      (metrics.py:276-285) */
+  AIWC_ERR_UNSUPPORTED = 4,    /* value outside the columnar format's range      */
+  AIWC_ERR_ARGUMENT = 5,       /* bad argument / misaligned buffer / wrong state */
+  AIWC_ERR_CUDA = 6,           /* CUDA runtime / driver failure                  */
+  AIWC_ERR_NCCL = 7
+};
+
+typedef struct aiwc_ctx aiwc_ctx;
+
+/* aiwc_opts.flags */
+#define AIWC_OPT_NO_CONSERVATION 1u /* skip finalize's conservation checks (caller does them) */
+#define AIWC_OPT_TIMING 2u          /* record CUDA events around each phase (aiwc_result.phase_ms) */
+
+/* aiwc_result.phase_ms indices */
+enum { AIWC_PH_PASS1 = 0, AIWC_PH_INGEST = 1, AIWC_PH_MEMORY = 2, AIWC_PH_BRANCH = 3, AIWC_PH_INGEST_TOTAL = 4,
+       AIWC_PH_FINALIZE_TOTAL = 5, AIWC_N_PHASES = 8 };
+
+typedef struct {
+  uint32_t history_len;       /* branch history bits, 1..16; 0 -> 16 (entropy.py:16)   */
+  uint32_t flags;             /* AIWC_OPT_*                                            */
+  uint64_t entry_cap;         /* TraceTooLarge cap in entries; 0 = unlimited           */
+  uint64_t dense_budget_bytes;/* max bytes for the dense address table; 0 = default    */
+} aiwc_opts;
+
+/* Per-trace description passed with the columns. */
+typedef struct {
+  uint64_t n_events;
+  uint32_t local_volume;      /* product of the launch's local size                   */
+  uint32_t n_opcodes;         /* opcode dictionary size                               */
+  uint32_t has_addr_stats;    /* 1 when addr_* below describe every memory address    */
+  uint32_t reserved;
+  uint64_t addr_min, addr_max, addr_and, addr_or;
+} aiwc_trace_info;
+
+typedef struct {
+  uint64_t n, min, max, sum;  /* sample count, extremes, exact sum                    */
+  uint64_t mid_lo, mid_hi;    /* order statistics at ranks (n-1)/2 and n/2            */
+} aiwc_dist;
+
+/* Exact integers plus unrounded fp64 entropies; the host finishes reals with
+ * the reference's expressions and round12 (metrics.py:287-386).  Array
+ * pointers reference ctx-owned host memory valid until the next call on ctx. */
+typedef struct {
+  uint64_t n_events;
+  uint64_t total_instructions, work_items, barriers_hit;
+  uint64_t opcode_coverage;                 /* coverage_count(opcodes, 0.9)              */
+  aiwc_dist itb, ipt;
+  uint64_t total_reads, total_writes, unique_reads, unique_writes;
+  uint64_t footprint, footprint_90;
+  double gmae, lmae[10];                    /* -sum p log2 p, levels 0 and 1..10         */
+  uint64_t branch_executions, branch_observations, branch_excluded;
+  uint64_t n_sites, branch_90;
+  double yokota, linear;
+  uint64_t entries;                         /* unique reads + unique writes + branches  */
+  uint32_t n_opcodes;  const uint64_t *opcode_counts;                 /* by opcode id   */
+  uint32_t n_widths;   const uint64_t *width_values, *width_counts;   /* first-seen order */
+  uint32_t n_site_list; const uint64_t *site_ids, *site_counts;      /* ascending site  */
+  uint32_t used_dense_table;                /* memory path taken (diagnostics)          */
+  uint32_t kernels_launched;                /* engine kernels launched for this trace   */
+  uint64_t d2h_bytes;                       /* device->host bytes read for this trace   */
+  double phase_ms[AIWC_N_PHASES];           /* with AIWC_OPT_TIMING: CUDA-event times   */
+} aiwc_result;
+
+typedef struct {
+  int32_t code;
+  int64_t event_index;        /* InvalidStream: first offending event              */
+  char rule[48];              /* InvalidStream rule id (trace.py:278-286)           */
+  uint64_t entries, cap;      /* TraceTooLarge                                      */
+  char message[256];
+} aiwc_error;
+
+int  aiwc_abi_version(void);
+int  aiwc_ctx_create(aiwc_ctx **out, int device, const aiwc_opts *opts);
+void aiwc_ctx_destroy(aiwc_ctx *ctx);
+
+/* Start a new accumulator (one kernel invocation) in ctx. */
+int  aiwc_reset(aiwc_ctx *ctx);
+
+/* consume(): fold one trace resident in device memory (16-byte aligned
+ * columns) into the ctx accumulator.  Asynchronous w.r.t. the host except for
+ * one small device->host read of the column counts. */
+int  aiwc_ingest(aiwc_ctx *ctx, const uint8_t *kind_dev, const uint64_t *payload_dev,
+                 const aiwc_trace_info *info, void *stream);
+
+/* Same as aiwc_ingest from HOST columns (pinned or pageable): copies to the
+ * ctx's device staging buffers on `stream` first. */
+int  aiwc_ingest_host(aiwc_ctx *ctx, const uint8_t *kind_host, const uint64_t *payload_host,
+                      const aiwc_trace_info *info, void *stream);
+
+/* finalize(): every metric of the accumulator; synchronizes `stream`. */
+int  aiwc_finalize(aiwc_ctx *ctx, aiwc_result *out, void *stream);
+
+/* Details of the last non-zero return on ctx. */
+int  aiwc_last_error(const aiwc_ctx *ctx, aiwc_error *err);
+
+/* Device-side synthetic trace generators.
+ * Writes n events starting at event index `first` of config `cfg` into the
+ * device columns; aiwc_synth_size returns the config's total event count and
+ * fills info (opcode count, local volume, exact address statistics). */
+uint64_t aiwc_synth_size(int cfg, uint64_t work_items, aiwc_trace_info *info);
+int  aiwc_synth_fill(int cfg, uint64_t work_items, uint64_t seed, uint8_t *kind_dev,
+                     uint64_t *payload_dev, uint64_t first, uint64_t n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AIWC_B200_H */

@@ -1,0 +1,35 @@
+"""B200-native AIWC metric path (arXiv:1805.04207).
+
+Drop-in for the reference package's trace -> feature-vector path: the same
+TraceEvent vocabulary, ``consume`` / ``finalize`` / ``merge_accumulators``,
+``AiwcReport`` schema and exceptions, computed by hand-written sm_100a CUDA
+kernels in ``libaiwc_b200.so`` behind a C ABI (include/aiwc_b200.h).
+"""
+
+from .errors import (
+    AiwcError, DeviceError, EmptyHistogram, EmptySample, IncompatibleReports, InvalidSkip, InvalidStream,
+    MalformedEvent, NoBranches, SchemaError, TraceTooLarge, UnsupportedTrace,
+)
+from .metrics import (
+    DistStats, KernelAccumulator, consume, default_entry_cap, finalize, lmae_profile, merge_accumulators,
+    summarize_distribution,
+)
+from .report import (
+    AiwcReport, DerivedMetrics, derive, emit_report, load_report, report_from_dict, report_to_dict, round12,
+)
+from .trace import (
+    Barrier, Branch, ColumnarTrace, Instruction, KernelBegin, KernelEnd, Memory, TraceEvent, WorkGroupBegin,
+    WorkGroupEnd, WorkItemBegin, WorkItemEnd, WorkItemId, WorkItemResume,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AiwcError", "AiwcReport", "Barrier", "Branch", "ColumnarTrace", "DerivedMetrics", "DeviceError", "DistStats",
+    "EmptyHistogram", "EmptySample", "IncompatibleReports", "Instruction", "InvalidSkip", "InvalidStream",
+    "KernelAccumulator", "KernelBegin", "KernelEnd", "MalformedEvent", "Memory", "NoBranches", "SchemaError",
+    "TraceEvent", "TraceTooLarge", "UnsupportedTrace", "WorkGroupBegin", "WorkGroupEnd", "WorkItemBegin",
+    "WorkItemEnd", "WorkItemId", "WorkItemResume", "consume", "default_entry_cap", "derive", "emit_report",
+    "finalize", "lmae_profile", "load_report", "merge_accumulators", "report_from_dict", "report_to_dict",
+    "round12", "summarize_distribution",
+]

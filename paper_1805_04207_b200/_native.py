@@ -1,0 +1,161 @@
+"""ctypes binding of libaiwc_b200.so (include/aiwc_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is present,
+every entry point raises ``DeviceError``.  Return codes map 1:1 onto the
+reference's exceptions (``pkg/src/aiwc/errors.py``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import AiwcError, DeviceError, InvalidStream, TraceTooLarge, UnsupportedTrace
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libaiwc_b200.so")
+
+OK, ERR_INVALID_STREAM, ERR_TOO_LARGE, ERR_INCONSISTENT, ERR_UNSUPPORTED, ERR_ARGUMENT, ERR_CUDA, ERR_NCCL = range(8)
+OPT_NO_CONSERVATION = 1  # Python's finalize() runs the reference's conservation checks itself
+
+u8p = ctypes.POINTER(ctypes.c_uint8)
+u64p = ctypes.POINTER(ctypes.c_uint64)
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("history_len", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+                ("entry_cap", ctypes.c_uint64), ("dense_budget_bytes", ctypes.c_uint64)]
+
+
+class TraceInfo(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_uint64), ("local_volume", ctypes.c_uint32), ("n_opcodes", ctypes.c_uint32),
+                ("has_addr_stats", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("addr_min", ctypes.c_uint64), ("addr_max", ctypes.c_uint64),
+                ("addr_and", ctypes.c_uint64), ("addr_or", ctypes.c_uint64)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("n", "min", "max", "sum", "mid_lo", "mid_hi")]
+
+
+class Result(ctypes.Structure):
+    _fields_ = [
+        ("n_events", ctypes.c_uint64),
+        ("total_instructions", ctypes.c_uint64), ("work_items", ctypes.c_uint64), ("barriers_hit", ctypes.c_uint64),
+        ("opcode_coverage", ctypes.c_uint64),
+        ("itb", Dist), ("ipt", Dist),
+        ("total_reads", ctypes.c_uint64), ("total_writes", ctypes.c_uint64),
+        ("unique_reads", ctypes.c_uint64), ("unique_writes", ctypes.c_uint64),
+        ("footprint", ctypes.c_uint64), ("footprint_90", ctypes.c_uint64),
+        ("gmae", ctypes.c_double), ("lmae", ctypes.c_double * 10),
+        ("branch_executions", ctypes.c_uint64), ("branch_observations", ctypes.c_uint64),
+        ("branch_excluded", ctypes.c_uint64), ("n_sites", ctypes.c_uint64), ("branch_90", ctypes.c_uint64),
+        ("yokota", ctypes.c_double), ("linear", ctypes.c_double),
+        ("entries", ctypes.c_uint64),
+        ("n_opcodes", ctypes.c_uint32), ("opcode_counts", u64p),
+        ("n_widths", ctypes.c_uint32), ("width_values", u64p), ("width_counts", u64p),
+        ("n_site_list", ctypes.c_uint32), ("site_ids", u64p), ("site_counts", u64p),
+        ("used_dense_table", ctypes.c_uint32), ("kernels_launched", ctypes.c_uint32),
+        ("d2h_bytes", ctypes.c_uint64), ("phase_ms", ctypes.c_double * 8),
+    ]
+
+
+OPT_TIMING = 2
+PHASES = ("pass1", "ingest", "memory", "branch", "ingest_total", "finalize_total")
+
+
+class Error(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_int32), ("event_index", ctypes.c_int64), ("rule", ctypes.c_char * 48),
+                ("entries", ctypes.c_uint64), ("cap", ctypes.c_uint64), ("message", ctypes.c_char * 256)]
+
+
+EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
+           "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill")
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libaiwc_b200.so and declare signatures (no device needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError(f"native engine {path} is not built (run __graft_entry__.build())")
+        lib = ctypes.CDLL(path)
+        vp = ctypes.c_void_p
+        lib.aiwc_abi_version.restype = ctypes.c_int
+        lib.aiwc_ctx_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int, ctypes.POINTER(Opts)]
+        lib.aiwc_ctx_destroy.argtypes = [vp]
+        lib.aiwc_ctx_destroy.restype = None
+        lib.aiwc_reset.argtypes = [vp]
+        lib.aiwc_ingest.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), vp]
+        lib.aiwc_ingest_host.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), vp]
+        lib.aiwc_finalize.argtypes = [vp, ctypes.POINTER(Result), vp]
+        lib.aiwc_last_error.argtypes = [vp, ctypes.POINTER(Error)]
+        lib.aiwc_synth_size.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(TraceInfo)]
+        lib.aiwc_synth_size.restype = ctypes.c_uint64
+        lib.aiwc_synth_fill.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp, vp, ctypes.c_uint64,
+                                        ctypes.c_uint64, vp]
+        for name in ("aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
+                     "aiwc_last_error", "aiwc_synth_fill"):
+            getattr(lib, name).restype = ctypes.c_int
+        if lib.aiwc_abi_version() != 1:
+            raise DeviceError("libaiwc_b200.so ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+class Context:
+    """One aiwc_ctx (one accumulator at a time) on one CUDA device."""
+
+    def __init__(self, device: int = 0, *, entry_cap: int = 0, history_len: int = 16,
+                 flags: int = OPT_NO_CONSERVATION):
+        self.lib = load_library()
+        self.device = device
+        self.entry_cap = entry_cap
+        opts = Opts(history_len, flags, entry_cap, 0)
+        h = ctypes.c_void_p()
+        rc = self.lib.aiwc_ctx_create(ctypes.byref(h), device, ctypes.byref(opts))
+        self.h = h
+        if rc != OK:
+            msg = self._message() if h.value else f"aiwc_ctx_create failed with code {rc}"
+            self.close()
+            raise DeviceError(msg)
+
+    def _message(self) -> str:
+        e = Error()
+        self.lib.aiwc_last_error(self.h, ctypes.byref(e))
+        return e.message.decode(errors="replace")
+
+    def check(self, rc: int) -> None:
+        if rc == OK:
+            return
+        e = Error()
+        self.lib.aiwc_last_error(self.h, ctypes.byref(e))
+        msg = e.message.decode(errors="replace")
+        if rc == ERR_TOO_LARGE:
+            raise TraceTooLarge(e.entries, e.cap)
+        if rc == ERR_INVALID_STREAM:
+            raise InvalidStream(e.event_index, e.rule.decode(), msg)
+        if rc == ERR_INCONSISTENT:
+            raise AiwcError(msg)
+        if rc == ERR_UNSUPPORTED:
+            raise UnsupportedTrace(msg)
+        if rc == ERR_ARGUMENT:
+            raise AiwcError(msg)
+        raise DeviceError(msg)
+
+    def close(self) -> None:
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.aiwc_ctx_destroy(self.h)
+        self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

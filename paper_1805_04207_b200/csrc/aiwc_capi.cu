@@ -1,0 +1,644 @@
+// aiwc_capi.cu -- the C ABI (include/aiwc_b200.h): context, buffers, the
+// ingest / finalize orchestration and the exact-integer host finishing
+// (coverage counts, order statistics) of pkg/src/aiwc/metrics.py:273-386.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "aiwc_util.cuh"
+
+using namespace aiwc;
+
+namespace {
+
+struct Buf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+cudaError_t grow(Buf& b, size_t bytes) {
+  if (bytes <= b.cap && b.p) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  bytes = std::max<size_t>(bytes, 256);
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e == cudaSuccess) b.cap = bytes;
+  return e;
+}
+
+template <typename T>
+T* P(Buf& b) { return reinterpret_cast<T*>(b.p); }
+
+int bitwidth64(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+__global__ void init_state_kernel(DevState* st) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(st);
+  const size_t n = sizeof(DevState) / 8;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) w[i] = 0;
+}
+// separate launch so the sentinels land after every block finished zeroing
+__global__ void init_sentinels_kernel(DevState* st) {
+  st->addr_min = ~0ull;
+  st->addr_and = ~0ull;
+}
+
+__global__ void widen_u32_kernel(const uint32_t* src, uint64_t n, uint64_t* dst) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+struct aiwc_ctx {
+  int device = 0;
+  int n_sms = 148;
+  aiwc_opts opts{};
+  aiwc_error err{};
+  int state = 0;  // 0 empty, 1 ingested, 2 finalized
+  Buf dev_state, ranges, opc, wcount, wfirst, itb_ovf, ipt_ovf, ipt_tab, dtab, rd, wr, br, partials, lvl0_ovf,
+      sparse_scr, branch_scr, branch_tab, kind_stage, pay_stage, sort_a, sort_b, sort_h;
+  DevState* h_state = nullptr;  // pinned
+  RangeSum* h_ranges = nullptr; // pinned
+  size_t h_ranges_cap = 0;
+  // per trace
+  aiwc_trace_info info{};
+  uint64_t n_instr = 0, n_rd = 0, n_wr = 0, n_br = 0, n_wgb = 0, n_wib = 0, n_wir = 0, n_wie = 0, n_bar = 0;
+  uint64_t n_events_seen = 0;
+  AddrMap am{};
+  bool dense = false;
+  uint64_t ipt_tab_len = 0;
+  uint32_t n_ranges = 0, tiles_per_cta = 0;
+  uint32_t kernels = 0;
+  uint32_t n_parts = 0;
+  uint64_t d2h = 0;
+  // optional phase timing (AIWC_OPT_TIMING): pairs of events per phase
+  cudaEvent_t ev[2 * AIWC_N_PHASES] = {};
+  bool timing = false;
+  uint32_t marked = 0;  // phases whose end event was recorded for the current trace
+  void mark(int phase, int end, cudaStream_t s) {
+    if (!timing) return;
+    cudaEventRecord(ev[2 * phase + end], s);
+    if (end) marked |= 1u << phase;
+  }
+  // host results
+  std::vector<uint64_t> opc_counts, width_vals, width_counts, site_ids, site_counts;
+  std::vector<uint64_t> itb_ovf_sorted, ipt_ovf_sorted, lvl0_sorted;
+};
+
+static int fail(aiwc_ctx* c, int code, const char* msg) {
+  if (c) {
+    c->err = aiwc_error{};
+    c->err.code = code;
+    c->err.event_index = -1;
+    snprintf(c->err.message, sizeof c->err.message, "%s", msg);
+  }
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      char m_[200];                                                                     \
+      snprintf(m_, sizeof m_, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return fail(ctx, AIWC_ERR_CUDA, m_);                                              \
+    }                                                                                   \
+  } while (0)
+
+extern "C" int aiwc_abi_version(void) { return AIWC_ABI_VERSION; }
+
+extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts) {
+  if (!out) return AIWC_ERR_ARGUMENT;
+  aiwc_ctx* ctx = new aiwc_ctx();
+  ctx->device = device;
+  if (opts) ctx->opts = *opts;
+  if (ctx->opts.history_len == 0) ctx->opts.history_len = 16;
+  if (ctx->opts.history_len > 16) {
+    delete ctx;
+    return AIWC_ERR_ARGUMENT;
+  }
+  *out = ctx;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device));
+  if (ctx->opts.dense_budget_bytes == 0) {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    ctx->opts.dense_budget_bytes = std::min<size_t>(fr / 4, 48ull << 30);
+  }
+  CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_state), sizeof(DevState)));
+  CK(grow(ctx->dev_state, sizeof(DevState)));
+  CK(grow(ctx->wcount, WIDTH_TABLE * 8));
+  CK(grow(ctx->wfirst, WIDTH_TABLE * 8));
+  ctx->n_parts = (uint32_t)ctx->n_sms * 4;
+  CK(grow(ctx->partials, (size_t)NLEVELS * ctx->n_parts * sizeof(double)));
+  CK(grow(ctx->branch_tab, (1u << 16) * 8));
+  if (ctx->opts.flags & AIWC_OPT_TIMING) {
+    ctx->timing = true;
+    for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+  }
+  return AIWC_OK;
+}
+
+extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  Buf* bufs[] = {&ctx->dev_state, &ctx->ranges, &ctx->opc, &ctx->wcount, &ctx->wfirst, &ctx->itb_ovf,
+                 &ctx->ipt_ovf, &ctx->ipt_tab, &ctx->dtab, &ctx->rd, &ctx->wr, &ctx->br, &ctx->partials,
+                 &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
+                 &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h};
+  for (Buf* b : bufs)
+    if (b->p) cudaFree(b->p);
+  if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  delete ctx;
+}
+
+extern "C" int aiwc_reset(aiwc_ctx* ctx) {
+  if (!ctx) return AIWC_ERR_ARGUMENT;
+  ctx->state = 0;
+  ctx->err = aiwc_error{};
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_last_error(const aiwc_ctx* ctx, aiwc_error* e) {
+  if (!ctx || !e) return AIWC_ERR_ARGUMENT;
+  *e = ctx->err;
+  return AIWC_OK;
+}
+
+static int encode_maps(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, uint64_t rows, CUtensorMap* km,
+                       CUtensorMap* pm) {
+  memset(km, 0, sizeof *km);
+  memset(pm, 0, sizeof *pm);
+  if (rows == 0) return AIWC_OK;
+  auto enc = get_encode();
+  if (!enc) return fail(ctx, AIWC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {16, rows};
+  cuuint32_t box[2] = {16, (cuuint32_t)(TILE / 16)};
+  cuuint32_t estr[2] = {1, 1};
+  cuuint64_t kstr[1] = {16};
+  CUresult r = enc(km, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(kind), dims, kstr, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, AIWC_ERR_CUDA, "tensor map (kind) encode failed");
+  cuuint64_t pstr[1] = {128};
+  r = enc(pm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(payload), dims, pstr, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(ctx, AIWC_ERR_CUDA, "tensor map (payload) encode failed");
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, const aiwc_trace_info* info,
+                           void* stream) {
+  if (!ctx || !info) return AIWC_ERR_ARGUMENT;
+  if (ctx->state != 0) return fail(ctx, AIWC_ERR_ARGUMENT, "ctx already holds a trace: call aiwc_reset first");
+  const uint64_t n = info->n_events;
+  if (n && (!kind || !payload)) return fail(ctx, AIWC_ERR_ARGUMENT, "null column pointer");
+  if ((reinterpret_cast<uintptr_t>(kind) & 15) || (reinterpret_cast<uintptr_t>(payload) & 15))
+    return fail(ctx, AIWC_ERR_ARGUMENT, "columns must be 16-byte aligned");
+  if (n >= (1ull << 32)) return fail(ctx, AIWC_ERR_UNSUPPORTED, "more than 2^32-1 events in one ingest");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  ctx->info = *info;
+  ctx->kernels = 0;
+  ctx->d2h = 0;
+  ctx->marked = 0;
+  ctx->mark(AIWC_PH_INGEST_TOTAL, 0, s);
+  DevState* st = P<DevState>(ctx->dev_state);
+  init_state_kernel<<<64, 256, 0, s>>>(st);
+  init_sentinels_kernel<<<1, 1, 0, s>>>(st);
+  ctx->kernels += 2;
+  CK(cudaMemsetAsync(ctx->wcount.p, 0, WIDTH_TABLE * 8, s));
+  CK(cudaMemsetAsync(ctx->wfirst.p, 0xFF, WIDTH_TABLE * 8, s));
+  const uint32_t n_opc = std::max<uint32_t>(info->n_opcodes, 1);
+  CK(grow(ctx->opc, (size_t)std::max<uint32_t>(n_opc, OBINS) * 8));
+  CK(cudaMemsetAsync(ctx->opc.p, 0, (size_t)std::max<uint32_t>(n_opc, OBINS) * 8, s));
+
+  // ---- pass 1: range summaries ----
+  const uint64_t n_tiles = (n + TILE - 1) / TILE;
+  uint32_t G = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)ctx->n_sms);
+  uint32_t tpc = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + G - 1) / G);
+  G = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + tpc - 1) / tpc);
+  ctx->n_ranges = G;
+  ctx->tiles_per_cta = tpc;
+  CK(grow(ctx->ranges, (size_t)G * sizeof(RangeSum)));
+  if (ctx->h_ranges_cap < G) {
+    if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
+    CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ranges), (size_t)G * sizeof(RangeSum)));
+    ctx->h_ranges_cap = G;
+  }
+  const bool with_stats = !info->has_addr_stats;
+  if (n) {
+    ctx->mark(AIWC_PH_PASS1, 0, s);
+    launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s);
+    ctx->mark(AIWC_PH_PASS1, 1, s);
+    ctx->kernels += 1;
+    CK(cudaGetLastError());
+  } else {
+    CK(cudaMemsetAsync(ctx->ranges.p, 0xFF, sizeof(RangeSum), s));
+  }
+  CK(cudaMemcpyAsync(ctx->h_ranges, ctx->ranges.p, (size_t)G * sizeof(RangeSum), cudaMemcpyDeviceToHost, s));
+  ctx->d2h += (size_t)G * sizeof(RangeSum);
+  if (with_stats) {  // addr_min .. addr_or are contiguous
+    CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 4 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    ctx->d2h += 4 * sizeof(unsigned long long);
+  }
+  CK(cudaStreamSynchronize(s));
+  ctx->n_instr = ctx->n_rd = ctx->n_wr = ctx->n_br = ctx->n_wgb = ctx->n_wib = ctx->n_wir = ctx->n_wie = ctx->n_bar = 0;
+  for (uint32_t i = 0; i < (n ? G : 0); ++i) {
+    const RangeSum& r = ctx->h_ranges[i];
+    ctx->n_instr += r.n_instr; ctx->n_rd += r.n_rd; ctx->n_wr += r.n_wr; ctx->n_br += r.n_br;
+    ctx->n_wgb += r.n_wgb; ctx->n_wib += r.n_wib; ctx->n_wir += r.n_wir; ctx->n_wie += r.n_wie; ctx->n_bar += r.n_bar;
+  }
+  ctx->n_events_seen = n;
+
+  // ---- memory path decision ----
+  const uint64_t M = ctx->n_rd + ctx->n_wr;
+  uint64_t amin, amax, aand, aor;
+  if (with_stats) {
+    amin = ctx->h_state->addr_min; amax = ctx->h_state->addr_max;
+    aand = ctx->h_state->addr_and; aor = ctx->h_state->addr_or;
+  } else {
+    amin = info->addr_min; amax = info->addr_max; aand = info->addr_and; aor = info->addr_or;
+  }
+  ctx->dense = false;
+  ctx->am = AddrMap{};
+  if (M) {
+    if (amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
+    AddrMap& am = ctx->am;
+    am.base = amin & ~1023ull;
+    am.hi = amax;
+    const uint64_t vary = aand ^ aor;
+    am.k = vary ? (uint32_t)__builtin_ctzll(vary) : 0u;
+    am.low_mask = am.k >= 64 ? ~0ull : ((1ull << am.k) - 1);
+    am.low_const = (amin - am.base) & am.low_mask;
+    const uint64_t span_keys = (amax - am.base) >> am.k;
+    am.n_keys = span_keys + 1;
+    const bool fits = span_keys < (1ull << 40) && am.n_keys * 8 <= ctx->opts.dense_budget_bytes &&
+                      am.n_keys <= 4 * M + (1ull << 20);
+    ctx->dense = fits;
+  }
+
+  // ---- buffers ----
+  const uint64_t n_itb_cap = ctx->n_bar + ctx->n_wie, n_ipt_cap = ctx->n_wie;
+  CK(grow(ctx->itb_ovf, std::max<uint64_t>(n_itb_cap, 1) * 4));
+  CK(grow(ctx->ipt_ovf, std::max<uint64_t>(n_ipt_cap, 1) * 4));
+  ctx->ipt_tab_len = 0;
+  if (ctx->n_bar + ctx->n_wir) {
+    ctx->ipt_tab_len = ctx->n_wgb * (uint64_t)std::max<uint32_t>(info->local_volume, 1);
+    CK(grow(ctx->ipt_tab, ctx->ipt_tab_len * 8));
+    CK(cudaMemsetAsync(ctx->ipt_tab.p, 0, ctx->ipt_tab_len * 8, s));
+  }
+  CK(grow(ctx->br, std::max<uint64_t>(ctx->n_br, 1) * 8));
+  if (M) {
+    if (ctx->dense) {
+      CK(grow(ctx->dtab, ctx->am.n_keys * 8));
+      CK(cudaMemsetAsync(ctx->dtab.p, 0, ctx->am.n_keys * 8, s));
+    } else {
+      CK(grow(ctx->rd, std::max<uint64_t>(ctx->n_rd, 1) * 8));
+      CK(grow(ctx->wr, std::max<uint64_t>(ctx->n_wr, 1) * 8));
+    }
+    CK(grow(ctx->lvl0_ovf, (M / CBINS + 2) * 8));
+  }
+
+  // ---- main ingest pass ----
+  if (n) {
+    CUtensorMap km, pm;
+    const uint64_t rows = n / 16;
+    int rc = encode_maps(ctx, kind, payload, rows, &km, &pm);
+    if (rc) return rc;
+    IngestArgs a{};
+    a.kind = kind; a.payload = payload; a.n = n; a.tma_rows = rows;
+    a.tiles_per_cta = tpc; a.n_opcodes = info->n_opcodes; a.local_volume = std::max<uint32_t>(info->local_volume, 1);
+    a.ranges = P<RangeSum>(ctx->ranges); a.st = st;
+    a.opc_counts = P<unsigned long long>(ctx->opc);
+    a.width_count = P<unsigned long long>(ctx->wcount); a.width_first = P<unsigned long long>(ctx->wfirst);
+    a.itb_ovf = P<uint32_t>(ctx->itb_ovf); a.ipt_ovf = P<uint32_t>(ctx->ipt_ovf);
+    a.ipt_tab = ctx->ipt_tab_len ? P<unsigned long long>(ctx->ipt_tab) : nullptr; a.ipt_tab_len = ctx->ipt_tab_len;
+    a.am = ctx->am;
+    a.dense = ctx->dense ? P<unsigned long long>(ctx->dtab) : nullptr;
+    a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
+    ctx->mark(AIWC_PH_INGEST, 0, s);
+    CK(launch_ingest(a, km, pm, G, ctx->dense, s));
+    ctx->mark(AIWC_PH_INGEST, 1, s);
+    ctx->kernels += 1;
+  }
+  ctx->mark(AIWC_PH_INGEST_TOTAL, 1, s);
+  ctx->state = 1;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_ingest_host(aiwc_ctx* ctx, const uint8_t* kind_host, const uint64_t* payload_host,
+                                const aiwc_trace_info* info, void* stream) {
+  if (!ctx || !info) return AIWC_ERR_ARGUMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint64_t n = info->n_events;
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->kind_stage, (n + 16) * 1));
+  CK(grow(ctx->pay_stage, (n + 16) * 8));
+  if (n) {
+    CK(cudaMemcpyAsync(ctx->kind_stage.p, kind_host, n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->pay_stage.p, payload_host, n * 8, cudaMemcpyHostToDevice, s));
+  }
+  return aiwc_ingest(ctx, P<uint8_t>(ctx->kind_stage), P<uint64_t>(ctx->pay_stage), info, stream);
+}
+
+// smallest k with the top-k counts covering >= 9/10 of the total (entropy.py:49-66),
+// counts given as a descending list of big values followed by a histogram of small ones
+static uint64_t coverage_from(const std::vector<uint64_t>& big_desc, const unsigned long long* small_hist,
+                              uint32_t n_small_bins, unsigned __int128 total) {
+  if (total == 0) return 0;
+  unsigned __int128 cum = 0;
+  uint64_t k = 0;
+  for (uint64_t c : big_desc) {
+    cum += c; ++k;
+    if (cum * 10 >= total * 9) return k;
+  }
+  for (int64_t c = (int64_t)n_small_bins - 1; c >= 1; --c) {
+    const uint64_t h = small_hist ? small_hist[c] : 0;
+    if (!h) continue;
+    const unsigned __int128 need = total * 9 - cum * 10;  // > 0 here
+    const unsigned __int128 per = (unsigned __int128)c * 10;
+    const unsigned __int128 take = (need + per - 1) / per;
+    if (take <= h) return k + (uint64_t)take;
+    cum += (unsigned __int128)h * c;
+    k += h;
+  }
+  return k;
+}
+
+static void order_stats(const unsigned long long* hist, const std::vector<uint64_t>& ovf_sorted, aiwc_dist* d) {
+  uint64_t small = 0;
+  for (int i = 0; i < HBINS; ++i) small += hist[i];
+  d->n = small + ovf_sorted.size();
+  if (!d->n) return;
+  auto at = [&](uint64_t rank) -> uint64_t {
+    if (rank >= small) return ovf_sorted[rank - small];
+    uint64_t c = 0;
+    for (int i = 0; i < HBINS; ++i) {
+      c += hist[i];
+      if (rank < c) return (uint64_t)i;
+    }
+    return 0;
+  };
+  d->min = at(0);
+  d->max = at(d->n - 1);
+  d->mid_lo = at((d->n - 1) / 2);
+  d->mid_hi = at(d->n / 2);
+}
+
+static int fetch_sorted_u32(aiwc_ctx* ctx, Buf& src, uint64_t n, std::vector<uint64_t>& out, cudaStream_t s) {
+  out.clear();
+  if (!n) return AIWC_OK;
+  CK(grow(ctx->sort_a, n * 8));
+  CK(grow(ctx->sort_b, n * 8));
+  CK(grow(ctx->sort_h, radix_hist_bytes(n)));
+  widen_u32_kernel<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 1024), 256, 0, s>>>(P<uint32_t>(src), n,
+                                                                                      P<uint64_t>(ctx->sort_a));
+  int k = 1;
+  radix_sort_u64(P<uint64_t>(ctx->sort_a), P<uint64_t>(ctx->sort_b), n, 0, 32, P<uint32_t>(ctx->sort_h), s, &k);
+  ctx->kernels += k;
+  out.resize(n);
+  CK(cudaMemcpyAsync(out.data(), ctx->sort_a.p, n * 8, cudaMemcpyDeviceToHost, s));
+  ctx->d2h += n * 8;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
+  if (!ctx || !out) return AIWC_ERR_ARGUMENT;
+  if (ctx->state != 1) return fail(ctx, AIWC_ERR_ARGUMENT, "finalize needs exactly one ingest since reset");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  DevState* st = P<DevState>(ctx->dev_state);
+  const uint64_t M = ctx->n_rd + ctx->n_wr;
+  ctx->mark(AIWC_PH_FINALIZE_TOTAL, 0, s);
+
+  // ---- device finishing: IPT slots, widths, memory ----
+  if (ctx->ipt_tab_len) {
+    launch_ipt_table(P<unsigned long long>(ctx->ipt_tab), ctx->ipt_tab_len, st, P<uint32_t>(ctx->ipt_ovf), s);
+    ctx->kernels += 1;
+  }
+  launch_width_list(P<unsigned long long>(ctx->wcount), P<unsigned long long>(ctx->wfirst), st, s);
+  ctx->kernels += 1;
+  ctx->mark(AIWC_PH_MEMORY, 0, s);
+  if (M) {
+    if (ctx->dense) {
+      const uint64_t chunks = (ctx->am.n_keys + 1023) / 1024;
+      const uint32_t nct = (uint32_t)std::min<uint64_t>(chunks, ctx->n_parts);
+      launch_dense_stats(P<unsigned long long>(ctx->dtab), ctx->am.n_keys, ctx->am.k, M, st,
+                         P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s);
+      launch_entropy_finish(st, P<double>(ctx->partials), nct, M, ctx->am.k, s);
+      ctx->kernels += 2;
+    } else {
+      CK(grow(ctx->sparse_scr, sparse_scratch_bytes(M)));
+      const int raw = bitwidth64((ctx->am.hi - ctx->am.base) >> ctx->am.k) > 63;
+      const uint32_t parts = std::min<uint32_t>(ctx->n_parts, 256);
+      ctx->kernels += sparse_memory_stats(P<uint64_t>(ctx->rd), ctx->n_rd, P<uint64_t>(ctx->wr), ctx->n_wr, ctx->am, M,
+                                          st, P<double>(ctx->partials), parts, P<uint64_t>(ctx->lvl0_ovf),
+                                          ctx->sparse_scr.p, ctx->sparse_scr.cap, s);
+      launch_entropy_finish(st, P<double>(ctx->partials), parts, M, raw ? 64u : ctx->am.k, s);
+      ctx->kernels += 1;
+    }
+  }
+  ctx->mark(AIWC_PH_MEMORY, 1, s);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
+  ctx->d2h += offsetof(DevState, host_end);
+  CK(cudaStreamSynchronize(s));
+
+  // ---- branches ----
+  if (ctx->n_br) {
+    const uint32_t site_bits = (uint32_t)bitwidth64(ctx->h_state->max_site);
+    CK(grow(ctx->branch_scr, branch_scratch_bytes(ctx->n_br)));
+    ctx->mark(AIWC_PH_BRANCH, 0, s);
+    ctx->kernels += branch_stats(P<uint64_t>(ctx->br), ctx->n_br, site_bits, ctx->opts.history_len, st,
+                                 P<unsigned long long>(ctx->branch_tab), ctx->branch_scr.p, ctx->branch_scr.cap, s);
+    ctx->mark(AIWC_PH_BRANCH, 1, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
+    ctx->d2h += offsetof(DevState, host_end);
+    CK(cudaStreamSynchronize(s));
+  }
+  DevState& h = *ctx->h_state;
+  if (h.flags) {
+    char m[160];
+    const char* what = (h.flags & F_ADDR_HINT) ? "memory address outside the declared address statistics"
+                       : (h.flags & F_BAD_OPCODE) ? "opcode id outside the opcode dictionary"
+                       : (h.flags & F_BAD_WIDTH)  ? "instruction width >= 65536 is not supported"
+                       : (h.flags & F_BAD_SITE)   ? "branch site >= 2^32 is not supported"
+                       : (h.flags & F_BAD_GROUP)  ? "group key >= 2^31 is not supported"
+                       : (h.flags & F_SLOT_RANGE) ? "work-item slot outside the group table (invalid stream)"
+                                                  : "unknown kind byte in the trace";
+    snprintf(m, sizeof m, "%s (flags=0x%llx)", what, (unsigned long long)h.flags);
+    const int code = (h.flags & (F_ADDR_HINT)) ? AIWC_ERR_ARGUMENT
+                     : (h.flags & (F_SLOT_RANGE | F_BAD_KIND)) ? AIWC_ERR_INCONSISTENT : AIWC_ERR_UNSUPPORTED;
+    return fail(ctx, code, m);
+  }
+
+  // ---- second-round small reads ----
+  int rc;
+  if ((rc = fetch_sorted_u32(ctx, ctx->itb_ovf, h.itb_ovf_n, ctx->itb_ovf_sorted, s))) return rc;
+  if ((rc = fetch_sorted_u32(ctx, ctx->ipt_ovf, h.ipt_ovf_n, ctx->ipt_ovf_sorted, s))) return rc;
+  ctx->lvl0_sorted.clear();
+  if (h.lvl0_ovf_n) {
+    const uint64_t L = h.lvl0_ovf_n;
+    CK(grow(ctx->sort_b, L * 8));
+    CK(grow(ctx->sort_h, radix_hist_bytes(L)));
+    int k = 0;
+    radix_sort_u64(P<uint64_t>(ctx->lvl0_ovf), P<uint64_t>(ctx->sort_b), L, 0, bitwidth64(M), P<uint32_t>(ctx->sort_h),
+                   s, &k);
+    ctx->kernels += k;
+    ctx->lvl0_sorted.resize(L);
+    CK(cudaMemcpyAsync(ctx->lvl0_sorted.data(), ctx->lvl0_ovf.p, L * 8, cudaMemcpyDeviceToHost, s));
+    ctx->d2h += L * 8;
+  }
+  const uint32_t n_opc = ctx->info.n_opcodes;
+  ctx->opc_counts.assign(n_opc, 0);
+  if (n_opc) CK(cudaMemcpyAsync(ctx->opc_counts.data(), ctx->opc.p, (size_t)n_opc * 8, cudaMemcpyDeviceToHost, s));
+  ctx->d2h += (size_t)n_opc * 8;
+  std::vector<unsigned long long> big_sites;
+  if (h.n_sites > (unsigned long long)MAX_SMALL_LIST) {
+    big_sites.resize(2 * h.n_sites);
+    // big list lives after the sort scratch inside branch_scr (see branch_stats)
+    const size_t off = ctx->n_br * 8 + ((radix_hist_bytes(ctx->n_br) + 15) & ~size_t(15));
+    CK(cudaMemcpyAsync(big_sites.data(), reinterpret_cast<uint8_t*>(ctx->branch_scr.p) + off, 2 * h.n_sites * 8,
+                       cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<unsigned long long> wc_full, wf_full;
+  if (h.n_widths_listed > (unsigned long long)MAX_SMALL_LIST) {
+    wc_full.resize(WIDTH_TABLE); wf_full.resize(WIDTH_TABLE);
+    CK(cudaMemcpyAsync(wc_full.data(), ctx->wcount.p, WIDTH_TABLE * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(wf_full.data(), ctx->wfirst.p, WIDTH_TABLE * 8, cudaMemcpyDeviceToHost, s));
+  }
+  ctx->mark(AIWC_PH_FINALIZE_TOTAL, 1, s);
+  CK(cudaStreamSynchronize(s));
+  std::reverse(ctx->lvl0_sorted.begin(), ctx->lvl0_sorted.end());
+
+  // ---- assemble ----
+  aiwc_result r{};
+  r.n_events = ctx->n_events_seen;
+  r.total_instructions = ctx->n_instr;
+  r.work_items = ctx->n_wib;
+  r.barriers_hit = ctx->n_bar;
+  {
+    std::vector<uint64_t> oc;
+    for (uint64_t c : ctx->opc_counts) if (c) oc.push_back(c);
+    std::sort(oc.begin(), oc.end(), std::greater<uint64_t>());
+    unsigned __int128 tot = 0;
+    for (uint64_t c : oc) tot += c;
+    r.opcode_coverage = coverage_from(oc, nullptr, 0, tot);
+  }
+  order_stats(h.itb_hist, ctx->itb_ovf_sorted, &r.itb);
+  r.itb.sum = h.itb_sum;
+  order_stats(h.ipt_hist, ctx->ipt_ovf_sorted, &r.ipt);
+  r.ipt.sum = h.ipt_sum;
+  r.total_reads = ctx->n_rd;
+  r.total_writes = ctx->n_wr;
+  r.unique_reads = h.unique_r;
+  r.unique_writes = h.unique_w;
+  r.footprint = h.footprint;
+  r.footprint_90 = M ? coverage_from(ctx->lvl0_sorted, h.cnt_hist0, CBINS, M) : 0;
+  for (int i = 0; i < NLEVELS; ++i) {
+    const double v = M ? h.entropy[i] : 0.0;
+    if (i == 0) r.gmae = v; else r.lmae[i - 1] = v;
+  }
+  r.branch_executions = ctx->n_br;
+  r.branch_observations = ctx->n_br ? h.n_obs : 0;
+  r.branch_excluded = ctx->n_br - r.branch_observations;
+  r.yokota = ctx->n_br ? h.yokota : 0.0;
+  r.linear = ctx->n_br ? h.linear : 0.0;
+  // sites: (site, first position) pairs -> counts
+  ctx->site_ids.clear(); ctx->site_counts.clear();
+  if (ctx->n_br) {
+    std::vector<std::pair<uint64_t, uint64_t>> heads;  // (position, site)
+    const uint64_t ns = h.n_sites;
+    for (uint64_t i = 0; i < ns; ++i) {
+      if (ns <= (uint64_t)MAX_SMALL_LIST) heads.emplace_back(h.site_list[2 * i + 1], h.site_list[2 * i]);
+      else heads.emplace_back(big_sites[2 * i + 1], big_sites[2 * i]);
+    }
+    std::sort(heads.begin(), heads.end());
+    for (size_t i = 0; i < heads.size(); ++i) {
+      const uint64_t end = i + 1 < heads.size() ? heads[i + 1].first : ctx->n_br;
+      ctx->site_ids.push_back(heads[i].second);
+      ctx->site_counts.push_back(end - heads[i].first);
+    }
+    std::vector<uint64_t> sc(ctx->site_counts);
+    std::sort(sc.begin(), sc.end(), std::greater<uint64_t>());
+    r.branch_90 = coverage_from(sc, nullptr, 0, ctx->n_br);
+  }
+  r.n_sites = ctx->site_ids.size();
+  // widths in first-appearance order
+  ctx->width_vals.clear(); ctx->width_counts.clear();
+  if (h.n_widths_listed <= (unsigned long long)MAX_SMALL_LIST) {
+    for (uint64_t i = 0; i < h.n_widths_listed; ++i) {
+      ctx->width_vals.push_back(h.width_list[3 * i]);
+      ctx->width_counts.push_back(h.width_list[3 * i + 1]);
+    }
+  } else {
+    std::vector<std::pair<uint64_t, uint32_t>> order;
+    for (uint32_t w = 0; w < WIDTH_TABLE; ++w) if (wc_full[w]) order.emplace_back(wf_full[w], w);
+    std::sort(order.begin(), order.end());
+    for (auto& o : order) { ctx->width_vals.push_back(o.second); ctx->width_counts.push_back(wc_full[o.second]); }
+  }
+  r.entries = r.unique_reads + r.unique_writes + r.branch_executions;
+  r.n_opcodes = n_opc;
+  r.opcode_counts = ctx->opc_counts.data();
+  r.n_widths = (uint32_t)ctx->width_vals.size();
+  r.width_values = ctx->width_vals.data();
+  r.width_counts = ctx->width_counts.data();
+  r.n_site_list = (uint32_t)ctx->site_ids.size();
+  r.site_ids = ctx->site_ids.data();
+  r.site_counts = ctx->site_counts.data();
+  r.used_dense_table = ctx->dense;
+  r.kernels_launched = ctx->kernels;
+  r.d2h_bytes = ctx->d2h;
+  if (ctx->timing) {
+    for (int ph = 0; ph < AIWC_N_PHASES; ++ph) {
+      float ms = 0.f;
+      if (!(ctx->marked >> ph & 1u)) continue;
+      if (cudaEventElapsedTime(&ms, ctx->ev[2 * ph], ctx->ev[2 * ph + 1]) == cudaSuccess) r.phase_ms[ph] = ms;
+      else cudaGetLastError();
+    }
+  }
+  *out = r;
+  ctx->state = 2;
+
+  // conservation (metrics.py:276-285)
+  uint64_t opc_total = 0, w_total = 0;
+  for (uint64_t c : ctx->opc_counts) opc_total += c;
+  for (uint64_t c : ctx->width_counts) w_total += c;
+  const char* bad = nullptr;
+  if (opc_total != r.total_instructions) bad = "accumulator inconsistent: opcode counts != total instructions";
+  else if (w_total != r.total_instructions) bad = "accumulator inconsistent: width samples != total instructions";
+  else if (r.itb.sum != r.total_instructions) bad = "accumulator inconsistent: ITB samples do not cover all instructions";
+  else if (r.ipt.sum != r.total_instructions) bad = "accumulator inconsistent: IPT samples do not cover all instructions";
+  else if (r.ipt.n != r.work_items) bad = "accumulator inconsistent: one IPT sample per work-item expected";
+  if (bad && !(ctx->opts.flags & AIWC_OPT_NO_CONSERVATION)) return fail(ctx, AIWC_ERR_INCONSISTENT, bad);
+  if (ctx->opts.entry_cap && r.entries > ctx->opts.entry_cap) {
+    fail(ctx, AIWC_ERR_TOO_LARGE, "trace state exceeds the in-memory cap");
+    ctx->err.entries = ctx->opts.entry_cap + 1;
+    ctx->err.cap = ctx->opts.entry_cap;
+    return AIWC_ERR_TOO_LARGE;
+  }
+  return AIWC_OK;
+}

@@ -1,0 +1,186 @@
+// aiwc_internal.cuh -- shared definitions of the sm_100a AIWC engine.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/aiwc_b200.h"
+
+namespace aiwc {
+
+// ---- ingest geometry -------------------------------------------------------
+constexpr int TPB = 256;              // threads per ingest CTA
+constexpr int EPT = 16;               // events per thread per tile (one 16 B kind row)
+constexpr int TILE = TPB * EPT;       // 4096 events per tile
+constexpr int STAGES = 3;             // TMA ring depth
+constexpr int OBINS = 16;             // lane-private opcode bins (ids 0..15)
+constexpr int WBINS = 16;             // lane-private width bins (widths 1..16)
+constexpr int HBINS = 1024;           // ITB / IPT value histogram bins (values 0..1023)
+constexpr int CBINS = 1024;           // count-of-counts bins (counts 1..1023)
+constexpr int NLEVELS = 11;           // address entropy at LSB-skip 0..10
+constexpr uint32_t WIDTH_TABLE = 65536;
+constexpr int MAX_SMALL_LIST = 256;   // widths / sites returned inline in DevState
+constexpr uint64_t IPT_END_FLAG = 1ull << 63;
+
+// ---- kind-byte classes (include/aiwc_b200.h) -------------------------------
+__host__ __device__ constexpr bool is_instr(uint32_t k) { return k & 0x01; }
+__host__ __device__ constexpr bool is_mem(uint32_t k) { return k & 0x06; }
+
+// error flags raised by kernels (DevState::flags)
+enum : uint64_t {
+  F_BAD_OPCODE = 1, F_BAD_WIDTH = 2, F_BAD_SITE = 4, F_ADDR_HINT = 8, F_BAD_GROUP = 16,
+  F_SLOT_RANGE = 32, F_BAD_KIND = 64
+};
+
+// Per-range summary computed from kind bytes alone (pass 1).
+struct RangeSum {
+  uint32_t n_instr, n_rd, n_wr, n_br, n_wgb, instr_after;
+  uint32_t n_wib, n_wir, n_wie, n_bar, n_other, pad;
+  int64_t last_bnd, last_wgb;   // global event index, -1 when absent
+};
+
+// Device-resident accumulator scalars and small tables. The prefix up to
+// `host_end` is what finalize copies back in one transfer.
+struct DevState {
+  // counters
+  unsigned long long itb_sum, ipt_sum, ipt_tab_n, ipt_tab_sum;
+  unsigned long long itb_ovf_n, ipt_ovf_n, lvl0_ovf_n;
+  unsigned long long unique_r, unique_w, footprint;
+  unsigned long long flags, max_site, max_width;
+  unsigned long long addr_min, addr_max, addr_and, addr_or;
+  unsigned long long n_obs, n_sites, n_uniq;      // branch observations, #sites, #unique keys (sparse)
+  unsigned long long n_widths_listed, n_sites_listed;
+  double entropy[NLEVELS];
+  double yokota, linear;
+  unsigned long long itb_hist[HBINS];
+  unsigned long long ipt_hist[HBINS];
+  unsigned long long cnt_hist0[CBINS];              // level-0 count-of-counts (footprint_90)
+  unsigned long long width_list[3 * MAX_SMALL_LIST]; // (value, count, first) first-seen order
+  unsigned long long site_list[2 * MAX_SMALL_LIST];  // (site, count) ascending
+  // ---- not copied back ----
+  unsigned long long host_end;
+  unsigned long long cnt_hist[NLEVELS][CBINS];      // count-of-counts per level (entropy)
+};
+
+// Memory-path description shared by the ingest and the dense-table kernels.
+struct AddrMap {
+  uint64_t base;       // min address rounded down to 1024
+  uint64_t hi;         // max address
+  uint64_t low_mask;   // (1 << k) - 1
+  uint64_t low_const;  // (addr - base) & low_mask for every address
+  uint32_t k;          // constant low bits dropped from keys
+  uint64_t n_keys;     // dense table length
+};
+
+struct IngestArgs {
+  const uint8_t* kind;
+  const uint64_t* payload;
+  uint64_t n;
+  uint64_t tma_rows;          // rows of 16 events covered by the tensor maps
+  uint32_t tiles_per_cta;
+  uint32_t n_opcodes;
+  uint32_t local_volume;
+  const RangeSum* ranges;
+  DevState* st;
+  unsigned long long* opc_counts;   // [n_opcodes]
+  unsigned long long* width_count;  // [WIDTH_TABLE]
+  unsigned long long* width_first;  // [WIDTH_TABLE]
+  uint32_t* itb_ovf;                // [n_bar + n_wie]
+  uint32_t* ipt_ovf;                // [n_wie]
+  unsigned long long* ipt_tab;      // [n_wgb * local_volume] or null
+  uint64_t ipt_tab_len;
+  // memory
+  AddrMap am;
+  unsigned long long* dense;        // dense mode: [am.n_keys] packed r | w << 32
+  uint64_t* rd_out;                 // compact mode
+  uint64_t* wr_out;
+  uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
+};
+
+// ---- small device helpers ----------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_sum(T v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_incl_max(uint32_t v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v = max(v, u);
+  }
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- host-side launchers (defined in the .cu files) -------------------------
+void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t n_ranges,
+                  uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s);
+cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
+                          bool dense, cudaStream_t s);
+void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
+void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
+                       cudaStream_t s);
+void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
+                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s);
+void launch_fill_dense(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr, AddrMap am,
+                       unsigned long long* dense, cudaStream_t s);
+void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_parts, uint64_t total_m, uint32_t k,
+                           cudaStream_t s);
+// sparse memory path; returns kernel count
+int sparse_memory_stats(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr, AddrMap am,
+                        uint64_t total_m, DevState* st, double* partials, uint32_t n_parts, uint64_t* lvl0_ovf,
+                        void* scratch, size_t scratch_bytes, cudaStream_t s);
+size_t sparse_scratch_bytes(uint64_t m);
+// branch path; returns kernel count
+int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t history_len, DevState* st,
+                 unsigned long long* tables, void* scratch, size_t scratch_bytes, cudaStream_t s);
+size_t branch_scratch_bytes(uint64_t n);
+// utilities
+void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
+                    cudaStream_t s, int* kernels);
+size_t radix_hist_bytes(uint64_t n);
+void sort_u32_list(uint32_t* v, uint64_t n, uint64_t* tmp_a, uint64_t* tmp_b, uint32_t* hist, cudaStream_t s,
+                   int* kernels);
+
+}  // namespace aiwc

@@ -1,0 +1,434 @@
+// aiwc_memory.cu -- memory footprint, 90% footprint and LSB-skip entropy.
+//
+// Replaces finalize's merged address Counter (pkg/src/aiwc/metrics.py:308-321)
+// and entropy.shannon_entropy / local_entropy / coverage_count
+// (pkg/src/aiwc/entropy.py:20-66).
+//
+// Both paths reduce to per-level COUNT-OF-COUNTS histograms: the entropy
+// -sum p log2 p (p = c / M) and the coverage count depend only on the multiset
+// of bin counts, so counts < CBINS are histogrammed exactly (integers) and the
+// rare larger counts contribute their fp64 term directly (plus, for level 0,
+// their exact value for the coverage walk).  Level n groups addresses by
+// addr >> n; keys are (addr - base) >> k with base 1024-aligned, so level n is
+// key >> max(0, n - k) and aligned blocks of 2^(10-k) keys hold every group.
+//
+//  dense path  keys index a table (r | w << 32 per key) filled by the ingest
+//              pass; one coalesced sweep computes unique reads / writes /
+//              footprint and all eleven levels (in-thread sums, warp shuffles,
+//              then smem across warps).
+//  sparse path addresses were compacted by the ingest pass; radix sort of the
+//              varying key bits + run-length reduction gives the unique
+//              (key, r, w) list, then each level is a run-length reduction of
+//              the previous one.
+#include <math.h>
+
+#include <algorithm>
+
+#include "aiwc_util.cuh"
+
+namespace aiwc {
+
+__device__ __forceinline__ double plogp(unsigned long long c, double m) {
+  const double p = (double)c / m;
+  return p * log2(p);
+}
+
+// level index j (key-space shift) -> smem histogram; big counts -> fp64 term
+struct LevelAcc {
+  uint32_t* h;           // smem [NLEVELS][CBINS]
+  double part[NLEVELS];  // sum of p log2 p over counts >= CBINS
+  unsigned long long* ovf;
+  unsigned long long* ovf_n;
+  double m;
+  __device__ __forceinline__ void rec(int j, unsigned long long c, uint32_t mult) {
+    if (c == 0) return;
+    if (c < (unsigned long long)CBINS) {
+      atomicAdd(&h[j * CBINS + c], mult);
+    } else {
+      part[j] += plogp(c, m) * mult;
+      if (j == 0)
+        for (uint32_t i = 0; i < mult; ++i) ovf[atomicAdd(ovf_n, 1ull)] = c;
+    }
+  }
+};
+
+constexpr int DS_T = 128;         // 4 warps x 8 keys per lane = 1024 keys per chunk
+constexpr int DS_K = 8;
+constexpr int DS_CHUNK = DS_T * DS_K;
+
+__device__ __forceinline__ void flush_levels(LevelAcc& L, int nlev, DevState* st, double* partials, uint32_t n_parts,
+                                             unsigned long long ur, unsigned long long uw, unsigned long long fp) {
+  // per-level fp64 partials: fixed-order block reduction (deterministic)
+  __shared__ double red[DS_T / 32][NLEVELS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < nlev; ++j) {
+    double v = L.part[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][j] = v;
+  }
+  ur = warp_sum(ur); uw = warp_sum(uw); fp = warp_sum(fp);
+  if (lane == 0) {
+    if (ur) atomicAdd(&st->unique_r, ur);
+    if (uw) atomicAdd(&st->unique_w, uw);
+    if (fp) atomicAdd(&st->footprint, fp);
+  }
+  __syncthreads();
+  if (threadIdx.x < nlev) {
+    double v = 0.0;
+    for (int w = 0; w < DS_T / 32; ++w) v += red[w][threadIdx.x];
+    partials[threadIdx.x * n_parts + blockIdx.x] = v;
+  }
+  for (int i = threadIdx.x; i < nlev * CBINS; i += DS_T) {
+    const uint32_t v = L.h[i];
+    if (v) {
+      if (i < CBINS) atomicAdd(&st->cnt_hist0[i], (unsigned long long)v);
+      else atomicAdd(&st->cnt_hist[i / CBINS][i % CBINS], (unsigned long long)v);
+    }
+  }
+}
+
+// one sweep over the dense key table
+__global__ void __launch_bounds__(DS_T) dense_stats_kernel(const unsigned long long* __restrict__ tab,
+                                                           uint64_t n_keys, int nlev, double m, DevState* st,
+                                                           double* partials, uint32_t n_parts,
+                                                           unsigned long long* lvl0_ovf) {
+  extern __shared__ uint32_t hsm[];
+  __shared__ unsigned long long wsum[DS_T / 32];
+  for (int i = threadIdx.x; i < nlev * CBINS; i += DS_T) hsm[i] = 0;
+  LevelAcc L;
+  L.h = hsm; L.m = m; L.ovf = lvl0_ovf; L.ovf_n = &st->lvl0_ovf_n;
+#pragma unroll
+  for (int j = 0; j < NLEVELS; ++j) L.part[j] = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long ur = 0, uw = 0, fp = 0;
+  const uint64_t n_chunks = (n_keys + DS_CHUNK - 1) / DS_CHUNK;
+  for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
+    const uint64_t k0 = ch * DS_CHUNK + (uint64_t)threadIdx.x * DS_K;
+    unsigned long long c[DS_K];
+    if (k0 + DS_K <= n_keys) {
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + k0);
+#pragma unroll
+      for (int q = 0; q < DS_K / 2; ++q) {
+        const ulonglong2 v = p[q];
+        c[2 * q] = v.x; c[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < DS_K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : 0ull;
+    }
+    // level 0: per-key totals; uniqueness flags
+#pragma unroll
+    for (int i = 0; i < DS_K; ++i) {
+      const unsigned long long r = c[i] & 0xFFFFFFFFull, w = c[i] >> 32;
+      ur += r != 0; uw += w != 0; fp += (r | w) != 0;
+      c[i] = r + w;
+    }
+    {  // run-length aggregate the thread's 8 level-0 counts
+      unsigned long long cur = c[0];
+      uint32_t run = 1;
+#pragma unroll
+      for (int i = 1; i < DS_K; ++i) {
+        if (c[i] == cur) { ++run; }
+        else { L.rec(0, cur, run); cur = c[i]; run = 1; }
+      }
+      L.rec(0, cur, run);
+    }
+    // levels 1..3 inside the thread
+    unsigned long long s1[4], s2[2], s3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
+    s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
+    s3 = s2[0] + s2[1];
+    if (nlev > 1) {
+      if (s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3]) L.rec(1, s1[0], 4);
+      else { L.rec(1, s1[0], 1); L.rec(1, s1[1], 1); L.rec(1, s1[2], 1); L.rec(1, s1[3], 1); }
+    }
+    if (nlev > 2) {
+      if (s2[0] == s2[1]) L.rec(2, s2[0], 2);
+      else { L.rec(2, s2[0], 1); L.rec(2, s2[1], 1); }
+    }
+    if (nlev > 3) L.rec(3, s3, 1);
+    // levels 4..8 across lanes
+    unsigned long long s = s3;
+#pragma unroll
+    for (int j = 4; j <= 8; ++j) {
+      s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
+      if (j < nlev && (lane & ((1 << (j - 3)) - 1)) == 0) L.rec(j, s, 1);
+    }
+    // levels 9, 10 across warps
+    if (nlev > 9) {
+      if (lane == 0) wsum[warp] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        L.rec(9, wsum[0] + wsum[1], 1);
+        L.rec(9, wsum[2] + wsum[3], 1);
+        if (nlev > 10) L.rec(10, wsum[0] + wsum[1] + wsum[2] + wsum[3], 1);
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  flush_levels(L, nlev, st, partials, n_parts, ur, uw, fp);
+}
+
+void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
+                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s) {
+  const int nlev = k >= 10 ? 1 : 11 - (int)k;
+  const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
+  cudaFuncSetAttribute(dense_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dense_stats_kernel<<<n_ctas, DS_T, smem, s>>>(tab, n_keys, nlev, (double)total_m, st, partials, n_ctas,
+                                                reinterpret_cast<unsigned long long*>(lvl0_ovf));
+}
+
+// ---------------------------------------------------------------------------
+// count statistics over a compact count array (sparse path, one level)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(DS_T) count_stats_kernel(const unsigned long long* __restrict__ ca,
+                                                           const unsigned long long* __restrict__ cb, uint64_t n,
+                                                           int level, double m, DevState* st, double* partials,
+                                                           uint32_t n_parts, unsigned long long* lvl0_ovf) {
+  __shared__ uint32_t h[CBINS];
+  __shared__ double red[DS_T / 32];
+  for (int i = threadIdx.x; i < CBINS; i += DS_T) h[i] = 0;
+  __syncthreads();
+  double part = 0.0;
+  unsigned long long ur = 0, uw = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * DS_T + threadIdx.x; i < n; i += (uint64_t)gridDim.x * DS_T) {
+    unsigned long long c = ca[i];
+    if (cb) {
+      const unsigned long long w = cb[i];
+      ur += c != 0; uw += w != 0;
+      c += w;
+    }
+    if (c == 0) continue;
+    if (c < (unsigned long long)CBINS) atomicAdd(&h[c], 1u);
+    else {
+      part += plogp(c, m);
+      if (level == 0) lvl0_ovf[atomicAdd(&st->lvl0_ovf_n, 1ull)] = c;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  ur = warp_sum(ur); uw = warp_sum(uw);
+  if (lane == 0) {
+    red[warp] = part;
+    if (ur) atomicAdd(&st->unique_r, ur);
+    if (uw) atomicAdd(&st->unique_w, uw);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < DS_T / 32; ++w) v += red[w];
+    partials[level * n_parts + blockIdx.x] = v;
+  }
+  for (int i = threadIdx.x; i < CBINS; i += DS_T) {
+    if (h[i]) {
+      if (level == 0) atomicAdd(&st->cnt_hist0[i], (unsigned long long)h[i]);
+      else atomicAdd(&st->cnt_hist[level][i], (unsigned long long)h[i]);
+    }
+  }
+}
+
+size_t sparse_scratch_bytes(uint64_t m) {
+  // keys, tmp, 2 level-key buffers, r, w, 2 level-count buffers + sort/RLE scratch
+  return m * 8 * 8 + radix_hist_bytes(m) + rle_scratch_elems(m) * 4 + 4096;
+}
+
+// key packing: (((addr - base) >> k) << 1) | is_write  when it fits 64 bits
+__global__ void pack_keys_kernel(const uint64_t* __restrict__ src, uint64_t n, uint64_t base, uint32_t k,
+                                 uint64_t flag, uint64_t* __restrict__ dst) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = (((src[i] - base) >> k) << 1) | flag;
+}
+
+__global__ void shift_copy_kernel(const uint64_t* __restrict__ src, uint64_t n, int sh, uint64_t* __restrict__ dst) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] >> sh;
+}
+
+static int bitwidth(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+static void set_u64(unsigned long long* dst, unsigned long long v, cudaStream_t s) {
+  // pageable H2D: the value is staged before cudaMemcpyAsync returns
+  cudaMemcpyAsync(dst, &v, 8, cudaMemcpyHostToDevice, s);
+}
+
+int sparse_memory_stats(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr, AddrMap am,
+                        uint64_t total_m, DevState* st, double* partials, uint32_t n_parts, uint64_t* lvl0_ovf,
+                        void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  int kernels = 0;
+  const uint64_t m = n_rd + n_wr;
+  if (m == 0) return 0;
+  (void)scratch_bytes;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(scratch);
+  uint64_t* tmp = keys + m;
+  uint64_t* lkey[2] = {tmp + m, tmp + 2 * m};
+  unsigned long long* ur = reinterpret_cast<unsigned long long*>(tmp + 3 * m);
+  unsigned long long* uw = ur + m;
+  unsigned long long* lcnt[2] = {uw + m, uw + 2 * m};
+  uint32_t* hist = reinterpret_cast<uint32_t*>(uw + 3 * m);
+  uint32_t* rscr = hist + radix_hist_bytes(m) / 4;
+  unsigned long long* ovf = reinterpret_cast<unsigned long long*>(lvl0_ovf);
+  const double dm = (double)total_m;
+  const int kbits = bitwidth((am.hi - am.base) >> am.k);
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>((m + 255) / 256, 148 * 8);
+  uint64_t U;
+  int nlev;
+  if (kbits <= 63) {
+    // one sort of tagged keys: (((addr - base) >> k) << 1) | is_write
+    pack_keys_kernel<<<blocks, 256, 0, s>>>(rd, n_rd, am.base, am.k, 0, keys);
+    pack_keys_kernel<<<blocks, 256, 0, s>>>(wr, n_wr, am.base, am.k, 1, keys + n_rd);
+    kernels += 2;
+    radix_sort_u64(keys, tmp, m, 0, kbits + 1, hist, s, &kernels);
+    U = rle_reduce(keys, nullptr, m, 1, RLE_RW, lkey[1], ur, uw, rscr, s, &kernels);
+    count_stats_kernel<<<n_parts, DS_T, 0, s>>>(ur, uw, U, 0, dm, st, partials, n_parts, ovf);
+    ++kernels;
+    rle_reduce(keys, nullptr, m, 1, RLE_ONES, lkey[0], lcnt[0], nullptr, rscr, s, &kernels);  // merged counts
+    nlev = am.k >= 10 ? 1 : 11 - (int)am.k;
+  } else {
+    // all 64 key bits significant: untagged sorts (reads, writes, all) of raw addresses
+    cudaMemcpyAsync(keys, rd, n_rd * 8, cudaMemcpyDeviceToDevice, s);
+    radix_sort_u64(keys, tmp, n_rd, 0, 64, hist, s, &kernels);
+    set_u64(&st->unique_r, rle_reduce(keys, nullptr, n_rd, 0, RLE_ONES, lkey[0], lcnt[0], nullptr, rscr, s, &kernels), s);
+    cudaMemcpyAsync(keys, wr, n_wr * 8, cudaMemcpyDeviceToDevice, s);
+    radix_sort_u64(keys, tmp, n_wr, 0, 64, hist, s, &kernels);
+    set_u64(&st->unique_w, rle_reduce(keys, nullptr, n_wr, 0, RLE_ONES, lkey[0], lcnt[0], nullptr, rscr, s, &kernels), s);
+    cudaMemcpyAsync(keys, rd, n_rd * 8, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(keys + n_rd, wr, n_wr * 8, cudaMemcpyDeviceToDevice, s);
+    radix_sort_u64(keys, tmp, m, 0, 64, hist, s, &kernels);
+    U = rle_reduce(keys, nullptr, m, 0, RLE_ONES, lkey[0], lcnt[0], nullptr, rscr, s, &kernels);
+    count_stats_kernel<<<n_parts, DS_T, 0, s>>>(lcnt[0], nullptr, U, 0, dm, st, partials, n_parts, ovf);
+    ++kernels;
+    nlev = 11;  // raw addresses: level n is key >> n
+  }
+  set_u64(&st->footprint, U, s);
+  int ci = 0;
+  uint64_t cn = U;
+  for (int j = 1; j < nlev; ++j) {
+    const int co = 1 - ci;
+    const uint64_t nn = rle_reduce(lkey[ci], lcnt[ci], cn, 1, RLE_SUM, lkey[co], lcnt[co], nullptr, rscr, s, &kernels);
+    count_stats_kernel<<<n_parts, DS_T, 0, s>>>(lcnt[co], nullptr, nn, j, dm, st, partials, n_parts, nullptr);
+    ++kernels;
+    ci = co; cn = nn;
+  }
+  return kernels;
+}
+
+// ---------------------------------------------------------------------------
+// entropy finishing: -(sum_c H[c] * p log2 p + big-count partials) per level
+// ---------------------------------------------------------------------------
+constexpr int EF_T = 1024;
+
+__global__ void __launch_bounds__(EF_T) entropy_finish_kernel(DevState* st, const double* partials,
+                                                              uint32_t n_parts, double m, int nlev, int k,
+                                                              int raw_levels) {
+  __shared__ double red[EF_T / 32];
+  __shared__ double lev[NLEVELS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < nlev; ++j) {
+    const unsigned long long* H = j == 0 ? st->cnt_hist0 : st->cnt_hist[j];
+    double v = 0.0;
+    for (int c = threadIdx.x; c < CBINS; c += EF_T) {
+      const unsigned long long h = H[c];
+      if (h && c) v += (double)h * plogp((unsigned long long)c, m);
+    }
+    for (uint32_t b = threadIdx.x; b < n_parts; b += EF_T) v += partials[j * n_parts + b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tsum = 0.0;
+      for (int w = 0; w < EF_T / 32; ++w) tsum += red[w];
+      lev[j] = -tsum;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < NLEVELS) {
+    const int n = threadIdx.x;
+    const int j = raw_levels ? n : (n <= k ? 0 : n - k);
+    st->entropy[n] = lev[j < nlev ? j : nlev - 1];
+  }
+}
+
+void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_parts, uint64_t total_m, uint32_t k,
+                           cudaStream_t s) {
+  // k == 64 marks the raw-address sparse path (levels are n directly)
+  const bool raw = k == 64;
+  const int nlev = raw ? 11 : (k >= 10 ? 1 : 11 - (int)k);
+  entropy_finish_kernel<<<1, EF_T, 0, s>>>(st, partials, n_parts, (double)total_m, nlev, raw ? 0 : (int)k, raw);
+}
+
+// ---------------------------------------------------------------------------
+// IPT of work-items that crossed a barrier (per-lifetime slot table)
+// ---------------------------------------------------------------------------
+__global__ void ipt_table_kernel(const unsigned long long* __restrict__ tab, uint64_t len, DevState* st,
+                                 uint32_t* ipt_ovf) {
+  __shared__ uint32_t h[HBINS];
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  unsigned long long sum = 0, cnt = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long e = tab[i];
+    if (!(e & IPT_END_FLAG)) continue;
+    const unsigned long long v = e & ~IPT_END_FLAG;
+    ++cnt; sum += v;
+    if (v < HBINS) atomicAdd(&h[v], 1u);
+    else ipt_ovf[atomicAdd(&st->ipt_ovf_n, 1ull)] = (uint32_t)v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < HBINS; i += blockDim.x)
+    if (h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)h[i]);
+  sum = warp_sum(sum); cnt = warp_sum(cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) {
+    atomicAdd(&st->ipt_sum, sum);
+    atomicAdd(&st->ipt_tab_n, cnt);
+  }
+}
+
+void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s) {
+  const uint32_t blocks = (uint32_t)std::min<uint64_t>((len + 255) / 256, 148 * 4);
+  ipt_table_kernel<<<blocks, 256, 0, s>>>(tab, len, st, ipt_ovf);
+}
+
+// ---------------------------------------------------------------------------
+// width Counter in first-appearance order (metrics.py:136, :298-306)
+// ---------------------------------------------------------------------------
+__global__ void width_list_kernel(const unsigned long long* __restrict__ count,
+                                  const unsigned long long* __restrict__ first, DevState* st) {
+  __shared__ unsigned long long lv[MAX_SMALL_LIST], lc[MAX_SMALL_LIST], lf[MAX_SMALL_LIST];
+  __shared__ unsigned int n;
+  if (threadIdx.x == 0) n = 0;
+  __syncthreads();
+  for (uint32_t w = threadIdx.x; w < WIDTH_TABLE; w += blockDim.x) {
+    const unsigned long long c = count[w];
+    if (c) {
+      const unsigned int i = atomicAdd(&n, 1u);
+      if (i < MAX_SMALL_LIST) { lv[i] = w; lc[i] = c; lf[i] = first[w]; }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int m = min(n, (unsigned int)MAX_SMALL_LIST);
+    for (unsigned int i = 1; i < m; ++i) {  // insertion sort by first index
+      const unsigned long long v = lv[i], c = lc[i], f = lf[i];
+      int j = (int)i - 1;
+      while (j >= 0 && lf[j] > f) { lv[j + 1] = lv[j]; lc[j + 1] = lc[j]; lf[j + 1] = lf[j]; --j; }
+      lv[j + 1] = v; lc[j + 1] = c; lf[j + 1] = f;
+    }
+    for (unsigned int i = 0; i < m; ++i) {
+      st->width_list[3 * i] = lv[i]; st->width_list[3 * i + 1] = lc[i]; st->width_list[3 * i + 2] = lf[i];
+    }
+    st->n_widths_listed = n;
+  }
+}
+
+void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
+                       cudaStream_t s) {
+  width_list_kernel<<<1, 1024, 0, s>>>(count, first, st);
+}
+
+}  // namespace aiwc

@@ -1,0 +1,268 @@
+// aiwc_util.cu -- device-wide building blocks: exclusive scan, stable LSD radix
+// sort of u64 keys over a bit range, and run-length reduction of sorted keys.
+// Used by the sparse address path (onesweep-style sort + RLE replacing the
+// reference's Counter/dict re-keying, metrics.py:308-321 / entropy.py:32-46)
+// and by the branch path (stable grouping of per-site outcome streams,
+// metrics.py:145-155).
+#include "aiwc_util.cuh"
+
+namespace aiwc {
+
+// ---------------------------------------------------------------------------
+// exclusive scan of u32 (in place), three kernels
+// ---------------------------------------------------------------------------
+constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
+
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total) {
+  __shared__ uint32_t ws[SCAN_T / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t inc = warp_incl_sum(v);
+  if (lane == 31) ws[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0u;
+    const uint32_t xi = warp_incl_sum(x);
+    ws[lane] = xi - x;
+    if (lane == 31) ws[0] = ws[0];  // keep
+    if (lane == (int)(blockDim.x >> 5) - 1) *total = xi;
+  }
+  __syncthreads();
+  const uint32_t r = ws[warp] + inc - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void scan_reduce_kernel(const uint32_t* d, uint64_t n, uint32_t* bsum) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_TILE;
+  uint32_t s = 0;
+  for (int i = 0; i < SCAN_I; ++i) {
+    const uint64_t idx = b0 + (uint64_t)i * SCAN_T + threadIdx.x;
+    if (idx < n) s += d[idx];
+  }
+  __shared__ uint32_t tot;
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void scan_top_kernel(uint32_t* bsum, uint32_t nb, uint32_t* total_out) {
+  __shared__ uint32_t carry_s;
+  __shared__ uint32_t tot;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < nb; base += SCAN_T) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < nb ? bsum[i] : 0u;
+    const uint32_t ex = block_excl_scan(v, &tot);
+    const uint32_t c = carry_s;
+    if (i < nb) bsum[i] = c + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = c + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total_out) *total_out = carry_s;
+}
+
+__global__ void scan_down_kernel(uint32_t* d, uint64_t n, const uint32_t* bsum) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_I;
+  uint32_t v[SCAN_I], s = 0;
+  for (int i = 0; i < SCAN_I; ++i) {
+    v[i] = (b0 + i < n) ? d[b0 + i] : 0u;
+    s += v[i];
+  }
+  __shared__ uint32_t tot;
+  uint32_t ex = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+  for (int i = 0; i < SCAN_I; ++i) {
+    if (b0 + i < n) d[b0 + i] = ex;
+    ex += v[i];
+  }
+}
+
+size_t scan_scratch_elems(uint64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1; }
+
+void scan_exclusive_u32(uint32_t* d, uint64_t n, uint32_t* scratch, uint32_t* total_out, cudaStream_t s,
+                        int* kernels) {
+  const uint32_t nb = (uint32_t)((n + SCAN_TILE - 1) / SCAN_TILE);
+  if (nb == 0) return;
+  scan_reduce_kernel<<<nb, SCAN_T, 0, s>>>(d, n, scratch);
+  scan_top_kernel<<<1, SCAN_T, 0, s>>>(scratch, nb, total_out);
+  scan_down_kernel<<<nb, SCAN_T, 0, s>>>(d, n, scratch);
+  if (kernels) *kernels += 3;
+}
+
+// ---------------------------------------------------------------------------
+// stable LSD radix sort, 8-bit digits
+// ---------------------------------------------------------------------------
+constexpr int RS_T = 256, RS_I = 8, RS_TILE = RS_T * RS_I;  // 2048 keys per block
+constexpr int RS_W = RS_T / 32;
+
+size_t radix_hist_bytes(uint64_t n) {
+  const uint64_t nb = (n + RS_TILE - 1) / RS_TILE;
+  return (256 * nb + scan_scratch_elems(256 * nb) + 16) * sizeof(uint32_t);
+}
+
+// Each warp owns 256 consecutive keys, item j of lane l is key warp_base + 32 j + l
+// (coalesced, and j-major/lane-minor order is the key order -> stable ranks).
+__global__ void __launch_bounds__(RS_T) radix_hist_kernel(const uint64_t* __restrict__ keys, uint64_t n, int shift,
+                                                          uint32_t mask, uint32_t* __restrict__ hist, uint32_t nb) {
+  __shared__ uint32_t h[256];
+  for (int i = threadIdx.x; i < 256; i += RS_T) h[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)warp * 32 * RS_I;
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {
+    const uint64_t i = base + 32 * j + lane;
+    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & mask], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += RS_T) hist[(uint64_t)d * nb + blockIdx.x] = h[d];
+}
+
+__global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __restrict__ keys,
+                                                             uint64_t* __restrict__ out, uint64_t n, int shift,
+                                                             uint32_t mask, const uint32_t* __restrict__ offs,
+                                                             uint32_t nb) {
+  __shared__ uint32_t cnt[RS_W][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_W * 256; i += RS_T) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)warp * 32 * RS_I;
+  uint64_t k[RS_I];
+  uint32_t d[RS_I];
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {
+    const uint64_t i = base + 32 * j + lane;
+    k[j] = i < n ? keys[i] : 0ull;
+    d[j] = i < n ? ((uint32_t)(k[j] >> shift) & mask) : 256u;
+    if (i < n) atomicAdd(&cnt[warp][d[j]], 1u);
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps + the block's global offset
+  for (int dg = threadIdx.x; dg < 256; dg += RS_T) {
+    uint32_t run = offs[(uint64_t)dg * nb + blockIdx.x];
+    for (int w = 0; w < RS_W; ++w) {
+      const uint32_t c = cnt[w][dg];
+      cnt[w][dg] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
+    if (d[j] < 256u) {
+      const uint32_t pos = cnt[warp][d[j]] + __popc(peers & lt);
+      out[pos] = k[j];
+    }
+    __syncwarp();
+    if (d[j] < 256u && (peers & lt) == 0) cnt[warp][d[j]] += __popc(peers);
+    __syncwarp();
+  }
+}
+
+void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
+                    cudaStream_t s, int* kernels) {
+  if (n <= 1 || bit_hi <= bit_lo) return;
+  const uint32_t nb = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+  uint32_t* hist = hist_scratch;
+  uint32_t* scan_tmp = hist_scratch + 256ull * nb;
+  uint64_t* src = keys;
+  uint64_t* dst = tmp;
+  for (int b = bit_lo; b < bit_hi; b += 8) {
+    const int bits = min(8, bit_hi - b);
+    const uint32_t mask = (1u << bits) - 1u;
+    radix_hist_kernel<<<nb, RS_T, 0, s>>>(src, n, b, mask, hist, nb);
+    scan_exclusive_u32(hist, 256ull * nb, scan_tmp, nullptr, s, kernels);
+    radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    if (kernels) *kernels += 2;
+    uint64_t* x = src; src = dst; dst = x;
+  }
+  if (src != keys) cudaMemcpyAsync(keys, src, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s);
+}
+
+// ---------------------------------------------------------------------------
+// run-length reduction over keys sorted by (key >> shift)
+// mode RLE_ONES: weight 1; RLE_RW: low key bit selects read(0)/write(1) count;
+// RLE_SUM: weights from `w`.
+// ---------------------------------------------------------------------------
+constexpr int RL_T = 256, RL_I = 8, RL_TILE = RL_T * RL_I;
+
+__device__ __forceinline__ bool rl_head(const uint64_t* keys, uint64_t i, int shift) {
+  return i == 0 || (keys[i] >> shift) != (keys[i - 1] >> shift);
+}
+
+__global__ void rle_count_kernel(const uint64_t* __restrict__ keys, uint64_t n, int shift, uint32_t* bc) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * RL_TILE + (uint64_t)threadIdx.x * RL_I;
+  uint32_t c = 0;
+  for (int i = 0; i < RL_I; ++i)
+    if (b0 + i < n && rl_head(keys, b0 + i, shift)) ++c;
+  __shared__ uint32_t tot;
+  block_excl_scan(c, &tot);
+  if (threadIdx.x == 0) bc[blockIdx.x] = tot;
+}
+
+__global__ void rle_write_kernel(const uint64_t* __restrict__ keys, const unsigned long long* __restrict__ wts,
+                                 uint64_t n, int shift, int mode, const uint32_t* bc, uint64_t* out_key,
+                                 unsigned long long* out_a, unsigned long long* out_b) {
+  const uint64_t b0 = (uint64_t)blockIdx.x * RL_TILE + (uint64_t)threadIdx.x * RL_I;
+  uint32_t c = 0;
+  for (int i = 0; i < RL_I; ++i)
+    if (b0 + i < n && rl_head(keys, b0 + i, shift)) ++c;
+  __shared__ uint32_t tot;
+  int64_t seg = (int64_t)bc[blockIdx.x] + block_excl_scan(c, &tot) - 1;
+  unsigned long long ra = 0, rb = 0;
+  for (int i = 0; i < RL_I; ++i) {
+    const uint64_t idx = b0 + i;
+    if (idx >= n) break;
+    const uint64_t key = keys[idx];
+    if (rl_head(keys, idx, shift)) {
+      if (seg >= 0 && (ra | rb)) {
+        if (ra) atomicAdd(&out_a[seg], ra);
+        if (rb) atomicAdd(&out_b[seg], rb);
+      }
+      ra = rb = 0;
+      ++seg;
+      out_key[seg] = key >> shift;
+    }
+    if (mode == RLE_RW) {
+      if (key & 1) ++rb; else ++ra;
+    } else if (mode == RLE_SUM) {
+      ra += wts[idx];
+    } else {
+      ++ra;
+    }
+  }
+  if (seg >= 0 && (ra | rb)) {
+    if (ra) atomicAdd(&out_a[seg], ra);
+    if (rb && out_b) atomicAdd(&out_b[seg], rb);
+  }
+}
+
+size_t rle_scratch_elems(uint64_t n) {
+  const uint64_t nb = (n + RL_TILE - 1) / RL_TILE;
+  return nb + scan_scratch_elems(nb) + 4;
+}
+
+// Returns the number of runs (synchronizes the stream once).
+uint64_t rle_reduce(const uint64_t* keys, const unsigned long long* wts, uint64_t n, int shift, int mode,
+                    uint64_t* out_key, unsigned long long* out_a, unsigned long long* out_b, uint32_t* scratch,
+                    cudaStream_t s, int* kernels) {
+  if (n == 0) return 0;
+  const uint32_t nb = (uint32_t)((n + RL_TILE - 1) / RL_TILE);
+  uint32_t* bc = scratch;
+  uint32_t* total = scratch + nb;
+  uint32_t* sscr = scratch + nb + 1;
+  rle_count_kernel<<<nb, RL_T, 0, s>>>(keys, n, shift, bc);
+  scan_exclusive_u32(bc, nb, sscr, total, s, kernels);
+  uint32_t h_total = 0;
+  cudaMemcpyAsync(&h_total, total, 4, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaMemsetAsync(out_a, 0, h_total * sizeof(unsigned long long), s);
+  if (out_b) cudaMemsetAsync(out_b, 0, h_total * sizeof(unsigned long long), s);
+  rle_write_kernel<<<nb, RL_T, 0, s>>>(keys, wts, n, shift, mode, bc, out_key, out_a, out_b);
+  if (kernels) *kernels += 2;
+  return h_total;
+}
+
+}  // namespace aiwc

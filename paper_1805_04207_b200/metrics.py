@@ -1,0 +1,436 @@
+"""Drop-in ``consume`` / ``finalize`` / ``merge_accumulators`` backed by the B200 engine.
+
+Mirrors ``pkg/src/aiwc/metrics.py`` (names, arguments, exceptions, report
+fields).  All O(events) work -- every histogram, address set, segment
+statistic and branch pattern table -- runs in libaiwc_b200.so on the GPU; this
+module only moves the trace in, and turns the engine's exact integers into
+report reals with the reference's own expressions (``metrics.py:287-386``), so
+ratios, means and the SIMD statistics are bit-identical to the reference.
+
+``consume`` accepts either an iterable of TraceEvent objects (encoded to
+columns by the native walker, which also runs the reference's stream
+validation) or a ``ColumnarTrace`` whose columns are numpy arrays or torch
+tensors (host or CUDA; CUDA columns are processed in place).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+from collections import Counter
+from dataclasses import dataclass, field
+from typing import Iterable, NamedTuple
+
+import numpy as np
+
+from . import _native
+from .errors import AiwcError, EmptySample, IncompatibleReports, InvalidStream, TraceTooLarge
+from .report import AiwcReport, round12
+from .trace import ColumnarTrace
+
+MEM_CAP_ENV = "AIWC_MEM_CAP_BYTES"
+BYTES_PER_ENTRY = 64
+DEFAULT_MEM_CAP_BYTES = 1 << 30
+
+
+def default_entry_cap() -> int:
+    """Entry cap from AIWC_MEM_CAP_BYTES, same rule as the reference (metrics.py:54-57)."""
+    raw = os.environ.get(MEM_CAP_ENV)
+    cap_bytes = int(raw) if raw else DEFAULT_MEM_CAP_BYTES
+    return max(1, cap_bytes // BYTES_PER_ENTRY)
+
+
+# ---------------------------------------------------------------------------
+# engine results
+# ---------------------------------------------------------------------------
+@dataclass
+class EngineResult:
+    """Exact integers + unrounded entropies returned by aiwc_finalize."""
+
+    n_events: int
+    total_instructions: int
+    work_items: int
+    barriers_hit: int
+    opcode_coverage: int
+    itb: tuple  # (n, min, max, sum, mid_lo, mid_hi)
+    ipt: tuple
+    total_reads: int
+    total_writes: int
+    unique_reads: int
+    unique_writes: int
+    footprint: int
+    footprint_90: int
+    gmae: float
+    lmae: list
+    branch_executions: int
+    branch_observations: int
+    branch_excluded: int
+    branch_90: int
+    yokota: float
+    linear: float
+    entries: int
+    opcode_counts: list
+    widths: list  # [(width, count)] first-seen order
+    sites: list   # [(site, executions)] ascending site
+    used_dense_table: bool
+    kernels_launched: int
+
+
+def _dist(d) -> tuple:
+    return (d.n, d.min, d.max, d.sum, d.mid_lo, d.mid_hi)
+
+
+def _copy_result(r: _native.Result) -> EngineResult:
+    return EngineResult(
+        n_events=r.n_events, total_instructions=r.total_instructions, work_items=r.work_items,
+        barriers_hit=r.barriers_hit, opcode_coverage=r.opcode_coverage, itb=_dist(r.itb), ipt=_dist(r.ipt),
+        total_reads=r.total_reads, total_writes=r.total_writes, unique_reads=r.unique_reads,
+        unique_writes=r.unique_writes, footprint=r.footprint, footprint_90=r.footprint_90,
+        gmae=r.gmae, lmae=list(r.lmae), branch_executions=r.branch_executions,
+        branch_observations=r.branch_observations, branch_excluded=r.branch_excluded, branch_90=r.branch_90,
+        yokota=r.yokota, linear=r.linear, entries=r.entries,
+        opcode_counts=[r.opcode_counts[i] for i in range(r.n_opcodes)],
+        widths=[(r.width_values[i], r.width_counts[i]) for i in range(r.n_widths)],
+        sites=[(r.site_ids[i], r.site_counts[i]) for i in range(r.n_site_list)],
+        used_dense_table=bool(r.used_dense_table), kernels_launched=r.kernels_launched,
+    )
+
+
+_pool: dict[int, list] = {}
+_pool_lock = threading.Lock()
+
+
+def _get_ctx(device: int) -> _native.Context:
+    with _pool_lock:
+        free = _pool.setdefault(device, [])
+        if free:
+            return free.pop()
+    return _native.Context(device)
+
+
+def _put_ctx(ctx: _native.Context) -> None:
+    with _pool_lock:
+        _pool.setdefault(ctx.device, []).append(ctx)
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def trace_info(tr: ColumnarTrace) -> _native.TraceInfo:
+    info = _native.TraceInfo()
+    info.n_events = tr.n_events
+    info.local_volume = max(1, tr.local_volume)
+    info.n_opcodes = len(tr.opcodes)
+    if tr.addr_stats is not None:
+        info.has_addr_stats = 1
+        info.addr_min, info.addr_max, info.addr_and, info.addr_or = (int(v) for v in tr.addr_stats)
+    return info
+
+
+def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
+    """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace."""
+    kind, payload = tr.kind, tr.payload
+    on_cuda = _is_torch(kind) and kind.is_cuda
+    if device is None:
+        device = kind.device.index if on_cuda else _default_device()
+    ctx = _get_ctx(device)
+    try:
+        lib = ctx.lib
+        ctx.check(lib.aiwc_reset(ctx.h))
+        info = trace_info(tr)
+        if on_cuda:
+            import torch
+
+            if kind.dtype != torch.uint8 or payload.dtype not in (torch.uint64, torch.int64):
+                raise AiwcError("CUDA columns must be uint8 kind and (u)int64 payload tensors")
+            kind = kind.contiguous()
+            payload = payload.contiguous()
+            if kind.data_ptr() % 16:
+                kind = kind.clone()
+            if payload.data_ptr() % 16:
+                payload = payload.clone()
+            stream = torch.cuda.current_stream(kind.device).cuda_stream
+            rc = lib.aiwc_ingest(ctx.h, ctypes.c_void_p(kind.data_ptr()), ctypes.c_void_p(payload.data_ptr()),
+                                 ctypes.byref(info), ctypes.c_void_p(stream))
+        else:
+            if _is_torch(kind):
+                kind, payload = kind.numpy(), payload.numpy()
+            kind = np.ascontiguousarray(kind, dtype=np.uint8)
+            payload = np.ascontiguousarray(payload).view(np.uint64)
+            rc = lib.aiwc_ingest_host(ctx.h, kind.ctypes.data_as(ctypes.c_void_p),
+                                      payload.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info), None)
+            stream = None
+        ctx.check(rc)
+        res = _native.Result()
+        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
+        return _copy_result(res)
+    finally:
+        _put_ctx(ctx)
+
+
+def _default_device() -> int:
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except ImportError:  # pragma: no cover
+        pass
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# accumulator
+# ---------------------------------------------------------------------------
+_OVERRIDABLE = ("opcode_histogram", "simd_width_counts", "itb_samples", "ipt_samples", "total_instructions",
+                "work_items", "barriers_hit")
+
+
+class KernelAccumulator:
+    """Device-computed accumulator for one invocation (or a merge of several).
+
+    Field names follow the reference (metrics.py:71-95).  Histogram-valued
+    fields are materialised from the engine's exact tables; assigning one of
+    them records an override that finalize's conservation checks see, as the
+    reference's tampered-accumulator tests expect (test_metrics.py:237-241).
+    """
+
+    def __init__(self, kernel_name: str, invocations: list[int], launches: list, result: EngineResult,
+                 opcodes: list[str], trace: ColumnarTrace | None = None,
+                 lmae_per_invocation: list | None = None):
+        object.__setattr__(self, "_over", {})
+        self.kernel_name = kernel_name
+        self.invocations = invocations
+        self.launches = launches
+        self.result = result
+        self.opcodes = opcodes
+        self.trace = trace
+        self.lmae_per_invocation = lmae_per_invocation
+
+    def __setattr__(self, name, value):
+        if name in _OVERRIDABLE:
+            self._over[name] = value
+        else:
+            object.__setattr__(self, name, value)
+
+    def __getattr__(self, name):
+        over = object.__getattribute__(self, "_over")
+        if name in over:
+            return over[name]
+        r = object.__getattribute__(self, "result")
+        if name == "opcode_histogram":
+            ops = object.__getattribute__(self, "opcodes")
+            return Counter({ops[i]: c for i, c in enumerate(r.opcode_counts) if c})
+        if name == "simd_width_counts":
+            return Counter(dict(r.widths))
+        if name == "total_instructions":
+            return r.total_instructions
+        if name == "work_items":
+            return r.work_items
+        if name == "barriers_hit":
+            return r.barriers_hit
+        if name in ("itb_samples", "ipt_samples", "read_addresses", "write_addresses", "branch_records"):
+            raise AiwcError(f"{name} is kept on the device; per-event materialisation is not exposed yet")
+        raise AttributeError(name)
+
+    def branch_executions(self) -> dict[int, int]:
+        return dict(self.result.sites)
+
+
+# ---------------------------------------------------------------------------
+# consume / finalize / merge
+# ---------------------------------------------------------------------------
+def consume(events: Iterable | ColumnarTrace, *, max_entries: int | None = None,
+            device: int | None = None) -> KernelAccumulator:
+    """Fold one trace into an accumulator on the GPU (ref metrics.py:98-196).
+
+    Raises InvalidStream at the first stream-invariant violation (validated
+    by the native walker for object streams) and TraceTooLarge when
+    unique read addresses + unique write addresses + branch executions exceed
+    ``max_entries`` (default from AIWC_MEM_CAP_BYTES), whichever the
+    reference would raise first.
+    """
+    cap = default_entry_cap() if max_entries is None else max_entries
+    violation = None
+    if isinstance(events, ColumnarTrace):
+        tr = events
+    else:
+        from .walker import encode_events
+
+        tr, violation = encode_events(events)
+    if violation is not None:
+        # the reference raises whichever of (cap crossing, first violation) comes first
+        # in stream order: the prefix before the violation decides
+        index, rule, detail = violation
+        if tr is not None and tr.n_events:
+            res = run_engine(tr, device)
+            if res.entries > cap:
+                raise TraceTooLarge(cap + 1, cap)
+        raise InvalidStream(index, rule, detail)
+    res = run_engine(tr, device)
+    if res.entries > cap:
+        raise TraceTooLarge(cap + 1, cap)
+    return KernelAccumulator(
+        kernel_name=tr.kernel_name,
+        invocations=[tr.invocation],
+        launches=[(tr.invocation, tuple(tr.global_size), tuple(tr.local_size))],
+        result=res, opcodes=list(tr.opcodes), trace=tr,
+    )
+
+
+class DistStats(NamedTuple):
+    minimum: int
+    maximum: int
+    median: float
+    mean: float
+    sd: float
+
+
+def summarize_distribution(samples: list[int]) -> DistStats:
+    """Order statistics, mean, population sd of a host sample list (ref metrics.py:207-223)."""
+    if not samples:
+        raise EmptySample("cannot summarize an empty sample")
+    ordered = sorted(samples)
+    n = len(ordered)
+    median = float(ordered[n // 2]) if n % 2 else (ordered[n // 2 - 1] + ordered[n // 2]) / 2.0
+    mean = sum(ordered) / n
+    var = sum((x - mean) ** 2 for x in ordered) / n
+    return DistStats(ordered[0], ordered[-1], median, mean, math.sqrt(var))
+
+
+def _dist_fields(d: tuple):
+    """(min, max, median, mean) exactly as summarize_distribution would give."""
+    n, lo, hi, total, mid_lo, mid_hi = d
+    if not n:
+        return 0, 0, 0.0, 0.0
+    median = float(mid_hi) if n % 2 else (mid_lo + mid_hi) / 2.0
+    return lo, hi, median, total / n
+
+
+def lmae_profile(acc: KernelAccumulator) -> list[float]:
+    """Locality entropy at skip levels 1..10 (ref metrics.py:226-232)."""
+    r = acc.result
+    if not r.footprint:
+        return [0.0] * 10
+    return [round12(v) for v in r.lmae]
+
+
+def finalize(acc: KernelAccumulator) -> AiwcReport:
+    """Every metric of the accumulator (ref metrics.py:273-386)."""
+    r = acc.result
+    over = acc._over
+    total = over.get("total_instructions", r.total_instructions)
+    # conservation (metrics.py:276-285); overrides model a tampered accumulator
+    opc_sum = sum(over["opcode_histogram"].values()) if "opcode_histogram" in over else sum(r.opcode_counts)
+    wid_sum = sum(over["simd_width_counts"].values()) if "simd_width_counts" in over else sum(c for _, c in r.widths)
+    itb_sum = sum(over["itb_samples"]) if "itb_samples" in over else r.itb[3]
+    ipt_sum = sum(over["ipt_samples"]) if "ipt_samples" in over else r.ipt[3]
+    ipt_n = len(over["ipt_samples"]) if "ipt_samples" in over else r.ipt[0]
+    work_items = over.get("work_items", r.work_items)
+    if opc_sum != total:
+        raise AiwcError("accumulator inconsistent: opcode counts != total instructions")
+    if wid_sum != total:
+        raise AiwcError("accumulator inconsistent: width samples != total instructions")
+    if itb_sum != total:
+        raise AiwcError("accumulator inconsistent: ITB samples do not cover all instructions")
+    if ipt_sum != total:
+        raise AiwcError("accumulator inconsistent: IPT samples do not cover all instructions")
+    if ipt_n != work_items:
+        raise AiwcError("accumulator inconsistent: one IPT sample per work-item expected")
+
+    itb_min, itb_max, itb_med, itb_mean = _dist_fields(r.itb)
+    ipt_min, ipt_max, ipt_med, _ = _dist_fields(r.ipt)
+
+    # SIMD width statistics: the reference's expressions over first-seen order (metrics.py:298-306)
+    widths = r.widths
+    width_total = sum(c for _, c in widths)
+    if width_total:
+        simd_sum = sum(w * c for w, c in widths)
+        simd_mean = simd_sum / width_total
+        simd_var = sum(c * (w - simd_mean) ** 2 for w, c in widths) / width_total
+        simd_max = max(w for w, _ in widths)
+        simd_sd = math.sqrt(simd_var)
+    else:
+        simd_sum, simd_mean, simd_sd, simd_max = 0, 0.0, 0.0, 0
+
+    ur, uw, tr_, tw = r.unique_reads, r.unique_writes, r.total_reads, r.total_writes
+    if r.footprint:
+        gmae = round12(r.gmae)
+        lmae = [round12(v) for v in r.lmae]
+        footprint_90 = r.footprint_90
+    else:
+        gmae, lmae, footprint_90 = 0.0, [0.0] * 10, 0
+
+    executions = r.branch_executions
+    no_branches = executions == 0
+    if no_branches:
+        yokota, linear, warmup = 0.0, 0.0, 0.0
+    elif r.branch_observations == 0:  # every stream shorter than the warm-up (NoBranches)
+        yokota, linear, warmup = 0.0, 0.0, 1.0
+    else:
+        yokota, linear = round12(r.yokota), round12(r.linear)
+        warmup = round12(r.branch_excluded / executions)
+
+    if acc.lmae_per_invocation is not None:
+        per_inv = [{"invocation": inv, "lmae": prof} for inv, prof in acc.lmae_per_invocation]
+    else:
+        per_inv = [{"invocation": acc.invocations[0], "lmae": list(lmae)}]
+
+    return AiwcReport(
+        kernel=acc.kernel_name,
+        invocations=list(acc.invocations),
+        opcode=r.opcode_coverage,
+        total_instruction_count=total,
+        work_items=work_items,
+        total_barriers_hit=over.get("barriers_hit", r.barriers_hit),
+        min_itb=itb_min, max_itb=itb_max, median_itb=round12(itb_med),
+        min_ipt=ipt_min, max_ipt=ipt_max, median_ipt=round12(ipt_med),
+        max_simd_width=simd_max, mean_simd_width=round12(simd_mean), sd_simd_width=round12(simd_sd),
+        total_memory_footprint=r.footprint, footprint_90=footprint_90,
+        unique_reads=ur, unique_writes=uw,
+        unique_rw_ratio=None if uw == 0 else round12(ur / uw),
+        total_reads=tr_, total_writes=tw,
+        reread_ratio=0.0 if tr_ == 0 else round12(ur / tr_),
+        rewrite_ratio=0.0 if tw == 0 else round12(uw / tw),
+        gmae=gmae, lmae=lmae,
+        total_unique_branch_instructions=len(r.sites),
+        branch_90=r.branch_90 if r.sites else 0,
+        yokota_entropy=yokota, linear_entropy=linear,
+        mean_itb=round12(itb_mean), simd_width_sum=simd_sum,
+        no_branches=no_branches, warmup_excluded_fraction=warmup,
+        no_reads=tr_ == 0, no_writes=tw == 0,
+        lmae_per_invocation=per_inv,
+    )
+
+
+def merge_accumulators(parts: list[KernelAccumulator], *, allow_name_mismatch: bool = False) -> KernelAccumulator:
+    """Application-level merge (ref metrics.py:235-270): histograms add, samples
+    concatenate, branch streams stay separate, per-part LMAE profiles are kept.
+
+    The merged accumulator is recomputed on the GPU from the parts' columns
+    concatenated in order (opcode dictionaries unified, group keys made
+    disjoint so no branch history crosses a part boundary), which is exactly
+    the reference's definition of a merge.
+    """
+    from .merge import concat_traces
+
+    if not parts:
+        raise EmptySample("nothing to merge")
+    names = {p.kernel_name for p in parts}
+    if len(names) > 1 and not allow_name_mismatch:
+        raise IncompatibleReports(f"kernel names differ: {sorted(names)}")
+    per_inv: list = []
+    for p in parts:
+        if p.lmae_per_invocation is not None:
+            per_inv.extend(p.lmae_per_invocation)
+        else:
+            per_inv.append((p.invocations[0], lmae_profile(p)))
+    tr = concat_traces([p.trace for p in parts])
+    res = run_engine(tr)
+    invocations = [i for p in parts for i in p.invocations]
+    launches = [l for p in parts for l in p.launches]
+    return KernelAccumulator(parts[0].kernel_name, invocations, launches, res, list(tr.opcodes), trace=tr,
+                             lmae_per_invocation=per_inv)
