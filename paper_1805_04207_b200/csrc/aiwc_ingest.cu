@@ -48,11 +48,13 @@ __device__ __forceinline__ void load_kind16(const uint8_t* kind, uint64_t e0, ui
 
 // SWAR class masks over 4 kind bytes
 __device__ __forceinline__ uint32_t m_wgb(uint32_t w) { return w & ~(w >> 1) & 0x40404040u; }
-__device__ __forceinline__ uint32_t m_wib(uint32_t w) {  // 0x30: bit4 & bit5 & !bit7
-  return (w & (w << 1) & ~(w >> 3)) & 0x20202020u;
+// each test is evaluated at one bit position of the byte; shifts never reach
+// across a byte boundary at that position
+__device__ __forceinline__ uint32_t m_wib(uint32_t w) {  // 0x30: bit4 & bit5 & !bit7, at bit5
+  return (w & (w << 1) & ~(w >> 2)) & 0x20202020u;
 }
-__device__ __forceinline__ uint32_t m_wir(uint32_t w) {  // 0xB0: bit4 & bit5 & bit7
-  return (w & (w >> 2) & (w >> 3)) & 0x10101010u;
+__device__ __forceinline__ uint32_t m_wir(uint32_t w) {  // 0xB0: bit4 & bit5 & bit7, at bit4
+  return (w & (w >> 1) & (w >> 3)) & 0x10101010u;
 }
 __device__ __forceinline__ uint32_t m_wie(uint32_t w) {  // 0x10: bit4 & !bit5 & !bit7
   return (w & ~(w >> 1) & ~(w >> 3)) & 0x10101010u;
