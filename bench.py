@@ -209,6 +209,11 @@ def run_ours(args) -> None:
     ms_step = ms / args.steps
     value = n * world / (ms_step / 1e3)
 
+    if args.no_e2e:
+        if rank == 0:
+            print(json.dumps({"ms_per_step": ms / args.steps, "value": n * world / (ms / args.steps / 1e3),
+                              "phases_ms": {p: statistics.median(v) for p, v in phases.items()}}), flush=True)
+        return
     # ---- e2e: public API from pinned host columns ----
     hk = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     hp = torch.empty(n, dtype=torch.int64, pin_memory=True)
@@ -307,6 +312,7 @@ def main():
     ap.add_argument("--ref-sample-wi", type=int, default=1 << 21)
     ap.add_argument("--ref-python-gen", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

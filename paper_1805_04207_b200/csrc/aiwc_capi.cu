@@ -78,7 +78,7 @@ struct aiwc_ctx {
   size_t h_ranges_cap = 0;
   // per trace
   aiwc_trace_info info{};
-  uint64_t n_instr = 0, n_rd = 0, n_wr = 0, n_br = 0, n_wgb = 0, n_wib = 0, n_wir = 0, n_wie = 0, n_bar = 0;
+  uint64_t n_instr = 0, n_rd = 0, n_wr = 0, n_br = 0, n_wgb = 0, n_wib = 0, n_bres = 0, n_bnd = 0, n_bar = 0;
   uint64_t n_events_seen = 0;
   AddrMap am{};
   bool dense = false;
@@ -235,16 +235,17 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
 
   // ---- pass 1: range summaries ----
   const uint64_t n_tiles = (n + TILE - 1) / TILE;
-  uint32_t G = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)ctx->n_sms);
+  uint32_t G = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)ctx->n_sms * CTAS_PER_SM);
   uint32_t tpc = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + G - 1) / G);
   G = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + tpc - 1) / tpc);
   ctx->n_ranges = G;
   ctx->tiles_per_cta = tpc;
-  CK(grow(ctx->ranges, (size_t)G * sizeof(RangeSum)));
-  if (ctx->h_ranges_cap < G) {
+  const uint32_t n_sub = G * P1_SUB;
+  CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
+  if (ctx->h_ranges_cap < n_sub) {
     if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
-    CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ranges), (size_t)G * sizeof(RangeSum)));
-    ctx->h_ranges_cap = G;
+    CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ranges), (size_t)n_sub * sizeof(RangeSum)));
+    ctx->h_ranges_cap = n_sub;
   }
   const bool with_stats = !info->has_addr_stats;
   if (n) {
@@ -254,21 +255,21 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     ctx->kernels += 1;
     CK(cudaGetLastError());
   } else {
-    CK(cudaMemsetAsync(ctx->ranges.p, 0xFF, sizeof(RangeSum), s));
+    CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_sub * sizeof(RangeSum), s));
   }
-  CK(cudaMemcpyAsync(ctx->h_ranges, ctx->ranges.p, (size_t)G * sizeof(RangeSum), cudaMemcpyDeviceToHost, s));
-  ctx->d2h += (size_t)G * sizeof(RangeSum);
+  CK(cudaMemcpyAsync(ctx->h_ranges, ctx->ranges.p, (size_t)n_sub * sizeof(RangeSum), cudaMemcpyDeviceToHost, s));
+  ctx->d2h += (size_t)n_sub * sizeof(RangeSum);
   if (with_stats) {  // addr_min .. addr_or are contiguous
     CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 4 * sizeof(unsigned long long),
                        cudaMemcpyDeviceToHost, s));
     ctx->d2h += 4 * sizeof(unsigned long long);
   }
   CK(cudaStreamSynchronize(s));
-  ctx->n_instr = ctx->n_rd = ctx->n_wr = ctx->n_br = ctx->n_wgb = ctx->n_wib = ctx->n_wir = ctx->n_wie = ctx->n_bar = 0;
-  for (uint32_t i = 0; i < (n ? G : 0); ++i) {
+  ctx->n_instr = ctx->n_rd = ctx->n_wr = ctx->n_br = ctx->n_wgb = ctx->n_wib = ctx->n_bres = ctx->n_bnd = ctx->n_bar = 0;
+  for (uint32_t i = 0; i < (n ? n_sub : 0); ++i) {
     const RangeSum& r = ctx->h_ranges[i];
     ctx->n_instr += r.n_instr; ctx->n_rd += r.n_rd; ctx->n_wr += r.n_wr; ctx->n_br += r.n_br;
-    ctx->n_wgb += r.n_wgb; ctx->n_wib += r.n_wib; ctx->n_wir += r.n_wir; ctx->n_wie += r.n_wie; ctx->n_bar += r.n_bar;
+    ctx->n_wgb += r.n_wgb; ctx->n_wib += r.n_wib; ctx->n_bres += r.n_bres; ctx->n_bnd += r.n_bnd; ctx->n_bar += r.n_bar;
   }
   ctx->n_events_seen = n;
 
@@ -300,11 +301,11 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   }
 
   // ---- buffers ----
-  const uint64_t n_itb_cap = ctx->n_bar + ctx->n_wie, n_ipt_cap = ctx->n_wie;
-  CK(grow(ctx->itb_ovf, std::max<uint64_t>(n_itb_cap, 1) * 4));
-  CK(grow(ctx->ipt_ovf, std::max<uint64_t>(n_ipt_cap, 1) * 4));
+  // ITB / IPT samples are closed by boundaries: n_bnd bounds both overflow lists
+  CK(grow(ctx->itb_ovf, std::max<uint64_t>(ctx->n_bnd, 1) * 4));
+  CK(grow(ctx->ipt_ovf, std::max<uint64_t>(ctx->n_bnd, 1) * 4));
   ctx->ipt_tab_len = 0;
-  if (ctx->n_bar + ctx->n_wir) {
+  if (ctx->n_bres) {
     ctx->ipt_tab_len = ctx->n_wgb * (uint64_t)std::max<uint32_t>(info->local_volume, 1);
     CK(grow(ctx->ipt_tab, ctx->ipt_tab_len * 8));
     CK(cudaMemsetAsync(ctx->ipt_tab.p, 0, ctx->ipt_tab_len * 8, s));
@@ -339,7 +340,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.dense = ctx->dense ? P<unsigned long long>(ctx->dtab) : nullptr;
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     ctx->mark(AIWC_PH_INGEST, 0, s);
-    CK(launch_ingest(a, km, pm, G, ctx->dense, s));
+    CK(launch_ingest(a, km, pm, G, ctx->dense, !ctx->dense || ctx->n_br > 0, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
     ctx->kernels += 1;
   }

@@ -12,7 +12,9 @@ namespace aiwc {
 constexpr int TPB = 256;              // threads per ingest CTA
 constexpr int EPT = 16;               // events per thread per tile (one 16 B kind row)
 constexpr int TILE = TPB * EPT;       // 4096 events per tile
-constexpr int STAGES = 3;             // TMA ring depth
+constexpr int STAGES = 2;             // TMA ring depth (two CTAs per SM -> four tiles in flight)
+constexpr int P1_SUB = 8;             // pass-1 sub-ranges per ingest range
+constexpr int CTAS_PER_SM = 2;        // ingest CTAs per SM (non-staging variant)
 constexpr int OBINS = 16;             // lane-private opcode bins (ids 0..15)
 constexpr int WBINS = 16;             // lane-private width bins (widths 1..16)
 constexpr int HBINS = 1024;           // ITB / IPT value histogram bins (values 0..1023)
@@ -35,7 +37,7 @@ enum : uint64_t {
 // Per-range summary computed from kind bytes alone (pass 1).
 struct RangeSum {
   uint32_t n_instr, n_rd, n_wr, n_br, n_wgb, instr_after;
-  uint32_t n_wib, n_wir, n_wie, n_bar, n_other, pad;
+  uint32_t n_wib, n_bres, n_bnd, n_bar, pad0, pad1;  // bres = barriers + resumes, bnd = all boundaries
   int64_t last_bnd, last_wgb;   // global event index, -1 when absent
 };
 
@@ -157,7 +159,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t n_ranges,
                   uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s);
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
-                          bool dense, cudaStream_t s);
+                          bool dense, bool stage, cudaStream_t s);
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);
