@@ -290,7 +290,9 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     am.base = amin & ~1023ull;
     am.hi = amax;
     const uint64_t vary = aand ^ aor;
-    am.k = vary ? (uint32_t)__builtin_ctzll(vary) : 0u;
+    // constant low bits dropped from keys; capped at 32 so the per-event check of
+    // the dropped bits is one 32-bit compare in the ingest kernel
+    am.k = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
     am.low_mask = am.k >= 64 ? ~0ull : ((1ull << am.k) - 1);
     am.low_const = (amin - am.base) & am.low_mask;
     const uint64_t span_keys = (amax - am.base) >> am.k;
@@ -338,8 +340,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.ipt_tab = ctx->ipt_tab_len ? P<unsigned long long>(ctx->ipt_tab) : nullptr; a.ipt_tab_len = ctx->ipt_tab_len;
     a.am = ctx->am;
     a.dense = ctx->dense ? P<unsigned long long>(ctx->dtab) : nullptr;
-    a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
-    ctx->mark(AIWC_PH_INGEST, 0, s);
+    a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);    ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, !ctx->dense || ctx->n_br > 0, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
     ctx->kernels += 1;

@@ -1,0 +1,204 @@
+// aiwc_dense.cu -- one sweep over the dense address table (the dense memory path).
+//
+// Replaces finalize's merged Counter, shannon_entropy, local_entropy x10 and
+// coverage_count over memory (pkg/src/aiwc/metrics.py:308-321,
+// pkg/src/aiwc/entropy.py:20-66) for traces whose address span fits a table
+// of (reads | writes << 32) counters indexed by key = (addr - base) >> k.
+//
+// Each 128-thread CTA sweeps 1024-key chunks (8 consecutive keys per thread,
+// next chunk prefetched while the current one is folded).  Level n groups
+// addresses by addr >> n, i.e. keys by key >> max(0, n - k): groups of up to 8
+// keys are summed inside a thread, up to 256 across the warp (xor shuffles),
+// 512 and 1024 across the CTA.  Every non-empty group adds one to the level's
+// count-of-counts histogram (warp-aggregated with match.any: in streaming
+// traces every lane carries the same count), counts >= CBINS add their fp64
+// p*log2(p) term to a thread-owned partial and, at level 0, their exact value
+// to the overflow list the coverage walk needs.
+#include <math.h>
+
+#include <algorithm>
+
+#include "aiwc_internal.cuh"
+
+namespace aiwc {
+
+namespace {
+
+constexpr int T = 128;      // threads per CTA
+constexpr int K = 8;        // keys per thread
+constexpr int CHUNK = T * K;
+
+__device__ __forceinline__ double plogp(unsigned long long c, double m) {
+  const double p = (double)c / m;
+  return p * log2(p);
+}
+
+struct DenseShared {
+  double part[NLEVELS][T];  // thread-owned big-count partials (deterministic reduction)
+  unsigned long long wsum[T / 32];
+};
+
+struct Ctx {
+  uint32_t* h;               // smem [nlev][CBINS] count-of-counts
+  double* part;              // &part[0][t]
+  unsigned long long* ovf;   // level-0 counts >= CBINS
+  unsigned long long* ovf_n;
+  double m;
+  int lane;
+  // one lane's group(s): c == 0 means "no group here"; safe in divergent code
+  __device__ __forceinline__ void rec(int j, unsigned long long c, uint32_t mult) {
+    if (c == 0) return;
+    if (c < (unsigned long long)CBINS) {
+      atomicAdd(&h[j * CBINS + (uint32_t)c], mult);
+    } else {
+      part[j * T] += plogp(c, m) * mult;
+      if (j == 0)
+        for (uint32_t i = 0; i < mult; ++i) ovf[atomicAdd(ovf_n, 1ull)] = c;
+    }
+  }
+  // called by all 32 lanes together.  Streaming traces give every lane the same
+  // count: then lane 0 adds the whole warp's groups at once (no 32-way conflict).
+  __device__ __forceinline__ void rec_warp(int j, unsigned long long c, uint32_t mult, bool participant,
+                                           uint32_t groups) {
+    if (!participant) c = 0;
+    const unsigned long long c0 = __shfl_sync(0xffffffffu, c, 0);  // lane 0 always participates
+    const bool same = __all_sync(0xffffffffu, !participant || c == c0);
+    if (same && c0 != 0 && c0 < (unsigned long long)CBINS) {
+      if (lane == 0) atomicAdd(&h[j * CBINS + (uint32_t)c0], mult * groups);
+    } else {
+      rec(j, c, mult);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long long* __restrict__ tab,
+                                                           uint64_t n_keys, int nlev, double m, DevState* st,
+                                                           double* partials, uint32_t n_parts,
+                                                           unsigned long long* lvl0_ovf) {
+  extern __shared__ uint32_t hsm[];
+  __shared__ DenseShared D;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < nlev * CBINS; i += T) hsm[i] = 0;
+#pragma unroll
+  for (int j = 0; j < NLEVELS; ++j) D.part[j][t] = 0.0;
+  __syncthreads();
+  Ctx X{hsm, &D.part[0][t], lvl0_ovf, &st->lvl0_ovf_n, m, lane};
+  unsigned long long ur = 0, uw = 0, fp = 0;
+  const uint64_t n_chunks = (n_keys + CHUNK - 1) / CHUNK;
+
+  auto load = [&](uint64_t ch, unsigned long long (&c)[K]) {
+    const uint64_t k0 = ch * CHUNK + (uint64_t)t * K;
+    if (k0 + K <= n_keys) {
+      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + k0);
+#pragma unroll
+      for (int q = 0; q < K / 2; ++q) {
+        const ulonglong2 v = __ldcs(p + q);  // streamed once: do not keep in L2
+        c[2 * q] = v.x; c[2 * q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : 0ull;
+    }
+  };
+
+  unsigned long long cur[K], nxt[K];
+  uint64_t ch = blockIdx.x;
+  if (ch < n_chunks) load(ch, cur);
+  for (; ch < n_chunks; ch += gridDim.x) {
+    if (ch + gridDim.x < n_chunks) load(ch + gridDim.x, nxt);
+    unsigned long long c[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const unsigned long long r = cur[i] & 0xFFFFFFFFull, w = cur[i] >> 32;
+      ur += r != 0; uw += w != 0; fp += (r | w) != 0;
+      c[i] = r + w;
+    }
+    // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
+    bool uni = true;
+#pragma unroll
+    for (int i = 1; i < K; ++i) uni &= c[i] == c[0];
+    if (__all_sync(0xffffffffu, uni)) {
+      X.rec_warp(0, c[0], K, true, 32);
+    } else {
+      unsigned long long v = c[0];
+      uint32_t run = 1;
+#pragma unroll
+      for (int i = 1; i < K; ++i) {
+        if (c[i] == v) { ++run; }
+        else { X.rec(0, v, run); v = c[i]; run = 1; }
+      }
+      X.rec(0, v, run);
+    }
+    unsigned long long s1[4], s2[2], s3;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
+    s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
+    s3 = s2[0] + s2[1];
+    if (nlev > 1) {
+      const bool u1 = s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3];
+      if (__all_sync(0xffffffffu, u1)) X.rec_warp(1, s1[0], 4, true, 32);
+      else { X.rec(1, s1[0], 1); X.rec(1, s1[1], 1); X.rec(1, s1[2], 1); X.rec(1, s1[3], 1); }
+    }
+    if (nlev > 2) {
+      if (__all_sync(0xffffffffu, s2[0] == s2[1])) X.rec_warp(2, s2[0], 2, true, 32);
+      else { X.rec(2, s2[0], 1); X.rec(2, s2[1], 1); }
+    }
+    if (nlev > 3) X.rec_warp(3, s3, 1, true, 32);
+    unsigned long long s = s3;
+#pragma unroll
+    for (int j = 4; j <= 8; ++j) {
+      s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
+      if (j < nlev) X.rec_warp(j, s, 1, (lane & ((1 << (j - 3)) - 1)) == 0, 32u >> (j - 3));
+    }
+    if (nlev > 9) {  // levels 9, 10 need the whole CTA (k < 2 only)
+      if (lane == 0) D.wsum[warp] = s;
+      __syncthreads();
+      if (t == 0) {
+        const unsigned long long g[3] = {D.wsum[0] + D.wsum[1], D.wsum[2] + D.wsum[3],
+                                         D.wsum[0] + D.wsum[1] + D.wsum[2] + D.wsum[3]};
+        for (int q = 0; q < 3; ++q) {
+          const int j = q < 2 ? 9 : 10;
+          if (j >= nlev || g[q] == 0) continue;
+          if (g[q] < (unsigned long long)CBINS) atomicAdd(&hsm[j * CBINS + (uint32_t)g[q]], 1u);
+          else D.part[j][0] += plogp(g[q], m);
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < K; ++i) cur[i] = nxt[i];
+  }
+  __syncthreads();
+  // ---- flush: counters, histograms, fixed-order fp64 partials ----
+  ur = warp_sum(ur); uw = warp_sum(uw); fp = warp_sum(fp);
+  if (lane == 0) {
+    if (ur) atomicAdd(&st->unique_r, ur);
+    if (uw) atomicAdd(&st->unique_w, uw);
+    if (fp) atomicAdd(&st->footprint, fp);
+  }
+  if (t < nlev) {
+    double v = 0.0;
+    for (int i = 0; i < T; ++i) v += D.part[t][i];
+    partials[t * n_parts + blockIdx.x] = v;
+  }
+  for (int i = t; i < nlev * CBINS; i += T) {
+    const uint32_t v = hsm[i];
+    if (v) {
+      if (i < CBINS) atomicAdd(&st->cnt_hist0[i], (unsigned long long)v);
+      else atomicAdd(&st->cnt_hist[i / CBINS][i % CBINS], (unsigned long long)v);
+    }
+  }
+}
+
+}  // namespace
+
+void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
+                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s) {
+  const int nlev = k >= 10 ? 1 : 11 - (int)k;
+  const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
+  cudaFuncSetAttribute(dense_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dense_stats_kernel<<<n_ctas, T, smem, s>>>(tab, n_keys, nlev, (double)total_m, st, partials, n_ctas,
+                                             reinterpret_cast<unsigned long long*>(lvl0_ovf));
+}
+
+}  // namespace aiwc

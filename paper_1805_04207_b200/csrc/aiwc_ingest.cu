@@ -12,13 +12,15 @@
 //  ingest  one persistent 256-thread CTA per range (two per SM).  Tiles of
 //          4096 events arrive by TMA (kind rows + payload rows with 128 B
 //          swizzle) through a 2-stage mbarrier ring; each thread owns 16
-//          consecutive events.  A block scan over per-thread kind summaries
-//          gives every thread its exact carry-in (segment count, work-item,
-//          group, output offsets); then each thread folds its 16 events:
-//          opcode/width histograms (lane-private u16 smem bins), memory
-//          addresses (dense-table RED.ADD or ordered compaction), and -- on
-//          the rare path -- ITB/IPT values (smem histograms + exact overflow
-//          lists), per-work-item IPT slots and ordered branch records.
+//          consecutive events.  An 8x8 bit-matrix transpose of the thread's
+//          16 kind bytes gives one 16-bit mask per kind bit; a block scan of
+//          the per-thread class counts gives every thread its exact carry-in
+//          (segment length, work-item, group, output offsets).  Each event
+//          class is then folded by its own converged set-bit loop:
+//          instructions -> lane-private u16 opcode / width bins, memory ->
+//          dense-table RED.ADD (or ordered compaction), rare events in stream
+//          order -> segment closes, branch records, group changes.  Segment
+//          closes are histogrammed after the tile by all threads together.
 #include "aiwc_internal.cuh"
 
 namespace aiwc {
@@ -47,14 +49,6 @@ __device__ __forceinline__ void load_kind16(const uint8_t* kind, uint64_t e0, ui
 }
 
 __device__ __forceinline__ uint32_t m_wgb(uint32_t w) { return w & ~(w >> 1) & 0x40404040u; }
-
-// bit 0 of each byte of four words -> 16-bit mask in event order (byte b of
-// word i -> bit 4i + b).  The multiply by 0x01020408 moves byte b's bit 0 to
-// bit 24 + b without carries.
-__device__ __forceinline__ uint32_t nib4(uint32_t x) { return ((x & 0x01010101u) * 0x01020408u) >> 24; }
-__device__ __forceinline__ uint32_t gather16(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  return nib4(a) | (nib4(b) << 4) | (nib4(c) << 8) | (nib4(d) << 12);
-}
 
 // per-class counts of 16 kind bytes.  Nibble packing: L holds bits 0..3
 // (instr, read, write, branch) of two words, H bits 4..7 (boundary, open,
@@ -201,40 +195,50 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
 // ---------------------------------------------------------------------------
 // main ingest pass
 // ---------------------------------------------------------------------------
-constexpr int BND_CAP = 512;  // close records buffered per tile (overflow is processed inline)
-
-struct IngestSmem {
-  uint64_t pay[STAGES][TILE];        // 128 B-swizzled payload rows (TMA); 1024 B aligned
-  uint8_t kind[STAGES][TILE];
-  uint16_t opc_priv[OBINS][TPB];     // lane-private opcode counts (flushed before they can wrap)
-  uint16_t wid_priv[WBINS][TPB];     // lane-private width counts (width 1..16)
-  uint32_t itb_h[HBINS];
-  uint32_t ipt_h[HBINS];
-  unsigned long long wfirst[WBINS];
-  uint4 closes[BND_CAP];             // segment closes of the tile: (seg, lid, gseq | bar << 31 | byres << 30)
-  uint32_t ws[TPB / 32][6];
-  uint32_t vpos[TPB];
-  uint32_t nc[5];
-  uint64_t bar[STAGES];
-  uint64_t stage_out[1];             // TILE entries when the kernel stages compaction output
-};
+constexpr int BND_CAP = 512;  // segment closes buffered per tile (overflow is processed inline)
 constexpr uint32_t PRIV_FLUSH_TILES = 65535 / EPT;  // u16 bins take at most EPT increments per tile
 
-__device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
-  const uint32_t row = pos >> 4, j = pos & 15;
-  return pay[row * 16 + ((((j >> 1) ^ (row & 7))) << 1) + (j & 1)];
+// TMA stages (dynamic smem, 1024 B aligned for the 128 B swizzle)
+struct StageSmem {
+  uint64_t pay[STAGES][TILE];  // payload rows, 16 B chunk c of row r stored at chunk c ^ (r & 7)
+  uint8_t kind[STAGES][TILE];
+  uint64_t bar[STAGES];
+  uint64_t stage_out[1];       // TILE entries when the variant stages compaction output
+};
+
+// CTA-private accumulators and per-tile scratch (static smem: direct addressing)
+struct LocalSmem {
+  uint16_t opc[OBINS][TPB];    // lane-private opcode counts (flushed before they can wrap)
+  uint16_t wid[WBINS][TPB];    // lane-private width counts, width 1..16
+  uint32_t itb_h[HBINS];
+  uint32_t ipt_h[HBINS];
+  uint4 closes[BND_CAP];       // (segment length, local id, gseq | barrier << 31 | resumed << 30)
+  unsigned long long wfirst[WBINS];
+  uint4 wtot[TPB / 32];        // per-warp inclusive totals of the packed scan values
+  uint32_t vpos[TPB];
+  uint32_t nc[5];
+};
+
+// 8x8 bit-matrix transpose: input byte i = event i (bit c = kind bit c);
+// output byte c = kind bit c of events 0..7 (bit i = event i)
+__device__ __forceinline__ uint64_t transpose8(uint64_t x) {
+  uint64_t t;
+  t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull; x ^= t ^ (t << 7);
+  t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull; x ^= t ^ (t << 14);
+  t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull; x ^= t ^ (t << 28);
+  return x;
 }
 
 // One segment close (metrics.py:156-174): ITB sample (barrier always, wi_end when
 // non-empty); IPT either straight to the histogram (work-item never crossed a
 // barrier) or accumulated in the work-item's lifetime slot.
-__device__ __forceinline__ void do_close(IngestSmem& S, const IngestArgs& a, uint32_t seg, uint32_t lid, uint32_t gz,
+__device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint32_t seg, uint32_t lid, uint32_t gz,
                                          unsigned long long& itb_sum, unsigned long long& ipt_sum,
                                          unsigned long long& flags) {
   const bool bar = gz >> 31, byres = (gz >> 30) & 1u;
   const uint32_t gseq = gz & 0x3FFFFFFFu;
   if (bar || seg) {
-    if (seg < (uint32_t)HBINS) atomicAdd(&S.itb_h[seg], 1u);
+    if (seg < (uint32_t)HBINS) atomicAdd(&L.itb_h[seg], 1u);
     else a.itb_ovf[atomicAdd(&a.st->itb_ovf_n, 1ull)] = seg;
     itb_sum += seg;
   }
@@ -243,25 +247,30 @@ __device__ __forceinline__ void do_close(IngestSmem& S, const IngestArgs& a, uin
     if (gseq == 0 || slot >= a.ipt_tab_len) flags |= F_SLOT_RANGE;
     else atomicAdd(&a.ipt_tab[slot], (unsigned long long)seg + (bar ? 0ull : IPT_END_FLAG));
   } else {
-    if (seg < (uint32_t)HBINS) atomicAdd(&S.ipt_h[seg], 1u);
+    if (seg < (uint32_t)HBINS) atomicAdd(&L.ipt_h[seg], 1u);
     else a.ipt_ovf[atomicAdd(&a.st->ipt_ovf_n, 1ull)] = seg;
     ipt_sum += seg;
   }
 }
 
-__device__ __forceinline__ void flush_private(IngestSmem& S, const IngestArgs& a, int t) {
+__device__ __forceinline__ void flush_private(LocalSmem& L, const IngestArgs& a, int t) {
   __syncthreads();
   if (t < OBINS) {
     unsigned long long sum = 0;
-    for (int i = 0; i < TPB; ++i) { sum += S.opc_priv[t][i]; S.opc_priv[t][i] = 0; }
+    for (int i = 0; i < TPB; ++i) { sum += L.opc[t][i]; L.opc[t][i] = 0; }
     if (sum) atomicAdd(&a.opc_counts[t], sum);
   } else if (t >= 32 && t < 32 + WBINS) {
     const int b = t - 32;
     unsigned long long sum = 0;
-    for (int i = 0; i < TPB; ++i) { sum += S.wid_priv[b][i]; S.wid_priv[b][i] = 0; }
+    for (int i = 0; i < TPB; ++i) { sum += L.wid[b][i]; L.wid[b][i] = 0; }
     if (sum) atomicAdd(&a.width_count[b + 1], sum);
   }
   __syncthreads();
+}
+
+__device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
+  const uint32_t row = pos >> 4, j = pos & 15;
+  return pay[row * 16 + ((((j >> 1) ^ (row & 7))) << 1) + (j & 1)];
 }
 
 template <bool DENSE, bool STAGE>
@@ -269,8 +278,11 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     ingest_kernel(const IngestArgs a, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap pmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  IngestSmem& S = *reinterpret_cast<IngestSmem*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ LocalSmem L;
+  // 1024 B alignment for the swizzle; pointer arithmetic on the shared array
+  // keeps the accesses in the shared window
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  StageSmem& S = *reinterpret_cast<StageSmem*>(smem_raw + pad);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint64_t n = a.n;
   const uint64_t n_tiles_total = (n + TILE - 1) / TILE;
@@ -280,10 +292,10 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   DevState* st = a.st;
 
   // ---- prologue: smem init + TMA ring fill ----
-  for (int i = t; i < OBINS * TPB; i += TPB) (&S.opc_priv[0][0])[i] = 0;
-  for (int i = t; i < WBINS * TPB; i += TPB) (&S.wid_priv[0][0])[i] = 0;
-  for (int i = t; i < HBINS; i += TPB) { S.itb_h[i] = 0; S.ipt_h[i] = 0; }
-  if (t < WBINS) S.wfirst[t] = ~0ull;
+  for (int i = t; i < OBINS * TPB; i += TPB) (&L.opc[0][0])[i] = 0;
+  for (int i = t; i < WBINS * TPB; i += TPB) (&L.wid[0][0])[i] = 0;
+  for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
+  if (t < WBINS) L.wfirst[t] = ~0ull;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     fence_barrier_init();
@@ -351,8 +363,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   uint32_t seen_w = 0;  // widths 1..16 already first-indexed by this thread
   unsigned long long itb_sum = 0, ipt_sum = 0, flags = 0, max_site = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
-  uint16_t* const opc_col = &S.opc_priv[0][t];
-  uint16_t* const wid_col = &S.wid_priv[0][t];
+  uint16_t* const opc_col = &L.opc[0][t];
+  uint16_t* const wid_col = &L.wid[0][t];
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -373,99 +385,157 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         S.pay[s][t * 16 + ((((j >> 1) ^ (t & 7))) << 1) + (j & 1)] = e < n ? a.payload[e] : 0ull;
       }
     }
-    // ---- per-thread class masks: bit j = event j of my 16 is in the class ----
-    const uint32_t ins16 = gather16(w[0], w[1], w[2], w[3]);
-    const uint32_t rd16 = gather16(w[0] >> 1, w[1] >> 1, w[2] >> 1, w[3] >> 1);
-    const uint32_t wr16 = gather16(w[0] >> 2, w[1] >> 2, w[2] >> 2, w[3] >> 2);
-    const uint32_t br16 = gather16(w[0] >> 3, w[1] >> 3, w[2] >> 3, w[3] >> 3);
-    const uint32_t bnd16 = gather16(w[0] >> 4, w[1] >> 4, w[2] >> 4, w[3] >> 4);
-    const uint32_t open16 = bnd16 & gather16(w[0] >> 5, w[1] >> 5, w[2] >> 5, w[3] >> 5);
-    const uint32_t wgb16 = gather16(m_wgb(w[0]) >> 6, m_wgb(w[1]) >> 6, m_wgb(w[2]) >> 6, m_wgb(w[3]) >> 6);
-    // rare: branch, boundary, group and kernel events (bits 3..6)
-    const uint32_t rare16 = gather16((w[0] >> 3) | (w[0] >> 4) | (w[0] >> 5) | (w[0] >> 6),
-                                     (w[1] >> 3) | (w[1] >> 4) | (w[1] >> 5) | (w[1] >> 6),
-                                     (w[2] >> 3) | (w[2] >> 4) | (w[2] >> 5) | (w[2] >> 6),
-                                     (w[3] >> 3) | (w[3] >> 4) | (w[3] >> 5) | (w[3] >> 6));
-    const uint32_t n_in = __popc(ins16), n_rd = __popc(rd16), n_wr = __popc(wr16), n_br = __popc(br16);
-    const uint32_t n_wg = __popc(wgb16), n_cl = __popc(bnd16 & ~open16);
+    // ---- kind bit-planes of my 16 events: plane c bit j = bit c of kind byte j ----
+    uint32_t ins16, rd16, wr16, br16, bnd16, p5, p6, p7;
+    {
+      const uint64_t x0 = transpose8((uint64_t)w[0] | ((uint64_t)w[1] << 32));
+      const uint64_t x1 = transpose8((uint64_t)w[2] | ((uint64_t)w[3] << 32));
+      const uint32_t a01 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x5140);
+      const uint32_t a23 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x7362);
+      const uint32_t b45 = __byte_perm((uint32_t)(x0 >> 32), (uint32_t)(x1 >> 32), 0x5140);
+      const uint32_t b67 = __byte_perm((uint32_t)(x0 >> 32), (uint32_t)(x1 >> 32), 0x7362);
+      ins16 = a01 & 0xFFFFu; rd16 = a01 >> 16; wr16 = a23 & 0xFFFFu; br16 = a23 >> 16;
+      bnd16 = b45 & 0xFFFFu; p5 = b45 >> 16; p6 = b67 & 0xFFFFu; p7 = b67 >> 16;
+    }
+    const uint32_t close16 = bnd16 & ~p5;          // barrier / wi_end
+    const uint32_t wgb16 = p6 & ~p7;               // wg_begin
+    const uint32_t rare16 = br16 | bnd16 | p5 | p6;  // branch, boundary, group, kernel events
     const int lp = bnd16 ? 31 - __clz(bnd16) : -1;
     const int lw = wgb16 ? 31 - __clz(wgb16) : -1;
+    const uint32_t n_in = __popc(ins16);
     const uint32_t after = __popc(ins16 >> (lp + 1));
-    // ---- block scan ----
-    const uint32_t A = n_in | (n_br << 16), B = n_rd | (n_wr << 16), C = n_wg | (n_cl << 16);
-    const uint32_t P = lp >= 0 ? (uint32_t)(16 * t + lp + 1) : 0u;
-    const uint32_t Q = lw >= 0 ? (uint32_t)(16 * t + lw + 1) : 0u;
-    const uint32_t Ai = warp_incl_sum(A), Bi = warp_incl_sum(B), Ci = warp_incl_sum(C);
-    const uint32_t Pi = warp_incl_max(P), Qi = warp_incl_max(Q);
-    if (lane == 31) { S.ws[warp][0] = Ai; S.ws[warp][1] = Bi; S.ws[warp][2] = Ci; S.ws[warp][3] = Pi; S.ws[warp][4] = Qi; }
-    __syncthreads();
-    uint32_t Ap = 0, Bp = 0, Cp = 0, Pp = 0, Qp = 0, TA = 0, TB = 0, TC = 0;
+    // ---- block scan of (instr | branch<<16), (read | write<<16), (wgb | close<<16), (lastpos | lastwgb<<16) ----
+    const uint32_t A = n_in | (__popc(br16) << 16), B = __popc(rd16) | (__popc(wr16) << 16);
+    const uint32_t C = __popc(wgb16) | (__popc(close16) << 16);
+    const uint32_t PQ = (lp >= 0 ? (uint32_t)(16 * t + lp + 1) : 0u) | ((lw >= 0 ? (uint32_t)(16 * t + lw + 1) : 0u) << 16);
+    uint32_t Ai = A, Bi = B, Ci = C, Mi = PQ;
 #pragma unroll
-    for (int q = 0; q < TPB / 32; ++q) {
-      const uint32_t a0 = S.ws[q][0], b0 = S.ws[q][1], c0 = S.ws[q][2];
-      if (q < warp) { Ap += a0; Bp += b0; Cp += c0; Pp = max(Pp, S.ws[q][3]); Qp = max(Qp, S.ws[q][4]); }
-      TA += a0; TB += b0; TC += c0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ua = __shfl_up_sync(0xffffffffu, Ai, o), ub = __shfl_up_sync(0xffffffffu, Bi, o);
+      const uint32_t uc = __shfl_up_sync(0xffffffffu, Ci, o), um = __shfl_up_sync(0xffffffffu, Mi, o);
+      if (lane >= o) { Ai += ua; Bi += ub; Ci += uc; Mi = __vmaxu2(Mi, um); }
     }
-    uint32_t Pe = __shfl_up_sync(0xffffffffu, Pi, 1), Qe = __shfl_up_sync(0xffffffffu, Qi, 1);
-    if (lane == 0) { Pe = 0; Qe = 0; }
+    if (lane == 31) L.wtot[warp] = make_uint4(Ai, Bi, Ci, Mi);
+    __syncthreads();
+    // exclusive prefix over earlier warps: lane q < 8 holds warp q's totals
+    uint4 wq = lane < TPB / 32 ? L.wtot[lane] : make_uint4(0u, 0u, 0u, 0u);
+    uint32_t pa = wq.x, pb = wq.y, pc = wq.z, pm = wq.w;
+    uint32_t TA = 0, TB = 0, TC = 0;
+#pragma unroll
+    for (int o = 1; o < TPB / 32; o <<= 1) {
+      const uint32_t ua = __shfl_up_sync(0xffffffffu, pa, o), ub = __shfl_up_sync(0xffffffffu, pb, o);
+      const uint32_t uc = __shfl_up_sync(0xffffffffu, pc, o), um = __shfl_up_sync(0xffffffffu, pm, o);
+      if (lane >= o) { pa += ua; pb += ub; pc += uc; pm = __vmaxu2(pm, um); }
+    }
+    TA = __shfl_sync(0xffffffffu, pa, TPB / 32 - 1);
+    TB = __shfl_sync(0xffffffffu, pb, TPB / 32 - 1);
+    TC = __shfl_sync(0xffffffffu, pc, TPB / 32 - 1);
+    const int src = warp > 0 ? warp - 1 : 0;
+    const uint32_t Ap = warp ? __shfl_sync(0xffffffffu, pa, src) : 0u;
+    const uint32_t Bp = warp ? __shfl_sync(0xffffffffu, pb, src) : 0u;
+    const uint32_t Cp = warp ? __shfl_sync(0xffffffffu, pc, src) : 0u;
+    const uint32_t Mp = warp ? __shfl_sync(0xffffffffu, pm, src) : 0u;
+    uint32_t Me = __shfl_up_sync(0xffffffffu, Mi, 1);
+    if (lane == 0) Me = 0;
     const uint32_t Aex = Ap + Ai - A, Bex = Bp + Bi - B, Cex = Cp + Ci - C;
-    const uint32_t Pex = max(Pp, Pe), Qex = max(Qp, Qe);
+    const uint32_t Mex = __vmaxu2(Mp, Me);
+    const uint32_t Pex = Mex & 0xFFFFu, Qex = Mex >> 16;
     const uint32_t ex_in = Aex & 0xFFFFu, ex_br = Aex >> 16, ex_rd = Bex & 0xFFFFu, ex_wr = Bex >> 16;
-    const uint32_t T_rd = TB & 0xFFFFu, T_wr = TB >> 16, T_br = TA >> 16;
-    S.vpos[t] = ex_in + n_in - after;  // instructions in the tile at positions <= my last boundary
+    const uint32_t T_rd = TB & 0xFFFFu, T_wr = TB >> 16, T_br = TA >> 16, T_cl = TC >> 16;
+    L.vpos[t] = ex_in + n_in - after;  // instructions in the tile at positions <= my last boundary
     __syncthreads();
     // ---- carry-in for this thread ----
-    uint32_t seg, lid, byres;
+    uint32_t seg_in, lid, byres;
     if (Pex) {
       const uint32_t pos = Pex - 1;
-      seg = ex_in - S.vpos[pos >> 4];
+      seg_in = ex_in - L.vpos[pos >> 4];
       lid = (uint32_t)pay_at(S.pay[s], pos);
       byres = S.kind[s][pos] == AIWC_K_WI_RESUME;
     } else {
-      seg = cseg + ex_in; lid = clid; byres = cbyres;
+      seg_in = cseg + ex_in; lid = clid; byres = cbyres;
     }
     uint32_t gkey = Qex ? (uint32_t)pay_at(S.pay[s], Qex - 1) : cgkey;
     uint32_t gseq = cgseq + (Cex & 0xFFFFu);
     uint32_t o_rd = ex_rd, o_wr = T_rd + ex_wr;
     uint32_t o_br = (DENSE ? 0u : T_rd + T_wr) + ex_br;
     uint32_t o_cl = Cex >> 16;
-    const uint32_t T_cl = TC >> 16;
     // ---- fold my 16 events, one converged loop per event class ----
     const uint64_t* prow = &S.pay[s][t * 16];
     const uint32_t sw = t & 7;
 #define PAY(j) prow[((((uint32_t)(j) >> 1) ^ sw) << 1) | ((uint32_t)(j) & 1u)]
-    // instructions: opcode / width histograms
-    for (uint32_t m = ins16; m; m &= m - 1) {
-      const uint32_t j = __ffs(m) - 1;
-      const uint64_t p = PAY(j);
-      const uint32_t opc = (uint32_t)(p >> 32), wd = (uint32_t)p;
-      if (opc < OBINS) ++opc_col[opc * TPB];
-      else if (opc < a.n_opcodes) atomicAdd(&a.opc_counts[opc], 1ull);
-      else flags |= F_BAD_OPCODE;
-      if (wd - 1u < (uint32_t)WBINS) {
-        ++wid_col[(wd - 1) * TPB];
-        if (!((seen_w >> (wd - 1)) & 1u)) {
-          seen_w |= 1u << (wd - 1);
-          atomicMin(&S.wfirst[wd - 1], (unsigned long long)(e0 + j));
+    // instructions: opcode / width histograms in lane-private bins
+    uint32_t slow16 = 0, tseen = 0;
+    for (uint32_t m = ins16; m;) {  // two events per iteration for ILP
+      const uint32_t j0 = __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t j1 = m ? __ffs(m) - 1 : j0;
+      const bool two = m != 0;
+      m &= m - 1;
+      const uint64_t p0 = PAY(j0), p1 = PAY(j1);
+      const uint32_t o0 = (uint32_t)(p0 >> 32), b0 = (uint32_t)p0 - 1u;
+      const uint32_t o1 = (uint32_t)(p1 >> 32), b1 = (uint32_t)p1 - 1u;
+      const bool f0 = (o0 < (uint32_t)OBINS) & (b0 < (uint32_t)WBINS);
+      const bool f1 = two & (o1 < (uint32_t)OBINS) & (b1 < (uint32_t)WBINS);
+      if (f0) { ++opc_col[o0 * TPB]; ++wid_col[b0 * TPB]; }
+      if (f1) { ++opc_col[o1 * TPB]; ++wid_col[b1 * TPB]; }
+      tseen |= (f0 ? 1u << b0 : 0u) | (f1 ? 1u << b1 : 0u);
+      slow16 |= (f0 ? 0u : 1u << j0) | ((two & !f1) ? 1u << j1 : 0u);
+    }
+    if (__any_sync(0xffffffffu, (slow16 | (tseen & ~seen_w)) != 0)) {
+      for (uint32_t fresh = tseen & ~seen_w; fresh; fresh &= fresh - 1) {  // first sight of a width
+        const uint32_t wb = __ffs(fresh) - 1;
+        for (uint32_t m = ins16 & ~slow16; m; m &= m - 1) {
+          const uint32_t j = __ffs(m) - 1;
+          if ((uint32_t)PAY(j) - 1u == wb) { atomicMin(&L.wfirst[wb], (unsigned long long)(e0 + j)); break; }
         }
-      } else if (wd < WIDTH_TABLE) {
-        atomicAdd(&a.width_count[wd], 1ull);
-        atomicMin(&a.width_first[wd], (unsigned long long)(e0 + j));
-      } else {
-        flags |= F_BAD_WIDTH;
+      }
+      seen_w |= tseen;
+      for (uint32_t m = slow16; m; m &= m - 1) {
+        const uint32_t j = __ffs(m) - 1;
+        const uint64_t p = PAY(j);
+        const uint32_t opc = (uint32_t)(p >> 32), wd = (uint32_t)p;
+        if (opc < OBINS) ++opc_col[opc * TPB];
+        else if (opc < a.n_opcodes) atomicAdd(&a.opc_counts[opc], 1ull);
+        else flags |= F_BAD_OPCODE;
+        if (wd - 1u < (uint32_t)WBINS) {
+          ++wid_col[(wd - 1) * TPB];
+          if (!((seen_w >> (wd - 1)) & 1u)) {
+            seen_w |= 1u << (wd - 1);
+            atomicMin(&L.wfirst[wd - 1], (unsigned long long)(e0 + j));
+          }
+        } else if (wd < WIDTH_TABLE) {
+          atomicAdd(&a.width_count[wd], 1ull);
+          atomicMin(&a.width_first[wd], (unsigned long long)(e0 + j));
+        } else {
+          flags |= F_BAD_WIDTH;
+        }
       }
     }
     // memory accesses: dense-table counters or compaction
-    for (uint32_t m = rd16 | wr16; m; m &= m - 1) {
+    if (DENSE) {
+      for (uint32_t m = rd16 | wr16; m;) {  // two events per iteration for ILP
+        const uint32_t j0 = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t j1 = m ? __ffs(m) - 1 : j0;
+        const bool two = m != 0;
+        m &= m - 1;
+        const uint64_t p0 = PAY(j0), p1 = PAY(j1);
+        const uint64_t off0 = p0 - a.am.base, off1 = p1 - a.am.base;
+        const uint64_t key0 = off0 >> a.am.k, key1 = off1 >> a.am.k;
+        const bool v0 = (p0 >= a.am.base) & (((uint32_t)off0 & (uint32_t)a.am.low_mask) == (uint32_t)a.am.low_const) &
+                        (key0 < a.am.n_keys);
+        const bool v1 = (p1 >= a.am.base) & (((uint32_t)off1 & (uint32_t)a.am.low_mask) == (uint32_t)a.am.low_const) &
+                        (key1 < a.am.n_keys);
+        if (v0) atomicAdd(&a.dense[key0], ((wr16 >> j0) & 1u) ? (1ull << 32) : 1ull);
+        if (two & v1) atomicAdd(&a.dense[key1], ((wr16 >> j1) & 1u) ? (1ull << 32) : 1ull);
+        flags |= (v0 & (v1 | !two)) ? 0ull : (unsigned long long)F_ADDR_HINT;
+      }
+    }
+    for (uint32_t m = DENSE ? 0u : (rd16 | wr16); m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint64_t p = PAY(j);
       const bool isw = (wr16 >> j) & 1u;
-      if (DENSE) {
-        const uint64_t off = p - a.am.base;
-        const uint64_t key = off >> a.am.k;
-        if (p < a.am.base || (off & a.am.low_mask) != a.am.low_const || key >= a.am.n_keys) flags |= F_ADDR_HINT;
-        else atomicAdd(&a.dense[key], isw ? (1ull << 32) : 1ull);
-      } else {
+      {
         S.stage_out[isw ? o_wr++ : o_rd++] = p;
         amin = min(amin, (unsigned long long)p); amax = max(amax, (unsigned long long)p);
         aand &= p; aor |= p;
@@ -473,7 +543,6 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     }
     // rare events in stream order: segment opens / closes, branches, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
-    const uint32_t seg_in = seg;
     int last_b = -1;  // my last boundary position so far
     for (uint32_t m = rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
@@ -494,8 +563,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
                               (last_b < 0 ? seg_in : 0u);
           const uint32_t gz = (gseq & 0x3FFFFFFFu) | ((k & 0x80u) << 24) | (byres << 30);
           if (gseq >> 30) flags |= F_BAD_GROUP;
-          if (o_cl < (uint32_t)BND_CAP) S.closes[o_cl] = make_uint4(cl, lid, gz, 0u);
-          else do_close(S, a, cl, lid, gz, itb_sum, ipt_sum, flags);
+          if (o_cl < (uint32_t)BND_CAP) L.closes[o_cl] = make_uint4(cl, lid, gz, 0u);
+          else do_close(L, a, cl, lid, gz, itb_sum, ipt_sum, flags);
           ++o_cl;
         }
         last_b = (int)j;
@@ -506,13 +575,15 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       }
     }
 #undef PAY
-    seg = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
-    if (t == TPB - 1) { S.nc[0] = seg; S.nc[1] = lid; S.nc[2] = byres; S.nc[3] = gseq; S.nc[4] = gkey; }
+    if (t == TPB - 1) {
+      L.nc[0] = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
+      L.nc[1] = lid; L.nc[2] = byres; L.nc[3] = gseq; L.nc[4] = gkey;
+    }
     __syncthreads();
     // ---- segment closes of the tile, all threads converged ----
     for (uint32_t i = t; i < min(T_cl, (uint32_t)BND_CAP); i += TPB) {
-      const uint4 c = S.closes[i];
-      do_close(S, a, c.x, c.y, c.z, itb_sum, ipt_sum, flags);
+      const uint4 c = L.closes[i];
+      do_close(L, a, c.x, c.y, c.z, itb_sum, ipt_sum, flags);
     }
     // ---- flush ordered compaction ----
     if (STAGE) {
@@ -523,7 +594,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       const uint32_t bb = DENSE ? 0u : T_rd + T_wr;
       for (uint32_t i = t; i < T_br; i += TPB) a.br_out[c_br + i] = S.stage_out[bb + i];
     }
-    cseg = S.nc[0]; clid = S.nc[1]; cbyres = S.nc[2]; cgseq = S.nc[3]; cgkey = S.nc[4];
+    cseg = L.nc[0]; clid = L.nc[1]; cbyres = L.nc[2]; cgseq = L.nc[3]; cgkey = L.nc[4];
     c_rd += T_rd; c_wr += T_wr; c_br += T_br;
     // ---- refill this stage ----
     if (t == 0 && it + STAGES < my_tiles) {
@@ -534,15 +605,15 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         tma_load_2d(S.pay[s], &pmap, 0, (int)r2, &S.bar[s]);
       }
     }
-    if ((it + 1) % PRIV_FLUSH_TILES == 0) flush_private(S, a, t);
+    if ((it + 1) % PRIV_FLUSH_TILES == 0) flush_private(L, a, t);
   }
 
   // ---- epilogue: flush CTA-private state ----
-  flush_private(S, a, t);
-  if (t >= 32 && t < 32 + WBINS && S.wfirst[t - 32] != ~0ull) atomicMin(&a.width_first[t - 32 + 1], S.wfirst[t - 32]);
+  flush_private(L, a, t);
+  if (t >= 32 && t < 32 + WBINS && L.wfirst[t - 32] != ~0ull) atomicMin(&a.width_first[t - 32 + 1], L.wfirst[t - 32]);
   for (int i = t; i < HBINS; i += TPB) {
-    if (S.itb_h[i]) atomicAdd(&st->itb_hist[i], (unsigned long long)S.itb_h[i]);
-    if (S.ipt_h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)S.ipt_h[i]);
+    if (L.itb_h[i]) atomicAdd(&st->itb_hist[i], (unsigned long long)L.itb_h[i]);
+    if (L.ipt_h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)L.ipt_h[i]);
   }
   itb_sum = warp_sum(itb_sum);
   ipt_sum = warp_sum(ipt_sum);
@@ -572,7 +643,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
 template <bool DENSE, bool STAGE>
 static cudaError_t launch_variant(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap,
                                   uint32_t n_ctas, cudaStream_t s) {
-  const size_t smem = sizeof(IngestSmem) + (STAGE ? (TILE - 1) * sizeof(uint64_t) : 0) + 1024;
+  const size_t smem = sizeof(StageSmem) + (STAGE ? (TILE - 1) * sizeof(uint64_t) : 0) + 1024;
   cudaError_t e = cudaFuncSetAttribute(ingest_kernel<DENSE, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

@@ -33,154 +33,7 @@ __device__ __forceinline__ double plogp(unsigned long long c, double m) {
   return p * log2(p);
 }
 
-// level index j (key-space shift) -> smem histogram; big counts -> fp64 term
-struct LevelAcc {
-  uint32_t* h;           // smem [NLEVELS][CBINS]
-  double part[NLEVELS];  // sum of p log2 p over counts >= CBINS
-  unsigned long long* ovf;
-  unsigned long long* ovf_n;
-  double m;
-  __device__ __forceinline__ void rec(int j, unsigned long long c, uint32_t mult) {
-    if (c == 0) return;
-    if (c < (unsigned long long)CBINS) {
-      atomicAdd(&h[j * CBINS + c], mult);
-    } else {
-      part[j] += plogp(c, m) * mult;
-      if (j == 0)
-        for (uint32_t i = 0; i < mult; ++i) ovf[atomicAdd(ovf_n, 1ull)] = c;
-    }
-  }
-};
-
-constexpr int DS_T = 128;         // 4 warps x 8 keys per lane = 1024 keys per chunk
-constexpr int DS_K = 8;
-constexpr int DS_CHUNK = DS_T * DS_K;
-
-__device__ __forceinline__ void flush_levels(LevelAcc& L, int nlev, DevState* st, double* partials, uint32_t n_parts,
-                                             unsigned long long ur, unsigned long long uw, unsigned long long fp) {
-  // per-level fp64 partials: fixed-order block reduction (deterministic)
-  __shared__ double red[DS_T / 32][NLEVELS];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = 0; j < nlev; ++j) {
-    double v = L.part[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][j] = v;
-  }
-  ur = warp_sum(ur); uw = warp_sum(uw); fp = warp_sum(fp);
-  if (lane == 0) {
-    if (ur) atomicAdd(&st->unique_r, ur);
-    if (uw) atomicAdd(&st->unique_w, uw);
-    if (fp) atomicAdd(&st->footprint, fp);
-  }
-  __syncthreads();
-  if (threadIdx.x < nlev) {
-    double v = 0.0;
-    for (int w = 0; w < DS_T / 32; ++w) v += red[w][threadIdx.x];
-    partials[threadIdx.x * n_parts + blockIdx.x] = v;
-  }
-  for (int i = threadIdx.x; i < nlev * CBINS; i += DS_T) {
-    const uint32_t v = L.h[i];
-    if (v) {
-      if (i < CBINS) atomicAdd(&st->cnt_hist0[i], (unsigned long long)v);
-      else atomicAdd(&st->cnt_hist[i / CBINS][i % CBINS], (unsigned long long)v);
-    }
-  }
-}
-
-// one sweep over the dense key table
-__global__ void __launch_bounds__(DS_T) dense_stats_kernel(const unsigned long long* __restrict__ tab,
-                                                           uint64_t n_keys, int nlev, double m, DevState* st,
-                                                           double* partials, uint32_t n_parts,
-                                                           unsigned long long* lvl0_ovf) {
-  extern __shared__ uint32_t hsm[];
-  __shared__ unsigned long long wsum[DS_T / 32];
-  for (int i = threadIdx.x; i < nlev * CBINS; i += DS_T) hsm[i] = 0;
-  LevelAcc L;
-  L.h = hsm; L.m = m; L.ovf = lvl0_ovf; L.ovf_n = &st->lvl0_ovf_n;
-#pragma unroll
-  for (int j = 0; j < NLEVELS; ++j) L.part[j] = 0.0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long ur = 0, uw = 0, fp = 0;
-  const uint64_t n_chunks = (n_keys + DS_CHUNK - 1) / DS_CHUNK;
-  for (uint64_t ch = blockIdx.x; ch < n_chunks; ch += gridDim.x) {
-    const uint64_t k0 = ch * DS_CHUNK + (uint64_t)threadIdx.x * DS_K;
-    unsigned long long c[DS_K];
-    if (k0 + DS_K <= n_keys) {
-      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + k0);
-#pragma unroll
-      for (int q = 0; q < DS_K / 2; ++q) {
-        const ulonglong2 v = p[q];
-        c[2 * q] = v.x; c[2 * q + 1] = v.y;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < DS_K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : 0ull;
-    }
-    // level 0: per-key totals; uniqueness flags
-#pragma unroll
-    for (int i = 0; i < DS_K; ++i) {
-      const unsigned long long r = c[i] & 0xFFFFFFFFull, w = c[i] >> 32;
-      ur += r != 0; uw += w != 0; fp += (r | w) != 0;
-      c[i] = r + w;
-    }
-    {  // run-length aggregate the thread's 8 level-0 counts
-      unsigned long long cur = c[0];
-      uint32_t run = 1;
-#pragma unroll
-      for (int i = 1; i < DS_K; ++i) {
-        if (c[i] == cur) { ++run; }
-        else { L.rec(0, cur, run); cur = c[i]; run = 1; }
-      }
-      L.rec(0, cur, run);
-    }
-    // levels 1..3 inside the thread
-    unsigned long long s1[4], s2[2], s3;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
-    s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
-    s3 = s2[0] + s2[1];
-    if (nlev > 1) {
-      if (s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3]) L.rec(1, s1[0], 4);
-      else { L.rec(1, s1[0], 1); L.rec(1, s1[1], 1); L.rec(1, s1[2], 1); L.rec(1, s1[3], 1); }
-    }
-    if (nlev > 2) {
-      if (s2[0] == s2[1]) L.rec(2, s2[0], 2);
-      else { L.rec(2, s2[0], 1); L.rec(2, s2[1], 1); }
-    }
-    if (nlev > 3) L.rec(3, s3, 1);
-    // levels 4..8 across lanes
-    unsigned long long s = s3;
-#pragma unroll
-    for (int j = 4; j <= 8; ++j) {
-      s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
-      if (j < nlev && (lane & ((1 << (j - 3)) - 1)) == 0) L.rec(j, s, 1);
-    }
-    // levels 9, 10 across warps
-    if (nlev > 9) {
-      if (lane == 0) wsum[warp] = s;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        L.rec(9, wsum[0] + wsum[1], 1);
-        L.rec(9, wsum[2] + wsum[3], 1);
-        if (nlev > 10) L.rec(10, wsum[0] + wsum[1] + wsum[2] + wsum[3], 1);
-      }
-      __syncthreads();
-    }
-  }
-  __syncthreads();
-  flush_levels(L, nlev, st, partials, n_parts, ur, uw, fp);
-}
-
-void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
-                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s) {
-  const int nlev = k >= 10 ? 1 : 11 - (int)k;
-  const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
-  cudaFuncSetAttribute(dense_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dense_stats_kernel<<<n_ctas, DS_T, smem, s>>>(tab, n_keys, nlev, (double)total_m, st, partials, n_ctas,
-                                                reinterpret_cast<unsigned long long*>(lvl0_ovf));
-}
+constexpr int DS_T = 128;  // threads per count-statistics CTA
 
 // ---------------------------------------------------------------------------
 // count statistics over a compact count array (sparse path, one level)
