@@ -35,7 +35,7 @@ from aiwc import errors as E  # noqa: E402
 from aiwc.buffers import make_buffer  # noqa: E402
 from aiwc.ir import parse_kernel  # noqa: E402
 from aiwc.metrics import consume, finalize  # noqa: E402
-from aiwc.report import derive, report_to_dict  # noqa: E402
+from aiwc.report import derive, emit_report, report_to_dict  # noqa: E402
 from aiwc.sim import NDRangeConfig, simulate  # noqa: E402
 from aiwc.trace import (  # noqa: E402
     Barrier, Branch, Instruction, KernelBegin, KernelEnd, Memory, WorkGroupBegin, WorkGroupEnd,
@@ -105,6 +105,15 @@ def encode(events):
     return np.array(kinds, np.uint8), np.array(pays, np.uint64), meta
 
 
+def repr_events(events):
+    """JSON-able event list: [class name, *fields] with nested tuples as lists."""
+    def conv(x):
+        if isinstance(x, tuple):
+            return [conv(v) for v in x]
+        return x
+    return [[type(e).__name__, *[conv(v) for v in e]] for e in events]
+
+
 def load_kernel(name):
     with open(os.path.join(REF, "kernels", name), encoding="utf-8") as fp:
         return parse_kernel(fp.read())
@@ -114,6 +123,13 @@ def sim(kernel, gsz, lsz, bufs):
     volume = gsz[0] * gsz[1] * gsz[2]
     cfg = NDRangeConfig(gsz, lsz, {k: make_buffer(v, volume) for k, v in bufs.items()})
     return simulate(load_kernel(kernel), cfg)
+
+
+def sim_inv(kernel, n, invocation):
+    from aiwc.sim import simulate as _sim
+
+    cfg = NDRangeConfig((n, 1, 1), (min(n, 64), 1, 1), {"a": make_buffer("iota", n)})
+    return _sim(load_kernel(kernel), cfg, invocation=invocation)
 
 
 WI0 = WorkItemId((0, 0, 0), (0, 0, 0), (0, 0, 0))
@@ -241,7 +257,66 @@ def expected(events, cap=None):
         rep = finalize(acc)
     except E.TraceTooLarge as exc:
         return {"error": "TraceTooLarge", "entries": exc.entries, "cap": exc.cap}
-    return {"report": report_to_dict(rep, derive(rep))}
+    return {"report": report_to_dict(rep, derive(rep)),
+            "json": emit_report(rep).decode("utf-8"), "csv": emit_report(rep, format="csv").decode("utf-8")}
+
+
+def invalid_cases():
+    """Streams violating one StreamChecker rule each (trace.py:278-286), with the
+    reference's InvalidStream (event index, rule, message) or TraceTooLarge."""
+    base = one_item(instrs(2) + [Instruction("load", 1), Memory("load", 64)])
+    wi_b = WorkItemId((1, 0, 0), (1, 0, 0), (0, 0, 0))
+    out = {
+        "not_kernel_begin_first": [Instruction("add", 1)] + base,
+        "empty": [],
+        "event_after_end": base + [Instruction("add", 1)],
+        "no_kernel_end": base[:-1],
+        "duplicate_kernel_begin": base[:1] + base,
+        "outside_segment_instr": base[:2] + [Instruction("add", 1)] + base[2:],
+        "outside_segment_mem": base[:2] + [Memory("load", 4)] + base[2:],
+        "outside_segment_branch": base[:2] + [Branch(3, True)] + base[2:],
+        "outside_segment_barrier": base[:2] + [Barrier()] + base[2:],
+        "kernel_end_open_group": base[:-2] + [KernelEnd()],
+        "wg_begin_nested": base[:2] + [WorkGroupBegin((0, 0, 0))] + base[2:],
+        "wg_end_mismatch": base[:-2] + [WorkGroupEnd((1, 0, 0)), KernelEnd()],
+        "wg_end_open_segment": base[:-3] + [WorkGroupEnd((0, 0, 0)), KernelEnd()],
+        "wi_outside_group": [base[0], WorkItemBegin(WI0)] + base[1:],
+        "wi_other_group": [KernelBegin("k", 0, (2, 1, 1), (1, 1, 1)), WorkGroupBegin((0, 0, 0)),
+                           WorkItemBegin(WorkItemId((1, 0, 0), (0, 0, 0), (1, 0, 0))), WorkItemEnd(WI0),
+                           WorkGroupEnd((0, 0, 0)), KernelEnd()],
+        "wi_local_range": [KernelBegin("k", 0, (2, 1, 1), (1, 1, 1)), WorkGroupBegin((0, 0, 0)),
+                           WorkItemBegin(WorkItemId((1, 0, 0), (1, 0, 0), (0, 0, 0))), WorkItemEnd(WI0),
+                           WorkGroupEnd((0, 0, 0)), KernelEnd()],
+        "wi_gid_arith": [KernelBegin("k", 0, (2, 1, 1), (2, 1, 1)), WorkGroupBegin((0, 0, 0)),
+                         WorkItemBegin(WorkItemId((0, 0, 0), (1, 0, 0), (0, 0, 0))),
+                         WorkGroupEnd((0, 0, 0)), KernelEnd()],
+        "segment_while_open": stream([WorkItemBegin(WI0), WorkItemBegin(wi_b), WorkItemEnd(wi_b), WorkItemEnd(WI0)]),
+        "wi_begin_twice": stream([WorkItemBegin(WI0), WorkItemEnd(WI0), WorkItemBegin(WI0), WorkItemEnd(WI0)]),
+        "resume_without_barrier": stream([WorkItemBegin(WI0), WorkItemEnd(WI0), WorkItemResume(WI0), WorkItemEnd(WI0)]),
+        "end_without_open": stream([WorkItemBegin(WI0), WorkItemEnd(WI0), WorkItemEnd(WI0)]),
+        "unfinished": stream([WorkItemBegin(WI0), Barrier(), WorkItemBegin(wi_b), WorkItemEnd(wi_b)]),
+        "barrier_divergence": stream([WorkItemBegin(WI0), Barrier(), WorkItemBegin(wi_b), WorkItemEnd(wi_b),
+                                      WorkItemResume(WI0), WorkItemEnd(WI0)]),
+        # cap crossing before a violation wins; after it, the violation wins (SURVEY App. C #7)
+        "cap_before_violation": [KernelBegin("k", 0, (1, 1, 1), (1, 1, 1)), WorkGroupBegin((0, 0, 0)), WorkItemBegin(WI0)]
+                                + [e for k in range(6) for e in (Instruction("load", 1), Memory("load", 8 * k))]
+                                + [WorkItemEnd(WI0), Barrier(), WorkGroupEnd((0, 0, 0)), KernelEnd()],
+        "branch_cap_then_violation": [KernelBegin("k", 0, (1, 1, 1), (1, 1, 1)), WorkGroupBegin((0, 0, 0)),
+                                      WorkItemBegin(WI0)] + [Instruction("br", 1), Branch(2, True)] * 5
+                                     + [WorkItemEnd(WI0), Instruction("add", 1), WorkGroupEnd((0, 0, 0)), KernelEnd()],
+    }
+    return out
+
+
+def expected_error(events, cap=None):
+    try:
+        acc = consume(iter(events), max_entries=cap)
+        finalize(acc)
+    except E.InvalidStream as exc:
+        return {"error": "InvalidStream", "event_index": exc.event_index, "rule": exc.rule, "message": str(exc)}
+    except E.TraceTooLarge as exc:
+        return {"error": "TraceTooLarge", "entries": exc.entries, "cap": exc.cap}
+    return {"error": None}
 
 
 def main():
@@ -279,6 +354,31 @@ def main():
     # on device by the synthetic generator (checked against the simulator below).
     add("C1_sweep4_262144", sim("sweep4.aiwck", (262144, 1, 1), (64, 1, 1), {"a": "iota"}), store_trace=False)
 
+    # merges (metrics.py:235-270; pkg/tests/test_metrics.py:264-303, test_acceptance.py:228-243)
+    from aiwc.metrics import merge_accumulators
+
+    def sweep_part(offset, n, invocation=0, name="k"):
+        return one_item([e for i in range(n) for e in (Instruction("load", 1), Memory("load", offset + 4 * i))],
+                        invocation=invocation, name=name)
+
+    merges = {
+        "self": ([sweep_part(4096, 256, 0), sweep_part(4096, 256, 1)], False),
+        "disjoint": ([sweep_part(4096, 256, 0), sweep_part(4096 + 4 * 256, 256, 1)], False),
+        "names": ([sweep_part(4096, 8, 0, "x"), sweep_part(8192, 8, 1, "y")], True),
+        "invocations": ([sim_inv("sweep4.aiwck", n, inv) for inv, n in enumerate((1024, 512, 256, 128))], False),
+        "random": ([random_events(random.Random(70 + i), 3000) for i in range(3)], True),
+        "branchy": ([sim("bfs_flags.aiwck", (2048, 1, 1), (256, 1, 1), {"flags": "bernoulli:0.5:seed=%d" % s,
+                                                                          "out": "zeros"}) for s in (1, 2)], False),
+    }
+    for mname, (parts, allow) in merges.items():
+        names = []
+        for i, ev in enumerate(parts):
+            names.append(f"merge_{mname}_part{i}")
+            add(names[-1], ev)
+        rep = finalize(merge_accumulators([consume(ev) for ev in parts], allow_name_mismatch=allow))
+        cases.append({"name": f"merge_{mname}", "merge": names, "allow_name_mismatch": allow,
+                      "report": report_to_dict(rep, derive(rep))})
+
     rng = random.Random(202)  # pkg/tests/test_metrics.py:306-313
     for i in range(60):
         add(f"random202_{i}", random_events(rng, 2500))
@@ -288,6 +388,14 @@ def main():
 
     np.savez_compressed(os.path.join(OUT, "traces.npz"),
                         kind=np.concatenate(kinds), payload=np.concatenate(pays))
+
+
+    inv = []
+    for name, ev in invalid_cases().items():
+        for cap in (None, 3):
+            inv.append({"name": f"{name}_cap{cap}", "cap": cap, "events": repr_events(ev), **expected_error(ev, cap)})
+    with open(os.path.join(OUT, "invalid.json"), "w", encoding="utf-8") as fp:
+        json.dump(inv, fp, indent=1)
     with open(os.path.join(OUT, "cases.json"), "w", encoding="utf-8") as fp:
         json.dump({"generator": "tests/golden/make_golden.py", "reference": "/root/reference/pkg (aiwc 0.1.0)",
                    "cases": cases}, fp, indent=1)
