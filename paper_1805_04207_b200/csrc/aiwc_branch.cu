@@ -12,8 +12,18 @@
 // executions with the same group id -- is a maximal run of equal
 // (record >> 1).  Execution i is an observation iff its run started at least
 // H executions earlier; its pattern is the previous H outcomes, oldest as MSB
-// (entropy.py:112-114).  Observations land in one pooled 2^H table of
-// (total << 32 | taken) counters.
+// (entropy.py:112-114).  Observations are counted into one pooled 2^H table.
+//
+//   branch_stage_kernel    one coalesced pass: record -> byte (taken | head << 1),
+//                          plus the (site, first position) list
+//   pattern_count_kernel   blocks = record chunks x pattern partitions; each
+//                          block walks its chunk (16-record warm-up halo) and
+//                          counts the observations of its 2^14-pattern partition
+//                          in shared memory (no global atomics, no contention
+//                          between blocks), then writes its partition to a
+//                          per-chunk partial table
+//   pattern_reduce_kernel  sums the per-chunk partials into the table
+//   branch_finish_kernel   yokota / linear in fixed reduction order
 #include <math.h>
 
 #include <algorithm>
@@ -22,46 +32,21 @@
 
 namespace aiwc {
 
-constexpr int PT_T = 256;
-constexpr int PT_CHUNK = 64;  // records per thread
+constexpr int PC_T = 512;                 // threads per counting block
+constexpr int PC_PER = 32;                // records per thread per step
+constexpr int PC_HALO = 16;               // warm-up window (>= history_len)
+constexpr int PC_PART_BITS = 14;          // patterns per partition: 2^14 (128 KB of counters)
+constexpr int PC_CHUNK_ALIGN = 16;
 
-__global__ void __launch_bounds__(PT_T) pattern_kernel(const uint64_t* __restrict__ rec, uint64_t n, uint32_t H,
-                                                       unsigned long long* __restrict__ tab) {
-  const uint32_t mask = (H >= 32) ? 0xFFFFFFFFu : ((1u << H) - 1u);
-  for (uint64_t c0 = ((uint64_t)blockIdx.x * PT_T + threadIdx.x) * PT_CHUNK; c0 < n;
-       c0 += (uint64_t)gridDim.x * PT_T * PT_CHUNK) {
-    const uint64_t c1 = min(n, c0 + PT_CHUNK);
-    const uint64_t s0 = c0 >= H ? c0 - H : 0;
-    uint64_t prev = s0 > 0 ? (rec[s0 - 1] >> 1) : ~0ull;
-    uint32_t since = s0 > 0 ? H : 0, hist = 0;
-    uint32_t run_pat = 0xFFFFFFFFu;
-    unsigned long long run_val = 0;
-    for (uint64_t i = s0; i < c1; ++i) {
-      const uint64_t r = rec[i];
-      const uint64_t key = r >> 1;
-      const uint32_t bit = (uint32_t)(r & 1);
-      if (i == 0 || key != prev) { since = 0; hist = 0; }
-      if (i >= c0 && since >= H) {
-        if (hist != run_pat) {
-          if (run_val) atomicAdd(&tab[run_pat], run_val);
-          run_pat = hist; run_val = 0;
-        }
-        run_val += (1ull << 32) | bit;
-      }
-      hist = ((hist << 1) | bit) & mask;
-      since = min(since + 1, H);
-      prev = key;
-    }
-    if (run_val) atomicAdd(&tab[run_pat], run_val);
-  }
-}
-
-// site boundaries of the site-sorted records: (site, first position)
-__global__ void site_heads_kernel(const uint64_t* __restrict__ rec, uint64_t n, DevState* st,
-                                  unsigned long long* big_list) {
+__global__ void branch_stage_kernel(const uint64_t* __restrict__ rec, uint64_t n, uint8_t* __restrict__ bits,
+                                    DevState* st, unsigned long long* big_list) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t site = rec[i] >> 32;
-    if (i == 0 || (rec[i - 1] >> 32) != site) {
+    const uint64_t r = rec[i];
+    const uint64_t prev = i ? rec[i - 1] : ~r;
+    const bool head = (i == 0) || ((prev >> 1) != (r >> 1));
+    bits[i] = (uint8_t)((r & 1) | (head ? 2 : 0));
+    const uint64_t site = r >> 32;
+    if (i == 0 || (prev >> 32) != site) {
       const unsigned long long j = atomicAdd(&st->n_sites, 1ull);
       if (j < (unsigned long long)MAX_SMALL_LIST) {
         st->site_list[2 * j] = site; st->site_list[2 * j + 1] = i;
@@ -69,6 +54,103 @@ __global__ void site_heads_kernel(const uint64_t* __restrict__ rec, uint64_t n, 
       big_list[2 * j] = site; big_list[2 * j + 1] = i;
     }
   }
+}
+
+__device__ __forceinline__ uint32_t byte_at(const uint8_t* bits, int64_t g, uint64_t n) {
+  return (g < 0 || (uint64_t)g >= n) ? 2u : bits[g];  // outside the array: a stream head
+}
+
+constexpr uint32_t NO_OBS = 0xFFFFFFFFu;
+
+// One walk over the staged bytes: code[i] = pattern << 1 | taken when record i
+// is an observation, NO_OBS otherwise.  Thread = 32 consecutive records after a
+// 16-record warm-up; starting "saturated" is exact because any head inside the
+// window resets it.
+__global__ void __launch_bounds__(256) pattern_walk_kernel(const uint8_t* __restrict__ bits, uint64_t n, uint32_t H,
+                                                           uint32_t* __restrict__ code) {
+  const uint32_t mask = (1u << H) - 1u;
+  for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * PC_PER; s < n;
+       s += (uint64_t)gridDim.x * blockDim.x * PC_PER) {
+    uint32_t since = H, hist = 0;
+    uint32_t out[PC_PER];
+    const int64_t base = (int64_t)s - PC_HALO;
+    const bool aligned = base >= 0 && (uint64_t)(base + PC_HALO + PC_PER) <= n;
+    uint4 q[3];
+    if (aligned) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) q[k] = *reinterpret_cast<const uint4*>(bits + base + 16 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+      uint32_t word;
+      if (aligned) word = k % 4 == 0 ? q[k / 4].x : k % 4 == 1 ? q[k / 4].y : k % 4 == 2 ? q[k / 4].z : q[k / 4].w;
+      else
+        word = byte_at(bits, base + 4 * k, n) | (byte_at(bits, base + 4 * k + 1, n) << 8) |
+               (byte_at(bits, base + 4 * k + 2, n) << 16) | (byte_at(bits, base + 4 * k + 3, n) << 24);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = 4 * k + b;
+        const uint32_t v = (word >> (8 * b)) & 0xFFu;
+        if (v & 2) { since = 0; hist = 0; }
+        if (i >= PC_HALO) out[i - PC_HALO] = since >= H ? (hist << 1) | (v & 1) : NO_OBS;
+        hist = ((hist << 1) | (v & 1)) & mask;
+        since = min(since + 1, H);
+      }
+    }
+    if (s + PC_PER <= n) {
+      uint4* dst = reinterpret_cast<uint4*>(code + s);
+#pragma unroll
+      for (int k = 0; k < PC_PER / 4; ++k) dst[k] = make_uint4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < PC_PER; ++k)
+        if (s + k < n) code[s + k] = out[k];
+    }
+  }
+}
+
+// Counts the observations of one 2^14-pattern partition in one chunk of codes,
+// entirely in shared memory, and writes the partition to the chunk's partial table.
+__global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __restrict__ code, uint64_t n,
+                                                             uint32_t H, uint32_t n_parts, uint64_t chunk_len,
+                                                             unsigned long long* __restrict__ partials) {
+  extern __shared__ uint32_t cnt[];  // [2][part_size]: total, taken
+  const uint32_t part = blockIdx.x % n_parts, chunk = blockIdx.x / n_parts;
+  const uint32_t part_size = (1u << H) / n_parts;
+  const uint32_t shift = 31 - __clz(part_size) + 1;  // code >> shift = partition
+  uint32_t* tot = cnt;
+  uint32_t* tk = cnt + part_size;
+  for (uint32_t i = threadIdx.x; i < 2 * part_size; i += PC_T) cnt[i] = 0;
+  __syncthreads();
+  const uint64_t c0 = (uint64_t)chunk * chunk_len, c1 = min(n, c0 + chunk_len);
+  auto count = [&](uint32_t c) {
+    if (c != NO_OBS && (c >> shift) == part) {
+      const uint32_t slot = (c >> 1) & (part_size - 1);
+      atomicAdd(&tot[slot], 1u);
+      if (c & 1) atomicAdd(&tk[slot], 1u);
+    }
+  };
+  const uint64_t v0 = (c0 + 3) & ~3ull, v1 = c1 & ~3ull;  // uint4-aligned body
+  for (uint64_t i = c0 + threadIdx.x; i < min(v0, c1); i += PC_T) count(code[i]);
+  for (uint64_t i = v0 + 4ull * threadIdx.x; i + 4 <= v1; i += 4ull * PC_T) {
+    const uint4 q = *reinterpret_cast<const uint4*>(code + i);
+    count(q.x); count(q.y); count(q.z); count(q.w);
+  }
+  for (uint64_t i = max(v1, v0) + threadIdx.x; i < c1; i += PC_T) count(code[i]);
+  __syncthreads();
+  unsigned long long* out = partials + (uint64_t)chunk * (1u << H) + (uint64_t)part * part_size;
+  for (uint32_t i = threadIdx.x; i < part_size; i += PC_T)
+    out[i] = ((unsigned long long)tot[i] << 32) | tk[i];
+}
+
+// tab[p] = sum over chunks of the partial tables
+__global__ void pattern_reduce_kernel(const unsigned long long* __restrict__ partials, uint32_t chunks, uint32_t size,
+                                      unsigned long long* __restrict__ tab) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= size) return;
+  unsigned long long v = 0;
+  for (uint32_t c = 0; c < chunks; ++c) v += partials[(uint64_t)c * size + p];
+  tab[p] = v;
 }
 
 constexpr int BF_T = 1024;
@@ -116,29 +198,52 @@ __global__ void __launch_bounds__(BF_T) branch_finish_kernel(const unsigned long
   }
 }
 
-size_t branch_scratch_bytes(uint64_t n) {
-  return n * 8 /* sort tmp */ + radix_hist_bytes(n) + 2 * 8 * (n + 1) /* site list */ + 4096;
+// ---- launch geometry and scratch layout --------------------------------------
+static uint32_t n_parts_for(uint32_t H) { return H > PC_PART_BITS ? 1u << (H - PC_PART_BITS) : 1u; }
+static uint32_t n_chunks_for(uint64_t n, uint32_t parts) {
+  const uint32_t blocks_target = 148 * 2;  // 128 KB smem: at most one block per SM at a time
+  const uint32_t chunks = std::max<uint32_t>(1, blocks_target / parts);
+  const uint64_t min_len = (uint64_t)PC_T * PC_PER;
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunks, (n + min_len - 1) / min_len));
 }
+
+// [sort tmp (8n) = observation codes (4n) + stage bytes (n)][partial tables][radix histograms][site list]
+static uint64_t partial_bytes(uint64_t n) { return (uint64_t)n_chunks_for(n, 4) * (1ull << 16) * 8; }
+static uint64_t branch_tmp_bytes(uint64_t n) { return ((8 * n + 15) & ~15ull) + partial_bytes(n); }
+
+size_t branch_site_list_offset(uint64_t n) {
+  return ((branch_tmp_bytes(n) + 15) & ~15ull) + ((radix_hist_bytes(n) + 15) & ~size_t(15));
+}
+
+size_t branch_scratch_bytes(uint64_t n) { return branch_site_list_offset(n) + 2 * 8 * (n + 1) + 4096; }
 
 int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t history_len, DevState* st,
                  unsigned long long* tables, void* scratch, size_t scratch_bytes, cudaStream_t s) {
   (void)scratch_bytes;
   int kernels = 0;
   if (n == 0) return 0;
-  uint64_t* tmp = reinterpret_cast<uint64_t*>(scratch);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(tmp + n);
-  unsigned long long* big = reinterpret_cast<unsigned long long*>(
-      reinterpret_cast<uint8_t*>(hist) + ((radix_hist_bytes(n) + 15) & ~size_t(15)));
+  uint8_t* base = reinterpret_cast<uint8_t*>(scratch);
+  uint64_t* tmp = reinterpret_cast<uint64_t*>(base);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(base + ((branch_tmp_bytes(n) + 15) & ~15ull));
+  unsigned long long* big = reinterpret_cast<unsigned long long*>(base + branch_site_list_offset(n));
   if (site_bits) radix_sort_u64(recs, tmp, n, 32, 32 + (int)site_bits, hist, s, &kernels);
-  const uint64_t per = (uint64_t)PT_T * PT_CHUNK;
-  const uint32_t blocks = (uint32_t)std::min<uint64_t>((n + per - 1) / per, 148 * 8);
-  const uint32_t size = 1u << history_len;
-  cudaMemsetAsync(tables, 0, size * sizeof(unsigned long long), s);
-  pattern_kernel<<<blocks, PT_T, 0, s>>>(recs, n, history_len, tables);
-  const uint32_t hb = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 8);
-  site_heads_kernel<<<hb, 256, 0, s>>>(recs, n, st, big);
+  // after the sort the tmp region is free: observation codes + stage bytes
+  const uint32_t H = history_len, size = 1u << H;
+  const uint32_t parts = n_parts_for(H), chunks = n_chunks_for(n, parts);
+  uint32_t* code = reinterpret_cast<uint32_t*>(base);
+  uint8_t* bits = base + 4 * ((n + 3) & ~3ull);
+  unsigned long long* partials = reinterpret_cast<unsigned long long*>(base + ((8 * n + 15) & ~15ull));
+  const uint32_t sb = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 8);
+  branch_stage_kernel<<<sb, 256, 0, s>>>(recs, n, bits, st, big);
+  const uint32_t wb = (uint32_t)std::min<uint64_t>((n + 256 * PC_PER - 1) / (256 * PC_PER), 148 * 8);
+  pattern_walk_kernel<<<wb, 256, 0, s>>>(bits, n, H, code);
+  const uint64_t chunk_len = ((n + chunks - 1) / chunks + PC_CHUNK_ALIGN - 1) / PC_CHUNK_ALIGN * PC_CHUNK_ALIGN;
+  const size_t smem = 2 * (size_t)(size / parts) * sizeof(uint32_t);
+  cudaFuncSetAttribute(pattern_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pattern_count_kernel<<<chunks * parts, PC_T, smem, s>>>(code, n, H, parts, chunk_len, partials);
+  pattern_reduce_kernel<<<(size + 255) / 256, 256, 0, s>>>(partials, chunks, size, tables);
   branch_finish_kernel<<<1, BF_T, 0, s>>>(tables, size, st);
-  return kernels + 3;
+  return kernels + 5;
 }
 
 }  // namespace aiwc

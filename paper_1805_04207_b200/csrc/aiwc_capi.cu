@@ -522,7 +522,7 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   if (h.n_sites > (unsigned long long)MAX_SMALL_LIST) {
     big_sites.resize(2 * h.n_sites);
     // big list lives after the sort scratch inside branch_scr (see branch_stats)
-    const size_t off = ctx->n_br * 8 + ((radix_hist_bytes(ctx->n_br) + 15) & ~size_t(15));
+    const size_t off = branch_site_list_offset(ctx->n_br);
     CK(cudaMemcpyAsync(big_sites.data(), reinterpret_cast<uint8_t*>(ctx->branch_scr.p) + off, 2 * h.n_sites * 8,
                        cudaMemcpyDeviceToHost, s));
   }

@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     }
     const uint32_t close16 = bnd16 & ~p5;          // barrier / wi_end
     const uint32_t wgb16 = p6 & ~p7;               // wg_begin
-    const uint32_t rare16 = br16 | bnd16 | p5 | p6;  // branch, boundary, group, kernel events
+    const uint32_t rare16 = bnd16 | p5 | p6;       // boundary, group, kernel events
     const int lp = bnd16 ? 31 - __clz(bnd16) : -1;
     const int lw = wgb16 ? 31 - __clz(wgb16) : -1;
     const uint32_t n_in = __popc(ins16);
@@ -541,21 +541,30 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         aand &= p; aor |= p;
       }
     }
-    // rare events in stream order: segment opens / closes, branches, groups
+    // branches: ordered records site << 32 | group << 1 | taken; the group is the last
+    // wg_begin before the branch in my chunk, else my carry-in group
+    if (STAGE) {
+      for (uint32_t m = br16; m; m &= m - 1) {
+        const uint32_t j = __ffs(m) - 1;
+        const uint64_t p = PAY(j);
+        const uint32_t before = wgb16 & ((1u << j) - 1u);
+        const uint32_t g = before ? (uint32_t)PAY(31 - __clz(before)) : gkey;
+        const uint64_t site = p >> 1;
+        flags |= ((site >> 32) ? (unsigned long long)F_BAD_SITE : 0ull) | ((g >> 31) ? (unsigned long long)F_BAD_GROUP : 0ull);
+        max_site = max(max_site, (unsigned long long)site);
+        S.stage_out[o_br + __popc(br16 & ((1u << j) - 1u))] = (site << 32) | ((uint64_t)g << 1) | (p & 1);
+      }
+    } else if (br16) {
+      flags |= F_BAD_KIND;  // the launcher stages whenever branches exist
+    }
+    // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
     for (uint32_t m = rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t k = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
-      if (k == AIWC_K_BRANCH) {
-        const uint64_t site = p >> 1;
-        if (site >> 32) flags |= F_BAD_SITE;
-        if (gkey >> 31) flags |= F_BAD_GROUP;
-        max_site = max(max_site, (unsigned long long)site);
-        if (STAGE) S.stage_out[o_br++] = (site << 32) | ((uint64_t)gkey << 1) | (p & 1);
-        else flags |= F_BAD_KIND;  // the launcher stages whenever branches exist
-      } else if (k & 0x10) {
+      if (k & 0x10) {
         if (k & 0x20) {  // wi_begin / wi_resume opens a segment
           lid = (uint32_t)p; byres = k >> 7;
         } else {         // barrier / wi_end closes it: instructions since the open

@@ -178,6 +178,7 @@ size_t sparse_scratch_bytes(uint64_t m);
 int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t history_len, DevState* st,
                  unsigned long long* tables, void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t branch_scratch_bytes(uint64_t n);
+size_t branch_site_list_offset(uint64_t n);
 // utilities
 void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
                     cudaStream_t s, int* kernels);

@@ -48,8 +48,8 @@ __host__ __device__ inline bool synth_geo(int cfg, uint64_t W, SynthGeo* g) {
     case 3:
       g->LV = 256; g->per_group = 2 + 256 * 32; g->n_opc = 4;
       g->B = g->A + align4k(4 * 4 * W);      // scratch (1024 elements)
-      g->C = g->B + 4096;                    // gather table 2^28 elements
-      g->D = g->C + (1ull << 30);            // store target
+      g->C = g->B + 4096;                    // gather table: 4W elements (2^28 at 2^26 work-items)
+      g->D = g->C + 16 * W;                  // store target
       break;
     case 4: g->LV = 256; g->per_group = 2 + 256 * 322; g->n_opc = 5; break;
     case 5:
@@ -94,7 +94,7 @@ __host__ __device__ inline void wi_event(int cfg, const SynthGeo& g, uint64_t se
         *k = AIWC_K_LOAD;
         if (it < 4) *p = g.A + 4 * (4 * gid + it);
         else if (it < 8) *p = g.B + 4 * ((4 * lid + (it - 4)) & 1023);
-        else *p = g.C + 4 * (hash3(seed, gid, it) & ((1ull << 28) - 1));
+        else *p = g.C + 4 * (hash3(seed, gid, it) % (4 * g.W));
       } else if (pos == 20) { *k = AIWC_K_INSTR; *p = ins(OP_STORE, 1); }
       else if (pos == 21) { *k = AIWC_K_STORE; *p = g.D + 4 * gid; }
       else { const uint64_t j = pos - 22; *k = AIWC_K_INSTR; *p = ins((j & 1) ? OP_FADD : OP_FMUL, (j & 2) ? 1 : 4); }

@@ -102,7 +102,7 @@ def python_trace(cfg: int, work_items: int, seed: int = DEFAULT_SEED) -> Columna
     if cfg == 2:
         B = A + _a4k(4 * 8 * W)
     elif cfg == 3:
-        B = A + _a4k(4 * 4 * W); C = B + 4096; D = C + (1 << 30)
+        B = A + _a4k(4 * 4 * W); C = B + 4096; D = C + 16 * W
     elif cfg == 5:
         B = A + _a4k(4 * 2 * W)
     ins = lambda op, w: (op << 32) | w  # noqa: E731
@@ -125,7 +125,7 @@ def python_trace(cfg: int, work_items: int, seed: int = DEFAULT_SEED) -> Columna
                 elif it < 8:
                     a = B + 4 * ((4 * lid + it - 4) & 1023)
                 else:
-                    a = C + 4 * (_hash3(seed, gid, it) & ((1 << 28) - 1))
+                    a = C + 4 * (_hash3(seed, gid, it) % (4 * W))
                 out += [(0x01, ins(0, 1)), (0x02, a)]
             out += [(0x01, ins(1, 1)), (0x04, D + 4 * gid)]
             for j in range(8):
