@@ -146,12 +146,42 @@ def run_reference(args) -> None:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def _timed(step, steps, stream, dev, world, local):
+    """Barrier + sync, K steps between CUDA events on `stream`, max over ranks."""
+    import torch
+
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        start.record(stream)
+        for _ in range(steps):
+            step()
+        end.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+    ms = start.elapsed_time(end)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms, wall], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = (float(v) for v in t.tolist())
+    return ms, wall, clk.summary()
+
+
 def run_ours(args) -> None:
-    import numpy as np
     import torch
 
     from paper_1805_04207_b200 import _native, consume, finalize, synth
+    from paper_1805_04207_b200 import dist as D
     from paper_1805_04207_b200.metrics import trace_info
+    from paper_1805_04207_b200.trace import ColumnarTrace
 
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
@@ -162,90 +192,88 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     cfg = args.config
     w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
-    # weak scaling: rank r owns work-groups [r*G, (r+1)*G) of a world*w work-item trace
-    tr = synth.device_trace(cfg, w)
-    n = tr.n_events
+    # weak scaling: the job is one world*w work-item trace; rank r owns the
+    # contiguous work-group shard synth.shard_range(cfg, world*w, r, world)
+    total_wi = world * w
+    first, count = synth.shard_range(cfg, total_wi, rank, world)
+    tr = synth.device_trace(cfg, total_wi, first=first, count=count)
+    n_total = synth.n_events(cfg, total_wi)
     stream = torch.cuda.current_stream(dev)
-    ctx = _native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING)
-    lib = ctx.lib
-    info = trace_info(tr)
-    kptr = ctypes.c_void_p(tr.kind.data_ptr())
-    pptr = ctypes.c_void_p(tr.payload.data_ptr())
-    sptr = ctypes.c_void_p(stream.cuda_stream)
     res = _native.Result()
 
-    def step():
-        ctx.check(lib.aiwc_reset(ctx.h))
-        ctx.check(lib.aiwc_ingest(ctx.h, kptr, pptr, ctypes.byref(info), sptr))
-        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), sptr))
+    if world == 1:
+        ctx = _native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING)
+        lib = ctx.lib
+        info = trace_info(tr)
+        kptr = ctypes.c_void_p(tr.kind.data_ptr())
+        pptr = ctypes.c_void_p(tr.payload.data_ptr())
+        sptr = ctypes.c_void_p(stream.cuda_stream)
+
+        def step():
+            ctx.check(lib.aiwc_reset(ctx.h))
+            ctx.check(lib.aiwc_ingest(ctx.h, kptr, pptr, ctypes.byref(info), sptr))
+            ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), sptr))
+            return list(res.phase_ms), res.kernels_launched
+    else:
+        backend = D.CudaBackend(local, timing=True)
+
+        def step():
+            before = backend.launches
+            D.sharded_result(backend, tr, first)
+            return backend.last_phase_ms, backend.launches - before
+
+    phases = {p: [] for p in _native.PHASES}
+    kernels = [0]
+
+    def timed_step():
+        ph, k = step()
+        for i, p in enumerate(_native.PHASES):
+            phases[p].append(ph[i])
+        kernels[0] += k
 
     for _ in range(max(3, args.warmup)):
         step()
-    torch.cuda.synchronize()
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.barrier()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    phases = {p: [] for p in _native.PHASES}
-    kernels = 0
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        start.record(stream)
-        for _ in range(args.steps):
-            step()
-            for i, p in enumerate(_native.PHASES):
-                phases[p].append(res.phase_ms[i])
-            kernels += res.kernels_launched
-        end.record(stream)
-        torch.cuda.synchronize()
-    ms = start.elapsed_time(end)
-    if world > 1:
-        import torch.distributed as dist
-
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms, _, clocks = _timed(timed_step, args.steps, stream, dev, world, local)
     ms_step = ms / args.steps
-    value = n * world / (ms_step / 1e3)
+    value = n_total / (ms_step / 1e3)
+    phase_med = {p: statistics.median(v) for p, v in phases.items()}
 
     if args.no_e2e:
         if rank == 0:
-            print(json.dumps({"ms_per_step": ms / args.steps, "value": n * world / (ms / args.steps / 1e3),
-                              "phases_ms": {p: statistics.median(v) for p, v in phases.items()}}), flush=True)
+            print(json.dumps({"ms_per_step": ms_step, "value": value, "phases_ms": phase_med}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
         return
-    # ---- e2e: public API from pinned host columns ----
-    hk = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    hp = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    # ---- e2e: the public API from pinned host columns (H2D + result D2H inside) ----
+    hk = torch.empty(count, dtype=torch.uint8, pin_memory=True)
+    hp = torch.empty(count, dtype=torch.int64, pin_memory=True)
     hk.copy_(tr.kind)
     hp.copy_(tr.payload)
-    from paper_1805_04207_b200.trace import ColumnarTrace
-
     host_tr = ColumnarTrace(hk, hp, tr.kernel_name, 0, tr.global_size, tr.local_size, tr.opcodes, [], tr.addr_stats)
+    if world == 1:
+        def e2e_step():
+            return finalize(consume(host_tr, max_entries=1 << 62, device=local))
+    else:
+        def e2e_step():
+            return D.sharded_report(backend, host_tr, first, tr.kernel_name, 0, tr.global_size, tr.local_size,
+                                    tr.opcodes)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    out = {}
     for _ in range(2):
-        finalize(consume(host_tr, max_entries=1 << 62, device=local))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e_start = torch.cuda.Event(enable_timing=True)
-    e_end = torch.cuda.Event(enable_timing=True)
-    e_start.record()
-    for _ in range(e2e_steps):
-        rep = finalize(consume(host_tr, max_entries=1 << 62, device=local))
-    e_end.record()
-    torch.cuda.synchronize()
-    e2e_ms = max(e_start.elapsed_time(e_end), (time.perf_counter() - t0) * 1e3) / e2e_steps
-    d2h = res.d2h_bytes
-    e2e_value = n * world / (e2e_ms / 1e3)
+        out["rep"] = e2e_step()
+    e_ms, e_wall, _ = _timed(lambda: out.__setitem__("rep", e2e_step()), e2e_steps, stream, dev, world, local)
+    rep = out["rep"]
+    e2e_ms = max(e_ms, e_wall) / e2e_steps
+    e2e_value = n_total / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (the ingest pass) ----
+    # ---- roofline of the dominant kernel (the ingest pass), per rank ----
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "measured" if peak else "fallback"
     peak = peak or 6650.0
-    ingest_ms = statistics.median(phases["ingest"])
-    achieved = ALG_BYTES_PER_EVENT * n / (ingest_ms / 1e3) / 1e9
-    step_alg = ALG_BYTES_PER_EVENT * n / (ms_step / 1e3) / 1e9
+    ingest_ms = phase_med["ingest"]
+    achieved = ALG_BYTES_PER_EVENT * count / (ingest_ms / 1e3) / 1e9
+    step_alg = ALG_BYTES_PER_EVENT * count / (ms_step / 1e3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -255,27 +283,28 @@ def run_ours(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
-            "config": {"workload": f"C{cfg} {synth.NAMES[cfg]}: {w} work-items x {world} ranks, "
-                                   f"{n} events per rank, local 256" if cfg != 1 else f"C1 sweep4 {w} work-items",
-                       "events_per_rank": n, "l2": "trace (9 B/event) larger than L2; no flush needed",
-                       "parallelism": f"work-group shards x{world}"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * n, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms, "path": "consume(ColumnarTrace on pinned host)+finalize"},
+            "config": {"workload": f"C{cfg} {synth.NAMES[cfg]}: {total_wi} work-items ({n_total} events), "
+                                   f"local {synth.LOCAL[cfg]}, {world} work-group shard(s)",
+                       "events_per_rank": count, "l2": "trace (9 B/event) larger than L2; no flush needed",
+                       "parallelism": "replica (N=1)" if world == 1 else
+                                      f"work-group shards x{world}; NCCL all-reduce + address all-to-all"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
+                    "d2h_bytes_per_step": res.d2h_bytes if world == 1 else backend.last_d2h, "ms_per_step": e2e_ms,
+                    "path": "consume(ColumnarTrace on pinned host)+finalize" if world == 1 else
+                            "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "aiwc::ingest_kernel<true>",
+                         "frac": achieved / peak, "traffic": None, "kernel": "aiwc::ingest_kernel",
                          "peak_source": peak_src, "alg_bytes_per_event": ALG_BYTES_PER_EVENT,
                          "step_alg_gbs": step_alg, "step_frac": step_alg / peak},
-            "phases_ms": {p: statistics.median(v) for p, v in phases.items()},
-            "gpu_launches": kernels,
-            "clocks": clk.summary(),
+            "phases_ms": phase_med,
+            "gpu_launches": kernels[0],
+            "clocks": clocks,
             "cpu_baseline": cpu,
             "report_check": {"total_memory_footprint": rep.total_memory_footprint, "gmae": rep.gmae,
                              "footprint_90": rep.footprint_90},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
-        import torch.distributed as dist
-
         dist.destroy_process_group()
 
 

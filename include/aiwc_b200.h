@@ -147,6 +147,52 @@ int  aiwc_finalize(aiwc_ctx *ctx, aiwc_result *out, void *stream);
 /* Details of the last non-zero return on ctx. */
 int  aiwc_last_error(const aiwc_ctx *ctx, aiwc_error *err);
 
+/* ---- multi-GPU (work-group shards) ----------------------------
+ * A ctx created with AIWC_OPT_SHARD ingests one rank's work-group shard:
+ * memory addresses stay compacted on the device and aiwc_finalize fills every
+ * non-memory field.  The caller exchanges addresses between ranks (owner of a
+ * key = key / keys_per_rank over the global key map) and each owner computes
+ * the memory partials of its key range with aiwc_memory_partial. */
+#define AIWC_OPT_SHARD 4u
+
+typedef struct {
+  const uint64_t *itb_hist, *ipt_hist;          /* 1024 bins each                      */
+  uint64_t n_itb_ovf, n_ipt_ovf;
+  const uint64_t *itb_ovf, *ipt_ovf;            /* ascending values >= 1024            */
+  uint32_t branch_table_size;                   /* 2^history_len                       */
+  const uint64_t *branch_table;                 /* total << 32 | taken per pattern     */
+  const uint64_t *width_first;                  /* first event index, per aiwc_result width */
+  uint64_t addr_stats[4];                       /* min, max, and, or of shard addresses */
+  const uint64_t *rd_dev, *wr_dev;              /* compacted addresses (device)        */
+} aiwc_shard_tables;
+
+typedef struct {
+  uint64_t unique_reads, unique_writes, footprint;
+  double level_sum[11];       /* sum of p log2 p over the owned keys, p = c / total_m  */
+  const uint64_t *cnt_hist0;  /* 1024 bins: level-0 count-of-counts                    */
+  uint64_t n_big;             /* level-0 counts >= 1024                                 */
+  const uint64_t *big;        /* their values                                           */
+  uint32_t kernels_launched;  /* engine kernels this call queued                        */
+} aiwc_memory_part;
+
+/* after aiwc_finalize on a shard ctx */
+int  aiwc_shard_tables_get(aiwc_ctx *ctx, aiwc_shard_tables *out);
+
+/* Group this shard's read and write addresses by owner, owner = min(nranks-1,
+ * ((addr - base) >> k) / keys_per_rank).  *reads_dev / *writes_dev hold the
+ * owner-grouped addresses (valid until the next call on ctx); counts[0..nranks)
+ * are read counts per owner, counts[nranks..2*nranks) write counts. */
+int  aiwc_partition_addresses(aiwc_ctx *ctx, uint64_t base, uint32_t k, uint64_t keys_per_rank,
+                              uint32_t nranks, uint64_t **reads_dev, uint64_t **writes_dev, uint64_t *counts,
+                              void *stream);
+
+/* Memory statistics of the owned keys [key_lo, key_lo + n_keys) of the global
+ * key map (base, k) from the received addresses (device).  key_lo must be a
+ * multiple of 1024.  Dense table or sort path, as in aiwc_finalize. */
+int  aiwc_memory_partial(aiwc_ctx *ctx, const uint64_t *reads_dev, uint64_t n_rd, const uint64_t *writes_dev,
+                         uint64_t n_wr, uint64_t base, uint32_t k, uint64_t key_lo, uint64_t n_keys,
+                         uint64_t total_m, aiwc_memory_part *out, void *stream);
+
 /* Device-side synthetic trace generators.
  * Writes n events starting at event index `first` of config `cfg` into the
  * device columns; aiwc_synth_size returns the config's total event count and

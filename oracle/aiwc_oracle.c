@@ -180,7 +180,7 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
   uint64_t *opc = (uint64_t *)calloc(prm->n_opcodes ? prm->n_opcodes : 1, 8);
   /* width Counter in insertion order (metrics.py:136, order drives the sd sum) */
   map64 wmap; map_init(&wmap, 64);
-  vec64 wvals = {0}, wcnts = {0};
+  vec64 wvals = {0}, wcnts = {0}, wfirst = {0};
   uint64_t *taken_tab = (uint64_t *)calloc(table, 8), *total_tab = (uint64_t *)calloc(table, 8);
   if (!opc || !taken_tab || !total_tab) return -1;
 
@@ -200,7 +200,7 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
         uint32_t op = (uint32_t)(p >> 32), w = (uint32_t)p;
         if (op < prm->n_opcodes) opc[op]++; else { status = 2; break; }
         int fresh; uint64_t s = map_slot(&wmap, w, &fresh);
-        if (fresh) { wmap.vals[s] = wvals.n; vec_push(&wvals, w); vec_push(&wcnts, 0); }
+        if (fresh) { wmap.vals[s] = wvals.n; vec_push(&wvals, w); vec_push(&wcnts, 0); vec_push(&wfirst, i); }
         wcnts.v[wmap.vals[s]]++;
         break;
       }
@@ -368,7 +368,30 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
     r->linear = kval(&l);
   }
 
+  if (prm->keep_raw) {  /* hand the accumulator over (ownership moves to r->raw) */
+    oracle_raw *w = &r->raw;
+    w->n_itb = itb.n; w->itb = itb.v; itb.v = NULL;
+    w->n_ipt = ipt.n; w->ipt = ipt.v; ipt.v = NULL;
+    w->n_opc = prm->n_opcodes; w->opc = opc; opc = NULL;
+    w->width_first = wfirst.v; wfirst.v = NULL;
+    w->n_sites = n_srec;
+    w->site_ids = site_ids.v; site_ids.v = NULL;
+    w->site_exec = (uint64_t *)malloc((n_srec + 1) * 8);
+    for (uint64_t s = 0; s < n_srec; s++) w->site_exec[s] = srec[s].executions;
+    w->table_size = table;
+    w->taken_tab = taken_tab; taken_tab = NULL;
+    w->total_tab = total_tab; total_tab = NULL;
+    map64 *hs[2] = {&rd, &wr};
+    for (int q = 0; q < 2; q++) {
+      uint64_t *a = (uint64_t *)malloc((hs[q]->size + 1) * 8), *c = (uint64_t *)malloc((hs[q]->size + 1) * 8), m = 0;
+      for (uint64_t i = 0; i < hs[q]->cap; i++)
+        if (hs[q]->used[i]) { a[m] = hs[q]->keys[i]; c[m] = hs[q]->vals[i]; m++; }
+      if (q) { w->n_wr = m; w->wr_addr = a; w->wr_cnt = c; } else { w->n_rd = m; w->rd_addr = a; w->rd_cnt = c; }
+    }
+  }
+
 done:
+  free(wfirst.v);
   map_free(&rd); map_free(&wr); map_free(&sites); map_free(&tal); map_free(&wmap);
   free(itb.v); free(ipt.v); free(site_ids.v); free(srec); free(tl); free(opc);
   free(wvals.v); free(wcnts.v); free(taken_tab); free(total_tab);
@@ -378,4 +401,8 @@ done:
 void oracle_free(oracle_result *r) {
   free(r->width_vals); free(r->width_counts);
   r->width_vals = r->width_counts = NULL;
+  oracle_raw *w = &r->raw;
+  free(w->itb); free(w->ipt); free(w->opc); free(w->width_first); free(w->site_ids); free(w->site_exec);
+  free(w->taken_tab); free(w->total_tab); free(w->rd_addr); free(w->rd_cnt); free(w->wr_addr); free(w->wr_cnt);
+  memset(w, 0, sizeof *w);
 }

@@ -7,7 +7,18 @@ typedef struct {
   uint32_t n_opcodes;    /* opcode dictionary size */
   uint32_t history_len;  /* branch history bits, 0 -> 16 (entropy.py:16) */
   uint64_t entry_cap;    /* TraceTooLarge cap (metrics.py:54-57); 0 = unlimited */
+  uint32_t keep_raw;     /* 1: also return the accumulator tables (oracle_raw) */
+  uint32_t pad;
 } oracle_params;
+
+/* The accumulator behind a result (metrics.py:71-95), for shard tests. */
+typedef struct {
+  uint64_t n_itb, n_ipt, n_opc, n_sites, table_size, n_rd, n_wr;
+  uint64_t *itb, *ipt, *opc, *width_first;  /* width_first parallels width_vals   */
+  uint64_t *site_ids, *site_exec;
+  uint64_t *taken_tab, *total_tab;
+  uint64_t *rd_addr, *rd_cnt, *wr_addr, *wr_cnt;
+} oracle_raw;
 
 typedef struct {
   uint64_t n, min, max, sum, mid_lo, mid_hi; /* mid_lo/hi: ranks (n-1)/2 and n/2 */
@@ -24,6 +35,7 @@ typedef struct {
   double gmae, lmae[10];
   uint64_t n_sites, branch90, executions, excluded, observations;
   double yokota, linear;
+  oracle_raw raw;
 } oracle_result;
 
 int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,

@@ -23,7 +23,16 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 class _Params(ctypes.Structure):
     _fields_ = [("n_opcodes", ctypes.c_uint32), ("history_len", ctypes.c_uint32),
-                ("entry_cap", ctypes.c_uint64)]
+                ("entry_cap", ctypes.c_uint64), ("keep_raw", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
+
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+
+
+class _Raw(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("n_itb", "n_ipt", "n_opc", "n_sites", "table_size", "n_rd", "n_wr")] + [
+        (n, _u64p) for n in ("itb", "ipt", "opc", "width_first", "site_ids", "site_exec", "taken_tab", "total_tab",
+                             "rd_addr", "rd_cnt", "wr_addr", "wr_cnt")]
 
 
 class _Dist(ctypes.Structure):
@@ -45,7 +54,40 @@ class _Result(ctypes.Structure):
         ("n_sites", ctypes.c_uint64), ("branch90", ctypes.c_uint64), ("executions", ctypes.c_uint64),
         ("excluded", ctypes.c_uint64), ("observations", ctypes.c_uint64),
         ("yokota", ctypes.c_double), ("linear", ctypes.c_double),
+        ("raw", _Raw),
     ]
+
+
+def accumulator(kind: np.ndarray, payload: np.ndarray, n_opcodes: int, history_len: int = 16) -> dict:
+    """The reference accumulator of one (shard of a) trace as numpy arrays:
+    ITB / IPT samples, opcode counts, widths with first event index, pooled
+    branch pattern tables, site executions, read / write address counts."""
+    lib = _load()
+    kind = np.ascontiguousarray(kind, dtype=np.uint8)
+    payload = np.ascontiguousarray(payload, dtype=np.uint64)
+    prm = _Params(n_opcodes, history_len, 0, 1, 0)
+    res = _Result()
+    if lib.oracle_run(kind.ctypes.data, payload.ctypes.data, kind.shape[0], ctypes.byref(prm), ctypes.byref(res)):
+        raise MemoryError("oracle allocation failed")
+    try:
+        if res.status:
+            raise ValueError("malformed columnar trace")
+        w = res.raw
+
+        def a(p, n):
+            return np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint64)
+
+        return {
+            "itb": a(w.itb, w.n_itb), "ipt": a(w.ipt, w.n_ipt), "opc": a(w.opc, w.n_opc),
+            "widths": [(res.width_vals[i], res.width_counts[i], w.width_first[i]) for i in range(res.n_widths)],
+            "sites": dict(zip(a(w.site_ids, w.n_sites).tolist(), a(w.site_exec, w.n_sites).tolist())),
+            "taken": a(w.taken_tab, w.table_size), "total": a(w.total_tab, w.table_size),
+            "rd": (a(w.rd_addr, w.n_rd), a(w.rd_cnt, w.n_rd)), "wr": (a(w.wr_addr, w.n_wr), a(w.wr_cnt, w.n_wr)),
+            "total_instructions": res.total_instructions, "work_items": res.work_items, "barriers": res.barriers,
+            "executions": res.executions,
+        }
+    finally:
+        lib.oracle_free(ctypes.byref(res))
 
 
 def build() -> str:
@@ -96,7 +138,7 @@ def run(kind: np.ndarray, payload: np.ndarray, *, kernel: str, invocation: int, 
     lib = _load()
     kind = np.ascontiguousarray(kind, dtype=np.uint8)
     payload = np.ascontiguousarray(payload, dtype=np.uint64)
-    prm = _Params(n_opcodes, history_len, entry_cap)
+    prm = _Params(n_opcodes, history_len, entry_cap, 0, 0)
     res = _Result()
     rc = lib.oracle_run(kind.ctypes.data, payload.ctypes.data, kind.shape[0], ctypes.byref(prm), ctypes.byref(res))
     if rc != 0:

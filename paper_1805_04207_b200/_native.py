@@ -62,7 +62,21 @@ class Result(ctypes.Structure):
 
 
 OPT_TIMING = 2
+OPT_SHARD = 4
 PHASES = ("pass1", "ingest", "memory", "branch", "ingest_total", "finalize_total")
+
+
+class ShardTables(ctypes.Structure):
+    _fields_ = [("itb_hist", u64p), ("ipt_hist", u64p), ("n_itb_ovf", ctypes.c_uint64), ("n_ipt_ovf", ctypes.c_uint64),
+                ("itb_ovf", u64p), ("ipt_ovf", u64p), ("branch_table_size", ctypes.c_uint32),
+                ("branch_table", u64p), ("width_first", u64p), ("addr_stats", ctypes.c_uint64 * 4),
+                ("rd_dev", ctypes.c_void_p), ("wr_dev", ctypes.c_void_p)]
+
+
+class MemoryPart(ctypes.Structure):
+    _fields_ = [("unique_reads", ctypes.c_uint64), ("unique_writes", ctypes.c_uint64), ("footprint", ctypes.c_uint64),
+                ("level_sum", ctypes.c_double * 11), ("cnt_hist0", u64p), ("n_big", ctypes.c_uint64),
+                ("big", u64p), ("kernels_launched", ctypes.c_uint32)]
 
 
 class Error(ctypes.Structure):
@@ -71,7 +85,8 @@ class Error(ctypes.Structure):
 
 
 EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
-           "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill")
+           "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill",
+           "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial")
 
 _lib = None
 _lock = threading.Lock()
@@ -100,8 +115,15 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_synth_size.restype = ctypes.c_uint64
         lib.aiwc_synth_fill.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp, vp, ctypes.c_uint64,
                                         ctypes.c_uint64, vp]
+        lib.aiwc_shard_tables_get.argtypes = [vp, ctypes.POINTER(ShardTables)]
+        lib.aiwc_partition_addresses.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
+                                                 ctypes.POINTER(u64p), ctypes.POINTER(u64p), u64p, vp]
+        lib.aiwc_memory_partial.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.POINTER(MemoryPart), vp]
         for name in ("aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
-                     "aiwc_last_error", "aiwc_synth_fill"):
+                     "aiwc_last_error", "aiwc_synth_fill", "aiwc_shard_tables_get", "aiwc_partition_addresses",
+                     "aiwc_memory_partial"):
             getattr(lib, name).restype = ctypes.c_int
         if lib.aiwc_abi_version() != 1:
             raise DeviceError("libaiwc_b200.so ABI version mismatch")

@@ -99,6 +99,10 @@ struct aiwc_ctx {
   // host results
   std::vector<uint64_t> opc_counts, width_vals, width_counts, site_ids, site_counts;
   std::vector<uint64_t> itb_ovf_sorted, ipt_ovf_sorted, lvl0_sorted;
+  std::vector<uint64_t> width_firsts, branch_tab_host;
+  // multi-GPU: owner partition and owned-key memory partials
+  Buf part_entries, part_cursor, mp_state, mp_tab, mp_partials, mp_ovf;
+  std::vector<uint64_t> mp_hist0, mp_big;
 };
 
 static int fail(aiwc_ctx* c, int code, const char* msg) {
@@ -161,7 +165,8 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   Buf* bufs[] = {&ctx->dev_state, &ctx->ranges, &ctx->opc, &ctx->wcount, &ctx->wfirst, &ctx->itb_ovf,
                  &ctx->ipt_ovf, &ctx->ipt_tab, &ctx->dtab, &ctx->rd, &ctx->wr, &ctx->br, &ctx->partials,
                  &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
-                 &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h};
+                 &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
+                 &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -299,7 +304,8 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     am.n_keys = span_keys + 1;
     const bool fits = span_keys < (1ull << 40) && am.n_keys * 8 <= ctx->opts.dense_budget_bytes &&
                       am.n_keys <= 4 * M + (1ull << 20);
-    ctx->dense = fits;
+    // a shard keeps its addresses compacted: they are exchanged with the key owners
+    ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
   }
 
   // ---- buffers ----
@@ -432,7 +438,8 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(ctx->device));
   DevState* st = P<DevState>(ctx->dev_state);
-  const uint64_t M = ctx->n_rd + ctx->n_wr;
+  const bool shard = ctx->opts.flags & AIWC_OPT_SHARD;
+  const uint64_t M = shard ? 0 : ctx->n_rd + ctx->n_wr;  // a shard's memory is finished by the key owners
   ctx->mark(AIWC_PH_FINALIZE_TOTAL, 0, s);
 
   // ---- device finishing: IPT slots, widths, memory ----
@@ -590,17 +597,30 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   }
   r.n_sites = ctx->site_ids.size();
   // widths in first-appearance order
-  ctx->width_vals.clear(); ctx->width_counts.clear();
+  ctx->width_vals.clear(); ctx->width_counts.clear(); ctx->width_firsts.clear();
   if (h.n_widths_listed <= (unsigned long long)MAX_SMALL_LIST) {
     for (uint64_t i = 0; i < h.n_widths_listed; ++i) {
       ctx->width_vals.push_back(h.width_list[3 * i]);
       ctx->width_counts.push_back(h.width_list[3 * i + 1]);
+      ctx->width_firsts.push_back(h.width_list[3 * i + 2]);
     }
   } else {
     std::vector<std::pair<uint64_t, uint32_t>> order;
     for (uint32_t w = 0; w < WIDTH_TABLE; ++w) if (wc_full[w]) order.emplace_back(wf_full[w], w);
     std::sort(order.begin(), order.end());
-    for (auto& o : order) { ctx->width_vals.push_back(o.second); ctx->width_counts.push_back(wc_full[o.second]); }
+    for (auto& o : order) {
+      ctx->width_vals.push_back(o.second); ctx->width_counts.push_back(wc_full[o.second]);
+      ctx->width_firsts.push_back(o.first);
+    }
+  }
+  if (shard) {  // the pooled pattern table is summed across ranks before the entropies
+    const size_t tb = (size_t(1) << ctx->opts.history_len);
+    ctx->branch_tab_host.assign(tb, 0);
+    if (ctx->n_br) {
+      CK(cudaMemcpyAsync(ctx->branch_tab_host.data(), ctx->branch_tab.p, tb * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      ctx->d2h += tb * 8;
+    }
   }
   r.entries = r.unique_reads + r.unique_writes + r.branch_executions;
   r.n_opcodes = n_opc;
@@ -644,3 +664,207 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   }
   return AIWC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// multi-GPU: shard tables, owner partition, owned-key memory partials
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int PA_T = 256, PA_MAXR = 64, PA_ITEMS = 8;
+
+__device__ __forceinline__ uint32_t owner_of(uint64_t addr, uint64_t base, uint32_t k, uint64_t kpr, uint32_t nranks) {
+  const uint64_t o = ((addr - base) >> k) / kpr;
+  return o < nranks ? (uint32_t)o : nranks - 1;
+}
+
+// per-owner totals of one address array
+__global__ void partition_count_kernel(const uint64_t* __restrict__ a, uint64_t n, uint64_t base, uint32_t k,
+                                       uint64_t kpr, uint32_t nranks, unsigned long long* counts) {
+  __shared__ unsigned int h[PA_MAXR];
+  for (int i = threadIdx.x; i < PA_MAXR; i += PA_T) h[i] = 0;
+  __syncthreads();
+  for (uint64_t i = (uint64_t)blockIdx.x * PA_T + threadIdx.x; i < n; i += (uint64_t)gridDim.x * PA_T)
+    atomicAdd(&h[owner_of(a[i], base, k, kpr, nranks)], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < (int)nranks; i += PA_T)
+    if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+}
+
+// owner-grouped copy: block-level reservation on per-owner cursors (order inside
+// an owner's run is irrelevant -- the owner only counts addresses)
+__global__ void partition_scatter_kernel(const uint64_t* __restrict__ a, uint64_t n, uint64_t base, uint32_t k,
+                                         uint64_t kpr, uint32_t nranks, unsigned long long* cursor,
+                                         uint64_t* __restrict__ out) {
+  __shared__ unsigned int h[PA_MAXR];
+  __shared__ unsigned long long b[PA_MAXR];
+  for (uint64_t c0 = (uint64_t)blockIdx.x * PA_T * PA_ITEMS; c0 < n; c0 += (uint64_t)gridDim.x * PA_T * PA_ITEMS) {
+    for (int i = threadIdx.x; i < PA_MAXR; i += PA_T) h[i] = 0;
+    __syncthreads();
+    uint32_t own[PA_ITEMS], slot[PA_ITEMS];
+    uint64_t v[PA_ITEMS];
+#pragma unroll
+    for (int j = 0; j < PA_ITEMS; ++j) {
+      const uint64_t i = c0 + (uint64_t)j * PA_T + threadIdx.x;
+      own[j] = PA_MAXR;
+      if (i < n) {
+        v[j] = a[i];
+        own[j] = owner_of(v[j], base, k, kpr, nranks);
+        slot[j] = atomicAdd(&h[own[j]], 1u);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < (int)nranks; i += PA_T)
+      b[i] = h[i] ? atomicAdd(&cursor[i], (unsigned long long)h[i]) : 0ull;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PA_ITEMS; ++j)
+      if (own[j] < PA_MAXR) out[b[own[j]] + slot[j]] = v[j];
+    __syncthreads();
+  }
+}
+
+// owned-range dense table from received addresses
+__global__ void fill_owned_kernel(const uint64_t* __restrict__ a, uint64_t n, unsigned long long inc, uint64_t base,
+                                  uint32_t k, uint64_t key_lo, uint64_t n_keys, unsigned long long* __restrict__ tab,
+                                  DevState* st) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = ((a[i] - base) >> k) - key_lo;
+    if (key < n_keys) atomicAdd(&tab[key], inc);
+    else atomicOr(&st->flags, (unsigned long long)F_SLOT_RANGE);
+  }
+}
+
+}  // namespace
+
+extern "C" int aiwc_shard_tables_get(aiwc_ctx* ctx, aiwc_shard_tables* out) {
+  if (!ctx || !out) return AIWC_ERR_ARGUMENT;
+  if (!(ctx->opts.flags & AIWC_OPT_SHARD) || ctx->state != 2)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "shard tables need a shard ctx after aiwc_finalize");
+  aiwc_shard_tables t{};
+  t.itb_hist = reinterpret_cast<const uint64_t*>(ctx->h_state->itb_hist);
+  t.ipt_hist = reinterpret_cast<const uint64_t*>(ctx->h_state->ipt_hist);
+  t.n_itb_ovf = ctx->itb_ovf_sorted.size(); t.itb_ovf = ctx->itb_ovf_sorted.data();
+  t.n_ipt_ovf = ctx->ipt_ovf_sorted.size(); t.ipt_ovf = ctx->ipt_ovf_sorted.data();
+  t.branch_table_size = (uint32_t)ctx->branch_tab_host.size();
+  t.branch_table = ctx->branch_tab_host.data();
+  t.width_first = ctx->width_firsts.data();
+  const DevState& h = *ctx->h_state;
+  t.addr_stats[0] = h.addr_min; t.addr_stats[1] = h.addr_max; t.addr_stats[2] = h.addr_and; t.addr_stats[3] = h.addr_or;
+  t.rd_dev = P<uint64_t>(ctx->rd); t.wr_dev = P<uint64_t>(ctx->wr);
+  *out = t;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_partition_addresses(aiwc_ctx* ctx, uint64_t base, uint32_t k, uint64_t keys_per_rank,
+                                        uint32_t nranks, uint64_t** reads_dev, uint64_t** writes_dev,
+                                        uint64_t* counts, void* stream) {
+  if (!ctx || !reads_dev || !writes_dev || !counts || nranks == 0 || nranks > (uint32_t)PA_MAXR || keys_per_rank == 0)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad partition arguments");
+  if (!(ctx->opts.flags & AIWC_OPT_SHARD) || ctx->state != 2)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "partition needs a shard ctx after aiwc_finalize");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->part_entries, std::max<uint64_t>(ctx->n_rd + ctx->n_wr, 1) * 8));
+  CK(grow(ctx->part_cursor, 2 * PA_MAXR * 8));
+  unsigned long long* cur = P<unsigned long long>(ctx->part_cursor);
+  CK(cudaMemsetAsync(cur, 0, 2 * PA_MAXR * 8, s));
+  const uint64_t* src[2] = {P<uint64_t>(ctx->rd), P<uint64_t>(ctx->wr)};
+  const uint64_t len[2] = {ctx->n_rd, ctx->n_wr};
+  auto blocks = [&](uint64_t n) {
+    return (uint32_t)std::min<uint64_t>(std::max<uint64_t>((n + PA_T * PA_ITEMS - 1) / (PA_T * PA_ITEMS), 1),
+                                        (uint64_t)ctx->n_sms * 8);
+  };
+  for (int q = 0; q < 2; ++q)
+    if (len[q]) partition_count_kernel<<<blocks(len[q]), PA_T, 0, s>>>(src[q], len[q], base, k, keys_per_rank, nranks,
+                                                                       cur + q * PA_MAXR);
+  std::vector<unsigned long long> c(2 * PA_MAXR, 0);
+  CK(cudaMemcpyAsync(c.data(), cur, 2 * PA_MAXR * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<unsigned long long> off(2 * PA_MAXR, 0);
+  for (int q = 0; q < 2; ++q) {
+    unsigned long long run = q ? ctx->n_rd : 0;  // reads first, then writes
+    for (uint32_t i = 0; i < nranks; ++i) {
+      off[q * PA_MAXR + i] = run;
+      run += c[q * PA_MAXR + i];
+      counts[q * nranks + i] = c[q * PA_MAXR + i];
+    }
+  }
+  CK(cudaMemcpyAsync(cur, off.data(), 2 * PA_MAXR * 8, cudaMemcpyHostToDevice, s));
+  for (int q = 0; q < 2; ++q)
+    if (len[q]) partition_scatter_kernel<<<blocks(len[q]), PA_T, 0, s>>>(src[q], len[q], base, k, keys_per_rank,
+                                                                         nranks, cur + q * PA_MAXR,
+                                                                         P<uint64_t>(ctx->part_entries));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  *reads_dev = P<uint64_t>(ctx->part_entries);
+  *writes_dev = P<uint64_t>(ctx->part_entries) + ctx->n_rd;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr,
+                                   uint64_t base, uint32_t k, uint64_t key_lo, uint64_t n_keys, uint64_t total_m,
+                                   aiwc_memory_part* out, void* stream) {
+  if (!ctx || !out || (n_rd && !rd) || (n_wr && !wr) || (key_lo & 1023) || k > 32)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad memory partial");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->mp_state, sizeof(DevState)));
+  DevState* st = P<DevState>(ctx->mp_state);
+  init_state_kernel<<<64, 256, 0, s>>>(st);
+  uint32_t launched = 1;
+  const uint64_t m = n_rd + n_wr, tm = std::max<uint64_t>(total_m, 1);
+  CK(grow(ctx->mp_ovf, (tm / CBINS + 2) * 8));
+  const bool dense = n_keys * 8 <= ctx->opts.dense_budget_bytes && n_keys <= 4 * m + (1ull << 20);
+  if (m && dense) {
+    CK(grow(ctx->mp_tab, std::max<uint64_t>(n_keys, 1) * 8));
+    CK(cudaMemsetAsync(ctx->mp_tab.p, 0, std::max<uint64_t>(n_keys, 1) * 8, s));
+    const uint64_t* src[2] = {rd, wr};
+    const uint64_t len[2] = {n_rd, n_wr};
+    for (int q = 0; q < 2; ++q)
+      if (len[q]) {
+        const uint32_t blocks = (uint32_t)std::min<uint64_t>((len[q] + 255) / 256, (uint64_t)ctx->n_sms * 8);
+        fill_owned_kernel<<<blocks, 256, 0, s>>>(src[q], len[q], q ? (1ull << 32) : 1ull, base, k, key_lo, n_keys,
+                                                 P<unsigned long long>(ctx->mp_tab), st);
+        ++launched;
+      }
+    const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
+    launch_dense_stats(P<unsigned long long>(ctx->mp_tab), n_keys, k, tm, st, P<double>(ctx->partials), nct,
+                       P<uint64_t>(ctx->mp_ovf), s);
+    launch_entropy_finish(st, P<double>(ctx->partials), nct, tm, k, s);
+    launched += 2;
+  } else if (m) {
+    // sort path over the received addresses with the global base / k
+    AddrMap am{};
+    am.base = base; am.k = k;
+    const uint64_t hi_key = key_lo + (n_keys ? n_keys - 1 : 0);
+    am.hi = base + (hi_key << k);
+    const bool raw = bitwidth64(hi_key) > 63;
+    CK(grow(ctx->sparse_scr, sparse_scratch_bytes(m)));
+    const uint32_t parts = std::min<uint32_t>(ctx->n_parts, 256);
+    launched += sparse_memory_stats(rd, n_rd, wr, n_wr, am, tm, st, P<double>(ctx->partials), parts,
+                                    P<uint64_t>(ctx->mp_ovf), ctx->sparse_scr.p, ctx->sparse_scr.cap, s);
+    launch_entropy_finish(st, P<double>(ctx->partials), parts, tm, raw ? 64u : k, s);
+    launched += 1;
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const DevState& h = *ctx->h_state;
+  if (h.flags & F_SLOT_RANGE) return fail(ctx, AIWC_ERR_ARGUMENT, "received address outside the owned key range");
+  ctx->mp_hist0.assign(h.cnt_hist0, h.cnt_hist0 + CBINS);
+  ctx->mp_big.resize(h.lvl0_ovf_n);
+  if (h.lvl0_ovf_n) {
+    CK(cudaMemcpyAsync(ctx->mp_big.data(), ctx->mp_ovf.p, h.lvl0_ovf_n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  aiwc_memory_part r{};
+  r.unique_reads = h.unique_r; r.unique_writes = h.unique_w; r.footprint = h.footprint;
+  for (int i = 0; i < NLEVELS; ++i) r.level_sum[i] = m ? -h.entropy[i] : 0.0;
+  r.cnt_hist0 = ctx->mp_hist0.data();
+  r.n_big = ctx->mp_big.size();
+  r.big = ctx->mp_big.data();
+  r.kernels_launched = launched;
+  *out = r;
+  return AIWC_OK;
+}
+

@@ -1,0 +1,408 @@
+"""Multi-GPU AIWC: work-group shards, key-range owners, one all-to-all.
+
+Every rank owns a contiguous range of work-groups.  Everything except the
+address statistics is local to a work-group -- segments and work-item
+lifetimes (ITB / IPT), per-(site, group) branch streams, opcode / width
+counts -- so those partials are combined exactly with sums (histograms,
+pattern tables) and gathers (overflow lists, site and width lists).  The
+reference's own shard-merge equality (`metrics.py:235-270`) is
+what makes this exact.
+
+Addresses need one exchange: after an all-reduce of the shards' address
+statistics every rank knows the global key map key = (addr - base) >> k;
+key ranges aligned to 1024 keys are assigned to owners (so every LSB-skip
+level <= 10 groups keys of a single owner), each rank sends its addresses to
+their owners with one all-to-all, and each owner computes unique counts,
+level-0 count-of-counts and sum(p log2 p) per level for its keys with the
+global access count M.  The owners' partials add up to the whole-trace values.
+
+The engine work is behind a small backend interface (`CudaBackend` runs the
+C ABI on the local GPU with NCCL; the CPU tests plug in an oracle-backed
+backend with gloo), so the exchange and combine logic here is the code the
+GPU path runs.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HBINS = 1024
+CBINS = 1024
+
+
+@dataclass
+class ShardPartial:
+    """Exact per-shard quantities (everything but the address statistics)."""
+
+    n_events: int
+    total_instructions: int
+    work_items: int
+    barriers_hit: int
+    total_reads: int
+    total_writes: int
+    opcode_counts: np.ndarray            # u64 per opcode id (shared dictionary)
+    widths: list                         # [(width, count, first global event index)]
+    itb_hist: np.ndarray                 # HBINS u64
+    itb_ovf: np.ndarray                  # values >= HBINS
+    itb_sum: int
+    ipt_hist: np.ndarray
+    ipt_ovf: np.ndarray
+    ipt_sum: int
+    branch_table: np.ndarray             # u64 total << 32 | taken, 2^H entries
+    sites: dict                          # site -> executions
+    branch_executions: int
+    addr_stats: tuple | None             # (min, max, and, or) of the shard's addresses
+    handle: object = None                # backend state (device address arrays)
+
+
+@dataclass
+class MemoryPartial:
+    unique_reads: int
+    unique_writes: int
+    footprint: int
+    level_sum: np.ndarray                # 11 x f64: sum of p log2 p over owned keys
+    cnt_hist0: np.ndarray                # CBINS u64
+    big: np.ndarray                      # level-0 counts >= CBINS
+
+
+@dataclass
+class KeyMap:
+    base: int
+    k: int
+    n_keys: int
+    keys_per_rank: int
+
+    def owned(self, rank: int) -> tuple[int, int]:
+        lo = rank * self.keys_per_rank
+        hi = min(self.n_keys, lo + self.keys_per_rank)
+        return lo, max(0, hi - lo)
+
+
+def key_map(stats: tuple, nranks: int) -> KeyMap:
+    """Global key map from the all-reduced address statistics (the engine's rule)."""
+    amin, amax, aand, aor = stats
+    base = amin & ~1023
+    vary = aand ^ aor
+    k = min((vary & -vary).bit_length() - 1, 32) if vary else 0
+    n_keys = ((amax - base) >> k) + 1
+    kpr = -(-n_keys // nranks)
+    kpr = -(-kpr // 1024) * 1024
+    return KeyMap(base, k, n_keys, kpr)
+
+
+# ---------------------------------------------------------------------------
+# host finishing of combined exact integers (same rules as aiwc_finalize)
+# ---------------------------------------------------------------------------
+def coverage90(big_desc, small_hist, total: int) -> int:
+    """Smallest k of the most frequent keys covering 9/10 of total (entropy.py:49-66)."""
+    if total == 0:
+        return 0
+    cum = 0
+    k = 0
+    for c in big_desc:
+        cum += int(c)
+        k += 1
+        if cum * 10 >= total * 9:
+            return k
+    if small_hist is not None:
+        for c in range(len(small_hist) - 1, 0, -1):
+            h = int(small_hist[c])
+            if not h:
+                continue
+            need = total * 9 - cum * 10
+            take = -(-need // (c * 10))
+            if take <= h:
+                return k + take
+            cum += h * c
+            k += h
+    return k
+
+
+def order_stats(hist: np.ndarray, ovf_sorted: np.ndarray, total_sum: int) -> tuple:
+    """(n, min, max, sum, mid_lo, mid_hi) of a histogram + sorted overflow values."""
+    small = int(hist.sum())
+    n = small + int(len(ovf_sorted))
+    if n == 0:
+        return (0, 0, 0, total_sum, 0, 0)
+    csum = np.cumsum(hist.astype(np.int64))
+
+    def at(rank: int) -> int:
+        if rank >= small:
+            return int(ovf_sorted[rank - small])
+        return int(np.searchsorted(csum, rank, side="right"))
+
+    return (n, at(0), at(n - 1), total_sum, at((n - 1) // 2), at(n // 2))
+
+
+def branch_entropies(table: np.ndarray):
+    """Yokota / linear from the pooled pattern table -- the reference's numpy
+    expressions (entropy.py:123-132) on the same integer tables."""
+    total_tab = (table >> np.uint64(32)).astype(np.int64)
+    taken_tab = (table & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    observations = int(total_tab.sum())
+    if observations == 0:
+        return 0.0, 0.0, 0
+    mask = total_tab > 0
+    totals = total_tab[mask].astype(np.float64)
+    p = taken_tab[mask] / totals
+    q = 1.0 - p
+    with np.errstate(divide="ignore", invalid="ignore"):
+        h = -(np.where(p > 0, p * np.log2(np.where(p > 0, p, 1.0)), 0.0)
+              + np.where(q > 0, q * np.log2(np.where(q > 0, q, 1.0)), 0.0))
+    weights = totals / observations
+    return float((weights * h).sum()), float((weights * np.minimum(p, q)).sum()), observations
+
+
+# ---------------------------------------------------------------------------
+# collectives (torch.distributed: NCCL on GPUs, gloo in the CPU tests)
+# ---------------------------------------------------------------------------
+def _allreduce_i64(vals: np.ndarray, op, group, device) -> np.ndarray:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(vals).view(np.int64).copy()).to(device)
+    dist.all_reduce(t, op=op, group=group)
+    return t.cpu().numpy().view(np.uint64)
+
+
+def _gather_objects(obj, group) -> list:
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def allreduce_stats(stats, group, device):
+    """(min, max, and, or) over ranks; empty shards contribute identities."""
+    import torch.distributed as dist
+
+    amin, amax, aand, aor = stats if stats is not None else ((1 << 64) - 1, 0, (1 << 64) - 1, 0)
+    flip = 1 << 63  # unsigned order as signed order
+    mn = _allreduce_i64(np.array([amin ^ flip], np.uint64), dist.ReduceOp.MIN, group, device)[0] ^ np.uint64(flip)
+    mx = _allreduce_i64(np.array([amax ^ flip], np.uint64), dist.ReduceOp.MAX, group, device)[0] ^ np.uint64(flip)
+    an = _allreduce_i64(np.array([aand], np.uint64), dist.ReduceOp.BAND, group, device)[0]
+    orr = _allreduce_i64(np.array([aor], np.uint64), dist.ReduceOp.BOR, group, device)[0]
+    return int(mn), int(mx), int(an), int(orr)
+
+
+def exchange(entries, counts: list[int], group, device):
+    """All-to-all of owner-grouped u64 entries; returns (received tensor, n)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    send_counts = torch.tensor(counts, dtype=torch.int64, device=device)
+    recv_counts = torch.empty(world, dtype=torch.int64, device=device)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    rc = [int(x) for x in recv_counts.cpu().tolist()]
+    recv = torch.empty(max(1, sum(rc)), dtype=torch.int64, device=device)
+    dist.all_to_all_single(recv[: sum(rc)], entries[: sum(counts)].to(device), rc, list(counts), group=group)
+    return recv, sum(rc)
+
+
+def comm_device(backend, group=None):
+    """Where collective buffers live: the backend's device under NCCL, host
+    memory under gloo (the CPU tests, and single-GPU tests of CudaBackend)."""
+    import torch
+    import torch.distributed as dist
+
+    return torch.device("cpu") if dist.get_backend(group) == "gloo" else backend.device
+
+
+def sharded_result(backend, shard, shard_offset: int, group=None):
+    """Every rank: exact whole-trace EngineResult from its work-group shard."""
+    import torch.distributed as dist
+
+    from .metrics import EngineResult
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    device = comm_device(backend, group)
+    sp: ShardPartial = backend.shard(shard, shard_offset)
+
+    # ---- sums: one packed all-reduce ----
+    scalars = np.array([sp.n_events, sp.total_instructions, sp.work_items, sp.barriers_hit, sp.total_reads,
+                        sp.total_writes, sp.itb_sum, sp.ipt_sum, sp.branch_executions], dtype=np.uint64)
+    packed = np.concatenate([scalars, sp.opcode_counts.astype(np.uint64), sp.itb_hist, sp.ipt_hist,
+                             sp.branch_table.astype(np.uint64)])
+    summed = _allreduce_i64(packed, dist.ReduceOp.SUM, group, device)
+    o = 0
+    sc = [int(v) for v in summed[o:o + len(scalars)]]; o += len(scalars)
+    n_opc = len(sp.opcode_counts)
+    opcode_counts = [int(v) for v in summed[o:o + n_opc]]; o += n_opc
+    itb_hist = summed[o:o + HBINS]; o += HBINS
+    ipt_hist = summed[o:o + HBINS]; o += HBINS
+    branch_table = summed[o:]
+    n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec = sc
+
+    # ---- gathers: overflow values, widths, sites ----
+    parts = _gather_objects((sp.itb_ovf.tolist(), sp.ipt_ovf.tolist(), sp.widths, sp.sites), group)
+    itb_ovf = np.sort(np.array([v for p in parts for v in p[0]], dtype=np.uint64))
+    ipt_ovf = np.sort(np.array([v for p in parts for v in p[1]], dtype=np.uint64))
+    wmap: dict = {}
+    for p in parts:
+        for w, c, first in p[2]:
+            c0, f0 = wmap.get(w, (0, None))
+            wmap[w] = (c0 + c, first if f0 is None else min(f0, first))
+    widths = [(w, c) for w, (c, _) in sorted(wmap.items(), key=lambda kv: kv[1][1])]
+    smap: dict = {}
+    for p in parts:
+        for s, c in p[3].items():
+            smap[s] = smap.get(s, 0) + c
+    sites = sorted(smap.items())
+
+    # ---- addresses: global key map, owner exchange, owner partials ----
+    total_m = total_reads + total_writes
+    if total_m:
+        stats = allreduce_stats(sp.addr_stats, group, device)
+        km = key_map(stats, world)
+        reads, writes, counts = backend.partition(sp, km, world)
+        recv_r, n_r = exchange(reads, counts[:world], group, device)
+        recv_w, n_w = exchange(writes, counts[world:], group, device)
+        lo, n_owned = km.owned(rank)
+        mp = backend.memory_partial(recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m)
+    else:
+        mp = MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(CBINS, np.uint64), np.zeros(0, np.uint64))
+    msum = _allreduce_i64(np.concatenate([np.array([mp.unique_reads, mp.unique_writes, mp.footprint], np.uint64),
+                                          mp.cnt_hist0.astype(np.uint64)]), dist.ReduceOp.SUM, group, device)
+    import torch
+
+    lsum = torch.from_numpy(np.asarray(mp.level_sum, dtype=np.float64).copy()).to(device)
+    dist.all_reduce(lsum, group=group)
+    level_sum = lsum.cpu().numpy()
+    big = np.sort(np.array([v for b in _gather_objects(mp.big.tolist(), group) for v in b], dtype=np.uint64))[::-1]
+    unique_r, unique_w, footprint = (int(v) for v in msum[:3])
+    hist0 = msum[3:]
+
+    # ---- finish with the same exact rules as aiwc_finalize ----
+    yokota, linear, observations = branch_entropies(branch_table)
+    ent = [-float(v) for v in level_sum] if total_m else [0.0] * 11
+    oc = sorted((c for c in opcode_counts if c), reverse=True)
+    return EngineResult(
+        n_events=n_events, total_instructions=total_instr, work_items=work_items, barriers_hit=barriers,
+        opcode_coverage=coverage90(oc, None, sum(oc)),
+        itb=order_stats(itb_hist, itb_ovf, itb_sum), ipt=order_stats(ipt_hist, ipt_ovf, ipt_sum),
+        total_reads=total_reads, total_writes=total_writes, unique_reads=unique_r, unique_writes=unique_w,
+        footprint=footprint, footprint_90=coverage90(big, hist0, total_m) if total_m else 0,
+        gmae=ent[0], lmae=ent[1:], branch_executions=br_exec, branch_observations=observations,
+        branch_excluded=br_exec - observations, branch_90=coverage90(sorted((c for _, c in sites), reverse=True), None, br_exec),
+        yokota=yokota, linear=linear, entries=unique_r + unique_w + br_exec,
+        opcode_counts=opcode_counts, widths=widths, sites=sites, used_dense_table=True, kernels_launched=0,
+    )
+
+
+def sharded_report(backend, shard, shard_offset: int, kernel_name: str, invocation: int, global_size, local_size,
+                   opcodes: list[str], group=None):
+    """AiwcReport of the whole trace, identical on every rank."""
+    from .metrics import KernelAccumulator, finalize
+
+    res = sharded_result(backend, shard, shard_offset, group)
+    acc = KernelAccumulator(kernel_name, [invocation], [(invocation, tuple(global_size), tuple(local_size))], res,
+                            list(opcodes))
+    return finalize(acc)
+
+
+# ---------------------------------------------------------------------------
+# CUDA backend: the C ABI on this rank's GPU
+# ---------------------------------------------------------------------------
+class _CudaArray:
+    """Zero-copy torch view of an engine-owned device buffer."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+
+@dataclass
+class CudaBackend:
+    """The C ABI on this rank's GPU.  `timing` records per-phase CUDA-event
+    times of the shard pass (last_phase_ms); `launches` counts the engine
+    kernels this backend queued (shard pass + partition + owner partial)."""
+
+    device_index: int = 0
+    timing: bool = False
+    ctx: object = None
+    last_phase_ms: list = field(default_factory=list)
+    last_d2h: int = 0
+    launches: int = 0
+
+    @property
+    def device(self):
+        import torch
+
+        return torch.device("cuda", self.device_index)
+
+    def _ctx(self):
+        from . import _native
+
+        if self.ctx is None:
+            flags = _native.OPT_NO_CONSERVATION | _native.OPT_SHARD | (_native.OPT_TIMING if self.timing else 0)
+            self.ctx = _native.Context(self.device_index, flags=flags)
+        return self.ctx
+
+    def shard(self, tr, shard_offset: int) -> ShardPartial:
+        from . import _native
+        from .metrics import _copy_result, ingest_columns
+
+        ctx = self._ctx()
+        lib = ctx.lib
+        ctx.check(lib.aiwc_reset(ctx.h))
+        stream = ingest_columns(ctx, tr)
+        res = _native.Result()
+        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
+        self.last_phase_ms = list(res.phase_ms)
+        self.last_d2h = res.d2h_bytes
+        self.launches += res.kernels_launched
+        r = _copy_result(res)
+        t = _native.ShardTables()
+        ctx.check(lib.aiwc_shard_tables_get(ctx.h, ctypes.byref(t)))
+        arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint64)  # noqa: E731
+        firsts = arr(t.width_first, len(r.widths))
+        return ShardPartial(
+            n_events=r.n_events, total_instructions=r.total_instructions, work_items=r.work_items,
+            barriers_hit=r.barriers_hit, total_reads=r.total_reads, total_writes=r.total_writes,
+            opcode_counts=np.array(r.opcode_counts, dtype=np.uint64),
+            widths=[(w, c, int(f) + shard_offset) for (w, c), f in zip(r.widths, firsts)],
+            itb_hist=arr(t.itb_hist, HBINS), itb_ovf=arr(t.itb_ovf, t.n_itb_ovf), itb_sum=r.itb[3],
+            ipt_hist=arr(t.ipt_hist, HBINS), ipt_ovf=arr(t.ipt_ovf, t.n_ipt_ovf), ipt_sum=r.ipt[3],
+            branch_table=arr(t.branch_table, t.branch_table_size) if t.branch_table_size else np.zeros(1 << 16, np.uint64),
+            sites=dict(r.sites), branch_executions=r.branch_executions,
+            addr_stats=tuple(int(v) for v in t.addr_stats) if (r.total_reads + r.total_writes) else None,
+        )
+
+    def partition(self, sp: ShardPartial, km: KeyMap, nranks: int):
+        import torch
+
+        ctx = self._ctx()
+        counts = (ctypes.c_uint64 * (2 * nranks))()
+        rp, wp = ctypes.POINTER(ctypes.c_uint64)(), ctypes.POINTER(ctypes.c_uint64)()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_partition_addresses(ctx.h, km.base, km.k, km.keys_per_rank, nranks, ctypes.byref(rp),
+                                                   ctypes.byref(wp), counts, ctypes.c_void_p(stream)))
+        c = [int(x) for x in counts]
+        self.launches += 2 * (int(sum(c[:nranks]) > 0) + int(sum(c[nranks:]) > 0))  # count + scatter per array
+        view = lambda p, n: torch.as_tensor(_CudaArray(ctypes.cast(p, ctypes.c_void_p).value, max(n, 1)),  # noqa: E731
+                                            device=self.device)
+        return view(rp, sum(c[:nranks])), view(wp, sum(c[nranks:])), c
+
+    def memory_partial(self, recv_r, n_r: int, recv_w, n_w: int, km: KeyMap, key_lo: int, n_keys: int,
+                       total_m: int) -> MemoryPartial:
+        import torch
+
+        from . import _native
+
+        ctx = self._ctx()
+        out = _native.MemoryPart()
+        recv_r, recv_w = recv_r.to(self.device), recv_w.to(self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_memory_partial(ctx.h, ctypes.c_void_p(recv_r.data_ptr()), n_r,
+                                              ctypes.c_void_p(recv_w.data_ptr()), n_w, km.base, km.k, key_lo, n_keys,
+                                              total_m, ctypes.byref(out), ctypes.c_void_p(stream)))
+        self.launches += out.kernels_launched
+        big = np.ctypeslib.as_array(out.big, shape=(out.n_big,)).copy() if out.n_big else np.zeros(0, np.uint64)
+        return MemoryPartial(out.unique_reads, out.unique_writes, out.footprint, np.array(out.level_sum[:]),
+                             np.ctypeslib.as_array(out.cnt_hist0, shape=(CBINS,)).copy(), big)

@@ -130,40 +130,46 @@ def trace_info(tr: ColumnarTrace) -> _native.TraceInfo:
     return info
 
 
+def ingest_columns(ctx, tr: ColumnarTrace):
+    """aiwc_ingest (device columns) or aiwc_ingest_host (host columns) of one
+    columnar trace into ctx; returns the stream handle the work was queued on."""
+    kind, payload = tr.kind, tr.payload
+    lib = ctx.lib
+    info = trace_info(tr)
+    if _is_torch(kind) and kind.is_cuda:
+        import torch
+
+        if kind.dtype != torch.uint8 or payload.dtype not in (torch.uint64, torch.int64):
+            raise AiwcError("CUDA columns must be uint8 kind and (u)int64 payload tensors")
+        kind = kind.contiguous()
+        payload = payload.contiguous()
+        if kind.data_ptr() % 16:
+            kind = kind.clone()
+        if payload.data_ptr() % 16:
+            payload = payload.clone()
+        stream = torch.cuda.current_stream(kind.device).cuda_stream
+        ctx.check(lib.aiwc_ingest(ctx.h, ctypes.c_void_p(kind.data_ptr()), ctypes.c_void_p(payload.data_ptr()),
+                                  ctypes.byref(info), ctypes.c_void_p(stream)))
+        return stream
+    if _is_torch(kind):
+        kind, payload = kind.numpy(), payload.numpy()
+    kind = np.ascontiguousarray(kind, dtype=np.uint8)
+    payload = np.ascontiguousarray(payload).view(np.uint64)
+    ctx.check(lib.aiwc_ingest_host(ctx.h, kind.ctypes.data_as(ctypes.c_void_p),
+                                   payload.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info), None))
+    return None
+
+
 def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
     """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace."""
-    kind, payload = tr.kind, tr.payload
-    on_cuda = _is_torch(kind) and kind.is_cuda
+    kind = tr.kind
     if device is None:
-        device = kind.device.index if on_cuda else _default_device()
+        device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
     ctx = _get_ctx(device)
     try:
         lib = ctx.lib
         ctx.check(lib.aiwc_reset(ctx.h))
-        info = trace_info(tr)
-        if on_cuda:
-            import torch
-
-            if kind.dtype != torch.uint8 or payload.dtype not in (torch.uint64, torch.int64):
-                raise AiwcError("CUDA columns must be uint8 kind and (u)int64 payload tensors")
-            kind = kind.contiguous()
-            payload = payload.contiguous()
-            if kind.data_ptr() % 16:
-                kind = kind.clone()
-            if payload.data_ptr() % 16:
-                payload = payload.clone()
-            stream = torch.cuda.current_stream(kind.device).cuda_stream
-            rc = lib.aiwc_ingest(ctx.h, ctypes.c_void_p(kind.data_ptr()), ctypes.c_void_p(payload.data_ptr()),
-                                 ctypes.byref(info), ctypes.c_void_p(stream))
-        else:
-            if _is_torch(kind):
-                kind, payload = kind.numpy(), payload.numpy()
-            kind = np.ascontiguousarray(kind, dtype=np.uint8)
-            payload = np.ascontiguousarray(payload).view(np.uint64)
-            rc = lib.aiwc_ingest_host(ctx.h, kind.ctypes.data_as(ctypes.c_void_p),
-                                      payload.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info), None)
-            stream = None
-        ctx.check(rc)
+        stream = ingest_columns(ctx, tr)
         res = _native.Result()
         ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
         return _copy_result(res)

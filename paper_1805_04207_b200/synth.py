@@ -47,6 +47,21 @@ def n_events(cfg: int, work_items: int) -> int:
     return int(info(cfg, work_items).n_events)
 
 
+def shard_range(cfg: int, work_items: int, rank: int, world: int) -> tuple[int, int]:
+    """(first event, event count) of rank's contiguous work-group shard.
+
+    Layout (aiwc_synth.cu): KERNEL_BEGIN, then `groups` work-groups of equal
+    length, then KERNEL_END; rank 0 also takes the kernel begin and the last
+    rank the kernel end, so the shards tile the whole trace."""
+    n = n_events(cfg, work_items)
+    groups = work_items // LOCAL[cfg]
+    per_group = (n - 2) // groups
+    g_lo, g_hi = groups * rank // world, groups * (rank + 1) // world
+    first = 0 if rank == 0 else 1 + g_lo * per_group
+    end = n if rank == world - 1 else 1 + g_hi * per_group
+    return first, end - first
+
+
 def _columnar(cfg: int, work_items: int, kind, payload, ti) -> ColumnarTrace:
     lv = LOCAL[cfg]
     return ColumnarTrace(kind, payload, NAMES[cfg], 0, (work_items, 1, 1), (lv, 1, 1), list(OPCODES[cfg]), [],

@@ -54,3 +54,18 @@ def test_event_counts_match_survey():
     want = {2: 268500994, 3: 2148007938, 4: 337649666, 5: 2046951426}
     for cfg, n in want.items():
         assert 2 + synth.FULL_WORK_ITEMS[cfg] // 256 * per_group[cfg] == n
+
+
+@pytest.mark.parametrize("cfg,w", [(1, 4096), (2, 8192), (5, 4096)])
+def test_shard_ranges_tile_the_trace_at_work_group_boundaries(cfg, w):
+    from paper_1805_04207_b200.trace import K_WG_BEGIN
+
+    tr = synth.python_trace(cfg, w)
+    for world in (1, 2, 3, 8):
+        pos = 0
+        for r in range(world):
+            first, count = synth.shard_range(cfg, w, r, world)
+            assert first == pos
+            assert first == 0 or tr.kind[first] == K_WG_BEGIN
+            pos += count
+        assert pos == tr.n_events

@@ -1,0 +1,157 @@
+"""Multi-rank path on CPU: two gloo ranks, each holding one work-group shard
+of a golden trace, run paper_1805_04207_b200.dist (address statistics
+all-reduce, key-range owners, all-to-all of addresses, owner partials,
+exact combine).  The engine steps are served by an oracle-backed test
+backend; the combined report must equal the reference's own report."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from conftest import ROOT, assert_report_matches, golden_cases
+
+CASES = ["wavefront_big", "bfs_flags", "sweep4", "long_segments", "hot_address", "random31337_3", "random202_5",
+         "coin_20k", "offgrid_groups", "branch_streams_per_group"]
+
+
+class OracleBackend:
+    """Test double for dist.CudaBackend: the C oracle's accumulator + numpy."""
+
+    device = torch.device("cpu")
+
+    def __init__(self, n_opcodes):
+        self.n_opcodes = n_opcodes
+
+    def shard(self, tr, offset):
+        from oracle import oracle
+        from paper_1805_04207_b200.dist import HBINS, ShardPartial
+
+        acc = oracle.accumulator(tr.kind, tr.payload, self.n_opcodes)
+
+        def hist(v):
+            v = v.astype(np.int64)
+            return (np.bincount(v[v < HBINS], minlength=HBINS).astype(np.uint64), np.sort(v[v >= HBINS]).astype(np.uint64))
+
+        ih, io = hist(acc["itb"])
+        ph, po = hist(acc["ipt"])
+        rd_a, rd_c = acc["rd"]
+        wr_a, wr_c = acc["wr"]
+        addrs = np.concatenate([rd_a, wr_a])
+        stats = None
+        if addrs.size:
+            stats = (int(addrs.min()), int(addrs.max()), int(np.bitwise_and.reduce(addrs)), int(np.bitwise_or.reduce(addrs)))
+        table = (acc["total"].astype(np.uint64) << np.uint64(32)) | acc["taken"].astype(np.uint64)
+        return ShardPartial(
+            n_events=tr.n_events, total_instructions=acc["total_instructions"], work_items=acc["work_items"],
+            barriers_hit=acc["barriers"], total_reads=int(rd_c.sum()), total_writes=int(wr_c.sum()),
+            opcode_counts=acc["opc"], widths=[(w, c, f + offset) for w, c, f in acc["widths"]],
+            itb_hist=ih, itb_ovf=io, itb_sum=int(acc["itb"].sum()), ipt_hist=ph, ipt_ovf=po,
+            ipt_sum=int(acc["ipt"].sum()), branch_table=table, sites=acc["sites"], branch_executions=acc["executions"],
+            addr_stats=stats, handle=(rd_a, rd_c, wr_a, wr_c))
+
+    def partition(self, sp, km, nranks):
+        rd_a, rd_c, wr_a, wr_c = sp.handle
+        out, counts = [], []
+        for a, c in ((rd_a, rd_c), (wr_a, wr_c)):
+            a = np.repeat(a, c.astype(np.int64))
+            keys = (a - np.uint64(km.base)) >> np.uint64(km.k)
+            own = np.minimum(keys // np.uint64(km.keys_per_rank), np.uint64(nranks - 1)).astype(np.int64)
+            order = np.argsort(own, kind="stable")
+            out.append(torch.from_numpy(a[order].view(np.int64).copy()))
+            counts += np.bincount(own, minlength=nranks).tolist()
+        return out[0], out[1], counts
+
+    def memory_partial(self, recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m):
+        from paper_1805_04207_b200.dist import CBINS, MemoryPartial
+
+        rd = recv_r[:n_r].numpy().view(np.uint64)
+        wr = recv_w[:n_w].numpy().view(np.uint64)
+        keys = [((a - np.uint64(km.base)) >> np.uint64(km.k)) for a in (rd, wr)]
+        for kk in keys:  # every received address belongs to this owner's key range
+            assert ((kk >= np.uint64(lo)) & (kk - np.uint64(lo) < np.uint64(max(n_owned, 1)))).all()
+        allk = np.concatenate(keys)
+        uk, c = np.unique(allk, return_counts=True)
+        sums = []
+        for lvl in range(11):
+            j = max(0, lvl - km.k)
+            if not uk.size:
+                sums.append(0.0)
+                continue
+            g = np.unique(uk >> np.uint64(j), return_inverse=True)[1]
+            tot = np.bincount(g, weights=c)
+            p = tot / total_m
+            sums.append(float((p * np.log2(p)).sum()))
+        return MemoryPartial(int(np.unique(keys[0]).size), int(np.unique(keys[1]).size), int(uk.size), np.array(sums),
+                             np.bincount(c[c < CBINS], minlength=CBINS).astype(np.uint64),
+                             c[c >= CBINS].astype(np.uint64))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, names, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    from conftest import golden_cases as gc
+    from paper_1805_04207_b200 import dist as D
+    from paper_1805_04207_b200 import report_to_dict
+    from paper_1805_04207_b200.trace import ColumnarTrace, K_WG_BEGIN
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        by_name = {c["name"]: (c, t) for c, t in gc()}
+        for name in names:
+            c, tr = by_name[name]
+            starts = np.nonzero(tr.kind == K_WG_BEGIN)[0]
+            # contiguous work-group ranges, one per rank (a rank may get none)
+            cuts = [0] + [int(starts[len(starts) * r // world]) for r in range(1, world)] + [tr.n_events]
+            lo, hi = cuts[rank], cuts[rank + 1]
+            shard = ColumnarTrace(tr.kind[lo:hi], tr.payload[lo:hi], tr.kernel_name, tr.invocation, tr.global_size,
+                                  tr.local_size, tr.opcodes, tr.extra_groups)
+            rep = D.sharded_report(OracleBackend(len(tr.opcodes)), shard, lo, tr.kernel_name, tr.invocation,
+                                   tr.global_size, tr.local_size, tr.opcodes)
+            q.put((rank, name, report_to_dict(rep)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_reports_match_reference(world):
+    from oracle import oracle
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=240) for _ in range(world * len(CASES))]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = {c["name"]: c["report"] for c, _ in golden_cases() if c["name"] in CASES}
+    for rank, name, rep in got:
+        assert_report_matches(rep, want[name])
+
+
+def test_key_map_owner_ranges_are_block_aligned():
+    from paper_1805_04207_b200.dist import key_map
+
+    km = key_map((4096 + 4, 4096 + 4 * 99999, 0, ~3 & ((1 << 64) - 1)), 3)
+    assert km.k == 2 and km.keys_per_rank % 1024 == 0
+    assert sum(km.owned(r)[1] for r in range(3)) == km.n_keys
