@@ -14,6 +14,12 @@
 // traces every lane carries the same count), counts >= CBINS add their fp64
 // p*log2(p) term to a thread-owned partial and, at level 0, their exact value
 // to the overflow list the coverage walk needs.
+//
+// Fast path: a warp whose 256 table entries are all equal (streaming and
+// strided traces: every key touched the same number of times, or not at all)
+// only extends a run-length counter held by the warp; every level <= 8 of a
+// run of R such chunks with key count c is R * (256 >> j) groups of count
+// c << j, recorded once when the run ends.
 #include <math.h>
 
 #include <algorithm>
@@ -101,54 +107,90 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
     }
   };
 
+  // warp-uniform run: run_n chunks of 256 keys, every entry == run_e (warp-uniform registers)
+  unsigned long long run_e = 0, run_n = 0;
+  const int fast_lev = nlev < 9 ? nlev : 9;
+  auto flush_run = [&]() {
+    if (run_n == 0) return;
+    const unsigned long long r = run_e & 0xFFFFFFFFull, w = run_e >> 32, c = r + w;
+    const unsigned long long keys = run_n * 256ull;
+    if (lane == 0) {
+      ur += r ? keys : 0ull; uw += w ? keys : 0ull; fp += keys;
+      for (int j = 0; j < fast_lev; ++j) {
+        const unsigned long long v = c << j, groups = keys >> j;
+        if (v < (unsigned long long)CBINS) atomicAdd(&hsm[j * CBINS + (uint32_t)v], (uint32_t)groups);
+        else X.part[j * T] += plogp(v, m) * (double)groups;
+      }
+    }
+    if (c >= (unsigned long long)CBINS) {  // level-0 overflow list: one entry per key
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(X.ovf_n, keys);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      for (unsigned long long i = lane; i < keys; i += 32) X.ovf[b + i] = c;
+    }
+    run_n = 0;
+  };
+
   unsigned long long cur[K], nxt[K];
   uint64_t ch = blockIdx.x;
   if (ch < n_chunks) load(ch, cur);
   for (; ch < n_chunks; ch += gridDim.x) {
     if (ch + gridDim.x < n_chunks) load(ch + gridDim.x, nxt);
-    unsigned long long c[K];
+    bool same = true;
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const unsigned long long r = cur[i] & 0xFFFFFFFFull, w = cur[i] >> 32;
-      ur += r != 0; uw += w != 0; fp += (r | w) != 0;
-      c[i] = r + w;
-    }
-    // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
-    bool uni = true;
-#pragma unroll
-    for (int i = 1; i < K; ++i) uni &= c[i] == c[0];
-    if (__all_sync(0xffffffffu, uni)) {
-      X.rec_warp(0, c[0], K, true, 32);
+    for (int i = 1; i < K; ++i) same &= cur[i] == cur[0];
+    const unsigned long long e0 = __shfl_sync(0xffffffffu, cur[0], 0);
+    unsigned long long s;  // sum of the warp's 256 counts (levels 9, 10)
+    if (__all_sync(0xffffffffu, same && cur[0] == e0)) {
+      // ---- warp-uniform chunk: extend the run ----
+      if (e0 != run_e) { flush_run(); run_e = e0; }
+      if (e0) ++run_n;
+      s = ((e0 & 0xFFFFFFFFull) + (e0 >> 32)) * 256ull;
     } else {
-      unsigned long long v = c[0];
-      uint32_t run = 1;
+      unsigned long long c[K];
 #pragma unroll
-      for (int i = 1; i < K; ++i) {
-        if (c[i] == v) { ++run; }
-        else { X.rec(0, v, run); v = c[i]; run = 1; }
+      for (int i = 0; i < K; ++i) {
+        const unsigned long long r = cur[i] & 0xFFFFFFFFull, w = cur[i] >> 32;
+        ur += r != 0; uw += w != 0; fp += (r | w) != 0;
+        c[i] = r + w;
       }
-      X.rec(0, v, run);
-    }
-    unsigned long long s1[4], s2[2], s3;
+      // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
+      bool uni = true;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
-    s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
-    s3 = s2[0] + s2[1];
-    if (nlev > 1) {
-      const bool u1 = s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3];
-      if (__all_sync(0xffffffffu, u1)) X.rec_warp(1, s1[0], 4, true, 32);
-      else { X.rec(1, s1[0], 1); X.rec(1, s1[1], 1); X.rec(1, s1[2], 1); X.rec(1, s1[3], 1); }
-    }
-    if (nlev > 2) {
-      if (__all_sync(0xffffffffu, s2[0] == s2[1])) X.rec_warp(2, s2[0], 2, true, 32);
-      else { X.rec(2, s2[0], 1); X.rec(2, s2[1], 1); }
-    }
-    if (nlev > 3) X.rec_warp(3, s3, 1, true, 32);
-    unsigned long long s = s3;
+      for (int i = 1; i < K; ++i) uni &= c[i] == c[0];
+      if (__all_sync(0xffffffffu, uni)) {
+        X.rec_warp(0, c[0], K, true, 32);
+      } else {
+        unsigned long long v = c[0];
+        uint32_t run = 1;
 #pragma unroll
-    for (int j = 4; j <= 8; ++j) {
-      s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
-      if (j < nlev) X.rec_warp(j, s, 1, (lane & ((1 << (j - 3)) - 1)) == 0, 32u >> (j - 3));
+        for (int i = 1; i < K; ++i) {
+          if (c[i] == v) { ++run; }
+          else { X.rec(0, v, run); v = c[i]; run = 1; }
+        }
+        X.rec(0, v, run);
+      }
+      unsigned long long s1[4], s2[2], s3;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
+      s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
+      s3 = s2[0] + s2[1];
+      if (nlev > 1) {
+        const bool u1 = s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3];
+        if (__all_sync(0xffffffffu, u1)) X.rec_warp(1, s1[0], 4, true, 32);
+        else { X.rec(1, s1[0], 1); X.rec(1, s1[1], 1); X.rec(1, s1[2], 1); X.rec(1, s1[3], 1); }
+      }
+      if (nlev > 2) {
+        if (__all_sync(0xffffffffu, s2[0] == s2[1])) X.rec_warp(2, s2[0], 2, true, 32);
+        else { X.rec(2, s2[0], 1); X.rec(2, s2[1], 1); }
+      }
+      if (nlev > 3) X.rec_warp(3, s3, 1, true, 32);
+      s = s3;
+#pragma unroll
+      for (int j = 4; j <= 8; ++j) {
+        s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
+        if (j < nlev) X.rec_warp(j, s, 1, (lane & ((1 << (j - 3)) - 1)) == 0, 32u >> (j - 3));
+      }
     }
     if (nlev > 9) {  // levels 9, 10 need the whole CTA (k < 2 only)
       if (lane == 0) D.wsum[warp] = s;
@@ -168,6 +210,7 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
 #pragma unroll
     for (int i = 0; i < K; ++i) cur[i] = nxt[i];
   }
+  flush_run();
   __syncthreads();
   // ---- flush: counters, histograms, fixed-order fp64 partials ----
   ur = warp_sum(ur); uw = warp_sum(uw); fp = warp_sum(fp);
