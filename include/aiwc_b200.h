@@ -12,8 +12,9 @@
  * Plain C types only.  Device pointers are CUDA global-memory addresses on the
  * ctx's device; `stream` is a cudaStream_t passed as void* (NULL = legacy
  * default stream).  One ctx per trace stream: a ctx is not thread-safe,
- * distinct ctxs are.  The ctx owns all scratch memory; the caller owns the
- * trace buffers until the call that received them returns.
+ * distinct ctxs are.  The ctx owns all scratch memory; trace buffers passed to
+ * aiwc_ingest must stay valid until the work that call queued on `stream` has
+ * completed (stream order; aiwc_finalize on the same stream implies it).
  */
 #ifndef AIWC_B200_H
 #define AIWC_B200_H

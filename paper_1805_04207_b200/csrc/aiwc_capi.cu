@@ -71,7 +71,7 @@ struct aiwc_ctx {
   aiwc_opts opts{};
   aiwc_error err{};
   int state = 0;  // 0 empty, 1 ingested, 2 finalized
-  Buf dev_state, ranges, opc, wcount, wfirst, itb_ovf, ipt_ovf, ipt_tab, dtab, rd, wr, br, partials, lvl0_ovf,
+  Buf dev_state, ranges, opc, wcount, wfirst, wpres, itb_ovf, ipt_ovf, ipt_tab, dtab, rd, wr, br, partials, lvl0_ovf,
       sparse_scr, branch_scr, branch_tab, kind_stage, pay_stage, sort_a, sort_b, sort_h;
   DevState* h_state = nullptr;  // pinned
   RangeSum* h_ranges = nullptr; // pinned
@@ -82,6 +82,7 @@ struct aiwc_ctx {
   uint64_t n_events_seen = 0;
   AddrMap am{};
   bool dense = false;
+  bool dense32 = false;     // u32 count|flags entries (fewer than 2^30 accesses)
   uint64_t ipt_tab_len = 0;
   uint32_t n_ranges = 0, tiles_per_cta = 0;
   uint32_t kernels = 0;
@@ -89,6 +90,10 @@ struct aiwc_ctx {
   uint64_t d2h = 0;
   // optional phase timing (AIWC_OPT_TIMING): pairs of events per phase
   cudaEvent_t ev[2 * AIWC_N_PHASES] = {};
+  // side stream: the dense table is cleared while pass 1 runs
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  size_t pre_zeroed = 0;
   bool timing = false;
   uint32_t marked = 0;  // phases whose end event was recorded for the current trace
   void mark(int phase, int end, cudaStream_t s) {
@@ -156,6 +161,9 @@ extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts
     ctx->timing = true;
     for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   }
+  CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   return AIWC_OK;
 }
 
@@ -166,13 +174,16 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
                  &ctx->ipt_ovf, &ctx->ipt_tab, &ctx->dtab, &ctx->rd, &ctx->wr, &ctx->br, &ctx->partials,
                  &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
                  &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
-                 &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf};
+                 &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
   if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
 }
 
@@ -247,12 +258,32 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   ctx->tiles_per_cta = tpc;
   const uint32_t n_sub = G * P1_SUB;
   CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
+  CK(grow(ctx->wpres, (size_t)G * sizeof(uint32_t)));
+  CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * sizeof(uint32_t), s));
   if (ctx->h_ranges_cap < n_sub) {
     if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
     CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ranges), (size_t)n_sub * sizeof(RangeSum)));
     ctx->h_ranges_cap = n_sub;
   }
   const bool with_stats = !info->has_addr_stats;
+  // Declared address statistics fix the key map before pass 1: clear a u32
+  // table of that size on the side stream meanwhile.  Bounded waste when the
+  // trace later takes another path: the table is <= 4 keys per event + 2^20.
+  ctx->pre_zeroed = 0;
+  if (n && !with_stats && info->addr_min <= info->addr_max && !(ctx->opts.flags & AIWC_OPT_SHARD)) {
+    const uint64_t b0 = info->addr_min & ~1023ull, vary = info->addr_and ^ info->addr_or;
+    const uint32_t k0 = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
+    const uint64_t sk = (info->addr_max - b0) >> k0;
+    if (sk < (1ull << 40) && (sk + 1) * 4 <= ctx->opts.dense_budget_bytes && sk + 1 <= 4 * n + (1ull << 20)) {
+      const size_t tb = (size_t)(sk + 1) * 4;
+      CK(grow(ctx->dtab, tb));
+      CK(cudaEventRecord(ctx->fork_ev, s));
+      CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
+      CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, ctx->aux));
+      CK(cudaEventRecord(ctx->join_ev, ctx->aux));
+      ctx->pre_zeroed = tb;
+    }
+  }
   if (n) {
     ctx->mark(AIWC_PH_PASS1, 0, s);
     launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s);
@@ -288,6 +319,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     amin = info->addr_min; amax = info->addr_max; aand = info->addr_and; aor = info->addr_or;
   }
   ctx->dense = false;
+  ctx->dense32 = M < E32_MAX_ACCESSES;
   ctx->am = AddrMap{};
   if (M) {
     if (amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
@@ -302,7 +334,11 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     am.low_const = (amin - am.base) & am.low_mask;
     const uint64_t span_keys = (amax - am.base) >> am.k;
     am.n_keys = span_keys + 1;
-    const bool fits = span_keys < (1ull << 40) && am.n_keys * 8 <= ctx->opts.dense_budget_bytes &&
+    am.off_max = (span_keys << am.k) | am.low_mask;
+    // u32 entries cost a second (flag) RED per access but halve the table:
+    // worth it when the table traffic dominates, i.e. at most one access per key
+    ctx->dense32 = M < E32_MAX_ACCESSES && M <= am.n_keys;
+    const bool fits = span_keys < (1ull << 40) && am.n_keys * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
                       am.n_keys <= 4 * M + (1ull << 20);
     // a shard keeps its addresses compacted: they are exchanged with the key owners
     ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
@@ -321,14 +357,20 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   CK(grow(ctx->br, std::max<uint64_t>(ctx->n_br, 1) * 8));
   if (M) {
     if (ctx->dense) {
-      CK(grow(ctx->dtab, ctx->am.n_keys * 8));
-      CK(cudaMemsetAsync(ctx->dtab.p, 0, ctx->am.n_keys * 8, s));
+      const size_t tb = ctx->am.n_keys * (ctx->dense32 ? 4 : 8);
+      if (ctx->pre_zeroed) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+      if (ctx->pre_zeroed < tb) {
+        CK(grow(ctx->dtab, tb));
+        CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, s));
+      }
     } else {
       CK(grow(ctx->rd, std::max<uint64_t>(ctx->n_rd, 1) * 8));
       CK(grow(ctx->wr, std::max<uint64_t>(ctx->n_wr, 1) * 8));
     }
     CK(grow(ctx->lvl0_ovf, (M / CBINS + 2) * 8));
   }
+
+  if (ctx->pre_zeroed && !ctx->dense) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
 
   // ---- main ingest pass ----
   if (n) {
@@ -342,14 +384,22 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.ranges = P<RangeSum>(ctx->ranges); a.st = st;
     a.opc_counts = P<unsigned long long>(ctx->opc);
     a.width_count = P<unsigned long long>(ctx->wcount); a.width_first = P<unsigned long long>(ctx->wfirst);
+    a.width_presence = P<uint32_t>(ctx->wpres);
     a.itb_ovf = P<uint32_t>(ctx->itb_ovf); a.ipt_ovf = P<uint32_t>(ctx->ipt_ovf);
     a.ipt_tab = ctx->ipt_tab_len ? P<unsigned long long>(ctx->ipt_tab) : nullptr; a.ipt_tab_len = ctx->ipt_tab_len;
     a.am = ctx->am;
-    a.dense = ctx->dense ? P<unsigned long long>(ctx->dtab) : nullptr;
+    a.dense = ctx->dense ? ctx->dtab.p : nullptr;
+    a.dense32 = ctx->dense32;
+    { const char* e = getenv("AIWC_DBG_SKIP"); a.dbg_skip = e ? (uint32_t)atoi(e) : 0u; }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);    ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, !ctx->dense || ctx->n_br > 0, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
     ctx->kernels += 1;
+    if (ctx->n_instr) {  // first index of each width 1..16 (the columns are only ours until here)
+      launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G, (uint64_t)tpc * TILE,
+                         P<unsigned long long>(ctx->wfirst), s);
+      ctx->kernels += 1;
+    }
   }
   ctx->mark(AIWC_PH_INGEST_TOTAL, 1, s);
   ctx->state = 1;
@@ -454,7 +504,7 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     if (ctx->dense) {
       const uint64_t chunks = (ctx->am.n_keys + 1023) / 1024;
       const uint32_t nct = (uint32_t)std::min<uint64_t>(chunks, ctx->n_parts);
-      launch_dense_stats(P<unsigned long long>(ctx->dtab), ctx->am.n_keys, ctx->am.k, M, st,
+      launch_dense_stats(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, ctx->am.k, M, st,
                          P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s);
       launch_entropy_finish(st, P<double>(ctx->partials), nct, M, ctx->am.k, s);
       ctx->kernels += 2;
@@ -828,7 +878,7 @@ extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n
         ++launched;
       }
     const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
-    launch_dense_stats(P<unsigned long long>(ctx->mp_tab), n_keys, k, tm, st, P<double>(ctx->partials), nct,
+    launch_dense_stats(ctx->mp_tab.p, false, n_keys, k, tm, st, P<double>(ctx->partials), nct,
                        P<uint64_t>(ctx->mp_ovf), s);
     launch_entropy_finish(st, P<double>(ctx->partials), nct, tm, k, s);
     launched += 2;

@@ -3,7 +3,8 @@
 // Replaces finalize's merged Counter, shannon_entropy, local_entropy x10 and
 // coverage_count over memory (pkg/src/aiwc/metrics.py:308-321,
 // pkg/src/aiwc/entropy.py:20-66) for traces whose address span fits a table
-// of (reads | writes << 32) counters indexed by key = (addr - base) >> k.
+// indexed by key = (addr - base) >> k.  Entries are u32 (count | read seen <<
+// 30 | write seen << 31) below 2^30 accesses, else u64 (reads | writes << 32).
 //
 // Each 128-thread CTA sweeps 1024-key chunks (8 consecutive keys per thread,
 // next chunk prefetched while the current one is folded).  Level n groups
@@ -77,7 +78,22 @@ struct Ctx {
   }
 };
 
-__global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long long* __restrict__ tab,
+// entry -> (access count, read seen, write seen)
+template <typename E>
+__device__ __forceinline__ void decode(E e, unsigned long long& c, uint32_t& r, uint32_t& w);
+template <>
+__device__ __forceinline__ void decode<uint32_t>(uint32_t e, unsigned long long& c, uint32_t& r, uint32_t& w) {
+  c = e & E32_COUNT; r = (e >> 30) & 1u; w = e >> 31;
+}
+template <>
+__device__ __forceinline__ void decode<unsigned long long>(unsigned long long e, unsigned long long& c, uint32_t& r,
+                                                           uint32_t& w) {
+  const unsigned long long lo = e & 0xFFFFFFFFull, hi = e >> 32;
+  c = lo + hi; r = lo != 0; w = hi != 0;
+}
+
+template <typename E>
+__global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__ tab,
                                                            uint64_t n_keys, int nlev, double m, DevState* st,
                                                            double* partials, uint32_t n_parts,
                                                            unsigned long long* lvl0_ovf) {
@@ -92,27 +108,31 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
   unsigned long long ur = 0, uw = 0, fp = 0;
   const uint64_t n_chunks = (n_keys + CHUNK - 1) / CHUNK;
 
-  auto load = [&](uint64_t ch, unsigned long long (&c)[K]) {
+  auto load = [&](uint64_t ch, E (&c)[K]) {
     const uint64_t k0 = ch * CHUNK + (uint64_t)t * K;
     if (k0 + K <= n_keys) {
-      const ulonglong2* p = reinterpret_cast<const ulonglong2*>(tab + k0);
+      const uint4* p = reinterpret_cast<const uint4*>(tab + k0);
+      constexpr int V = K * (int)sizeof(E) / 16;
 #pragma unroll
-      for (int q = 0; q < K / 2; ++q) {
-        const ulonglong2 v = __ldcs(p + q);  // streamed once: do not keep in L2
-        c[2 * q] = v.x; c[2 * q + 1] = v.y;
+      for (int q = 0; q < V; ++q) {
+        const uint4 v = __ldcs(p + q);  // streamed once: do not keep in L2
+        *reinterpret_cast<uint4*>(&c[q * (16 / sizeof(E))]) = v;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : 0ull;
+      for (int i = 0; i < K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : (E)0;
     }
   };
 
   // warp-uniform run: run_n chunks of 256 keys, every entry == run_e (warp-uniform registers)
-  unsigned long long run_e = 0, run_n = 0;
+  E run_e = 0;
+  unsigned long long run_n = 0;
   const int fast_lev = nlev < 9 ? nlev : 9;
   auto flush_run = [&]() {
     if (run_n == 0) return;
-    const unsigned long long r = run_e & 0xFFFFFFFFull, w = run_e >> 32, c = r + w;
+    unsigned long long c;
+    uint32_t r, w;
+    decode<E>(run_e, c, r, w);
     const unsigned long long keys = run_n * 256ull;
     if (lane == 0) {
       ur += r ? keys : 0ull; uw += w ? keys : 0ull; fp += keys;
@@ -131,7 +151,7 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
     run_n = 0;
   };
 
-  unsigned long long cur[K], nxt[K];
+  E cur[K], nxt[K];
   uint64_t ch = blockIdx.x;
   if (ch < n_chunks) load(ch, cur);
   for (; ch < n_chunks; ch += gridDim.x) {
@@ -139,20 +159,23 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
     bool same = true;
 #pragma unroll
     for (int i = 1; i < K; ++i) same &= cur[i] == cur[0];
-    const unsigned long long e0 = __shfl_sync(0xffffffffu, cur[0], 0);
+    const E e0 = __shfl_sync(0xffffffffu, cur[0], 0);
     unsigned long long s;  // sum of the warp's 256 counts (levels 9, 10)
     if (__all_sync(0xffffffffu, same && cur[0] == e0)) {
       // ---- warp-uniform chunk: extend the run ----
       if (e0 != run_e) { flush_run(); run_e = e0; }
       if (e0) ++run_n;
-      s = ((e0 & 0xFFFFFFFFull) + (e0 >> 32)) * 256ull;
+      unsigned long long c0;
+      uint32_t r0, w0;
+      decode<E>(e0, c0, r0, w0);
+      s = c0 * 256ull;
     } else {
       unsigned long long c[K];
 #pragma unroll
       for (int i = 0; i < K; ++i) {
-        const unsigned long long r = cur[i] & 0xFFFFFFFFull, w = cur[i] >> 32;
-        ur += r != 0; uw += w != 0; fp += (r | w) != 0;
-        c[i] = r + w;
+        uint32_t r, w;
+        decode<E>(cur[i], c[i], r, w);
+        ur += r; uw += w; fp += c[i] != 0;
       }
       // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
       bool uni = true;
@@ -235,13 +258,22 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const unsigned long l
 
 }  // namespace
 
-void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
+void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
                         double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s) {
   const int nlev = k >= 10 ? 1 : 11 - (int)k;
   const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
-  cudaFuncSetAttribute(dense_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dense_stats_kernel<<<n_ctas, T, smem, s>>>(tab, n_keys, nlev, (double)total_m, st, partials, n_ctas,
-                                             reinterpret_cast<unsigned long long*>(lvl0_ovf));
+  unsigned long long* ovf = reinterpret_cast<unsigned long long*>(lvl0_ovf);
+  if (e32) {
+    cudaFuncSetAttribute(dense_stats_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dense_stats_kernel<uint32_t><<<n_ctas, T, smem, s>>>(static_cast<const uint32_t*>(tab), n_keys, nlev,
+                                                         (double)total_m, st, partials, n_ctas, ovf);
+  } else {
+    cudaFuncSetAttribute(dense_stats_kernel<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dense_stats_kernel<unsigned long long><<<n_ctas, T, smem, s>>>(static_cast<const unsigned long long*>(tab),
+                                                                   n_keys, nlev, (double)total_m, st, partials,
+                                                                   n_ctas, ovf);
+  }
 }
 
 }  // namespace aiwc

@@ -17,10 +17,15 @@
 //          the per-thread class counts gives every thread its exact carry-in
 //          (segment length, work-item, group, output offsets).  Each event
 //          class is then folded by its own converged set-bit loop:
-//          instructions -> lane-private u16 opcode / width bins, memory ->
-//          dense-table RED.ADD (or ordered compaction), rare events in stream
-//          order -> segment closes, branch records, group changes.  Segment
-//          closes are histogrammed after the tile by all threads together.
+//          instructions -> opcode / width bins counted from bit-planes (the
+//          16 payloads' low bytes are packed and transposed like the kinds;
+//          bin v's count is popc of its minterm, no per-event loop), memory ->
+//          a per-warp list of event indices that the warp then folds into the
+//          dense table with coalesced REDs (lane i takes the warp's i-th access,
+//          so one RED instruction covers consecutive keys of streaming traces),
+//          or ordered compaction; rare events in stream order -> segment
+//          closes, branch records, group changes.  Segment closes are
+//          histogrammed after the tile by all threads together.
 #include "aiwc_internal.cuh"
 
 namespace aiwc {
@@ -195,8 +200,9 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
 // ---------------------------------------------------------------------------
 // main ingest pass
 // ---------------------------------------------------------------------------
-constexpr int BND_CAP = 512;  // segment closes buffered per tile (overflow is processed inline)
-constexpr uint32_t PRIV_FLUSH_TILES = 65535 / EPT;  // u16 bins take at most EPT increments per tile
+constexpr int BND_CAP = 256;  // segment closes buffered per tile (overflow is processed inline)
+constexpr uint32_t ACC_FLUSH_TILES = 65535 / EPT;  // 16-bit register counters take <= EPT per tile
+constexpr int NWARP = TPB / 32;
 
 // TMA stages (dynamic smem, 1024 B aligned for the 128 B swizzle)
 struct StageSmem {
@@ -208,13 +214,12 @@ struct StageSmem {
 
 // CTA-private accumulators and per-tile scratch (static smem: direct addressing)
 struct LocalSmem {
-  uint16_t opc[OBINS][TPB];    // lane-private opcode counts (flushed before they can wrap)
-  uint16_t wid[WBINS][TPB];    // lane-private width counts, width 1..16
+  uint16_t midx[NWARP][TILE / NWARP];  // per-warp memory-event list: tile position | write << 15
   uint32_t itb_h[HBINS];
   uint32_t ipt_h[HBINS];
   uint4 closes[BND_CAP];       // (segment length, local id, gseq | barrier << 31 | resumed << 30)
-  unsigned long long wfirst[WBINS];
-  uint4 wtot[TPB / 32];        // per-warp inclusive totals of the packed scan values
+  uint32_t wpres;              // widths 1..16 seen in this CTA's range (bit w - 1)
+  uint4 wtot[NWARP];           // per-warp inclusive totals of the packed scan values
   uint32_t vpos[TPB];
   uint32_t nc[5];
 };
@@ -253,24 +258,32 @@ __device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint
   }
 }
 
-__device__ __forceinline__ void flush_private(LocalSmem& L, const IngestArgs& a, int t) {
-  __syncthreads();
-  if (t < OBINS) {
-    unsigned long long sum = 0;
-    for (int i = 0; i < TPB; ++i) { sum += L.opc[t][i]; L.opc[t][i] = 0; }
-    if (sum) atomicAdd(&a.opc_counts[t], sum);
-  } else if (t >= 32 && t < 32 + WBINS) {
-    const int b = t - 32;
-    unsigned long long sum = 0;
-    for (int i = 0; i < TPB; ++i) { sum += L.wid[b][i]; L.wid[b][i] = 0; }
-    if (sum) atomicAdd(&a.width_count[b + 1], sum);
+// add the per-thread packed bin counters (16-bit fields, bin 2i low / 2i + 1 high)
+// to the global opcode / width counters; warp-converged
+__device__ __forceinline__ void flush_counts(uint32_t (&oacc)[8], uint32_t (&wacc)[8], const IngestArgs& a, int lane,
+                                             uint32_t& pres, unsigned long long& flags) {
+#pragma unroll
+  for (int v = 0; v < 16; ++v) {
+    uint32_t co = (oacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
+    uint32_t cw = (wacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
+    const uint32_t wv = v ? (uint32_t)v : 16u;  // width bin v holds width v, bin 0 width 16
+    if (cw) pres |= 1u << (wv - 1);
+    co = warp_sum(co);
+    cw = warp_sum(cw);
+    if (lane == 0) {
+      if (co) {
+        atomicAdd(&a.opc_counts[v], (unsigned long long)co);
+        if ((uint32_t)v >= a.n_opcodes) flags |= F_BAD_OPCODE;
+      }
+      if (cw) atomicAdd(&a.width_count[wv], (unsigned long long)cw);
+    }
   }
-  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { oacc[i] = 0; wacc[i] = 0; }
 }
 
 __device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
-  const uint32_t row = pos >> 4, j = pos & 15;
-  return pay[row * 16 + ((((j >> 1) ^ (row & 7))) << 1) + (j & 1)];
+  return pay[pos ^ (((pos >> 4) & 7u) << 1)];  // 128 B swizzle: chunk (j >> 1) ^ (row & 7)
 }
 
 template <bool DENSE, bool STAGE>
@@ -292,10 +305,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   DevState* st = a.st;
 
   // ---- prologue: smem init + TMA ring fill ----
-  for (int i = t; i < OBINS * TPB; i += TPB) (&L.opc[0][0])[i] = 0;
-  for (int i = t; i < WBINS * TPB; i += TPB) (&L.wid[0][0])[i] = 0;
   for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
-  if (t < WBINS) L.wfirst[t] = ~0ull;
+  if (t == 0) L.wpres = 0;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     fence_barrier_init();
@@ -360,11 +371,11 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   }
   __syncthreads();
 
-  uint32_t seen_w = 0;  // widths 1..16 already first-indexed by this thread
+  uint32_t oacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // opcode bins 0..15, two 16-bit fields each
+  uint32_t wacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width bins (bin v = width v, bin 0 = 16)
+  uint32_t pres = 0;                                     // widths 1..16 seen by this thread
   unsigned long long itb_sum = 0, ipt_sum = 0, flags = 0, max_site = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
-  uint16_t* const opc_col = &L.opc[0][t];
-  uint16_t* const wid_col = &L.wid[0][t];
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -396,6 +407,12 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       const uint32_t b67 = __byte_perm((uint32_t)(x0 >> 32), (uint32_t)(x1 >> 32), 0x7362);
       ins16 = a01 & 0xFFFFu; rd16 = a01 >> 16; wr16 = a23 & 0xFFFFu; br16 = a23 >> 16;
       bnd16 = b45 & 0xFFFFu; p5 = b45 >> 16; p6 = b67 & 0xFFFFu; p7 = b67 >> 16;
+    }
+    {  // kind bytes outside the columnar alphabet (include/aiwc_b200.h)
+      const uint32_t lo4 = ins16 | rd16 | wr16 | br16, hi3 = bnd16 | p5 | p6;
+      const uint32_t bad = (ins16 & (rd16 | wr16 | br16)) | (rd16 & (wr16 | br16)) | (wr16 & br16) | (lo4 & hi3) |
+                           (p7 & (ins16 | br16)) | (p7 & ~(rd16 | wr16 | hi3)) | (p6 & (bnd16 | p5));
+      if (bad) flags |= F_BAD_KIND;
     }
     const uint32_t close16 = bnd16 & ~p5;          // barrier / wi_end
     const uint32_t wgb16 = p6 & ~p7;               // wg_begin
@@ -460,76 +477,113 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     uint32_t o_br = (DENSE ? 0u : T_rd + T_wr) + ex_br;
     uint32_t o_cl = Cex >> 16;
     // ---- fold my 16 events, one converged loop per event class ----
+    // 128 B swizzle: event j of row r sits at u64 index 16 r + (j ^ ((r & 7) << 1))
     const uint64_t* prow = &S.pay[s][t * 16];
-    const uint32_t sw = t & 7;
-#define PAY(j) prow[((((uint32_t)(j) >> 1) ^ sw) << 1) | ((uint32_t)(j) & 1u)]
-    // instructions: opcode / width histograms in lane-private bins
-    uint32_t slow16 = 0, tseen = 0;
-    for (uint32_t m = ins16; m;) {  // two events per iteration for ILP
-      const uint32_t j0 = __ffs(m) - 1;
-      m &= m - 1;
-      const uint32_t j1 = m ? __ffs(m) - 1 : j0;
-      const bool two = m != 0;
-      m &= m - 1;
-      const uint64_t p0 = PAY(j0), p1 = PAY(j1);
-      const uint32_t o0 = (uint32_t)(p0 >> 32), b0 = (uint32_t)p0 - 1u;
-      const uint32_t o1 = (uint32_t)(p1 >> 32), b1 = (uint32_t)p1 - 1u;
-      const bool f0 = (o0 < (uint32_t)OBINS) & (b0 < (uint32_t)WBINS);
-      const bool f1 = two & (o1 < (uint32_t)OBINS) & (b1 < (uint32_t)WBINS);
-      if (f0) { ++opc_col[o0 * TPB]; ++wid_col[b0 * TPB]; }
-      if (f1) { ++opc_col[o1 * TPB]; ++wid_col[b1 * TPB]; }
-      tseen |= (f0 ? 1u << b0 : 0u) | (f1 ? 1u << b1 : 0u);
-      slow16 |= (f0 ? 0u : 1u << j0) | ((two & !f1) ? 1u << j1 : 0u);
-    }
-    if (__any_sync(0xffffffffu, (slow16 | (tseen & ~seen_w)) != 0)) {
-      for (uint32_t fresh = tseen & ~seen_w; fresh; fresh &= fresh - 1) {  // first sight of a width
-        const uint32_t wb = __ffs(fresh) - 1;
-        for (uint32_t m = ins16 & ~slow16; m; m &= m - 1) {
-          const uint32_t j = __ffs(m) - 1;
-          if ((uint32_t)PAY(j) - 1u == wb) { atomicMin(&L.wfirst[wb], (unsigned long long)(e0 + j)); break; }
-        }
+    const uint32_t sw = t & 7, sw2 = sw << 1;
+#define PAY(j) prow[(uint32_t)(j) ^ sw2]
+    // instructions: opcode / width bins from bit-planes.  The fast bins take
+    // opcode < 16 and width 1..16; the low nibbles of those bytes are
+    // transposed into 4 planes each and bin v counts popc(minterm_v & fast).
+    uint32_t bad = 0;  // events outside the fast bins (meaningful for instructions only)
+    uint32_t op[4], wp[4];
+    {
+      const uint4* prow4 = reinterpret_cast<const uint4*>(prow);
+      uint32_t lo2[8], hi2[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // chunk c = events 2c, 2c + 1
+        const uint4 v = prow4[c ^ sw];
+        if ((v.y | (v.x - 1u)) > 15u) bad |= 1u << (2 * c);
+        if ((v.w | (v.z - 1u)) > 15u) bad |= 2u << (2 * c);
+        lo2[c] = __byte_perm(v.x, v.z, 0x0040);  // width bytes of events 2c, 2c + 1
+        hi2[c] = __byte_perm(v.y, v.w, 0x0040);  // opcode bytes
       }
-      seen_w |= tseen;
-      for (uint32_t m = slow16; m; m &= m - 1) {
+      uint32_t lw4[4], hw4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        lw4[q] = __byte_perm(lo2[2 * q], lo2[2 * q + 1], 0x5410);
+        hw4[q] = __byte_perm(hi2[2 * q], hi2[2 * q + 1], 0x5410);
+      }
+      const uint64_t o0 = transpose8((uint64_t)hw4[0] | ((uint64_t)hw4[1] << 32));
+      const uint64_t o1 = transpose8((uint64_t)hw4[2] | ((uint64_t)hw4[3] << 32));
+      const uint64_t x0 = transpose8((uint64_t)lw4[0] | ((uint64_t)lw4[1] << 32));
+      const uint64_t x1 = transpose8((uint64_t)lw4[2] | ((uint64_t)lw4[3] << 32));
+      const uint32_t o01 = __byte_perm((uint32_t)o0, (uint32_t)o1, 0x5140), o23 = __byte_perm((uint32_t)o0, (uint32_t)o1, 0x7362);
+      const uint32_t w01 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x5140), w23 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x7362);
+      op[0] = o01 & 0xFFFFu; op[1] = o01 >> 16; op[2] = o23 & 0xFFFFu; op[3] = o23 >> 16;
+      wp[0] = w01 & 0xFFFFu; wp[1] = w01 >> 16; wp[2] = w23 & 0xFFFFu; wp[3] = w23 >> 16;
+    }
+    {
+      const uint32_t fast = ins16 & ~bad;
+      uint32_t q[4], r[4];
+      q[0] = fast & ~op[0] & ~op[1]; q[1] = fast & op[0] & ~op[1]; q[2] = fast & ~op[0] & op[1]; q[3] = fast & op[0] & op[1];
+      r[0] = ~op[2] & ~op[3]; r[1] = op[2] & ~op[3]; r[2] = ~op[2] & op[3]; r[3] = op[2] & op[3];
+#pragma unroll
+      for (int v = 0; v < 16; v += 2)
+        oacc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
+      q[0] = fast & ~wp[0] & ~wp[1]; q[1] = fast & wp[0] & ~wp[1]; q[2] = fast & ~wp[0] & wp[1]; q[3] = fast & wp[0] & wp[1];
+      r[0] = ~wp[2] & ~wp[3]; r[1] = wp[2] & ~wp[3]; r[2] = ~wp[2] & wp[3]; r[3] = wp[2] & wp[3];
+#pragma unroll
+      for (int v = 0; v < 16; v += 2)
+        wacc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
+    }
+    // the rest one by one: opcodes >= 16, widths outside 1..16
+    for (uint32_t m = ins16 & bad; m; m &= m - 1) {
+      const uint32_t j = __ffs(m) - 1;
+      const uint64_t p = PAY(j);
+      const uint32_t opc = (uint32_t)(p >> 32), wd = (uint32_t)p;
+      if (opc < a.n_opcodes) atomicAdd(&a.opc_counts[opc], 1ull);
+      else flags |= F_BAD_OPCODE;
+      if (wd < WIDTH_TABLE) {
+        atomicAdd(&a.width_count[wd], 1ull);
+        if (wd - 1u < (uint32_t)WBINS) pres |= 1u << (wd - 1);  // first index found after the pass
+        else { atomicMin(&a.width_first[wd], (unsigned long long)(e0 + j)); atomicMax(&a.st->max_width, (unsigned long long)wd); }
+      } else {
+        flags |= F_BAD_WIDTH;
+      }
+    }
+    // memory accesses: dense-table counters (warp-coalesced) or ordered compaction
+    if (DENSE && !(a.dbg_skip & 2)) {
+      // my accesses go to the warp's list (pre-swizzled smem index | write << 15)
+      // at my in-warp exclusive offset ...
+      const uint32_t bx = Bi - B;
+      uint32_t slot = (bx & 0xFFFFu) + (bx >> 16);
+      uint16_t* const midx = L.midx[warp];
+      const uint32_t rowb = 16u * t;
+      for (uint32_t m = rd16 | wr16; m; m &= m - 1) {
         const uint32_t j = __ffs(m) - 1;
-        const uint64_t p = PAY(j);
-        const uint32_t opc = (uint32_t)(p >> 32), wd = (uint32_t)p;
-        if (opc < OBINS) ++opc_col[opc * TPB];
-        else if (opc < a.n_opcodes) atomicAdd(&a.opc_counts[opc], 1ull);
-        else flags |= F_BAD_OPCODE;
-        if (wd - 1u < (uint32_t)WBINS) {
-          ++wid_col[(wd - 1) * TPB];
-          if (!((seen_w >> (wd - 1)) & 1u)) {
-            seen_w |= 1u << (wd - 1);
-            atomicMin(&L.wfirst[wd - 1], (unsigned long long)(e0 + j));
+        midx[slot++] = (uint16_t)((rowb | (j ^ sw2)) | (((wr16 >> j) & 1u) << 15));
+      }
+      __syncwarp();
+      // ... and lane i folds accesses i, i + 32, ... of the warp in stream order
+      const uint32_t wt = L.wtot[warp].y, n_mem = (wt & 0xFFFFu) + (wt >> 16);
+      const uint64_t* const pay = S.pay[s];
+      const uint64_t base = a.am.base, off_max = a.am.off_max;
+      const uint32_t k = a.am.k, lmask = (uint32_t)a.am.low_mask, lconst = (uint32_t)a.am.low_const;
+      uint32_t inval = 0;
+      if (a.dense32) {
+        uint32_t* const tab = static_cast<uint32_t*>(a.dense);
+        for (uint32_t i = lane; i < n_mem; i += 32) {
+          const uint32_t e = midx[i];
+          const uint64_t off = pay[e & 0x0FFFu] - base;
+          const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
+          inval |= !v;
+          if (v) {
+            uint32_t* const q = tab + (off >> k);
+            atomicAdd(q, 1u);
+            atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
           }
-        } else if (wd < WIDTH_TABLE) {
-          atomicAdd(&a.width_count[wd], 1ull);
-          atomicMin(&a.width_first[wd], (unsigned long long)(e0 + j));
-        } else {
-          flags |= F_BAD_WIDTH;
+        }
+      } else {
+        unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
+        for (uint32_t i = lane; i < n_mem; i += 32) {
+          const uint32_t e = midx[i];
+          const uint64_t off = pay[e & 0x0FFFu] - base;
+          const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
+          inval |= !v;
+          if (v) atomicAdd(tab + (off >> k), (e & 0x8000u) ? (1ull << 32) : 1ull);
         }
       }
-    }
-    // memory accesses: dense-table counters or compaction
-    if (DENSE) {
-      for (uint32_t m = rd16 | wr16; m;) {  // two events per iteration for ILP
-        const uint32_t j0 = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t j1 = m ? __ffs(m) - 1 : j0;
-        const bool two = m != 0;
-        m &= m - 1;
-        const uint64_t p0 = PAY(j0), p1 = PAY(j1);
-        const uint64_t off0 = p0 - a.am.base, off1 = p1 - a.am.base;
-        const uint64_t key0 = off0 >> a.am.k, key1 = off1 >> a.am.k;
-        const bool v0 = (p0 >= a.am.base) & (((uint32_t)off0 & (uint32_t)a.am.low_mask) == (uint32_t)a.am.low_const) &
-                        (key0 < a.am.n_keys);
-        const bool v1 = (p1 >= a.am.base) & (((uint32_t)off1 & (uint32_t)a.am.low_mask) == (uint32_t)a.am.low_const) &
-                        (key1 < a.am.n_keys);
-        if (v0) atomicAdd(&a.dense[key0], ((wr16 >> j0) & 1u) ? (1ull << 32) : 1ull);
-        if (two & v1) atomicAdd(&a.dense[key1], ((wr16 >> j1) & 1u) ? (1ull << 32) : 1ull);
-        flags |= (v0 & (v1 | !two)) ? 0ull : (unsigned long long)F_ADDR_HINT;
-      }
+      if (inval) flags |= F_ADDR_HINT;
     }
     for (uint32_t m = DENSE ? 0u : (rd16 | wr16); m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
@@ -560,7 +614,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
-    for (uint32_t m = rare16; m; m &= m - 1) {
+    for (uint32_t m = (a.dbg_skip & 4) ? 0u : rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t k = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
@@ -614,12 +668,15 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         tma_load_2d(S.pay[s], &pmap, 0, (int)r2, &S.bar[s]);
       }
     }
-    if ((it + 1) % PRIV_FLUSH_TILES == 0) flush_private(L, a, t);
+    if ((it + 1) % ACC_FLUSH_TILES == 0) flush_counts(oacc, wacc, a, lane, pres, flags);
   }
 
   // ---- epilogue: flush CTA-private state ----
-  flush_private(L, a, t);
-  if (t >= 32 && t < 32 + WBINS && L.wfirst[t - 32] != ~0ull) atomicMin(&a.width_first[t - 32 + 1], L.wfirst[t - 32]);
+  flush_counts(oacc, wacc, a, lane, pres, flags);
+  pres = __reduce_or_sync(0xffffffffu, pres);
+  if (lane == 0 && pres) atomicOr(&L.wpres, pres);
+  __syncthreads();
+  if (t == 0 && L.wpres) a.width_presence[blockIdx.x] = L.wpres;
   for (int i = t; i < HBINS; i += TPB) {
     if (L.itb_h[i]) atomicAdd(&st->itb_hist[i], (unsigned long long)L.itb_h[i]);
     if (L.ipt_h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)L.ipt_h[i]);

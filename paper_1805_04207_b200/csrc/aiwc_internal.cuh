@@ -23,6 +23,10 @@ constexpr int NLEVELS = 11;           // address entropy at LSB-skip 0..10
 constexpr uint32_t WIDTH_TABLE = 65536;
 constexpr int MAX_SMALL_LIST = 256;   // widths / sites returned inline in DevState
 constexpr uint64_t IPT_END_FLAG = 1ull << 63;
+// dense-table entries: u32 = access count (bits 0..29) | read seen (bit 30) | write seen (bit 31)
+// when the trace has fewer than 2^30 accesses, else u64 = reads | writes << 32
+constexpr uint32_t E32_COUNT = 0x3FFFFFFFu, E32_READ = 1u << 30, E32_WRITE = 1u << 31;
+constexpr uint64_t E32_MAX_ACCESSES = 1ull << 30;
 
 // ---- kind-byte classes (include/aiwc_b200.h) -------------------------------
 __host__ __device__ constexpr bool is_instr(uint32_t k) { return k & 0x01; }
@@ -72,6 +76,7 @@ struct AddrMap {
   uint64_t low_const;  // (addr - base) & low_mask for every address
   uint32_t k;          // constant low bits dropped from keys
   uint64_t n_keys;     // dense table length
+  uint64_t off_max;    // largest valid addr - base: ((n_keys - 1) << k) | low_mask
 };
 
 struct IngestArgs {
@@ -86,17 +91,20 @@ struct IngestArgs {
   DevState* st;
   unsigned long long* opc_counts;   // [n_opcodes]
   unsigned long long* width_count;  // [WIDTH_TABLE]
-  unsigned long long* width_first;  // [WIDTH_TABLE]
+  unsigned long long* width_first;  // [WIDTH_TABLE] (widths > 16; 1..16 found by width_first_kernel)
+  uint32_t* width_presence;         // [n_ranges]: widths 1..16 present in the range (bit w - 1)
   uint32_t* itb_ovf;                // [n_bar + n_wie]
   uint32_t* ipt_ovf;                // [n_wie]
   unsigned long long* ipt_tab;      // [n_wgb * local_volume] or null
   uint64_t ipt_tab_len;
   // memory
   AddrMap am;
-  unsigned long long* dense;        // dense mode: [am.n_keys] packed r | w << 32
+  void* dense;                      // dense mode: [am.n_keys] u32 (dense32) or u64 entries
+  uint32_t dense32;
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
+  uint32_t dbg_skip;                // EXPERIMENT: bit0 instr, bit1 memory, bit2 rare
 };
 
 // ---- small device helpers ----------------------------------------------------
@@ -161,12 +169,12 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
                           bool dense, bool stage, cudaStream_t s);
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
+void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
+                        uint32_t n_ranges, uint64_t range_len, unsigned long long* width_first, cudaStream_t s);
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);
-void launch_dense_stats(const unsigned long long* tab, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
+void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
                         double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s);
-void launch_fill_dense(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr, AddrMap am,
-                       unsigned long long* dense, cudaStream_t s);
 void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_parts, uint64_t total_m, uint32_t k,
                            cudaStream_t s);
 // sparse memory path; returns kernel count

@@ -250,13 +250,55 @@ void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st,
 // ---------------------------------------------------------------------------
 // width Counter in first-appearance order (metrics.py:136, :298-306)
 // ---------------------------------------------------------------------------
+// First event index of each width 1..16 counted by the ingest's bit-plane
+// bins: CTA w - 1 scans only the first ingest range whose presence mask has
+// width w, tile by tile in stream order, and stops at the first hit.
+__global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restrict__ kind,
+                                                          const uint64_t* __restrict__ payload, uint64_t n,
+                                                          const uint32_t* __restrict__ presence, uint32_t n_ranges,
+                                                          uint64_t range_len, unsigned long long* width_first) {
+  const uint32_t w = blockIdx.x + 1;
+  __shared__ int s_r;
+  __shared__ unsigned long long s_pos;
+  if (threadIdx.x == 0) {
+    int r0 = -1;
+    for (uint32_t r = 0; r < n_ranges; ++r)
+      if ((presence[r] >> (w - 1)) & 1u) { r0 = (int)r; break; }
+    s_r = r0;
+    s_pos = ~0ull;
+  }
+  __syncthreads();
+  if (s_r < 0) return;
+  const uint64_t lo = (uint64_t)s_r * range_len, hi = min(n, lo + range_len);
+  for (uint64_t base = lo; base < hi; base += 256 * 16) {
+#pragma unroll 4
+    for (int j = 0; j < 16; ++j) {
+      const uint64_t e = base + (uint64_t)j * 256 + threadIdx.x;
+      if (e < hi && kind[e] == AIWC_K_INSTR && (uint32_t)payload[e] == w) {
+        atomicMin(&s_pos, (unsigned long long)e);
+        break;
+      }
+    }
+    __syncthreads();
+    if (s_pos != ~0ull) break;
+  }
+  if (threadIdx.x == 0 && s_pos != ~0ull) atomicMin(&width_first[w], s_pos);
+}
+
+void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
+                        uint32_t n_ranges, uint64_t range_len, unsigned long long* width_first, cudaStream_t s) {
+  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ranges, range_len, width_first);
+}
+
 __global__ void width_list_kernel(const unsigned long long* __restrict__ count,
                                   const unsigned long long* __restrict__ first, DevState* st) {
   __shared__ unsigned long long lv[MAX_SMALL_LIST], lc[MAX_SMALL_LIST], lf[MAX_SMALL_LIST];
   __shared__ unsigned int n;
   if (threadIdx.x == 0) n = 0;
   __syncthreads();
-  for (uint32_t w = threadIdx.x; w < WIDTH_TABLE; w += blockDim.x) {
+  // widths 1..16 plus whatever the slow path saw (width 0 or > 16)
+  const uint32_t lim = (uint32_t)min((unsigned long long)WIDTH_TABLE, max(17ull, st->max_width + 1));
+  for (uint32_t w = threadIdx.x; w < lim; w += blockDim.x) {
     const unsigned long long c = count[w];
     if (c) {
       const unsigned int i = atomicAdd(&n, 1u);
