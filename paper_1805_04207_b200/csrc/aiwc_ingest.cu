@@ -234,6 +234,23 @@ __device__ __forceinline__ uint64_t transpose8(uint64_t x) {
   return x;
 }
 
+// Bit-planes 0..3 of the low nibbles of 16 bytes (b[q] = bytes of events
+// 4q..4q+3).  Packing bytes q and q + 1 as nibbles puts event e + 4h, bit c
+// at index [e1 e0 h c1 c0]; swapping index bits 4<->1 and 3<->0 (two delta
+// swaps) gives index [c1 c0 h e1 e0] = byte c holds plane c of 8 events.
+// Returns planes 0 | 1 << 16; planes 2 | 3 << 16 in p23.
+__device__ __forceinline__ uint32_t nibble_planes(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3, uint32_t& p23) {
+  uint32_t x = (b0 & 0x0F0F0F0Fu) | ((b1 & 0x0F0F0F0Fu) << 4);  // events 0..7
+  uint32_t y = (b2 & 0x0F0F0F0Fu) | ((b3 & 0x0F0F0F0Fu) << 4);  // events 8..15
+  uint32_t t;
+  t = (x ^ (x >> 14)) & 0x0000CCCCu; x ^= t ^ (t << 14);
+  t = (x ^ (x >> 7)) & 0x00AA00AAu; x ^= t ^ (t << 7);
+  t = (y ^ (y >> 14)) & 0x0000CCCCu; y ^= t ^ (t << 14);
+  t = (y ^ (y >> 7)) & 0x00AA00AAu; y ^= t ^ (t << 7);
+  p23 = __byte_perm(x, y, 0x7362);
+  return __byte_perm(x, y, 0x5140);
+}
+
 // One segment close (metrics.py:156-174): ITB sample (barrier always, wi_end when
 // non-empty); IPT either straight to the histogram (work-item never crossed a
 // barrier) or accumulated in the work-item's lifetime slot.
@@ -503,12 +520,9 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         lw4[q] = __byte_perm(lo2[2 * q], lo2[2 * q + 1], 0x5410);
         hw4[q] = __byte_perm(hi2[2 * q], hi2[2 * q + 1], 0x5410);
       }
-      const uint64_t o0 = transpose8((uint64_t)hw4[0] | ((uint64_t)hw4[1] << 32));
-      const uint64_t o1 = transpose8((uint64_t)hw4[2] | ((uint64_t)hw4[3] << 32));
-      const uint64_t x0 = transpose8((uint64_t)lw4[0] | ((uint64_t)lw4[1] << 32));
-      const uint64_t x1 = transpose8((uint64_t)lw4[2] | ((uint64_t)lw4[3] << 32));
-      const uint32_t o01 = __byte_perm((uint32_t)o0, (uint32_t)o1, 0x5140), o23 = __byte_perm((uint32_t)o0, (uint32_t)o1, 0x7362);
-      const uint32_t w01 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x5140), w23 = __byte_perm((uint32_t)x0, (uint32_t)x1, 0x7362);
+      uint32_t o23, w23;
+      const uint32_t o01 = nibble_planes(hw4[0], hw4[1], hw4[2], hw4[3], o23);
+      const uint32_t w01 = nibble_planes(lw4[0], lw4[1], lw4[2], lw4[3], w23);
       op[0] = o01 & 0xFFFFu; op[1] = o01 >> 16; op[2] = o23 & 0xFFFFu; op[3] = o23 >> 16;
       wp[0] = w01 & 0xFFFFu; wp[1] = w01 >> 16; wp[2] = w23 & 0xFFFFu; wp[3] = w23 >> 16;
     }
