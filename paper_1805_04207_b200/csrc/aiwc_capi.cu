@@ -74,11 +74,9 @@ struct aiwc_ctx {
   Buf dev_state, ranges, opc, wcount, wfirst, wpres, itb_ovf, ipt_ovf, ipt_tab, dtab, rd, wr, br, partials, lvl0_ovf,
       sparse_scr, branch_scr, branch_tab, kind_stage, pay_stage, sort_a, sort_b, sort_h;
   DevState* h_state = nullptr;  // pinned
-  RangeSum* h_ranges = nullptr; // pinned
-  size_t h_ranges_cap = 0;
   // per trace
   aiwc_trace_info info{};
-  uint64_t n_instr = 0, n_rd = 0, n_wr = 0, n_br = 0, n_wgb = 0, n_wib = 0, n_bres = 0, n_bnd = 0, n_bar = 0;
+  uint64_t n_instr = 0, n_rd = 0, n_wr = 0, n_br = 0, n_wgb = 0, n_bres = 0;
   uint64_t n_events_seen = 0;
   AddrMap am{};
   bool dense = false;
@@ -178,7 +176,6 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
-  if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
@@ -260,11 +257,6 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
   CK(grow(ctx->wpres, (size_t)G * sizeof(uint32_t)));
   CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * sizeof(uint32_t), s));
-  if (ctx->h_ranges_cap < n_sub) {
-    if (ctx->h_ranges) cudaFreeHost(ctx->h_ranges);
-    CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ranges), (size_t)n_sub * sizeof(RangeSum)));
-    ctx->h_ranges_cap = n_sub;
-  }
   const bool with_stats = !info->has_addr_stats;
   // Declared address statistics fix the key map before pass 1: clear a u32
   // table of that size on the side stream meanwhile.  Bounded waste when the
@@ -293,19 +285,15 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   } else {
     CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_sub * sizeof(RangeSum), s));
   }
-  CK(cudaMemcpyAsync(ctx->h_ranges, ctx->ranges.p, (size_t)n_sub * sizeof(RangeSum), cudaMemcpyDeviceToHost, s));
-  ctx->d2h += (size_t)n_sub * sizeof(RangeSum);
-  if (with_stats) {  // addr_min .. addr_or are contiguous
-    CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 4 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, s));
-    ctx->d2h += 4 * sizeof(unsigned long long);
-  }
+  // addr_min .. addr_or and the pass-1 totals are contiguous: one 80-byte read
+  CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     s));
+  ctx->d2h += 10 * sizeof(unsigned long long);
   CK(cudaStreamSynchronize(s));
-  ctx->n_instr = ctx->n_rd = ctx->n_wr = ctx->n_br = ctx->n_wgb = ctx->n_wib = ctx->n_bres = ctx->n_bnd = ctx->n_bar = 0;
-  for (uint32_t i = 0; i < (n ? n_sub : 0); ++i) {
-    const RangeSum& r = ctx->h_ranges[i];
-    ctx->n_instr += r.n_instr; ctx->n_rd += r.n_rd; ctx->n_wr += r.n_wr; ctx->n_br += r.n_br;
-    ctx->n_wgb += r.n_wgb; ctx->n_wib += r.n_wib; ctx->n_bres += r.n_bres; ctx->n_bnd += r.n_bnd; ctx->n_bar += r.n_bar;
+  {
+    const unsigned long long* tt = ctx->h_state->p1_tot;
+    ctx->n_instr = tt[0]; ctx->n_rd = tt[1]; ctx->n_wr = tt[2]; ctx->n_br = tt[3]; ctx->n_wgb = tt[4];
+    ctx->n_bres = tt[5];
   }
   ctx->n_events_seen = n;
 
@@ -345,9 +333,9 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   }
 
   // ---- buffers ----
-  // ITB / IPT samples are closed by boundaries: n_bnd bounds both overflow lists
-  CK(grow(ctx->itb_ovf, std::max<uint64_t>(ctx->n_bnd, 1) * 4));
-  CK(grow(ctx->ipt_ovf, std::max<uint64_t>(ctx->n_bnd, 1) * 4));
+  // an ITB / IPT sample >= HBINS spans >= HBINS distinct instructions: that bounds both overflow lists
+  CK(grow(ctx->itb_ovf, (ctx->n_instr / HBINS + 2) * 4));
+  CK(grow(ctx->ipt_ovf, (ctx->n_instr / HBINS + 2) * 4));
   ctx->ipt_tab_len = 0;
   if (ctx->n_bres) {
     ctx->ipt_tab_len = ctx->n_wgb * (uint64_t)std::max<uint32_t>(info->local_volume, 1);
@@ -597,8 +585,8 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   aiwc_result r{};
   r.n_events = ctx->n_events_seen;
   r.total_instructions = ctx->n_instr;
-  r.work_items = ctx->n_wib;
-  r.barriers_hit = ctx->n_bar;
+  r.work_items = h.n_wib;
+  r.barriers_hit = h.n_bar;
   {
     std::vector<uint64_t> oc;
     for (uint64_t c : ctx->opc_counts) if (c) oc.push_back(c);

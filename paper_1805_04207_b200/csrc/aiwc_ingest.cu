@@ -59,7 +59,7 @@ __device__ __forceinline__ uint32_t m_wgb(uint32_t w) { return w & ~(w >> 1) & 0
 // (instr, read, write, branch) of two words, H bits 4..7 (boundary, open,
 // group, variant); each class is then one masked popcount per packed word.
 struct KindCounts {
-  uint32_t instr = 0, rd = 0, wr = 0, br = 0, bnd = 0, wgb = 0, bres = 0, wib = 0, bar = 0;
+  uint32_t instr = 0, rd = 0, wr = 0, br = 0, wgb = 0, bres = 0;
   __device__ __forceinline__ void add(const uint32_t w[4]) {
     const uint32_t L0 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
     const uint32_t L1 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
@@ -69,11 +69,8 @@ struct KindCounts {
     rd += __popc(L0 & 0x22222222u) + __popc(L1 & 0x22222222u);
     wr += __popc(L0 & 0x44444444u) + __popc(L1 & 0x44444444u);
     br += __popc(L0 & 0x88888888u) + __popc(L1 & 0x88888888u);
-    bnd += __popc(H0 & 0x11111111u) + __popc(H1 & 0x11111111u);
     wgb += __popc(H0 & ~(H0 >> 1) & 0x44444444u) + __popc(H1 & ~(H1 >> 1) & 0x44444444u);
-    bres += __popc(H0 & (H0 >> 3) & 0x11111111u) + __popc(H1 & (H1 >> 3) & 0x11111111u);
-    wib += __popc(H0 & (H0 >> 1) & ~(H0 >> 3) & 0x11111111u) + __popc(H1 & (H1 >> 1) & ~(H1 >> 3) & 0x11111111u);
-    bar += __popc(H0 & ~(H0 >> 1) & (H0 >> 3) & 0x11111111u) + __popc(H1 & ~(H1 >> 1) & (H1 >> 3) & 0x11111111u);
+    bres |= (H0 & (H0 >> 3)) | (H1 & (H1 >> 3));  // boundary with the variant bit: barrier / resume
   }
 };
 
@@ -118,14 +115,14 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   }
   // block reduction
   constexpr int NW = P1_THREADS / 32;
-  __shared__ uint32_t s_cnt[NW][9];
+  __shared__ uint32_t s_cnt[NW][6];
   __shared__ long long s_pos[NW][2];
   __shared__ unsigned long long s_addr[NW][4];
   __shared__ long long s_lb;
-  uint32_t v[9] = {kc.instr, kc.rd, kc.wr, kc.br, kc.bnd, kc.wgb, kc.bres, kc.wib, kc.bar};
+  uint32_t v[6] = {kc.instr, kc.rd, kc.wr, kc.br, kc.wgb, __reduce_or_sync(0xffffffffu, kc.bres & 0x11111111u) ? 1u : 0u};
   const int lane = t & 31, warp = t >> 5;
 #pragma unroll
-  for (int i = 0; i < 9; ++i) v[i] = warp_sum(v[i]);
+  for (int i = 0; i < 5; ++i) v[i] = warp_sum(v[i]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     last_bnd = max(last_bnd, __shfl_xor_sync(0xffffffffu, last_bnd, o));
@@ -139,26 +136,32 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   }
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < 9; ++i) s_cnt[warp][i] = v[i];
+    for (int i = 0; i < 6; ++i) s_cnt[warp][i] = v[i];
     s_pos[warp][0] = last_bnd; s_pos[warp][1] = last_wgb;
     s_addr[warp][0] = amin; s_addr[warp][1] = amax; s_addr[warp][2] = aand; s_addr[warp][3] = aor;
   }
   __syncthreads();
   if (t == 0) {
     RangeSum r{};
-    uint32_t tot[9] = {0};
+    uint32_t tot[6] = {0};
     long long lb = -1, lw = -1;
     unsigned long long mn = ~0ull, mx = 0, an = ~0ull, o = 0;
     for (int w = 0; w < NW; ++w) {
-      for (int i = 0; i < 9; ++i) tot[i] += s_cnt[w][i];
+      for (int i = 0; i < 6; ++i) tot[i] += s_cnt[w][i];
       lb = max(lb, s_pos[w][0]); lw = max(lw, s_pos[w][1]);
       mn = min(mn, s_addr[w][0]); mx = max(mx, s_addr[w][1]); an &= s_addr[w][2]; o |= s_addr[w][3];
     }
-    r.n_instr = tot[0]; r.n_rd = tot[1]; r.n_wr = tot[2]; r.n_br = tot[3]; r.n_bnd = tot[4];
-    r.n_wgb = tot[5]; r.n_bres = tot[6]; r.n_wib = tot[7]; r.n_bar = tot[8];
+    r.n_instr = tot[0]; r.n_rd = tot[1]; r.n_wr = tot[2]; r.n_br = tot[3];
+    r.n_wgb = tot[4]; r.any_bres = tot[5] ? 1u : 0u;
     r.last_bnd = lb; r.last_wgb = lw;
     out[blockIdx.x] = r;
     s_lb = lb;
+    atomicAdd(&st->p1_tot[0], (unsigned long long)tot[0]);
+    atomicAdd(&st->p1_tot[1], (unsigned long long)tot[1]);
+    atomicAdd(&st->p1_tot[2], (unsigned long long)tot[2]);
+    if (tot[3]) atomicAdd(&st->p1_tot[3], (unsigned long long)tot[3]);
+    if (tot[4]) atomicAdd(&st->p1_tot[4], (unsigned long long)tot[4]);
+    if (tot[5]) atomicAdd(&st->p1_tot[5], 1ull);
     if (with_stats && tot[1] + tot[2] > 0) {
       atomicMin(&st->addr_min, mn); atomicMax(&st->addr_max, mx);
       atomicAnd(&st->addr_and, an); atomicOr(&st->addr_or, o);
@@ -393,6 +396,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   uint32_t pres = 0;                                     // widths 1..16 seen by this thread
   unsigned long long itb_sum = 0, ipt_sum = 0, flags = 0, max_site = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
+  uint32_t n_wib = 0, n_bar = 0;  // WI_BEGIN / BARRIER events (metrics.py: work_items, barriers_hit)
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -431,6 +435,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
                            (p7 & (ins16 | br16)) | (p7 & ~(rd16 | wr16 | hi3)) | (p6 & (bnd16 | p5));
       if (bad) flags |= F_BAD_KIND;
     }
+    n_wib += __popc(bnd16 & p5 & ~p7);
+    n_bar += __popc(bnd16 & ~p5 & p7);
     const uint32_t close16 = bnd16 & ~p5;          // barrier / wi_end
     const uint32_t wgb16 = p6 & ~p7;               // wg_begin
     const uint32_t rare16 = bnd16 | p5 | p6;       // boundary, group, kernel events
@@ -697,6 +703,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   }
   itb_sum = warp_sum(itb_sum);
   ipt_sum = warp_sum(ipt_sum);
+  n_wib = warp_sum(n_wib);
+  n_bar = warp_sum(n_bar);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     flags |= __shfl_xor_sync(0xffffffffu, flags, o);
@@ -710,6 +718,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   }
   if (lane == 0) {
     if (itb_sum) atomicAdd(&st->itb_sum, itb_sum);
+    if (n_wib) atomicAdd(&st->n_wib, (unsigned long long)n_wib);
+    if (n_bar) atomicAdd(&st->n_bar, (unsigned long long)n_bar);
     if (ipt_sum) atomicAdd(&st->ipt_sum, ipt_sum);
     if (flags) atomicOr(&st->flags, flags);
     if (max_site) atomicMax(&st->max_site, max_site);

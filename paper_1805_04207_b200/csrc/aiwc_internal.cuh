@@ -38,10 +38,12 @@ enum : uint64_t {
   F_SLOT_RANGE = 32, F_BAD_KIND = 64
 };
 
-// Per-range summary computed from kind bytes alone (pass 1).
+// Per-range summary computed from kind bytes alone (pass 1): what the ingest
+// carry-in and the host's buffer sizing need.  Work-items and barriers are
+// counted by the ingest itself.
 struct RangeSum {
   uint32_t n_instr, n_rd, n_wr, n_br, n_wgb, instr_after;
-  uint32_t n_wib, n_bres, n_bnd, n_bar, pad0, pad1;  // bres = barriers + resumes, bnd = all boundaries
+  uint32_t any_bres, pad;       // a barrier or resume occurs (work-item lifetime slots needed)
   int64_t last_bnd, last_wgb;   // global event index, -1 when absent
 };
 
@@ -54,7 +56,9 @@ struct DevState {
   unsigned long long unique_r, unique_w, footprint;
   unsigned long long flags, max_site, max_width;
   unsigned long long addr_min, addr_max, addr_and, addr_or;
+  unsigned long long p1_tot[6];                    // pass-1 totals: instr, rd, wr, br, wgb, ranges with bres
   unsigned long long n_obs, n_sites, n_uniq;      // branch observations, #sites, #unique keys (sparse)
+  unsigned long long n_wib, n_bar;                 // work-items begun, barriers hit (ingest)
   unsigned long long n_widths_listed, n_sites_listed;
   double entropy[NLEVELS];
   double yokota, linear;

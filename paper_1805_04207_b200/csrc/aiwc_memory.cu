@@ -175,35 +175,32 @@ int sparse_memory_stats(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, u
 // ---------------------------------------------------------------------------
 constexpr int EF_T = 1024;
 
+// one CTA per level j: -(sum over the count-of-counts histogram and the big-count
+// partials); report level n (0..10) reads level j(n) = raw ? n : max(0, n - k)
 __global__ void __launch_bounds__(EF_T) entropy_finish_kernel(DevState* st, const double* partials,
                                                               uint32_t n_parts, double m, int nlev, int k,
                                                               int raw_levels) {
   __shared__ double red[EF_T / 32];
-  __shared__ double lev[NLEVELS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int j = 0; j < nlev; ++j) {
-    const unsigned long long* H = j == 0 ? st->cnt_hist0 : st->cnt_hist[j];
-    double v = 0.0;
-    for (int c = threadIdx.x; c < CBINS; c += EF_T) {
-      const unsigned long long h = H[c];
-      if (h && c) v += (double)h * plogp((unsigned long long)c, m);
-    }
-    for (uint32_t b = threadIdx.x; b < n_parts; b += EF_T) v += partials[j * n_parts + b];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tsum = 0.0;
-      for (int w = 0; w < EF_T / 32; ++w) tsum += red[w];
-      lev[j] = -tsum;
-    }
-    __syncthreads();
+  const int j = blockIdx.x;
+  const unsigned long long* H = j == 0 ? st->cnt_hist0 : st->cnt_hist[j];
+  double v = 0.0;
+  for (int c = threadIdx.x; c < CBINS; c += EF_T) {
+    const unsigned long long h = H[c];
+    if (h && c) v += (double)h * plogp((unsigned long long)c, m);
   }
+  for (uint32_t b = threadIdx.x; b < n_parts; b += EF_T) v += partials[j * n_parts + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
   if (threadIdx.x < NLEVELS) {
+    double tsum = 0.0;
+    for (int w = 0; w < EF_T / 32; ++w) tsum += red[w];
     const int n = threadIdx.x;
-    const int j = raw_levels ? n : (n <= k ? 0 : n - k);
-    st->entropy[n] = lev[j < nlev ? j : nlev - 1];
+    int jn = raw_levels ? n : (n <= k ? 0 : n - k);
+    if (jn >= nlev) jn = nlev - 1;
+    if (jn == j) st->entropy[n] = -tsum;
   }
 }
 
@@ -212,7 +209,7 @@ void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_part
   // k == 64 marks the raw-address sparse path (levels are n directly)
   const bool raw = k == 64;
   const int nlev = raw ? 11 : (k >= 10 ? 1 : 11 - (int)k);
-  entropy_finish_kernel<<<1, EF_T, 0, s>>>(st, partials, n_parts, (double)total_m, nlev, raw ? 0 : (int)k, raw);
+  entropy_finish_kernel<<<nlev, EF_T, 0, s>>>(st, partials, n_parts, (double)total_m, nlev, raw ? 0 : (int)k, raw);
 }
 
 // ---------------------------------------------------------------------------
