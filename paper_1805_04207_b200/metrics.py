@@ -27,6 +27,7 @@ import numpy as np
 
 from . import _native
 from .errors import AiwcError, EmptySample, IncompatibleReports, InvalidStream, TraceTooLarge
+from .fields import FIELDS, materialize, merge_fields
 from .report import AiwcReport, round12
 from .trace import ColumnarTrace
 
@@ -206,8 +207,10 @@ class KernelAccumulator:
 
     def __init__(self, kernel_name: str, invocations: list[int], launches: list, result: EngineResult,
                  opcodes: list[str], trace: ColumnarTrace | None = None,
-                 lmae_per_invocation: list | None = None):
+                 lmae_per_invocation: list | None = None, parts: list | None = None):
         object.__setattr__(self, "_over", {})
+        object.__setattr__(self, "_fields", None)
+        self.parts = parts
         self.kernel_name = kernel_name
         self.invocations = invocations
         self.launches = launches
@@ -238,9 +241,24 @@ class KernelAccumulator:
             return r.work_items
         if name == "barriers_hit":
             return r.barriers_hit
-        if name in ("itb_samples", "ipt_samples", "read_addresses", "write_addresses", "branch_records"):
-            raise AiwcError(f"{name} is kept on the device; per-event materialisation is not exposed yet")
+        if name in FIELDS:
+            return self.per_event_fields()[name]
         raise AttributeError(name)
+
+    def per_event_fields(self) -> dict:
+        """itb/ipt sample lists, address Counters and branch streams, rebuilt
+        from the consumed columns on first access (fields.py)."""
+        f = object.__getattribute__(self, "_fields")
+        if f is None:
+            parts = object.__getattribute__(self, "parts")
+            if parts:
+                f = merge_fields([q.per_event_fields() for q in parts])
+            elif object.__getattribute__(self, "trace") is not None:
+                f = materialize(object.__getattribute__(self, "trace"))
+            else:
+                raise AiwcError("this accumulator was built without its trace columns")
+            object.__setattr__(self, "_fields", f)
+        return f
 
     def branch_executions(self) -> dict[int, int]:
         return dict(self.result.sites)
@@ -439,4 +457,4 @@ def merge_accumulators(parts: list[KernelAccumulator], *, allow_name_mismatch: b
     invocations = [i for p in parts for i in p.invocations]
     launches = [l for p in parts for l in p.launches]
     return KernelAccumulator(parts[0].kernel_name, invocations, launches, res, list(tr.opcodes), trace=tr,
-                             lmae_per_invocation=per_inv)
+                             lmae_per_invocation=per_inv, parts=list(parts))
