@@ -98,6 +98,27 @@ def _dist_env():
 # ---------------------------------------------------------------------------
 # reference arm: the C restatement of the reference path on the host cores
 # ---------------------------------------------------------------------------
+def host_threads() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return max(1, os.cpu_count() or 1)
+
+
+def reference_sample(cfg: int, w: int, args, threads: int):
+    """A bounded prefix of whole work-groups of the same trace (a valid trace),
+    sized for ~10 s of CPU work per step: 2^21 work-items per 2 threads."""
+    from paper_1805_04207_b200 import synth
+
+    sample_wi = min(w, args.ref_sample_wi * max(1, threads // 2))
+    if args.ref_python_gen:
+        return sample_wi, synth.python_trace(cfg, sample_wi)
+    import torch
+
+    torch.cuda.set_device(0)
+    return sample_wi, synth.device_trace(cfg, sample_wi).to_numpy()
+
+
 def run_reference(args) -> None:
     world, rank, _ = _dist_env()
     if rank != 0:
@@ -110,22 +131,18 @@ def run_reference(args) -> None:
     oracle.build()
     cfg = args.config
     w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
-    # bounded sample: the first whole work-groups of the same trace (a valid trace)
-    sample_wi = min(w, args.ref_sample_wi)
-    tr = synth.python_trace(cfg, sample_wi) if args.ref_python_gen else None
-    if tr is None:
-        import torch
-
-        torch.cuda.set_device(0)
-        tr = synth.device_trace(cfg, sample_wi).to_numpy()
+    threads = host_threads()
+    sample_wi, tr = reference_sample(cfg, w, args, threads)
     kind, payload = tr.kind, tr.payload.view(np.uint64)
     n = int(kind.shape[0])
+    run = lambda: oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes),  # noqa: E731
+                             threads=threads)
     for _ in range(args.warmup):
-        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+        run()
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+        run()
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
     v = n / dt
@@ -135,9 +152,10 @@ def run_reference(args) -> None:
         "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
         "config": {"workload": f"C{cfg} {synth.NAMES[cfg]} prefix of {sample_wi} work-items ({n} events)",
                    "full_workload_work_items": w},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"first {sample_wi} work-items of C{cfg} ({n} events), oracle/aiwc_oracle.c, "
-                                   "single-threaded restatement of consume+finalize"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"first {sample_wi} work-items of C{cfg} ({n} events); oracle/aiwc_oracle_mt.c: "
+                                   f"consume+finalize restatement on {threads} threads (work-group shards + "
+                                   "address-owner merge, SURVEY 8d(ii))"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -309,24 +327,26 @@ def run_ours(args) -> None:
 
 
 def cpu_baseline(cfg, w, args):
-    """Oracle (C restatement of the reference path) on a bounded prefix, rank 0 only."""
+    """Oracle (C restatement of the reference path) on all host threads, on a
+    bounded prefix of the same trace, rank 0 only."""
     import numpy as np
 
     from oracle import oracle
-    from paper_1805_04207_b200 import synth
 
     try:
         oracle.build()
-        sample_wi = min(w, args.ref_sample_wi)
-        tr = synth.device_trace(cfg, sample_wi).to_numpy()
+        threads = host_threads()
+        sample_wi, tr = reference_sample(cfg, w, args, threads)
         kind, payload = tr.kind, tr.payload.view(np.uint64)
+        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes), threads=threads)
         t0 = time.perf_counter()
-        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes))
+        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes), threads=threads)
         dt = time.perf_counter() - t0
-        return {"value": kind.shape[0] / dt, "unit": UNIT, "cores": 1, "kind": "port",
-                "sample": f"first {sample_wi} work-items of C{cfg} ({kind.shape[0]} events), oracle/aiwc_oracle.c"}
+        return {"value": kind.shape[0] / dt, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": f"first {sample_wi} work-items of C{cfg} ({kind.shape[0]} events), "
+                          f"oracle/aiwc_oracle_mt.c on {threads} threads"}
     except Exception as exc:  # pragma: no cover
-        return {"value": None, "unit": UNIT, "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
 
 
 def main():

@@ -24,246 +24,128 @@
 
 #include "aiwc_oracle.h"
 
-/* ---- kind codes (include/aiwc_b200.h) ---------------------------------- */
-enum {
-  K_INSTR = 0x01, K_LOAD = 0x02, K_ATOMIC_LOAD = 0x82, K_STORE = 0x04, K_ATOMIC_STORE = 0x84,
-  K_BRANCH = 0x08, K_WI_END = 0x10, K_BARRIER = 0x90, K_WI_BEGIN = 0x30, K_WI_RESUME = 0xB0,
-  K_WG_BEGIN = 0x40, K_WG_END = 0xC0, K_KERNEL_BEGIN = 0x20, K_KERNEL_END = 0xA0
-};
+#include "oracle_util.h"
 
-/* ---- u64 -> u64 open-addressing map (stands in for Python's Counter/dict) -- */
-typedef struct {
-  uint64_t *keys, *vals;
-  uint8_t *used;
-  uint64_t cap, size;
-} map64;
 
-static uint64_t mix64(uint64_t x) {
-  x ^= x >> 30; x *= 0xbf58476d1ce4e5b9ULL;
-  x ^= x >> 27; x *= 0x94d049bb133111ebULL;
-  return x ^ (x >> 31);
+
+
+int oacc_init(acc_state *a, const oracle_params *prm) {
+  memset(a, 0, sizeof *a);
+  a->H = prm->history_len ? prm->history_len : 16;
+  a->cap = prm->entry_cap;
+  a->table = 1ULL << a->H;
+  a->n_opcodes = prm->n_opcodes;
+  if (map_init(&a->rd, 1024) || map_init(&a->wr, 1024) || map_init(&a->sites, 64) || map_init(&a->tal, 1024) ||
+      map_init(&a->wmap, 64))
+    return -1;
+  a->opc = (uint64_t *)calloc(prm->n_opcodes ? prm->n_opcodes : 1, 8);
+  a->taken_tab = (uint64_t *)calloc(a->table, 8);
+  a->total_tab = (uint64_t *)calloc(a->table, 8);
+  a->current = -1;     /* index into tl; -1 = None */
+  a->open_group = 0;   /* checker.open_group (metrics.py:149) */
+  return (a->opc && a->taken_tab && a->total_tab) ? 0 : -1;
 }
 
-static int map_init(map64 *m, uint64_t cap) {
-  m->cap = 16;
-  while (m->cap < cap * 2) m->cap <<= 1;
-  m->size = 0;
-  m->keys = (uint64_t *)malloc(m->cap * 8);
-  m->vals = (uint64_t *)malloc(m->cap * 8);
-  m->used = (uint8_t *)calloc(m->cap, 1);
-  return (m->keys && m->vals && m->used) ? 0 : -1;
+void oacc_free(acc_state *a) {
+  map_free(&a->rd); map_free(&a->wr); map_free(&a->sites); map_free(&a->tal); map_free(&a->wmap);
+  free(a->itb.v); free(a->ipt.v); free(a->site_ids.v); free(a->wvals.v); free(a->wcnts.v); free(a->wfirst.v);
+  free(a->srec); free(a->tl); free(a->opc); free(a->taken_tab); free(a->total_tab);
+  memset(a, 0, sizeof *a);
 }
 
-static void map_free(map64 *m) { free(m->keys); free(m->vals); free(m->used); memset(m, 0, sizeof *m); }
-
-/* returns slot; *fresh = 1 when the key was inserted (value zeroed) */
-static uint64_t map_slot(map64 *m, uint64_t key, int *fresh);
-
-static int map_grow(map64 *m) {
-  map64 n;
-  if (map_init(&n, m->cap) != 0) return -1; /* doubles capacity */
-  for (uint64_t i = 0; i < m->cap; i++)
-    if (m->used[i]) {
-      int f;
-      uint64_t s = map_slot(&n, m->keys[i], &f);
-      n.vals[s] = m->vals[i];
-    }
-  map_free(m);
-  *m = n;
-  return 0;
-}
-
-static uint64_t map_slot(map64 *m, uint64_t key, int *fresh) {
-  if ((m->size + 1) * 2 > m->cap) map_grow(m);
-  uint64_t mask = m->cap - 1, i = mix64(key) & mask;
-  while (m->used[i]) {
-    if (m->keys[i] == key) { *fresh = 0; return i; }
-    i = (i + 1) & mask;
-  }
-  m->used[i] = 1; m->keys[i] = key; m->vals[i] = 0; m->size++;
-  *fresh = 1;
-  return i;
-}
-
-static int map_find(const map64 *m, uint64_t key, uint64_t *slot) {
-  uint64_t mask = m->cap - 1, i = mix64(key) & mask;
-  while (m->used[i]) {
-    if (m->keys[i] == key) { *slot = i; return 1; }
-    i = (i + 1) & mask;
-  }
-  return 0;
-}
-
-/* ---- growable u64 vector (Python list) ---------------------------------- */
-typedef struct { uint64_t *v; uint64_t n, cap; } vec64;
-static int vec_push(vec64 *a, uint64_t x) {
-  if (a->n == a->cap) {
-    uint64_t nc = a->cap ? a->cap * 2 : 1024;
-    uint64_t *nv = (uint64_t *)realloc(a->v, nc * 8);
-    if (!nv) return -1;
-    a->v = nv; a->cap = nc;
-  }
-  a->v[a->n++] = x;
-  return 0;
-}
-
-static int cmp_u64(const void *a, const void *b) {
-  uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
-  return (x > y) - (x < y);
-}
-static int cmp_u64_desc(const void *a, const void *b) { return cmp_u64(b, a); }
-
-/* Neumaier-compensated sum: numpy's pairwise sum is ~eps accurate, a naive
- * running sum over 10^8 terms is not. */
-typedef struct { double s, c; } ksum;
-static void kadd(ksum *k, double x) {
-  double t = k->s + x;
-  if (fabs(k->s) >= fabs(x)) k->c += (k->s - t) + x; else k->c += (x - t) + k->s;
-  k->s = t;
-}
-static double kval(const ksum *k) { return k->s + k->c; }
-
-/* coverage_count (entropy.py:49-66): smallest k of the most frequent keys with
- * cumulative >= 9/10 of the total; the Fraction compare is the exact integer
- * test 10*cum >= 9*total (reference.py:57). Sorts `counts` in place. */
-static uint64_t coverage90(uint64_t *counts, uint64_t n) {
-  if (n == 0) return 0;
-  qsort(counts, n, 8, cmp_u64_desc);
-  unsigned __int128 total = 0, cum = 0;
-  for (uint64_t i = 0; i < n; i++) total += counts[i];
-  for (uint64_t i = 0; i < n; i++) {
-    cum += counts[i];
-    if (cum * 10 >= total * 9) return i + 1;
-  }
-  return n;
-}
-
-/* shannon_entropy (entropy.py:20-29): p = c/total; -(sum p*log2 p).
- * A single key gives -(0.0) = -0.0, as in the reference. */
-static double shannon(const uint64_t *counts, uint64_t n, uint64_t total) {
-  ksum k = {0.0, 0.0};
-  double t = (double)total;
-  for (uint64_t i = 0; i < n; i++) {
-    double p = (double)counts[i] / t;
-    kadd(&k, p * log2(p));
-  }
-  return -kval(&k);
-}
-
-typedef struct { uint64_t addr, count; } addr_count;
-static int cmp_addr(const void *a, const void *b) {
-  uint64_t x = ((const addr_count *)a)->addr, y = ((const addr_count *)b)->addr;
-  return (x > y) - (x < y);
-}
-
-typedef struct {
-  uint64_t last_group; /* group of this site's current stream */
-  uint64_t executions; /* branch_executions() (metrics.py:91-95) */
-  uint32_t hist;       /* last history_len outcomes of the current stream, oldest = MSB */
-  uint64_t len;        /* length of the current stream */
-} site_rec;
-
-typedef struct { uint64_t segment, total; } tally;
-
-int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
-               const oracle_params *prm, oracle_result *r) {
-  memset(r, 0, sizeof *r);
-  const uint32_t H = prm->history_len ? prm->history_len : 16;
-  const uint64_t cap = prm->entry_cap;
-  const uint64_t table = 1ULL << H;
-
-  map64 rd, wr, sites, tal;
-  if (map_init(&rd, 1024) || map_init(&wr, 1024) || map_init(&sites, 64) || map_init(&tal, 1024)) return -1;
-  vec64 itb = {0}, ipt = {0}, site_ids = {0};
-  site_rec *srec = NULL; uint64_t n_srec = 0, cap_srec = 0;
-  tally *tl = NULL; uint64_t n_tl = 0, cap_tl = 0;
-  uint64_t *opc = (uint64_t *)calloc(prm->n_opcodes ? prm->n_opcodes : 1, 8);
-  /* width Counter in insertion order (metrics.py:136, order drives the sd sum) */
-  map64 wmap; map_init(&wmap, 64);
-  vec64 wvals = {0}, wcnts = {0}, wfirst = {0};
-  uint64_t *taken_tab = (uint64_t *)calloc(table, 8), *total_tab = (uint64_t *)calloc(table, 8);
-  if (!opc || !taken_tab || !total_tab) return -1;
-
-  uint64_t entries = 0, barriers = 0, work_items = 0, total_instr = 0;
-  uint64_t excluded = 0;
-  int64_t current = -1;          /* index into tl; -1 = None */
-  uint64_t open_group = 0;       /* checker.open_group (metrics.py:149) */
+/* consume()'s loop (metrics.py:125-180) over events [lo, hi); returns 0, or
+ * 1 = TraceTooLarge, 2 = malformed columnar input */
+int oacc_feed(acc_state *a, const uint8_t *kind, const uint64_t *payload, uint64_t lo, uint64_t hi) {
+  const uint32_t H = a->H;
+  const uint64_t cap = a->cap, table = a->table;
+  tally *tl = a->tl;
+  int64_t current = a->current;
+  uint64_t open_group = a->open_group;
   int status = 0;
-
-  for (uint64_t i = 0; i < n && status == 0; i++) {
+  for (uint64_t i = lo; i < hi && status == 0; i++) {
     const uint8_t k = kind[i];
     const uint64_t p = payload[i];
     switch (k) {
       case K_INSTR: { /* metrics.py:131-136 */
+        if (current < 0) { status = 2; break; }
         tl[current].segment++; tl[current].total++;
-        total_instr++;
+        a->total_instr++;
         uint32_t op = (uint32_t)(p >> 32), w = (uint32_t)p;
-        if (op < prm->n_opcodes) opc[op]++; else { status = 2; break; }
-        int fresh; uint64_t s = map_slot(&wmap, w, &fresh);
-        if (fresh) { wmap.vals[s] = wvals.n; vec_push(&wvals, w); vec_push(&wcnts, 0); vec_push(&wfirst, i); }
-        wcnts.v[wmap.vals[s]]++;
+        if (op < a->n_opcodes) a->opc[op]++; else { status = 2; break; }
+        int fresh; uint64_t s = map_slot(&a->wmap, w, &fresh);
+        if (fresh) { a->wmap.vals[s] = a->wvals.n; vec_push(&a->wvals, w); vec_push(&a->wcnts, 0); vec_push(&a->wfirst, i); }
+        a->wcnts.v[a->wmap.vals[s]]++;
         break;
       }
       case K_LOAD: case K_ATOMIC_LOAD: case K_STORE: case K_ATOMIC_STORE: { /* metrics.py:137-144 */
-        map64 *h = (k & 0x02) ? &rd : &wr;
+        map64 *h = (k & 0x02) ? &a->rd : &a->wr;
         int fresh; uint64_t s = map_slot(h, p, &fresh);
         if (fresh) {
-          entries++;
-          if (cap && entries > cap) { status = 1; r->entries_at_fail = entries; break; }
+          a->entries++;
+          if (cap && a->entries > cap) { status = 1; a->entries_at_fail = a->entries; break; }
         }
         h->vals[s]++;
         break;
       }
       case K_BRANCH: { /* metrics.py:145-155; histories per (site, group) stream */
         uint64_t site = p >> 1, bit = p & 1;
-        int fresh; uint64_t s = map_slot(&sites, site, &fresh);
+        int fresh; uint64_t s = map_slot(&a->sites, site, &fresh);
         if (fresh) {
-          if (n_srec == cap_srec) { cap_srec = cap_srec ? cap_srec * 2 : 64; srec = (site_rec *)realloc(srec, cap_srec * sizeof *srec); }
-          sites.vals[s] = n_srec;
-          srec[n_srec].executions = 0; srec[n_srec].len = 0; srec[n_srec].hist = 0;
-          srec[n_srec].last_group = open_group;
-          n_srec++;
-          vec_push(&site_ids, site);
+          if (a->n_srec == a->cap_srec) {
+            a->cap_srec = a->cap_srec ? a->cap_srec * 2 : 64;
+            a->srec = (site_rec *)realloc(a->srec, a->cap_srec * sizeof *a->srec);
+          }
+          a->sites.vals[s] = a->n_srec;
+          site_rec *nr = &a->srec[a->n_srec];
+          nr->executions = 0; nr->len = 0; nr->hist = 0; nr->last_group = open_group;
+          a->n_srec++;
+          vec_push(&a->site_ids, site);
         }
-        site_rec *sr = &srec[sites.vals[s]];
+        site_rec *sr = &a->srec[a->sites.vals[s]];
         if (!fresh && sr->last_group != open_group) { /* streams[-1][0] != group -> new stream */
-          excluded += sr->len < H ? sr->len : H;
+          a->excluded += sr->len < H ? sr->len : H;
           sr->len = 0; sr->hist = 0; sr->last_group = open_group;
         }
         /* branch_entropy (entropy.py:102-117): execution t >= H of a stream is an
          * observation keyed by the previous H outcomes, oldest as MSB */
-        if (sr->len >= H) { total_tab[sr->hist]++; taken_tab[sr->hist] += bit; }
+        if (sr->len >= H) { a->total_tab[sr->hist]++; a->taken_tab[sr->hist] += bit; }
         sr->hist = (uint32_t)(((sr->hist << 1) | bit) & (table - 1));
         sr->len++;
         sr->executions++;
-        entries++;
-        if (cap && entries > cap) { status = 1; r->entries_at_fail = entries; }
+        a->entries++;
+        if (cap && a->entries > cap) { status = 1; a->entries_at_fail = a->entries; }
         break;
       }
       case K_BARRIER: /* metrics.py:156-161: always sampled, even 0 */
-        barriers++;
-        vec_push(&itb, tl[current].segment);
+        if (current < 0) { status = 2; break; }
+        a->barriers++;
+        vec_push(&a->itb, tl[current].segment);
         tl[current].segment = 0;
         current = -1;
         break;
       case K_WI_BEGIN: { /* metrics.py:162-165: fresh tally keyed by global id */
-        work_items++;
-        if (n_tl == cap_tl) { cap_tl = cap_tl ? cap_tl * 2 : 1024; tl = (tally *)realloc(tl, cap_tl * sizeof *tl); }
-        tl[n_tl].segment = 0; tl[n_tl].total = 0;
-        int fresh; uint64_t s = map_slot(&tal, (open_group << 32) | (uint32_t)p, &fresh);
-        tal.vals[s] = n_tl;
-        current = (int64_t)n_tl++;
+        a->work_items++;
+        if (a->n_tl == a->cap_tl) {
+          a->cap_tl = a->cap_tl ? a->cap_tl * 2 : 1024;
+          a->tl = (tally *)realloc(a->tl, a->cap_tl * sizeof *a->tl);
+          tl = a->tl;
+        }
+        tl[a->n_tl].segment = 0; tl[a->n_tl].total = 0;
+        int fresh; uint64_t s = map_slot(&a->tal, (open_group << 32) | (uint32_t)p, &fresh);
+        a->tal.vals[s] = a->n_tl;
+        current = (int64_t)a->n_tl++;
         break;
       }
       case K_WI_RESUME: { /* metrics.py:166-168 */
         uint64_t s;
-        if (!map_find(&tal, (open_group << 32) | (uint32_t)p, &s)) { status = 2; break; }
-        current = (int64_t)tal.vals[s];
+        if (!map_find(&a->tal, (open_group << 32) | (uint32_t)p, &s)) { status = 2; break; }
+        current = (int64_t)a->tal.vals[s];
         break;
       }
       case K_WI_END: /* metrics.py:169-174: trailing segment only when non-empty */
-        if (tl[current].segment > 0) vec_push(&itb, tl[current].segment);
-        vec_push(&ipt, tl[current].total);
+        if (current < 0) { status = 2; break; }
+        if (tl[current].segment > 0) vec_push(&a->itb, tl[current].segment);
+        vec_push(&a->ipt, tl[current].total);
         current = -1;
         break;
       case K_WG_BEGIN: open_group = p; break;
@@ -271,6 +153,33 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
       default: status = 2; break;
     }
   }
+  a->current = current;
+  a->open_group = open_group;
+  return status;
+}
+
+/* the streams still open at the end are whole: their first H executions are warm-up */
+void oacc_close_streams(acc_state *a) {
+  for (uint64_t s = 0; s < a->n_srec; s++) a->excluded += a->srec[s].len < a->H ? a->srec[s].len : a->H;
+}
+
+int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
+               const oracle_params *prm, oracle_result *r) {
+  memset(r, 0, sizeof *r);
+  acc_state A;
+  if (oacc_init(&A, prm)) return -1;
+  const uint64_t table = A.table;
+  int status = oacc_feed(&A, kind, payload, 0, n);
+  r->entries_at_fail = A.entries_at_fail;
+  oacc_close_streams(&A);
+  /* finalize's view of the accumulator */
+  vec64 itb = A.itb, ipt = A.ipt, wvals = A.wvals, wcnts = A.wcnts;
+  map64 rd = A.rd, wr = A.wr;
+  site_rec *srec = A.srec;
+  const uint64_t n_srec = A.n_srec;
+  uint64_t *opc = A.opc, *taken_tab = A.taken_tab, *total_tab = A.total_tab;
+  const uint64_t total_instr = A.total_instr, work_items = A.work_items, barriers = A.barriers;
+  uint64_t excluded = A.excluded;
   r->status = status;
   if (status != 0) goto done;
 
@@ -344,7 +253,6 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
 
   /* branches (metrics.py:323-341, entropy.py:76-133) */
   {
-    for (uint64_t s = 0; s < n_srec; s++) excluded += srec[s].len < H ? srec[s].len : H;
     r->n_sites = n_srec;
     uint64_t *ex = (uint64_t *)malloc((n_srec + 1) * 8);
     for (uint64_t s = 0; s < n_srec; s++) { ex[s] = srec[s].executions; r->executions += ex[s]; }
@@ -373,9 +281,9 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
     w->n_itb = itb.n; w->itb = itb.v; itb.v = NULL;
     w->n_ipt = ipt.n; w->ipt = ipt.v; ipt.v = NULL;
     w->n_opc = prm->n_opcodes; w->opc = opc; opc = NULL;
-    w->width_first = wfirst.v; wfirst.v = NULL;
+    w->width_first = A.wfirst.v; A.wfirst.v = NULL;
     w->n_sites = n_srec;
-    w->site_ids = site_ids.v; site_ids.v = NULL;
+    w->site_ids = A.site_ids.v; A.site_ids.v = NULL;
     w->site_exec = (uint64_t *)malloc((n_srec + 1) * 8);
     for (uint64_t s = 0; s < n_srec; s++) w->site_exec[s] = srec[s].executions;
     w->table_size = table;
@@ -391,10 +299,10 @@ int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
   }
 
 done:
-  free(wfirst.v);
-  map_free(&rd); map_free(&wr); map_free(&sites); map_free(&tal); map_free(&wmap);
-  free(itb.v); free(ipt.v); free(site_ids.v); free(srec); free(tl); free(opc);
-  free(wvals.v); free(wcnts.v); free(taken_tab); free(total_tab);
+  /* ownership of what was handed to r went with it; the rest is freed */
+  A.itb = itb; A.ipt = ipt; A.wvals = wvals; A.wcnts = wcnts;
+  A.opc = opc; A.taken_tab = taken_tab; A.total_tab = total_tab;
+  oacc_free(&A);
   return 0;
 }
 

@@ -41,4 +41,8 @@ typedef struct {
 int oracle_run(const uint8_t *kind, const uint64_t *payload, uint64_t n,
                const oracle_params *p, oracle_result *r);
 void oracle_free(oracle_result *r);
+/* the same on `threads` host threads (work-group shards + owner merge; aiwc_oracle_mt.c).
+ * Uncapped only (entry_cap = 0, keep_raw = 0), else status 3. */
+int oracle_run_mt(const uint8_t *kind, const uint64_t *payload, uint64_t n,
+                  const oracle_params *p, uint32_t threads, oracle_result *r);
 #endif

@@ -90,11 +90,18 @@ def accumulator(kind: np.ndarray, payload: np.ndarray, n_opcodes: int, history_l
         lib.oracle_free(ctypes.byref(res))
 
 
+SOURCES = ("aiwc_oracle.c", "aiwc_oracle_mt.c")
+DEPS = SOURCES + ("aiwc_oracle.h", "oracle_util.h")
+
+
 def build() -> str:
     """Compile liboracle.so from the C restatement (plain gcc)."""
-    src = os.path.join(HERE, "aiwc_oracle.c")
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", LIB, src, "-lm"])
+    newest = max(os.path.getmtime(os.path.join(HERE, f)) for f in DEPS)
+    if not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        tmp = f"{LIB}.{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", tmp, *[os.path.join(HERE, f) for f in SOURCES],
+                               "-lm", "-lpthread"])
+        os.replace(tmp, LIB)  # atomic: concurrent test processes never load a half-written library
     return LIB
 
 
@@ -110,6 +117,9 @@ def _load():
         lib.oracle_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
                                    ctypes.POINTER(_Params), ctypes.POINTER(_Result)]
         lib.oracle_run.restype = ctypes.c_int
+        lib.oracle_run_mt.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                      ctypes.POINTER(_Params), ctypes.c_uint32, ctypes.POINTER(_Result)]
+        lib.oracle_run_mt.restype = ctypes.c_int
         lib.oracle_free.argtypes = [ctypes.POINTER(_Result)]
         _lib = lib
     return _lib
@@ -133,14 +143,22 @@ def _median(d) -> float:
 
 
 def run(kind: np.ndarray, payload: np.ndarray, *, kernel: str, invocation: int, n_opcodes: int,
-        entry_cap: int = 0, history_len: int = 16) -> dict:
-    """Full report dict (AiwcReport fields, no derived keys) for one columnar trace."""
+        entry_cap: int = 0, history_len: int = 16, threads: int = 1) -> dict:
+    """Full report dict (AiwcReport fields, no derived keys) for one columnar trace.
+    threads > 1 runs the work-group-sharded driver (aiwc_oracle_mt.c; uncapped only)."""
     lib = _load()
     kind = np.ascontiguousarray(kind, dtype=np.uint8)
     payload = np.ascontiguousarray(payload, dtype=np.uint64)
     prm = _Params(n_opcodes, history_len, entry_cap, 0, 0)
     res = _Result()
-    rc = lib.oracle_run(kind.ctypes.data, payload.ctypes.data, kind.shape[0], ctypes.byref(prm), ctypes.byref(res))
+    if threads > 1:
+        if entry_cap:
+            raise ValueError("the multi-threaded oracle runs uncapped")
+        rc = lib.oracle_run_mt(kind.ctypes.data, payload.ctypes.data, kind.shape[0], ctypes.byref(prm), threads,
+                               ctypes.byref(res))
+    else:
+        rc = lib.oracle_run(kind.ctypes.data, payload.ctypes.data, kind.shape[0], ctypes.byref(prm),
+                            ctypes.byref(res))
     if rc != 0:
         raise MemoryError("oracle allocation failed")
     try:
