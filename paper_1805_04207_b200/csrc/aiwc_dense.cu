@@ -151,11 +151,12 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
     run_n = 0;
   };
 
-  E cur[K], nxt[K];
+  E cur[K], nxt[K], nx2[K];  // two chunks in flight ahead of the one being folded
   uint64_t ch = blockIdx.x;
   if (ch < n_chunks) load(ch, cur);
+  if (ch + gridDim.x < n_chunks) load(ch + gridDim.x, nxt);
   for (; ch < n_chunks; ch += gridDim.x) {
-    if (ch + gridDim.x < n_chunks) load(ch + gridDim.x, nxt);
+    if (ch + 2ull * gridDim.x < n_chunks) load(ch + 2ull * gridDim.x, nx2);
     bool same = true;
 #pragma unroll
     for (int i = 1; i < K; ++i) same &= cur[i] == cur[0];
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
       __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < K; ++i) cur[i] = nxt[i];
+    for (int i = 0; i < K; ++i) { cur[i] = nxt[i]; nxt[i] = nx2[i]; }
   }
   flush_run();
   __syncthreads();

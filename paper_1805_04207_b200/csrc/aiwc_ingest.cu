@@ -55,6 +55,25 @@ __device__ __forceinline__ void load_kind16(const uint8_t* kind, uint64_t e0, ui
 
 __device__ __forceinline__ uint32_t m_wgb(uint32_t w) { return w & ~(w >> 1) & 0x40404040u; }
 
+// 16 kind bytes -> masks with bit 8b + i set when event 4i + b is a work-item
+// boundary / a work-group begin (only the last chunk holding one is decoded)
+__device__ __forceinline__ uint32_t chunk_bnd(const uint32_t w[4]) {
+  return ((w[0] & 0x10101010u) >> 4) | ((w[1] & 0x10101010u) >> 3) | ((w[2] & 0x10101010u) >> 2) |
+         ((w[3] & 0x10101010u) >> 1);
+}
+__device__ __forceinline__ uint32_t chunk_wgb(const uint32_t w[4]) {
+  return (m_wgb(w[0]) >> 6) | (m_wgb(w[1]) >> 5) | (m_wgb(w[2]) >> 4) | (m_wgb(w[3]) >> 3);
+}
+__device__ __forceinline__ long long last_event(long long e0, uint32_t m) {
+  if (e0 < 0) return -1;
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    const uint32_t x = (m >> i) & 0x01010101u;
+    if (x) return e0 + 4 * i + ((31 - __clz(x)) >> 3);
+  }
+  return -1;
+}
+
 // per-class counts of 16 kind bytes.  Nibble packing: L holds bits 0..3
 // (instr, read, write, branch) of two words, H bits 4..7 (boundary, open,
 // group, variant); each class is then one masked popcount per packed word.
@@ -85,7 +104,8 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   const uint64_t re = min(n, rb + sub_len);
   const int t = threadIdx.x;
   KindCounts kc;
-  long long last_bnd = -1, last_wgb = -1;
+  long long lb_e0 = -1, lw_e0 = -1;  // last chunk holding a boundary / group begin, and its mask
+  uint32_t lb_m = 0, lw_m = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   constexpr int U = 4;  // 16-byte loads in flight per thread
   for (uint64_t base = rb + 16ull * U * t; base < re; base += 16ull * U * P1_THREADS) {
@@ -96,12 +116,12 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
     for (int u = 0; u < U; ++u) {
       kc.add(w[u]);
       const uint64_t e0 = base + 16 * u;
+      const uint32_t bm = chunk_bnd(w[u]), gm = chunk_wgb(w[u]);
+      if (bm) { lb_e0 = (long long)e0; lb_m = bm; }
+      if (gm) { lw_e0 = (long long)e0; lw_m = gm; }
+      if (with_stats) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t bm = w[u][i] & 0x10101010u, gm = m_wgb(w[u][i]);
-        if (bm) last_bnd = (long long)(e0 + 4 * i + ((31 - __clz(bm)) >> 3));
-        if (gm) last_wgb = (long long)(e0 + 4 * i + ((31 - __clz(gm)) >> 3));
-        if (with_stats) {
+        for (int i = 0; i < 4; ++i) {
           uint32_t mm = w[u][i] & 0x06060606u;
           while (mm) {
             const int b = (__ffs(mm) - 1) >> 3;
@@ -113,6 +133,7 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
       }
     }
   }
+  long long last_bnd = last_event(lb_e0, lb_m), last_wgb = last_event(lw_e0, lw_m);
   // block reduction
   constexpr int NW = P1_THREADS / 32;
   __shared__ uint32_t s_cnt[NW][6];

@@ -255,17 +255,14 @@ __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restr
                                                           const uint32_t* __restrict__ presence, uint32_t n_ranges,
                                                           uint64_t range_len, unsigned long long* width_first) {
   const uint32_t w = blockIdx.x + 1;
-  __shared__ int s_r;
+  __shared__ uint32_t s_r;
   __shared__ unsigned long long s_pos;
-  if (threadIdx.x == 0) {
-    int r0 = -1;
-    for (uint32_t r = 0; r < n_ranges; ++r)
-      if ((presence[r] >> (w - 1)) & 1u) { r0 = (int)r; break; }
-    s_r = r0;
-    s_pos = ~0ull;
-  }
+  if (threadIdx.x == 0) { s_r = ~0u; s_pos = ~0ull; }
   __syncthreads();
-  if (s_r < 0) return;
+  for (uint32_t r = threadIdx.x; r < n_ranges; r += blockDim.x)  // first range holding width w
+    if ((presence[r] >> (w - 1)) & 1u) { atomicMin(&s_r, r); break; }
+  __syncthreads();
+  if (s_r == ~0u) return;
   const uint64_t lo = (uint64_t)s_r * range_len, hi = min(n, lo + range_len);
   for (uint64_t base = lo; base < hi; base += 256 * 16) {
 #pragma unroll 4
