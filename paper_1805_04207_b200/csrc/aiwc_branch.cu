@@ -239,7 +239,7 @@ int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t histor
   pattern_walk_kernel<<<wb, 256, 0, s>>>(bits, n, H, code);
   const uint64_t chunk_len = ((n + chunks - 1) / chunks + PC_CHUNK_ALIGN - 1) / PC_CHUNK_ALIGN * PC_CHUNK_ALIGN;
   const size_t smem = 2 * (size_t)(size / parts) * sizeof(uint32_t);
-  cudaFuncSetAttribute(pattern_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  set_smem_once(pattern_count_kernel, (int)smem);
   pattern_count_kernel<<<chunks * parts, PC_T, smem, s>>>(code, n, H, parts, chunk_len, partials);
   pattern_reduce_kernel<<<(size + 255) / 256, 256, 0, s>>>(partials, chunks, size, tables);
   branch_finish_kernel<<<1, BF_T, 0, s>>>(tables, size, st);

@@ -40,10 +40,21 @@ __global__ void init_state_kernel(DevState* st) {
   const size_t n = sizeof(DevState) / 8;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) w[i] = 0;
 }
-// separate launch so the sentinels land after every block finished zeroing
-__global__ void init_sentinels_kernel(DevState* st) {
-  st->addr_min = ~0ull;
-  st->addr_and = ~0ull;
+// one launch for every per-trace reset: DevState (with the min / and sentinels),
+// the width count / first-index tables and the per-range width presence masks
+__global__ void init_trace_kernel(DevState* st, unsigned long long* wcount, unsigned long long* wfirst,
+                                  uint32_t* wpres, uint32_t n_ranges) {
+  unsigned long long* w = reinterpret_cast<unsigned long long*>(st);
+  const size_t n = sizeof(DevState) / 8;
+  const size_t i_min = offsetof(DevState, addr_min) / 8, i_and = offsetof(DevState, addr_and) / 8;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    w[i] = (i == i_min || i == i_and) ? ~0ull : 0ull;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < WIDTH_TABLE; i += stride) {
+    wcount[i] = 0;
+    wfirst[i] = ~0ull;
+  }
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_ranges; i += stride) wpres[i] = 0;
 }
 
 __global__ void widen_u32_kernel(const uint32_t* src, uint64_t n, uint64_t* dst) {
@@ -237,16 +248,6 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   ctx->marked = 0;
   ctx->mark(AIWC_PH_INGEST_TOTAL, 0, s);
   DevState* st = P<DevState>(ctx->dev_state);
-  init_state_kernel<<<64, 256, 0, s>>>(st);
-  init_sentinels_kernel<<<1, 1, 0, s>>>(st);
-  ctx->kernels += 2;
-  CK(cudaMemsetAsync(ctx->wcount.p, 0, WIDTH_TABLE * 8, s));
-  CK(cudaMemsetAsync(ctx->wfirst.p, 0xFF, WIDTH_TABLE * 8, s));
-  const uint32_t n_opc = std::max<uint32_t>(info->n_opcodes, 1);
-  CK(grow(ctx->opc, (size_t)std::max<uint32_t>(n_opc, OBINS) * 8));
-  CK(cudaMemsetAsync(ctx->opc.p, 0, (size_t)std::max<uint32_t>(n_opc, OBINS) * 8, s));
-
-  // ---- pass 1: range summaries ----
   const uint64_t n_tiles = (n + TILE - 1) / TILE;
   uint32_t G = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)ctx->n_sms * CTAS_PER_SM);
   uint32_t tpc = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + G - 1) / G);
@@ -256,7 +257,24 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   const uint32_t n_sub = G * P1_SUB;
   CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
   CK(grow(ctx->wpres, (size_t)G * sizeof(uint32_t)));
-  CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * sizeof(uint32_t), s));
+  init_trace_kernel<<<64, 256, 0, s>>>(st, P<unsigned long long>(ctx->wcount), P<unsigned long long>(ctx->wfirst),
+                                       P<uint32_t>(ctx->wpres), G);
+  ctx->kernels += 1;
+  // opcode counters live in DevState (part of finalize's one read) unless the dictionary is large
+  const bool opc_big = info->n_opcodes > (uint32_t)MAX_SMALL_LIST;
+  if (opc_big) {
+    CK(grow(ctx->opc, (size_t)info->n_opcodes * 8));
+    CK(cudaMemsetAsync(ctx->opc.p, 0, (size_t)info->n_opcodes * 8, s));
+  }
+  // tensor maps depend only on the columns: encode them before pass 1's round trip
+  CUtensorMap km, pm;
+  const uint64_t rows = n / 16;
+  if (n) {
+    const int rc = encode_maps(ctx, kind, payload, rows, &km, &pm);
+    if (rc) return rc;
+  }
+
+  // ---- pass 1: range summaries ----
   const bool with_stats = !info->has_addr_stats;
   // Declared address statistics fix the key map before pass 1: clear a u32
   // table of that size on the side stream meanwhile.  Bounded waste when the
@@ -362,15 +380,11 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
 
   // ---- main ingest pass ----
   if (n) {
-    CUtensorMap km, pm;
-    const uint64_t rows = n / 16;
-    int rc = encode_maps(ctx, kind, payload, rows, &km, &pm);
-    if (rc) return rc;
     IngestArgs a{};
     a.kind = kind; a.payload = payload; a.n = n; a.tma_rows = rows;
     a.tiles_per_cta = tpc; a.n_opcodes = info->n_opcodes; a.local_volume = std::max<uint32_t>(info->local_volume, 1);
     a.ranges = P<RangeSum>(ctx->ranges); a.st = st;
-    a.opc_counts = P<unsigned long long>(ctx->opc);
+    a.opc_counts = opc_big ? P<unsigned long long>(ctx->opc) : st->opc_small;
     a.width_count = P<unsigned long long>(ctx->wcount); a.width_first = P<unsigned long long>(ctx->wfirst);
     a.width_presence = P<uint32_t>(ctx->wpres);
     a.itb_ovf = P<uint32_t>(ctx->itb_ovf); a.ipt_ovf = P<uint32_t>(ctx->ipt_ovf);
@@ -378,7 +392,6 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.am = ctx->am;
     a.dense = ctx->dense ? ctx->dtab.p : nullptr;
     a.dense32 = ctx->dense32;
-    { const char* e = getenv("AIWC_DBG_SKIP"); a.dbg_skip = e ? (uint32_t)atoi(e) : 0u; }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);    ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, !ctx->dense || ctx->n_br > 0, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
@@ -560,9 +573,13 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     ctx->d2h += L * 8;
   }
   const uint32_t n_opc = ctx->info.n_opcodes;
-  ctx->opc_counts.assign(n_opc, 0);
-  if (n_opc) CK(cudaMemcpyAsync(ctx->opc_counts.data(), ctx->opc.p, (size_t)n_opc * 8, cudaMemcpyDeviceToHost, s));
-  ctx->d2h += (size_t)n_opc * 8;
+  if (n_opc > (uint32_t)MAX_SMALL_LIST) {
+    ctx->opc_counts.assign(n_opc, 0);
+    CK(cudaMemcpyAsync(ctx->opc_counts.data(), ctx->opc.p, (size_t)n_opc * 8, cudaMemcpyDeviceToHost, s));
+    ctx->d2h += (size_t)n_opc * 8;
+  } else {
+    ctx->opc_counts.assign(h.opc_small, h.opc_small + n_opc);
+  }
   std::vector<unsigned long long> big_sites;
   if (h.n_sites > (unsigned long long)MAX_SMALL_LIST) {
     big_sites.resize(2 * h.n_sites);
@@ -578,7 +595,12 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     CK(cudaMemcpyAsync(wf_full.data(), ctx->wfirst.p, WIDTH_TABLE * 8, cudaMemcpyDeviceToHost, s));
   }
   ctx->mark(AIWC_PH_FINALIZE_TOTAL, 1, s);
-  CK(cudaStreamSynchronize(s));
+  // a second round trip only when the second round queued work (overflow lists,
+  // big dictionaries) or the phase events must be read
+  const bool second_round = h.itb_ovf_n || h.ipt_ovf_n || h.lvl0_ovf_n || n_opc > (uint32_t)MAX_SMALL_LIST ||
+                            h.n_sites > (unsigned long long)MAX_SMALL_LIST ||
+                            h.n_widths_listed > (unsigned long long)MAX_SMALL_LIST;
+  if (second_round || ctx->timing) CK(cudaStreamSynchronize(s));
   std::reverse(ctx->lvl0_sorted.begin(), ctx->lvl0_sorted.end());
 
   // ---- assemble ----

@@ -265,12 +265,11 @@ void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, 
   const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(lvl0_ovf);
   if (e32) {
-    cudaFuncSetAttribute(dense_stats_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set_smem_once(dense_stats_kernel<uint32_t>, (int)smem);
     dense_stats_kernel<uint32_t><<<n_ctas, T, smem, s>>>(static_cast<const uint32_t*>(tab), n_keys, nlev,
                                                          (double)total_m, st, partials, n_ctas, ovf);
   } else {
-    cudaFuncSetAttribute(dense_stats_kernel<unsigned long long>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    set_smem_once(dense_stats_kernel<unsigned long long>, (int)smem);
     dense_stats_kernel<unsigned long long><<<n_ctas, T, smem, s>>>(static_cast<const unsigned long long*>(tab),
                                                                    n_keys, nlev, (double)total_m, st, partials,
                                                                    n_ctas, ovf);

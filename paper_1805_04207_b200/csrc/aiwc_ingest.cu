@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       }
     }
     // memory accesses: dense-table counters (warp-coalesced) or ordered compaction
-    if (DENSE && !(a.dbg_skip & 2)) {
+    if (DENSE) {
       // my accesses go to the warp's list (pre-swizzled smem index | write << 15)
       // at my in-warp exclusive offset ...
       const uint32_t bx = Bi - B;
@@ -655,7 +655,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
-    for (uint32_t m = (a.dbg_skip & 4) ? 0u : rare16; m; m &= m - 1) {
+    for (uint32_t m = rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t k = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
@@ -755,8 +755,7 @@ template <bool DENSE, bool STAGE>
 static cudaError_t launch_variant(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap,
                                   uint32_t n_ctas, cudaStream_t s) {
   const size_t smem = sizeof(StageSmem) + (STAGE ? (TILE - 1) * sizeof(uint64_t) : 0) + 1024;
-  cudaError_t e = cudaFuncSetAttribute(ingest_kernel<DENSE, STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = set_smem_once(ingest_kernel<DENSE, STAGE>, (int)smem);
   if (e != cudaSuccess) return e;
   ingest_kernel<DENSE, STAGE><<<n_ctas, TPB, smem, s>>>(a, kmap, pmap);
   return cudaGetLastError();

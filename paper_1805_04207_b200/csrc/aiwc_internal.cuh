@@ -67,6 +67,7 @@ struct DevState {
   unsigned long long cnt_hist0[CBINS];              // level-0 count-of-counts (footprint_90)
   unsigned long long width_list[3 * MAX_SMALL_LIST]; // (value, count, first) first-seen order
   unsigned long long site_list[2 * MAX_SMALL_LIST];  // (site, count) ascending
+  unsigned long long opc_small[MAX_SMALL_LIST];      // opcode counts when the dictionary has <= 256 ids
   // ---- not copied back ----
   unsigned long long host_end;
   unsigned long long cnt_hist[NLEVELS][CBINS];      // count-of-counts per level (entropy)
@@ -108,8 +109,14 @@ struct IngestArgs {
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
-  uint32_t dbg_skip;                // EXPERIMENT: bit0 instr, bit1 memory, bit2 rare
 };
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+cudaError_t set_smem_attr(const void* kernel, int bytes);
+template <typename K>
+inline cudaError_t set_smem_once(K kernel, int bytes) {
+  return set_smem_attr(reinterpret_cast<const void*>(kernel), bytes);
+}
 
 // ---- small device helpers ----------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -4,6 +4,8 @@
 // reference's Counter/dict re-keying, metrics.py:308-321 / entropy.py:32-46)
 // and by the branch path (stable grouping of per-site outcome streams,
 // metrics.py:145-155).
+#include <mutex>
+
 #include "aiwc_util.cuh"
 
 namespace aiwc {
@@ -263,6 +265,22 @@ uint64_t rle_reduce(const uint64_t* keys, const unsigned long long* wts, uint64_
   rle_write_kernel<<<nb, RL_T, 0, s>>>(keys, wts, n, shift, mode, bc, out_key, out_a, out_b);
   if (kernels) *kernels += 2;
   return h_total;
+}
+
+// per (kernel, device) high-water mark of the dynamic shared memory attribute
+cudaError_t set_smem_attr(const void* kernel, int bytes) {
+  struct Entry { const void* k; int dev, bytes; };
+  static Entry seen[64];
+  static int n_seen = 0;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n_seen; ++i)
+    if (seen[i].k == kernel && seen[i].dev == dev && seen[i].bytes >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && n_seen < 64) seen[n_seen++] = Entry{kernel, dev, bytes};
+  return e;
 }
 
 }  // namespace aiwc
