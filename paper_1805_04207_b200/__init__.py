@@ -18,13 +18,18 @@ from .report import (
     AiwcReport, DerivedMetrics, derive, emit_report, load_report, report_from_dict, report_to_dict, round12,
 )
 from .trace import (
-    Barrier, Branch, ColumnarTrace, Instruction, KernelBegin, KernelEnd, Memory, TraceEvent, WorkGroupBegin,
-    WorkGroupEnd, WorkItemBegin, WorkItemEnd, WorkItemId, WorkItemResume,
+    Barrier, Branch, ColumnarTrace, Instruction, KernelBegin, KernelEnd, Memory, TraceEvent, ValidationReport,
+    Violation, WorkGroupBegin, WorkGroupEnd, WorkItemBegin, WorkItemEnd, WorkItemId, WorkItemResume, validate_stream,
 )
+from .entropy import BranchStats, branch_entropy, coverage_count, local_entropy, shannon_entropy
+from .tracefile import consume_file, decode_event, encode_event, iter_trace, load_trace, read_trace, write_trace
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "BranchStats", "ValidationReport", "Violation", "branch_entropy", "consume_file", "coverage_count",
+    "decode_event", "encode_event", "iter_trace", "load_trace", "local_entropy", "read_trace", "shannon_entropy",
+    "validate_stream", "write_trace",
     "AiwcError", "AiwcReport", "Barrier", "Branch", "ColumnarTrace", "DerivedMetrics", "DeviceError", "DistStats",
     "EmptyHistogram", "EmptySample", "IncompatibleReports", "Instruction", "InvalidSkip", "InvalidStream",
     "KernelAccumulator", "KernelBegin", "KernelEnd", "MalformedEvent", "Memory", "NoBranches", "SchemaError",

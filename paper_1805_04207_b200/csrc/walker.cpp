@@ -18,6 +18,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -164,23 +165,69 @@ int unsupported(const char* msg) {
   return -1;
 }
 
-// returns 0 ok, 1 stop (violation), -1 Python error
-int feed(Walker& w, PyObject* ev) {
-  const long long i = ++w.index;
-  const int c = ev_code(ev);
-  if (c == E_NONE) {
-    PyObject* r = PyObject_Repr(ev);
-    PyErr_Format(PyExc_TypeError, "not a trace event: %U", r);
-    Py_XDECREF(r);
-    return -1;
+// One event with native field values (both front doors fill it).
+struct Rec {
+  int c = E_NONE;
+  uint64_t oid = 0, width = 0;         // instruction
+  uint8_t memk = 0;                    // memory kind byte
+  uint64_t addr = 0;
+  uint64_t site = 0;                   // branch
+  int taken = 0;
+  V3 g{}, gid{}, lid{};                // group id (wg / wi events), global / local id (wi events)
+  PyObject* name = nullptr;            // kernel_begin (borrowed)
+  PyObject* inv = nullptr;
+  V3 gsz{}, lsz{};
+};
+
+// opcode dictionary, shared by both front doors (ids in first-appearance order)
+struct OpDict {
+  std::unordered_map<std::string, uint64_t> str_ids;
+};
+
+int opcode_id_str(Walker& w, OpDict& d, const char* s, size_t n, uint64_t* oid) {
+  std::string key(s, n);
+  auto it = d.str_ids.find(key);
+  if (it != d.str_ids.end()) { *oid = it->second; return 0; }
+  PyObject* u = PyUnicode_DecodeUTF8(s, (Py_ssize_t)n, "strict");
+  if (!u) return -1;
+  const uint64_t id = (uint64_t)PyList_GET_SIZE(w.opc_list);
+  PyObject* v = PyLong_FromUnsignedLongLong(id);
+  const int rc = PyDict_SetItem(w.opc_dict, u, v);
+  Py_DECREF(v);
+  if (rc < 0 || PyList_Append(w.opc_list, u) < 0) { Py_DECREF(u); return -1; }
+  Py_DECREF(u);
+  d.str_ids.emplace(std::move(key), id);
+  *oid = id;
+  return 0;
+}
+
+int opcode_id_obj(Walker& w, OpDict& d, PyObject* op, uint64_t* oid) {
+  if (PyUnicode_Check(op)) {
+    Py_ssize_t n;
+    const char* s = PyUnicode_AsUTF8AndSize(op, &n);
+    if (s) return opcode_id_str(w, d, s, (size_t)n, oid);
+    PyErr_Clear();  // not encodable: key it by object below
   }
+  PyObject* id = PyDict_GetItemWithError(w.opc_dict, op);
+  if (id) { *oid = PyLong_AsUnsignedLongLong(id); return 0; }
+  if (PyErr_Occurred()) return -1;
+  *oid = (uint64_t)PyList_GET_SIZE(w.opc_list);
+  PyObject* v = PyLong_FromUnsignedLongLong(*oid);
+  const int rc = PyDict_SetItem(w.opc_dict, op, v);
+  Py_DECREF(v);
+  if (rc < 0) return -1;
+  return PyList_Append(w.opc_list, op);
+}
+
+// StreamChecker (trace.py:289-424) + columnar encoding of one event.
+// returns 0 ok, 1 stop (violation), -1 Python error
+int feed_rec(Walker& w, const Rec& r) {
+  const long long i = ++w.index;
+  const int c = r.c;
   if (w.ended) { w.flag(i, "kernel_end.last", "event after kernel_end"); return 1; }
   if (!w.have_header) {
     if (c == E_KB) {
-      PyObject* name = PyTuple_GET_ITEM(ev, 0);
-      PyObject* inv = PyTuple_GET_ITEM(ev, 1);
-      if (!get_v3(PyTuple_GET_ITEM(ev, 2), &w.gsz) || !get_v3(PyTuple_GET_ITEM(ev, 3), &w.lsz))
-        return unsupported("kernel_begin sizes must be 3 integers");
+      w.gsz = r.gsz; w.lsz = r.lsz;
       for (int d = 0; d < 3; ++d) {
         if (w.lsz.v[d] <= 0 || w.gsz.v[d] <= 0) return unsupported("launch sizes must be positive");
         w.grid.v[d] = (w.gsz.v[d] + w.lsz.v[d] - 1) / w.lsz.v[d];
@@ -189,8 +236,8 @@ int feed(Walker& w, PyObject* ev) {
         return unsupported("more than 2^31 work-groups");
       if ((uint64_t)(w.lsz.v[0] * w.lsz.v[1] * w.lsz.v[2]) >= (1ull << 31))
         return unsupported("local size volume >= 2^31");
-      Py_INCREF(name); w.kernel_name_obj = name;
-      Py_INCREF(inv); w.invocation_obj = inv;
+      Py_INCREF(r.name); w.kernel_name_obj = r.name;
+      Py_INCREF(r.inv); w.invocation_obj = r.inv;
       w.have_header = true;
       w.push(AIWC_K_KERNEL_BEGIN, 0);
       return 0;
@@ -206,42 +253,13 @@ int feed(Walker& w, PyObject* ev) {
         return 1;
       }
       if (c == E_INS) {
-        PyObject* op = PyTuple_GET_ITEM(ev, 0);
-        uint64_t width;
-        if (!get_u64(PyTuple_GET_ITEM(ev, 1), &width) || width >= (1ull << 32))
-          return unsupported("instruction width must be an integer in [0, 2^32)");
-        PyObject* id = PyDict_GetItemWithError(w.opc_dict, op);
-        uint64_t oid;
-        if (id) {
-          oid = PyLong_AsUnsignedLongLong(id);
-        } else {
-          if (PyErr_Occurred()) return -1;
-          oid = (uint64_t)PyList_GET_SIZE(w.opc_list);
-          PyObject* v = PyLong_FromUnsignedLongLong(oid);
-          if (PyDict_SetItem(w.opc_dict, op, v) < 0) { Py_DECREF(v); return -1; }
-          Py_DECREF(v);
-          PyList_Append(w.opc_list, op);
-        }
-        w.push(AIWC_K_INSTR, (oid << 32) | width);
+        w.push(AIWC_K_INSTR, (r.oid << 32) | r.width);
       } else if (c == E_MEM) {
-        PyObject* op = PyTuple_GET_ITEM(ev, 0);
-        uint64_t addr;
-        if (!get_u64(PyTuple_GET_ITEM(ev, 1), &addr)) return unsupported("memory address must be an integer in [0, 2^64)");
-        uint8_t k;
-        if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "load") == 0) k = AIWC_K_LOAD;
-        else if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "atomic_load") == 0) k = AIWC_K_ATOMIC_LOAD;
-        else if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "atomic_store") == 0) k = AIWC_K_ATOMIC_STORE;
-        else k = AIWC_K_STORE;  // metrics.py:138: anything not in READ_OPS is a write
-        w.push(k, addr);
-        w.amin = std::min(w.amin, addr); w.amax = std::max(w.amax, addr);
-        w.aand &= addr; w.aor |= addr; ++w.n_mem;
+        w.push(r.memk, r.addr);
+        w.amin = std::min(w.amin, r.addr); w.amax = std::max(w.amax, r.addr);
+        w.aand &= r.addr; w.aor |= r.addr; ++w.n_mem;
       } else {
-        uint64_t site;
-        if (!get_u64(PyTuple_GET_ITEM(ev, 0), &site) || site >= (1ull << 32))
-          return unsupported("branch site must be an integer in [0, 2^32)");
-        const int t = PyObject_IsTrue(PyTuple_GET_ITEM(ev, 1));
-        if (t < 0) return -1;
-        w.push(AIWC_K_BRANCH, (site << 1) | (uint64_t)t);
+        w.push(AIWC_K_BRANCH, (r.site << 1) | (uint64_t)r.taken);
       }
       return 0;
     }
@@ -262,17 +280,13 @@ int feed(Walker& w, PyObject* ev) {
       return 0;
     case E_WGB: {
       if (w.group_open) { w.flag(i, "wg.nesting", "wg_begin while another group is open"); return 1; }
-      V3 g;
-      if (!get_v3(PyTuple_GET_ITEM(ev, 0), &g)) return unsupported("group id must be 3 integers");
-      w.group_open = true; w.open_group = g;
+      w.group_open = true; w.open_group = r.g;
       w.reset_group();
-      w.push(AIWC_K_WG_BEGIN, w.group_key(g));
+      w.push(AIWC_K_WG_BEGIN, w.group_key(r.g));
       return 0;
     }
     case E_WGE: {
-      V3 g;
-      if (!get_v3(PyTuple_GET_ITEM(ev, 0), &g)) return unsupported("group id must be 3 integers");
-      if (!w.group_open || !(g == w.open_group)) { w.flag(i, "wg.nesting", "wg_end does not match open group"); return 1; }
+      if (!w.group_open || !(r.g == w.open_group)) { w.flag(i, "wg.nesting", "wg_end does not match open group"); return 1; }
       if (w.seg_open) { w.flag(i, "wi.nesting", "wg_end with open work-item segment"); return 1; }
       for (size_t s = 0; s < w.wi_order.size(); ++s)
         if (w.wi_status[s] != ST_DONE && w.wi_status[s] != 0) {
@@ -295,16 +309,11 @@ int feed(Walker& w, PyObject* ev) {
       }
       w.group_open = false;
       w.reset_group();
-      w.push(AIWC_K_WG_END, w.group_key(g));
+      w.push(AIWC_K_WG_END, w.group_key(r.g));
       return 0;
     }
     default: {  // work-item events
-      PyObject* wi = PyTuple_GET_ITEM(ev, 0);
-      if (!PyTuple_Check(wi) || PyTuple_GET_SIZE(wi) != 3) return unsupported("work_item must be a WorkItemId");
-      V3 gid, lid, grp;
-      if (!get_v3(PyTuple_GET_ITEM(wi, 0), &gid) || !get_v3(PyTuple_GET_ITEM(wi, 1), &lid) ||
-          !get_v3(PyTuple_GET_ITEM(wi, 2), &grp))
-        return unsupported("work-item ids must be 3 integers");
+      const V3 &gid = r.gid, &lid = r.lid, &grp = r.g;
       if (!w.group_open) { w.flag(i, "wi.nesting", "work-item event outside a work-group"); return 1; }
       if (!(grp == w.open_group)) { w.flag(i, "wi.nesting", "work-item belongs to a different group"); return 1; }
       for (int d = 0; d < 3; ++d) {  // _check_id (trace.py:410-418)
@@ -349,27 +358,369 @@ int feed(Walker& w, PyObject* ev) {
   }
 }
 
-PyObject* py_encode(PyObject*, PyObject* args) {
+// object front door: a TraceEvent (ours or the reference's NamedTuples)
+int feed(Walker& w, OpDict& d, PyObject* ev) {
+  const int c = ev_code(ev);
+  if (c == E_NONE) {
+    PyObject* r = PyObject_Repr(ev);
+    PyErr_Format(PyExc_TypeError, "not a trace event: %U", r);
+    Py_XDECREF(r);
+    return -1;
+  }
+  Rec r;
+  r.c = c;
+  const bool open_or_header = !w.ended && w.have_header;
+  switch (c) {
+    case E_KB:
+      if (w.have_header || w.ended) break;  // rule violation: fields are not looked at
+      r.name = PyTuple_GET_ITEM(ev, 0);
+      r.inv = PyTuple_GET_ITEM(ev, 1);
+      if (!get_v3(PyTuple_GET_ITEM(ev, 2), &r.gsz) || !get_v3(PyTuple_GET_ITEM(ev, 3), &r.lsz))
+        return unsupported("kernel_begin sizes must be 3 integers");
+      break;
+    case E_INS:
+      if (!open_or_header || !w.seg_open) break;
+      if (!get_u64(PyTuple_GET_ITEM(ev, 1), &r.width) || r.width >= (1ull << 32))
+        return unsupported("instruction width must be an integer in [0, 2^32)");
+      if (opcode_id_obj(w, d, PyTuple_GET_ITEM(ev, 0), &r.oid) < 0) return -1;
+      break;
+    case E_MEM: {
+      if (!open_or_header || !w.seg_open) break;
+      PyObject* op = PyTuple_GET_ITEM(ev, 0);
+      if (!get_u64(PyTuple_GET_ITEM(ev, 1), &r.addr)) return unsupported("memory address must be an integer in [0, 2^64)");
+      if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "load") == 0) r.memk = AIWC_K_LOAD;
+      else if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "atomic_load") == 0) r.memk = AIWC_K_ATOMIC_LOAD;
+      else if (PyUnicode_Check(op) && PyUnicode_CompareWithASCIIString(op, "atomic_store") == 0) r.memk = AIWC_K_ATOMIC_STORE;
+      else r.memk = AIWC_K_STORE;  // metrics.py:138: anything not in READ_OPS is a write
+      break;
+    }
+    case E_BR: {
+      if (!open_or_header || !w.seg_open) break;
+      if (!get_u64(PyTuple_GET_ITEM(ev, 0), &r.site) || r.site >= (1ull << 32))
+        return unsupported("branch site must be an integer in [0, 2^32)");
+      const int t = PyObject_IsTrue(PyTuple_GET_ITEM(ev, 1));
+      if (t < 0) return -1;
+      r.taken = t;
+      break;
+    }
+    case E_WGB:
+      if (!open_or_header || w.group_open) break;
+      if (!get_v3(PyTuple_GET_ITEM(ev, 0), &r.g)) return unsupported("group id must be 3 integers");
+      break;
+    case E_WGE:
+      if (!open_or_header) break;
+      if (!get_v3(PyTuple_GET_ITEM(ev, 0), &r.g)) return unsupported("group id must be 3 integers");
+      break;
+    case E_WIB: case E_WIR: case E_WIE: {
+      if (!open_or_header) break;
+      PyObject* wi = PyTuple_GET_ITEM(ev, 0);
+      if (!PyTuple_Check(wi) || PyTuple_GET_SIZE(wi) != 3) return unsupported("work_item must be a WorkItemId");
+      if (!get_v3(PyTuple_GET_ITEM(wi, 0), &r.gid) || !get_v3(PyTuple_GET_ITEM(wi, 1), &r.lid) ||
+          !get_v3(PyTuple_GET_ITEM(wi, 2), &r.g))
+        return unsupported("work-item ids must be 3 integers");
+      break;
+    }
+    default: break;
+  }
+  return feed_rec(w, r);
+}
+
+// ---- .aiwctrace canonical lines (trace.py:100-138 writes exactly these) -------
+// A line is taken natively only in the writer's canonical form (fixed key
+// order, compact separators, plain strings without escapes, plain decimal
+// integers); any other line goes to the Python decode_event restatement, so
+// rejection rules and messages stay the reference's (trace.py:177-244).
+struct Cur {
+  const char* p;
+  const char* e;
+  bool lit(const char* s) {
+    const size_t n = strlen(s);
+    if ((size_t)(e - p) < n || memcmp(p, s, n) != 0) return false;
+    p += n;
+    return true;
+  }
+  bool uint(uint64_t* out) {  // 0 | [1-9][0-9]*, < 2^64
+    if (p >= e || *p < '0' || *p > '9') return false;
+    if (*p == '0') { ++p; *out = 0; return p >= e || *p < '0' || *p > '9'; }
+    uint64_t v = 0;
+    while (p < e && *p >= '0' && *p <= '9') {
+      const uint64_t dgt = (uint64_t)(*p - '0');
+      if (v > (~0ull - dgt) / 10) return false;
+      v = v * 10 + dgt;
+      ++p;
+    }
+    *out = v;
+    return true;
+  }
+  bool v3(V3* out) {  // [a,b,c] of non-negative ints < 2^62
+    if (!lit("[")) return false;
+    for (int d = 0; d < 3; ++d) {
+      uint64_t x;
+      if ((d && !lit(",")) || !uint(&x) || x >= (1ull << 62)) return false;
+      out->v[d] = (long long)x;
+    }
+    return lit("]");
+  }
+  bool str(const char** s, size_t* n) {  // "..." without escapes / control chars, non-empty
+    if (!lit("\"")) return false;
+    const char* b = p;
+    while (p < e && *p != '"') {
+      if (*p == '\\' || (unsigned char)*p < 0x20) return false;
+      ++p;
+    }
+    if (p >= e || p == b) return false;
+    *s = b; *n = (size_t)(p - b);
+    ++p;
+    return true;
+  }
+  bool end() { return lit("}") && p == e; }
+};
+
+// 1 parsed, 0 not canonical (caller falls back), -1 Python error
+int parse_canonical(Walker& w, OpDict& d, const char* b, const char* e, Rec* r, PyObject** tmp) {
+  Cur c{b, e};
+  if (!c.lit("{\"ev\":\"")) return 0;
+  if (c.lit("instr\",\"opcode\":")) {
+    const char* s; size_t n;
+    if (!c.str(&s, &n) || !c.lit(",\"width\":") || !c.uint(&r->width) || !c.end()) return 0;
+    if (r->width == 0 || r->width >= (1ull << 32)) return 0;
+    // non-ASCII opcode bytes: let Python validate the UTF-8
+    for (size_t k = 0; k < n; ++k) if ((unsigned char)s[k] >= 0x80) return 0;
+    if (opcode_id_str(w, d, s, n, &r->oid) < 0) return -1;
+    r->c = E_INS;
+    return 1;
+  }
+  if (c.lit("mem\",\"op\":\"")) {
+    if (c.lit("load\"")) r->memk = AIWC_K_LOAD;
+    else if (c.lit("store\"")) r->memk = AIWC_K_STORE;
+    else if (c.lit("atomic_load\"")) r->memk = AIWC_K_ATOMIC_LOAD;
+    else if (c.lit("atomic_store\"")) r->memk = AIWC_K_ATOMIC_STORE;
+    else return 0;
+    if (!c.lit(",\"addr\":") || !c.uint(&r->addr) || !c.end()) return 0;
+    r->c = E_MEM;
+    return 1;
+  }
+  if (c.lit("branch\",\"site\":")) {
+    if (!c.uint(&r->site) || r->site >= (1ull << 32) || !c.lit(",\"taken\":")) return 0;
+    if (c.lit("true")) r->taken = 1;
+    else if (c.lit("false")) r->taken = 0;
+    else return 0;
+    if (!c.end()) return 0;
+    r->c = E_BR;
+    return 1;
+  }
+  if (c.lit("barrier\"")) { if (!c.end()) return 0; r->c = E_BAR; return 1; }
+  if (c.lit("kernel_end\"")) { if (!c.end()) return 0; r->c = E_KE; return 1; }
+  int wi = -1;
+  if (c.lit("wi_begin\"")) wi = E_WIB;
+  else if (c.lit("wi_resume\"")) wi = E_WIR;
+  else if (c.lit("wi_end\"")) wi = E_WIE;
+  if (wi >= 0) {
+    if (!c.lit(",\"global\":") || !c.v3(&r->gid) || !c.lit(",\"local\":") || !c.v3(&r->lid) ||
+        !c.lit(",\"group\":") || !c.v3(&r->g) || !c.end())
+      return 0;
+    r->c = wi;
+    return 1;
+  }
+  if (c.lit("wg_begin\",\"group\":")) { if (!c.v3(&r->g) || !c.end()) return 0; r->c = E_WGB; return 1; }
+  if (c.lit("wg_end\",\"group\":")) { if (!c.v3(&r->g) || !c.end()) return 0; r->c = E_WGE; return 1; }
+  if (c.lit("kernel_begin\",\"kernel\":")) {
+    const char* s; size_t n;
+    uint64_t inv;
+    if (!c.str(&s, &n) || !c.lit(",\"invocation\":") || !c.uint(&inv) || !c.lit(",\"global_size\":") ||
+        !c.v3(&r->gsz) || !c.lit(",\"local_size\":") || !c.v3(&r->lsz) || !c.end())
+      return 0;
+    for (int k = 0; k < 3; ++k) if (r->gsz.v[k] < 1 || r->lsz.v[k] < 1) return 0;
+    for (size_t k = 0; k < n; ++k) if ((unsigned char)s[k] >= 0x80) return 0;
+    tmp[0] = PyUnicode_DecodeUTF8(s, (Py_ssize_t)n, "strict");
+    tmp[1] = PyLong_FromUnsignedLongLong(inv);
+    if (!tmp[0] || !tmp[1]) return -1;
+    r->name = tmp[0]; r->inv = tmp[1];
+    r->c = E_KB;
+    return 1;
+  }
+  return 0;
+}
+
+// ---- validate_stream (trace.py:427-437): every violation, reference state rules ----
+// A separate, collect-everything restatement of StreamChecker.feed / finish
+// (trace.py:309-424): it keeps going after a violation exactly as the
+// reference does (which state each rule updates, several flags per event).
+struct Checker {
+  bool have_header = false, ended = false;
+  V3 lsz{{1, 1, 1}};
+  bool group_open = false;
+  V3 open_group{};
+  bool seg_open = false;
+  V3 seg_gid{};
+  std::unordered_map<V3, size_t, V3Hash> idx;  // insertion-ordered status dict
+  std::vector<V3> order;
+  std::vector<int> status;                      // 0 absent (never), ST_*
+  std::unordered_map<V3, long long, V3Hash> barrier_counts;
+  long long index = -1;
+  std::vector<std::tuple<long long, std::string, std::string>> v;
+  void flag(long long i, const char* rule, const std::string& d) { v.emplace_back(i, rule, d); }
+  void clear_group() { idx.clear(); order.clear(); status.clear(); barrier_counts.clear(); }
+  void set_status(const V3& k, int st) {
+    auto it = idx.find(k);
+    if (it == idx.end()) { idx.emplace(k, order.size()); order.push_back(k); status.push_back(st); }
+    else status[it->second] = st;
+  }
+  int get_status(const V3& k) const {
+    auto it = idx.find(k);
+    return it == idx.end() ? 0 : status[it->second];
+  }
+};
+
+void check_all(Checker& k, const Rec& r) {
+  const long long i = ++k.index;
+  const int t = r.c;
+  if (k.ended) { k.flag(i, "kernel_end.last", "event after kernel_end"); return; }
+  if (!k.have_header) {
+    if (t == E_KB) { k.have_header = true; k.lsz = r.lsz; return; }
+    k.flag(i, "kernel_begin.first", "first event must be kernel_begin");
+    k.have_header = true;
+    k.lsz = V3{{1, 1, 1}};
+  }
+  if (t == E_INS || t == E_MEM || t == E_BR) {
+    static const char* nm[] = {"", "", "", "", "", "", "", "Instruction", "Branch", "Memory"};
+    if (!k.seg_open) k.flag(i, "event.outside_segment", std::string(nm[t]) + " outside a work-item segment");
+    return;
+  }
+  if (t == E_BAR) {
+    if (!k.seg_open) { k.flag(i, "event.outside_segment", "Barrier outside a work-item segment"); return; }
+    k.set_status(k.seg_gid, ST_AT_BARRIER);
+    k.barrier_counts[k.seg_gid] += 1;
+    k.seg_open = false;
+    return;
+  }
+  if (t == E_KB) { k.flag(i, "kernel_begin.first", "duplicate kernel_begin"); return; }
+  if (t == E_KE) {
+    if (k.group_open) k.flag(i, "wg.nesting", "kernel_end with open work-group");
+    k.ended = true;
+    return;
+  }
+  if (t == E_WGB) {
+    if (k.group_open) k.flag(i, "wg.nesting", "wg_begin while another group is open");
+    k.group_open = true; k.open_group = r.g;
+    k.clear_group();
+    return;
+  }
+  if (t == E_WGE) {
+    if (!k.group_open || !(r.g == k.open_group)) k.flag(i, "wg.nesting", "wg_end does not match open group");
+    if (k.seg_open) { k.flag(i, "wi.nesting", "wg_end with open work-item segment"); k.seg_open = false; }
+    for (size_t s = 0; s < k.order.size(); ++s)
+      if (k.status[s] != ST_DONE) { k.flag(i, "wi.unfinished", "work-item " + v3s(k.order[s]) + " never ended"); break; }
+    std::vector<long long> counts;
+    for (auto& kv : k.barrier_counts) counts.push_back(kv.second);
+    std::sort(counts.begin(), counts.end());
+    counts.erase(std::unique(counts.begin(), counts.end()), counts.end());
+    if (counts.size() > 1) {
+      std::string lst = "[";
+      for (size_t q = 0; q < counts.size(); ++q) lst += (q ? ", " : "") + std::to_string(counts[q]);
+      lst += "]";
+      k.flag(i, "barrier.divergence", "work-items of group " + (k.group_open ? v3s(k.open_group) : std::string("None")) +
+                                          " hit differing barrier counts " + lst);
+    }
+    k.group_open = false;
+    k.clear_group();
+    return;
+  }
+  // work-item events
+  if (!k.group_open) { k.flag(i, "wi.nesting", "work-item event outside a work-group"); return; }
+  if (!(r.g == k.open_group)) k.flag(i, "wi.nesting", "work-item belongs to a different group");
+  for (int d = 0; d < 3; ++d) {  // _check_id (trace.py:410-418)
+    if (r.lid.v[d] >= k.lsz.v[d]) {
+      k.flag(i, "wi.id_arithmetic", "local_id[" + std::to_string(d) + "] >= local_size[" + std::to_string(d) + "]");
+      break;
+    }
+    if (r.gid.v[d] != r.g.v[d] * k.lsz.v[d] + r.lid.v[d]) {
+      k.flag(i, "wi.id_arithmetic", "global_id != group_id*local_size + local_id");
+      break;
+    }
+  }
+  const V3& key = r.gid;
+  if (t == E_WIB) {
+    if (k.seg_open) k.flag(i, "wi.nesting", "segment opened while another is open");
+    if (k.idx.count(key)) k.flag(i, "wi.nesting", "wi_begin for an already-started work-item");
+    k.set_status(key, ST_OPEN);
+    if (!k.barrier_counts.count(key)) k.barrier_counts[key] = 0;
+    k.seg_open = true; k.seg_gid = key;
+  } else if (t == E_WIR) {
+    if (k.seg_open) k.flag(i, "wi.nesting", "segment opened while another is open");
+    if (k.get_status(key) != ST_AT_BARRIER) k.flag(i, "wi.resume_without_barrier", "resume of a work-item not waiting at a barrier");
+    k.set_status(key, ST_OPEN);
+    k.seg_open = true; k.seg_gid = key;
+  } else {
+    if (!k.seg_open || !(k.seg_gid == key)) k.flag(i, "wi.nesting", "wi_end without matching open segment");
+    else k.seg_open = false;
+    k.set_status(key, ST_DONE);
+  }
+}
+
+// full conversion of a TraceEvent for the checker (no rule short-cuts)
+int rec_from_obj(PyObject* ev, Rec* r) {
+  const int c = ev_code(ev);
+  if (c == E_NONE) {
+    PyObject* rp = PyObject_Repr(ev);
+    PyErr_Format(PyExc_TypeError, "not a trace event: %U", rp);
+    Py_XDECREF(rp);
+    return -1;
+  }
+  r->c = c;
+  switch (c) {
+    case E_KB:
+      if (!get_v3(PyTuple_GET_ITEM(ev, 3), &r->lsz) || !get_v3(PyTuple_GET_ITEM(ev, 2), &r->gsz))
+        return unsupported("kernel_begin sizes must be 3 integers");
+      break;
+    case E_WGB: case E_WGE:
+      if (!get_v3(PyTuple_GET_ITEM(ev, 0), &r->g)) return unsupported("group id must be 3 integers");
+      break;
+    case E_WIB: case E_WIR: case E_WIE: {
+      PyObject* wi = PyTuple_GET_ITEM(ev, 0);
+      if (!PyTuple_Check(wi) || PyTuple_GET_SIZE(wi) != 3) return unsupported("work_item must be a WorkItemId");
+      if (!get_v3(PyTuple_GET_ITEM(wi, 0), &r->gid) || !get_v3(PyTuple_GET_ITEM(wi, 1), &r->lid) ||
+          !get_v3(PyTuple_GET_ITEM(wi, 2), &r->g))
+        return unsupported("work-item ids must be 3 integers");
+      break;
+    }
+    default: break;
+  }
+  return 0;
+}
+
+PyObject* py_validate(PyObject*, PyObject* args) {
   PyObject* iterable;
   if (!PyArg_ParseTuple(args, "O", &iterable)) return nullptr;
   PyObject* it = PyObject_GetIter(iterable);
   if (!it) return nullptr;
-  Walker w;
-  w.opc_dict = PyDict_New();
-  w.opc_list = PyList_New(0);
-  int rc = 0;
+  Checker k;
   PyObject* ev;
   while ((ev = PyIter_Next(it))) {
-    rc = feed(w, ev);
+    Rec r;
+    const int rc = rec_from_obj(ev, &r);
     Py_DECREF(ev);
-    if (rc) break;
+    if (rc < 0) { Py_DECREF(it); return nullptr; }
+    check_all(k, r);
   }
   Py_DECREF(it);
+  if (PyErr_Occurred()) return nullptr;
+  if (!k.have_header) k.flag(0, "kernel_begin.first", "empty stream");  // finish() (trace.py:420-424)
+  else if (!k.ended) k.flag(std::max(k.index, 0LL), "kernel_end.last", "stream has no kernel_end");
+  PyObject* out = PyList_New((Py_ssize_t)k.v.size());
+  for (size_t q = 0; q < k.v.size(); ++q)
+    PyList_SET_ITEM(out, q, Py_BuildValue("(Lss)", std::get<0>(k.v[q]), std::get<1>(k.v[q]).c_str(),
+                                          std::get<2>(k.v[q]).c_str()));
+  return out;
+}
+
+// the result dict of both front doors; consumes the walker's references
+PyObject* finish(Walker& w, int rc, long long last_line, PyObject* pending) {
   auto cleanup = [&]() {
     Py_XDECREF(w.opc_dict); Py_XDECREF(w.opc_list);
     Py_XDECREF(w.kernel_name_obj); Py_XDECREF(w.invocation_obj);
   };
-  if (rc < 0 || PyErr_Occurred()) { cleanup(); return nullptr; }
+  if (rc < 0 && !pending) { cleanup(); return nullptr; }
   if (rc == 0) {  // finish() (trace.py:420-424)
     if (!w.have_header) w.flag(0, "kernel_begin.first", "empty stream");
     else if (!w.ended) w.flag(std::max(w.index, 0LL), "kernel_end.last", "stream has no kernel_end");
@@ -394,13 +745,98 @@ PyObject* py_encode(PyObject*, PyObject* args) {
   }
   PyObject* name = w.kernel_name_obj ? w.kernel_name_obj : Py_None;
   PyObject* inv = w.invocation_obj ? w.invocation_obj : Py_None;
-  PyObject* out = Py_BuildValue("{s:N,s:N,s:O,s:O,s:(LLL),s:(LLL),s:O,s:N,s:N,s:N,s:O}", "kind", kinds, "payload", pays,
-                                "kernel_name", name, "invocation", inv, "global_size", w.gsz.v[0], w.gsz.v[1],
-                                w.gsz.v[2], "local_size", w.lsz.v[0], w.lsz.v[1], w.lsz.v[2], "opcodes", w.opc_list,
-                                "extra_groups", extras, "addr_stats", stats, "violation", violation, "have_header",
-                                w.have_header ? Py_True : Py_False);
+  PyObject* err = pending ? pending : Py_None;
+  PyObject* out = Py_BuildValue("{s:N,s:N,s:O,s:O,s:(LLL),s:(LLL),s:O,s:N,s:N,s:N,s:O,s:L,s:O}", "kind", kinds,
+                                "payload", pays, "kernel_name", name, "invocation", inv, "global_size", w.gsz.v[0],
+                                w.gsz.v[1], w.gsz.v[2], "local_size", w.lsz.v[0], w.lsz.v[1], w.lsz.v[2], "opcodes",
+                                w.opc_list, "extra_groups", extras, "addr_stats", stats, "violation", violation,
+                                "have_header", w.have_header ? Py_True : Py_False, "last_line", last_line, "error",
+                                err);
+  Py_XDECREF(pending);
   cleanup();
   return out;
+}
+
+PyObject* py_encode(PyObject*, PyObject* args) {
+  PyObject* iterable;
+  if (!PyArg_ParseTuple(args, "O", &iterable)) return nullptr;
+  PyObject* it = PyObject_GetIter(iterable);
+  if (!it) return nullptr;
+  Walker w;
+  OpDict d;
+  w.opc_dict = PyDict_New();
+  w.opc_list = PyList_New(0);
+  int rc = 0;
+  PyObject* ev;
+  while ((ev = PyIter_Next(it))) {
+    rc = feed(w, d, ev);
+    Py_DECREF(ev);
+    if (rc) break;
+  }
+  Py_DECREF(it);
+  if (PyErr_Occurred()) rc = -1;
+  return finish(w, rc, -1, nullptr);
+}
+
+// encode_lines(data: bytes, decode_event) -- the lines of an .aiwctrace file
+// (iter_trace, trace.py:246-256): '#' lines are comments, canonical lines are
+// parsed natively, every other line is decoded by decode_event(line, line_no)
+// (the reference's json.loads path, with its MalformedEvent rules).  Stops at
+// the first violation; a MalformedEvent (or decode error) is returned in
+// "error" with the encoded prefix, so the caller can order it against the
+// entry cap exactly as the reference's lazy consume() would.
+PyObject* py_encode_lines(PyObject*, PyObject* args) {
+  Py_buffer buf;
+  PyObject* decode;
+  if (!PyArg_ParseTuple(args, "y*O", &buf, &decode)) return nullptr;
+  Walker w;
+  OpDict d;
+  w.opc_dict = PyDict_New();
+  w.opc_list = PyList_New(0);
+  const char* p = static_cast<const char*>(buf.buf);
+  const char* end = p + buf.len;
+  long long line_no = 0, last_line = -1;
+  int rc = 0;
+  PyObject* pending = nullptr;
+  while (p < end && rc == 0) {
+    const char* nl = static_cast<const char*>(memchr(p, '\n', (size_t)(end - p)));
+    const char* le = nl ? nl : end;
+    ++line_no;
+    const char* b = p;
+    p = nl ? nl + 1 : end;
+    if (le > b && *b == '#') continue;
+    last_line = line_no;
+    Rec r;
+    PyObject* tmp[2] = {nullptr, nullptr};
+    int got = parse_canonical(w, d, b, le, &r, tmp);
+    if (got == 1) {
+      rc = feed_rec(w, r);
+    } else if (got == 0) {
+      PyObject* ev = nullptr;
+      PyObject* line = PyUnicode_DecodeUTF8(b, (Py_ssize_t)(le - b), "strict");
+      if (line) {
+        ev = PyObject_CallFunction(decode, "OL", line, line_no);
+        Py_DECREF(line);
+      }
+      if (!ev) {  // MalformedEvent / UnicodeDecodeError: hand back with the prefix
+        PyObject *t, *v, *tb;
+        PyErr_Fetch(&t, &v, &tb);
+        PyErr_NormalizeException(&t, &v, &tb);
+        pending = v ? v : (Py_INCREF(Py_None), Py_None);
+        Py_XDECREF(t); Py_XDECREF(tb);
+        rc = -1;
+      } else {
+        rc = feed(w, d, ev);
+        Py_DECREF(ev);
+      }
+    } else {
+      rc = -1;
+    }
+    Py_XDECREF(tmp[0]); Py_XDECREF(tmp[1]);
+  }
+  PyBuffer_Release(&buf);
+  if (rc < 0 && !pending) return finish(w, -1, last_line, nullptr);
+  return finish(w, pending ? 2 : rc, last_line, pending);
 }
 
 PyObject* py_init(PyObject*, PyObject* args) {
@@ -414,6 +850,9 @@ PyObject* py_init(PyObject*, PyObject* args) {
 
 PyMethodDef methods[] = {
     {"encode", py_encode, METH_VARARGS, "encode(iterable) -> dict of columns, dictionaries and first violation"},
+    {"encode_lines", py_encode_lines, METH_VARARGS,
+     "encode_lines(data, decode_event) -> the same for the lines of an .aiwctrace file"},
+    {"validate", py_validate, METH_VARARGS, "validate(iterable) -> [(event_index, rule, detail)] (every violation)"},
     {"init", py_init, METH_VARARGS, "init(UnsupportedTrace class)"},
     {nullptr, nullptr, 0, nullptr}};
 

@@ -227,3 +227,28 @@ class ColumnarTrace:
                 yield KernelEnd()
             else:
                 raise ValueError(f"bad kind code {k:#x}")
+
+
+# ---------------------------------------------------------------------------
+# stream validation (trace.py:263-275, 427-437): every violation, natively
+# ---------------------------------------------------------------------------
+class Violation(NamedTuple):
+    event_index: int
+    rule: str
+    detail: str
+
+
+class ValidationReport(NamedTuple):
+    violations: list
+
+    @property
+    def ok(self) -> bool:
+        return not self.violations
+
+
+def validate_stream(events) -> ValidationReport:
+    """Check a stream against every trace invariant; violations are data, not
+    failures (the reference's StreamChecker rules, run by the native walker)."""
+    from .walker import _walker
+
+    return ValidationReport([Violation(*v) for v in _walker().validate(events)])

@@ -1,0 +1,174 @@
+""".aiwctrace files: the reference's line rules (tests/golden/tracefile_lines.json,
+made by the reference's decode_event) and the columnar fast path (native
+canonical parser + Python fallback) against the object path, on CPU; reports
+from consume_file against the reference's goldens on the GPU."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, assert_report_matches, golden_cases
+
+with open(os.path.join(GOLDEN, "tracefile_lines.json"), encoding="utf-8") as _fp:
+    LINES = json.load(_fp)
+
+DERIVED = ("granularity", "barriers_per_instruction", "instructions_per_operand", "load_imbalance")
+
+
+@pytest.mark.parametrize("i", range(len(LINES)))
+def test_decode_event_matches_reference(i):
+    from paper_1805_04207_b200 import MalformedEvent
+    from paper_1805_04207_b200.tracefile import decode_event, encode_event
+
+    case = LINES[i]
+    if "error" in case:
+        with pytest.raises(MalformedEvent) as ei:
+            decode_event(case["line"], i + 1)
+        assert str(ei.value) == case["error"]
+    else:
+        assert encode_event(decode_event(case["line"], i + 1)) == case["event"]
+
+
+def _events(tr):
+    return list(tr.iter_events())
+
+
+def _write(path, lines):
+    with open(path, "w", encoding="utf-8", newline="\n") as fp:
+        for ln in lines:
+            fp.write(ln + "\n")
+
+
+def _same_columns(a, b):
+    assert a.kernel_name == b.kernel_name and a.invocation == b.invocation
+    assert tuple(a.global_size) == tuple(b.global_size) and tuple(a.local_size) == tuple(b.local_size)
+    assert list(a.opcodes) == list(b.opcodes)
+    assert [tuple(g) for g in a.extra_groups] == [tuple(g) for g in b.extra_groups]
+    np.testing.assert_array_equal(np.asarray(a.kind), np.asarray(b.kind))
+    np.testing.assert_array_equal(np.asarray(a.payload).view(np.uint64), np.asarray(b.payload).view(np.uint64))
+
+
+CASES = ["wavefront_big", "bfs_flags", "sweep4", "hot_address", "offgrid_groups", "branch_streams_per_group",
+         "random202_1", "random31337_4", "long_segments", "merge_branchy_part0"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_file_columns_equal_object_path(name, tmp_path):
+    from paper_1805_04207_b200.tracefile import encode_event, load_trace
+    from paper_1805_04207_b200.walker import encode_events
+
+    tr = {c["name"]: t for c, t in golden_cases() if t is not None}[name]
+    events = _events(tr)
+    path = tmp_path / "t.aiwctrace"
+    _write(path, ["# produced by test_tracefile"] + [encode_event(e) for e in events])
+    got, violation, err, last = load_trace(str(path))
+    assert violation is None and err is None
+    want, v2 = encode_events(events)
+    assert v2 is None
+    _same_columns(got, want)
+    assert last == len(events) + 1
+
+
+def test_non_canonical_lines_fall_back_to_the_reference_rules(tmp_path):
+    """Re-ordered keys, spaces, escapes, non-ASCII and CRLF lines decode like json.loads."""
+    from paper_1805_04207_b200.tracefile import encode_event, load_trace
+    from paper_1805_04207_b200.walker import encode_events
+
+    tr = {c["name"]: t for c, t in golden_cases() if t is not None}["random202_2"]
+    events = _events(tr)
+    lines = []
+    for k, e in enumerate(events):
+        ln = encode_event(e)
+        obj = json.loads(ln)
+        if k % 5 == 1:
+            ln = json.dumps(dict(reversed(list(obj.items()))))  # other key order, spaces
+        elif k % 5 == 2:
+            ln = json.dumps(obj, ensure_ascii=True, indent=None, separators=(", ", ": "))
+        elif k % 5 == 3 and obj["ev"] == "instr":
+            obj["opcode"] = obj["opcode"] + "é\"q"
+            ln = json.dumps(obj, separators=(",", ":"), ensure_ascii=False)
+        lines.append(ln)
+    path = tmp_path / "t.aiwctrace"
+    _write(path, lines)
+    got, violation, err, _ = load_trace(str(path))
+    ev2 = []
+    for k, e in enumerate(events):
+        if k % 5 == 3 and type(e).__name__ == "Instruction":
+            e = type(e)(e.opcode + "é\"q", e.width)
+        ev2.append(e)
+    want, _ = encode_events(ev2)
+    assert violation is None and err is None
+    _same_columns(got, want)
+    # CRLF / lone-CR files are read in text mode, like the reference
+    with open(path, "w", encoding="utf-8", newline="\r\n") as fp:
+        fp.write("\n".join(lines) + "\n")
+    got2, violation, err, _ = load_trace(str(path))
+    assert violation is None and err is None
+    _same_columns(got2, want)
+
+
+def test_malformed_line_and_blank_line_errors(tmp_path):
+    from paper_1805_04207_b200 import MalformedEvent
+    from paper_1805_04207_b200.tracefile import load_trace
+
+    head = ['{"ev":"kernel_begin","kernel":"k","invocation":0,"global_size":[2,1,1],"local_size":[2,1,1]}',
+            '{"ev":"wg_begin","group":[0,0,0]}',
+            '{"ev":"wi_begin","global":[0,0,0],"local":[0,0,0],"group":[0,0,0]}']
+    for bad, msg in [("", "line 5: blank line"), ("   ", "line 5: blank line"),
+                     ('{"ev":"instr","opcode":"add","width":0}', "line 5: field 'width' must be >= 1"),
+                     ('{"ev":"mem","op":"load","addr":4096.0}', "line 5: field 'addr' must be a non-negative integer")]:
+        path = tmp_path / "b.aiwctrace"
+        _write(path, head + ['# comment', bad, '{"ev":"kernel_end"}'])
+        tr, violation, err, last = load_trace(str(path))
+        assert isinstance(err, MalformedEvent) and str(err) == msg
+        assert tr.n_events == 3 and last == 5
+
+
+@pytest.mark.parametrize("case", [c for c in json.load(open(os.path.join(GOLDEN, "invalid.json"), encoding="utf-8"))
+                                  if c.get("cap") is None][:25], ids=lambda c: c["name"])
+def test_stream_violations_from_files(case, tmp_path):
+    """The reference's InvalidStream (index, rule) for invalid streams written to files."""
+    from test_cpu_api import events_from_json  # the invalid fixtures' event decoder
+
+    from paper_1805_04207_b200.tracefile import encode_event, load_trace
+
+    events = events_from_json(case["events"])
+    path = tmp_path / "v.aiwctrace"
+    _write(path, [encode_event(e) for e in events])
+    _, violation, err, _ = load_trace(str(path))
+    assert err is None
+    if case.get("error") == "InvalidStream":
+        assert violation is not None and (violation[0], violation[1]) == (case["event_index"], case["rule"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["wavefront_big", "bfs_flags", "sweep4", "random31337_4", "branch_streams_per_group"])
+def test_consume_file_report_matches_reference(name, tmp_path):
+    from paper_1805_04207_b200 import finalize, report_to_dict
+    from paper_1805_04207_b200.tracefile import consume_file, encode_event
+
+    c, tr = {c["name"]: (c, t) for c, t in golden_cases() if t is not None}[name]
+    path = tmp_path / "t.aiwctrace"
+    _write(path, [encode_event(e) for e in _events(tr)])
+    rep = report_to_dict(finalize(consume_file(str(path), max_entries=1 << 40)))
+    assert_report_matches(rep, {k: v for k, v in c["report"].items() if k not in DERIVED})
+
+
+@pytest.mark.gpu
+def test_consume_file_cap_before_malformed_line(tmp_path):
+    """TraceTooLarge wins when the cap is crossed before a malformed line (lazy consume order)."""
+    from paper_1805_04207_b200 import MalformedEvent, TraceTooLarge
+    from paper_1805_04207_b200.tracefile import consume_file
+
+    head = ['{"ev":"kernel_begin","kernel":"k","invocation":0,"global_size":[1,1,1],"local_size":[1,1,1]}',
+            '{"ev":"wg_begin","group":[0,0,0]}',
+            '{"ev":"wi_begin","global":[0,0,0],"local":[0,0,0],"group":[0,0,0]}']
+    mem = [f'{{"ev":"mem","op":"load","addr":{64 * k}}}' for k in range(6)]
+    path = tmp_path / "c.aiwctrace"
+    _write(path, head + mem + ["{oops", '{"ev":"kernel_end"}'])
+    with pytest.raises(TraceTooLarge):
+        consume_file(str(path), max_entries=3)
+    with pytest.raises(MalformedEvent):
+        consume_file(str(path), max_entries=100)
