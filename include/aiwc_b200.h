@@ -194,6 +194,36 @@ int  aiwc_memory_partial(aiwc_ctx *ctx, const uint64_t *reads_dev, uint64_t n_rd
                          uint64_t n_wr, uint64_t base, uint32_t k, uint64_t key_lo, uint64_t n_keys,
                          uint64_t total_m, aiwc_memory_part *out, void *stream);
 
+/* ---- stream validation (StreamChecker, trace.py:289-424) -------------------------
+ * First violation of a columnar trace, decoded as ColumnarTrace.iter_events
+ * would (group from the last wg_begin, work-item ids from the local linear id).
+ * Returns AIWC_OK (valid: out->event_index = -1), AIWC_ERR_INVALID_STREAM
+ * (out filled, also readable through aiwc_last_error), or AIWC_ERR_UNSUPPORTED
+ * (a kind byte outside the alphabet, or a local volume above 1024, which the
+ * device checker's per-work-item tables do not hold).  `detail` is the
+ * reference's text; groups outside the launch grid (dictionary keys) print as
+ * "key K" -- detail_code / group_key / local_id / counts let a caller that
+ * holds the dictionary format them itself. */
+enum { AIWC_V_NONE = 0, AIWC_V_KB_NOT_FIRST, AIWC_V_KB_DUP, AIWC_V_AFTER_KE, AIWC_V_KE_OPEN_GROUP,
+       AIWC_V_OUTSIDE_SEG, AIWC_V_BAR_OUTSIDE, AIWC_V_WGB_OPEN, AIWC_V_WGE_MISMATCH, AIWC_V_WGE_OPEN_SEG,
+       AIWC_V_UNFINISHED, AIWC_V_DIVERGENCE, AIWC_V_WI_OUTSIDE_GROUP, AIWC_V_WI_ID, AIWC_V_OPEN_WHILE_OPEN,
+       AIWC_V_WIB_STARTED, AIWC_V_WIR_NOT_BARRIER, AIWC_V_WIE_NO_SEG, AIWC_V_NO_KE, AIWC_V_EMPTY };
+
+typedef struct {
+  int64_t event_index;         /* -1: valid stream                                  */
+  char rule[48];
+  char detail[256];
+  uint32_t detail_code;        /* AIWC_V_*                                          */
+  uint32_t metric_kind;        /* kind byte of an event outside a segment           */
+  uint64_t group_key;          /* never ended / divergence: the group               */
+  uint64_t local_id;           /* never ended: the work-item's local linear id      */
+  uint32_t n_counts, pad;      /* divergence: distinct barrier counts, ascending    */
+  uint64_t counts[64];
+} aiwc_violation;
+
+int  aiwc_validate(aiwc_ctx *ctx, const uint8_t *kind_dev, const uint64_t *payload_dev, const aiwc_trace_info *info,
+                   const int64_t global_size[3], const int64_t local_size[3], aiwc_violation *out, void *stream);
+
 /* Device-side synthetic trace generators.
  * Writes n events starting at event index `first` of config `cfg` into the
  * device columns; aiwc_synth_size returns the config's total event count and

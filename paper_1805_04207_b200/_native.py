@@ -79,6 +79,16 @@ class MemoryPart(ctypes.Structure):
                 ("big", u64p), ("kernels_launched", ctypes.c_uint32)]
 
 
+class Violation(ctypes.Structure):
+    _fields_ = [("event_index", ctypes.c_int64), ("rule", ctypes.c_char * 48), ("detail", ctypes.c_char * 256),
+                ("detail_code", ctypes.c_uint32), ("metric_kind", ctypes.c_uint32), ("group_key", ctypes.c_uint64),
+                ("local_id", ctypes.c_uint64), ("n_counts", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("counts", ctypes.c_uint64 * 64)]
+
+
+V_UNFINISHED, V_DIVERGENCE = 10, 11  # AIWC_V_* codes whose text names a group
+
+
 class Error(ctypes.Structure):
     _fields_ = [("code", ctypes.c_int32), ("event_index", ctypes.c_int64), ("rule", ctypes.c_char * 48),
                 ("entries", ctypes.c_uint64), ("cap", ctypes.c_uint64), ("message", ctypes.c_char * 256)]
@@ -86,7 +96,7 @@ class Error(ctypes.Structure):
 
 EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
            "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill",
-           "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial")
+           "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial", "aiwc_validate")
 
 _lib = None
 _lock = threading.Lock()
@@ -121,9 +131,11 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_memory_partial.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.POINTER(MemoryPart), vp]
+        i64x3 = ctypes.c_int64 * 3
+        lib.aiwc_validate.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), i64x3, i64x3, ctypes.POINTER(Violation), vp]
         for name in ("aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
                      "aiwc_last_error", "aiwc_synth_fill", "aiwc_shard_tables_get", "aiwc_partition_addresses",
-                     "aiwc_memory_partial"):
+                     "aiwc_memory_partial", "aiwc_validate"):
             getattr(lib, name).restype = ctypes.c_int
         if lib.aiwc_abi_version() != 1:
             raise DeviceError("libaiwc_b200.so ABI version mismatch")

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "aiwc_util.cuh"
@@ -116,6 +117,8 @@ struct aiwc_ctx {
   std::vector<uint64_t> width_firsts, branch_tab_host;
   // multi-GPU: owner partition and owned-key memory partials
   Buf part_entries, part_cursor, mp_state, mp_tab, mp_partials, mp_ovf;
+  // stream validation
+  Buf v_state, v_tiles, v_scan, v_spos, v_spay, v_sgap, v_gstart, v_recs, v_counts;
   std::vector<uint64_t> mp_hist0, mp_big;
 };
 
@@ -183,7 +186,9 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
                  &ctx->ipt_ovf, &ctx->ipt_tab, &ctx->dtab, &ctx->rd, &ctx->wr, &ctx->br, &ctx->partials,
                  &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
                  &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
-                 &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres};
+                 &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres,
+                 &ctx->v_state, &ctx->v_tiles, &ctx->v_scan, &ctx->v_spos, &ctx->v_spay, &ctx->v_sgap,
+                 &ctx->v_gstart, &ctx->v_recs, &ctx->v_counts};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -928,3 +933,170 @@ extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n
   return AIWC_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// stream validation (aiwc_validate.cu)
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void v_init_kernel(ValidateState* vs) {
+  vs->first_ke = ~0ull; vs->winner = ~0ull;
+  vs->n_struct = 0; vs->n_groups = 0; vs->bad_kind = 0; vs->counts_used = 0; vs->kb0 = 0;
+}
+
+std::string tup(const int64_t v[3]) {
+  return "(" + std::to_string(v[0]) + ", " + std::to_string(v[1]) + ", " + std::to_string(v[2]) + ")";
+}
+
+// group tuple of a key: linear index in the launch grid, else a dictionary key
+bool group_of(uint64_t key, const int64_t grid[3], int64_t out[3]) {
+  const uint64_t vol = (uint64_t)(grid[0] * grid[1] * grid[2]);
+  if (key >= vol) return false;
+  out[0] = (int64_t)(key % (uint64_t)grid[0]);
+  out[1] = (int64_t)((key / (uint64_t)grid[0]) % (uint64_t)grid[1]);
+  out[2] = (int64_t)(key / (uint64_t)(grid[0] * grid[1]));
+  return true;
+}
+
+}  // namespace
+
+extern "C" int aiwc_validate(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, const aiwc_trace_info* info,
+                             const int64_t global_size[3], const int64_t local_size[3], aiwc_violation* out,
+                             void* stream) {
+  if (!ctx || !info || !out || !global_size || !local_size) return AIWC_ERR_ARGUMENT;
+  const uint64_t n = info->n_events;
+  if (n && (!kind || !payload)) return fail(ctx, AIWC_ERR_ARGUMENT, "null column pointer");
+  if (n >= (1ull << 32)) return fail(ctx, AIWC_ERR_UNSUPPORTED, "more than 2^32-1 events in one trace");
+  int64_t grid[3];
+  uint64_t lv = 1;
+  for (int d = 0; d < 3; ++d) {
+    if (global_size[d] < 1 || local_size[d] < 1) return fail(ctx, AIWC_ERR_ARGUMENT, "launch sizes must be positive");
+    grid[d] = (global_size[d] + local_size[d] - 1) / local_size[d];
+    lv *= (uint64_t)local_size[d];
+  }
+  if (lv > VALIDATE_LV_MAX)
+    return fail(ctx, AIWC_ERR_UNSUPPORTED, "device validation holds work-groups of at most 1024 work-items");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  *out = aiwc_violation{};
+  out->event_index = -1;
+  const uint64_t tiles = (n + VALIDATE_TILE - 1) / VALIDATE_TILE;
+  CK(grow(ctx->v_state, sizeof(ValidateState)));
+  CK(grow(ctx->v_tiles, std::max<uint64_t>(tiles, 1) * 8));
+  CK(grow(ctx->v_scan, (std::max<uint64_t>(tiles, 1) / 1024 + 2) * 4 * 4));
+  ValidateState* vs = P<ValidateState>(ctx->v_state);
+  ValidateBufs b{};
+  b.tile_s = P<uint32_t>(ctx->v_tiles);
+  b.tile_g = b.tile_s + std::max<uint64_t>(tiles, 1);
+  b.scan_scratch = P<uint32_t>(ctx->v_scan);
+  int kernels = 0;
+  v_init_kernel<<<1, 1, 0, s>>>(vs);
+  validate_phase1(kind, n, vs, b, s, &kernels);
+  ValidateState hv{};
+  CK(cudaMemcpyAsync(&hv, vs, sizeof hv, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (hv.bad_kind) return fail(ctx, AIWC_ERR_UNSUPPORTED, "kind byte outside the columnar alphabet");
+  const uint64_t S = hv.n_struct, NG = hv.n_groups;
+  CK(grow(ctx->v_spos, std::max<uint64_t>(S, 1) * 8));
+  CK(grow(ctx->v_spay, std::max<uint64_t>(S, 1) * 8));
+  CK(grow(ctx->v_sgap, std::max<uint64_t>(S, 1) * 8));
+  CK(grow(ctx->v_gstart, std::max<uint64_t>(NG, 1) * 4));
+  CK(grow(ctx->v_recs, (NG + 1) * sizeof(ValidateRecord)));
+  const uint32_t counts_cap = 1u << 20;
+  CK(grow(ctx->v_counts, counts_cap * 4));
+  b.spos = P<uint64_t>(ctx->v_spos); b.spay = P<uint64_t>(ctx->v_spay); b.sgap = P<uint64_t>(ctx->v_sgap);
+  b.gstart = P<uint32_t>(ctx->v_gstart); b.recs = P<ValidateRecord>(ctx->v_recs);
+  b.counts = P<uint32_t>(ctx->v_counts); b.counts_cap = counts_cap;
+  const uint32_t n_ctas = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((NG + 1 + 3) / 4, (uint64_t)ctx->n_sms * 8));
+  validate_phase2(kind, payload, n, (uint32_t)lv, vs, b, S, NG, n_ctas, s, &kernels);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(&hv, vs, sizeof hv, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  // ---- the first violation, or the end-of-stream rules (finish(), trace.py:420-424) ----
+  uint32_t code = AIWC_V_NONE;
+  ValidateRecord rec{};
+  std::vector<uint32_t> counts;
+  if (hv.winner != ~0ull) {
+    const uint64_t r = hv.winner & 0xFFFFFFFFull;
+    CK(cudaMemcpy(&rec, P<ValidateRecord>(ctx->v_recs) + r, sizeof rec, cudaMemcpyDeviceToHost));
+    code = rec.code;
+    if (rec.n_counts) {
+      counts.resize(rec.n_counts);
+      CK(cudaMemcpy(counts.data(), P<uint32_t>(ctx->v_counts) + rec.counts_off, rec.n_counts * 4,
+                    cudaMemcpyDeviceToHost));
+    }
+  } else if (n == 0) {
+    code = AIWC_V_EMPTY; rec.index = 0;
+  } else if (hv.first_ke == ~0ull) {
+    code = AIWC_V_NO_KE; rec.index = n - 1;
+  }
+  if (code == AIWC_V_NONE) return AIWC_OK;
+  out->event_index = (int64_t)rec.index;
+  out->detail_code = code;
+  out->metric_kind = rec.cls;
+  out->group_key = rec.group_key;
+  out->local_id = rec.local_id;
+  std::sort(counts.begin(), counts.end());
+  counts.erase(std::unique(counts.begin(), counts.end()), counts.end());
+  out->n_counts = (uint32_t)std::min<size_t>(counts.size(), 64);
+  for (uint32_t i = 0; i < out->n_counts; ++i) out->counts[i] = counts[i];
+  // the reference's rule ids and detail text (trace.py:278-424)
+  std::string rule, detail;
+  int64_t g[3];
+  const bool in_grid = group_of(rec.group_key, grid, g);
+  switch (code) {
+    case AIWC_V_KB_NOT_FIRST: rule = "kernel_begin.first"; detail = "first event must be kernel_begin"; break;
+    case AIWC_V_KB_DUP: rule = "kernel_begin.first"; detail = "duplicate kernel_begin"; break;
+    case AIWC_V_EMPTY: rule = "kernel_begin.first"; detail = "empty stream"; break;
+    case AIWC_V_AFTER_KE: rule = "kernel_end.last"; detail = "event after kernel_end"; break;
+    case AIWC_V_NO_KE: rule = "kernel_end.last"; detail = "stream has no kernel_end"; break;
+    case AIWC_V_KE_OPEN_GROUP: rule = "wg.nesting"; detail = "kernel_end with open work-group"; break;
+    case AIWC_V_OUTSIDE_SEG:
+      rule = "event.outside_segment";
+      detail = std::string(rec.cls == AIWC_K_INSTR ? "Instruction" : rec.cls == AIWC_K_BRANCH ? "Branch" : "Memory") +
+               " outside a work-item segment";
+      break;
+    case AIWC_V_BAR_OUTSIDE: rule = "event.outside_segment"; detail = "Barrier outside a work-item segment"; break;
+    case AIWC_V_WGB_OPEN: rule = "wg.nesting"; detail = "wg_begin while another group is open"; break;
+    case AIWC_V_WGE_MISMATCH: rule = "wg.nesting"; detail = "wg_end does not match open group"; break;
+    case AIWC_V_WGE_OPEN_SEG: rule = "wi.nesting"; detail = "wg_end with open work-item segment"; break;
+    case AIWC_V_UNFINISHED: {
+      rule = "wi.unfinished";
+      if (in_grid) {
+        const int64_t l[3] = {(int64_t)(rec.local_id % (uint64_t)local_size[0]),
+                              (int64_t)((rec.local_id / (uint64_t)local_size[0]) % (uint64_t)local_size[1]),
+                              (int64_t)(rec.local_id / (uint64_t)(local_size[0] * local_size[1]))};
+        const int64_t gid[3] = {g[0] * local_size[0] + l[0], g[1] * local_size[1] + l[1], g[2] * local_size[2] + l[2]};
+        detail = "work-item " + tup(gid) + " never ended";
+      } else {
+        detail = "work-item (local " + std::to_string(rec.local_id) + " of group key " + std::to_string(rec.group_key) +
+                 ") never ended";
+      }
+      break;
+    }
+    case AIWC_V_DIVERGENCE: {
+      rule = "barrier.divergence";
+      std::string lst = "[";
+      for (size_t i = 0; i < counts.size(); ++i) lst += (i ? ", " : "") + std::to_string(counts[i]);
+      lst += "]";
+      detail = "work-items of group " + (in_grid ? tup(g) : "key " + std::to_string(rec.group_key)) +
+               " hit differing barrier counts " + lst;
+      break;
+    }
+    case AIWC_V_WI_OUTSIDE_GROUP: rule = "wi.nesting"; detail = "work-item event outside a work-group"; break;
+    case AIWC_V_WI_ID: rule = "wi.id_arithmetic"; detail = "local_id[2] >= local_size[2]"; break;
+    case AIWC_V_OPEN_WHILE_OPEN: rule = "wi.nesting"; detail = "segment opened while another is open"; break;
+    case AIWC_V_WIB_STARTED: rule = "wi.nesting"; detail = "wi_begin for an already-started work-item"; break;
+    case AIWC_V_WIR_NOT_BARRIER: rule = "wi.resume_without_barrier"; detail = "resume of a work-item not waiting at a barrier"; break;
+    case AIWC_V_WIE_NO_SEG: rule = "wi.nesting"; detail = "wi_end without matching open segment"; break;
+    default: rule = "unknown"; break;
+  }
+  snprintf(out->rule, sizeof out->rule, "%s", rule.c_str());
+  snprintf(out->detail, sizeof out->detail, "%s", detail.c_str());
+  ctx->err = aiwc_error{};
+  ctx->err.code = AIWC_ERR_INVALID_STREAM;
+  ctx->err.event_index = out->event_index;
+  snprintf(ctx->err.rule, sizeof ctx->err.rule, "%s", rule.c_str());
+  snprintf(ctx->err.message, sizeof ctx->err.message, "%s", detail.c_str());
+  return AIWC_ERR_INVALID_STREAM;
+}

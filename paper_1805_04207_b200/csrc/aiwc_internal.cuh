@@ -111,6 +111,35 @@ struct IngestArgs {
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
 };
 
+// ---- stream validation (aiwc_validate.cu) ---------------------------------------
+struct ValidateState {
+  unsigned long long first_ke;   // first kernel_end index (~0: none)
+  unsigned long long winner;     // min(index << 32 | range) over flagged ranges (~0: none)
+  uint32_t n_struct, n_groups;   // structural events, work-group begins
+  uint32_t bad_kind, counts_used;
+  uint32_t kb0, pad;             // event 0 is the kernel_begin (the header every later range assumes)
+};
+struct ValidateRecord {
+  uint64_t index;
+  uint32_t code, cls;            // violation code (aiwc_validate.cu), metric kind byte
+  uint64_t group_key, local_id;
+  uint32_t n_counts, counts_off; // distinct barrier counts (barrier.divergence)
+};
+struct ValidateBufs {
+  uint32_t *tile_s, *tile_g, *scan_scratch;
+  uint64_t *spos, *spay, *sgap;
+  uint32_t* gstart;
+  ValidateRecord* recs;
+  uint32_t* counts;
+  uint32_t counts_cap;
+};
+constexpr uint32_t VALIDATE_LV_MAX = 1024;   // larger work-groups are validated on the host
+constexpr int VALIDATE_TILE = 4096;
+void validate_phase1(const uint8_t* kind, uint64_t n, ValidateState* vs, const ValidateBufs& b, cudaStream_t s,
+                     int* kernels);
+void validate_phase2(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t lv, ValidateState* vs,
+                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, cudaStream_t s, int* kernels);
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 cudaError_t set_smem_attr(const void* kernel, int bytes);
 template <typename K>

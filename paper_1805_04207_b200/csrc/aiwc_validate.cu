@@ -1,0 +1,306 @@
+// aiwc_validate.cu -- first stream violation of a columnar trace, on the device.
+//
+// The reference validates every stream inside consume() with StreamChecker
+// (pkg/src/aiwc/trace.py:289-424; metrics.py:126-129,181-184) and raises
+// InvalidStream(event_index, rule, detail) at the first violation.  A
+// columnar trace decodes to events as ColumnarTrace.iter_events does (group
+// from the last wg_begin, work-item ids from the local linear id), so the
+// same rules apply to it.  Three steps:
+//
+//  K1  compaction of the structural events (everything except instructions,
+//      memory accesses and branches: kernel / group / work-item boundaries and
+//      barriers) with, for each, the first metric event of the gap after it;
+//      work-group begins are listed separately.  Two passes (counts, writes)
+//      around a device scan.
+//  K2  one warp per work-group range (a wg_begin up to the next one; range 0
+//      is the prefix before the first) replays the checker over the range's
+//      structural events with per-local-id status / barrier-count tables in
+//      shared memory, checking every gap against the open segment.  Each
+//      range assumes a valid prefix (no group or segment open, header seen,
+//      ended iff a kernel_end precedes it), which holds for the range holding
+//      the true first violation -- so the minimum over ranges is exact.
+//  K3  the host reads the winning range's record and formats the message.
+#include "aiwc_internal.cuh"
+#include "aiwc_util.cuh"
+
+namespace aiwc {
+
+namespace {
+
+constexpr int VT = 256;       // K1 threads
+constexpr int VEPT = 16;      // events per thread
+constexpr int VTILE = VT * VEPT;
+static_assert(VTILE == VALIDATE_TILE, "tile size shared with the host");
+constexpr int K2_WARPS = 4;   // ranges per K2 CTA
+constexpr uint32_t LV_MAX = VALIDATE_LV_MAX;
+
+__device__ __forceinline__ bool structural(uint32_t k) { return (k & 0x0Fu) == 0u && k != 0u; }
+__device__ __forceinline__ bool metric(uint32_t k) {
+  return k == AIWC_K_INSTR || k == AIWC_K_LOAD || k == AIWC_K_ATOMIC_LOAD || k == AIWC_K_STORE ||
+         k == AIWC_K_ATOMIC_STORE || k == AIWC_K_BRANCH;
+}
+__device__ __forceinline__ bool known(uint32_t k) {
+  return metric(k) || k == AIWC_K_WI_END || k == AIWC_K_BARRIER || k == AIWC_K_WI_BEGIN || k == AIWC_K_WI_RESUME ||
+         k == AIWC_K_WG_BEGIN || k == AIWC_K_WG_END || k == AIWC_K_KERNEL_BEGIN || k == AIWC_K_KERNEL_END;
+}
+
+__device__ __forceinline__ uint8_t kind_at(const uint8_t* kind, uint64_t i, uint64_t n) { return i < n ? kind[i] : 0; }
+
+// K1a: per-tile counts of structural events and of work-group begins
+__global__ void __launch_bounds__(VT) v_count_kernel(const uint8_t* __restrict__ kind, uint64_t n,
+                                                     uint32_t* __restrict__ s_cnt, uint32_t* __restrict__ g_cnt,
+                                                     ValidateState* vs) {
+  __shared__ uint32_t red[2][VT / 32];
+  const uint64_t tile = blockIdx.x;
+  const uint64_t e0 = tile * VTILE + (uint64_t)threadIdx.x * VEPT;
+  uint32_t sc = 0, gc = 0;
+  unsigned long long first_ke = ~0ull;
+  bool bad = false;
+  for (int j = 0; j < VEPT; ++j) {
+    const uint64_t e = e0 + j;
+    if (e >= n) break;
+    const uint32_t k = kind[e];
+    sc += structural(k);
+    gc += k == AIWC_K_WG_BEGIN;
+    if (k == AIWC_K_KERNEL_END && first_ke == ~0ull) first_ke = e;
+    bad |= !known(k);
+  }
+  if (first_ke != ~0ull) atomicMin(&vs->first_ke, first_ke);
+  if (tile == 0 && threadIdx.x == 0) vs->kb0 = n && kind[0] == AIWC_K_KERNEL_BEGIN;
+  if (bad) atomicOr(&vs->bad_kind, 1u);
+  sc = warp_sum(sc); gc = warp_sum(gc);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { red[0][warp] = sc; red[1][warp] = gc; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t a = 0, b = 0;
+    for (int w = 0; w < VT / 32; ++w) { a += red[0][w]; b += red[1][w]; }
+    s_cnt[tile] = a; g_cnt[tile] = b;
+  }
+}
+
+// K1b: write the structural entries (position | kind << 32), their payloads,
+// the gap after each (first metric index << 8 | its kind, or ~0) and the
+// compact indices of the work-group begins
+__global__ void __launch_bounds__(VT) v_write_kernel(const uint8_t* __restrict__ kind, const uint64_t* __restrict__ payload,
+                                                     uint64_t n, const uint32_t* __restrict__ s_off,
+                                                     const uint32_t* __restrict__ g_off, uint64_t* __restrict__ spos,
+                                                     uint64_t* __restrict__ spay, uint64_t* __restrict__ sgap,
+                                                     uint32_t* __restrict__ gstart) {
+  __shared__ uint32_t wsum[2][VT / 32];
+  const uint64_t tile = blockIdx.x;
+  const uint64_t e0 = tile * VTILE + (uint64_t)threadIdx.x * VEPT;
+  uint32_t smask = 0, gmask = 0;
+  uint8_t ks[VEPT];
+  for (int j = 0; j < VEPT; ++j) {
+    ks[j] = kind_at(kind, e0 + j, n);
+    if (structural(ks[j])) smask |= 1u << j;
+    if (ks[j] == AIWC_K_WG_BEGIN) gmask |= 1u << j;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t sc = __popc(smask), gc = __popc(gmask);
+  uint32_t si = sc, gi = gc;  // inclusive warp scans
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, si, o), b = __shfl_up_sync(0xffffffffu, gi, o);
+    if (lane >= o) { si += a; gi += b; }
+  }
+  if (lane == 31) { wsum[0][warp] = si; wsum[1][warp] = gi; }
+  __syncthreads();
+  uint32_t sb = s_off[tile], gb = g_off[tile];
+  for (int w = 0; w < warp; ++w) { sb += wsum[0][w]; gb += wsum[1][w]; }
+  uint32_t s = sb + si - sc, g = gb + gi - gc;
+  for (int j = 0; j < VEPT; ++j) {
+    if (!((smask >> j) & 1u)) continue;
+    const uint64_t e = e0 + j;
+    spos[s] = e | ((uint64_t)ks[j] << 32);
+    spay[s] = payload[e];
+    const uint32_t nk = j + 1 < VEPT ? ks[j + 1] : kind_at(kind, e + 1, n);
+    sgap[s] = metric(nk) ? (((e + 1) << 8) | nk) : ~0ull;
+    if (ks[j] == AIWC_K_WG_BEGIN) gstart[g++] = s;
+    ++s;
+  }
+}
+
+// K2 violation codes (host formats the reference's detail text)
+enum : uint32_t {
+  V_NONE = 0, V_KB_NOT_FIRST, V_KB_DUP, V_AFTER_KE, V_KE_OPEN_GROUP, V_OUTSIDE_SEG, V_BAR_OUTSIDE, V_WGB_OPEN,
+  V_WGE_MISMATCH, V_WGE_OPEN_SEG, V_UNFINISHED, V_DIVERGENCE, V_WI_OUTSIDE_GROUP, V_WI_ID, V_OPEN_WHILE_OPEN,
+  V_WIB_STARTED, V_WIR_NOT_BARRIER, V_WIE_NO_SEG
+};
+
+enum : uint8_t { S_ABSENT = 0, S_OPEN = 1, S_AT_BARRIER = 2, S_DONE = 3 };
+
+struct WarpTables {
+  uint8_t status[LV_MAX];
+  uint32_t bcount[LV_MAX];
+  uint32_t order[LV_MAX];  // insertion rank in the status dict (for "never ended")
+};
+
+__global__ void __launch_bounds__(K2_WARPS * 32) v_check_kernel(const uint64_t* __restrict__ spos,
+                                                                const uint64_t* __restrict__ spay,
+                                                                const uint64_t* __restrict__ sgap, uint64_t S,
+                                                                const uint32_t* __restrict__ gstart, uint64_t NG,
+                                                                uint32_t lv, ValidateState* vs, ValidateRecord* recs,
+                                                                uint32_t* counts_buf, uint32_t counts_cap) {
+  __shared__ WarpTables T[K2_WARPS];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  WarpTables& tb = T[wib];
+  const unsigned long long first_ke = vs->first_ke;
+  for (uint64_t r = (uint64_t)blockIdx.x * K2_WARPS + wib; r <= NG; r += (uint64_t)gridDim.x * K2_WARPS) {
+    const uint64_t lo = r == 0 ? 0 : gstart[r - 1];
+    const uint64_t hi = r < NG ? gstart[r] : S;
+    // state at the range start under a valid prefix
+    bool header = r != 0 && vs->kb0, ended = false, gopen = false, sopen = false;
+    uint64_t gkey = 0;
+    uint32_t slid = 0, n_ins = 0;
+    if (r != 0) ended = first_ke < (spos[lo] & 0xFFFFFFFFull);
+    uint32_t code = V_NONE, cls = 0;
+    uint64_t at = 0, aux_g = 0, aux_l = 0;
+    auto clear = [&]() {
+      for (uint32_t i = lane; i < lv; i += 32) { tb.status[i] = S_ABSENT; tb.bcount[i] = 0; }
+      n_ins = 0;
+      __syncwarp();
+    };
+    clear();
+    for (uint64_t s = lo; s < hi && code == V_NONE; ++s) {
+      const uint64_t pk = spos[s];
+      const uint64_t pos = pk & 0xFFFFFFFFull;
+      const uint32_t k = (uint32_t)(pk >> 32);
+      const uint64_t p = spay[s];
+      // ---- the structural event (StreamChecker.feed order of checks) ----
+      if (ended) { code = V_AFTER_KE; at = pos; break; }
+      if (!header) {
+        if (k == AIWC_K_KERNEL_BEGIN) { header = true; goto gap; }
+        code = V_KB_NOT_FIRST; at = pos; break;
+      }
+      switch (k) {
+        case AIWC_K_BARRIER:
+          if (!sopen) { code = V_BAR_OUTSIDE; at = pos; break; }
+          if (lane == 0) { tb.status[slid] = S_AT_BARRIER; tb.bcount[slid] += 1; }
+          sopen = false;
+          break;
+        case AIWC_K_KERNEL_BEGIN: code = V_KB_DUP; at = pos; break;
+        case AIWC_K_KERNEL_END:
+          if (gopen) { code = V_KE_OPEN_GROUP; at = pos; break; }
+          ended = true;
+          break;
+        case AIWC_K_WG_BEGIN:
+          if (gopen) { code = V_WGB_OPEN; at = pos; break; }
+          gopen = true; gkey = p;
+          clear();
+          break;
+        case AIWC_K_WG_END: {
+          if (!gopen || p != gkey) { code = V_WGE_MISMATCH; at = pos; break; }
+          if (sopen) { code = V_WGE_OPEN_SEG; at = pos; break; }
+          // first work-item (insertion order) not done
+          uint32_t best = 0xFFFFFFFFu, best_lid = 0;
+          for (uint32_t i = lane; i < lv; i += 32)
+            if (tb.status[i] != S_ABSENT && tb.status[i] != S_DONE && tb.order[i] < best) { best = tb.order[i]; best_lid = i; }
+          for (int o = 16; o > 0; o >>= 1) {
+            const uint32_t ob = __shfl_xor_sync(0xffffffffu, best, o), ol = __shfl_xor_sync(0xffffffffu, best_lid, o);
+            if (ob < best) { best = ob; best_lid = ol; }
+          }
+          if (best != 0xFFFFFFFFu) { code = V_UNFINISHED; at = pos; aux_g = gkey; aux_l = best_lid; break; }
+          // barrier counts of every work-item seen (barrier_counts keys) must agree
+          uint32_t lo_c = 0xFFFFFFFFu, hi_c = 0;
+          for (uint32_t i = lane; i < lv; i += 32)
+            if (tb.status[i] != S_ABSENT) { lo_c = min(lo_c, tb.bcount[i]); hi_c = max(hi_c, tb.bcount[i]); }
+          for (int o = 16; o > 0; o >>= 1) {
+            lo_c = min(lo_c, __shfl_xor_sync(0xffffffffu, lo_c, o));
+            hi_c = max(hi_c, __shfl_xor_sync(0xffffffffu, hi_c, o));
+          }
+          if (lo_c != 0xFFFFFFFFu && lo_c != hi_c) { code = V_DIVERGENCE; at = pos; aux_g = gkey; break; }
+          gopen = false;
+          clear();
+          break;
+        }
+        default: {  // work-item events
+          const uint32_t lid = (uint32_t)min(p, (uint64_t)0xFFFFFFFFull);
+          if (!gopen) { code = V_WI_OUTSIDE_GROUP; at = pos; break; }
+          if (p >= lv) { code = V_WI_ID; at = pos; break; }
+          if (k == AIWC_K_WI_BEGIN) {
+            if (sopen) { code = V_OPEN_WHILE_OPEN; at = pos; break; }
+            if (tb.status[lid] != S_ABSENT) { code = V_WIB_STARTED; at = pos; break; }
+            if (lane == 0) { tb.status[lid] = S_OPEN; tb.order[lid] = n_ins; }
+            ++n_ins;
+            sopen = true; slid = lid;
+          } else if (k == AIWC_K_WI_RESUME) {
+            if (sopen) { code = V_OPEN_WHILE_OPEN; at = pos; break; }
+            if (tb.status[lid] != S_AT_BARRIER) { code = V_WIR_NOT_BARRIER; at = pos; break; }
+            if (lane == 0) tb.status[lid] = S_OPEN;
+            sopen = true; slid = lid;
+          } else {
+            if (!sopen || slid != lid) { code = V_WIE_NO_SEG; at = pos; break; }
+            sopen = false;
+            if (lane == 0) tb.status[lid] = S_DONE;
+          }
+          break;
+        }
+      }
+      if (code != V_NONE) break;
+    gap:
+      __syncwarp();
+      {  // the first metric event between this structural event and the next
+        const uint64_t gp = sgap[s];
+        if (gp != ~0ull) {
+          if (ended) { code = V_AFTER_KE; at = gp >> 8; }
+          else if (!sopen) { code = V_OUTSIDE_SEG; at = gp >> 8; cls = (uint32_t)(gp & 0xFF); }
+        }
+      }
+    }
+    // the next range's wg_begin meets a group this range left open
+    if (code == V_NONE && gopen && r < NG) { code = V_WGB_OPEN; at = spos[hi] & 0xFFFFFFFFull; }
+    if (code != V_NONE && lane == 0) {
+      ValidateRecord& rec = recs[r];
+      rec.index = at; rec.code = code; rec.cls = cls; rec.group_key = aux_g; rec.local_id = aux_l;
+      rec.n_counts = 0; rec.counts_off = 0;
+      if (code == V_DIVERGENCE) {  // the distinct counts, for the message (rare)
+        uint32_t m = 0;
+        const uint32_t off = atomicAdd(&vs->counts_used, lv);
+        if (off + lv <= counts_cap) {
+          for (uint32_t i = 0; i < lv; ++i)
+            if (tb.status[i] != S_ABSENT) counts_buf[off + m++] = tb.bcount[i];
+          rec.n_counts = m; rec.counts_off = off;
+        }
+      }
+      atomicMin(&vs->winner, ((unsigned long long)at << 32) | (unsigned long long)min(r, (uint64_t)0xFFFFFFFFull));
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void v_prefix_kernel(const uint8_t* kind, uint64_t n, ValidateState* vs, ValidateRecord* rec0) {
+  // a metric event at index 0 (no structural event before it): the header is missing
+  if (n && metric(kind[0])) {
+    rec0->index = 0; rec0->code = V_KB_NOT_FIRST; rec0->cls = 0;
+    atomicMin(&vs->winner, 0ull);
+  }
+}
+
+}  // namespace
+
+void validate_phase1(const uint8_t* kind, uint64_t n, ValidateState* vs, const ValidateBufs& b, cudaStream_t s,
+                     int* kernels) {
+  const uint64_t tiles = (n + VTILE - 1) / VTILE;
+  if (!tiles) return;
+  v_count_kernel<<<(unsigned)tiles, VT, 0, s>>>(kind, n, b.tile_s, b.tile_g, vs);
+  ++*kernels;
+  scan_exclusive_u32(b.tile_s, tiles, b.scan_scratch, &vs->n_struct, s, kernels);
+  scan_exclusive_u32(b.tile_g, tiles, b.scan_scratch, &vs->n_groups, s, kernels);
+}
+
+void validate_phase2(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t lv, ValidateState* vs,
+                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, cudaStream_t s, int* kernels) {
+  const uint64_t tiles = (n + VTILE - 1) / VTILE;
+  if (tiles) {
+    v_write_kernel<<<(unsigned)tiles, VT, 0, s>>>(kind, payload, n, b.tile_s, b.tile_g, b.spos, b.spay, b.sgap,
+                                                  b.gstart);
+    ++*kernels;
+  }
+  v_prefix_kernel<<<1, 1, 0, s>>>(kind, n, vs, b.recs);
+  v_check_kernel<<<n_ctas, K2_WARPS * 32, 0, s>>>(b.spos, b.spay, b.sgap, S, b.gstart, NG, lv, vs, b.recs, b.counts,
+                                                  b.counts_cap);
+  *kernels += 2;
+}
+
+}  // namespace aiwc

@@ -77,4 +77,5 @@ def concat_traces(parts: list[ColumnarTrace]) -> ColumnarTrace:
     first = parts[0]
     # group keys are already disjoint; a 1-D grid with key_base groups decodes them
     return ColumnarTrace(kind, payload, first.kernel_name, first.invocation, (key_base * lv, 1, 1), (lv, 1, 1),
-                         [o for o, _ in sorted(opcodes.items(), key=lambda kv: kv[1])], [], addr_stats)
+                         [o for o, _ in sorted(opcodes.items(), key=lambda kv: kv[1])], [], addr_stats,
+                         validated=all(p.validated for p in parts))

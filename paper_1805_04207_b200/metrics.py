@@ -161,6 +161,64 @@ def ingest_columns(ctx, tr: ColumnarTrace):
     return None
 
 
+def _device_columns(tr: ColumnarTrace, device: int) -> ColumnarTrace:
+    """The trace with its columns in CUDA memory on `device` (no copy if already there)."""
+    import torch
+
+    kind, payload = tr.kind, tr.payload
+    if _is_torch(kind) and kind.is_cuda:
+        return tr
+    dev = torch.device("cuda", device)
+    k = torch.as_tensor(np.ascontiguousarray(kind, dtype=np.uint8) if not _is_torch(kind) else kind).to(dev)
+    pl = payload if _is_torch(payload) else torch.from_numpy(np.ascontiguousarray(payload).view(np.int64))
+    return ColumnarTrace(k, pl.to(dev), tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
+                         tr.extra_groups, tr.addr_stats, tr.validated)
+
+
+def validate_columnar(tr: ColumnarTrace, device: int | None = None) -> tuple | None:
+    """First stream violation (event_index, rule, detail) of a columnar trace, as
+    StreamChecker would report it for tr.iter_events() (trace.py:289-424), or
+    None.  Runs on the device (aiwc_validate); work-groups of more than 1024
+    work-items are checked by the native host walker instead."""
+    kind = tr.kind
+    if device is None:
+        device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
+    lsz = tuple(int(x) for x in tr.local_size)
+    if lsz[0] * lsz[1] * lsz[2] > 1024:
+        from .walker import _walker
+
+        v = _walker().validate(tr.iter_events())
+        return tuple(v[0]) if v else None
+    dtr = _device_columns(tr, device)
+    ctx = _get_ctx(device)
+    try:
+        import torch
+
+        info = trace_info(dtr)
+        out = _native.Violation()
+        i64x3 = ctypes.c_int64 * 3
+        stream = torch.cuda.current_stream(dtr.kind.device).cuda_stream
+        rc = ctx.lib.aiwc_validate(ctx.h, ctypes.c_void_p(dtr.kind.data_ptr()), ctypes.c_void_p(dtr.payload.data_ptr()),
+                                   ctypes.byref(info), i64x3(*[int(x) for x in tr.global_size]), i64x3(*lsz),
+                                   ctypes.byref(out), ctypes.c_void_p(stream))
+        if rc == _native.OK:
+            return None
+        if rc != _native.ERR_INVALID_STREAM:
+            ctx.check(rc)
+        detail = out.detail.decode(errors="replace")
+        if out.detail_code == _native.V_UNFINISHED:  # exact ids, dictionary groups included
+            g = tr.group_of_key(out.group_key)
+            loc = tr.local_of_id(out.local_id)
+            gid = tuple(g[d] * lsz[d] + loc[d] for d in range(3))
+            detail = f"work-item {gid} never ended"
+        elif out.detail_code == _native.V_DIVERGENCE:
+            counts = [int(out.counts[i]) for i in range(out.n_counts)]
+            detail = f"work-items of group {tr.group_of_key(out.group_key)} hit differing barrier counts {counts}"
+        return (int(out.event_index), out.rule.decode(), detail)
+    finally:
+        _put_ctx(ctx)
+
+
 def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
     """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace."""
     kind = tr.kind
@@ -281,6 +339,18 @@ def consume(events: Iterable | ColumnarTrace, *, max_entries: int | None = None,
     violation = None
     if isinstance(events, ColumnarTrace):
         tr = events
+        if not tr.validated:  # columns from an untrusted producer: StreamChecker on the device
+            if device is None:
+                kind = tr.kind
+                device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
+            tr = _device_columns(tr, device)
+            violation = validate_columnar(tr, device)
+            if violation is not None and violation[2] != "stream has no kernel_end":
+                # consume() stops before the violating event; finish()'s rule sees every event
+                index = violation[0]
+                prefix = ColumnarTrace(tr.kind[:index], tr.payload[:index], tr.kernel_name, tr.invocation,
+                                       tr.global_size, tr.local_size, tr.opcodes, tr.extra_groups, None)
+                tr = prefix if index else None
     else:
         from .walker import encode_events
 

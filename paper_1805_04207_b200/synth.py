@@ -65,7 +65,7 @@ def shard_range(cfg: int, work_items: int, rank: int, world: int) -> tuple[int, 
 def _columnar(cfg: int, work_items: int, kind, payload, ti) -> ColumnarTrace:
     lv = LOCAL[cfg]
     return ColumnarTrace(kind, payload, NAMES[cfg], 0, (work_items, 1, 1), (lv, 1, 1), list(OPCODES[cfg]), [],
-                         (ti.addr_min, ti.addr_max, ti.addr_and, ti.addr_or))
+                         (ti.addr_min, ti.addr_max, ti.addr_and, ti.addr_or), validated=True)
 
 
 def device_trace(cfg: int, work_items: int | None = None, seed: int = DEFAULT_SEED, device: int = 0,
@@ -193,4 +193,5 @@ def python_trace(cfg: int, work_items: int, seed: int = DEFAULT_SEED) -> Columna
     if mem.any():
         a = payload[mem]
         stats = (int(a.min()), int(a.max()), 0, (1 << 64) - 4)
-    return ColumnarTrace(kind, payload, NAMES[cfg], 0, (W, 1, 1), (LV, 1, 1), list(OPCODES[cfg]), [], stats)
+    return ColumnarTrace(kind, payload, NAMES[cfg], 0, (W, 1, 1), (LV, 1, 1), list(OPCODES[cfg]), [], stats,
+                         validated=True)

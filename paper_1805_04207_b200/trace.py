@@ -161,6 +161,9 @@ class ColumnarTrace:
     opcodes: list[str] = field(default_factory=list)
     extra_groups: list[Vec3] = field(default_factory=list)
     addr_stats: tuple[int, int, int, int] | None = None
+    # True when the producer guarantees a valid stream (native walker, .aiwctrace
+    # loader, synthetic generators, merges of such); consume() validates the rest
+    validated: bool = False
 
     @property
     def n_events(self) -> int:
@@ -192,7 +195,7 @@ class ColumnarTrace:
             return a.cpu().numpy()
         return ColumnarTrace(host(self.kind), host(self.payload), self.kernel_name, self.invocation,
                              tuple(self.global_size), tuple(self.local_size), list(self.opcodes),
-                             list(self.extra_groups), self.addr_stats)
+                             list(self.extra_groups), self.addr_stats, self.validated)
 
     def iter_events(self):
         """Decode back to TraceEvent objects (debugging / CPU baselines)."""

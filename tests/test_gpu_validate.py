@@ -1,0 +1,114 @@
+"""Device stream validation of columnar traces (aiwc_validate) against the
+collect-all StreamChecker restatement (validate_stream, itself pinned to the
+reference by test_validation.py) on the same decoded events: golden traces
+mutated at random in the columnar layout (events dropped, duplicated, swapped,
+local ids / group keys / kinds changed) must give the same first violation --
+index, rule and detail text -- and consume() must raise it as InvalidStream."""
+
+import random
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+STRUCT = [0x10, 0x90, 0x30, 0xB0, 0x40, 0xC0, 0x20, 0xA0]
+
+
+def _traces():
+    return [(c["name"], t) for c, t in golden_cases() if t is not None and "error" not in c and t.n_events < 20000]
+
+
+def _mutate(tr, rng):
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    k = np.array(tr.kind, dtype=np.uint8).copy()
+    p = np.array(tr.payload, dtype=np.uint64).copy()
+    for _ in range(rng.randint(1, 3)):
+        n = len(k)
+        i = rng.randrange(n)
+        op = rng.choice(["drop", "dup", "swap", "lid", "key", "kind"])
+        if op == "drop":
+            k, p = np.delete(k, i), np.delete(p, i)
+        elif op == "dup":
+            k, p = np.insert(k, i, k[i]), np.insert(p, i, p[i])
+        elif op == "swap" and i + 1 < n:
+            k[[i, i + 1]] = k[[i + 1, i]]
+            p[[i, i + 1]] = p[[i + 1, i]]
+        elif op == "lid":
+            j = np.flatnonzero((k == 0x30) | (k == 0xB0) | (k == 0x10))
+            if j.size:
+                q = rng.choice(j.tolist())
+                p[q] = np.uint64(rng.randrange(int(np.prod(tr.local_size)) + 2))
+        elif op == "key":
+            j = np.flatnonzero((k == 0x40) | (k == 0xC0))
+            if j.size:
+                q = rng.choice(j.tolist())
+                grid = int(np.prod([-(-tr.global_size[d] // tr.local_size[d]) for d in range(3)]))
+                p[q] = np.uint64(rng.randrange(grid + len(tr.extra_groups)))
+        elif op == "kind":  # a representable event of another kind (payload in its range)
+            k[i] = rng.choice(STRUCT + [0x01])
+            if k[i] == 0x01:
+                p[i] = np.uint64(0 << 32 | 1)
+            elif k[i] in (0x40, 0xC0):
+                grid = int(np.prod([-(-tr.global_size[d] // tr.local_size[d]) for d in range(3)]))
+                p[i] = np.uint64(rng.randrange(grid + len(tr.extra_groups)))
+            elif k[i] in (0x10, 0x30, 0xB0):
+                p[i] = np.uint64(rng.randrange(int(np.prod(tr.local_size))))
+            else:
+                p[i] = np.uint64(0)
+    return ColumnarTrace(k, p, tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
+                         tr.extra_groups)
+
+
+def _expected(tr):
+    from paper_1805_04207_b200.trace import validate_stream
+
+    v = validate_stream(tr.iter_events()).violations
+    return tuple(v[0]) if v else None
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_device_first_violation_matches_checker(seed):
+    from paper_1805_04207_b200.metrics import validate_columnar
+
+    rng = random.Random(seed)
+    traces = _traces()
+    checked = 0
+    for _ in range(40):
+        name, tr = rng.choice(traces)
+        if len(tr.opcodes) == 0:
+            continue
+        mt = _mutate(tr, rng)
+        want = _expected(mt)
+        got = validate_columnar(mt, 0)
+        assert got == want, (name, seed, got, want)
+        checked += 1
+    assert checked
+
+
+def test_valid_golden_traces_pass():
+    from paper_1805_04207_b200.metrics import validate_columnar
+
+    for name, tr in _traces():
+        assert validate_columnar(tr, 0) is None, name
+
+
+def test_consume_raises_for_untrusted_columns():
+    from paper_1805_04207_b200 import InvalidStream, consume
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    name, tr = [x for x in _traces() if x[0] == "wavefront_big"][0]
+    k = np.array(tr.kind).copy()
+    p = np.array(tr.payload).copy()
+    i = int(np.flatnonzero(k == 0x10)[3])  # drop a wi_end: the group ends with an unfinished work-item
+    bad = ColumnarTrace(np.delete(k, i), np.delete(p, i), tr.kernel_name, tr.invocation, tr.global_size, tr.local_size,
+                        tr.opcodes, tr.extra_groups)
+    want = _expected(bad)
+    with pytest.raises(InvalidStream) as ei:
+        consume(bad, max_entries=1 << 40)
+    assert (ei.value.event_index, ei.value.rule) == want[:2]
+    assert str(ei.value).endswith(f"({want[2]})")
