@@ -119,6 +119,7 @@ struct aiwc_ctx {
   Buf part_entries, part_cursor, mp_state, mp_tab, mp_partials, mp_ovf;
   // stream validation
   Buf v_state, v_tiles, v_scan, v_spos, v_spay, v_sgap, v_gstart, v_recs, v_counts;
+  Buf v_srange, v_fwge, v_keys, v_keys_tmp, v_hist, v_prevk, v_unf, v_bmm;
   std::vector<uint64_t> mp_hist0, mp_big;
 };
 
@@ -188,7 +189,8 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
                  &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
                  &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres,
                  &ctx->v_state, &ctx->v_tiles, &ctx->v_scan, &ctx->v_spos, &ctx->v_spay, &ctx->v_sgap,
-                 &ctx->v_gstart, &ctx->v_recs, &ctx->v_counts};
+                 &ctx->v_gstart, &ctx->v_recs, &ctx->v_counts, &ctx->v_srange, &ctx->v_fwge, &ctx->v_keys,
+                 &ctx->v_keys_tmp, &ctx->v_hist, &ctx->v_prevk, &ctx->v_unf, &ctx->v_bmm};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (ctx->h_state) cudaFreeHost(ctx->h_state);
@@ -941,7 +943,7 @@ namespace {
 
 __global__ void v_init_kernel(ValidateState* vs) {
   vs->first_ke = ~0ull; vs->winner = ~0ull;
-  vs->n_struct = 0; vs->n_groups = 0; vs->bad_kind = 0; vs->counts_used = 0; vs->kb0 = 0;
+  vs->n_struct = 0; vs->n_groups = 0; vs->bad_kind = 0; vs->counts_used = 0; vs->kb0 = 0; vs->dp = 0;
 }
 
 std::string tup(const int64_t v[3]) {
@@ -1001,12 +1003,24 @@ extern "C" int aiwc_validate(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t*
   CK(grow(ctx->v_spay, std::max<uint64_t>(S, 1) * 8));
   CK(grow(ctx->v_sgap, std::max<uint64_t>(S, 1) * 8));
   CK(grow(ctx->v_gstart, std::max<uint64_t>(NG, 1) * 4));
-  CK(grow(ctx->v_recs, (NG + 1) * sizeof(ValidateRecord)));
+  CK(grow(ctx->v_recs, (NG + 3) * sizeof(ValidateRecord)));
+  CK(grow(ctx->v_srange, std::max<uint64_t>(S, 1) * 4));
+  CK(grow(ctx->v_fwge, (NG + 1) * 4));
+  CK(grow(ctx->v_keys, std::max<uint64_t>(S, 1) * 8));
+  CK(grow(ctx->v_keys_tmp, std::max<uint64_t>(S, 1) * 8));
+  CK(grow(ctx->v_hist, radix_hist_bytes(std::max<uint64_t>(S, 1))));
+  CK(grow(ctx->v_prevk, std::max<uint64_t>(S, 1)));
+  CK(grow(ctx->v_unf, (NG + 1) * 8));
+  CK(grow(ctx->v_bmm, (NG + 1) * 8));
   const uint32_t counts_cap = 1u << 20;
   CK(grow(ctx->v_counts, counts_cap * 4));
   b.spos = P<uint64_t>(ctx->v_spos); b.spay = P<uint64_t>(ctx->v_spay); b.sgap = P<uint64_t>(ctx->v_sgap);
   b.gstart = P<uint32_t>(ctx->v_gstart); b.recs = P<ValidateRecord>(ctx->v_recs);
   b.counts = P<uint32_t>(ctx->v_counts); b.counts_cap = counts_cap;
+  b.srange = P<uint32_t>(ctx->v_srange); b.first_wge = P<uint32_t>(ctx->v_fwge);
+  b.keys = P<uint64_t>(ctx->v_keys); b.keys_tmp = P<uint64_t>(ctx->v_keys_tmp); b.sort_hist = P<uint32_t>(ctx->v_hist);
+  b.prevk = P<uint8_t>(ctx->v_prevk); b.unf = P<unsigned long long>(ctx->v_unf);
+  b.bmin = P<uint32_t>(ctx->v_bmm); b.bmax = b.bmin + (NG + 1);
   const uint32_t n_ctas = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((NG + 1 + 3) / 4, (uint64_t)ctx->n_sms * 8));
   validate_phase2(kind, payload, n, (uint32_t)lv, vs, b, S, NG, n_ctas, s, &kernels);
   CK(cudaGetLastError());
@@ -1017,8 +1031,9 @@ extern "C" int aiwc_validate(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t*
   ValidateRecord rec{};
   std::vector<uint32_t> counts;
   if (hv.winner != ~0ull) {
-    const uint64_t r = hv.winner & 0xFFFFFFFFull;
-    CK(cudaMemcpy(&rec, P<ValidateRecord>(ctx->v_recs) + r, sizeof rec, cudaMemcpyDeviceToHost));
+    const uint64_t low = hv.winner & 0xFFFFFFFFull;
+    const uint64_t slot = low == 0xFFFFFFFFull ? NG + 2 : hv.dp ? NG + 1 : low;
+    CK(cudaMemcpy(&rec, P<ValidateRecord>(ctx->v_recs) + slot, sizeof rec, cudaMemcpyDeviceToHost));
     code = rec.code;
     if (rec.n_counts) {
       counts.resize(rec.n_counts);

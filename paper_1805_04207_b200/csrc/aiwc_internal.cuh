@@ -117,7 +117,7 @@ struct ValidateState {
   unsigned long long winner;     // min(index << 32 | range) over flagged ranges (~0: none)
   uint32_t n_struct, n_groups;   // structural events, work-group begins
   uint32_t bad_kind, counts_used;
-  uint32_t kb0, pad;             // event 0 is the kernel_begin (the header every later range assumes)
+  uint32_t kb0, dp;              // event 0 is the kernel_begin; the data-parallel checker ran
 };
 struct ValidateRecord {
   uint64_t index;
@@ -129,7 +129,13 @@ struct ValidateBufs {
   uint32_t *tile_s, *tile_g, *scan_scratch;
   uint64_t *spos, *spay, *sgap;
   uint32_t* gstart;
-  ValidateRecord* recs;
+  uint32_t *srange, *first_wge;   // per entry: its range; per range: first wg_end entry
+  uint64_t *keys, *keys_tmp;      // (range, local id, entry) sort keys
+  uint32_t* sort_hist;
+  uint8_t* prevk;
+  unsigned long long* unf;
+  uint32_t *bmin, *bmax;
+  ValidateRecord* recs;           // [0, NG]: replay ranges; NG + 1: data-parallel winner; NG + 2: index-0 event
   uint32_t* counts;
   uint32_t counts_cap;
 };
