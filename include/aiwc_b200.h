@@ -65,6 +65,7 @@ typedef struct aiwc_ctx aiwc_ctx;
 /* aiwc_opts.flags */
 #define AIWC_OPT_NO_CONSERVATION 1u /* skip finalize's conservation checks (caller does them) */
 #define AIWC_OPT_TIMING 2u          /* record CUDA events around each phase (aiwc_result.phase_ms) */
+#define AIWC_OPT_VALIDATE_REPLAY 8u /* aiwc_validate: always use the per-work-group replay checker (testing) */
 
 /* aiwc_result.phase_ms indices */
 enum { AIWC_PH_PASS1 = 0, AIWC_PH_INGEST = 1, AIWC_PH_MEMORY = 2, AIWC_PH_BRANCH = 3, AIWC_PH_INGEST_TOTAL = 4,

@@ -63,6 +63,7 @@ class Result(ctypes.Structure):
 
 OPT_TIMING = 2
 OPT_SHARD = 4
+OPT_VALIDATE_REPLAY = 8
 PHASES = ("pass1", "ingest", "memory", "branch", "ingest_total", "finalize_total")
 
 

@@ -1022,7 +1022,8 @@ extern "C" int aiwc_validate(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t*
   b.prevk = P<uint8_t>(ctx->v_prevk); b.unf = P<unsigned long long>(ctx->v_unf);
   b.bmin = P<uint32_t>(ctx->v_bmm); b.bmax = b.bmin + (NG + 1);
   const uint32_t n_ctas = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((NG + 1 + 3) / 4, (uint64_t)ctx->n_sms * 8));
-  validate_phase2(kind, payload, n, (uint32_t)lv, vs, b, S, NG, n_ctas, s, &kernels);
+  validate_phase2(kind, payload, n, (uint32_t)lv, vs, b, S, NG, n_ctas, (ctx->opts.flags & AIWC_OPT_VALIDATE_REPLAY) != 0,
+                  s, &kernels);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(&hv, vs, sizeof hv, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

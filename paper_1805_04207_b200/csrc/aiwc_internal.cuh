@@ -144,7 +144,8 @@ constexpr int VALIDATE_TILE = 4096;
 void validate_phase1(const uint8_t* kind, uint64_t n, ValidateState* vs, const ValidateBufs& b, cudaStream_t s,
                      int* kernels);
 void validate_phase2(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t lv, ValidateState* vs,
-                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, cudaStream_t s, int* kernels);
+                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, bool force_replay,
+                     cudaStream_t s, int* kernels);
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
 cudaError_t set_smem_attr(const void* kernel, int bytes);

@@ -480,7 +480,8 @@ __global__ void vs_set_dp(ValidateState* vs) { vs->dp = 1; }
 }  // namespace
 
 void validate_phase2(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t lv, ValidateState* vs,
-                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, cudaStream_t s, int* kernels) {
+                     const ValidateBufs& b, uint64_t S, uint64_t NG, uint32_t n_ctas, bool force_replay,
+                     cudaStream_t s, int* kernels) {
   const uint64_t tiles = (n + VTILE - 1) / VTILE;
   cudaMemsetAsync(b.first_wge, 0xFF, (NG + 1) * 4, s);
   if (tiles) {
@@ -491,7 +492,7 @@ void validate_phase2(const uint8_t* kind, const uint64_t* payload, uint64_t n, u
   v_prefix_kernel<<<1, 1, 0, s>>>(kind, n, vs, b.recs + NG + 2);
   ++*kernels;
   const int lb = bitwidth(lv - 1), rb = bitwidth(NG + 1);
-  if (rb + lb <= 32) {  // data-parallel checker
+  if (rb + lb <= 32 && !force_replay) {  // data-parallel checker
     const unsigned grid = (unsigned)std::min<uint64_t>((S + 255) / 256 + 1, 148ull * 16);
     cudaMemsetAsync(b.prevk, 0xFF, std::max<uint64_t>(S, 1), s);
     cudaMemsetAsync(b.unf, 0xFF, (NG + 1) * 8, s);
