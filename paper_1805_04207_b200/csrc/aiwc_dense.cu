@@ -151,88 +151,97 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
     run_n = 0;
   };
 
-  E cur[K], nxt[K], nx2[K];  // two chunks in flight ahead of the one being folded
-  uint64_t ch = blockIdx.x;
-  if (ch < n_chunks) load(ch, cur);
-  if (ch + gridDim.x < n_chunks) load(ch + gridDim.x, nxt);
-  for (; ch < n_chunks; ch += gridDim.x) {
-    if (ch + 2ull * gridDim.x < n_chunks) load(ch + 2ull * gridDim.x, nx2);
-    bool same = true;
+  // fold one chunk (all lanes, CTA-uniform)
+  auto fold = [&](const E (&cur)[K]) {
+      bool same = true;
 #pragma unroll
-    for (int i = 1; i < K; ++i) same &= cur[i] == cur[0];
-    const E e0 = __shfl_sync(0xffffffffu, cur[0], 0);
-    unsigned long long s;  // sum of the warp's 256 counts (levels 9, 10)
-    if (__all_sync(0xffffffffu, same && cur[0] == e0)) {
-      // ---- warp-uniform chunk: extend the run ----
-      if (e0 != run_e) { flush_run(); run_e = e0; }
-      if (e0) ++run_n;
-      unsigned long long c0;
-      uint32_t r0, w0;
-      decode<E>(e0, c0, r0, w0);
-      s = c0 * 256ull;
-    } else {
-      unsigned long long c[K];
-#pragma unroll
-      for (int i = 0; i < K; ++i) {
-        uint32_t r, w;
-        decode<E>(cur[i], c[i], r, w);
-        ur += r; uw += w; fp += c[i] != 0;
-      }
-      // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
-      bool uni = true;
-#pragma unroll
-      for (int i = 1; i < K; ++i) uni &= c[i] == c[0];
-      if (__all_sync(0xffffffffu, uni)) {
-        X.rec_warp(0, c[0], K, true, 32);
+      for (int i = 1; i < K; ++i) same &= cur[i] == cur[0];
+      const E e0 = __shfl_sync(0xffffffffu, cur[0], 0);
+      unsigned long long s;  // sum of the warp's 256 counts (levels 9, 10)
+      if (__all_sync(0xffffffffu, same && cur[0] == e0)) {
+        // ---- warp-uniform chunk: extend the run ----
+        if (e0 != run_e) { flush_run(); run_e = e0; }
+        if (e0) ++run_n;
+        unsigned long long c0;
+        uint32_t r0, w0;
+        decode<E>(e0, c0, r0, w0);
+        s = c0 * 256ull;
       } else {
-        unsigned long long v = c[0];
-        uint32_t run = 1;
+        unsigned long long c[K];
 #pragma unroll
-        for (int i = 1; i < K; ++i) {
-          if (c[i] == v) { ++run; }
-          else { X.rec(0, v, run); v = c[i]; run = 1; }
+        for (int i = 0; i < K; ++i) {
+          uint32_t r, w;
+          decode<E>(cur[i], c[i], r, w);
+          ur += r; uw += w; fp += c[i] != 0;
         }
-        X.rec(0, v, run);
-      }
-      unsigned long long s1[4], s2[2], s3;
+        // level 0: one warp-wide add when every lane's 8 counts agree, else per-thread runs
+        bool uni = true;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
-      s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
-      s3 = s2[0] + s2[1];
-      if (nlev > 1) {
-        const bool u1 = s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3];
-        if (__all_sync(0xffffffffu, u1)) X.rec_warp(1, s1[0], 4, true, 32);
-        else { X.rec(1, s1[0], 1); X.rec(1, s1[1], 1); X.rec(1, s1[2], 1); X.rec(1, s1[3], 1); }
-      }
-      if (nlev > 2) {
-        if (__all_sync(0xffffffffu, s2[0] == s2[1])) X.rec_warp(2, s2[0], 2, true, 32);
-        else { X.rec(2, s2[0], 1); X.rec(2, s2[1], 1); }
-      }
-      if (nlev > 3) X.rec_warp(3, s3, 1, true, 32);
-      s = s3;
+        for (int i = 1; i < K; ++i) uni &= c[i] == c[0];
+        if (__all_sync(0xffffffffu, uni)) {
+          X.rec_warp(0, c[0], K, true, 32);
+        } else {
+          unsigned long long v = c[0];
+          uint32_t run = 1;
 #pragma unroll
-      for (int j = 4; j <= 8; ++j) {
-        s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
-        if (j < nlev) X.rec_warp(j, s, 1, (lane & ((1 << (j - 3)) - 1)) == 0, 32u >> (j - 3));
-      }
-    }
-    if (nlev > 9) {  // levels 9, 10 need the whole CTA (k < 2 only)
-      if (lane == 0) D.wsum[warp] = s;
-      __syncthreads();
-      if (t == 0) {
-        const unsigned long long g[3] = {D.wsum[0] + D.wsum[1], D.wsum[2] + D.wsum[3],
-                                         D.wsum[0] + D.wsum[1] + D.wsum[2] + D.wsum[3]};
-        for (int q = 0; q < 3; ++q) {
-          const int j = q < 2 ? 9 : 10;
-          if (j >= nlev || g[q] == 0) continue;
-          if (g[q] < (unsigned long long)CBINS) atomicAdd(&hsm[j * CBINS + (uint32_t)g[q]], 1u);
-          else D.part[j][0] += plogp(g[q], m);
+          for (int i = 1; i < K; ++i) {
+            if (c[i] == v) { ++run; }
+            else { X.rec(0, v, run); v = c[i]; run = 1; }
+          }
+          X.rec(0, v, run);
+        }
+        unsigned long long s1[4], s2[2], s3;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) s1[i] = c[2 * i] + c[2 * i + 1];
+        s2[0] = s1[0] + s1[1]; s2[1] = s1[2] + s1[3];
+        s3 = s2[0] + s2[1];
+        if (nlev > 1) {
+          const bool u1 = s1[0] == s1[1] && s1[1] == s1[2] && s1[2] == s1[3];
+          if (__all_sync(0xffffffffu, u1)) X.rec_warp(1, s1[0], 4, true, 32);
+          else { X.rec(1, s1[0], 1); X.rec(1, s1[1], 1); X.rec(1, s1[2], 1); X.rec(1, s1[3], 1); }
+        }
+        if (nlev > 2) {
+          if (__all_sync(0xffffffffu, s2[0] == s2[1])) X.rec_warp(2, s2[0], 2, true, 32);
+          else { X.rec(2, s2[0], 1); X.rec(2, s2[1], 1); }
+        }
+        if (nlev > 3) X.rec_warp(3, s3, 1, true, 32);
+        s = s3;
+#pragma unroll
+        for (int j = 4; j <= 8; ++j) {
+          s += __shfl_xor_sync(0xffffffffu, s, 1 << (j - 4));
+          if (j < nlev) X.rec_warp(j, s, 1, (lane & ((1 << (j - 3)) - 1)) == 0, 32u >> (j - 3));
         }
       }
-      __syncthreads();
-    }
+      if (nlev > 9) {  // levels 9, 10 need the whole CTA (k < 2 only)
+        if (lane == 0) D.wsum[warp] = s;
+        __syncthreads();
+        if (t == 0) {
+          const unsigned long long g[3] = {D.wsum[0] + D.wsum[1], D.wsum[2] + D.wsum[3],
+                                           D.wsum[0] + D.wsum[1] + D.wsum[2] + D.wsum[3]};
+          for (int q = 0; q < 3; ++q) {
+            const int j = q < 2 ? 9 : 10;
+            if (j >= nlev || g[q] == 0) continue;
+            if (g[q] < (unsigned long long)CBINS) atomicAdd(&hsm[j * CBINS + (uint32_t)g[q]], 1u);
+            else D.part[j][0] += plogp(g[q], m);
+          }
+        }
+        __syncthreads();
+      }
+  };
+
+  // four chunks in flight: fold two per iteration while the next two load
+  E c0[K], c1[K], n0[K], n1[K];
+  const uint64_t g = gridDim.x;
+  uint64_t ch = blockIdx.x;
+  if (ch < n_chunks) load(ch, c0);
+  if (ch + g < n_chunks) load(ch + g, c1);
+  for (; ch < n_chunks; ch += 2 * g) {
+    if (ch + 2 * g < n_chunks) load(ch + 2 * g, n0);
+    if (ch + 3 * g < n_chunks) load(ch + 3 * g, n1);
+    fold(c0);
+    if (ch + g < n_chunks) fold(c1);
 #pragma unroll
-    for (int i = 0; i < K; ++i) { cur[i] = nxt[i]; nxt[i] = nx2[i]; }
+    for (int i = 0; i < K; ++i) { c0[i] = n0[i]; c1[i] = n1[i]; }
   }
   flush_run();
   __syncthreads();

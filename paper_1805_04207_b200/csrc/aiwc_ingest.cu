@@ -79,7 +79,8 @@ __device__ __forceinline__ long long last_event(long long e0, uint32_t m) {
 // group, variant); each class is then one masked popcount per packed word.
 struct KindCounts {
   uint32_t instr = 0, rd = 0, wr = 0, br = 0, wgb = 0, bres = 0;
-  __device__ __forceinline__ void add(const uint32_t w[4]) {
+  // gm: the chunk's work-group-begin mask (chunk_wgb), one bit per wg_begin
+  __device__ __forceinline__ void add(const uint32_t w[4], uint32_t gm) {
     const uint32_t L0 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
     const uint32_t L1 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
     const uint32_t H0 = ((w[0] >> 4) & 0x0F0F0F0Fu) | (w[1] & 0xF0F0F0F0u);
@@ -88,7 +89,7 @@ struct KindCounts {
     rd += __popc(L0 & 0x22222222u) + __popc(L1 & 0x22222222u);
     wr += __popc(L0 & 0x44444444u) + __popc(L1 & 0x44444444u);
     br += __popc(L0 & 0x88888888u) + __popc(L1 & 0x88888888u);
-    wgb += __popc(H0 & ~(H0 >> 1) & 0x44444444u) + __popc(H1 & ~(H1 >> 1) & 0x44444444u);
+    wgb += __popc(gm);
     bres |= (H0 & (H0 >> 3)) | (H1 & (H1 >> 3));  // boundary with the variant bit: barrier / resume
   }
 };
@@ -114,9 +115,9 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
     for (int u = 0; u < U; ++u) load_kind16(kind, base + 16 * u, re, w[u]);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      kc.add(w[u]);
       const uint64_t e0 = base + 16 * u;
       const uint32_t bm = chunk_bnd(w[u]), gm = chunk_wgb(w[u]);
+      kc.add(w[u], gm);
       if (bm) { lb_e0 = (long long)e0; lb_m = bm; }
       if (gm) { lw_e0 = (long long)e0; lw_m = gm; }
       if (with_stats) {
