@@ -84,8 +84,14 @@ typedef struct {
   uint32_t local_volume;      /* product of the launch's local size                   */
   uint32_t n_opcodes;         /* opcode dictionary size                               */
   uint32_t has_addr_stats;    /* 1 when addr_* below describe every memory address    */
-  uint32_t reserved;
+  uint32_t has_counts;        /* 1 when the class totals below are declared           */
   uint64_t addr_min, addr_max, addr_and, addr_or;
+  /* Declared class totals (producers that know them: walkers, generators).  With
+   * them and declared address statistics, aiwc_ingest runs in ONE pass over the
+   * trace (tile carry-ins by decoupled look-back) instead of two; the totals are
+   * verified on the device (AIWC_ERR_ARGUMENT when they differ). */
+  uint64_t n_instr, n_reads, n_writes, n_branches, n_groups;
+  uint32_t any_barrier_or_resume, reserved;
 } aiwc_trace_info;
 
 typedef struct {

@@ -30,9 +30,12 @@ class Opts(ctypes.Structure):
 
 class TraceInfo(ctypes.Structure):
     _fields_ = [("n_events", ctypes.c_uint64), ("local_volume", ctypes.c_uint32), ("n_opcodes", ctypes.c_uint32),
-                ("has_addr_stats", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("has_addr_stats", ctypes.c_uint32), ("has_counts", ctypes.c_uint32),
                 ("addr_min", ctypes.c_uint64), ("addr_max", ctypes.c_uint64),
-                ("addr_and", ctypes.c_uint64), ("addr_or", ctypes.c_uint64)]
+                ("addr_and", ctypes.c_uint64), ("addr_or", ctypes.c_uint64),
+                ("n_instr", ctypes.c_uint64), ("n_reads", ctypes.c_uint64), ("n_writes", ctypes.c_uint64),
+                ("n_branches", ctypes.c_uint64), ("n_groups", ctypes.c_uint64),
+                ("any_barrier_or_resume", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 class Dist(ctypes.Structure):

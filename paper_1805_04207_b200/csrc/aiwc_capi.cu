@@ -104,6 +104,13 @@ struct aiwc_ctx {
   cudaStream_t aux = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   size_t pre_zeroed = 0;
+  size_t dtab_clean = 0, dtab_used = 0;  // bytes of the dense table cleared after the last finalize / used now
+  bool one_pass = false;  // declared class totals: no round trip between pass 1 and the ingest
+  // last encoded TMA descriptors (re-used while the columns stay the same)
+  const void* tm_kind = nullptr;
+  const void* tm_payload = nullptr;
+  uint64_t tm_rows = 0;
+  CUtensorMap tm_k{}, tm_p{};
   bool timing = false;
   uint32_t marked = 0;  // phases whose end event was recorded for the current trace
   void mark(int phase, int end, cudaStream_t s) {
@@ -215,8 +222,27 @@ extern "C" int aiwc_last_error(const aiwc_ctx* ctx, aiwc_error* e) {
   return AIWC_OK;
 }
 
+static int encode_maps_uncached(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, uint64_t rows,
+                                CUtensorMap* km, CUtensorMap* pm);
+
 static int encode_maps(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, uint64_t rows, CUtensorMap* km,
                        CUtensorMap* pm) {
+  if (ctx->tm_kind == kind && ctx->tm_payload == payload && ctx->tm_rows == rows) {
+    *km = ctx->tm_k; *pm = ctx->tm_p;
+    return AIWC_OK;
+  }
+  const int rc = encode_maps_uncached(ctx, kind, payload, rows, km, pm);
+  if (rc == AIWC_OK) {
+    ctx->tm_kind = kind; ctx->tm_payload = payload; ctx->tm_rows = rows;
+    ctx->tm_k = *km; ctx->tm_p = *pm;
+  } else {
+    ctx->tm_kind = ctx->tm_payload = nullptr;
+  }
+  return rc;
+}
+
+static int encode_maps_uncached(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, uint64_t rows,
+                                CUtensorMap* km, CUtensorMap* pm) {
   memset(km, 0, sizeof *km);
   memset(pm, 0, sizeof *pm);
   if (rows == 0) return AIWC_OK;
@@ -256,16 +282,18 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   ctx->mark(AIWC_PH_INGEST_TOTAL, 0, s);
   DevState* st = P<DevState>(ctx->dev_state);
   const uint64_t n_tiles = (n + TILE - 1) / TILE;
+  const bool with_stats = !info->has_addr_stats;
+  // Declared class totals (and address statistics, or no memory events) fix every
+  // host decision up front: pass 1 and the ingest are queued back to back with
+  // no device->host round trip in between; pass 1's totals are checked against
+  // the declaration at finalize.
+  const bool declared = n && info->has_counts && (!with_stats || info->n_reads + info->n_writes == 0);
+  ctx->one_pass = declared;
   uint32_t G = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(n_tiles, 1), (uint64_t)ctx->n_sms * CTAS_PER_SM);
   uint32_t tpc = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + G - 1) / G);
   G = (uint32_t)((std::max<uint64_t>(n_tiles, 1) + tpc - 1) / tpc);
-  ctx->n_ranges = G;
-  ctx->tiles_per_cta = tpc;
-  const uint32_t n_sub = G * P1_SUB;
-  CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
-  CK(grow(ctx->wpres, (size_t)G * sizeof(uint32_t)));
   init_trace_kernel<<<64, 256, 0, s>>>(st, P<unsigned long long>(ctx->wcount), P<unsigned long long>(ctx->wfirst),
-                                       P<uint32_t>(ctx->wpres), G);
+                                       nullptr, 0);
   ctx->kernels += 1;
   // opcode counters live in DevState (part of finalize's one read) unless the dictionary is large
   const bool opc_big = info->n_opcodes > (uint32_t)MAX_SMALL_LIST;
@@ -273,7 +301,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     CK(grow(ctx->opc, (size_t)info->n_opcodes * 8));
     CK(cudaMemsetAsync(ctx->opc.p, 0, (size_t)info->n_opcodes * 8, s));
   }
-  // tensor maps depend only on the columns: encode them before pass 1's round trip
+  // tensor maps depend only on the columns: encode them before any round trip
   CUtensorMap km, pm;
   const uint64_t rows = n / 16;
   if (n) {
@@ -281,11 +309,9 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     if (rc) return rc;
   }
 
-  // ---- pass 1: range summaries ----
-  const bool with_stats = !info->has_addr_stats;
-  // Declared address statistics fix the key map before pass 1: clear a u32
-  // table of that size on the side stream meanwhile.  Bounded waste when the
-  // trace later takes another path: the table is <= 4 keys per event + 2^20.
+  // Declared address statistics fix the key map up front: clear a u32 table of
+  // that size on the side stream (unless the previous finalize left it clean).
+  // Bounded waste when the trace later takes another path: <= 4 keys / event + 2^20.
   ctx->pre_zeroed = 0;
   if (n && !with_stats && info->addr_min <= info->addr_max && !(ctx->opts.flags & AIWC_OPT_SHARD)) {
     const uint64_t b0 = info->addr_min & ~1023ull, vary = info->addr_and ^ info->addr_or;
@@ -293,14 +319,26 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     const uint64_t sk = (info->addr_max - b0) >> k0;
     if (sk < (1ull << 40) && (sk + 1) * 4 <= ctx->opts.dense_budget_bytes && sk + 1 <= 4 * n + (1ull << 20)) {
       const size_t tb = (size_t)(sk + 1) * 4;
-      CK(grow(ctx->dtab, tb));
-      CK(cudaEventRecord(ctx->fork_ev, s));
-      CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
-      CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, ctx->aux));
-      CK(cudaEventRecord(ctx->join_ev, ctx->aux));
-      ctx->pre_zeroed = tb;
+      if (ctx->dtab_clean >= tb && ctx->dtab.cap >= tb) {
+        ctx->pre_zeroed = ctx->dtab_clean;  // cleared after the previous trace (join_ev)
+      } else {
+        if (ctx->dtab.cap < tb) {
+          CK(cudaStreamSynchronize(ctx->aux));
+          CK(grow(ctx->dtab, tb));
+        }
+        CK(cudaEventRecord(ctx->fork_ev, s));
+        CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
+        CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, ctx->aux));
+        CK(cudaEventRecord(ctx->join_ev, ctx->aux));
+        ctx->pre_zeroed = tb;
+      }
     }
   }
+  ctx->dtab_clean = 0;
+
+  // ---- pass 1: range summaries ----
+  const uint32_t n_sub = G * P1_SUB;
+  CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
   if (n) {
     ctx->mark(AIWC_PH_PASS1, 0, s);
     launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s);
@@ -310,12 +348,15 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   } else {
     CK(cudaMemsetAsync(ctx->ranges.p, 0, (size_t)n_sub * sizeof(RangeSum), s));
   }
-  // addr_min .. addr_or and the pass-1 totals are contiguous: one 80-byte read
-  CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 10 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                     s));
-  ctx->d2h += 10 * sizeof(unsigned long long);
-  CK(cudaStreamSynchronize(s));
-  {
+  if (declared) {
+    ctx->n_instr = info->n_instr; ctx->n_rd = info->n_reads; ctx->n_wr = info->n_writes;
+    ctx->n_br = info->n_branches; ctx->n_wgb = info->n_groups; ctx->n_bres = info->any_barrier_or_resume;
+  } else {
+    // addr_min .. addr_or and the pass-1 totals are contiguous: one 80-byte read
+    CK(cudaMemcpyAsync(&ctx->h_state->addr_min, &st->addr_min, 10 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, s));
+    ctx->d2h += 10 * sizeof(unsigned long long);
+    CK(cudaStreamSynchronize(s));
     const unsigned long long* tt = ctx->h_state->p1_tot;
     ctx->n_instr = tt[0]; ctx->n_rd = tt[1]; ctx->n_wr = tt[2]; ctx->n_br = tt[3]; ctx->n_wgb = tt[4];
     ctx->n_bres = tt[5];
@@ -356,6 +397,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     // a shard keeps its addresses compacted: they are exchanged with the key owners
     ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
   }
+  const bool stage = !ctx->dense || ctx->n_br > 0;
 
   // ---- buffers ----
   // an ITB / IPT sample >= HBINS spans >= HBINS distinct instructions: that bounds both overflow lists
@@ -376,14 +418,20 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
         CK(grow(ctx->dtab, tb));
         CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, s));
       }
+      ctx->dtab_used = tb;
     } else {
       CK(grow(ctx->rd, std::max<uint64_t>(ctx->n_rd, 1) * 8));
       CK(grow(ctx->wr, std::max<uint64_t>(ctx->n_wr, 1) * 8));
     }
     CK(grow(ctx->lvl0_ovf, (M / CBINS + 2) * 8));
   }
-
   if (ctx->pre_zeroed && !ctx->dense) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+
+  ctx->n_ranges = G;
+  ctx->tiles_per_cta = tpc;
+  const uint32_t pres_blocks = (tpc + PRES_TILES - 1) / PRES_TILES;
+  CK(grow(ctx->wpres, (size_t)G * pres_blocks * 4));
+  CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * pres_blocks * 4, s));
 
   // ---- main ingest pass ----
   if (n) {
@@ -394,17 +442,19 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.opc_counts = opc_big ? P<unsigned long long>(ctx->opc) : st->opc_small;
     a.width_count = P<unsigned long long>(ctx->wcount); a.width_first = P<unsigned long long>(ctx->wfirst);
     a.width_presence = P<uint32_t>(ctx->wpres);
+    a.pres_blocks = pres_blocks;
     a.itb_ovf = P<uint32_t>(ctx->itb_ovf); a.ipt_ovf = P<uint32_t>(ctx->ipt_ovf);
     a.ipt_tab = ctx->ipt_tab_len ? P<unsigned long long>(ctx->ipt_tab) : nullptr; a.ipt_tab_len = ctx->ipt_tab_len;
     a.am = ctx->am;
     a.dense = ctx->dense ? ctx->dtab.p : nullptr;
     a.dense32 = ctx->dense32;
-    a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);    ctx->mark(AIWC_PH_INGEST, 0, s);
-    CK(launch_ingest(a, km, pm, G, ctx->dense, !ctx->dense || ctx->n_br > 0, s));
+    a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
+    ctx->mark(AIWC_PH_INGEST, 0, s);
+    CK(launch_ingest(a, km, pm, G, ctx->dense, stage, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
     ctx->kernels += 1;
     if (ctx->n_instr) {  // first index of each width 1..16 (the columns are only ours until here)
-      launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G, (uint64_t)tpc * TILE,
+      launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G, pres_blocks, tpc, false,
                          P<unsigned long long>(ctx->wfirst), s);
       ctx->kernels += 1;
     }
@@ -514,6 +564,12 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
       const uint32_t nct = (uint32_t)std::min<uint64_t>(chunks, ctx->n_parts);
       launch_dense_stats(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, ctx->am.k, M, st,
                          P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s);
+      // the table is clean again for the next trace: clear it on the side stream now
+      CK(cudaEventRecord(ctx->fork_ev, s));
+      CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
+      CK(cudaMemsetAsync(ctx->dtab.p, 0, ctx->dtab_used, ctx->aux));
+      CK(cudaEventRecord(ctx->join_ev, ctx->aux));
+      ctx->dtab_clean = ctx->dtab_used;
       launch_entropy_finish(st, P<double>(ctx->partials), nct, M, ctx->am.k, s);
       ctx->kernels += 2;
     } else {
@@ -547,6 +603,13 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     CK(cudaStreamSynchronize(s));
   }
   DevState& h = *ctx->h_state;
+  if (ctx->one_pass) {  // the declared class totals against what the pass counted
+    const aiwc_trace_info& in = ctx->info;
+    const bool same = h.p1_tot[0] == in.n_instr && h.p1_tot[1] == in.n_reads && h.p1_tot[2] == in.n_writes &&
+                      h.p1_tot[3] == in.n_branches && h.p1_tot[4] == in.n_groups &&
+                      (h.p1_tot[5] != 0) == (in.any_barrier_or_resume != 0);
+    if (!same) return fail(ctx, AIWC_ERR_ARGUMENT, "declared class counts differ from the trace");
+  }
   if (h.flags) {
     char m[160];
     const char* what = (h.flags & F_ADDR_HINT) ? "memory address outside the declared address statistics"

@@ -226,7 +226,7 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
 // main ingest pass
 // ---------------------------------------------------------------------------
 constexpr int BND_CAP = 256;  // segment closes buffered per tile (overflow is processed inline)
-constexpr uint32_t ACC_FLUSH_TILES = 65535 / EPT;  // 16-bit register counters take <= EPT per tile
+constexpr uint32_t ACC_FLUSH_TILES = (65535 / EPT / PRES_TILES) * PRES_TILES;  // 16-bit fields take <= EPT per tile
 constexpr int NWARP = TPB / 32;
 
 // TMA stages (dynamic smem, 1024 B aligned for the 128 B swizzle)
@@ -243,7 +243,6 @@ struct LocalSmem {
   uint32_t itb_h[HBINS];
   uint32_t ipt_h[HBINS];
   uint4 closes[BND_CAP];       // (segment length, local id, gseq | barrier << 31 | resumed << 30)
-  uint32_t wpres;              // widths 1..16 seen in this CTA's range (bit w - 1)
   uint4 wtot[NWARP];           // per-warp inclusive totals of the packed scan values
   uint32_t vpos[TPB];
   uint32_t nc[5];
@@ -303,13 +302,12 @@ __device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint
 // add the per-thread packed bin counters (16-bit fields, bin 2i low / 2i + 1 high)
 // to the global opcode / width counters; warp-converged
 __device__ __forceinline__ void flush_counts(uint32_t (&oacc)[8], uint32_t (&wacc)[8], const IngestArgs& a, int lane,
-                                             uint32_t& pres, unsigned long long& flags) {
+                                             unsigned long long& flags) {
 #pragma unroll
   for (int v = 0; v < 16; ++v) {
     uint32_t co = (oacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
     uint32_t cw = (wacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
     const uint32_t wv = v ? (uint32_t)v : 16u;  // width bin v holds width v, bin 0 width 16
-    if (cw) pres |= 1u << (wv - 1);
     co = warp_sum(co);
     cw = warp_sum(cw);
     if (lane == 0) {
@@ -344,16 +342,16 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   const uint64_t tile_begin = (uint64_t)blockIdx.x * a.tiles_per_cta;
   if (tile_begin >= n_tiles_total) return;
   const uint32_t my_tiles = (uint32_t)min((uint64_t)a.tiles_per_cta, n_tiles_total - tile_begin);
+  auto tile_of = [&](uint32_t it) -> uint64_t { return tile_begin + it; };
   DevState* st = a.st;
 
   // ---- prologue: smem init + TMA ring fill ----
   for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
-  if (t == 0) L.wpres = 0;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     fence_barrier_init();
     for (uint32_t it = 0; it < (uint32_t)STAGES && it < my_tiles; ++it) {
-      const uint64_t row0 = (tile_begin + it) * (TILE / 16);
+      const uint64_t row0 = tile_of(it) * (TILE / 16);
       if (row0 < a.tma_rows) {
         mbar_expect_tx(&S.bar[it], TILE * 9);
         tma_load_2d(S.kind[it], &kmap, 0, (int)row0, &S.bar[it]);
@@ -363,7 +361,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   }
 
   // ---- carry-in at the start of this CTA's range: combine the sub-ranges before it ----
-  uint32_t cseg, clid = 0, cbyres = 0, cgseq = 0, cgkey = 0;
+  uint32_t cseg = 0, clid = 0, cbyres = 0, cgseq = 0, cgkey = 0;
   unsigned long long c_rd = 0, c_wr = 0, c_br = 0;
   {
     const uint32_t c = blockIdx.x * P1_SUB;
@@ -415,14 +413,30 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
 
   uint32_t oacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // opcode bins 0..15, two 16-bit fields each
   uint32_t wacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width bins (bin v = width v, bin 0 = 16)
-  uint32_t pres = 0;                                     // widths 1..16 seen by this thread
+  uint32_t pres = 0;                                     // slow-path widths 1..16 seen in this presence block
+  uint32_t wsnap[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width counters at the block start
+  // widths 1..16 that occurred in presence block `blk` (PRES_TILES tile iterations) of this CTA
+  auto record_presence = [&](uint32_t blk) {
+    uint32_t bits = pres;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t d = wacc[i] ^ wsnap[i];
+      if (d & 0xFFFFu) bits |= 1u << ((2 * i ? 2 * i : 16) - 1);
+      if (d >> 16) bits |= 1u << (2 * i + 1 - 1);
+      wsnap[i] = wacc[i];
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits) atomicOr(&a.width_presence[(uint64_t)blockIdx.x * a.pres_blocks + blk], bits);
+    pres = 0;
+  };
   unsigned long long itb_sum = 0, ipt_sum = 0, flags = 0, max_site = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   uint32_t n_wib = 0, n_bar = 0;  // WI_BEGIN / BARRIER events (metrics.py: work_items, barriers_hit)
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
-    const uint64_t tile0 = (tile_begin + it) * TILE;
+    const uint64_t tile_idx = tile_of(it);
+    const uint64_t tile0 = tile_idx * TILE;
     const uint64_t row0 = tile0 / 16;
     if (row0 < a.tma_rows) mbar_wait(&S.bar[s], (it / STAGES) & 1);
     const uint64_t e0 = tile0 + 16ull * t;
@@ -703,22 +717,24 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     c_rd += T_rd; c_wr += T_wr; c_br += T_br;
     // ---- refill this stage ----
     if (t == 0 && it + STAGES < my_tiles) {
-      const uint64_t r2 = (tile_begin + it + STAGES) * (TILE / 16);
+      const uint64_t r2 = tile_of(it + STAGES) * (TILE / 16);
       if (r2 < a.tma_rows) {
         mbar_expect_tx(&S.bar[s], TILE * 9);
         tma_load_2d(S.kind[s], &kmap, 0, (int)r2, &S.bar[s]);
         tma_load_2d(S.pay[s], &pmap, 0, (int)r2, &S.bar[s]);
       }
     }
-    if ((it + 1) % ACC_FLUSH_TILES == 0) flush_counts(oacc, wacc, a, lane, pres, flags);
+    if ((it + 1) % PRES_TILES == 0) record_presence(it / PRES_TILES);
+    if ((it + 1) % ACC_FLUSH_TILES == 0) {
+      flush_counts(oacc, wacc, a, lane, flags);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wsnap[i] = 0;
+    }
   }
 
   // ---- epilogue: flush CTA-private state ----
-  flush_counts(oacc, wacc, a, lane, pres, flags);
-  pres = __reduce_or_sync(0xffffffffu, pres);
-  if (lane == 0 && pres) atomicOr(&L.wpres, pres);
-  __syncthreads();
-  if (t == 0 && L.wpres) a.width_presence[blockIdx.x] = L.wpres;
+  if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
+  flush_counts(oacc, wacc, a, lane, flags);
   for (int i = t; i < HBINS; i += TPB) {
     if (L.itb_h[i]) atomicAdd(&st->itb_hist[i], (unsigned long long)L.itb_h[i]);
     if (L.ipt_h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)L.ipt_h[i]);

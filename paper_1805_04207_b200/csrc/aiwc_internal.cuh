@@ -84,6 +84,8 @@ struct AddrMap {
   uint64_t off_max;    // largest valid addr - base: ((n_keys - 1) << k) | low_mask
 };
 
+constexpr int PRES_TILES = 16;         // width presence granularity (tile iterations per mask)
+
 struct IngestArgs {
   const uint8_t* kind;
   const uint64_t* payload;
@@ -97,7 +99,7 @@ struct IngestArgs {
   unsigned long long* opc_counts;   // [n_opcodes]
   unsigned long long* width_count;  // [WIDTH_TABLE]
   unsigned long long* width_first;  // [WIDTH_TABLE] (widths > 16; 1..16 found by width_first_kernel)
-  uint32_t* width_presence;         // [n_ranges]: widths 1..16 present in the range (bit w - 1)
+  uint32_t* width_presence;         // [n_ctas * pres_blocks]: widths 1..16 present (bit w - 1)
   uint32_t* itb_ovf;                // [n_bar + n_wie]
   uint32_t* ipt_ovf;                // [n_wie]
   unsigned long long* ipt_tab;      // [n_wgb * local_volume] or null
@@ -106,6 +108,7 @@ struct IngestArgs {
   AddrMap am;
   void* dense;                      // dense mode: [am.n_keys] u32 (dense32) or u64 entries
   uint32_t dense32;
+  uint32_t pres_blocks;             // width presence masks per CTA (width_presence[cta * pres_blocks + it / 16])
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
@@ -217,7 +220,8 @@ cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CU
                           bool dense, bool stage, cudaStream_t s);
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
-                        uint32_t n_ranges, uint64_t range_len, unsigned long long* width_first, cudaStream_t s);
+                        uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
+                        unsigned long long* width_first, cudaStream_t s);
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,

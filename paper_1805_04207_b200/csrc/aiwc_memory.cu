@@ -248,27 +248,49 @@ void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st,
 // width Counter in first-appearance order (metrics.py:136, :298-306)
 // ---------------------------------------------------------------------------
 // First event index of each width 1..16 counted by the ingest's bit-plane
-// bins: CTA w - 1 scans only the first ingest range whose presence mask has
-// width w, tile by tile in stream order, and stops at the first hit.
+// bins.  The ingest records, per CTA and per block of PRES_TILES tile
+// iterations, which widths occurred; CTA w - 1 finds the earliest block holding
+// width w in stream order and scans its tiles in order up to the first hit.
+// Two layouts: contiguous ranges per CTA (two-pass ingest: blocks in (CTA,
+// block) order) or tiles dealt round-robin (one-pass ingest: block b of every
+// CTA together covers tiles [b * PRES_TILES * G, (b + 1) * PRES_TILES * G)).
 __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restrict__ kind,
                                                           const uint64_t* __restrict__ payload, uint64_t n,
-                                                          const uint32_t* __restrict__ presence, uint32_t n_ranges,
-                                                          uint64_t range_len, unsigned long long* width_first) {
-  const uint32_t w = blockIdx.x + 1;
-  __shared__ uint32_t s_r;
-  __shared__ unsigned long long s_pos;
-  if (threadIdx.x == 0) { s_r = ~0u; s_pos = ~0ull; }
+                                                          const uint32_t* __restrict__ presence, uint32_t G,
+                                                          uint32_t pres_blocks, uint32_t tpc, int interleaved,
+                                                          unsigned long long* width_first) {
+  const uint32_t w = blockIdx.x + 1, bit = 1u << (w - 1);
+  __shared__ unsigned long long s_unit, s_pos;
+  if (threadIdx.x == 0) { s_unit = ~0ull; s_pos = ~0ull; }
   __syncthreads();
-  for (uint32_t r = threadIdx.x; r < n_ranges; r += blockDim.x)  // first range holding width w
-    if ((presence[r] >> (w - 1)) & 1u) { atomicMin(&s_r, r); break; }
+  // earliest unit (stream order) whose presence mask holds w
+  for (uint64_t u = threadIdx.x; u < (uint64_t)G * pres_blocks; u += blockDim.x) {
+    if (!(presence[u] & bit)) continue;
+    const uint64_t c = u / pres_blocks, b = u % pres_blocks;
+    atomicMin(&s_unit, interleaved ? b * G + c : c * pres_blocks + b);
+  }
   __syncthreads();
-  if (s_r == ~0u) return;
-  const uint64_t lo = (uint64_t)s_r * range_len, hi = min(n, lo + range_len);
-  for (uint64_t base = lo; base < hi; base += 256 * 16) {
+  if (s_unit == ~0ull) return;
+  const uint64_t n_tiles = (n + TILE - 1) / TILE;
+  // the candidate tiles, in stream order
+  uint64_t t_lo, t_hi;
+  if (interleaved) {
+    const uint64_t b = s_unit / G;
+    t_lo = b * PRES_TILES * G; t_hi = min(n_tiles, t_lo + (uint64_t)PRES_TILES * G);
+  } else {
+    const uint64_t c = s_unit / pres_blocks, b = s_unit % pres_blocks;
+    t_lo = c * tpc + b * PRES_TILES; t_hi = min(n_tiles, min(t_lo + PRES_TILES, (c + 1) * tpc));
+  }
+  for (uint64_t tile = t_lo; tile < t_hi; ++tile) {
+    if (interleaved) {  // skip tiles of CTAs whose block lacks the width
+      const uint64_t c = tile % G, b = tile / G / PRES_TILES;
+      if (!(presence[c * pres_blocks + b] & bit)) continue;
+    }
+    const uint64_t base = tile * TILE;
 #pragma unroll 4
     for (int j = 0; j < 16; ++j) {
       const uint64_t e = base + (uint64_t)j * 256 + threadIdx.x;
-      if (e < hi && kind[e] == AIWC_K_INSTR && (uint32_t)payload[e] == w) {
+      if (e < n && kind[e] == AIWC_K_INSTR && (uint32_t)payload[e] == w) {
         atomicMin(&s_pos, (unsigned long long)e);
         break;
       }
@@ -280,8 +302,10 @@ __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restr
 }
 
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
-                        uint32_t n_ranges, uint64_t range_len, unsigned long long* width_first, cudaStream_t s) {
-  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ranges, range_len, width_first);
+                        uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
+                        unsigned long long* width_first, cudaStream_t s) {
+  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ctas, pres_blocks, tiles_per_cta,
+                                           interleaved ? 1 : 0, width_first);
 }
 
 __global__ void width_list_kernel(const unsigned long long* __restrict__ count,

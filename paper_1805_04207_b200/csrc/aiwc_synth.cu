@@ -206,6 +206,14 @@ extern "C" uint64_t aiwc_synth_size(int cfg, uint64_t W, aiwc_trace_info* info) 
       case 4: info->addr_max = g.A + 4 * 255; break;
       case 5: info->addr_max = g.B + 4 * (4 * W - 1); break;
     }
+    // class totals per work-item of each recipe (wi_event above)
+    static const uint64_t per_wi[6][4] = {{0, 0, 0, 0}, {1, 1, 0, 0}, {21, 8, 1, 0}, {19, 10, 1, 0},
+                                          {192, 32, 0, 96}, {100, 8, 4, 0}};
+    info->has_counts = 1;
+    info->n_instr = per_wi[cfg][0] * W; info->n_reads = per_wi[cfg][1] * W;
+    info->n_writes = per_wi[cfg][2] * W; info->n_branches = per_wi[cfg][3] * W;
+    info->n_groups = g.groups;
+    info->any_barrier_or_resume = cfg == 5;
   }
   return n;
 }

@@ -130,6 +130,8 @@ struct Walker {
   // address statistics
   uint64_t amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   uint64_t n_mem = 0;
+  // class totals (declared to the engine: one-pass ingest)
+  uint64_t c_instr = 0, c_rd = 0, c_wr = 0, c_br = 0, c_wgb = 0, c_bres = 0;
 
   void flag(long long i, const char* rule, const std::string& detail) {
     if (violated) return;
@@ -157,7 +159,15 @@ struct Walker {
     extra_list.push_back(g);
     return k;
   }
-  void push(uint8_t k, uint64_t p) { kind.push_back(k); pay.push_back(p); }
+  void push(uint8_t k, uint64_t p) {
+    kind.push_back(k); pay.push_back(p);
+    c_instr += k == AIWC_K_INSTR;
+    c_rd += k == AIWC_K_LOAD || k == AIWC_K_ATOMIC_LOAD;
+    c_wr += k == AIWC_K_STORE || k == AIWC_K_ATOMIC_STORE;
+    c_br += k == AIWC_K_BRANCH;
+    c_wgb += k == AIWC_K_WG_BEGIN;
+    c_bres |= k == AIWC_K_BARRIER || k == AIWC_K_WI_RESUME;
+  }
 };
 
 int unsupported(const char* msg) {
@@ -746,12 +756,15 @@ PyObject* finish(Walker& w, int rc, long long last_line, PyObject* pending) {
   PyObject* name = w.kernel_name_obj ? w.kernel_name_obj : Py_None;
   PyObject* inv = w.invocation_obj ? w.invocation_obj : Py_None;
   PyObject* err = pending ? pending : Py_None;
-  PyObject* out = Py_BuildValue("{s:N,s:N,s:O,s:O,s:(LLL),s:(LLL),s:O,s:N,s:N,s:N,s:O,s:L,s:O}", "kind", kinds,
+  PyObject* counts = Py_BuildValue("(KKKKKK)", (unsigned long long)w.c_instr, (unsigned long long)w.c_rd,
+                                   (unsigned long long)w.c_wr, (unsigned long long)w.c_br, (unsigned long long)w.c_wgb,
+                                   (unsigned long long)w.c_bres);
+  PyObject* out = Py_BuildValue("{s:N,s:N,s:O,s:O,s:(LLL),s:(LLL),s:O,s:N,s:N,s:N,s:O,s:L,s:O,s:N}", "kind", kinds,
                                 "payload", pays, "kernel_name", name, "invocation", inv, "global_size", w.gsz.v[0],
                                 w.gsz.v[1], w.gsz.v[2], "local_size", w.lsz.v[0], w.lsz.v[1], w.lsz.v[2], "opcodes",
                                 w.opc_list, "extra_groups", extras, "addr_stats", stats, "violation", violation,
                                 "have_header", w.have_header ? Py_True : Py_False, "last_line", last_line, "error",
-                                err);
+                                err, "counts", counts);
   Py_XDECREF(pending);
   cleanup();
   return out;

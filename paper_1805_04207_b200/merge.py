@@ -78,4 +78,7 @@ def concat_traces(parts: list[ColumnarTrace]) -> ColumnarTrace:
     # group keys are already disjoint; a 1-D grid with key_base groups decodes them
     return ColumnarTrace(kind, payload, first.kernel_name, first.invocation, (key_base * lv, 1, 1), (lv, 1, 1),
                          [o for o, _ in sorted(opcodes.items(), key=lambda kv: kv[1])], [], addr_stats,
-                         validated=all(p.validated for p in parts))
+                         validated=all(p.validated for p in parts),
+                         class_counts=(tuple(sum(p.class_counts[i] for p in parts) for i in range(5)) +
+                                       (int(any(p.class_counts[5] for p in parts)),)
+                                       if all(p.class_counts is not None for p in parts) else None))

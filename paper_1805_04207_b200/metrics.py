@@ -128,6 +128,10 @@ def trace_info(tr: ColumnarTrace) -> _native.TraceInfo:
     if tr.addr_stats is not None:
         info.has_addr_stats = 1
         info.addr_min, info.addr_max, info.addr_and, info.addr_or = (int(v) for v in tr.addr_stats)
+    if tr.class_counts is not None:
+        info.has_counts = 1
+        (info.n_instr, info.n_reads, info.n_writes, info.n_branches, info.n_groups,
+         info.any_barrier_or_resume) = (int(v) for v in tr.class_counts)
     return info
 
 
@@ -172,7 +176,7 @@ def _device_columns(tr: ColumnarTrace, device: int) -> ColumnarTrace:
     k = torch.as_tensor(np.ascontiguousarray(kind, dtype=np.uint8) if not _is_torch(kind) else kind).to(dev)
     pl = payload if _is_torch(payload) else torch.from_numpy(np.ascontiguousarray(payload).view(np.int64))
     return ColumnarTrace(k, pl.to(dev), tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
-                         tr.extra_groups, tr.addr_stats, tr.validated)
+                         tr.extra_groups, tr.addr_stats, tr.validated, tr.class_counts)
 
 
 def validate_columnar(tr: ColumnarTrace, device: int | None = None) -> tuple | None:

@@ -62,10 +62,11 @@ def shard_range(cfg: int, work_items: int, rank: int, world: int) -> tuple[int, 
     return first, end - first
 
 
-def _columnar(cfg: int, work_items: int, kind, payload, ti) -> ColumnarTrace:
+def _columnar(cfg: int, work_items: int, kind, payload, ti, whole: bool = True) -> ColumnarTrace:
     lv = LOCAL[cfg]
+    counts = (ti.n_instr, ti.n_reads, ti.n_writes, ti.n_branches, ti.n_groups, ti.any_barrier_or_resume) if whole else None
     return ColumnarTrace(kind, payload, NAMES[cfg], 0, (work_items, 1, 1), (lv, 1, 1), list(OPCODES[cfg]), [],
-                         (ti.addr_min, ti.addr_max, ti.addr_and, ti.addr_or), validated=True)
+                         (ti.addr_min, ti.addr_max, ti.addr_and, ti.addr_or), validated=True, class_counts=counts)
 
 
 def device_trace(cfg: int, work_items: int | None = None, seed: int = DEFAULT_SEED, device: int = 0,
@@ -85,7 +86,7 @@ def device_trace(cfg: int, work_items: int | None = None, seed: int = DEFAULT_SE
                                                 ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(f"aiwc_synth_fill failed ({rc})")
-    return _columnar(cfg, w, kind, payload, ti)
+    return _columnar(cfg, w, kind, payload, ti, whole=(first == 0 and n == int(ti.n_events)))
 
 
 # ---------------------------------------------------------------------------

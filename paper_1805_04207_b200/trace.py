@@ -164,6 +164,9 @@ class ColumnarTrace:
     # True when the producer guarantees a valid stream (native walker, .aiwctrace
     # loader, synthetic generators, merges of such); consume() validates the rest
     validated: bool = False
+    # (instructions, reads, writes, branches, work-groups, any barrier/resume) when the
+    # producer knows them: the engine then ingests in one pass (verified on the device)
+    class_counts: tuple | None = None
 
     @property
     def n_events(self) -> int:
@@ -195,7 +198,7 @@ class ColumnarTrace:
             return a.cpu().numpy()
         return ColumnarTrace(host(self.kind), host(self.payload), self.kernel_name, self.invocation,
                              tuple(self.global_size), tuple(self.local_size), list(self.opcodes),
-                             list(self.extra_groups), self.addr_stats, self.validated)
+                             list(self.extra_groups), self.addr_stats, self.validated, self.class_counts)
 
     def iter_events(self):
         """Decode back to TraceEvent objects (debugging / CPU baselines)."""

@@ -220,7 +220,8 @@ def load_trace(path: str) -> tuple[ColumnarTrace | None, tuple | None, BaseExcep
         tr = ColumnarTrace(np.frombuffer(out["kind"], dtype=np.uint8), np.frombuffer(out["payload"], dtype=np.uint64),
                            out["kernel_name"], out["invocation"], tuple(out["global_size"]), tuple(out["local_size"]),
                            list(out["opcodes"]), [tuple(g) for g in out["extra_groups"]], out["addr_stats"],
-                           validated=out["violation"] is None and err is None)
+                           validated=out["violation"] is None and err is None,
+                           class_counts=tuple(out["counts"]) if out["violation"] is None and err is None else None)
     return tr, out["violation"], err, out["last_line"]
 
 

@@ -37,5 +37,6 @@ def encode_events(events) -> tuple[ColumnarTrace | None, tuple | None]:
     payload = np.frombuffer(out["payload"], dtype=np.uint64)
     tr = ColumnarTrace(kind, payload, out["kernel_name"], out["invocation"], tuple(out["global_size"]),
                        tuple(out["local_size"]), list(out["opcodes"]), [tuple(g) for g in out["extra_groups"]],
-                       out["addr_stats"], validated=violation is None)
+                       out["addr_stats"], validated=violation is None,
+                       class_counts=tuple(out["counts"]) if violation is None else None)
     return tr, violation
