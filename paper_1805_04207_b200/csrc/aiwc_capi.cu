@@ -448,6 +448,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.am = ctx->am;
     a.dense = ctx->dense ? ctx->dtab.p : nullptr;
     a.dense32 = ctx->dense32;
+    a.smem_keys = (ctx->dense && !ctx->dense32 && ctx->am.n_keys <= SMEM_TABLE_KEYS) ? (uint32_t)ctx->am.n_keys : 0u;
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, stage, s));

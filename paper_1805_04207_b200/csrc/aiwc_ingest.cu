@@ -234,7 +234,6 @@ struct StageSmem {
   uint64_t pay[STAGES][TILE];  // payload rows, 16 B chunk c of row r stored at chunk c ^ (r & 7)
   uint8_t kind[STAGES][TILE];
   uint64_t bar[STAGES];
-  uint64_t stage_out[1];       // TILE entries when the variant stages compaction output
 };
 
 // CTA-private accumulators and per-tile scratch (static smem: direct addressing)
@@ -327,7 +326,7 @@ __device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
 }
 
 template <bool DENSE, bool STAGE>
-__global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
+__global__ void __launch_bounds__(TPB, 2)
     ingest_kernel(const IngestArgs a, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap pmap) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -337,6 +336,8 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
   StageSmem& S = *reinterpret_cast<StageSmem*>(smem_raw + pad);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  // small dense tables: per-CTA read / write counters after the TMA stages
+  uint32_t* const stab = reinterpret_cast<uint32_t*>(smem_raw + pad + sizeof(StageSmem));
   const uint64_t n = a.n;
   const uint64_t n_tiles_total = (n + TILE - 1) / TILE;
   const uint64_t tile_begin = (uint64_t)blockIdx.x * a.tiles_per_cta;
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
 
   // ---- prologue: smem init + TMA ring fill ----
   for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
+  for (uint32_t i = t; i < 2 * a.smem_keys; i += TPB) stab[i] = 0;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     fence_barrier_init();
@@ -532,8 +534,9 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
     }
     uint32_t gkey = Qex ? (uint32_t)pay_at(S.pay[s], Qex - 1) : cgkey;
     uint32_t gseq = cgseq + (Cex & 0xFFFFu);
-    uint32_t o_rd = ex_rd, o_wr = T_rd + ex_wr;
-    uint32_t o_br = (DENSE ? 0u : T_rd + T_wr) + ex_br;
+    // ordered outputs go straight to their global slots (tile base + exclusive rank)
+    uint64_t o_rd = c_rd + ex_rd, o_wr = c_wr + ex_wr;
+    const uint64_t o_br = c_br + ex_br;
     uint32_t o_cl = Cex >> 16;
     // ---- fold my 16 events, one converged loop per event class ----
     // 128 B swizzle: event j of row r sits at u64 index 16 r + (j ^ ((r & 7) << 1))
@@ -636,7 +639,10 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
           const uint64_t off = pay[e & 0x0FFFu] - base;
           const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
           inval |= !v;
-          if (v) atomicAdd(tab + (off >> k), (e & 0x8000u) ? (1ull << 32) : 1ull);
+          if (v) {
+            if (a.smem_keys) atomicAdd(&stab[((e >> 15) ? a.smem_keys : 0u) + (uint32_t)(off >> k)], 1u);
+            else atomicAdd(tab + (off >> k), (e & 0x8000u) ? (1ull << 32) : 1ull);
+          }
         }
       }
       if (inval) flags |= F_ADDR_HINT;
@@ -645,11 +651,10 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       const uint32_t j = __ffs(m) - 1;
       const uint64_t p = PAY(j);
       const bool isw = (wr16 >> j) & 1u;
-      {
-        S.stage_out[isw ? o_wr++ : o_rd++] = p;
-        amin = min(amin, (unsigned long long)p); amax = max(amax, (unsigned long long)p);
-        aand &= p; aor |= p;
-      }
+      if (isw) a.wr_out[o_wr++] = p;
+      else a.rd_out[o_rd++] = p;
+      amin = min(amin, (unsigned long long)p); amax = max(amax, (unsigned long long)p);
+      aand &= p; aor |= p;
     }
     // branches: ordered records site << 32 | group << 1 | taken; the group is the last
     // wg_begin before the branch in my chunk, else my carry-in group
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
         const uint64_t site = p >> 1;
         flags |= ((site >> 32) ? (unsigned long long)F_BAD_SITE : 0ull) | ((g >> 31) ? (unsigned long long)F_BAD_GROUP : 0ull);
         max_site = max(max_site, (unsigned long long)site);
-        S.stage_out[o_br + __popc(br16 & ((1u << j) - 1u))] = (site << 32) | ((uint64_t)g << 1) | (p & 1);
+        a.br_out[o_br + __popc(br16 & ((1u << j) - 1u))] = (site << 32) | ((uint64_t)g << 1) | (p & 1);
       }
     } else if (br16) {
       flags |= F_BAD_KIND;  // the launcher stages whenever branches exist
@@ -704,15 +709,6 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
       const uint4 c = L.closes[i];
       do_close(L, a, c.x, c.y, c.z, itb_sum, ipt_sum, flags);
     }
-    // ---- flush ordered compaction ----
-    if (STAGE) {
-      if (!DENSE) {
-        for (uint32_t i = t; i < T_rd; i += TPB) a.rd_out[c_rd + i] = S.stage_out[i];
-        for (uint32_t i = t; i < T_wr; i += TPB) a.wr_out[c_wr + i] = S.stage_out[T_rd + i];
-      }
-      const uint32_t bb = DENSE ? 0u : T_rd + T_wr;
-      for (uint32_t i = t; i < T_br; i += TPB) a.br_out[c_br + i] = S.stage_out[bb + i];
-    }
     cseg = L.nc[0]; clid = L.nc[1]; cbyres = L.nc[2]; cgseq = L.nc[3]; cgkey = L.nc[4];
     c_rd += T_rd; c_wr += T_wr; c_br += T_br;
     // ---- refill this stage ----
@@ -733,6 +729,14 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
   }
 
   // ---- epilogue: flush CTA-private state ----
+  if (DENSE && a.smem_keys) {
+    __syncthreads();
+    unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
+    for (uint32_t i = t; i < a.smem_keys; i += TPB) {
+      const uint32_t r = stab[i], w = stab[a.smem_keys + i];
+      if (r | w) atomicAdd(tab + i, (unsigned long long)r | ((unsigned long long)w << 32));
+    }
+  }
   if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
   flush_counts(oacc, wacc, a, lane, flags);
   for (int i = t; i < HBINS; i += TPB) {
@@ -771,7 +775,7 @@ __global__ void __launch_bounds__(TPB, STAGE ? 1 : 2)
 template <bool DENSE, bool STAGE>
 static cudaError_t launch_variant(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap,
                                   uint32_t n_ctas, cudaStream_t s) {
-  const size_t smem = sizeof(StageSmem) + (STAGE ? (TILE - 1) * sizeof(uint64_t) : 0) + 1024;
+  const size_t smem = sizeof(StageSmem) + 1024 + 8ull * a.smem_keys;
   cudaError_t e = set_smem_once(ingest_kernel<DENSE, STAGE>, (int)smem);
   if (e != cudaSuccess) return e;
   ingest_kernel<DENSE, STAGE><<<n_ctas, TPB, smem, s>>>(a, kmap, pmap);

@@ -84,6 +84,7 @@ struct AddrMap {
   uint64_t off_max;    // largest valid addr - base: ((n_keys - 1) << k) | low_mask
 };
 
+constexpr uint32_t SMEM_TABLE_KEYS = 1024;  // small dense tables live in shared memory per CTA
 constexpr int PRES_TILES = 16;         // width presence granularity (tile iterations per mask)
 
 struct IngestArgs {
@@ -108,7 +109,9 @@ struct IngestArgs {
   AddrMap am;
   void* dense;                      // dense mode: [am.n_keys] u32 (dense32) or u64 entries
   uint32_t dense32;
-  uint32_t pres_blocks;             // width presence masks per CTA (width_presence[cta * pres_blocks + it / 16])
+  uint32_t pres_blocks;
+  uint32_t smem_keys;               // > 0: the (u64-format) dense table has this few keys and is
+                                    // accumulated per CTA in shared memory, flushed once at the end             // width presence masks per CTA (width_presence[cta * pres_blocks + it / 16])
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
@@ -217,7 +220,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t n_ranges,
                   uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s);
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
-                          bool dense, bool stage, cudaStream_t s);
+                          bool dense, bool stage, cudaStream_t s);  // smem grows by 8 * a.smem_keys
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
                         uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
