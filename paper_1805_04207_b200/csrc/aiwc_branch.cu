@@ -123,20 +123,32 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   for (uint32_t i = threadIdx.x; i < 2 * part_size; i += PC_T) cnt[i] = 0;
   __syncthreads();
   const uint64_t c0 = (uint64_t)chunk * chunk_len, c1 = min(n, c0 + chunk_len);
-  auto count = [&](uint32_t c) {
+  // coalesced 16-byte loads, four in flight per thread; equal neighbours inside a
+  // load are merged before touching shared memory (loop back-edges repeat one
+  // pattern for long stretches and would serialise on one bin)
+  auto add = [&](uint32_t c, uint32_t k) {
     if (c != NO_OBS && (c >> shift) == part) {
       const uint32_t slot = (c >> 1) & (part_size - 1);
-      atomicAdd(&tot[slot], 1u);
-      if (c & 1) atomicAdd(&tk[slot], 1u);
+      atomicAdd(&tot[slot], k);
+      if (c & 1) atomicAdd(&tk[slot], k);
     }
   };
+  auto count4 = [&](const uint4 q) {
+    if (q.x == q.y && q.y == q.z && q.z == q.w) { add(q.x, 4); return; }
+    add(q.x, 1); add(q.y, 1); add(q.z, 1); add(q.w, 1);
+  };
   const uint64_t v0 = (c0 + 3) & ~3ull, v1 = c1 & ~3ull;  // uint4-aligned body
-  for (uint64_t i = c0 + threadIdx.x; i < min(v0, c1); i += PC_T) count(code[i]);
-  for (uint64_t i = v0 + 4ull * threadIdx.x; i + 4 <= v1; i += 4ull * PC_T) {
-    const uint4 q = *reinterpret_cast<const uint4*>(code + i);
-    count(q.x); count(q.y); count(q.z); count(q.w);
+  for (uint64_t i = c0 + threadIdx.x; i < min(v0, c1); i += PC_T) add(code[i], 1);
+  const uint4* q4 = reinterpret_cast<const uint4*>(code);
+  const uint64_t nq = v1 > v0 ? (v1 - v0) / 4 : 0, q0 = v0 / 4;
+  uint64_t j = threadIdx.x;
+  for (; j + 3 * PC_T < nq; j += 4 * PC_T) {
+    const uint4 a0 = __ldcs(q4 + q0 + j), a1 = __ldcs(q4 + q0 + j + PC_T);
+    const uint4 a2 = __ldcs(q4 + q0 + j + 2 * PC_T), a3 = __ldcs(q4 + q0 + j + 3 * PC_T);
+    count4(a0); count4(a1); count4(a2); count4(a3);
   }
-  for (uint64_t i = max(v1, v0) + threadIdx.x; i < c1; i += PC_T) count(code[i]);
+  for (; j < nq; j += PC_T) count4(__ldcs(q4 + q0 + j));
+  for (uint64_t i = max(v1, v0) + threadIdx.x; i < c1; i += PC_T) add(code[i], 1);
   __syncthreads();
   unsigned long long* out = partials + (uint64_t)chunk * (1u << H) + (uint64_t)part * part_size;
   for (uint32_t i = threadIdx.x; i < part_size; i += PC_T)
@@ -153,49 +165,53 @@ __global__ void pattern_reduce_kernel(const unsigned long long* __restrict__ par
   tab[p] = v;
 }
 
-constexpr int BF_T = 1024;
+constexpr int BF_T = 256, BF_BLOCKS = 64;
 
-// yokota = sum_t w_t h(p_t), linear = sum_t w_t min(p_t, 1 - p_t), w_t = total_t / observations
-__global__ void __launch_bounds__(BF_T) branch_finish_kernel(const unsigned long long* __restrict__ tab,
-                                                             uint32_t size, DevState* st) {
-  __shared__ unsigned long long ro[BF_T / 32];
+// per-block partial sums of observations, total * h(p) and total * min(p, 1 - p)
+// over the pooled pattern table (entropy.py:123-132); fixed-order final reduction
+__global__ void __launch_bounds__(BF_T) branch_partial_kernel(const unsigned long long* __restrict__ tab,
+                                                              uint32_t size, double* __restrict__ part) {
   __shared__ double ry[BF_T / 32], rl[BF_T / 32];
+  __shared__ unsigned long long ro[BF_T / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long obs = 0;
-  for (uint32_t i = threadIdx.x; i < size; i += BF_T) obs += tab[i] >> 32;
-  obs = warp_sum(obs);
-  if (lane == 0) ro[warp] = obs;
-  __syncthreads();
-  obs = 0;
-  for (int w = 0; w < BF_T / 32; ++w) obs += ro[w];
   double y = 0.0, l = 0.0;
-  if (obs) {
-    const double dobs = (double)obs;
-    for (uint32_t i = threadIdx.x; i < size; i += BF_T) {
-      const unsigned long long e = tab[i];
-      const unsigned long long tot = e >> 32;
-      if (!tot) continue;
-      const double dt = (double)tot;
-      const double p = (double)(e & 0xFFFFFFFFull) / dt;
-      const double q = 1.0 - p;
-      const double h = -((p > 0 ? p * log2(p) : 0.0) + (q > 0 ? q * log2(q) : 0.0));
-      const double wgt = dt / dobs;
-      y += wgt * h;
-      l += wgt * (p < q ? p : q);
-    }
+  for (uint32_t i = blockIdx.x * BF_T + threadIdx.x; i < size; i += BF_T * gridDim.x) {
+    const unsigned long long e = tab[i];
+    const unsigned long long tot = e >> 32;
+    if (!tot) continue;
+    obs += tot;
+    const double dt = (double)tot;
+    const double p = (double)(e & 0xFFFFFFFFull) / dt;
+    const double q = 1.0 - p;
+    const double h = -((p > 0 ? p * log2(p) : 0.0) + (q > 0 ? q * log2(q) : 0.0));
+    y += dt * h;
+    l += dt * (p < q ? p : q);
   }
+  obs = warp_sum(obs);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     y += __shfl_xor_sync(0xffffffffu, y, o);
     l += __shfl_xor_sync(0xffffffffu, l, o);
   }
-  if (lane == 0) { ry[warp] = y; rl[warp] = l; }
+  if (lane == 0) { ro[warp] = obs; ry[warp] = y; rl[warp] = l; }
   __syncthreads();
   if (threadIdx.x == 0) {
+    unsigned long long to = 0;
     double ty = 0.0, tl = 0.0;
-    for (int w = 0; w < BF_T / 32; ++w) { ty += ry[w]; tl += rl[w]; }
-    st->yokota = ty; st->linear = tl; st->n_obs = obs;
+    for (int w = 0; w < BF_T / 32; ++w) { to += ro[w]; ty += ry[w]; tl += rl[w]; }
+    part[3 * blockIdx.x] = (double)to; part[3 * blockIdx.x + 1] = ty; part[3 * blockIdx.x + 2] = tl;
   }
+}
+
+// yokota = sum w h(p), linear = sum w min(p, 1 - p), w = total / observations
+__global__ void branch_finish_kernel(const double* __restrict__ part, uint32_t blocks, DevState* st) {
+  if (threadIdx.x) return;
+  double obs = 0.0, y = 0.0, l = 0.0;
+  for (uint32_t b = 0; b < blocks; ++b) { obs += part[3 * b]; y += part[3 * b + 1]; l += part[3 * b + 2]; }
+  st->n_obs = (unsigned long long)obs;
+  st->yokota = obs > 0 ? y / obs : 0.0;
+  st->linear = obs > 0 ? l / obs : 0.0;
 }
 
 // ---- launch geometry and scratch layout --------------------------------------
@@ -226,15 +242,18 @@ int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t histor
   uint64_t* tmp = reinterpret_cast<uint64_t*>(base);
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + ((branch_tmp_bytes(n) + 15) & ~15ull));
   unsigned long long* big = reinterpret_cast<unsigned long long*>(base + branch_site_list_offset(n));
-  if (site_bits) radix_sort_u64(recs, tmp, n, 32, 32 + (int)site_bits, hist, s, &kernels);
-  // after the sort the tmp region is free: observation codes + stage bytes
+  // stable grouping by site; the result stays in whichever buffer the last digit wrote
+  const uint64_t* sorted = site_bits ? radix_sort_u64_any(recs, tmp, n, 32, 32 + (int)site_bits, hist, s, &kernels)
+                                     : recs;
+  // the other 8n-byte buffer is free: observation codes + stage bytes
+  uint8_t* free8n = sorted == tmp ? reinterpret_cast<uint8_t*>(recs) : base;
   const uint32_t H = history_len, size = 1u << H;
   const uint32_t parts = n_parts_for(H), chunks = n_chunks_for(n, parts);
-  uint32_t* code = reinterpret_cast<uint32_t*>(base);
-  uint8_t* bits = base + 4 * ((n + 3) & ~3ull);
+  uint32_t* code = reinterpret_cast<uint32_t*>(free8n);
+  uint8_t* bits = free8n + 4 * ((n + 3) & ~3ull);
   unsigned long long* partials = reinterpret_cast<unsigned long long*>(base + ((8 * n + 15) & ~15ull));
   const uint32_t sb = (uint32_t)std::min<uint64_t>((n + 255) / 256, 148 * 8);
-  branch_stage_kernel<<<sb, 256, 0, s>>>(recs, n, bits, st, big);
+  branch_stage_kernel<<<sb, 256, 0, s>>>(sorted, n, bits, st, big);
   const uint32_t wb = (uint32_t)std::min<uint64_t>((n + 256 * PC_PER - 1) / (256 * PC_PER), 148 * 8);
   pattern_walk_kernel<<<wb, 256, 0, s>>>(bits, n, H, code);
   const uint64_t chunk_len = ((n + chunks - 1) / chunks + PC_CHUNK_ALIGN - 1) / PC_CHUNK_ALIGN * PC_CHUNK_ALIGN;
@@ -242,8 +261,12 @@ int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t histor
   set_smem_once(pattern_count_kernel, (int)smem);
   pattern_count_kernel<<<chunks * parts, PC_T, smem, s>>>(code, n, H, parts, chunk_len, partials);
   pattern_reduce_kernel<<<(size + 255) / 256, 256, 0, s>>>(partials, chunks, size, tables);
-  branch_finish_kernel<<<1, BF_T, 0, s>>>(tables, size, st);
-  return kernels + 5;
+  // the per-chunk partial tables are consumed: their space holds the finish partials
+  double* fin = reinterpret_cast<double*>(partials);
+  const uint32_t fb = std::min<uint32_t>(BF_BLOCKS, (size + BF_T - 1) / BF_T);
+  branch_partial_kernel<<<fb, BF_T, 0, s>>>(tables, size, fin);
+  branch_finish_kernel<<<1, 32, 0, s>>>(fin, fb, st);
+  return kernels + 6;
 }
 
 }  // namespace aiwc

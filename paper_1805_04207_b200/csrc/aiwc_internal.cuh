@@ -245,6 +245,8 @@ size_t branch_site_list_offset(uint64_t n);
 void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
                     cudaStream_t s, int* kernels);
 size_t radix_hist_bytes(uint64_t n);
+uint64_t* radix_sort_u64_any(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
+                             cudaStream_t s, int* kernels);
 void sort_u32_list(uint32_t* v, uint64_t n, uint64_t* tmp_a, uint64_t* tmp_b, uint32_t* hist, cudaStream_t s,
                    int* kernels);
 

@@ -163,6 +163,28 @@ __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __r
   }
 }
 
+// stable sort of keys by bits [bit_lo, bit_hi); returns the buffer holding the
+// result (keys or tmp: odd digit counts end in tmp, no copy back)
+uint64_t* radix_sort_u64_any(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
+                             cudaStream_t s, int* kernels) {
+  if (n <= 1 || bit_hi <= bit_lo) return keys;
+  const uint32_t nb = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+  uint32_t* hist = hist_scratch;
+  uint32_t* scan_tmp = hist_scratch + 256ull * nb;
+  uint64_t* src = keys;
+  uint64_t* dst = tmp;
+  for (int b = bit_lo; b < bit_hi; b += 8) {
+    const int bits = min(8, bit_hi - b);
+    const uint32_t mask = (1u << bits) - 1u;
+    radix_hist_kernel<<<nb, RS_T, 0, s>>>(src, n, b, mask, hist, nb);
+    scan_exclusive_u32(hist, 256ull * nb, scan_tmp, nullptr, s, kernels);
+    radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    if (kernels) *kernels += 2;
+    uint64_t* x = src; src = dst; dst = x;
+  }
+  return src;
+}
+
 void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
                     cudaStream_t s, int* kernels) {
   if (n <= 1 || bit_hi <= bit_lo) return;
