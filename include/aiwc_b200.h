@@ -239,6 +239,64 @@ uint64_t aiwc_synth_size(int cfg, uint64_t work_items, aiwc_trace_info *info);
 int  aiwc_synth_fill(int cfg, uint64_t work_items, uint64_t seed, uint8_t *kind_dev,
                      uint64_t *payload_dev, uint64_t first, uint64_t n, void *stream);
 
+/* ---- .aiwck NDRange producer (aiwc.sim.simulate_events, pkg/src/aiwc/sim.py:171-372) ----
+ * The reference's in-process trace producer, on the device.  The kernel source
+ * is parsed on the host (paper_1805_04207_b200/ir.py, ir.py:300-374) and
+ * lowered to records of AIWC_SIM_WORDS int32:
+ *   [kind, sem|atomic, width, dst, src0, src1, src2, buffer, target0, target1, opcode id, line]
+ * kind: 0 compute, 1 load, 2 store, 3 br, 4 jmp, 5 barrier, 6 ret; an operand
+ * word is mode << 30 | index (0 register, 1 constant-pool slot, 2 built-in
+ * gid0..lsz2); targets are instruction indices.  aiwc_sim_plan interprets the
+ * launch (counts, faults, layout; synchronizes `stream`), aiwc_sim_emit writes
+ * the events in exactly the order sim.py yields them (sim.py:244-344). */
+#define AIWC_SIM_WORDS 12
+#define AIWC_SIM_MAX_WIDTH (1u << 20)   /* widest register value the device path holds  */
+#define AIWC_SIM_FORCE_SEQUENTIAL 1u    /* skip speculation (tests)                        */
+
+enum {
+  AIWC_SIM_OK = 0,
+  AIWC_SIM_OUT_OF_BOUNDS = 1,   /* OutOfBoundsAccess(buffer, index, line)      sim.py:305-306 */
+  AIWC_SIM_WIDTH = 2,           /* SimulationError: register lanes != width     sim.py:216-221 */
+  AIWC_SIM_NONE_LEN = 3,        /* TypeError: register never written (len)      sim.py:211     */
+  AIWC_SIM_NONE_INDEX = 4,      /* TypeError: register never written ([0])      sim.py:230     */
+  AIWC_SIM_DIVERGENCE = 5,      /* BarrierDivergence                            sim.py:262-275 */
+  AIWC_SIM_STEP_LIMIT = 6,      /* StepLimitExceeded                            sim.py:235-238 */
+  AIWC_SIM_UNSUPPORTED = 7      /* width above AIWC_SIM_MAX_WIDTH, > 2^32 work-items        */
+};
+
+typedef struct aiwc_sim aiwc_sim;
+
+typedef struct {
+  const int32_t *code;        /* host: n_instr records                                   */
+  const uint64_t *imm;        /* host: constant pool (values mod 2^64)                   */
+  const uint64_t *buf_base;   /* host: byte address of each buffer (sim.py:132-141)      */
+  const uint64_t *buf_len;    /* host: elements of each buffer                           */
+  const uint64_t *mem_dev;    /* device: initial values, buffers concatenated in order   */
+  uint32_t n_instr, n_imm, n_regs, max_width, n_buffers, flags;
+  uint64_t global_size[3], local_size[3];
+  uint64_t step_limit;        /* sim.py DEFAULT_STEP_LIMIT = 10^8                        */
+} aiwc_sim_launch;
+
+typedef struct {
+  uint64_t n_events;          /* columns aiwc_sim_emit writes                            */
+  uint64_t prefix_events;     /* fault: events sim.py yields before raising (step limit:
+                                 UINT64_MAX, find the (limit+1)-th instruction event)    */
+  uint64_t n_instr, n_reads, n_writes, n_branches, n_groups, n_barriers;
+  int32_t error;              /* AIWC_SIM_*                                              */
+  int32_t line;               /* faulting line; divergence: culprit's last branch (-1)   */
+  uint64_t wi, wi2;           /* fault / divergence culprit, waiting work-item (stream order) */
+  int64_t index;              /* out-of-bounds index                                     */
+  uint32_t buffer, reg, lanes, width;
+  uint32_t sequential;        /* 1: a cross-work-item dependence forced the sequential mode */
+  uint32_t n_round;           /* divergence: the barrier round                           */
+} aiwc_sim_result;
+
+aiwc_sim   *aiwc_sim_create(void);
+void        aiwc_sim_destroy(aiwc_sim *sim);
+const char *aiwc_sim_last_error(const aiwc_sim *sim);
+int  aiwc_sim_plan(aiwc_sim *sim, const aiwc_sim_launch *launch, aiwc_sim_result *out, void *stream);
+int  aiwc_sim_emit(aiwc_sim *sim, uint8_t *kind_dev, uint64_t *payload_dev, uint64_t n_events, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -98,9 +98,30 @@ class Error(ctypes.Structure):
                 ("entries", ctypes.c_uint64), ("cap", ctypes.c_uint64), ("message", ctypes.c_char * 256)]
 
 
+class SimLaunch(ctypes.Structure):
+    _fields_ = [("code", ctypes.c_void_p), ("imm", ctypes.c_void_p), ("buf_base", ctypes.c_void_p),
+                ("buf_len", ctypes.c_void_p), ("mem_dev", ctypes.c_void_p), ("n_instr", ctypes.c_uint32),
+                ("n_imm", ctypes.c_uint32), ("n_regs", ctypes.c_uint32), ("max_width", ctypes.c_uint32),
+                ("n_buffers", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("global_size", ctypes.c_uint64 * 3),
+                ("local_size", ctypes.c_uint64 * 3), ("step_limit", ctypes.c_uint64)]
+
+
+class SimResult(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_uint64), ("prefix_events", ctypes.c_uint64), ("n_instr", ctypes.c_uint64),
+                ("n_reads", ctypes.c_uint64), ("n_writes", ctypes.c_uint64), ("n_branches", ctypes.c_uint64),
+                ("n_groups", ctypes.c_uint64), ("n_barriers", ctypes.c_uint64), ("error", ctypes.c_int32),
+                ("line", ctypes.c_int32), ("wi", ctypes.c_uint64), ("wi2", ctypes.c_uint64), ("index", ctypes.c_int64),
+                ("buffer", ctypes.c_uint32), ("reg", ctypes.c_uint32), ("lanes", ctypes.c_uint32),
+                ("width", ctypes.c_uint32), ("sequential", ctypes.c_uint32), ("n_round", ctypes.c_uint32)]
+
+
+SIM_OK, SIM_OUT_OF_BOUNDS, SIM_WIDTH, SIM_NONE_LEN, SIM_NONE_INDEX, SIM_DIVERGENCE, SIM_STEP_LIMIT, SIM_UNSUPPORTED = range(8)
+SIM_FORCE_SEQUENTIAL = 1
+
 EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
            "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill",
-           "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial", "aiwc_validate")
+           "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial", "aiwc_validate",
+           "aiwc_sim_create", "aiwc_sim_destroy", "aiwc_sim_last_error", "aiwc_sim_plan", "aiwc_sim_emit")
 
 _lib = None
 _lock = threading.Lock()
@@ -137,7 +158,15 @@ def load_library(path: str = LIB_PATH):
                                             ctypes.POINTER(MemoryPart), vp]
         i64x3 = ctypes.c_int64 * 3
         lib.aiwc_validate.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), i64x3, i64x3, ctypes.POINTER(Violation), vp]
-        for name in ("aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
+        lib.aiwc_sim_create.restype = vp
+        lib.aiwc_sim_create.argtypes = []
+        lib.aiwc_sim_destroy.argtypes = [vp]
+        lib.aiwc_sim_destroy.restype = None
+        lib.aiwc_sim_last_error.argtypes = [vp]
+        lib.aiwc_sim_last_error.restype = ctypes.c_char_p
+        lib.aiwc_sim_plan.argtypes = [vp, ctypes.POINTER(SimLaunch), ctypes.POINTER(SimResult), vp]
+        lib.aiwc_sim_emit.argtypes = [vp, vp, vp, ctypes.c_uint64, vp]
+        for name in ("aiwc_sim_plan", "aiwc_sim_emit", "aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
                      "aiwc_last_error", "aiwc_synth_fill", "aiwc_shard_tables_get", "aiwc_partition_addresses",
                      "aiwc_memory_partial", "aiwc_validate"):
             getattr(lib, name).restype = ctypes.c_int

@@ -15,47 +15,49 @@ namespace aiwc {
 // ---------------------------------------------------------------------------
 constexpr int SCAN_T = 1024, SCAN_I = 4, SCAN_TILE = SCAN_T * SCAN_I;
 
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* total) {
-  __shared__ uint32_t ws[SCAN_T / 32];
+template <typename T>
+__device__ __forceinline__ T block_excl_scan(T v, T* total) {
+  __shared__ T ws[SCAN_T / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t inc = warp_incl_sum(v);
+  const T inc = warp_incl_sum(v);
   if (lane == 31) ws[warp] = inc;
   __syncthreads();
   if (warp == 0) {
-    const uint32_t x = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0u;
-    const uint32_t xi = warp_incl_sum(x);
+    const T x = lane < (int)(blockDim.x >> 5) ? ws[lane] : (T)0;
+    const T xi = warp_incl_sum(x);
     ws[lane] = xi - x;
-    if (lane == 31) ws[0] = ws[0];  // keep
     if (lane == (int)(blockDim.x >> 5) - 1) *total = xi;
   }
   __syncthreads();
-  const uint32_t r = ws[warp] + inc - v;
+  const T r = ws[warp] + inc - v;
   __syncthreads();
   return r;
 }
 
-__global__ void scan_reduce_kernel(const uint32_t* d, uint64_t n, uint32_t* bsum) {
+template <typename T>
+__global__ void scan_reduce_kernel(const T* d, uint64_t n, T* bsum) {
   const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_TILE;
-  uint32_t s = 0;
+  T s = 0;
   for (int i = 0; i < SCAN_I; ++i) {
     const uint64_t idx = b0 + (uint64_t)i * SCAN_T + threadIdx.x;
     if (idx < n) s += d[idx];
   }
-  __shared__ uint32_t tot;
+  __shared__ T tot;
   block_excl_scan(s, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 
-__global__ void scan_top_kernel(uint32_t* bsum, uint32_t nb, uint32_t* total_out) {
-  __shared__ uint32_t carry_s;
-  __shared__ uint32_t tot;
+template <typename T>
+__global__ void scan_top_kernel(T* bsum, uint32_t nb, T* total_out) {
+  __shared__ T carry_s;
+  __shared__ T tot;
   if (threadIdx.x == 0) carry_s = 0;
   __syncthreads();
   for (uint32_t base = 0; base < nb; base += SCAN_T) {
     const uint32_t i = base + threadIdx.x;
-    const uint32_t v = i < nb ? bsum[i] : 0u;
-    const uint32_t ex = block_excl_scan(v, &tot);
-    const uint32_t c = carry_s;
+    const T v = i < nb ? bsum[i] : (T)0;
+    const T ex = block_excl_scan(v, &tot);
+    const T c = carry_s;
     if (i < nb) bsum[i] = c + ex;
     __syncthreads();
     if (threadIdx.x == 0) carry_s = c + tot;
@@ -64,15 +66,16 @@ __global__ void scan_top_kernel(uint32_t* bsum, uint32_t nb, uint32_t* total_out
   if (threadIdx.x == 0 && total_out) *total_out = carry_s;
 }
 
-__global__ void scan_down_kernel(uint32_t* d, uint64_t n, const uint32_t* bsum) {
+template <typename T>
+__global__ void scan_down_kernel(T* d, uint64_t n, const T* bsum) {
   const uint64_t b0 = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_I;
-  uint32_t v[SCAN_I], s = 0;
+  T v[SCAN_I], s = 0;
   for (int i = 0; i < SCAN_I; ++i) {
-    v[i] = (b0 + i < n) ? d[b0 + i] : 0u;
+    v[i] = (b0 + i < n) ? d[b0 + i] : (T)0;
     s += v[i];
   }
-  __shared__ uint32_t tot;
-  uint32_t ex = block_excl_scan(s, &tot) + bsum[blockIdx.x];
+  __shared__ T tot;
+  T ex = block_excl_scan(s, &tot) + bsum[blockIdx.x];
   for (int i = 0; i < SCAN_I; ++i) {
     if (b0 + i < n) d[b0 + i] = ex;
     ex += v[i];
@@ -81,14 +84,24 @@ __global__ void scan_down_kernel(uint32_t* d, uint64_t n, const uint32_t* bsum) 
 
 size_t scan_scratch_elems(uint64_t n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 1; }
 
-void scan_exclusive_u32(uint32_t* d, uint64_t n, uint32_t* scratch, uint32_t* total_out, cudaStream_t s,
-                        int* kernels) {
+template <typename T>
+static void scan_exclusive(T* d, uint64_t n, T* scratch, T* total_out, cudaStream_t s, int* kernels) {
   const uint32_t nb = (uint32_t)((n + SCAN_TILE - 1) / SCAN_TILE);
   if (nb == 0) return;
-  scan_reduce_kernel<<<nb, SCAN_T, 0, s>>>(d, n, scratch);
-  scan_top_kernel<<<1, SCAN_T, 0, s>>>(scratch, nb, total_out);
-  scan_down_kernel<<<nb, SCAN_T, 0, s>>>(d, n, scratch);
+  scan_reduce_kernel<T><<<nb, SCAN_T, 0, s>>>(d, n, scratch);
+  scan_top_kernel<T><<<1, SCAN_T, 0, s>>>(scratch, nb, total_out);
+  scan_down_kernel<T><<<nb, SCAN_T, 0, s>>>(d, n, scratch);
   if (kernels) *kernels += 3;
+}
+
+void scan_exclusive_u32(uint32_t* d, uint64_t n, uint32_t* scratch, uint32_t* total_out, cudaStream_t s,
+                        int* kernels) {
+  scan_exclusive<uint32_t>(d, n, scratch, total_out, s, kernels);
+}
+
+void scan_exclusive_u64(unsigned long long* d, uint64_t n, unsigned long long* scratch, unsigned long long* total_out,
+                        cudaStream_t s, int* kernels) {
+  scan_exclusive<unsigned long long>(d, n, scratch, total_out, s, kernels);
 }
 
 // ---------------------------------------------------------------------------
