@@ -86,10 +86,11 @@ typedef struct {
   uint32_t has_addr_stats;    /* 1 when addr_* below describe every memory address    */
   uint32_t has_counts;        /* 1 when the class totals below are declared           */
   uint64_t addr_min, addr_max, addr_and, addr_or;
-  /* Declared class totals (producers that know them: walkers, generators).  With
-   * them and declared address statistics, aiwc_ingest runs in ONE pass over the
-   * trace (tile carry-ins by decoupled look-back) instead of two; the totals are
-   * verified on the device (AIWC_ERR_ARGUMENT when they differ). */
+  /* Declared class totals (producers that know them: walkers, generators, the
+   * device NDRange producer).  With them aiwc_ingest makes every host decision
+   * up front and queues pass 1 and the ingest with no device->host round trip;
+   * pass 1's totals are checked against them at finalize (AIWC_ERR_ARGUMENT
+   * when they differ). */
   uint64_t n_instr, n_reads, n_writes, n_branches, n_groups;
   uint32_t any_barrier_or_resume, reserved;
 } aiwc_trace_info;
@@ -251,7 +252,8 @@ int  aiwc_synth_fill(int cfg, uint64_t work_items, uint64_t seed, uint8_t *kind_
  * the events in exactly the order sim.py yields them (sim.py:244-344). */
 #define AIWC_SIM_WORDS 12
 #define AIWC_SIM_MAX_WIDTH (1u << 20)   /* widest register value the device path holds  */
-#define AIWC_SIM_FORCE_SEQUENTIAL 1u    /* skip speculation (tests)                        */
+#define AIWC_SIM_FORCE_SEQUENTIAL 1u    /* run the whole launch in the sequential schedule  */
+#define AIWC_SIM_FORCE_GROUP 2u         /* start in the group schedule (tests)              */
 
 enum {
   AIWC_SIM_OK = 0,
@@ -287,7 +289,8 @@ typedef struct {
   uint64_t wi, wi2;           /* fault / divergence culprit, waiting work-item (stream order) */
   int64_t index;              /* out-of-bounds index                                     */
   uint32_t buffer, reg, lanes, width;
-  uint32_t sequential;        /* 1: a cross-work-item dependence forced the sequential mode */
+  uint32_t sequential;        /* schedule used: 0 speculative per work-item, 2 per work-group
+                                 (a work-item read another's store), 1 whole launch sequential */
   uint32_t n_round;           /* divergence: the barrier round                           */
 } aiwc_sim_result;
 

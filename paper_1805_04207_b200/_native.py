@@ -116,7 +116,8 @@ class SimResult(ctypes.Structure):
 
 
 SIM_OK, SIM_OUT_OF_BOUNDS, SIM_WIDTH, SIM_NONE_LEN, SIM_NONE_INDEX, SIM_DIVERGENCE, SIM_STEP_LIMIT, SIM_UNSUPPORTED = range(8)
-SIM_FORCE_SEQUENTIAL = 1
+SIM_FORCE_SEQUENTIAL, SIM_FORCE_GROUP = 1, 2
+SIM_SCHEDULE_FLAGS = {"auto": 0, "group": SIM_FORCE_GROUP, "sequential": SIM_FORCE_SEQUENTIAL}
 
 EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
            "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill",

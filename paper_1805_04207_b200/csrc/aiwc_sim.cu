@@ -13,8 +13,11 @@
 //    element the earliest (group, round, local id) store key and whether one
 //    or several work-items stored it; pass VERIFY re-runs every load against
 //    those tables.  A dependence (or a full store log) switches the launch to
-//  * sequential mode: one thread executing the reference's schedule literally
-//    with real stores.
+//  * group mode: one thread per work-group executing the reference's schedule
+//    for that group literally (real stores, barrier rounds in local order),
+//    groups in parallel.  Exact unless two groups touch an element one of them
+//    stores -- recorded per element during the pass -- which switches to
+//  * sequential mode: one thread executing the whole launch literally.
 //
 // Either way COUNT leaves per-segment event / instruction counts; a scan lays
 // the segments out in the reference's order and pass EMIT writes each event
@@ -39,6 +42,8 @@ enum : int32_t { K_COMPUTE = 0, K_LOAD, K_STORE, K_BR, K_JMP, K_BARRIER, K_RET }
 enum : int { MODE_COUNT = 0, MODE_VERIFY = 1, MODE_EMIT = 2, MODE_DETAIL = 3 };
 enum : int { END_BARRIER = 0, END_RET = 1, END_ERROR = 2, END_CAP = 3 };
 enum : uint32_t { SF_LOG = 1, SF_KEY = 2, SF_PHASES = 4, SF_CONFLICT = 8 };
+enum : int { MEM_SPEC = 0, MEM_SEQ = 1, MEM_GROUP = 2 };
+enum : int { STOP_NONE = 0, STOP_FAULT = 1, STOP_CAP = 2, STOP_DIV = 3 };
 constexpr uint32_t FIN_NEVER = 0xFFFFFFFFu;
 constexpr uint32_t OWN_EMPTY = 0xFFFFFFFFu, OWN_MULTI = 0xFFFFFFFEu;
 constexpr uint32_t LOGCAP = 32;
@@ -81,7 +86,8 @@ struct SimArgs {
   u64 stride;
   u64 *log_e, *log_v;  // own-store log, entry i of slot s at [i * stride + s]
   u64* smin;
-  uint32_t* sown;
+  uint32_t* sown;      // speculative: storing work-item / group mode: storing group (or MULTI)
+  uint32_t* sacc;      // group mode: accessing group (or MULTI)
   int kb_l, kb_p;      // key = g << (kb_p + kb_l) | p << kb_l | l
   uint32_t pmax;       // largest phase the key holds
   uint32_t* nph;       // per work-item: segments opened
@@ -94,7 +100,7 @@ struct SimArgs {
   u64* opay;
   const u64* segpos;   // exclusive scan of segment lengths (S + 1 entries)
   const u64* gseg;     // per group: first segment index (G + 1 entries)
-  // sequential mode per-work-item state (one group)
+  // group / sequential mode: per-work-item state of the groups in flight, [slot * V + l]
   uint32_t* s_pc;
   int32_t* s_br;
   uint8_t* s_status;
@@ -176,31 +182,48 @@ __device__ __forceinline__ u64 sem_eval(int sem, u64 x, u64 y, u64 z) {
 
 __device__ __forceinline__ int arity(int sem) { return sem <= 3 ? 1 : (sem >= 23 ? 3 : 2); }
 
-template <int MODE, bool SPEC>
+template <int MODE, int MEM>
 struct Machine {
   const SimArgs& a;
-  u64 slot, w;
+  u64 slot, w, grp;
   const u64 (&bi)[15];
   uint32_t nlog = 0;
 
-  __device__ Machine(const SimArgs& a_, u64 slot_, u64 w_, const u64 (&bi_)[15]) : a(a_), slot(slot_), w(w_), bi(bi_) {}
+  __device__ Machine(const SimArgs& a_, u64 slot_, u64 w_, u64 g_, const u64 (&bi_)[15])
+      : a(a_), slot(slot_), w(w_), grp(g_), bi(bi_) {}
 
   __device__ __forceinline__ u64& reg(uint32_t r, uint32_t lane) const {
     return a.regs[((u64)r * a.wmax + lane) * a.stride + slot];
   }
   __device__ __forceinline__ uint32_t& rl(uint32_t r) const { return a.rlen[(u64)r * a.stride + slot]; }
 
+  // group mode, pass COUNT: which groups touch / store an element
+  __device__ __forceinline__ void mark(uint32_t* tab, u64 e) const {
+    const uint32_t g = (uint32_t)grp, old = atomicCAS(&tab[e], OWN_EMPTY, g);
+    if (old != OWN_EMPTY && old != g && old != OWN_MULTI) atomicExch(&tab[e], OWN_MULTI);
+  }
+
   __device__ __forceinline__ u64 load_elem(u64 e) const {
-    if (SPEC) {
+    if (MEM == MEM_SPEC) {
       for (uint32_t i = 0; i < nlog; ++i)
         if (a.log_e[(u64)i * a.stride + slot] == e) return a.log_v[(u64)i * a.stride + slot];
     }
+    if (MEM == MEM_GROUP && MODE == MODE_COUNT) mark(a.sacc, e);
     return a.mem[e];
   }
-  __device__ __forceinline__ void store_elem(u64 e, u64 v) {
-    if (!SPEC) {
+  __device__ __forceinline__ void store_elem(u64 e, u64 v, u64 key) {
+    if (MEM != MEM_SPEC) {
+      if (MEM == MEM_GROUP && MODE == MODE_COUNT) {
+        mark(a.sown, e);
+        mark(a.sacc, e);
+      }
       a.mem[e] = v;
       return;
+    }
+    if (MODE == MODE_COUNT) {
+      atomicMin(&a.smin[e], key);
+      const uint32_t old = atomicCAS(&a.sown[e], OWN_EMPTY, (uint32_t)w);
+      if (old != OWN_EMPTY && old != (uint32_t)w && old != OWN_MULTI) atomicExch(&a.sown[e], OWN_MULTI);
     }
     for (uint32_t i = 0; i < nlog; ++i)
       if (a.log_e[(u64)i * a.stride + slot] == e) {
@@ -300,7 +323,7 @@ struct Machine {
             const uint32_t d = (uint32_t)q0.w;
             for (uint32_t lane = 0; lane < width; ++lane) {
               const u64 e = e0 + lane;
-              if (MODE == MODE_VERIFY) {
+              if (MEM == MEM_SPEC && MODE == MODE_VERIFY) {
                 const uint32_t own = a.sown[e];
                 if (own != OWN_EMPTY && own != (uint32_t)w && a.smin[e] < key) atomicOr(&a.gl->flags, SF_CONFLICT);
               }
@@ -324,15 +347,8 @@ struct Machine {
               sval = smode == 1 ? __ldg(a.imm + sidx) : bi[sidx];
             }
             for (uint32_t lane = 0; lane < width; ++lane) {
-              const u64 e = e0 + lane;
               emit(pos, atomic ? AIWC_K_ATOMIC_STORE : AIWC_K_STORE, addr0 + 4ull * lane);
-              const u64 v = vec ? reg(sidx, lane) : sval;
-              if (SPEC && MODE == MODE_COUNT) {
-                atomicMin(&a.smin[e], key);
-                const uint32_t old = atomicCAS(&a.sown[e], OWN_EMPTY, (uint32_t)w);
-                if (old != OWN_EMPTY && old != (uint32_t)w && old != OWN_MULTI) atomicExch(&a.sown[e], OWN_MULTI);
-              }
-              store_elem(e, v);
+              store_elem(e0 + lane, vec ? reg(sidx, lane) : sval, key);
             }
             t.wr += width;
           }
@@ -378,6 +394,13 @@ __device__ __forceinline__ void flush_totals(const SimArgs& a, Totals& t) {  // 
   }
 }
 
+__device__ __forceinline__ void record_segment(const SimArgs& a, u64 w, uint32_t p, uint32_t cnt, uint32_t ni) {
+  if (p < a.pcap) {
+    a.segcnt[w * a.pcap + p] = cnt;
+    a.seginstr[w * a.pcap + p] = ni;
+  }
+}
+
 // ---- speculative mode: one thread per work-item, all its barrier rounds ----
 template <int MODE>
 __global__ void __launch_bounds__(SPEC_TPB) sim_spec_kernel(SimArgs a) {
@@ -392,7 +415,7 @@ __global__ void __launch_bounds__(SPEC_TPB) sim_spec_kernel(SimArgs a) {
       u64 gkey;
       builtins_of(a, g, l, bi, lin_l, gkey);
       for (uint32_t r = 0; r < a.n_regs; ++r) a.rlen[(u64)r * a.stride + slot] = 0;
-      Machine<MODE, true> m(a, slot, w, bi);
+      Machine<MODE, MEM_SPEC> m(a, slot, w, g, bi);
       uint32_t pc = 0, p = 0;
       u64 charges = 0;
       int32_t last_br = -1;
@@ -410,16 +433,12 @@ __global__ void __launch_bounds__(SPEC_TPB) sim_spec_kernel(SimArgs a) {
         const u64 pos0 = pos;
         uint32_t ni = 0;
         end = m.segment(key, pc, charges, last_br, pos, ni, tot, nullptr);
-        if (MODE == MODE_COUNT && p < a.pcap) {
-          a.segcnt[w * a.pcap + p] = (uint32_t)(pos - pos0);
-          a.seginstr[w * a.pcap + p] = ni;
-        }
+        if (MODE == MODE_COUNT) record_segment(a, w, p, (uint32_t)(pos - pos0), ni);
         if (MODE == MODE_EMIT && (end == END_BARRIER || end == END_RET)) {
           a.okind[pos] = end == END_BARRIER ? AIWC_K_BARRIER : AIWC_K_WI_END;
           a.opay[pos] = end == END_BARRIER ? 0ull : lin_l;
         }
         if (end != END_BARRIER) break;
-        if (MODE == MODE_COUNT && p + 1 >= a.pcap) atomicOr(&a.gl->flags, SF_PHASES);
       }
       if (MODE == MODE_COUNT) {
         a.nph[w] = p + 1;
@@ -442,7 +461,7 @@ __global__ void __launch_bounds__(SPEC_TPB) sim_spec_kernel(SimArgs a) {
   if (MODE == MODE_COUNT) flush_totals(a, tot);
 }
 
-// one work-item again, recording its fault and its last branch line
+// one work-item again (speculative mode), recording its fault and its last branch line
 __global__ void sim_detail_kernel(SimArgs a, u64 w) {
   if (threadIdx.x || blockIdx.x) return;
   const u64 g = w / a.V, l = w % a.V;
@@ -451,7 +470,7 @@ __global__ void sim_detail_kernel(SimArgs a, u64 w) {
   u64 gkey;
   builtins_of(a, g, l, bi, lin_l, gkey);
   for (uint32_t r = 0; r < a.n_regs; ++r) a.rlen[(u64)r * a.stride] = 0;
-  Machine<MODE_DETAIL, true> m(a, 0, w, bi);
+  Machine<MODE_DETAIL, MEM_SPEC> m(a, 0, w, g, bi);
   uint32_t pc = 0;
   u64 charges = 0, pos = 0;
   int32_t last_br = -1;
@@ -466,125 +485,173 @@ __global__ void sim_detail_kernel(SimArgs a, u64 w) {
   a.gl->last_br = last_br;
 }
 
-// ---- sequential mode: the reference's schedule, one thread ----
+struct GroupStop {
+  int stop;
+  uint32_t round, l;          // fault / cap: round and local id; divergence: round
+  uint32_t culprit, waiting;  // divergence: local ids
+  int32_t last_br;            // divergence: culprit's last branch
+  Fault f;
+};
+
+// one work-group in the reference's schedule (sim.py:242-280): barrier rounds,
+// work-items in local order until their next barrier / return.  `sb` is the
+// first per-work-item state slot; the memory is written through.
+template <int MODE, int MEM>
+__device__ void run_group(const SimArgs& a, u64 g, u64 sb, u64& charges, Totals& tot, GroupStop& gs) {
+  enum : uint8_t { READY = 0, AT_BARRIER = 1, DONE = 2 };
+  gs.stop = STOP_NONE;
+  for (u64 l = 0; l < a.V; ++l) {
+    a.s_pc[sb + l] = 0;
+    a.s_br[sb + l] = -1;
+    a.s_status[sb + l] = READY;
+    for (uint32_t r = 0; r < a.n_regs; ++r) a.rlen[(u64)r * a.stride + sb + l] = 0;
+    if (MODE == MODE_COUNT) a.nph[g * a.V + l] = 0;
+  }
+  u64 gkey = 0;
+  {
+    u64 bi0[15];
+    uint32_t l0;
+    builtins_of(a, g, 0, bi0, l0, gkey);
+  }
+  if (MODE == MODE_EMIT) {
+    a.okind[1 + 2 * g + a.segpos[a.gseg[g]]] = AIWC_K_WG_BEGIN;
+    a.opay[1 + 2 * g + a.segpos[a.gseg[g]]] = gkey;
+  }
+  for (uint32_t p = 0;; ++p) {
+    bool any_done = false, all_done = true;
+    for (u64 l = 0; l < a.V; ++l) {
+      if (a.s_status[sb + l] != READY) {
+        all_done &= a.s_status[sb + l] == DONE;
+        continue;
+      }
+      const u64 w = g * a.V + l;
+      u64 bi[15];
+      uint32_t lin_l;
+      builtins_of(a, g, l, bi, lin_l, gkey);
+      Machine<MODE, MEM> m(a, sb + l, w, g, bi);
+      u64 pos = 0;
+      if (MODE == MODE_EMIT) {
+        const u64 open = 2 + 2 * g + a.segpos[a.gseg[g] + (u64)p * a.V + l];
+        a.okind[open] = p ? AIWC_K_WI_RESUME : AIWC_K_WI_BEGIN;
+        a.opay[open] = lin_l;
+        pos = open + 1;
+      }
+      const u64 pos0 = pos;
+      uint32_t ni = 0, pc = a.s_pc[sb + l];
+      int32_t last_br = a.s_br[sb + l];
+      const int end = m.segment(mk_key(a, g, p, l), pc, charges, last_br, pos, ni, tot, &gs.f);
+      a.s_pc[sb + l] = pc;
+      a.s_br[sb + l] = last_br;
+      if (MODE == MODE_COUNT) {
+        record_segment(a, w, p, (uint32_t)(pos - pos0), ni);
+        a.nph[w] = p + 1;
+        a.wend[w] = (uint8_t)end;
+        a.gnph[g] = max(a.gnph[g], p + 1);
+        atomicMax(&a.gl->max_nph, p + 1);
+      }
+      if (MODE == MODE_EMIT && (end == END_BARRIER || end == END_RET)) {
+        a.okind[pos] = end == END_BARRIER ? AIWC_K_BARRIER : AIWC_K_WI_END;
+        a.opay[pos] = end == END_BARRIER ? 0ull : lin_l;
+      }
+      if (end == END_ERROR || end == END_CAP) {
+        gs.stop = end == END_ERROR ? STOP_FAULT : STOP_CAP;
+        gs.round = p;
+        gs.l = (uint32_t)l;
+        return;
+      }
+      if (end == END_RET) {
+        a.s_status[sb + l] = DONE;
+        any_done = true;
+      } else {
+        a.s_status[sb + l] = AT_BARRIER;
+        all_done = false;
+      }
+    }
+    if (all_done) break;
+    if (any_done) {  // sim.py:262-275: first finished work-item, first one waiting
+      u64 c = 0, wt = 0;
+      while (a.s_status[sb + c] != DONE) ++c;
+      while (a.s_status[sb + wt] != AT_BARRIER) ++wt;
+      gs.stop = STOP_DIV;
+      gs.round = p;
+      gs.culprit = (uint32_t)c;
+      gs.waiting = (uint32_t)wt;
+      gs.last_br = a.s_br[sb + c];
+      return;
+    }
+    for (u64 l = 0; l < a.V; ++l) a.s_status[sb + l] = READY;
+  }
+  if (MODE == MODE_EMIT) {
+    a.okind[2 + 2 * g + a.segpos[a.gseg[g + 1]]] = AIWC_K_WG_END;
+    a.opay[2 + 2 * g + a.segpos[a.gseg[g + 1]]] = gkey;
+  }
+}
+
+// ---- group mode: one thread per work-group, groups in parallel ----
+// g_only != ~0: run that group alone and record its stop in the globals (detail run)
+template <int MODE>
+__global__ void sim_group_kernel(SimArgs a, u64 g_only) {
+  const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x, T = (u64)gridDim.x * blockDim.x;
+  Totals tot;
+  const u64 g0 = g_only != ~0ull ? (t == 0 ? g_only : a.G) : t;
+  const u64 step = g_only != ~0ull ? a.G : T;
+  for (u64 g = g0; g < a.G; g += step) {
+    u64 charges = 0;
+    GroupStop gs;
+    gs.f = Fault{0, -1, 0, 0, 0, 0, 0};
+    run_group<MODE, MEM_GROUP>(a, g, t * a.V, charges, tot, gs);
+    if (MODE == MODE_COUNT) {
+      const uint32_t r = gs.stop == STOP_DIV ? gs.round : 0;
+      a.gfin_min[g] = r;
+      a.gfin_max[g] = gs.stop == STOP_DIV ? r + 1 : r;
+      if (gs.stop == STOP_FAULT) atomicMin(&a.gl->err_key, mk_key(a, g, gs.round, gs.l));
+    }
+    if (MODE == MODE_DETAIL) {
+      a.gl->f = gs.f;
+      a.gl->culprit = (uint32_t)(g * a.V + gs.culprit);
+      a.gl->waiting = (uint32_t)(g * a.V + gs.waiting);
+      a.gl->last_br = gs.last_br;
+    }
+  }
+  if (MODE == MODE_COUNT) flush_totals(a, tot);
+}
+
+// ---- sequential mode: the whole launch in the reference's schedule, one thread ----
 template <int MODE>
 __global__ void sim_seq_kernel(SimArgs a) {
   if (threadIdx.x || blockIdx.x) return;
   Totals tot;
-  SimGlobals* gl = a.gl;
-  u64 charges = 0;
-  enum : uint8_t { READY = 0, AT_BARRIER = 1, DONE = 2 };
+  u64 charges = 0;  // launch-wide: the (limit+1)-th charge is the step-limit fault itself
   for (u64 g = 0; g < a.G; ++g) {
-    for (u64 l = 0; l < a.V; ++l) {
-      a.s_pc[l] = 0;
-      a.s_br[l] = -1;
-      a.s_status[l] = READY;
-      for (uint32_t r = 0; r < a.n_regs; ++r) a.rlen[(u64)r * a.stride + l] = 0;
-      if (MODE == MODE_COUNT) a.nph[g * a.V + l] = 0;
-    }
-    u64 gkey = 0;
-    {
-      u64 bi0[15];
-      uint32_t l0;
-      builtins_of(a, g, 0, bi0, l0, gkey);
-    }
-    if (MODE == MODE_EMIT) {
-      a.okind[1 + 2 * g + a.segpos[a.gseg[g]]] = AIWC_K_WG_BEGIN;
-      a.opay[1 + 2 * g + a.segpos[a.gseg[g]]] = gkey;
-    }
-    for (uint32_t p = 0;; ++p) {
-      bool any_done = false, all_done = true;
-      for (u64 l = 0; l < a.V; ++l) {
-        if (a.s_status[l] != READY) {
-          all_done &= a.s_status[l] == DONE;
-          continue;
-        }
-        const u64 w = g * a.V + l;
-        u64 bi[15];
-        uint32_t lin_l;
-        builtins_of(a, g, l, bi, lin_l, gkey);
-        Machine<MODE, false> m(a, l, w, bi);
-        u64 pos = 0;
-        if (MODE == MODE_EMIT) {
-          const u64 open = 2 + 2 * g + a.segpos[a.gseg[g] + (u64)p * a.V + l];
-          a.okind[open] = p ? AIWC_K_WI_RESUME : AIWC_K_WI_BEGIN;
-          a.opay[open] = lin_l;
-          pos = open + 1;
-        }
-        const u64 pos0 = pos;
-        uint32_t ni = 0, pc = a.s_pc[l];
-        int32_t last_br = a.s_br[l];
-        Fault f{0, -1, 0, 0, 0, 0, 0};
-        const int end = m.segment(0, pc, charges, last_br, pos, ni, tot, &f);
-        a.s_pc[l] = pc;
-        a.s_br[l] = last_br;
-        if (MODE == MODE_COUNT) {
-          if (p < a.pcap) {
-            a.segcnt[w * a.pcap + p] = (uint32_t)(pos - pos0);
-            a.seginstr[w * a.pcap + p] = ni;
-          } else {
-            gl->flags |= SF_PHASES;
-          }
-          a.nph[w] = p + 1;
-          a.wend[w] = (uint8_t)end;
-          a.gnph[g] = max(a.gnph[g], p + 1);
-          gl->max_nph = max(gl->max_nph, p + 1);
-        }
-        if (MODE == MODE_EMIT && (end == END_BARRIER || end == END_RET)) {
-          a.okind[pos] = end == END_BARRIER ? AIWC_K_BARRIER : AIWC_K_WI_END;
-          a.opay[pos] = end == END_BARRIER ? 0ull : lin_l;
-        }
-        if (end == END_ERROR || end == END_CAP) {
-          if (MODE == MODE_COUNT) {
-            gl->s_stop = end == END_ERROR ? 1 : 2;
-            gl->f = f;
-            gl->s_group = (uint32_t)g;
-            gl->s_round = p;
-            gl->s_wi = (uint32_t)w;
-            add_totals(a, tot);
-          }
-          return;
-        }
-        if (end == END_RET) {
-          a.s_status[l] = DONE;
-          any_done = true;
-        } else {
-          a.s_status[l] = AT_BARRIER;
-          all_done = false;
-        }
+    GroupStop gs;
+    gs.f = Fault{0, -1, 0, 0, 0, 0, 0};
+    run_group<MODE, MEM_SEQ>(a, g, 0, charges, tot, gs);
+    if (gs.stop != STOP_NONE) {
+      if (MODE == MODE_COUNT) {
+        SimGlobals* gl = a.gl;
+        gl->s_stop = gs.stop;
+        gl->f = gs.f;
+        gl->s_group = (uint32_t)g;
+        gl->s_round = gs.round;
+        gl->s_wi = (uint32_t)(g * a.V + gs.l);
+        gl->culprit = (uint32_t)(g * a.V + gs.culprit);
+        gl->waiting = (uint32_t)(g * a.V + gs.waiting);
+        gl->last_br = gs.last_br;
+        add_totals(a, tot);
       }
-      if (all_done) break;
-      if (any_done) {  // sim.py:262-275
-        if (MODE == MODE_COUNT) {
-          u64 c = 0, wt = 0;
-          while (a.s_status[c] != DONE) ++c;
-          while (a.s_status[wt] != AT_BARRIER) ++wt;
-          gl->s_stop = 3;
-          gl->s_group = (uint32_t)g;
-          gl->s_round = p;
-          gl->culprit = (uint32_t)(g * a.V + c);
-          gl->waiting = (uint32_t)(g * a.V + wt);
-          gl->last_br = a.s_br[c];
-          add_totals(a, tot);
-        }
-        return;
-      }
-      for (u64 l = 0; l < a.V; ++l) a.s_status[l] = READY;
-    }
-    if (MODE == MODE_EMIT) {
-      a.okind[2 + 2 * g + a.segpos[a.gseg[g + 1]]] = AIWC_K_WG_END;
-      a.opay[2 + 2 * g + a.segpos[a.gseg[g + 1]]] = gkey;
+      return;
     }
   }
   if (MODE == MODE_COUNT) add_totals(a, tot);
 }
 
 // ---- layout and fault resolution helpers ----
-__global__ void sim_init_kernel(SimArgs a, u64 n_elem, bool tables) {
+__global__ void sim_init_kernel(SimArgs a, u64 n_elem, int mode) {
   const u64 i0 = (u64)blockIdx.x * blockDim.x + threadIdx.x, st = (u64)gridDim.x * blockDim.x;
-  if (tables)
+  if (mode != MEM_SEQ)
     for (u64 i = i0; i < n_elem; i += st) {
-      a.smin[i] = ~0ull;
+      if (mode == MEM_SPEC) a.smin[i] = ~0ull;
+      else a.sacc[i] = OWN_EMPTY;
       a.sown[i] = OWN_EMPTY;
     }
   for (u64 g = i0; g < a.G; g += st) {
@@ -602,6 +669,15 @@ __global__ void sim_init_kernel(SimArgs a, u64 n_elem, bool tables) {
     a.gl->last_br = -1;
     a.gl->f.line = -1;
   }
+}
+
+// group mode: an element stored by one group and touched by another
+__global__ void sim_group_check_kernel(SimArgs a, u64 n_elem) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem; i += (u64)gridDim.x * blockDim.x)
+    if (a.sown[i] != OWN_EMPTY && a.sacc[i] == OWN_MULTI) {
+      atomicOr(&a.gl->flags, SF_CONFLICT);
+      return;
+    }
 }
 
 __global__ void sim_group_seg_kernel(SimArgs a, u64* gseg) {
@@ -687,11 +763,12 @@ int bitwidth(u64 x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
 struct aiwc_sim {
   std::string err;
-  DBuf code, imm, bbase, blen, boff, mem, regs, rlen, log_e, log_v, smin, sown, nph, wend, segcnt, seginstr, gnph,
-      gfin_min, gfin_max, gseg, segv, scan_scratch, gl, s_pc, s_br, s_status;
+  DBuf code, imm, bbase, blen, boff, mem, regs, rlen, log_e, log_v, smin, sown, sacc, nph, wend, segcnt, seginstr,
+      gnph, gfin_min, gfin_max, gseg, segv, scan_scratch, gl, s_pc, s_br, s_status;
   SimArgs a{};
-  bool planned = false, sequential = false;
-  u64 n_events = 0, n_elem = 0, spec_grid = 0;
+  bool planned = false;
+  int mode = MEM_SPEC;
+  u64 n_events = 0, n_elem = 0, spec_grid = 0, group_grid = 0;
   const u64* mem_init = nullptr;
 };
 
@@ -714,21 +791,32 @@ int read_globals(aiwc_sim* sim, SimGlobals& h, cudaStream_t st) {
   return AIWC_OK;
 }
 
-// pass COUNT (speculative or sequential), growing the per-phase arrays until they fit
-int run_count(aiwc_sim* sim, bool seq, SimGlobals& h, cudaStream_t st) {
+int fresh_memory(aiwc_sim* sim, cudaStream_t st) {
+  if (sim->n_elem)
+    SCK(cudaMemcpyAsync(sim->mem.p, sim->mem_init, sim->n_elem * 8, cudaMemcpyDeviceToDevice, st));
+  return AIWC_OK;
+}
+
+// pass COUNT in `mode`, growing the per-round arrays until every round fits
+int run_count(aiwc_sim* sim, int mode, SimGlobals& h, cudaStream_t st) {
   SimArgs& a = sim->a;
   for (;;) {
     SCK(sim->segcnt.grow(a.n_wi * a.pcap * 4));
     SCK(sim->seginstr.grow(a.n_wi * a.pcap * 4));
     a.segcnt = sim->segcnt.as<uint32_t>();
     a.seginstr = sim->seginstr.as<uint32_t>();
-    sim_init_kernel<<<592, 256, 0, st>>>(a, sim->n_elem, !seq);
-    if (seq) {
-      if (sim->n_elem) SCK(cudaMemcpyAsync(a.mem, sim->mem_init, sim->n_elem * 8, cudaMemcpyDeviceToDevice, st));
-      SCK(cudaMemsetAsync(a.nph, 0, a.n_wi * 4, st));
-      sim_seq_kernel<MODE_COUNT><<<1, 32, 0, st>>>(a);
-    } else {
+    sim_init_kernel<<<592, 256, 0, st>>>(a, sim->n_elem, mode);
+    if (mode == MEM_SPEC) {
       sim_spec_kernel<MODE_COUNT><<<(unsigned)sim->spec_grid, SPEC_TPB, 0, st>>>(a);
+    } else {
+      if (int r = fresh_memory(sim, st)) return r;
+      SCK(cudaMemsetAsync(a.nph, 0, a.n_wi * 4, st));
+      if (mode == MEM_GROUP) {
+        sim_group_kernel<MODE_COUNT><<<(unsigned)sim->group_grid, 32, 0, st>>>(a, ~0ull);
+        sim_group_check_kernel<<<592, 256, 0, st>>>(a, sim->n_elem);
+      } else {
+        sim_seq_kernel<MODE_COUNT><<<1, 32, 0, st>>>(a);
+      }
     }
     SCK(cudaGetLastError());
     if (int r = read_globals(sim, h, st)) return r;
@@ -744,9 +832,9 @@ extern "C" aiwc_sim* aiwc_sim_create(void) { return new (std::nothrow) aiwc_sim(
 extern "C" void aiwc_sim_destroy(aiwc_sim* sim) {
   if (!sim) return;
   DBuf* bufs[] = {&sim->code, &sim->imm, &sim->bbase, &sim->blen, &sim->boff, &sim->mem, &sim->regs,
-                  &sim->rlen, &sim->log_e, &sim->log_v, &sim->smin, &sim->sown, &sim->nph, &sim->wend,
-                  &sim->segcnt, &sim->seginstr, &sim->gnph, &sim->gfin_min, &sim->gfin_max, &sim->gseg,
-                  &sim->segv, &sim->scan_scratch, &sim->gl, &sim->s_pc, &sim->s_br, &sim->s_status};
+                  &sim->rlen, &sim->log_e, &sim->log_v, &sim->smin, &sim->sown, &sim->sacc, &sim->nph,
+                  &sim->wend, &sim->segcnt, &sim->seginstr, &sim->gnph, &sim->gfin_min, &sim->gfin_max,
+                  &sim->gseg, &sim->segv, &sim->scan_scratch, &sim->gl, &sim->s_pc, &sim->s_br, &sim->s_status};
   for (DBuf* b : bufs)
     if (b->p) cudaFree(b->p);
   delete sim;
@@ -805,13 +893,17 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
   a.boff = sim->boff.as<u64>();
   sim->mem_init = reinterpret_cast<const u64*>(L->mem_dev);
   SCK(sim->mem.grow(std::max<u64>(sim->n_elem, 1) * 8));
-  // speculative grid: enough threads to fill the GPU, register file within ~1 GiB
-  const u64 per_slot = (u64)a.n_regs * a.wmax * 8 + (u64)a.n_regs * 4 + 2ull * LOGCAP * 8;
+  // register-file slots: speculative mode one per thread, group mode V per thread
+  // (one group each), sequential mode V; register file within ~1 GiB where possible
+  const u64 per_slot = (u64)a.n_regs * a.wmax * 8 + (u64)a.n_regs * 4 + 2ull * LOGCAP * 8 + 9;
   u64 slots = std::min<u64>((a.n_wi + SPEC_TPB - 1) / SPEC_TPB, 148ull * 16) * SPEC_TPB;
   while (slots > SPEC_TPB && slots * per_slot > (1ull << 30)) slots /= 2;
   slots = std::max<u64>(slots / SPEC_TPB, 1) * SPEC_TPB;
   sim->spec_grid = slots / SPEC_TPB;
-  const u64 stride = std::max<u64>(slots, V);
+  u64 gthreads = std::min<u64>(G, 148ull * 64);
+  while (gthreads > 32 && gthreads * V * per_slot > (1ull << 30)) gthreads /= 2;
+  sim->group_grid = (gthreads + 31) / 32;
+  const u64 stride = std::max<u64>(slots, sim->group_grid * 32 * V);
   if (stride * per_slot > (48ull << 30)) {
     out->error = AIWC_SIM_UNSUPPORTED;
     return sim_fail(sim, AIWC_ERR_UNSUPPORTED, "register file of one work-group exceeds 48 GiB");
@@ -819,10 +911,11 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
   a.stride = stride;
   SCK(sim->regs.grow(stride * a.n_regs * a.wmax * 8));
   SCK(sim->rlen.grow(stride * a.n_regs * 4));
-  SCK(sim->log_e.grow(stride * LOGCAP * 8));
-  SCK(sim->log_v.grow(stride * LOGCAP * 8));
+  SCK(sim->log_e.grow(slots * LOGCAP * 8));
+  SCK(sim->log_v.grow(slots * LOGCAP * 8));
   SCK(sim->smin.grow(std::max<u64>(sim->n_elem, 1) * 8));
   SCK(sim->sown.grow(std::max<u64>(sim->n_elem, 1) * 4));
+  SCK(sim->sacc.grow(std::max<u64>(sim->n_elem, 1) * 4));
   SCK(sim->nph.grow(a.n_wi * 4));
   SCK(sim->wend.grow(a.n_wi));
   SCK(sim->gnph.grow(G * 4));
@@ -830,15 +923,16 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
   SCK(sim->gfin_max.grow(G * 4));
   SCK(sim->gseg.grow((G + 1) * 8));
   SCK(sim->gl.grow(sizeof(SimGlobals)));
-  SCK(sim->s_pc.grow(V * 4));
-  SCK(sim->s_br.grow(V * 4));
-  SCK(sim->s_status.grow(V));
+  SCK(sim->s_pc.grow(stride * 4));
+  SCK(sim->s_br.grow(stride * 4));
+  SCK(sim->s_status.grow(stride));
   a.regs = sim->regs.as<u64>();
   a.rlen = sim->rlen.as<uint32_t>();
   a.log_e = sim->log_e.as<u64>();
   a.log_v = sim->log_v.as<u64>();
   a.smin = sim->smin.as<u64>();
   a.sown = sim->sown.as<uint32_t>();
+  a.sacc = sim->sacc.as<uint32_t>();
   a.nph = sim->nph.as<uint32_t>();
   a.wend = sim->wend.as<uint8_t>();
   a.gnph = sim->gnph.as<uint32_t>();
@@ -855,58 +949,61 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
   a.pcap = 2;
   const u64 limit = std::min<u64>(L->step_limit, 1ull << 62);
 
-  // ---- pass COUNT (+ VERIFY) speculatively; the sequential mode on any dependence ----
+  // ---- speculative -> group -> sequential, each only when the previous one cannot prove exactness ----
   SimGlobals h{};
-  bool seq = (L->flags & AIWC_SIM_FORCE_SEQUENTIAL) || a.kb_p < 1;
-  if (!seq) {
+  int mode = (L->flags & AIWC_SIM_FORCE_SEQUENTIAL) || a.kb_p < 1 ? MEM_SEQ
+             : (L->flags & AIWC_SIM_FORCE_GROUP)                   ? MEM_GROUP
+                                                                   : MEM_SPEC;
+  if (mode == MEM_SPEC) {
     a.mem = const_cast<u64*>(sim->mem_init);
     a.cap = limit + 1;
-    if (int r = run_count(sim, false, h, st)) return r;
-    seq = (h.flags & (SF_LOG | SF_KEY)) != 0;
-    if (!seq) {
+    if (int r = run_count(sim, MEM_SPEC, h, st)) return r;
+    bool dep = (h.flags & (SF_LOG | SF_KEY)) != 0;
+    if (!dep) {
       sim_spec_kernel<MODE_VERIFY><<<(unsigned)sim->spec_grid, SPEC_TPB, 0, st>>>(a);
       SCK(cudaGetLastError());
       SimGlobals hv;
       if (int r = read_globals(sim, hv, st)) return r;
-      seq = (hv.flags & (SF_CONFLICT | SF_LOG)) != 0;
+      dep = (hv.flags & (SF_CONFLICT | SF_LOG)) != 0;
     }
+    if (dep) mode = MEM_GROUP;
   }
-  if (seq) {
+  if (mode == MEM_GROUP) {
+    a.mem = sim->mem.as<u64>();
+    a.cap = limit + 1;
+    if (int r = run_count(sim, MEM_GROUP, h, st)) return r;
+    if (h.flags & SF_CONFLICT) mode = MEM_SEQ;
+  }
+  if (mode == MEM_SEQ) {
     a.mem = sim->mem.as<u64>();
     a.cap = limit;
-    if (int r = run_count(sim, true, h, st)) return r;
+    if (int r = run_count(sim, MEM_SEQ, h, st)) return r;
   }
-  sim->sequential = seq;
-  out->sequential = seq;
+  sim->mode = mode;
+  out->sequential = mode == MEM_SEQ ? 1u : (mode == MEM_GROUP ? 2u : 0u);
 
   // ---- layout: segments in (group, round, local id) order ----
   u64* gseg = sim->gseg.as<u64>();
+  u64* scan_total = sim->gl.as<u64>() + (offsetof(SimGlobals, ord) / 8);
   sim_group_seg_kernel<<<(unsigned)std::min<u64>((G + 255) / 256, 4096), 256, 0, st>>>(a, gseg);
   SCK(sim->scan_scratch.grow(aiwc::scan_scratch_elems(G + 1) * 8));
   u64 S = 0;
-  {
-    u64* total = sim->gl.as<u64>() + (offsetof(SimGlobals, ord) / 8);
-    SCK(cudaMemsetAsync(total, 0, 8, st));
-    aiwc::scan_exclusive_u64(gseg, G, sim->scan_scratch.as<u64>(), total, st, nullptr);
-    SCK(cudaMemcpyAsync(&S, total, 8, cudaMemcpyDeviceToHost, st));
-    SCK(cudaMemcpyAsync(gseg + G, total, 8, cudaMemcpyDeviceToDevice, st));
-    SCK(cudaStreamSynchronize(st));
-  }
+  SCK(cudaMemsetAsync(scan_total, 0, 8, st));
+  aiwc::scan_exclusive_u64(gseg, G, sim->scan_scratch.as<u64>(), scan_total, st, nullptr);
+  SCK(cudaMemcpyAsync(gseg + G, scan_total, 8, cudaMemcpyDeviceToDevice, st));
+  SCK(cudaMemcpyAsync(&S, scan_total, 8, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
   a.gseg = gseg;
   SCK(sim->segv.grow((S + 1) * 8));
   u64* segv = sim->segv.as<u64>();
-  SCK(cudaMemsetAsync(segv, 0, (S + 1) * 8, st));
   sim_segv_kernel<<<(unsigned)std::min<u64>((a.n_wi + 255) / 256, 8192), 256, 0, st>>>(a, segv);
   u64 seg_total = 0;
-  {
-    SCK(sim->scan_scratch.grow(aiwc::scan_scratch_elems(S + 1) * 8));
-    u64* total = sim->gl.as<u64>() + (offsetof(SimGlobals, ord) / 8);
-    SCK(cudaMemsetAsync(total, 0, 8, st));
-    aiwc::scan_exclusive_u64(segv, S, sim->scan_scratch.as<u64>(), total, st, nullptr);
-    SCK(cudaMemcpyAsync(segv + S, total, 8, cudaMemcpyDeviceToDevice, st));
-    SCK(cudaMemcpyAsync(&seg_total, total, 8, cudaMemcpyDeviceToHost, st));
-    SCK(cudaStreamSynchronize(st));
-  }
+  SCK(sim->scan_scratch.grow(aiwc::scan_scratch_elems(S + 1) * 8));
+  SCK(cudaMemsetAsync(scan_total, 0, 8, st));
+  aiwc::scan_exclusive_u64(segv, S, sim->scan_scratch.as<u64>(), scan_total, st, nullptr);
+  SCK(cudaMemcpyAsync(segv + S, scan_total, 8, cudaMemcpyDeviceToDevice, st));
+  SCK(cudaMemcpyAsync(&seg_total, scan_total, 8, cudaMemcpyDeviceToHost, st));
+  SCK(cudaStreamSynchronize(st));
   a.segpos = segv;
   sim->n_events = 2 + 2 * G + seg_total;
   out->n_events = sim->n_events;
@@ -944,24 +1041,30 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
     out->buffer = f.buf;
     out->index = f.index;
   };
+  auto fault_prefix = [&](u64 w, u64 p) -> int {  // events up to and including the faulting instruction
+    u64 ev;
+    if (int r = open_event(w / V, p, w % V, ev)) return r;
+    uint32_t cnt = 0;
+    if (int r = dev_u32(sim->segcnt.as<uint32_t>() + w * a.pcap + p, cnt)) return r;
+    out->prefix_events = ev + 1 + cnt;
+    out->wi = w;
+    return AIWC_OK;
+  };
+  auto round_end = [&](u64 g, uint32_t r) -> int {  // events through barrier round r of group g
+    u64 gs, sp;
+    if (int e = dev_u64(gseg + g, gs)) return e;
+    if (int e = dev_u64(segv + gs + (u64)(r + 1) * V, sp)) return e;
+    out->prefix_events = 2 + 2 * g + sp;
+    return AIWC_OK;
+  };
 
-  if (seq) {
-    if (h.s_stop == 1 || h.s_stop == 2) {
-      const u64 w = h.s_wi, g = w / V, l = w % V;
-      u64 ev;
-      if (int r = open_event(g, h.s_round, l, ev)) return r;
-      uint32_t cnt = 0;
-      if (int r = dev_u32(sim->segcnt.as<uint32_t>() + w * a.pcap + h.s_round, cnt)) return r;
-      out->prefix_events = ev + 1 + cnt;
-      out->wi = w;
-      if (h.s_stop == 1) fault_out(h.f);
+  if (mode == MEM_SEQ) {
+    if (h.s_stop == STOP_FAULT || h.s_stop == STOP_CAP) {
+      if (int r = fault_prefix(h.s_wi, h.s_round)) return r;
+      if (h.s_stop == STOP_FAULT) fault_out(h.f);
       else out->error = AIWC_SIM_STEP_LIMIT;
-    } else if (h.s_stop == 3) {
-      const u64 g = h.s_group;
-      u64 gs, sp;
-      if (int r = dev_u64(gseg + g, gs)) return r;
-      if (int r = dev_u64(segv + gs + (u64)(h.s_round + 1) * V, sp)) return r;
-      out->prefix_events = 2 + 2 * g + sp;
+    } else if (h.s_stop == STOP_DIV) {
+      if (int r = round_end(h.s_group, h.s_round)) return r;
       out->error = AIWC_SIM_DIVERGENCE;
       out->wi = h.culprit;
       out->wi2 = h.waiting;
@@ -1010,34 +1113,35 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
     if (step) {
       out->error = AIWC_SIM_STEP_LIMIT;
       out->prefix_events = ~0ull;
-    } else if (have_e) {
-      const u64 w = eg * V + el;
-      sim_detail_kernel<<<1, 32, 0, st>>>(a, w);
+    } else if (have_e || have_d) {
       SimGlobals hd;
-      if (int r = read_globals(sim, hd, st)) return r;
-      fault_out(hd.f);
-      u64 ev;
-      if (int r = open_event(eg, ep, el, ev)) return r;
-      uint32_t cnt = 0;
-      if (int r = dev_u32(sim->segcnt.as<uint32_t>() + w * a.pcap + ep, cnt)) return r;
-      out->prefix_events = ev + 1 + cnt;
-      out->wi = w;
-    } else if (have_d) {
-      sim_culprit_kernel<<<(unsigned)std::min<u64>((V + 255) / 256, 4096), 256, 0, st>>>(a);
-      SimGlobals hc;
-      if (int r = read_globals(sim, hc, st)) return r;
-      sim_detail_kernel<<<1, 32, 0, st>>>(a, hc.culprit);
-      SimGlobals hd;
-      if (int r = read_globals(sim, hd, st)) return r;
-      u64 gs, sp;
-      if (int r = dev_u64(gseg + dg, gs)) return r;
-      if (int r = dev_u64(segv + gs + (u64)(dr + 1) * V, sp)) return r;
-      out->prefix_events = 2 + 2 * dg + sp;
-      out->error = AIWC_SIM_DIVERGENCE;
-      out->wi = hc.culprit;
-      out->wi2 = hc.waiting;
-      out->line = hd.last_br;
-      out->n_round = dr;
+      const u64 w_e = eg * V + el;
+      if (mode == MEM_SPEC) {
+        if (have_d) {
+          sim_culprit_kernel<<<(unsigned)std::min<u64>((V + 255) / 256, 4096), 256, 0, st>>>(a);
+          if (int r = read_globals(sim, hd, st)) return r;
+        }
+        const u64 culprit = have_d ? hd.culprit : 0, waiting = have_d ? hd.waiting : 0;
+        sim_detail_kernel<<<1, 32, 0, st>>>(a, have_e ? w_e : culprit);
+        if (int r = read_globals(sim, hd, st)) return r;
+        hd.culprit = (uint32_t)culprit;
+        hd.waiting = (uint32_t)waiting;
+      } else {  // group mode: the group again, alone, from the initial memory
+        if (int r = fresh_memory(sim, st)) return r;
+        sim_group_kernel<MODE_DETAIL><<<1, 32, 0, st>>>(a, have_e ? eg : dg);
+        if (int r = read_globals(sim, hd, st)) return r;
+      }
+      if (have_e) {
+        fault_out(hd.f);
+        if (int r = fault_prefix(w_e, ep)) return r;
+      } else {
+        if (int r = round_end(dg, dr)) return r;
+        out->error = AIWC_SIM_DIVERGENCE;
+        out->wi = hd.culprit;
+        out->wi2 = hd.waiting;
+        out->line = hd.last_br;
+        out->n_round = dr;
+      }
     }
   }
   sim->planned = true;
@@ -1054,11 +1158,12 @@ extern "C" int aiwc_sim_emit(aiwc_sim* sim, uint8_t* kind_dev, uint64_t* payload
   SimArgs a = sim->a;
   a.okind = kind_dev;
   a.opay = reinterpret_cast<u64*>(payload_dev);
-  if (sim->sequential) {
-    if (sim->n_elem) SCK(cudaMemcpyAsync(a.mem, sim->mem_init, sim->n_elem * 8, cudaMemcpyDeviceToDevice, st));
-    sim_seq_kernel<MODE_EMIT><<<1, 32, 0, st>>>(a);
-  } else {
+  if (sim->mode == MEM_SPEC) {
     sim_spec_kernel<MODE_EMIT><<<(unsigned)sim->spec_grid, SPEC_TPB, 0, st>>>(a);
+  } else {
+    if (int r = fresh_memory(sim, st)) return r;
+    if (sim->mode == MEM_GROUP) sim_group_kernel<MODE_EMIT><<<(unsigned)sim->group_grid, 32, 0, st>>>(a, ~0ull);
+    else sim_seq_kernel<MODE_EMIT><<<1, 32, 0, st>>>(a);
   }
   sim_ends_kernel<<<1, 1, 0, st>>>(kind_dev, a.opay, n_events);
   SCK(cudaGetLastError());

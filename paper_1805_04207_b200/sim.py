@@ -21,6 +21,7 @@ launch re-runs in the exact sequential schedule on the device.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, field
 from typing import Iterator
 
@@ -88,6 +89,16 @@ def assign_bases(params: tuple, buffers: dict) -> dict:
     return out
 
 
+def _as_u64(values) -> np.ndarray:
+    """Buffer contents as u64 lanes: integer / bool arrays keep their bits (fast
+    path); anything else is reduced element-wise with ``v & (2^64 - 1)`` like
+    the reference (sim.py:186), which also rejects non-integers the same way."""
+    arr = values if isinstance(values, np.ndarray) else np.asarray(values)
+    if arr.ndim == 1 and arr.dtype.kind in "iub":
+        return np.ascontiguousarray(arr.astype(np.int64, copy=False)).view(np.uint64)
+    return np.asarray([v & _MASK for v in values], dtype=np.uint64)
+
+
 def _prepare(program: KernelProgram, cfg: NDRangeConfig):
     cfg.validate()
     missing = [p for p in program.params if p not in cfg.buffers]
@@ -97,11 +108,33 @@ def _prepare(program: KernelProgram, cfg: NDRangeConfig):
     return bases
 
 
+_POOL: dict = {}
+_POOL_LOCK = threading.Lock()
+
+
+def _acquire(lib, device: int) -> ctypes.c_void_p:
+    """A producer handle for `device`; handles keep their device scratch between
+    launches, so repeated launches do not re-allocate."""
+    with _POOL_LOCK:
+        free = _POOL.setdefault(device, [])
+        if free:
+            return free.pop()
+    h = ctypes.c_void_p(lib.aiwc_sim_create())
+    if not h.value:
+        raise DeviceError("aiwc_sim_create failed")
+    return h
+
+
+def _release(device: int, h: ctypes.c_void_p) -> None:
+    with _POOL_LOCK:
+        _POOL.setdefault(device, []).append(h)
+
+
 class _Launch:
     """One planned launch on the device: counts, layout, first fault."""
 
     def __init__(self, program: KernelProgram, cfg: NDRangeConfig, bases: dict, step_limit: int, device: int,
-                 sequential: bool = False):
+                 schedule: str = "auto"):
         import torch
 
         self.program, self.cfg, self.step_limit = program, cfg, step_limit
@@ -109,9 +142,15 @@ class _Launch:
         self.lib = _native.load_library()
         self.dev = torch.device("cuda", device)
         params = program.params
-        vals = [np.asarray([int(v) & _MASK for v in cfg.buffers[p]], dtype=np.uint64) for p in params]
-        mem = np.concatenate(vals) if vals else np.zeros(0, np.uint64)
-        self.mem = torch.from_numpy(mem.view(np.int64) if mem.size else np.zeros(1, np.int64)).to(self.dev)
+        bufs = [cfg.buffers[p] for p in params]
+        if bufs and all(isinstance(b, torch.Tensor) and b.is_cuda for b in bufs):
+            # device-resident buffers: concatenated on the device, no host round trip
+            self.mem = torch.cat([b.to(self.dev).reshape(-1).to(torch.int64) for b in bufs] +
+                                 [torch.zeros(1, dtype=torch.int64, device=self.dev)])
+        else:
+            vals = [_as_u64(b if not isinstance(b, torch.Tensor) else b.cpu().numpy()) for b in bufs]
+            mem = np.concatenate(vals) if vals else np.zeros(0, np.uint64)
+            self.mem = torch.from_numpy(mem.view(np.int64) if mem.size else np.zeros(1, np.int64)).to(self.dev)
         self.code = np.ascontiguousarray(self.cp.code, dtype=np.int32)
         self.imm = np.ascontiguousarray(self.cp.imm, dtype=np.uint64)
         self.bbase = np.array([bases[p] & _MASK for p in params] or [0], dtype=np.uint64)
@@ -124,13 +163,14 @@ class _Launch:
         L.mem_dev = self.mem.data_ptr()
         L.n_instr, L.n_imm = len(self.code), len(self.imm)
         L.n_regs, L.max_width, L.n_buffers = self.cp.n_regs, self.cp.max_width, len(params)
-        L.flags = _native.SIM_FORCE_SEQUENTIAL if sequential else 0
+        if schedule not in _native.SIM_SCHEDULE_FLAGS:
+            raise ValueError(f"schedule must be one of {sorted(_native.SIM_SCHEDULE_FLAGS)}")
+        L.flags = _native.SIM_SCHEDULE_FLAGS[schedule]
         for d in range(3):
             L.global_size[d], L.local_size[d] = cfg.global_size[d], cfg.local_size[d]
         L.step_limit = max(0, min(int(step_limit), (1 << 62)))
-        self.h = ctypes.c_void_p(self.lib.aiwc_sim_create())
-        if not self.h.value:
-            raise DeviceError("aiwc_sim_create failed")
+        self.device = device
+        self.h = _acquire(self.lib, device)
         self.res = _native.SimResult()
         with torch.cuda.device(self.dev):
             self.stream = torch.cuda.current_stream(self.dev).cuda_stream
@@ -144,6 +184,11 @@ class _Launch:
         if rc == _native.ERR_UNSUPPORTED:
             raise UnsupportedTrace(msg)
         raise DeviceError(msg or f"aiwc_sim_plan failed with code {rc}")
+
+    @property
+    def schedule(self) -> str:
+        """The schedule the device used: speculative / group / sequential."""
+        return {0: "speculative", 1: "sequential", 2: "group"}[int(self.res.sequential)]
 
     def emit(self):
         import torch
@@ -200,7 +245,7 @@ class _Launch:
 
     def close(self) -> None:
         if getattr(self, "h", None) is not None and self.h.value:
-            self.lib.aiwc_sim_destroy(self.h)
+            _release(self.device, self.h)
             self.h = ctypes.c_void_p()
 
     def __del__(self):
@@ -225,11 +270,12 @@ def _device(device: int | None) -> int:
 
 
 def simulate_trace(program: KernelProgram, cfg: NDRangeConfig, *, step_limit: int = DEFAULT_STEP_LIMIT,
-                   invocation: int = 0, device: int | None = None, sequential: bool = False) -> ColumnarTrace:
+                   invocation: int = 0, device: int | None = None, schedule: str = "auto") -> ColumnarTrace:
     """The launch's trace as a device-resident ColumnarTrace (validated, class
-    totals declared), or the reference's fault for it."""
+    totals declared), or the reference's fault for it.  ``schedule`` forces the
+    group or sequential device schedule (default: the cheapest exact one)."""
     bases = _prepare(program, cfg)
-    launch = _Launch(program, cfg, bases, step_limit, _device(device), sequential)
+    launch = _Launch(program, cfg, bases, step_limit, _device(device), schedule)
     try:
         exc = launch.exception()
         if exc is not None:
@@ -265,21 +311,21 @@ def _events_then_raise(launch: _Launch, invocation: int) -> Iterator:
 
 
 def simulate_events(program: KernelProgram, cfg: NDRangeConfig, *, step_limit: int = DEFAULT_STEP_LIMIT,
-                    invocation: int = 0, device: int | None = None, sequential: bool = False) -> Iterator:
+                    invocation: int = 0, device: int | None = None, schedule: str = "auto") -> Iterator:
     """Stream the trace of one kernel invocation (sim.py:347-356): ConfigError
     at call time, faults after the events that precede them."""
     bases = _prepare(program, cfg)
     dev = _device(device)
 
     def run():
-        launch = _Launch(program, cfg, bases, step_limit, dev, sequential)
+        launch = _Launch(program, cfg, bases, step_limit, dev, schedule)
         yield from _events_then_raise(launch, invocation)
 
     return run()
 
 
 def simulate(program: KernelProgram, cfg: NDRangeConfig, *, step_limit: int = DEFAULT_STEP_LIMIT,
-             invocation: int = 0, device: int | None = None, sequential: bool = False) -> list:
+             invocation: int = 0, device: int | None = None, schedule: str = "auto") -> list:
     """Materialised variant of simulate_events (sim.py:359-372)."""
     return list(simulate_events(program, cfg, step_limit=step_limit, invocation=invocation, device=device,
-                                sequential=sequential))
+                                schedule=schedule))

@@ -5,7 +5,7 @@ Every golden launch -- the reference's kernels and test programs, semantic
 edge cases (Python floor division / modulo, INT64_MIN, shifts, vector lanes)
 and 120 seeded random programs with loops, diamonds, barriers, private and
 shared memory, faults, divergence and step limits -- runs through both device
-modes (speculative and forced sequential).  The event stream must be
+modes (speculative with automatic fallback, forced group, forced sequential).  The event stream must be
 byte-identical to the reference's canonical lines (count + sha256, lines
 where recorded), the fault must be the same class with the same message and
 line, and it must come after exactly the same events.  Valid traces also go
@@ -26,7 +26,7 @@ torch = pytest.importorskip("torch")
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "sim.json")))
 
 
-def _run(case, sequential):
+def _run(case, schedule):
     from paper_1805_04207_b200 import encode_event, ir, sim
 
     prog = ir.parse_kernel(case["source"])
@@ -34,17 +34,17 @@ def _run(case, sequential):
     lines, err = [], None
     try:
         for ev in sim.simulate_events(prog, cfg, step_limit=case["step_limit"], invocation=case["invocation"],
-                                      sequential=sequential):
+                                      schedule=schedule):
             lines.append(encode_event(ev))
     except Exception as exc:  # noqa: BLE001
         err = {"type": type(exc).__name__, "message": str(exc), "line": getattr(exc, "line", None)}
     return lines, err
 
 
-@pytest.mark.parametrize("sequential", [False, True], ids=["speculative", "sequential"])
+@pytest.mark.parametrize("schedule", ["auto", "group", "sequential"])
 @pytest.mark.parametrize("case", GOLD["cases"], ids=lambda c: c["name"])
-def test_events_match_reference(case, sequential):
-    lines, err = _run(case, sequential)
+def test_events_match_reference(case, schedule):
+    lines, err = _run(case, schedule)
     if "lines" in case and lines != case["lines"]:
         for i, (a, b) in enumerate(zip(lines, case["lines"])):
             assert a == b, f"event {i}"
@@ -98,6 +98,30 @@ def test_large_launch_matches_sequential_mode():
     cfg = sim.NDRangeConfig((n, 1, 1), (256, 1, 1), {"a": [0] * (2 * n), "b": rng.integers(0, 1 << 20, n).tolist()})
     prog = ir.parse_kernel(src)
     a = sim.simulate_trace(prog, cfg)
-    b = sim.simulate_trace(prog, cfg, sequential=True)
-    assert torch.equal(a.kind, b.kind) and torch.equal(a.payload, b.payload)
+    for schedule in ("group", "sequential"):
+        b = sim.simulate_trace(prog, cfg, schedule=schedule)
+        assert torch.equal(a.kind, b.kind) and torch.equal(a.payload, b.payload)
     assert_report_matches(report_to_dict(finalize(consume(a))), oracle.run_trace(a.to_numpy()))
+
+
+def test_schedule_selection():
+    """Private stores stay speculative; a neighbour read after a barrier (a
+    dependence inside the group) takes the group schedule; a chain across
+    groups takes the sequential one."""
+    from paper_1805_04207_b200 import ir, sim
+
+    def schedule_of(src, gsz, lsz, bufs):
+        cfg = sim.NDRangeConfig(gsz, lsz, bufs)
+        launch = sim._Launch(ir.parse_kernel(src), cfg, sim._prepare(ir.parse_kernel(src), cfg), 10 ** 8, 0)
+        try:
+            return launch.schedule
+        finally:
+            launch.close()
+
+    private = "kernel p(a)\nentry:\n  store buf[a][gid0], 1\n  load r0, buf[a][gid0]\n  ret\n"
+    assert schedule_of(private, (64, 1, 1), (8, 1, 1), {"a": [0] * 64}) == "speculative"
+    nb = ("kernel nb(a)\nentry:\n  store buf[a][gid0], gid0\n  barrier\n  add r0, lid0, 1\n  rem r0, r0, lsz0\n"
+          "  sub r1, gid0, lid0\n  add r0, r0, r1\n  load r1, buf[a][r0]\n  ret\n")
+    assert schedule_of(nb, (64, 1, 1), (8, 1, 1), {"a": [0] * 64}) == "group"
+    chain = "kernel c(a)\nentry:\n  load r0, buf[a][gid0]\n  add r1, gid0, 1\n  store buf[a][r1], r0\n  ret\n"
+    assert schedule_of(chain, (64, 1, 1), (8, 1, 1), {"a": [0] * 65}) == "sequential"
