@@ -911,8 +911,9 @@ extern "C" int aiwc_sim_plan(aiwc_sim* sim, const aiwc_sim_launch* L, aiwc_sim_r
   a.stride = stride;
   SCK(sim->regs.grow(stride * a.n_regs * a.wmax * 8));
   SCK(sim->rlen.grow(stride * a.n_regs * 4));
-  SCK(sim->log_e.grow(slots * LOGCAP * 8));
-  SCK(sim->log_v.grow(slots * LOGCAP * 8));
+  // log entry i of slot s lives at [i * stride + s]: the logs span the whole stride
+  SCK(sim->log_e.grow(stride * LOGCAP * 8));
+  SCK(sim->log_v.grow(stride * LOGCAP * 8));
   SCK(sim->smin.grow(std::max<u64>(sim->n_elem, 1) * 8));
   SCK(sim->sown.grow(std::max<u64>(sim->n_elem, 1) * 4));
   SCK(sim->sacc.grow(std::max<u64>(sim->n_elem, 1) * 4));
