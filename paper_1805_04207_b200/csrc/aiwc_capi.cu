@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -93,6 +94,8 @@ struct aiwc_ctx {
   AddrMap am{};
   bool dense = false;
   bool dense32 = false;     // u32 count|flags entries (fewer than 2^30 accesses)
+  bool hot_off = false;     // AIWC_HOT_WINDOW=0 disables the shared-memory hot-key window (measurement)
+  int dense_entry = 0;      // AIWC_DENSE_ENTRY=32|64 forces the entry width (measurement), 0 = rule
   uint64_t ipt_tab_len = 0;
   uint32_t n_ranges = 0, tiles_per_cta = 0;
   uint32_t kernels = 0;
@@ -102,6 +105,8 @@ struct aiwc_ctx {
   cudaEvent_t ev[2 * AIWC_N_PHASES] = {};
   // side stream: the dense table is cleared while pass 1 runs
   cudaStream_t aux = nullptr;
+  cudaStream_t aux2 = nullptr;  // hot-key sampler, concurrent with pass 1
+  cudaEvent_t p1_ev = nullptr, hot_ev = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   size_t pre_zeroed = 0;
   size_t dtab_clean = 0, dtab_used = 0;  // bytes of the dense table cleared after the last finalize / used now
@@ -163,6 +168,8 @@ extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts
     return AIWC_ERR_ARGUMENT;
   }
   *out = ctx;
+  if (const char* de = getenv("AIWC_DENSE_ENTRY")) ctx->dense_entry = atoi(de);
+  if (const char* hw = getenv("AIWC_HOT_WINDOW")) ctx->hot_off = atoi(hw) == 0;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device));
   if (ctx->opts.dense_budget_bytes == 0) {
@@ -182,6 +189,9 @@ extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts
     for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
   }
   CK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->aux2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->p1_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->hot_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming));
   return AIWC_OK;
@@ -206,6 +216,9 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
+  if (ctx->p1_ev) cudaEventDestroy(ctx->p1_ev);
+  if (ctx->hot_ev) cudaEventDestroy(ctx->hot_ev);
   delete ctx;
 }
 
@@ -340,6 +353,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   const uint32_t n_sub = G * P1_SUB;
   CK(grow(ctx->ranges, (size_t)n_sub * sizeof(RangeSum)));
   if (n) {
+    CK(cudaEventRecord(ctx->p1_ev, s));  // the columns (and DevState init) are ready here
     ctx->mark(AIWC_PH_PASS1, 0, s);
     launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s);
     ctx->mark(AIWC_PH_PASS1, 1, s);
@@ -390,8 +404,13 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     am.n_keys = span_keys + 1;
     am.off_max = (span_keys << am.k) | am.low_mask;
     // u32 entries cost a second (flag) RED per access but halve the table:
-    // worth it when the table traffic dominates, i.e. at most one access per key
-    ctx->dense32 = M < E32_MAX_ACCESSES && M <= am.n_keys;
+    // worth it when the table traffic dominates (few accesses per key)
+    // With the hot-key window (keys of one contended 1024-key block counted in shared
+    // memory) the flag RED of the u32 form stays cheap up to a few accesses per key.
+    const bool hot_window = am.n_keys > SMEM_TABLE_KEYS && M >= HOT_MIN_ACCESSES && !ctx->hot_off;
+    ctx->dense32 = M < E32_MAX_ACCESSES && (M <= am.n_keys || (hot_window && M <= 4 * am.n_keys));
+    if (ctx->dense_entry == 32) ctx->dense32 = M < E32_MAX_ACCESSES && am.n_keys > SMEM_TABLE_KEYS;
+    if (ctx->dense_entry == 64) ctx->dense32 = false;
     const bool fits = span_keys < (1ull << 40) && am.n_keys * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
                       am.n_keys <= 4 * M + (1ull << 20);
     // a shard keeps its addresses compacted: they are exchanged with the key owners
@@ -448,7 +467,20 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     a.am = ctx->am;
     a.dense = ctx->dense ? ctx->dtab.p : nullptr;
     a.dense32 = ctx->dense32;
-    a.smem_keys = (ctx->dense && !ctx->dense32 && ctx->am.n_keys <= SMEM_TABLE_KEYS) ? (uint32_t)ctx->am.n_keys : 0u;
+    a.smem_keys = 0; a.hot_lo = 0; a.hot_dev = nullptr;
+    if (ctx->dense && !ctx->dense32 && ctx->am.n_keys <= SMEM_TABLE_KEYS) {
+      a.smem_keys = (uint32_t)ctx->am.n_keys;  // the whole (small) table per CTA
+    } else if (ctx->dense && ctx->am.n_keys > SMEM_TABLE_KEYS && M >= HOT_MIN_ACCESSES && !ctx->hot_off) {
+      // a 1024-key window holding many accesses (shared scratch, lookup tables) is
+      // counted per CTA in shared memory: its keys would otherwise serialise in L2
+      a.smem_keys = SMEM_TABLE_KEYS;
+      a.hot_dev = &st->hot_key;
+      CK(cudaStreamWaitEvent(ctx->aux2, ctx->p1_ev, 0));
+      launch_hot_sample(kind, payload, n, ctx->am, &st->hot_key, ctx->aux2);
+      CK(cudaEventRecord(ctx->hot_ev, ctx->aux2));
+      CK(cudaStreamWaitEvent(s, ctx->hot_ev, 0));
+      ctx->kernels += 1;
+    }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, stage, s));

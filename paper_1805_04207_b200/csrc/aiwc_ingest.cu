@@ -26,6 +26,8 @@
 //          or ordered compaction; rare events in stream order -> segment
 //          closes, branch records, group changes.  Segment closes are
 //          histogrammed after the tile by all threads together.
+#include <type_traits>
+
 #include "aiwc_internal.cuh"
 
 namespace aiwc {
@@ -349,6 +351,9 @@ __global__ void __launch_bounds__(TPB, 2)
   // ---- prologue: smem init + TMA ring fill ----
   for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
   for (uint32_t i = t; i < 2 * a.smem_keys; i += TPB) stab[i] = 0;
+  // shared-memory window of the dense table: [hot_lo, hot_lo + hot_n)
+  const uint64_t hot_lo = a.hot_dev ? *a.hot_dev : a.hot_lo;
+  const uint32_t hot_n = hot_lo == ~0ull ? 0u : a.smem_keys;
   if (t == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
     fence_barrier_init();
@@ -619,32 +624,44 @@ __global__ void __launch_bounds__(TPB, 2)
       const uint64_t base = a.am.base, off_max = a.am.off_max;
       const uint32_t k = a.am.k, lmask = (uint32_t)a.am.low_mask, lconst = (uint32_t)a.am.low_const;
       uint32_t inval = 0;
-      if (a.dense32) {
-        uint32_t* const tab = static_cast<uint32_t*>(a.dense);
-        for (uint32_t i = lane; i < n_mem; i += 32) {
-          const uint32_t e = midx[i];
-          const uint64_t off = pay[e & 0x0FFFu] - base;
-          const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
-          inval |= !v;
-          if (v) {
-            uint32_t* const q = tab + (off >> k);
-            atomicAdd(q, 1u);
-            atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
+      // the window check is compiled in only when a window exists (CTA-uniform branch)
+      auto fold = [&](auto with_window) {
+        constexpr bool HOT = decltype(with_window)::value;
+        if (a.dense32) {
+          uint32_t* const tab = static_cast<uint32_t*>(a.dense);
+          for (uint32_t i = lane; i < n_mem; i += 32) {
+            const uint32_t e = midx[i];
+            const uint64_t off = pay[e & 0x0FFFu] - base;
+            const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
+            inval |= !v;
+            if (v) {
+              const uint64_t key = off >> k, rel = key - hot_lo;
+              if (HOT && rel < hot_n) {
+                atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+              } else {
+                uint32_t* const q = tab + key;
+                atomicAdd(q, 1u);
+                atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
+              }
+            }
+          }
+        } else {
+          unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
+          for (uint32_t i = lane; i < n_mem; i += 32) {
+            const uint32_t e = midx[i];
+            const uint64_t off = pay[e & 0x0FFFu] - base;
+            const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
+            inval |= !v;
+            if (v) {
+              const uint64_t key = off >> k, rel = key - hot_lo;
+              if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+              else atomicAdd(tab + key, (e & 0x8000u) ? (1ull << 32) : 1ull);
+            }
           }
         }
-      } else {
-        unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
-        for (uint32_t i = lane; i < n_mem; i += 32) {
-          const uint32_t e = midx[i];
-          const uint64_t off = pay[e & 0x0FFFu] - base;
-          const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
-          inval |= !v;
-          if (v) {
-            if (a.smem_keys) atomicAdd(&stab[((e >> 15) ? a.smem_keys : 0u) + (uint32_t)(off >> k)], 1u);
-            else atomicAdd(tab + (off >> k), (e & 0x8000u) ? (1ull << 32) : 1ull);
-          }
-        }
-      }
+      };
+      if (hot_n) fold(std::true_type{});
+      else fold(std::false_type{});
       if (inval) flags |= F_ADDR_HINT;
     }
     for (uint32_t m = DENSE ? 0u : (rd16 | wr16); m; m &= m - 1) {
@@ -729,12 +746,19 @@ __global__ void __launch_bounds__(TPB, 2)
   }
 
   // ---- epilogue: flush CTA-private state ----
-  if (DENSE && a.smem_keys) {
+  if (DENSE && hot_n) {
     __syncthreads();
-    unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
-    for (uint32_t i = t; i < a.smem_keys; i += TPB) {
-      const uint32_t r = stab[i], w = stab[a.smem_keys + i];
-      if (r | w) atomicAdd(tab + i, (unsigned long long)r | ((unsigned long long)w << 32));
+    for (uint32_t i = t; i < hot_n; i += TPB) {
+      const uint32_t r = stab[i], w = stab[hot_n + i];
+      if (!(r | w)) continue;
+      if (a.dense32) {
+        uint32_t* const q = static_cast<uint32_t*>(a.dense) + hot_lo + i;
+        atomicAdd(q, r + w);
+        atomicOr(q, (r ? E32_READ : 0u) | (w ? E32_WRITE : 0u));
+      } else {
+        atomicAdd(static_cast<unsigned long long*>(a.dense) + hot_lo + i,
+                  (unsigned long long)r | ((unsigned long long)w << 32));
+      }
     }
   }
   if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
@@ -770,6 +794,74 @@ __global__ void __launch_bounds__(TPB, 2)
       atomicAnd(&st->addr_and, aand); atomicOr(&st->addr_or, aor);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// hot-key window choice: one CTA samples HS_SAMPLES events at hashed positions,
+// counts the 1024-key blocks of the sampled memory accesses in a shared hash
+// table and elects the most frequent block when it carries >= 1/64 of them.
+// Keys of that block are then counted in shared memory by every ingest CTA
+// (contended same-address REDs become one add per key per CTA).
+// ---------------------------------------------------------------------------
+constexpr int HS_T = 1024, HS_SAMPLES = 4096, HS_SLOTS = 4096;
+
+__global__ void __launch_bounds__(HS_T) hot_sample_kernel(const uint8_t* __restrict__ kind,
+                                                          const uint64_t* __restrict__ payload, uint64_t n,
+                                                          AddrMap am, unsigned long long* hot_out) {
+  __shared__ uint32_t hk[HS_SLOTS], hc[HS_SLOTS];
+  __shared__ unsigned long long red[HS_T / 32];
+  __shared__ uint32_t rmem[HS_T / 32];
+  const int t = threadIdx.x;
+  for (int i = t; i < HS_SLOTS; i += HS_T) { hk[i] = ~0u; hc[i] = 0; }
+  __syncthreads();
+  uint32_t nmem = 0;
+  constexpr int PER = HS_SAMPLES / HS_T;
+  uint64_t pos[PER], pv[PER];
+  uint8_t kk[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    uint64_t x = (uint64_t)(t * PER + j) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    x = (x ^ (x >> 31)) * 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    pos[j] = x % n;
+  }
+  // all loads in flight at once (kind and payload independently): two memory round trips
+#pragma unroll
+  for (int j = 0; j < PER; ++j) { kk[j] = kind[pos[j]]; pv[j] = payload[pos[j]]; }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    if (!is_mem(kk[j])) continue;
+    const uint64_t off = pv[j] - am.base;
+    if (off > am.off_max || (off & am.low_mask) != am.low_const) continue;
+    const uint32_t blk = (uint32_t)((off >> am.k) >> 10);
+    ++nmem;
+    uint32_t h = (blk * 2654435761u) >> 20;  // 12-bit slot
+    for (int probe = 0; probe < 64; ++probe, h = (h + 1) & (HS_SLOTS - 1)) {
+      const uint32_t old = atomicCAS(&hk[h], ~0u, blk);
+      if (old == ~0u || old == blk) { atomicAdd(&hc[h], 1u); break; }
+    }
+  }
+  __syncthreads();
+  unsigned long long best = 0;  // count << 32 | block
+  for (int i = t; i < HS_SLOTS; i += HS_T)
+    if (hc[i]) best = max(best, ((unsigned long long)hc[i] << 32) | hk[i]);
+  nmem = warp_sum(nmem);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((t & 31) == 0) { red[t >> 5] = best; rmem[t >> 5] = nmem; }
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long b = 0;
+    uint32_t m = 0;
+    for (int w = 0; w < HS_T / 32; ++w) { b = max(b, red[w]); m += rmem[w]; }
+    const uint32_t cnt = (uint32_t)(b >> 32);
+    *hot_out = (cnt >= 16 && 64ull * cnt >= m) ? (unsigned long long)(uint32_t)b << 10 : ~0ull;
+  }
+}
+
+void launch_hot_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n, const AddrMap& am,
+                       unsigned long long* hot_out, cudaStream_t s) {
+  hot_sample_kernel<<<1, HS_T, 0, s>>>(kind, payload, n, am, hot_out);
 }
 
 template <bool DENSE, bool STAGE>

@@ -71,6 +71,7 @@ struct DevState {
   // ---- not copied back ----
   unsigned long long host_end;
   unsigned long long cnt_hist[NLEVELS][CBINS];      // count-of-counts per level (entropy)
+  unsigned long long hot_key;                       // hot_sample_kernel: first key of the hot window, ~0 none
 };
 
 // Memory-path description shared by the ingest and the dense-table kernels.
@@ -84,7 +85,8 @@ struct AddrMap {
   uint64_t off_max;    // largest valid addr - base: ((n_keys - 1) << k) | low_mask
 };
 
-constexpr uint32_t SMEM_TABLE_KEYS = 1024;  // small dense tables live in shared memory per CTA
+constexpr uint32_t SMEM_TABLE_KEYS = 1024;  // small dense tables / the hot window live in shared memory per CTA
+constexpr uint64_t HOT_MIN_ACCESSES = 1ull << 20;  // traces with fewer accesses skip the hot-window sampler
 constexpr int PRES_TILES = 16;         // width presence granularity (tile iterations per mask)
 
 struct IngestArgs {
@@ -110,8 +112,11 @@ struct IngestArgs {
   void* dense;                      // dense mode: [am.n_keys] u32 (dense32) or u64 entries
   uint32_t dense32;
   uint32_t pres_blocks;
-  uint32_t smem_keys;               // > 0: the (u64-format) dense table has this few keys and is
-                                    // accumulated per CTA in shared memory, flushed once at the end             // width presence masks per CTA (width_presence[cta * pres_blocks + it / 16])
+  uint32_t smem_keys;               // > 0: keys [hot_lo, hot_lo + smem_keys) of the dense table are
+                                    // accumulated per CTA in shared memory (read / write u32 counters)
+                                    // and added to the table once at the end
+  uint64_t hot_lo;                  // window base when hot_dev is null (small tables: 0)
+  const unsigned long long* hot_dev;  // device-chosen window base (hot_sample_kernel), ~0 = no window
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
@@ -221,6 +226,10 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
                   uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s);
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
                           bool dense, bool stage, cudaStream_t s);  // smem grows by 8 * a.smem_keys
+// hot-key window: samples memory events, writes the most frequent 1024-key block of the
+// dense table (when it holds >= 1/64 of the sampled accesses) to *hot_out, else ~0
+void launch_hot_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n, const AddrMap& am,
+                       unsigned long long* hot_out, cudaStream_t s);
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
                         uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
