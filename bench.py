@@ -310,6 +310,7 @@ def run_ours(args) -> None:
     ingest_ms = phase_med["ingest"]
     achieved = ALG_BYTES_PER_EVENT * count / (ingest_ms / 1e3) / 1e9
     step_alg = ALG_BYTES_PER_EVENT * count / (ms_step / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(cfg) if world == 1 else (None, None)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -329,7 +330,9 @@ def run_ours(args) -> None:
                     "path": "consume(ColumnarTrace on pinned host)+finalize" if world == 1 else
                             "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "aiwc::ingest_kernel",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
+                         "traffic_source": traffic_src, "alg_bytes": ALG_BYTES_PER_EVENT * count,
+                         "kernel": "aiwc::ingest_kernel",
                          "peak_source": peak_src, "alg_bytes_per_event": ALG_BYTES_PER_EVENT,
                          "step_alg_gbs": step_alg, "step_frac": step_alg / peak},
             "phases_ms": phase_med,
@@ -343,6 +346,18 @@ def run_ours(args) -> None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_traffic(cfg: int):
+    """DRAM bytes (read + write) per launch of the ingest kernel on this config, from the
+    committed `ncu --set full` capture (tools/ncu_traffic.py), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", f"ncu_traffic_C{cfg}.json")
+    try:
+        with open(path, encoding="utf-8") as fp:
+            d = json.load(fp)
+        return d["traffic_bytes"], d.get("source")
+    except (OSError, ValueError, KeyError):
+        return None, None
 
 
 def cpu_baseline(cfg, w, args):
