@@ -193,6 +193,54 @@ def _timed(step, steps, stream, dev, world, local):
     return ms, wall, clk.summary()
 
 
+def _timed_lanes(lane_step, streams, steps, phases, kernels, stream, local):
+    """K steps split over len(streams) host threads (one engine context and CUDA
+    stream each), between CUDA events on `stream` that every lane stream joins."""
+    import torch
+
+    from paper_1805_04207_b200 import _native
+
+    n = len(streams)
+    share = [steps // n + (1 if i < steps % n else 0) for i in range(n)]
+    out = [[] for _ in range(n)]
+    errs = []
+
+    def run(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                for _ in range(share[i]):
+                    out[i].append(lane_step(i))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        start.record(stream)
+        for s in streams:
+            s.wait_event(start)
+        th = [threading.Thread(target=run, args=(i,)) for i in range(n)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for s in streams:
+            stream.wait_stream(s)
+        end.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+    if errs:
+        raise errs[0]
+    for res in out:
+        for ph, k in res:
+            for i, p in enumerate(_native.PHASES):
+                phases[p].append(ph[i])
+            kernels[0] += k
+    return start.elapsed_time(end), wall, clk.summary()
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -219,19 +267,31 @@ def run_ours(args) -> None:
     stream = torch.cuda.current_stream(dev)
     res = _native.Result()
 
+    n_streams = max(1, args.streams) if world == 1 else 1
     if world == 1:
-        ctx = _native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING)
-        lib = ctx.lib
+        # one engine context per CUDA stream; with several, concurrent host threads
+        # each push whole trace -> report steps (the reference allows distinct
+        # streams to run concurrently, pkg/README.md:192-193), so one stream's
+        # small kernels and host round trip overlap another stream's ingest
         info = trace_info(tr)
         kptr = ctypes.c_void_p(tr.kind.data_ptr())
         pptr = ctypes.c_void_p(tr.payload.data_ptr())
-        sptr = ctypes.c_void_p(stream.cuda_stream)
+        lanes = []
+        for i in range(n_streams):
+            cs = stream if i == 0 else torch.cuda.Stream(dev)
+            lanes.append((_native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING), cs,
+                          _native.Result()))
 
-        def step():
+        def lane_step(i):
+            ctx, cs, r = lanes[i]
+            lib, sptr = ctx.lib, ctypes.c_void_p(cs.cuda_stream)
             ctx.check(lib.aiwc_reset(ctx.h))
             ctx.check(lib.aiwc_ingest(ctx.h, kptr, pptr, ctypes.byref(info), sptr))
-            ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), sptr))
-            return list(res.phase_ms), res.kernels_launched
+            ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(r), sptr))
+            return list(r.phase_ms), r.kernels_launched
+
+        def step():
+            return lane_step(0)
     else:
         backend = D.CudaBackend(local, timing=True)
 
@@ -251,7 +311,19 @@ def run_ours(args) -> None:
 
     for _ in range(max(3, args.warmup)):
         step()
-    ms, _, clocks = _timed(timed_step, args.steps, stream, dev, world, local)
+    if n_streams > 1:
+        for i in range(1, n_streams):
+            for _ in range(max(3, args.warmup)):
+                lane_step(i)
+        ms, _, clocks = _timed_lanes(lane_step, [c[1] for c in lanes], args.steps, {p: [] for p in phases}, kernels,
+                                     stream, local)
+        # per-kernel (phase) times for the roofline come from a separate single-stream
+        # run: overlapping streams stretch each kernel's event-to-event duration
+        k_timed = kernels[0]
+        _timed(timed_step, args.steps, stream, dev, world, local)
+        kernels[0] = k_timed
+    else:
+        ms, _, clocks = _timed(timed_step, args.steps, stream, dev, world, local)
     ms_step = ms / args.steps
     value = n_total / (ms_step / 1e3)
     phase_med = {p: statistics.median(v) for p, v in phases.items()}
@@ -323,10 +395,11 @@ def run_ours(args) -> None:
             "config": {"workload": f"C{cfg} {synth.NAMES[cfg]}: {total_wi} work-items ({n_total} events), "
                                    f"local {synth.LOCAL[cfg]}, {world} work-group shard(s)",
                        "events_per_rank": count, "l2": "trace (9 B/event) larger than L2; no flush needed",
-                       "parallelism": "replica (N=1)" if world == 1 else
+                       "streams": n_streams,
+                       "parallelism": f"replica (N=1), {n_streams} concurrent trace streams" if world == 1 else
                                       f"work-group shards x{world}; NCCL all-reduce + address all-to-all"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
-                    "d2h_bytes_per_step": res.d2h_bytes if world == 1 else backend.last_d2h, "ms_per_step": e2e_ms,
+                    "d2h_bytes_per_step": lanes[0][2].d2h_bytes if world == 1 else backend.last_d2h, "ms_per_step": e2e_ms,
                     "path": "consume(ColumnarTrace on pinned host)+finalize" if world == 1 else
                             "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -395,6 +468,8 @@ def main():
     ap.add_argument("--ref-sample-wi", type=int, default=1 << 21)
     ap.add_argument("--ref-python-gen", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="N=1: engine contexts / CUDA streams with whole steps in flight concurrently")
     ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":

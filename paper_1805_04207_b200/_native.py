@@ -14,7 +14,7 @@ import threading
 from .errors import AiwcError, DeviceError, InvalidStream, TraceTooLarge, UnsupportedTrace
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libaiwc_b200.so")
+LIB_PATH = os.environ.get("AIWC_LIB") or os.path.join(HERE, "libaiwc_b200.so")  # AIWC_LIB: measurement builds
 
 OK, ERR_INVALID_STREAM, ERR_TOO_LARGE, ERR_INCONSISTENT, ERR_UNSUPPORTED, ERR_ARGUMENT, ERR_CUDA, ERR_NCCL = range(8)
 OPT_NO_CONSERVATION = 1  # Python's finalize() runs the reference's conservation checks itself

@@ -30,6 +30,11 @@
 
 #include "aiwc_internal.cuh"
 
+// AIWC_ABL: measurement-only ablation builds (tools/dbg/ablate.sh); 0 in the product
+#ifndef AIWC_ABL
+#define AIWC_ABL 0
+#endif
+
 namespace aiwc {
 
 // ---------------------------------------------------------------------------
@@ -559,8 +564,10 @@ __global__ void __launch_bounds__(TPB, 2)
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // chunk c = events 2c, 2c + 1
         const uint4 v = prow4[c ^ sw];
-        if ((v.y | (v.x - 1u)) > 15u) bad |= 1u << (2 * c);
-        if ((v.w | (v.z - 1u)) > 15u) bad |= 2u << (2 * c);
+        if (!(AIWC_ABL & 16)) {
+          if ((v.y | (v.x - 1u)) > 15u) bad |= 1u << (2 * c);
+          if ((v.w | (v.z - 1u)) > 15u) bad |= 2u << (2 * c);
+        }
         lo2[c] = __byte_perm(v.x, v.z, 0x0040);  // width bytes of events 2c, 2c + 1
         hi2[c] = __byte_perm(v.y, v.w, 0x0040);  // opcode bytes
       }
@@ -576,7 +583,7 @@ __global__ void __launch_bounds__(TPB, 2)
       op[0] = o01 & 0xFFFFu; op[1] = o01 >> 16; op[2] = o23 & 0xFFFFu; op[3] = o23 >> 16;
       wp[0] = w01 & 0xFFFFu; wp[1] = w01 >> 16; wp[2] = w23 & 0xFFFFu; wp[3] = w23 >> 16;
     }
-    {
+    if (!(AIWC_ABL & 1)) {
       const uint32_t fast = ins16 & ~bad;
       uint32_t q[4], r[4];
       q[0] = fast & ~op[0] & ~op[1]; q[1] = fast & op[0] & ~op[1]; q[2] = fast & ~op[0] & op[1]; q[3] = fast & op[0] & op[1];
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(TPB, 2)
       }
     }
     // memory accesses: dense-table counters (warp-coalesced) or ordered compaction
-    if (DENSE) {
+    if (DENSE && !(AIWC_ABL & 2)) {
       // my accesses go to the warp's list (pre-swizzled smem index | write << 15)
       // at my in-warp exclusive offset ...
       const uint32_t bx = Bi - B;
@@ -641,7 +648,7 @@ __global__ void __launch_bounds__(TPB, 2)
               } else {
                 uint32_t* const q = tab + key;
                 atomicAdd(q, 1u);
-                atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
+                if (!(AIWC_ABL & 4)) atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
               }
             }
           }
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(TPB, 2)
     // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
-    for (uint32_t m = rare16; m; m &= m - 1) {
+    for (uint32_t m = (AIWC_ABL & 8) ? 0u : rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t k = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
