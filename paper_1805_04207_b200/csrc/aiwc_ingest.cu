@@ -281,6 +281,32 @@ __device__ __forceinline__ uint32_t nibble_planes(uint32_t b0, uint32_t b1, uint
   return __byte_perm(x, y, 0x5140);
 }
 
+// Bin counts of 16 events from the 4 bit-planes of their values: bin v gets
+// popc(minterm_v & fast), two bins per packed 32-bit counter (bin 2i low, 2i + 1
+// high).  Planes 2 / 3 that no fast event of the warp sets are skipped
+// (warp-uniform votes): traces with few opcode ids / narrow widths pay for 4 or 8
+// minterms instead of 16.
+__device__ __forceinline__ void bin_counts(uint32_t (&acc)[8], const uint32_t (&p)[4], uint32_t fast) {
+  uint32_t q[4];
+  q[0] = fast & ~p[0] & ~p[1]; q[1] = fast & p[0] & ~p[1]; q[2] = fast & ~p[0] & p[1]; q[3] = fast & p[0] & p[1];
+  const bool hi3 = __any_sync(0xffffffffu, fast & p[3]);
+  const bool hi2 = __any_sync(0xffffffffu, fast & p[2]);
+  if (!hi3 && !hi2) {
+    acc[0] += __popc(q[0]) + (__popc(q[1]) << 16);
+    acc[1] += __popc(q[2]) + (__popc(q[3]) << 16);
+  } else if (!hi3) {
+    const uint32_t r[2] = {~p[2], p[2]};
+#pragma unroll
+    for (int v = 0; v < 8; v += 2)
+      acc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
+  } else {
+    const uint32_t r[4] = {~p[2] & ~p[3], p[2] & ~p[3], ~p[2] & p[3], p[2] & p[3]};
+#pragma unroll
+    for (int v = 0; v < 16; v += 2)
+      acc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
+  }
+}
+
 // One segment close (metrics.py:156-174): ITB sample (barrier always, wi_end when
 // non-empty); IPT either straight to the histogram (work-item never crossed a
 // barrier) or accumulated in the work-item's lifetime slot.
@@ -585,17 +611,8 @@ __global__ void __launch_bounds__(TPB, 2)
     }
     if (!(AIWC_ABL & 1)) {
       const uint32_t fast = ins16 & ~bad;
-      uint32_t q[4], r[4];
-      q[0] = fast & ~op[0] & ~op[1]; q[1] = fast & op[0] & ~op[1]; q[2] = fast & ~op[0] & op[1]; q[3] = fast & op[0] & op[1];
-      r[0] = ~op[2] & ~op[3]; r[1] = op[2] & ~op[3]; r[2] = ~op[2] & op[3]; r[3] = op[2] & op[3];
-#pragma unroll
-      for (int v = 0; v < 16; v += 2)
-        oacc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
-      q[0] = fast & ~wp[0] & ~wp[1]; q[1] = fast & wp[0] & ~wp[1]; q[2] = fast & ~wp[0] & wp[1]; q[3] = fast & wp[0] & wp[1];
-      r[0] = ~wp[2] & ~wp[3]; r[1] = wp[2] & ~wp[3]; r[2] = ~wp[2] & wp[3]; r[3] = wp[2] & wp[3];
-#pragma unroll
-      for (int v = 0; v < 16; v += 2)
-        wacc[v >> 1] += __popc(q[v & 3] & r[v >> 2]) + (__popc(q[(v + 1) & 3] & r[v >> 2]) << 16);
+      bin_counts(oacc, op, fast);
+      bin_counts(wacc, wp, fast);
     }
     // the rest one by one: opcodes >= 16, widths outside 1..16
     for (uint32_t m = ins16 & bad; m; m &= m - 1) {
