@@ -32,7 +32,7 @@
 
 namespace aiwc {
 
-constexpr int PC_T = 512;                 // threads per counting block
+constexpr int PC_T = 1024;                // threads per counting block (one block per SM: loads in flight)
 constexpr int PC_PER = 32;                // records per thread per step
 constexpr int PC_HALO = 16;               // warm-up window (>= history_len)
 constexpr int PC_PART_BITS = 14;          // patterns per partition: 2^14 (128 KB of counters)
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   for (uint32_t i = threadIdx.x; i < 2 * part_size; i += PC_T) cnt[i] = 0;
   __syncthreads();
   const uint64_t c0 = (uint64_t)chunk * chunk_len, c1 = min(n, c0 + chunk_len);
-  // coalesced 16-byte loads, four in flight per thread; equal neighbours inside a
+  // coalesced 16-byte loads, eight in flight per thread; equal neighbours inside a
   // load are merged before touching shared memory (loop back-edges repeat one
   // pattern for long stretches and would serialise on one bin)
   auto add = [&](uint32_t c, uint32_t k) {
@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   const uint4* q4 = reinterpret_cast<const uint4*>(code);
   const uint64_t nq = v1 > v0 ? (v1 - v0) / 4 : 0, q0 = v0 / 4;
   uint64_t j = threadIdx.x;
-  for (; j + 3 * PC_T < nq; j += 4 * PC_T) {
-    const uint4 a0 = __ldcs(q4 + q0 + j), a1 = __ldcs(q4 + q0 + j + PC_T);
-    const uint4 a2 = __ldcs(q4 + q0 + j + 2 * PC_T), a3 = __ldcs(q4 + q0 + j + 3 * PC_T);
-    count4(a0); count4(a1); count4(a2); count4(a3);
+  for (; j + 7 * PC_T < nq; j += 8 * PC_T) {  // eight 16-byte loads in flight per thread
+    uint4 a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldcs(q4 + q0 + j + u * PC_T);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) count4(a[u]);
   }
   for (; j < nq; j += PC_T) count4(__ldcs(q4 + q0 + j));
   for (uint64_t i = max(v1, v0) + threadIdx.x; i < c1; i += PC_T) add(code[i], 1);
