@@ -107,7 +107,7 @@ void scan_exclusive_u64(unsigned long long* d, uint64_t n, unsigned long long* s
 // ---------------------------------------------------------------------------
 // stable LSD radix sort, 8-bit digits
 // ---------------------------------------------------------------------------
-constexpr int RS_T = 256, RS_I = 8, RS_TILE = RS_T * RS_I;  // 2048 keys per block
+constexpr int RS_T = 256, RS_I = 16, RS_TILE = RS_T * RS_I;  // 4096 keys per block
 constexpr int RS_W = RS_T / 32;
 
 size_t radix_hist_bytes(uint64_t n) {
@@ -124,11 +124,16 @@ __global__ void __launch_bounds__(RS_T) radix_hist_kernel(const uint64_t* __rest
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t base = (uint64_t)blockIdx.x * RS_TILE + (uint64_t)warp * 32 * RS_I;
+  // all loads in flight before the first shared-memory atomic
+  uint32_t d[RS_I];
 #pragma unroll
   for (int j = 0; j < RS_I; ++j) {
     const uint64_t i = base + 32 * j + lane;
-    if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> shift) & mask], 1u);
+    d[j] = i < n ? (uint32_t)(__ldcs(keys + i) >> shift) & mask : 256u;
   }
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j)
+    if (d[j] < 256u) atomicAdd(&h[d[j]], 1u);
   __syncthreads();
   for (int d = threadIdx.x; d < 256; d += RS_T) hist[(uint64_t)d * nb + blockIdx.x] = h[d];
 }
@@ -145,9 +150,13 @@ __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __r
   uint64_t k[RS_I];
   uint32_t d[RS_I];
 #pragma unroll
+  for (int j = 0; j < RS_I; ++j) {  // all loads in flight before the first atomic
+    const uint64_t i = base + 32 * j + lane;
+    k[j] = i < n ? __ldcs(keys + i) : 0ull;
+  }
+#pragma unroll
   for (int j = 0; j < RS_I; ++j) {
     const uint64_t i = base + 32 * j + lane;
-    k[j] = i < n ? keys[i] : 0ull;
     d[j] = i < n ? ((uint32_t)(k[j] >> shift) & mask) : 256u;
     if (i < n) atomicAdd(&cnt[warp][d[j]], 1u);
   }
