@@ -287,11 +287,19 @@ __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restr
       if (!(presence[c * pres_blocks + b] & bit)) continue;
     }
     const uint64_t base = tile * TILE;
-#pragma unroll 4
+    // all 32 loads of the tile in flight at once (one memory round trip)
+    uint8_t k[16];
+    uint32_t p[16];
+#pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint64_t e = base + (uint64_t)j * 256 + threadIdx.x;
-      if (e < n && kind[e] == AIWC_K_INSTR && (uint32_t)payload[e] == w) {
-        atomicMin(&s_pos, (unsigned long long)e);
+      k[j] = e < n ? kind[e] : 0;
+      p[j] = e < n ? (uint32_t)payload[e] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (k[j] == AIWC_K_INSTR && p[j] == w) {
+        atomicMin(&s_pos, base + (uint64_t)j * 256 + threadIdx.x);
         break;
       }
     }
