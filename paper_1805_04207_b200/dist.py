@@ -218,8 +218,6 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
     """Every rank: exact whole-trace EngineResult from its work-group shard."""
     import torch.distributed as dist
 
-    from .metrics import EngineResult
-
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     device = comm_device(backend, group)
@@ -242,19 +240,7 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
 
     # ---- gathers: overflow values, widths, sites ----
     parts = _gather_objects((sp.itb_ovf.tolist(), sp.ipt_ovf.tolist(), sp.widths, sp.sites), group)
-    itb_ovf = np.sort(np.array([v for p in parts for v in p[0]], dtype=np.uint64))
-    ipt_ovf = np.sort(np.array([v for p in parts for v in p[1]], dtype=np.uint64))
-    wmap: dict = {}
-    for p in parts:
-        for w, c, first in p[2]:
-            c0, f0 = wmap.get(w, (0, None))
-            wmap[w] = (c0 + c, first if f0 is None else min(f0, first))
-    widths = [(w, c) for w, (c, _) in sorted(wmap.items(), key=lambda kv: kv[1][1])]
-    smap: dict = {}
-    for p in parts:
-        for s, c in p[3].items():
-            smap[s] = smap.get(s, 0) + c
-    sites = sorted(smap.items())
+    itb_ovf, ipt_ovf, widths, sites = _merge_lists(parts)
 
     # ---- addresses: global key map, owner exchange, owner partials ----
     total_m = total_reads + total_writes
@@ -278,8 +264,18 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
     big = np.sort(np.array([v for b in _gather_objects(mp.big.tolist(), group) for v in b], dtype=np.uint64))[::-1]
     unique_r, unique_w, footprint = (int(v) for v in msum[:3])
     hist0 = msum[3:]
+    return _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum,
+                     br_exec, opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, branch_table, widths, sites,
+                     unique_r, unique_w, footprint, hist0, big, level_sum)
 
-    # ---- finish with the same exact rules as aiwc_finalize ----
+
+def _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec,
+              opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, branch_table, widths, sites, unique_r, unique_w,
+              footprint, hist0, big, level_sum):
+    """EngineResult of combined exact integers, finished with the same rules as aiwc_finalize."""
+    from .metrics import EngineResult
+
+    total_m = total_reads + total_writes
     yokota, linear, observations = branch_entropies(branch_table)
     ent = [-float(v) for v in level_sum] if total_m else [0.0] * 11
     oc = sorted((c for c in opcode_counts if c), reverse=True)
@@ -294,6 +290,95 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
         yokota=yokota, linear=linear, entries=unique_r + unique_w + br_exec,
         opcode_counts=opcode_counts, widths=widths, sites=sites, used_dense_table=True, kernels_launched=0,
     )
+
+
+def _merge_lists(parts):
+    """Overflow samples, width list (first appearance order) and site counts of shard partials."""
+    itb_ovf = np.sort(np.array([v for p in parts for v in p[0]], dtype=np.uint64))
+    ipt_ovf = np.sort(np.array([v for p in parts for v in p[1]], dtype=np.uint64))
+    wmap: dict = {}
+    for p in parts:
+        for w, c, first in p[2]:
+            c0, f0 = wmap.get(w, (0, None))
+            wmap[w] = (c0 + c, first if f0 is None else min(f0, first))
+    widths = [(w, c) for w, (c, _) in sorted(wmap.items(), key=lambda kv: kv[1][1])]
+    smap: dict = {}
+    for p in parts:
+        for s, c in p[3].items():
+            smap[s] = smap.get(s, 0) + c
+    return itb_ovf, ipt_ovf, widths, sorted(smap.items())
+
+
+def chunk_cuts(kind, limit: int) -> list[int]:
+    """Cut points (event indices) splitting a trace into chunks of at most `limit`
+    events, each cut at a wg_begin, so every work-group, segment and (site, group)
+    branch stream lies inside one chunk."""
+    from .trace import K_WG_BEGIN
+
+    if type(kind).__module__.startswith("torch"):
+        import torch
+
+        starts = torch.nonzero(kind == K_WG_BEGIN).flatten().cpu().numpy()
+    else:
+        starts = np.nonzero(np.asarray(kind) == K_WG_BEGIN)[0]
+    n = int(kind.shape[0])
+    cuts = [0]
+    while n - cuts[-1] > limit:
+        # the last group start that keeps this chunk within the limit
+        i = int(np.searchsorted(starts, cuts[-1] + limit, side="right")) - 1
+        if i < 0 or int(starts[i]) <= cuts[-1]:
+            from .errors import UnsupportedTrace
+
+            raise UnsupportedTrace(f"a work-group spans more than {limit} events")
+        cuts.append(int(starts[i]))
+    cuts.append(n)
+    return cuts
+
+
+def chunked_result(backend, tr, cuts: list[int]):
+    """One trace larger than one ingest allows, on one GPU: each chunk (whole
+    work-groups) is a shard pass; sums and lists combine as across ranks, and the
+    chunks' compacted addresses are finished by one owner (this GPU)."""
+    import torch
+
+    from .trace import ColumnarTrace
+
+    parts, rd, wr = [], [], []
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        sub = ColumnarTrace(tr.kind[lo:hi], tr.payload[lo:hi], tr.kernel_name, tr.invocation, tr.global_size,
+                            tr.local_size, tr.opcodes, tr.extra_groups, None, validated=True)
+        sp = backend.shard(sub, lo)
+        r, w = backend.addresses(sp)
+        parts.append(sp)
+        rd.append(r.clone())
+        wr.append(w.clone())
+    tot = lambda f: sum(int(getattr(p, f)) for p in parts)  # noqa: E731
+    n_events, total_instr, work_items, barriers = tot("n_events"), tot("total_instructions"), tot("work_items"), \
+        tot("barriers_hit")
+    total_reads, total_writes = tot("total_reads"), tot("total_writes")
+    itb_sum, ipt_sum, br_exec = tot("itb_sum"), tot("ipt_sum"), tot("branch_executions")
+    opcode_counts = [int(v) for v in np.sum([p.opcode_counts.astype(np.uint64) for p in parts], axis=0)]
+    itb_hist = np.sum([p.itb_hist for p in parts], axis=0)
+    ipt_hist = np.sum([p.ipt_hist for p in parts], axis=0)
+    branch_table = np.sum([p.branch_table.astype(np.uint64) for p in parts], axis=0)
+    itb_ovf, ipt_ovf, widths, sites = _merge_lists(
+        [(p.itb_ovf.tolist(), p.ipt_ovf.tolist(), p.widths, p.sites) for p in parts])
+    total_m = total_reads + total_writes
+    if total_m:
+        st = [p.addr_stats for p in parts if p.addr_stats is not None]
+        stats = (min(s[0] for s in st), max(s[1] for s in st), int(np.bitwise_and.reduce([np.uint64(s[2]) for s in st])),
+                 int(np.bitwise_or.reduce([np.uint64(s[3]) for s in st])))
+        km = key_map(stats, 1)
+        reads = torch.cat(rd) if total_reads else torch.zeros(1, dtype=torch.int64, device=backend.device)
+        writes = torch.cat(wr) if total_writes else torch.zeros(1, dtype=torch.int64, device=backend.device)
+        mp = backend.memory_partial(reads, total_reads, writes, total_writes, km, 0, km.n_keys, total_m)
+    else:
+        mp = MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(CBINS, np.uint64), np.zeros(0, np.uint64))
+    big = np.sort(mp.big.astype(np.uint64))[::-1]
+    return _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum,
+                     br_exec, opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, branch_table, widths, sites,
+                     mp.unique_reads, mp.unique_writes, mp.footprint, mp.cnt_hist0.astype(np.uint64), big,
+                     np.asarray(mp.level_sum, dtype=np.float64))
 
 
 def sharded_report(backend, shard, shard_offset: int, kernel_name: str, invocation: int, global_size, local_size,
@@ -373,6 +458,19 @@ class CudaBackend:
             sites=dict(r.sites), branch_executions=r.branch_executions,
             addr_stats=tuple(int(v) for v in t.addr_stats) if (r.total_reads + r.total_writes) else None,
         )
+
+    def addresses(self, sp: ShardPartial):
+        """Zero-copy device views of the last shard's compacted read / write addresses."""
+        import torch
+
+        from . import _native
+
+        ctx = self._ctx()
+        t = _native.ShardTables()
+        ctx.check(ctx.lib.aiwc_shard_tables_get(ctx.h, ctypes.byref(t)))
+        view = lambda p, n: torch.as_tensor(_CudaArray(ctypes.cast(p, ctypes.c_void_p).value, max(n, 1)),  # noqa: E731
+                                            device=self.device)[:n]
+        return view(t.rd_dev, int(sp.total_reads)), view(t.wr_dev, int(sp.total_writes))
 
     def partition(self, sp: ShardPartial, km: KeyMap, nranks: int):
         import torch

@@ -223,11 +223,25 @@ def validate_columnar(tr: ColumnarTrace, device: int | None = None) -> tuple | N
         _put_ctx(ctx)
 
 
+def max_ingest_events() -> int:
+    """Events one aiwc_ingest takes (the engine's u32 event indices); larger traces
+    are cut at work-group starts and combined exactly (dist.chunked_result).
+    AIWC_MAX_INGEST_EVENTS lowers it (tests of the chunked path)."""
+    limit = (1 << 32) - 1
+    env = os.environ.get("AIWC_MAX_INGEST_EVENTS")
+    return min(limit, int(env)) if env else limit
+
+
 def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
     """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace."""
     kind = tr.kind
     if device is None:
         device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
+    limit = max_ingest_events()
+    if tr.n_events > limit:
+        from . import dist as D
+
+        return D.chunked_result(D.CudaBackend(device), tr, D.chunk_cuts(tr.kind, limit))
     ctx = _get_ctx(device)
     try:
         lib = ctx.lib

@@ -153,3 +153,20 @@ def test_derive_degenerate():
     d = derive(rep)
     assert d.barriers_per_instruction == 0.04
     assert isinstance(rep, AiwcReport)
+
+
+def test_chunk_cuts_split_at_work_group_starts():
+    from paper_1805_04207_b200.dist import chunk_cuts
+    from paper_1805_04207_b200.errors import UnsupportedTrace
+    from paper_1805_04207_b200.trace import K_WG_BEGIN
+
+    kind = np.zeros(100, np.uint8)
+    starts = [1, 12, 30, 31, 55, 80, 97]
+    kind[starts] = K_WG_BEGIN
+    cuts = chunk_cuts(kind, 30)
+    assert cuts[0] == 0 and cuts[-1] == 100
+    assert all(b - a <= 30 for a, b in zip(cuts, cuts[1:]))
+    assert all(c in starts for c in cuts[1:-1])
+    assert chunk_cuts(kind, 100) == [0, 100]
+    with pytest.raises(UnsupportedTrace):
+        chunk_cuts(kind, 20)  # 55..80 is one 25-event group
