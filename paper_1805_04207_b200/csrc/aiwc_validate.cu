@@ -46,6 +46,30 @@ __device__ __forceinline__ bool known(uint32_t k) {
 
 __device__ __forceinline__ uint8_t kind_at(const uint8_t* kind, uint64_t i, uint64_t n) { return i < n ? kind[i] : 0; }
 
+// the 16 kind bytes of one thread (columns are 16-byte aligned): one 16-byte load
+__device__ __forceinline__ void load_kinds(const uint8_t* kind, uint64_t e0, uint64_t n, uint8_t (&ks)[VEPT]) {
+  if (e0 + VEPT <= n) {
+    const uint4 v = *reinterpret_cast<const uint4*>(kind + e0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < VEPT; ++j) ks[j] = (uint8_t)(w[j >> 2] >> (8 * (j & 3)));
+  } else {
+#pragma unroll
+    for (int j = 0; j < VEPT; ++j) ks[j] = kind_at(kind, e0 + j, n);
+  }
+}
+
+// per kind byte: known (bit 0) | structural (bit 8) | wg_begin (bit 16) | kernel_end (bit 24);
+// a 1 KB shared table turns the per-byte class tests into one load and one add
+__device__ __forceinline__ uint32_t kind_flags(uint32_t k) {
+  return (known(k) ? 1u : 0u) | (structural(k) ? 1u << 8 : 0u) | (k == AIWC_K_WG_BEGIN ? 1u << 16 : 0u) |
+         (k == AIWC_K_KERNEL_END ? 1u << 24 : 0u);
+}
+__device__ __forceinline__ void fill_flags(uint32_t* tbl) {
+  for (uint32_t k = threadIdx.x; k < 256; k += blockDim.x) tbl[k] = kind_flags(k);
+  __syncthreads();
+}
+
 // K1a: per-tile counts of structural events and of work-group begins
 __global__ void __launch_bounds__(VT) v_count_kernel(const uint8_t* __restrict__ kind, uint64_t n,
                                                      uint32_t* __restrict__ s_cnt, uint32_t* __restrict__ g_cnt,
@@ -53,18 +77,22 @@ __global__ void __launch_bounds__(VT) v_count_kernel(const uint8_t* __restrict__
   __shared__ uint32_t red[2][VT / 32];
   const uint64_t tile = blockIdx.x;
   const uint64_t e0 = tile * VTILE + (uint64_t)threadIdx.x * VEPT;
-  uint32_t sc = 0, gc = 0;
+  __shared__ uint32_t tbl[256];
+  fill_flags(tbl);
   unsigned long long first_ke = ~0ull;
-  bool bad = false;
-  for (int j = 0; j < VEPT; ++j) {
-    const uint64_t e = e0 + j;
-    if (e >= n) break;
-    const uint32_t k = kind[e];
-    sc += structural(k);
-    gc += k == AIWC_K_WG_BEGIN;
-    if (k == AIWC_K_KERNEL_END && first_ke == ~0ull) first_ke = e;
-    bad |= !known(k);
+  uint8_t ks[VEPT];
+  load_kinds(kind, e0, n, ks);
+  const uint32_t valid = e0 >= n ? 0u : (uint32_t)min((uint64_t)VEPT, n - e0);
+  uint32_t acc = 0;  // four 8-bit sums of the flags (<= 16 each)
+#pragma unroll
+  for (int j = 0; j < VEPT; ++j)
+    if ((uint32_t)j < valid) acc += tbl[ks[j]];
+  if (acc >> 24) {  // a kernel_end among my events (rare): its first index
+    for (uint32_t j = 0; j < valid; ++j)
+      if (ks[j] == AIWC_K_KERNEL_END) { first_ke = e0 + j; break; }
   }
+  const bool bad = (acc & 0xFFu) != valid;
+  uint32_t sc = (acc >> 8) & 0xFFu, gc = (acc >> 16) & 0xFFu;
   if (first_ke != ~0ull) atomicMin(&vs->first_ke, first_ke);
   if (tile == 0 && threadIdx.x == 0) vs->kb0 = n && kind[0] == AIWC_K_KERNEL_BEGIN;
   if (bad) atomicOr(&vs->bad_kind, 1u);
@@ -93,8 +121,9 @@ __global__ void __launch_bounds__(VT) v_write_kernel(const uint8_t* __restrict__
   const uint64_t e0 = tile * VTILE + (uint64_t)threadIdx.x * VEPT;
   uint32_t smask = 0, gmask = 0;
   uint8_t ks[VEPT];
+  load_kinds(kind, e0, n, ks);
+#pragma unroll
   for (int j = 0; j < VEPT; ++j) {
-    ks[j] = kind_at(kind, e0 + j, n);
     if (structural(ks[j])) smask |= 1u << j;
     if (ks[j] == AIWC_K_WG_BEGIN) gmask |= 1u << j;
   }
