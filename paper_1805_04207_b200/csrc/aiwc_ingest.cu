@@ -60,34 +60,17 @@ __device__ __forceinline__ void load_kind16(const uint8_t* kind, uint64_t e0, ui
   }
 }
 
-__device__ __forceinline__ uint32_t m_wgb(uint32_t w) { return w & ~(w >> 1) & 0x40404040u; }
-
-// 16 kind bytes -> masks with bit 8b + i set when event 4i + b is a work-item
-// boundary / a work-group begin (only the last chunk holding one is decoded)
-__device__ __forceinline__ uint32_t chunk_bnd(const uint32_t w[4]) {
-  return ((w[0] & 0x10101010u) >> 4) | ((w[1] & 0x10101010u) >> 3) | ((w[2] & 0x10101010u) >> 2) |
-         ((w[3] & 0x10101010u) >> 1);
-}
-__device__ __forceinline__ uint32_t chunk_wgb(const uint32_t w[4]) {
-  return (m_wgb(w[0]) >> 6) | (m_wgb(w[1]) >> 5) | (m_wgb(w[2]) >> 4) | (m_wgb(w[3]) >> 3);
-}
-__device__ __forceinline__ long long last_event(long long e0, uint32_t m) {
-  if (e0 < 0) return -1;
-#pragma unroll
-  for (int i = 3; i >= 0; --i) {
-    const uint32_t x = (m >> i) & 0x01010101u;
-    if (x) return e0 + 4 * i + ((31 - __clz(x)) >> 3);
-  }
-  return -1;
-}
-
-// per-class counts of 16 kind bytes.  Nibble packing: L holds bits 0..3
-// (instr, read, write, branch) of two words, H bits 4..7 (boundary, open,
-// group, variant); each class is then one masked popcount per packed word.
+// Per-class counts of 16 kind bytes (w[i] = events 4i..4i+3).  Nibble packing:
+// L0 / L1 hold bits 0..3 (instr, read, write, branch) of events 0..7 / 8..15,
+// H0 / H1 bits 4..7 (boundary, open, group, variant): byte b of H0 has event b
+// in its low nibble and event 4 + b in its high nibble (H1: 8 + b, 12 + b).
+// Each class is one masked popcount per packed word; the boundary and
+// work-group-begin positions stay in that nibble form (decoded once, at the end).
 struct KindCounts {
   uint32_t instr = 0, rd = 0, wr = 0, br = 0, wgb = 0, bres = 0;
-  // gm: the chunk's work-group-begin mask (chunk_wgb), one bit per wg_begin
-  __device__ __forceinline__ void add(const uint32_t w[4], uint32_t gm) {
+  // mb*: boundary bits (nibble bit 0), mw*: wg_begin bits (group bit without the variant bit)
+  __device__ __forceinline__ void add(const uint32_t w[4], uint32_t& mb0, uint32_t& mb1, uint32_t& mw0,
+                                      uint32_t& mw1) {
     const uint32_t L0 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
     const uint32_t L1 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
     const uint32_t H0 = ((w[0] >> 4) & 0x0F0F0F0Fu) | (w[1] & 0xF0F0F0F0u);
@@ -96,10 +79,24 @@ struct KindCounts {
     rd += __popc(L0 & 0x22222222u) + __popc(L1 & 0x22222222u);
     wr += __popc(L0 & 0x44444444u) + __popc(L1 & 0x44444444u);
     br += __popc(L0 & 0x88888888u) + __popc(L1 & 0x88888888u);
-    wgb += __popc(gm);
+    mb0 = H0 & 0x11111111u;
+    mb1 = H1 & 0x11111111u;
+    mw0 = H0 & ~(H0 >> 1) & 0x44444444u;
+    mw1 = H1 & ~(H1 >> 1) & 0x44444444u;
+    wgb += __popc(mw0) + __popc(mw1);
     bres |= (H0 & (H0 >> 3)) | (H1 & (H1 >> 3));  // boundary with the variant bit: barrier / resume
   }
 };
+
+// last event index of a nibble-form mask pair of the chunk at e0 (-1 if none)
+__device__ __forceinline__ long long last_nib_event(long long e0, uint32_t m0, uint32_t m1) {
+  if (e0 < 0) return -1;
+  if (m1 & 0xF0F0F0F0u) return e0 + 12 + ((31 - __clz(m1 & 0xF0F0F0F0u)) >> 3);
+  if (m1 & 0x0F0F0F0Fu) return e0 + 8 + ((31 - __clz(m1 & 0x0F0F0F0Fu)) >> 3);
+  if (m0 & 0xF0F0F0F0u) return e0 + 4 + ((31 - __clz(m0 & 0xF0F0F0F0u)) >> 3);
+  if (m0 & 0x0F0F0F0Fu) return e0 + ((31 - __clz(m0 & 0x0F0F0F0Fu)) >> 3);
+  return -1;
+}
 
 __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __restrict__ kind,
                                                            const uint64_t* __restrict__ payload, uint64_t n,
@@ -112,8 +109,8 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   const uint64_t re = min(n, rb + sub_len);
   const int t = threadIdx.x;
   KindCounts kc;
-  long long lb_e0 = -1, lw_e0 = -1;  // last chunk holding a boundary / group begin, and its mask
-  uint32_t lb_m = 0, lw_m = 0;
+  long long lb_e0 = -1, lw_e0 = -1;  // last chunk holding a boundary / group begin, and its masks
+  uint32_t lb_m0 = 0, lb_m1 = 0, lw_m0 = 0, lw_m1 = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   constexpr int U = 4;  // 16-byte loads in flight per thread
   for (uint64_t base = rb + 16ull * U * t; base < re; base += 16ull * U * P1_THREADS) {
@@ -123,10 +120,10 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t e0 = base + 16 * u;
-      const uint32_t bm = chunk_bnd(w[u]), gm = chunk_wgb(w[u]);
-      kc.add(w[u], gm);
-      if (bm) { lb_e0 = (long long)e0; lb_m = bm; }
-      if (gm) { lw_e0 = (long long)e0; lw_m = gm; }
+      uint32_t mb0, mb1, mw0, mw1;
+      kc.add(w[u], mb0, mb1, mw0, mw1);
+      if (mb0 | mb1) { lb_e0 = (long long)e0; lb_m0 = mb0; lb_m1 = mb1; }
+      if (mw0 | mw1) { lw_e0 = (long long)e0; lw_m0 = mw0; lw_m1 = mw1; }
       if (with_stats) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -141,7 +138,7 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
       }
     }
   }
-  long long last_bnd = last_event(lb_e0, lb_m), last_wgb = last_event(lw_e0, lw_m);
+  long long last_bnd = last_nib_event(lb_e0, lb_m0, lb_m1), last_wgb = last_nib_event(lw_e0, lw_m0, lw_m1);
   // block reduction
   constexpr int NW = P1_THREADS / 32;
   __shared__ uint32_t s_cnt[NW][6];
