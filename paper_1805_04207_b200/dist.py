@@ -330,6 +330,14 @@ def chunk_cuts(kind, limit: int) -> list[int]:
             from .errors import UnsupportedTrace
 
             raise UnsupportedTrace(f"a work-group spans more than {limit} events")
+        # prefer a cut at a 16-aligned event (the chunk's device columns then need no
+        # aligned copy) among the last few group starts that fit
+        for j in range(i, max(i - 64, -1), -1):
+            if int(starts[j]) <= cuts[-1]:
+                break
+            if int(starts[j]) % 16 == 0:
+                i = j
+                break
         cuts.append(int(starts[i]))
     cuts.append(n)
     return cuts
