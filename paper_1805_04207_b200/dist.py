@@ -178,16 +178,19 @@ def _gather_objects(obj, group) -> list:
 
 
 def allreduce_stats(stats, group, device):
-    """(min, max, and, or) over ranks; empty shards contribute identities."""
+    """(min, max, and, or) over ranks; empty shards contribute identities.  One
+    all-gather of the four words (NCCL has no bitwise reductions), combined on
+    the host in unsigned arithmetic."""
+    import torch
     import torch.distributed as dist
 
     amin, amax, aand, aor = stats if stats is not None else ((1 << 64) - 1, 0, (1 << 64) - 1, 0)
-    flip = 1 << 63  # unsigned order as signed order
-    mn = _allreduce_i64(np.array([amin ^ flip], np.uint64), dist.ReduceOp.MIN, group, device)[0] ^ np.uint64(flip)
-    mx = _allreduce_i64(np.array([amax ^ flip], np.uint64), dist.ReduceOp.MAX, group, device)[0] ^ np.uint64(flip)
-    an = _allreduce_i64(np.array([aand], np.uint64), dist.ReduceOp.BAND, group, device)[0]
-    orr = _allreduce_i64(np.array([aor], np.uint64), dist.ReduceOp.BOR, group, device)[0]
-    return int(mn), int(mx), int(an), int(orr)
+    mine = torch.from_numpy(np.array([amin, amax, aand, aor], np.uint64).view(np.int64).copy()).to(device)
+    parts = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, mine, group=group)
+    v = np.stack([p.cpu().numpy().view(np.uint64) for p in parts])
+    return (int(v[:, 0].min()), int(v[:, 1].max()), int(np.bitwise_and.reduce(v[:, 2])),
+            int(np.bitwise_or.reduce(v[:, 3])))
 
 
 def exchange(entries, counts: list[int], group, device):
