@@ -886,15 +886,76 @@ __global__ void partition_scatter_kernel(const uint64_t* __restrict__ a, uint64_
   }
 }
 
-// owned-range dense table from received addresses
+// owned-range hot window: the most frequent 1024-key block among 4096 sampled
+// received addresses (>= 1/64 of them), else ~0 -- a block many ranks' accesses
+// hit (shared scratch) would otherwise serialise as same-address REDs in L2
+__global__ void __launch_bounds__(1024) owned_hot_sample_kernel(const uint64_t* __restrict__ a, uint64_t n,
+                                                                uint64_t base, uint32_t k, uint64_t key_lo,
+                                                                uint64_t n_keys, unsigned long long* hot_out) {
+  constexpr int SLOTS = 4096, PER = 4;
+  __shared__ uint32_t hk[SLOTS], hc[SLOTS];
+  __shared__ unsigned long long red[32];
+  const int t = threadIdx.x;
+  for (int i = t; i < SLOTS; i += 1024) { hk[i] = ~0u; hc[i] = 0; }
+  __syncthreads();
+  uint64_t v[PER];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    uint64_t x = (uint64_t)(t * PER + j) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
+    x = (x ^ (x >> 31)) * 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 29;
+    v[j] = n ? a[x % n] : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const uint64_t key = ((v[j] - base) >> k) - key_lo;
+    if (!n || key >= n_keys) continue;
+    const uint32_t blk = (uint32_t)(key >> 10);
+    uint32_t h = (blk * 2654435761u) >> 20;
+    for (int probe = 0; probe < 64; ++probe, h = (h + 1) & (SLOTS - 1)) {
+      const uint32_t old = atomicCAS(&hk[h], ~0u, blk);
+      if (old == ~0u || old == blk) { atomicAdd(&hc[h], 1u); break; }
+    }
+  }
+  __syncthreads();
+  unsigned long long best = 0;
+  for (int i = t; i < SLOTS; i += 1024)
+    if (hc[i]) best = max(best, ((unsigned long long)hc[i] << 32) | hk[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((t & 31) == 0) red[t >> 5] = best;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long b = 0;
+    for (int w = 0; w < 32; ++w) b = max(b, red[w]);
+    const uint32_t cnt = (uint32_t)(b >> 32);
+    *hot_out = (n >= (1u << 20) && cnt >= 64) ? (unsigned long long)(uint32_t)b << 10 : ~0ull;
+  }
+}
+
+// owned-range dense table from received addresses (keys of the hot window are
+// counted per CTA in shared memory and added once)
 __global__ void fill_owned_kernel(const uint64_t* __restrict__ a, uint64_t n, unsigned long long inc, uint64_t base,
                                   uint32_t k, uint64_t key_lo, uint64_t n_keys, unsigned long long* __restrict__ tab,
-                                  DevState* st) {
+                                  DevState* st, const unsigned long long* hot) {
+  __shared__ uint32_t win[1024];
+  const uint64_t hot_lo = *hot;
+  const uint32_t hn = hot_lo == ~0ull ? 0u : 1024u;
+  for (uint32_t i = threadIdx.x; i < hn; i += blockDim.x) win[i] = 0;
+  __syncthreads();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t key = ((a[i] - base) >> k) - key_lo;
-    if (key < n_keys) atomicAdd(&tab[key], inc);
-    else atomicOr(&st->flags, (unsigned long long)F_SLOT_RANGE);
+    if (key < n_keys) {
+      const uint64_t rel = key - hot_lo;
+      if (rel < hn) atomicAdd(&win[rel], 1u);
+      else atomicAdd(&tab[key], inc);
+    } else {
+      atomicOr(&st->flags, (unsigned long long)F_SLOT_RANGE);
+    }
   }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < hn; i += blockDim.x)
+    if (win[i]) atomicAdd(&tab[hot_lo + i], (unsigned long long)win[i] * inc);
 }
 
 }  // namespace
@@ -986,9 +1047,10 @@ extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n
     for (int q = 0; q < 2; ++q)
       if (len[q]) {
         const uint32_t blocks = (uint32_t)std::min<uint64_t>((len[q] + 255) / 256, (uint64_t)ctx->n_sms * 8);
+        owned_hot_sample_kernel<<<1, 1024, 0, s>>>(src[q], len[q], base, k, key_lo, n_keys, &st->hot_key);
         fill_owned_kernel<<<blocks, 256, 0, s>>>(src[q], len[q], q ? (1ull << 32) : 1ull, base, k, key_lo, n_keys,
-                                                 P<unsigned long long>(ctx->mp_tab), st);
-        ++launched;
+                                                 P<unsigned long long>(ctx->mp_tab), st, &st->hot_key);
+        launched += 2;
       }
     const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
     launch_dense_stats(ctx->mp_tab.p, false, n_keys, k, tm, st, P<double>(ctx->partials), nct,
