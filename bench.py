@@ -57,27 +57,40 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self._nv = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run_nvml(self) -> bool:
-        """NVML sampling every 2 ms (short timed regions still get many samples)."""
+    def _nvml_open(self) -> bool:
         try:
             import pynvml as nv
 
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
-            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-            bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+            return True
         except Exception:
+            self._nv = None
+            return False
+
+    def _sample_nvml(self) -> None:
+        nv = self._nv
+        bits = (0x8, 0x40, 0x20, 0x4)  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+            self.samples.append([str(sm), str(self._mx)] + ["Active" if r & b else "Not Active" for b in bits])
+        except Exception:
+            pass
+
+    def _run_nvml(self) -> bool:
+        """NVML sampling every 2 ms (short timed regions still get samples: one is
+        also taken synchronously on entry and on exit)."""
+        if self._nv is None:
             return False
         while not self._stop.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
-            except Exception:
-                pass
+            self._sample_nvml()
             self._stop.wait(0.002)
         return True
 
@@ -96,10 +109,14 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def __enter__(self):
+        if self._nvml_open():
+            self._sample_nvml()
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        if self._nv is not None:
+            self._sample_nvml()
         self._stop.set()
         self._t.join(timeout=6)
 
