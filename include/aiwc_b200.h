@@ -202,6 +202,21 @@ int  aiwc_memory_partial(aiwc_ctx *ctx, const uint64_t *reads_dev, uint64_t n_rd
                          uint64_t n_wr, uint64_t base, uint32_t k, uint64_t key_lo, uint64_t n_keys,
                          uint64_t total_m, aiwc_memory_part *out, void *stream);
 
+/* Run-length form of this shard's addresses for the owners (pre-aggregation):
+ * maximal stretches of consecutive keys with one owner (<= 65536 keys each),
+ * two words per run -- global key, length | is_write << 63 -- grouped by owner;
+ * counts[0..nranks) are runs per owner.  Valid until the next call on ctx.
+ * Streaming shards become a handful of runs; the caller compares the run count
+ * with the access count to choose between this and aiwc_partition_addresses. */
+int  aiwc_partition_runs(aiwc_ctx *ctx, uint64_t base, uint32_t k, uint64_t keys_per_rank, uint32_t nranks,
+                         uint64_t **runs_dev, uint64_t *counts, void *stream);
+
+/* Owner side of the run exchange: memory statistics of the owned keys
+ * [key_lo, key_lo + n_keys) (dense table) from the received runs. */
+int  aiwc_memory_partial_runs(aiwc_ctx *ctx, const uint64_t *runs_dev, uint64_t n_runs, uint32_t k,
+                              uint64_t key_lo, uint64_t n_keys, uint64_t total_m, aiwc_memory_part *out,
+                              void *stream);
+
 /* ---- stream validation (StreamChecker, trace.py:289-424) -------------------------
  * First violation of a columnar trace, decoded as ColumnarTrace.iter_events
  * would (group from the last wg_begin, work-item ids from the local linear id).

@@ -152,6 +152,10 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_synth_fill.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, vp, vp, ctypes.c_uint64,
                                         ctypes.c_uint64, vp]
         lib.aiwc_shard_tables_get.argtypes = [vp, ctypes.POINTER(ShardTables)]
+        lib.aiwc_partition_runs.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
+                                            ctypes.POINTER(u64p), u64p, vp]
+        lib.aiwc_memory_partial_runs.argtypes = [vp, vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64,
+                                                 ctypes.c_uint64, ctypes.c_uint64, ctypes.POINTER(MemoryPart), vp]
         lib.aiwc_partition_addresses.argtypes = [vp, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32,
                                                  ctypes.POINTER(u64p), ctypes.POINTER(u64p), u64p, vp]
         lib.aiwc_memory_partial.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint64,

@@ -128,7 +128,7 @@ struct aiwc_ctx {
   std::vector<uint64_t> itb_ovf_sorted, ipt_ovf_sorted, lvl0_sorted;
   std::vector<uint64_t> width_firsts, branch_tab_host;
   // multi-GPU: owner partition and owned-key memory partials
-  Buf part_entries, part_cursor, mp_state, mp_tab, mp_partials, mp_ovf;
+  Buf part_entries, part_cursor, mp_state, mp_tab, mp_partials, mp_ovf, run_pos, run_blk, run_scan;
   // stream validation
   Buf v_state, v_tiles, v_scan, v_spos, v_spay, v_sgap, v_gstart, v_recs, v_counts;
   Buf v_srange, v_fwge, v_keys, v_keys_tmp, v_hist, v_prevk, v_unf, v_bmm;
@@ -205,6 +205,7 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
                  &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
                  &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
                  &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres,
+                 &ctx->run_pos, &ctx->run_blk, &ctx->run_scan,
                  &ctx->v_state, &ctx->v_tiles, &ctx->v_scan, &ctx->v_spos, &ctx->v_spay, &ctx->v_sgap,
                  &ctx->v_gstart, &ctx->v_recs, &ctx->v_counts, &ctx->v_srange, &ctx->v_fwge, &ctx->v_keys,
                  &ctx->v_keys_tmp, &ctx->v_hist, &ctx->v_prevk, &ctx->v_unf, &ctx->v_bmm};
@@ -891,7 +892,8 @@ __global__ void partition_scatter_kernel(const uint64_t* __restrict__ a, uint64_
 // hit (shared scratch) would otherwise serialise as same-address REDs in L2
 __global__ void __launch_bounds__(1024) owned_hot_sample_kernel(const uint64_t* __restrict__ a, uint64_t n,
                                                                 uint64_t base, uint32_t k, uint64_t key_lo,
-                                                                uint64_t n_keys, unsigned long long* hot_out) {
+                                                                uint64_t n_keys, unsigned long long* hot_out,
+                                                                uint32_t stride = 1, bool keys = false) {
   constexpr int SLOTS = 4096, PER = 4;
   __shared__ uint32_t hk[SLOTS], hc[SLOTS];
   __shared__ unsigned long long red[32];
@@ -904,11 +906,11 @@ __global__ void __launch_bounds__(1024) owned_hot_sample_kernel(const uint64_t* 
     uint64_t x = (uint64_t)(t * PER + j) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull;
     x = (x ^ (x >> 31)) * 0xBF58476D1CE4E5B9ull;
     x ^= x >> 29;
-    v[j] = n ? a[x % n] : 0ull;
+    v[j] = n ? a[(x % n) * stride] : 0ull;
   }
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    const uint64_t key = ((v[j] - base) >> k) - key_lo;
+    const uint64_t key = (keys ? v[j] : (v[j] - base) >> k) - key_lo;
     if (!n || key >= n_keys) continue;
     const uint32_t blk = (uint32_t)(key >> 10);
     uint32_t h = (blk * 2654435761u) >> 20;
@@ -956,6 +958,157 @@ __global__ void fill_owned_kernel(const uint64_t* __restrict__ a, uint64_t n, un
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < hn; i += blockDim.x)
     if (win[i]) atomicAdd(&tab[hot_lo + i], (unsigned long long)win[i] * inc);
+}
+
+// ---- run-length exchange (pre-aggregation on the sending rank) ----
+// A run is a maximal stretch of one compacted address array whose keys go up by
+// one with a single owner (streaming traces: a whole shard is a few runs),
+// capped at RUN_MAX keys.  It travels as two words: global key, length | write << 63.
+constexpr int RN_T = 256, RN_I = 8, RN_TILE = RN_T * RN_I;
+constexpr uint64_t RUN_MAX = 1ull << 16;
+
+// run heads of one tile, warp-contiguous (element warp_base + 32 j + lane, all loads
+// coalesced; the predecessor comes from the neighbouring lane): bit j of the
+// returned ballot word hm[j] marks lane `lane`'s element j as a head
+__device__ __forceinline__ void tile_heads(const uint64_t* __restrict__ a, uint64_t n, uint64_t base, uint32_t k,
+                                           uint64_t kpr, uint32_t nranks, uint32_t (&hm)[RN_I]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t wb = (uint64_t)blockIdx.x * RN_TILE + (uint64_t)warp * 32 * RN_I;
+  uint64_t v[RN_I];
+#pragma unroll
+  for (int j = 0; j < RN_I; ++j) {
+    const uint64_t i = wb + 32 * j + lane;
+    v[j] = i < n ? __ldcs(a + i) : 0ull;
+  }
+  uint64_t prev_last = (wb && wb - 1 < n) ? a[wb - 1] : 0ull;  // element before the warp's first
+#pragma unroll
+  for (int j = 0; j < RN_I; ++j) {
+    const uint64_t i = wb + 32 * j + lane;
+    uint64_t p = __shfl_up_sync(0xffffffffu, v[j], 1);
+    const uint64_t last_prev_row = __shfl_sync(0xffffffffu, j ? v[j - 1] : prev_last, 31);
+    if (lane == 0) p = last_prev_row;
+    bool h = false;
+    if (i < n) {
+      if (i == 0 || (i & (RUN_MAX - 1)) == 0) {
+        h = true;
+      } else {
+        const uint64_t k1 = (v[j] - base) >> k, k0 = (p - base) >> k;
+        h = k1 != k0 + 1;
+        for (uint32_t o = 1; o < nranks && !h; ++o) h = k1 == (uint64_t)o * kpr;
+      }
+    }
+    hm[j] = __ballot_sync(0xffffffffu, h);
+  }
+}
+
+// heads per tile
+__global__ void __launch_bounds__(RN_T) run_count_kernel(const uint64_t* __restrict__ a, uint64_t n, uint64_t base,
+                                                          uint32_t k, uint64_t kpr, uint32_t nranks,
+                                                          uint32_t* __restrict__ blk) {
+  __shared__ uint32_t ws[RN_T / 32];
+  uint32_t hm[RN_I];
+  tile_heads(a, n, base, k, kpr, nranks, hm);
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < RN_I; ++j) c += __popc(hm[j]);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < RN_T / 32; ++w) t += ws[w];
+    blk[blockIdx.x] = t;
+  }
+}
+
+// head indices in stream order (blk holds the exclusive scan of the tile counts)
+__global__ void __launch_bounds__(RN_T) run_pos_kernel(const uint64_t* __restrict__ a, uint64_t n, uint64_t base,
+                                                        uint32_t k, uint64_t kpr, uint32_t nranks,
+                                                        const uint32_t* __restrict__ blk, uint64_t* __restrict__ pos) {
+  __shared__ uint32_t ws[RN_T / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t hm[RN_I];
+  tile_heads(a, n, base, k, kpr, nranks, hm);
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < RN_I; ++j) c += __popc(hm[j]);
+  if (lane == 0) ws[warp] = c;
+  __syncthreads();
+  uint32_t o = blk[blockIdx.x];
+  for (int w = 0; w < warp; ++w) o += ws[w];
+  const uint64_t wb = (uint64_t)blockIdx.x * RN_TILE + (uint64_t)warp * 32 * RN_I;
+#pragma unroll
+  for (int j = 0; j < RN_I; ++j) {
+    if ((hm[j] >> lane) & 1u) pos[o + __popc(hm[j] & ((1u << lane) - 1u))] = wb + 32 * j + lane;
+    o += __popc(hm[j]);
+  }
+}
+
+// runs per owner (pass 0) / owner-grouped runs (pass 1, cursors hold the offsets)
+__global__ void run_emit_kernel(const uint64_t* __restrict__ a, uint64_t n, const uint64_t* __restrict__ pos,
+                                uint64_t n_runs, uint64_t base, uint32_t k, uint64_t kpr, uint32_t nranks,
+                                unsigned long long wflag, int pass, unsigned long long* cursor,
+                                uint64_t* __restrict__ out) {
+  // whole warps iterate together; a warp whose runs share one owner (the common
+  // case) reserves its slots with a single atomic
+  const int lane = threadIdx.x & 31;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t n_pad = (n_runs + 31) & ~31ull;
+  for (uint64_t h = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; h < n_pad; h += T) {
+    const bool valid = h < n_runs;
+    uint64_t st = 0, en = 0;
+    uint32_t o = PA_MAXR;
+    if (valid) {
+      st = pos[h];
+      en = h + 1 < n_runs ? pos[h + 1] : n;
+      o = owner_of(a[st], base, k, kpr, nranks);
+    }
+    const uint32_t o0 = __shfl_sync(0xffffffffu, o, 0);
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    unsigned long long slot = 0;
+    if (__all_sync(0xffffffffu, !valid || o == o0)) {
+      unsigned long long b = 0;
+      if (lane == 0 && vm) b = atomicAdd(&cursor[o0], (unsigned long long)__popc(vm));
+      slot = __shfl_sync(0xffffffffu, b, 0) + __popc(vm & ((1u << lane) - 1u));
+    } else if (valid) {
+      slot = atomicAdd(&cursor[o], 1ull);
+    }
+    if (pass == 1 && valid) {
+      out[2 * slot] = (a[st] - base) >> k;
+      out[2 * slot + 1] = (en - st) | wflag;
+    }
+  }
+}
+
+// owned-range dense table from runs: one warp per run; keys of the hot window
+// are counted per CTA in shared memory
+__global__ void apply_runs_kernel(const uint64_t* __restrict__ runs, uint64_t n_runs, uint64_t key_lo,
+                                  uint64_t n_keys, unsigned long long* __restrict__ tab, DevState* st,
+                                  const unsigned long long* hot) {
+  __shared__ uint32_t win[2][1024];
+  const uint64_t hot_lo = *hot;
+  const uint32_t hn = hot_lo == ~0ull ? 0u : 1024u;
+  for (uint32_t i = threadIdx.x; i < 2 * hn; i += blockDim.x) (&win[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_runs; r += nw) {
+    const uint64_t key = runs[2 * r] - key_lo, lw = runs[2 * r + 1];
+    const uint64_t len = lw & 0xFFFFFFFFull;
+    const uint32_t w = (uint32_t)(lw >> 63);
+    if (key >= n_keys || len > n_keys - key) {
+      if (lane == 0) atomicOr(&st->flags, (unsigned long long)F_SLOT_RANGE);
+      continue;
+    }
+    for (uint64_t i = lane; i < len; i += 32) {
+      const uint64_t rel = key + i - hot_lo;
+      if (rel < hn) atomicAdd(&win[w][rel], 1u);
+      else atomicAdd(&tab[key + i], w ? (1ull << 32) : 1ull);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < hn; i += blockDim.x)
+    if (win[0][i] | win[1][i])
+      atomicAdd(&tab[hot_lo + i], (unsigned long long)win[0][i] | ((unsigned long long)win[1][i] << 32));
 }
 
 }  // namespace
@@ -1025,6 +1178,117 @@ extern "C" int aiwc_partition_addresses(aiwc_ctx* ctx, uint64_t base, uint32_t k
   return AIWC_OK;
 }
 
+// the owner's statistics back to the host (both owner entry points)
+static int owned_result(aiwc_ctx* ctx, DevState* st, uint64_t m, uint32_t launched, aiwc_memory_part* out,
+                        cudaStream_t s) {
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  const DevState& h = *ctx->h_state;
+  if (h.flags & F_SLOT_RANGE) return fail(ctx, AIWC_ERR_ARGUMENT, "received address outside the owned key range");
+  ctx->mp_hist0.assign(h.cnt_hist0, h.cnt_hist0 + CBINS);
+  ctx->mp_big.resize(h.lvl0_ovf_n);
+  if (h.lvl0_ovf_n) {
+    CK(cudaMemcpyAsync(ctx->mp_big.data(), ctx->mp_ovf.p, h.lvl0_ovf_n * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  aiwc_memory_part r{};
+  r.unique_reads = h.unique_r; r.unique_writes = h.unique_w; r.footprint = h.footprint;
+  for (int i = 0; i < NLEVELS; ++i) r.level_sum[i] = m ? -h.entropy[i] : 0.0;
+  r.cnt_hist0 = ctx->mp_hist0.data();
+  r.n_big = ctx->mp_big.size();
+  r.big = ctx->mp_big.data();
+  r.kernels_launched = launched;
+  *out = r;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_partition_runs(aiwc_ctx* ctx, uint64_t base, uint32_t k, uint64_t keys_per_rank,
+                                   uint32_t nranks, uint64_t** runs_dev, uint64_t* counts, void* stream) {
+  if (!ctx || !runs_dev || !counts || nranks == 0 || nranks > (uint32_t)PA_MAXR || keys_per_rank == 0)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad partition arguments");
+  if (!(ctx->opts.flags & AIWC_OPT_SHARD) || ctx->state != 2)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "partition needs a shard ctx after aiwc_finalize");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  const uint64_t* src[2] = {P<uint64_t>(ctx->rd), P<uint64_t>(ctx->wr)};
+  const uint64_t len[2] = {ctx->n_rd, ctx->n_wr};
+  CK(grow(ctx->run_pos, std::max<uint64_t>(ctx->n_rd + ctx->n_wr, 1) * 8));
+  CK(grow(ctx->part_cursor, 2 * PA_MAXR * 8));
+  uint64_t* pos = P<uint64_t>(ctx->run_pos);
+  uint64_t nrun[2] = {0, 0};
+  for (int q = 0; q < 2; ++q) {
+    if (!len[q]) continue;
+    const uint64_t nb = (len[q] + RN_TILE - 1) / RN_TILE;
+    CK(grow(ctx->run_blk, (nb + 1) * 4));
+    CK(grow(ctx->run_scan, (scan_scratch_elems(nb) + 16) * 4));
+    uint32_t* blk = P<uint32_t>(ctx->run_blk);
+    run_count_kernel<<<(unsigned)nb, RN_T, 0, s>>>(src[q], len[q], base, k, keys_per_rank, nranks, blk);
+    scan_exclusive_u32(blk, nb, P<uint32_t>(ctx->run_scan), blk + nb, s, nullptr);
+    uint32_t tot = 0;
+    CK(cudaMemcpyAsync(&tot, blk + nb, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nrun[q] = tot;
+    run_pos_kernel<<<(unsigned)nb, RN_T, 0, s>>>(src[q], len[q], base, k, keys_per_rank, nranks, blk,
+                                                pos + (q ? nrun[0] : 0));
+  }
+  const uint64_t R = nrun[0] + nrun[1];
+  CK(grow(ctx->part_entries, std::max<uint64_t>(R, 1) * 16));
+  unsigned long long* cur = P<unsigned long long>(ctx->part_cursor);
+  CK(cudaMemsetAsync(cur, 0, PA_MAXR * 8, s));
+  auto grid = [&](uint64_t n) { return (unsigned)std::min<uint64_t>(std::max<uint64_t>((n + 255) / 256, 1), 148 * 16); };
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) {
+      std::vector<unsigned long long> c(PA_MAXR, 0), off(PA_MAXR, 0);
+      CK(cudaMemcpyAsync(c.data(), cur, PA_MAXR * 8, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      unsigned long long run = 0;
+      for (uint32_t o = 0; o < nranks; ++o) { off[o] = run; run += c[o]; counts[o] = c[o]; }
+      CK(cudaMemcpyAsync(cur, off.data(), PA_MAXR * 8, cudaMemcpyHostToDevice, s));
+    }
+    for (int q = 0; q < 2; ++q)
+      if (nrun[q])
+        run_emit_kernel<<<grid(nrun[q]), 256, 0, s>>>(src[q], len[q], pos + (q ? nrun[0] : 0), nrun[q], base, k,
+                                                     keys_per_rank, nranks, q ? (1ull << 63) : 0ull, pass, cur,
+                                                     P<uint64_t>(ctx->part_entries));
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  *runs_dev = P<uint64_t>(ctx->part_entries);
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_memory_partial_runs(aiwc_ctx* ctx, const uint64_t* runs, uint64_t n_runs, uint32_t k,
+                                        uint64_t key_lo, uint64_t n_keys, uint64_t total_m, aiwc_memory_part* out,
+                                        void* stream) {
+  if (!ctx || !out || (n_runs && !runs) || (key_lo & 1023) || k > 32)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad memory partial");
+  if (n_keys * 8 > ctx->opts.dense_budget_bytes)
+    return fail(ctx, AIWC_ERR_UNSUPPORTED, "owned key range exceeds the dense-table budget");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->mp_state, sizeof(DevState)));
+  DevState* st = P<DevState>(ctx->mp_state);
+  init_state_kernel<<<64, 256, 0, s>>>(st);
+  uint32_t launched = 1;
+  const uint64_t tm = std::max<uint64_t>(total_m, 1);
+  CK(grow(ctx->mp_ovf, (tm / CBINS + 2) * 8));
+  if (n_runs) {
+    CK(grow(ctx->mp_tab, std::max<uint64_t>(n_keys, 1) * 8));
+    CK(cudaMemsetAsync(ctx->mp_tab.p, 0, std::max<uint64_t>(n_keys, 1) * 8, s));
+    owned_hot_sample_kernel<<<1, 1024, 0, s>>>(runs, n_runs, 0, 0, key_lo, n_keys, &st->hot_key, 2, true);
+    const uint32_t blocks = (uint32_t)std::min<uint64_t>((n_runs + 7) / 8, (uint64_t)ctx->n_sms * 8);
+    apply_runs_kernel<<<blocks, 256, 0, s>>>(runs, n_runs, key_lo, n_keys, P<unsigned long long>(ctx->mp_tab), st,
+                                             &st->hot_key);
+    const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
+    launch_dense_stats(ctx->mp_tab.p, false, n_keys, k, tm, st, P<double>(ctx->partials), nct,
+                       P<uint64_t>(ctx->mp_ovf), s);
+    launch_entropy_finish(st, P<double>(ctx->partials), nct, tm, k, s);
+    launched += 4;
+  }
+  return owned_result(ctx, st, n_runs, launched, out, s);
+}
+
 extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, uint64_t n_wr,
                                    uint64_t base, uint32_t k, uint64_t key_lo, uint64_t n_keys, uint64_t total_m,
                                    aiwc_memory_part* out, void* stream) {
@@ -1071,26 +1335,7 @@ extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n
     launch_entropy_finish(st, P<double>(ctx->partials), parts, tm, raw ? 64u : k, s);
     launched += 1;
   }
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  const DevState& h = *ctx->h_state;
-  if (h.flags & F_SLOT_RANGE) return fail(ctx, AIWC_ERR_ARGUMENT, "received address outside the owned key range");
-  ctx->mp_hist0.assign(h.cnt_hist0, h.cnt_hist0 + CBINS);
-  ctx->mp_big.resize(h.lvl0_ovf_n);
-  if (h.lvl0_ovf_n) {
-    CK(cudaMemcpyAsync(ctx->mp_big.data(), ctx->mp_ovf.p, h.lvl0_ovf_n * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-  }
-  aiwc_memory_part r{};
-  r.unique_reads = h.unique_r; r.unique_writes = h.unique_w; r.footprint = h.footprint;
-  for (int i = 0; i < NLEVELS; ++i) r.level_sum[i] = m ? -h.entropy[i] : 0.0;
-  r.cnt_hist0 = ctx->mp_hist0.data();
-  r.n_big = ctx->mp_big.size();
-  r.big = ctx->mp_big.data();
-  r.kernels_launched = launched;
-  *out = r;
-  return AIWC_OK;
+  return owned_result(ctx, st, m, launched, out, s);
 }
 
 

@@ -193,6 +193,16 @@ def allreduce_stats(stats, group, device):
             int(np.bitwise_or.reduce(v[:, 3])))
 
 
+RUNS_TABLE_BUDGET = 16 << 30  # bytes of one owner's dense table in the run exchange
+LAST_EXCHANGE = None  # "runs" or "raw": the address exchange the last sharded_result used
+RUN_MIN_AVG = 32      # accesses per run below which the raw exchange is used
+
+
+def runs_dense_ok(km: KeyMap, total_m: int) -> bool:
+    """Owners can hold their key ranges as dense tables (the run exchange needs one)."""
+    return km.keys_per_rank * 8 <= RUNS_TABLE_BUDGET and km.n_keys <= 4 * total_m + (1 << 20)
+
+
 def exchange(entries, counts: list[int], group, device):
     """All-to-all of owner-grouped u64 entries; returns (received tensor, n)."""
     import torch
@@ -250,11 +260,26 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
     if total_m:
         stats = allreduce_stats(sp.addr_stats, group, device)
         km = key_map(stats, world)
-        reads, writes, counts = backend.partition(sp, km, world)
-        recv_r, n_r = exchange(reads, counts[:world], group, device)
-        recv_w, n_w = exchange(writes, counts[world:], group, device)
         lo, n_owned = km.owned(rank)
-        mp = backend.memory_partial(recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m)
+        use_runs = False
+        if hasattr(backend, "partition_runs") and runs_dense_ok(km, total_m):
+            # pre-aggregation: runs of consecutive keys per owner; chosen (on every
+            # rank alike) when runs average >= RUN_MIN_AVG accesses (the owner
+            # applies one run per warp: short runs would idle its lanes)
+            runs, rcounts = backend.partition_runs(sp, km, world)
+            tot = _allreduce_i64(np.array([sum(rcounts), sp.total_reads + sp.total_writes], np.uint64),
+                                 dist.ReduceOp.SUM, group, device)
+            use_runs = RUN_MIN_AVG * int(tot[0]) <= int(tot[1])
+        global LAST_EXCHANGE
+        LAST_EXCHANGE = "runs" if use_runs else "raw"
+        if use_runs:
+            recv, n_words = exchange(runs, [2 * c for c in rcounts], group, device)
+            mp = backend.memory_partial_runs(recv, n_words // 2, km, lo, n_owned, total_m)
+        else:
+            reads, writes, counts = backend.partition(sp, km, world)
+            recv_r, n_r = exchange(reads, counts[:world], group, device)
+            recv_w, n_w = exchange(writes, counts[world:], group, device)
+            mp = backend.memory_partial(recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m)
     else:
         mp = MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(CBINS, np.uint64), np.zeros(0, np.uint64))
     msum = _allreduce_i64(np.concatenate([np.array([mp.unique_reads, mp.unique_writes, mp.footprint], np.uint64),
@@ -482,6 +507,39 @@ class CudaBackend:
         view = lambda p, n: torch.as_tensor(_CudaArray(ctypes.cast(p, ctypes.c_void_p).value, max(n, 1)),  # noqa: E731
                                             device=self.device)[:n]
         return view(t.rd_dev, int(sp.total_reads)), view(t.wr_dev, int(sp.total_writes))
+
+    def partition_runs(self, sp: ShardPartial, km: KeyMap, nranks: int):
+        """Owner-grouped runs of this shard's addresses (two int64 words per run)."""
+        import torch
+
+        ctx = self._ctx()
+        counts = (ctypes.c_uint64 * nranks)()
+        rp = ctypes.POINTER(ctypes.c_uint64)()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_partition_runs(ctx.h, km.base, km.k, km.keys_per_rank, nranks, ctypes.byref(rp), counts,
+                                              ctypes.c_void_p(stream)))
+        c = [int(x) for x in counts]
+        self.launches += 6
+        runs = torch.as_tensor(_CudaArray(ctypes.cast(rp, ctypes.c_void_p).value, max(2 * sum(c), 1)),
+                               device=self.device)
+        return runs, c
+
+    def memory_partial_runs(self, recv, n_runs: int, km: KeyMap, key_lo: int, n_keys: int,
+                            total_m: int) -> MemoryPartial:
+        import torch
+
+        from . import _native
+
+        ctx = self._ctx()
+        out = _native.MemoryPart()
+        recv = recv.to(self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_memory_partial_runs(ctx.h, ctypes.c_void_p(recv.data_ptr()), n_runs, km.k, key_lo,
+                                                   n_keys, total_m, ctypes.byref(out), ctypes.c_void_p(stream)))
+        self.launches += out.kernels_launched
+        big = np.ctypeslib.as_array(out.big, shape=(out.n_big,)).copy() if out.n_big else np.zeros(0, np.uint64)
+        return MemoryPartial(out.unique_reads, out.unique_writes, out.footprint, np.array(out.level_sum[:]),
+                             np.ctypeslib.as_array(out.cnt_hist0, shape=(CBINS,)).copy(), big)
 
     def partition(self, sp: ShardPartial, km: KeyMap, nranks: int):
         import torch

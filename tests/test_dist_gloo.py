@@ -65,12 +65,49 @@ class OracleBackend:
             counts += np.bincount(own, minlength=nranks).tolist()
         return out[0], out[1], counts
 
-    def memory_partial(self, recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m):
-        from paper_1805_04207_b200.dist import CBINS, MemoryPartial
+    def partition_runs(self, sp, km, nranks):
+        """Runs of consecutive keys with one owner (the engine's aiwc_partition_runs)."""
+        rd_a, rd_c, wr_a, wr_c = sp.handle
+        runs = []
+        for w, (a, c) in enumerate(((rd_a, rd_c), (wr_a, wr_c))):
+            a = np.sort(np.repeat(a, c.astype(np.int64)))  # the oracle's address order is arbitrary
+            if not a.size:
+                continue
+            keys = ((a - np.uint64(km.base)) >> np.uint64(km.k)).astype(np.int64)
+            own = np.minimum(keys // km.keys_per_rank, nranks - 1)
+            idx = np.arange(keys.size)
+            head = np.ones(keys.size, bool)
+            head[1:] = (keys[1:] != keys[:-1] + 1) | (own[1:] != own[:-1]) | (idx[1:] % 65536 == 0)
+            hp = np.nonzero(head)[0]
+            lens = np.diff(np.append(hp, keys.size))
+            for h, n in zip(hp, lens):
+                runs.append((int(own[h]), int(keys[h]), int(n) | (w << 63)))
+        runs.sort(key=lambda r: r[0])  # owner-grouped
+        flat = np.array([[k, lw] for _, k, lw in runs], dtype=np.uint64).reshape(-1)
+        counts = np.bincount([r[0] for r in runs], minlength=nranks).tolist() if runs else [0] * nranks
+        return torch.from_numpy(flat.view(np.int64).copy() if flat.size else np.zeros(1, np.int64)), counts
 
+    def memory_partial_runs(self, recv, n_runs, km, lo, n_owned, total_m):
+        r = recv[: 2 * n_runs].numpy().view(np.uint64).reshape(-1, 2)
+        keys = [np.zeros(0, np.uint64), np.zeros(0, np.uint64)]
+        for w in (0, 1):
+            sel = r[(r[:, 1] >> np.uint64(63)) == np.uint64(w)]
+            if sel.size:
+                lens = (sel[:, 1] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+                starts = np.repeat(sel[:, 0], lens)
+                offs = np.arange(lens.sum()) - np.repeat(np.cumsum(lens) - lens, lens)
+                keys[w] = starts + offs.astype(np.uint64)
+        return self._partial_from_keys(keys, km, lo, n_owned, total_m)
+
+    def memory_partial(self, recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m):
         rd = recv_r[:n_r].numpy().view(np.uint64)
         wr = recv_w[:n_w].numpy().view(np.uint64)
         keys = [((a - np.uint64(km.base)) >> np.uint64(km.k)) for a in (rd, wr)]
+        return self._partial_from_keys(keys, km, lo, n_owned, total_m)
+
+    def _partial_from_keys(self, keys, km, lo, n_owned, total_m):
+        from paper_1805_04207_b200.dist import CBINS, MemoryPartial
+
         for kk in keys:  # every received address belongs to this owner's key range
             assert ((kk >= np.uint64(lo)) & (kk - np.uint64(lo) < np.uint64(max(n_owned, 1)))).all()
         allk = np.concatenate(keys)
@@ -124,7 +161,7 @@ def _worker(rank, world, port, names, q):
                                   tr.local_size, tr.opcodes, tr.extra_groups)
             rep = D.sharded_report(OracleBackend(len(tr.opcodes)), shard, lo, tr.kernel_name, tr.invocation,
                                    tr.global_size, tr.local_size, tr.opcodes)
-            q.put((rank, name, report_to_dict(rep)))
+            q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
     finally:
         dist.destroy_process_group()
 
@@ -145,8 +182,11 @@ def test_sharded_reports_match_reference(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     want = {c["name"]: c["report"] for c, _ in golden_cases() if c["name"] in CASES}
-    for rank, name, rep in got:
+    modes = set()
+    for rank, name, rep, mode in got:
         assert_report_matches(rep, want[name])
+        modes.add(mode)
+    assert {"runs", "raw"} <= modes  # both address exchanges were exercised
 
 
 def test_key_map_owner_ranges_are_block_aligned():

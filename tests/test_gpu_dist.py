@@ -60,13 +60,13 @@ def _worker(rank, world, port, q):
                                   tr.extra_groups)
             rep = D.sharded_report(backend, shard, lo, tr.kernel_name, tr.invocation, tr.global_size,
                                    tr.local_size, tr.opcodes)
-            q.put((rank, name, report_to_dict(rep)))
+            q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
         for cfg, w in SYNTH:
             first, count = synth.shard_range(cfg, w, rank, world)
             shard = synth.device_trace(cfg, w, first=first, count=count)
             rep = D.sharded_report(backend, shard, first, shard.kernel_name, 0, shard.global_size,
                                    shard.local_size, shard.opcodes)
-            q.put((rank, f"C{cfg}", report_to_dict(rep)))
+            q.put((rank, f"C{cfg}", report_to_dict(rep), D.LAST_EXCHANGE))
     finally:
         dist.destroy_process_group()
 
@@ -89,5 +89,8 @@ def test_sharded_cuda_backend_matches_whole_trace(world):
     want = {c["name"]: c["report"] for c, _ in golden_cases() if c["name"] in GOLDEN}
     for cfg, w in SYNTH:
         want[f"C{cfg}"] = report_to_dict(finalize(consume(synth.device_trace(cfg, w))))
-    for rank, name, rep in got:
+    modes = set()
+    for rank, name, rep, mode in got:
         assert_report_matches(rep, want[name])
+        modes.add(mode)
+    assert {"runs", "raw"} <= modes  # both address exchanges ran through the CUDA engine
