@@ -292,7 +292,10 @@ def run_ours(args) -> None:
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # the multi-GPU (work-group shard) path; AIWC_BENCH_SHARDED=1 forces it at one
+    # rank under torchrun (a single-GPU check of the N>1 code path)
+    sharded = world > 1 or os.environ.get("AIWC_BENCH_SHARDED") == "1"
+    if sharded:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -307,8 +310,8 @@ def run_ours(args) -> None:
     stream = torch.cuda.current_stream(dev)
     res = _native.Result()
 
-    n_streams = max(1, args.streams) if world == 1 else 1
-    if world == 1:
+    n_streams = max(1, args.streams) if not sharded else 1
+    if not sharded:
         # one engine context per CUDA stream; with several, concurrent host threads
         # each push whole trace -> report steps (the reference allows distinct
         # streams to run concurrently, pkg/README.md:192-193), so one stream's
@@ -370,7 +373,7 @@ def run_ours(args) -> None:
 
     # device stream validation of the same columns (what consume() runs for untrusted columnar input)
     validate_ms = None
-    if world == 1:
+    if not sharded:
         vctx = _native.Context(local)
         vout = _native.Violation()
         i64x3 = ctypes.c_int64 * 3
@@ -389,7 +392,7 @@ def run_ours(args) -> None:
         if rank == 0:
             print(json.dumps({"ms_per_step": ms_step, "value": value, "phases_ms": phase_med,
                               "validate_ms": validate_ms}), flush=True)
-        if world > 1:
+        if sharded:
             dist.destroy_process_group()
         return
     # ---- e2e: the public API from pinned host columns (H2D + result D2H inside) ----
@@ -398,7 +401,7 @@ def run_ours(args) -> None:
     hk.copy_(tr.kind)
     hp.copy_(tr.payload)
     host_tr = ColumnarTrace(hk, hp, tr.kernel_name, 0, tr.global_size, tr.local_size, tr.opcodes, [], tr.addr_stats)
-    if world == 1:
+    if not sharded:
         def e2e_step():
             return finalize(consume(host_tr, max_entries=1 << 62, device=local))
     else:
@@ -422,10 +425,10 @@ def run_ours(args) -> None:
     ingest_ms = phase_med["ingest"]
     achieved = ALG_BYTES_PER_EVENT * count / (ingest_ms / 1e3) / 1e9
     step_alg = ALG_BYTES_PER_EVENT * count / (ms_step / 1e3) / 1e9
-    traffic, traffic_src = ncu_traffic(cfg) if world == 1 else (None, None)
+    traffic, traffic_src = ncu_traffic(cfg) if not sharded else (None, None)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, w, args)
     if rank == 0:
         line = {
@@ -436,11 +439,11 @@ def run_ours(args) -> None:
                                    f"local {synth.LOCAL[cfg]}, {world} work-group shard(s)",
                        "events_per_rank": count, "l2": "trace (9 B/event) larger than L2; no flush needed",
                        "streams": n_streams,
-                       "parallelism": f"replica (N=1), {n_streams} concurrent trace streams" if world == 1 else
+                       "parallelism": f"replica (N=1), {n_streams} concurrent trace streams" if not sharded else
                                       f"work-group shards x{world}; NCCL all-reduce + address all-to-all"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
-                    "d2h_bytes_per_step": lanes[0][2].d2h_bytes if world == 1 else backend.last_d2h, "ms_per_step": e2e_ms,
-                    "path": "consume(ColumnarTrace on pinned host)+finalize" if world == 1 else
+                    "d2h_bytes_per_step": lanes[0][2].d2h_bytes if not sharded else backend.last_d2h, "ms_per_step": e2e_ms,
+                    "path": "consume(ColumnarTrace on pinned host)+finalize" if not sharded else
                             "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
@@ -457,7 +460,7 @@ def run_ours(args) -> None:
                              "footprint_90": rep.footprint_90},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
 
 
