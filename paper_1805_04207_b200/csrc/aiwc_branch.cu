@@ -114,11 +114,11 @@ __global__ void __launch_bounds__(256) pattern_walk_kernel(const uint8_t* __rest
 __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __restrict__ code, uint64_t n,
                                                              uint32_t H, uint32_t n_parts, uint64_t chunk_len,
                                                              unsigned long long* __restrict__ partials) {
-  extern __shared__ uint32_t cnt[];  // [2][part_size]: total, taken
+  extern __shared__ uint32_t cnt[];  // [2][part_size]: not taken, taken (one atomic per observation)
   const uint32_t part = blockIdx.x % n_parts, chunk = blockIdx.x / n_parts;
   const uint32_t part_size = (1u << H) / n_parts;
   const uint32_t shift = 31 - __clz(part_size) + 1;  // code >> shift = partition
-  uint32_t* tot = cnt;
+  uint32_t* nt = cnt;
   uint32_t* tk = cnt + part_size;
   for (uint32_t i = threadIdx.x; i < 2 * part_size; i += PC_T) cnt[i] = 0;
   __syncthreads();
@@ -129,8 +129,7 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   auto add = [&](uint32_t c, uint32_t k) {
     if (c != NO_OBS && (c >> shift) == part) {
       const uint32_t slot = (c >> 1) & (part_size - 1);
-      atomicAdd(&tot[slot], k);
-      if (c & 1) atomicAdd(&tk[slot], k);
+      atomicAdd(((c & 1) ? tk : nt) + slot, k);
     }
   };
   auto count4 = [&](const uint4 q) {
@@ -154,7 +153,7 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   __syncthreads();
   unsigned long long* out = partials + (uint64_t)chunk * (1u << H) + (uint64_t)part * part_size;
   for (uint32_t i = threadIdx.x; i < part_size; i += PC_T)
-    out[i] = ((unsigned long long)tot[i] << 32) | tk[i];
+    out[i] = ((unsigned long long)(nt[i] + tk[i]) << 32) | tk[i];
 }
 
 // tab[p] = sum over chunks of the partial tables
