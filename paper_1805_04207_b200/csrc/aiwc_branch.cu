@@ -38,20 +38,34 @@ constexpr int PC_HALO = 16;               // warm-up window (>= history_len)
 constexpr int PC_PART_BITS = 14;          // patterns per partition: 2^14 (128 KB of counters)
 constexpr int PC_CHUNK_ALIGN = 16;
 
+__device__ __forceinline__ void stage_one(uint64_t i, uint64_t r, uint64_t prev, uint8_t* __restrict__ bits,
+                                          DevState* st, unsigned long long* big_list) {
+  const bool head = (i == 0) || ((prev >> 1) != (r >> 1));
+  bits[i] = (uint8_t)((r & 1) | (head ? 2 : 0));
+  const uint64_t site = r >> 32;
+  if (i == 0 || (prev >> 32) != site) {
+    const unsigned long long j = atomicAdd(&st->n_sites, 1ull);
+    if (j < (unsigned long long)MAX_SMALL_LIST) {
+      st->site_list[2 * j] = site; st->site_list[2 * j + 1] = i;
+    }
+    big_list[2 * j] = site; big_list[2 * j + 1] = i;
+  }
+}
+
+// two consecutive records per thread from one 16-byte load (the first one's
+// predecessor is re-read, usually an L1 hit); records are 16-byte aligned
 __global__ void branch_stage_kernel(const uint64_t* __restrict__ rec, uint64_t n, uint8_t* __restrict__ bits,
                                     DevState* st, unsigned long long* big_list) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t r = rec[i];
-    const uint64_t prev = i ? rec[i - 1] : ~r;
-    const bool head = (i == 0) || ((prev >> 1) != (r >> 1));
-    bits[i] = (uint8_t)((r & 1) | (head ? 2 : 0));
-    const uint64_t site = r >> 32;
-    if (i == 0 || (prev >> 32) != site) {
-      const unsigned long long j = atomicAdd(&st->n_sites, 1ull);
-      if (j < (unsigned long long)MAX_SMALL_LIST) {
-        st->site_list[2 * j] = site; st->site_list[2 * j + 1] = i;
-      }
-      big_list[2 * j] = site; big_list[2 * j + 1] = i;
+  const uint64_t T = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; 2 * p < n; p += T) {
+    const uint64_t i = 2 * p;
+    if (i + 1 < n) {
+      const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(rec + i);
+      const uint64_t prev = i ? rec[i - 1] : ~v.x;
+      stage_one(i, v.x, prev, bits, st, big_list);
+      stage_one(i + 1, v.y, v.x, bits, st, big_list);
+    } else {
+      stage_one(i, rec[i], i ? rec[i - 1] : ~rec[i], bits, st, big_list);
     }
   }
 }
