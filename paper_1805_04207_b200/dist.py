@@ -228,7 +228,13 @@ def comm_device(backend, group=None):
 
 
 def sharded_result(backend, shard, shard_offset: int, group=None):
-    """Every rank: exact whole-trace EngineResult from its work-group shard."""
+    """Every rank: exact whole-trace EngineResult from its work-group shard.
+
+    Collectives: one object all-gather of the small per-shard partials (counts,
+    opcode / ITB / IPT histograms, overflow and width / site lists, address
+    statistics), the 2^16 branch pattern table all-reduce only when the trace
+    has branches, the address exchange (run-count all-reduce + two all-to-alls),
+    and one object all-gather of the owners' memory partials."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -236,29 +242,30 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
     device = comm_device(backend, group)
     sp: ShardPartial = backend.shard(shard, shard_offset)
 
-    # ---- sums: one packed all-reduce ----
-    scalars = np.array([sp.n_events, sp.total_instructions, sp.work_items, sp.barriers_hit, sp.total_reads,
-                        sp.total_writes, sp.itb_sum, sp.ipt_sum, sp.branch_executions], dtype=np.uint64)
-    packed = np.concatenate([scalars, sp.opcode_counts.astype(np.uint64), sp.itb_hist, sp.ipt_hist,
-                             sp.branch_table.astype(np.uint64)])
-    summed = _allreduce_i64(packed, dist.ReduceOp.SUM, group, device)
-    o = 0
-    sc = [int(v) for v in summed[o:o + len(scalars)]]; o += len(scalars)
-    n_opc = len(sp.opcode_counts)
-    opcode_counts = [int(v) for v in summed[o:o + n_opc]]; o += n_opc
-    itb_hist = summed[o:o + HBINS]; o += HBINS
-    ipt_hist = summed[o:o + HBINS]; o += HBINS
-    branch_table = summed[o:]
+    # ---- small partials: one object all-gather, summed / merged on the host ----
+    scalars = [int(sp.n_events), int(sp.total_instructions), int(sp.work_items), int(sp.barriers_hit),
+               int(sp.total_reads), int(sp.total_writes), int(sp.itb_sum), int(sp.ipt_sum),
+               int(sp.branch_executions)]
+    parts = _gather_objects((scalars, sp.opcode_counts.astype(np.uint64), sp.itb_hist, sp.ipt_hist,
+                             sp.itb_ovf.tolist(), sp.ipt_ovf.tolist(), sp.widths, sp.sites, sp.addr_stats), group)
+    sc = [sum(p[0][i] for p in parts) for i in range(len(scalars))]
+    opcode_counts = [int(v) for v in np.sum([p[1] for p in parts], axis=0)]
+    itb_hist = np.sum([p[2] for p in parts], axis=0).astype(np.uint64)
+    ipt_hist = np.sum([p[3] for p in parts], axis=0).astype(np.uint64)
+    itb_ovf, ipt_ovf, widths, sites = _merge_lists([p[4:8] for p in parts])
     n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec = sc
-
-    # ---- gathers: overflow values, widths, sites ----
-    parts = _gather_objects((sp.itb_ovf.tolist(), sp.ipt_ovf.tolist(), sp.widths, sp.sites), group)
-    itb_ovf, ipt_ovf, widths, sites = _merge_lists(parts)
+    # ---- branch pattern tables (each (site, group) stream is whole on one rank) ----
+    if br_exec:
+        branch_table = _allreduce_i64(sp.branch_table.astype(np.uint64), dist.ReduceOp.SUM, group, device)
+    else:
+        branch_table = np.zeros(len(sp.branch_table), np.uint64)
 
     # ---- addresses: global key map, owner exchange, owner partials ----
     total_m = total_reads + total_writes
     if total_m:
-        stats = allreduce_stats(sp.addr_stats, group, device)
+        st = [p[8] for p in parts if p[8] is not None]
+        stats = (min(x[0] for x in st), max(x[1] for x in st), int(np.bitwise_and.reduce([np.uint64(x[2]) for x in st])),
+                 int(np.bitwise_or.reduce([np.uint64(x[3]) for x in st])))
         km = key_map(stats, world)
         lo, n_owned = km.owned(rank)
         use_runs = False
@@ -267,9 +274,8 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
             # rank alike) when runs average >= RUN_MIN_AVG accesses (the owner
             # applies one run per warp: short runs would idle its lanes)
             runs, rcounts = backend.partition_runs(sp, km, world)
-            tot = _allreduce_i64(np.array([sum(rcounts), sp.total_reads + sp.total_writes], np.uint64),
-                                 dist.ReduceOp.SUM, group, device)
-            use_runs = RUN_MIN_AVG * int(tot[0]) <= int(tot[1])
+            tot = _allreduce_i64(np.array([sum(rcounts)], np.uint64), dist.ReduceOp.SUM, group, device)
+            use_runs = RUN_MIN_AVG * int(tot[0]) <= total_m
         global LAST_EXCHANGE
         LAST_EXCHANGE = "runs" if use_runs else "raw"
         if use_runs:
@@ -282,16 +288,18 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
             mp = backend.memory_partial(recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m)
     else:
         mp = MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(CBINS, np.uint64), np.zeros(0, np.uint64))
-    msum = _allreduce_i64(np.concatenate([np.array([mp.unique_reads, mp.unique_writes, mp.footprint], np.uint64),
-                                          mp.cnt_hist0.astype(np.uint64)]), dist.ReduceOp.SUM, group, device)
-    import torch
-
-    lsum = torch.from_numpy(np.asarray(mp.level_sum, dtype=np.float64).copy()).to(device)
-    dist.all_reduce(lsum, group=group)
-    level_sum = lsum.cpu().numpy()
-    big = np.sort(np.array([v for b in _gather_objects(mp.big.tolist(), group) for v in b], dtype=np.uint64))[::-1]
-    unique_r, unique_w, footprint = (int(v) for v in msum[:3])
-    hist0 = msum[3:]
+    # ---- owners' partials: one object all-gather (level sums added in rank order) ----
+    mparts = _gather_objects((int(mp.unique_reads), int(mp.unique_writes), int(mp.footprint),
+                              np.asarray(mp.level_sum, dtype=np.float64), mp.cnt_hist0.astype(np.uint64),
+                              mp.big.astype(np.uint64)), group)
+    unique_r = sum(m[0] for m in mparts)
+    unique_w = sum(m[1] for m in mparts)
+    footprint = sum(m[2] for m in mparts)
+    level_sum = np.zeros(11)
+    for m in mparts:
+        level_sum = level_sum + m[3]
+    hist0 = np.sum([m[4] for m in mparts], axis=0).astype(np.uint64)
+    big = np.sort(np.concatenate([m[5] for m in mparts]).astype(np.uint64))[::-1]
     return _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum,
                      br_exec, opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, branch_table, widths, sites,
                      unique_r, unique_w, footprint, hist0, big, level_sum)
