@@ -348,6 +348,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
       }
     }
   }
+  const size_t clean_prev = ctx->dtab_clean;  // undeclared traces: the previous finalize's clear may suffice
   ctx->dtab_clean = 0;
 
   // ---- pass 1: range summaries ----
@@ -433,8 +434,10 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   if (M) {
     if (ctx->dense) {
       const size_t tb = ctx->am.n_keys * (ctx->dense32 ? 4 : 8);
-      if (ctx->pre_zeroed) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
-      if (ctx->pre_zeroed < tb) {
+      size_t zeroed = ctx->pre_zeroed;
+      if (!zeroed && clean_prev >= tb && ctx->dtab.cap >= tb) zeroed = clean_prev;  // cleared on aux (join_ev)
+      if (zeroed) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
+      if (zeroed < tb) {
         CK(grow(ctx->dtab, tb));
         CK(cudaMemsetAsync(ctx->dtab.p, 0, tb, s));
       }
