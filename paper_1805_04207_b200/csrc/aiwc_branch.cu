@@ -14,14 +14,16 @@
 // H executions earlier; its pattern is the previous H outcomes, oldest as MSB
 // (entropy.py:112-114).  Observations are counted into one pooled 2^H table.
 //
-//   branch_stage_kernel    one coalesced pass: record -> byte (taken | head << 1),
-//                          plus the (site, first position) list
-//   pattern_count_kernel   blocks = record chunks x pattern partitions; each
-//                          block walks its chunk (16-record warm-up halo) and
-//                          counts the observations of its 2^14-pattern partition
-//                          in shared memory (no global atomics, no contention
-//                          between blocks), then writes its partition to a
-//                          per-chunk partial table
+//   branch_stage_kernel    one coalesced pass (two records per 16-byte load):
+//                          record -> byte (taken | head << 1), plus the
+//                          (site, first position) list
+//   pattern_walk_kernel    one walk over the bytes (16-record warm-up per 32
+//                          records): code = pattern << 1 | taken per observation
+//   pattern_count_kernel   blocks = code chunks x 2^14-pattern partitions; each
+//                          block counts its partition's observations in shared
+//                          memory (taken / not-taken counters: one atomic per
+//                          observation, no global atomics), then writes its
+//                          partition to a per-chunk partial table
 //   pattern_reduce_kernel  sums the per-chunk partials into the table
 //   branch_finish_kernel   yokota / linear in fixed reduction order
 #include <math.h>
