@@ -650,6 +650,7 @@ __global__ void __launch_bounds__(TPB, 2)
         constexpr bool HOT = decltype(with_window)::value;
         if (a.dense32) {
           uint32_t* const tab = static_cast<uint32_t*>(a.dense);
+#pragma unroll 4  // several accesses per lane in flight (C2 ingest -2.5 %, C5 -4 %)
           for (uint32_t i = lane; i < n_mem; i += 32) {
             const uint32_t e = midx[i];
             const uint64_t off = pay[e & 0x0FFFu] - base;
@@ -668,6 +669,7 @@ __global__ void __launch_bounds__(TPB, 2)
           }
         } else {
           unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
+#pragma unroll 4  // several accesses per lane in flight (C2 ingest -2.5 %, C5 -4 %)
           for (uint32_t i = lane; i < n_mem; i += 32) {
             const uint32_t e = midx[i];
             const uint64_t off = pay[e & 0x0FFFu] - base;
