@@ -48,20 +48,42 @@ __global__ void __launch_bounds__(DS_T) count_stats_kernel(const unsigned long l
   __syncthreads();
   double part = 0.0;
   unsigned long long ur = 0, uw = 0;
-  for (uint64_t i = (uint64_t)blockIdx.x * DS_T + threadIdx.x; i < n; i += (uint64_t)gridDim.x * DS_T) {
-    unsigned long long c = ca[i];
-    if (cb) {
-      const unsigned long long w = cb[i];
-      ur += c != 0; uw += w != 0;
-      c += w;
+  uint32_t cur = 0, run = 0;  // equal consecutive small counts of this thread: one atomic per run
+  // a few CTAs walk the whole array: UNR elements per thread in flight
+  constexpr int UNR = 8;
+  const uint64_t G = (uint64_t)gridDim.x * DS_T;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * DS_T + threadIdx.x; i0 < n; i0 += UNR * G) {
+    unsigned long long cv[UNR], wv[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const uint64_t i = i0 + u * G;
+      cv[u] = i < n ? ca[i] : 0ull;
+      wv[u] = (cb && i < n) ? cb[i] : 0ull;
     }
-    if (c == 0) continue;
-    if (c < (unsigned long long)CBINS) atomicAdd(&h[c], 1u);
-    else {
-      part += plogp(c, m);
-      if (level == 0) lvl0_ovf[atomicAdd(&st->lvl0_ovf_n, 1ull)] = c;
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      unsigned long long c = cv[u];
+      if (cb) {
+        const unsigned long long w = wv[u];
+        ur += c != 0; uw += w != 0;
+        c += w;
+      }
+      if (c == 0) continue;
+      if (c < (unsigned long long)CBINS) {
+        if ((uint32_t)c == cur) {
+          ++run;
+        } else {
+          if (run) atomicAdd(&h[cur], run);
+          cur = (uint32_t)c;
+          run = 1;
+        }
+      } else {
+        part += plogp(c, m);
+        if (level == 0) lvl0_ovf[atomicAdd(&st->lvl0_ovf_n, 1ull)] = c;
+      }
     }
   }
+  if (run) atomicAdd(&h[cur], run);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
