@@ -78,12 +78,74 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
+// ---- region compaction: clustered address spans keep the dense path ----
+// The memory statistics only depend on the multiset of accesses per address
+// group addr >> n (n <= 10), i.e. inside 1024-byte blocks.  Remapping every
+// occupied 1 MB region (addr >> 20) to consecutive 1 MB slots, low 20 bits
+// kept, preserves every group, count and entropy exactly; a trace whose
+// accesses sit in a few far-apart buffers then spans a few MB instead of the
+// distance between its buffers.
+constexpr uint32_t REG_SHIFT = 20, REG_SLOTS = 16384, REG_MAX = 4096;
+constexpr uint64_t REG_EMPTY = ~0ull, REG_BASE = 1ull << 20;
+
+__device__ __forceinline__ uint32_t reg_hash(uint64_t r) {
+  return (uint32_t)((r * 0x9E3779B97F4A7C15ull) >> (64 - 14));  // REG_SLOTS = 2^14
+}
+
+// distinct regions of the memory events: misc[0] = count, misc[1] = overflow
+__global__ void region_mark_kernel(const uint8_t* __restrict__ kind, const uint64_t* __restrict__ payload, uint64_t n,
+                                   unsigned long long* keys, uint32_t* misc) {
+  uint64_t last = REG_EMPTY;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    if (!is_mem(kind[i])) continue;
+    const uint64_t r = payload[i] >> REG_SHIFT;
+    if (r == last) continue;
+    last = r;
+    uint32_t h = reg_hash(r);
+    for (uint32_t probe = 0;; ++probe, h = (h + 1) & (REG_SLOTS - 1)) {
+      if (probe == 64) { atomicOr(&misc[1], 1u); break; }
+      const unsigned long long old = atomicCAS(&keys[h], REG_EMPTY, (unsigned long long)r);
+      if (old == REG_EMPTY) { if (atomicAdd(&misc[0], 1u) >= REG_MAX) atomicOr(&misc[1], 1u); break; }
+      if (old == r) break;
+    }
+  }
+}
+
+// remapped payload column (memory events only change) + its address statistics
+__global__ void region_remap_kernel(const uint8_t* __restrict__ kind, const uint64_t* __restrict__ payload, uint64_t n,
+                                    const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                    uint64_t* __restrict__ out, unsigned long long* stats) {
+  unsigned long long mn = ~0ull, mx = 0, an = ~0ull, o = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t p = payload[i];
+    if (is_mem(kind[i])) {
+      const uint64_t r = p >> REG_SHIFT;
+      uint32_t h = reg_hash(r);
+      while (keys[h] != r) h = (h + 1) & (REG_SLOTS - 1);  // every region was inserted
+      p = REG_BASE + ((uint64_t)vals[h] << REG_SHIFT) + (p & ((1ull << REG_SHIFT) - 1));
+      mn = min(mn, (unsigned long long)p); mx = max(mx, (unsigned long long)p); an &= p; o |= p;
+    }
+    out[i] = p;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+    an &= __shfl_xor_sync(0xffffffffu, an, d);
+    o |= __shfl_xor_sync(0xffffffffu, o, d);
+  }
+  if ((threadIdx.x & 31) == 0 && mn <= mx) {
+    atomicMin(&stats[0], mn); atomicMax(&stats[1], mx); atomicAnd(&stats[2], an); atomicOr(&stats[3], o);
+  }
+}
+
 struct aiwc_ctx {
   int device = 0;
   int n_sms = 148;
   aiwc_opts opts{};
   aiwc_error err{};
   int state = 0;  // 0 empty, 1 ingested, 2 finalized
+  Buf reg_keys, reg_vals, reg_misc, remap_pay;  // region compaction of clustered address spans
   Buf dev_state, ranges, opc, wcount, wfirst, wpres, itb_ovf, ipt_ovf, ipt_tab, dtab, rd, wr, br, partials, lvl0_ovf,
       sparse_scr, branch_scr, branch_tab, kind_stage, pay_stage, sort_a, sort_b, sort_h;
   DevState* h_state = nullptr;  // pinned
@@ -95,6 +157,7 @@ struct aiwc_ctx {
   bool dense = false;
   bool dense32 = false;     // u32 count|flags entries (fewer than 2^30 accesses)
   bool hot_off = false;     // AIWC_HOT_WINDOW=0 disables the shared-memory hot-key window (measurement)
+  bool region_off = false;  // AIWC_REGIONS=0 disables region compaction of wide address spans (measurement)
   int dense_entry = 0;      // AIWC_DENSE_ENTRY=32|64 forces the entry width (measurement), 0 = rule
   uint64_t ipt_tab_len = 0;
   uint32_t n_ranges = 0, tiles_per_cta = 0;
@@ -170,6 +233,7 @@ extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts
   *out = ctx;
   if (const char* de = getenv("AIWC_DENSE_ENTRY")) ctx->dense_entry = atoi(de);
   if (const char* hw = getenv("AIWC_HOT_WINDOW")) ctx->hot_off = atoi(hw) == 0;
+  if (const char* rg = getenv("AIWC_REGIONS")) ctx->region_off = atoi(rg) == 0;
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device));
   if (ctx->opts.dense_budget_bytes == 0) {
@@ -205,7 +269,8 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
                  &ctx->lvl0_ovf, &ctx->sparse_scr, &ctx->branch_scr, &ctx->branch_tab, &ctx->kind_stage,
                  &ctx->pay_stage, &ctx->sort_a, &ctx->sort_b, &ctx->sort_h, &ctx->part_entries,
                  &ctx->part_cursor, &ctx->mp_state, &ctx->mp_tab, &ctx->mp_partials, &ctx->mp_ovf, &ctx->wpres,
-                 &ctx->run_pos, &ctx->run_blk, &ctx->run_scan,
+                 &ctx->run_pos, &ctx->run_blk, &ctx->run_scan, &ctx->reg_keys, &ctx->reg_vals, &ctx->reg_misc,
+                 &ctx->remap_pay,
                  &ctx->v_state, &ctx->v_tiles, &ctx->v_scan, &ctx->v_spos, &ctx->v_spay, &ctx->v_sgap,
                  &ctx->v_gstart, &ctx->v_recs, &ctx->v_counts, &ctx->v_srange, &ctx->v_fwge, &ctx->v_keys,
                  &ctx->v_keys_tmp, &ctx->v_hist, &ctx->v_prevk, &ctx->v_unf, &ctx->v_bmm};
@@ -275,6 +340,51 @@ static int encode_maps_uncached(aiwc_ctx* ctx, const uint8_t* kind, const uint64
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(ctx, AIWC_ERR_CUDA, "tensor map (payload) encode failed");
+  return AIWC_OK;
+}
+
+// Region compaction (see region_mark_kernel): *out = the remapped payload column
+// (ctx-owned) and stats[4] its address statistics, or *out = null when the
+// accesses touch too many regions (the sparse path then handles the trace).
+static int region_compact(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, uint64_t n, cudaStream_t s,
+                          const uint64_t** out, unsigned long long* stats) {
+  *out = nullptr;
+  CK(grow(ctx->reg_keys, REG_SLOTS * 8));
+  CK(grow(ctx->reg_vals, REG_SLOTS * 4));
+  CK(grow(ctx->reg_misc, 64));
+  unsigned long long* keys = P<unsigned long long>(ctx->reg_keys);
+  uint32_t* misc = P<uint32_t>(ctx->reg_misc);
+  CK(cudaMemsetAsync(keys, 0xFF, REG_SLOTS * 8, s));
+  CK(cudaMemsetAsync(misc, 0, 64, s));
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)ctx->n_sms * 8);
+  region_mark_kernel<<<grid, 256, 0, s>>>(kind, payload, n, keys, misc);
+  uint32_t hm[2];
+  CK(cudaMemcpyAsync(hm, misc, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  ctx->kernels += 1;
+  if (hm[1] || hm[0] == 0 || hm[0] > REG_MAX) return AIWC_OK;
+  std::vector<unsigned long long> hk(REG_SLOTS);
+  CK(cudaMemcpyAsync(hk.data(), keys, REG_SLOTS * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::vector<unsigned long long> regs;
+  for (unsigned long long k : hk)
+    if (k != REG_EMPTY) regs.push_back(k);
+  std::sort(regs.begin(), regs.end());  // slots in address order
+  std::vector<uint32_t> hv(REG_SLOTS, 0);
+  for (uint32_t i = 0; i < REG_SLOTS; ++i)
+    if (hk[i] != REG_EMPTY) hv[i] = (uint32_t)(std::lower_bound(regs.begin(), regs.end(), hk[i]) - regs.begin());
+  CK(cudaMemcpyAsync(ctx->reg_vals.p, hv.data(), REG_SLOTS * 4, cudaMemcpyHostToDevice, s));
+  CK(grow(ctx->remap_pay, (n + 1) * 8));
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(misc + 4);
+  const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+  CK(cudaMemcpyAsync(st, init, 32, cudaMemcpyHostToDevice, s));
+  region_remap_kernel<<<grid, 256, 0, s>>>(kind, payload, n, keys, P<uint32_t>(ctx->reg_vals),
+                                           P<uint64_t>(ctx->remap_pay), st);
+  CK(cudaMemcpyAsync(stats, st, 32, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  ctx->kernels += 1;
+  *out = P<uint64_t>(ctx->remap_pay);
   return AIWC_OK;
 }
 
@@ -388,35 +498,52 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   } else {
     amin = info->addr_min; amax = info->addr_max; aand = info->addr_and; aor = info->addr_or;
   }
-  ctx->dense = false;
-  ctx->dense32 = M < E32_MAX_ACCESSES;
-  ctx->am = AddrMap{};
-  if (M) {
-    if (amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
-    AddrMap& am = ctx->am;
-    am.base = amin & ~1023ull;
-    am.hi = amax;
-    const uint64_t vary = aand ^ aor;
-    // constant low bits dropped from keys; capped at 32 so the per-event check of
-    // the dropped bits is one 32-bit compare in the ingest kernel
-    am.k = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
-    am.low_mask = am.k >= 64 ? ~0ull : ((1ull << am.k) - 1);
-    am.low_const = (amin - am.base) & am.low_mask;
-    const uint64_t span_keys = (amax - am.base) >> am.k;
-    am.n_keys = span_keys + 1;
-    am.off_max = (span_keys << am.k) | am.low_mask;
-    // u32 entries cost a second (flag) RED per access but halve the table:
-    // worth it when the table traffic dominates (few accesses per key)
-    // With the hot-key window (keys of one contended 1024-key block counted in shared
-    // memory) the flag RED of the u32 form stays cheap up to a few accesses per key.
-    const bool hot_window = am.n_keys > SMEM_TABLE_KEYS && M >= HOT_MIN_ACCESSES && !ctx->hot_off;
-    ctx->dense32 = M < E32_MAX_ACCESSES && (M <= am.n_keys || (hot_window && M <= 4 * am.n_keys));
-    if (ctx->dense_entry == 32) ctx->dense32 = M < E32_MAX_ACCESSES && am.n_keys > SMEM_TABLE_KEYS;
-    if (ctx->dense_entry == 64) ctx->dense32 = false;
-    const bool fits = span_keys < (1ull << 40) && am.n_keys * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
-                      am.n_keys <= 4 * M + (1ull << 20);
-    // a shard keeps its addresses compacted: they are exchanged with the key owners
-    ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
+  auto decide_memory = [&](uint64_t amin, uint64_t amax, uint64_t aand, uint64_t aor) {
+    ctx->dense = false;
+    ctx->dense32 = M < E32_MAX_ACCESSES;
+    ctx->am = AddrMap{};
+    if (M) {
+      AddrMap& am = ctx->am;
+      am.base = amin & ~1023ull;
+      am.hi = amax;
+      const uint64_t vary = aand ^ aor;
+      // constant low bits dropped from keys; capped at 32 so the per-event check of
+      // the dropped bits is one 32-bit compare in the ingest kernel
+      am.k = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
+      am.low_mask = am.k >= 64 ? ~0ull : ((1ull << am.k) - 1);
+      am.low_const = (amin - am.base) & am.low_mask;
+      const uint64_t span_keys = (amax - am.base) >> am.k;
+      am.n_keys = span_keys + 1;
+      am.off_max = (span_keys << am.k) | am.low_mask;
+      // u32 entries cost a second (flag) RED per access but halve the table:
+      // worth it when the table traffic dominates (few accesses per key)
+      // With the hot-key window (keys of one contended 1024-key block counted in shared
+      // memory) the flag RED of the u32 form stays cheap up to a few accesses per key.
+      const bool hot_window = am.n_keys > SMEM_TABLE_KEYS && M >= HOT_MIN_ACCESSES && !ctx->hot_off;
+      ctx->dense32 = M < E32_MAX_ACCESSES && (M <= am.n_keys || (hot_window && M <= 4 * am.n_keys));
+      if (ctx->dense_entry == 32) ctx->dense32 = M < E32_MAX_ACCESSES && am.n_keys > SMEM_TABLE_KEYS;
+      if (ctx->dense_entry == 64) ctx->dense32 = false;
+      const bool fits = span_keys < (1ull << 40) && am.n_keys * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
+                        am.n_keys <= 4 * M + (1ull << 20);
+      // a shard keeps its addresses compacted: they are exchanged with the key owners
+      ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
+    }
+  };
+  if (M && amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
+  decide_memory(amin, amax, aand, aor);
+  // a span too wide for the table: if the accesses sit in few 1 MB regions, squeeze
+  // the regions together (exact for every memory statistic) and keep the dense path
+  if (M && n && !ctx->dense && !(ctx->opts.flags & AIWC_OPT_SHARD) && !ctx->region_off) {
+    const uint64_t* np = nullptr;
+    unsigned long long rs[4];
+    const int rc = region_compact(ctx, kind, payload, n, s, &np, rs);
+    if (rc) return rc;
+    if (np) {
+      payload = np;
+      const int rc2 = encode_maps(ctx, kind, payload, rows, &km, &pm);
+      if (rc2) return rc2;
+      decide_memory(rs[0], rs[1], rs[2], rs[3]);
+    }
   }
   const bool stage = !ctx->dense || ctx->n_br > 0;
 
