@@ -374,7 +374,10 @@ static int region_compact(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* pa
   for (uint32_t i = 0; i < REG_SLOTS; ++i)
     if (hk[i] != REG_EMPTY) hv[i] = (uint32_t)(std::lower_bound(regs.begin(), regs.end(), hk[i]) - regs.begin());
   CK(cudaMemcpyAsync(ctx->reg_vals.p, hv.data(), REG_SLOTS * 4, cudaMemcpyHostToDevice, s));
-  CK(grow(ctx->remap_pay, (n + 1) * 8));
+  if (grow(ctx->remap_pay, (n + 1) * 8) != cudaSuccess) {  // no room for the remapped column: sparse path
+    cudaGetLastError();
+    return AIWC_OK;
+  }
   unsigned long long* st = reinterpret_cast<unsigned long long*>(misc + 4);
   const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
   CK(cudaMemcpyAsync(st, init, 32, cudaMemcpyHostToDevice, s));
