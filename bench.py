@@ -416,6 +416,18 @@ def run_ours(args) -> None:
     rep = out["rep"]
     e2e_ms = max(e_ms, e_wall) / e2e_steps
     e2e_value = n_total / (e2e_ms / 1e3)
+    # The e2e ceiling is the host link: time a bare pinned-host -> device copy of the same
+    # two columns (no compute) so the line says how close the API path gets to it.
+    dk = torch.empty(count, dtype=torch.uint8, device=dev)
+    dp = torch.empty(count, dtype=torch.int64, device=dev)
+
+    def bare_h2d():
+        dk.copy_(hk, non_blocking=True)
+        dp.copy_(hp, non_blocking=True)
+    bare_h2d()
+    h_ms, _, _ = _timed(bare_h2d, 3, torch.cuda.current_stream(dev), dev, 1, local)
+    h2d_peak = 9 * count / (h_ms / 3 / 1e3) / 1e9
+    del dk, dp
 
     # ---- roofline of the dominant kernel (the ingest pass), per rank ----
     peaks = measured_peaks()
@@ -443,6 +455,8 @@ def run_ours(args) -> None:
                                       f"work-group shards x{world}; NCCL all-reduce + address all-to-all"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
                     "d2h_bytes_per_step": lanes[0][2].d2h_bytes if not sharded else backend.last_d2h, "ms_per_step": e2e_ms,
+                    "h2d_gbs": 9 * count / (e2e_ms / 1e3) / 1e9, "bare_h2d_gbs": h2d_peak,
+                    "link_frac": (9 * count / (e2e_ms / 1e3) / 1e9) / h2d_peak,
                     "path": "consume(ColumnarTrace on pinned host)+finalize" if not sharded else
                             "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -35,6 +35,8 @@ def test_bench_contract_and_sharded_path_agree():
         assert key in single, key
     assert single["value"] > 0 and single["e2e"]["value"] > 0 and single["gpu_launches"] > 0
     assert single["roofline"]["bound"] == "hbm" and 0 < single["roofline"]["frac"] < 1
+    e2e = single["e2e"]
+    assert e2e["h2d_bytes_per_step"] > 0 and e2e["bare_h2d_gbs"] > 0 and 0 < e2e["link_frac"] < 1.2
     sharded = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
                      "--master-addr", "127.0.0.1", "--master-port", "29561", "bench.py", "--gpus", "1", *ARGS],
                     env={"AIWC_BENCH_SHARDED": "1"})
