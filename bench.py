@@ -12,12 +12,17 @@ inside the timed region.  The trace (2.4 GB) is larger than L2, so no L2 flush
 is needed between steps.
 
 `--impl reference` times the reference algorithm's CPU restatement
-(oracle/aiwc_oracle.c; the Python reference cannot travel to the GPU box) on a
-bounded prefix of the same trace, on rank 0 only.
+(oracle/aiwc_oracle_mt.c; the Python reference cannot travel to the GPU box)
+on all host threads, on a bounded prefix of the same trace, rank 0 only.  Its
+input comes from the pure-numpy generator (oracle/synth_np.py), so that arm
+never loads the product library; both arms print the identical `config`.
 
-Under torchrun (N>1) every rank processes its own work-group shard of an
-N-times larger trace (weak scaling) and the per-rank reductions are combined
-over NCCL (paper_1805_04207_b200/dist.py).
+`--gpus N` (N>1) re-executes itself under torch.distributed.run with one rank
+per GPU unless it already runs under torchrun.  Every rank processes its own
+work-group shard: `--scaling weak` (default) of an N-times larger trace,
+`--scaling strong` of the one fixed-size trace (e.g. `--config 3`, the 2 B-event
+north_star target), and the per-rank reductions are combined over NCCL
+(paper_1805_04207_b200/dist.py).
 """
 
 from __future__ import annotations
@@ -145,38 +150,52 @@ def host_threads() -> int:
         return max(1, os.cpu_count() or 1)
 
 
-def reference_sample(cfg: int, w: int, args, threads: int):
+def reference_sample(cfg: int, total_wi: int, args, threads: int):
     """A bounded prefix of whole work-groups of the same trace (a valid trace),
-    sized for ~10 s of CPU work per step: 2^21 work-items per 2 threads."""
-    from paper_1805_04207_b200 import synth
+    sized for ~10 s of CPU work per step: 2^21 work-items per 2 threads.  Built
+    by the pure-numpy generator (oracle/synth_np.py, bit-identical to the device
+    generator) so the reference arm never loads the product library."""
+    from oracle import synth_np
 
-    sample_wi = min(w, args.ref_sample_wi * max(1, threads // 2))
-    if args.ref_python_gen:
-        return sample_wi, synth.python_trace(cfg, sample_wi)
-    import torch
+    lv = synth_np.LOCAL[cfg]
+    sample_wi = min(total_wi, args.ref_sample_wi * max(1, threads // 2))
+    sample_wi -= sample_wi % lv
+    kind, payload = synth_np.trace(cfg, sample_wi)
+    if sample_wi < total_wi:
+        # a prefix of whole work-groups is a valid trace once it is closed by kernel_end
+        kind[-1], payload[-1] = synth_np.K_KE, 0
+    return sample_wi, kind, payload
 
-    torch.cuda.set_device(0)
-    return sample_wi, synth.device_trace(cfg, sample_wi).to_numpy()
+
+def bench_config(cfg: int, world: int, w: int, scaling: str) -> dict:
+    """The workload both arms report (identical dict: the driver compares them)."""
+    from oracle import synth_np
+
+    total_wi = world * w if scaling == "weak" else w
+    n_total = synth_np.n_events(cfg, total_wi)
+    return {"workload": f"C{cfg} {synth_np.NAMES[cfg]}: {total_wi} work-items ({n_total} events), "
+                        f"local {synth_np.LOCAL[cfg]}",
+            "events": n_total, "work_items": total_wi, "scaling": scaling,
+            "l2": "trace (9 B/event) larger than the 126 MB L2; no flush needed" if 9 * n_total > (252 << 20) else
+                  "trace smaller than L2",
+            "parallelism": "replica (N=1)" if world == 1 else f"work-group shards x{world} ({scaling} scaling)"}
 
 
 def run_reference(args) -> None:
     world, rank, _ = _dist_env()
     if rank != 0:
         return
-    import numpy as np
-
-    from oracle import oracle
-    from paper_1805_04207_b200 import synth
+    from oracle import oracle, synth_np
 
     oracle.build()
     cfg = args.config
-    w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
+    w = args.work_items or synth_np.FULL_WORK_ITEMS[cfg]
+    config = bench_config(cfg, world, w, args.scaling)
     threads = host_threads()
-    sample_wi, tr = reference_sample(cfg, w, args, threads)
-    kind, payload = tr.kind, tr.payload.view(np.uint64)
+    sample_wi, kind, payload = reference_sample(cfg, config["work_items"], args, threads)
     n = int(kind.shape[0])
-    run = lambda: oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes),  # noqa: E731
-                             threads=threads)
+    run = lambda: oracle.run(kind, payload, kernel=synth_np.NAMES[cfg], invocation=0,  # noqa: E731
+                             n_opcodes=len(synth_np.OPCODES[cfg]), threads=threads)
     for _ in range(args.warmup):
         run()
     times = []
@@ -186,16 +205,16 @@ def run_reference(args) -> None:
         times.append(time.perf_counter() - t0)
     dt = statistics.median(times)
     v = n / dt
+    whole = sample_wi == config["work_items"]
+    sample = (f"{'the whole trace' if whole else f'first {sample_wi} work-items'} of C{cfg} ({n} events, numpy "
+              f"generator oracle/synth_np.py); oracle/aiwc_oracle_mt.c: consume+finalize restatement on {threads} "
+              "threads (work-group shards + address-owner merge, SURVEY 8d(ii)); median step")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
-        "config": {"workload": f"C{cfg} {synth.NAMES[cfg]} prefix of {sample_wi} work-items ({n} events)",
-                   "full_workload_work_items": w},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"first {sample_wi} work-items of C{cfg} ({n} events); oracle/aiwc_oracle_mt.c: "
-                                   f"consume+finalize restatement on {threads} threads (work-group shards + "
-                                   "address-owner merge, SURVEY 8d(ii))"},
+        "config": config,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -290,6 +309,8 @@ def run_ours(args) -> None:
     from paper_1805_04207_b200.trace import ColumnarTrace
 
     world, rank, local = _dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     # the multi-GPU (work-group shard) path; AIWC_BENCH_SHARDED=1 forces it at one
@@ -301,32 +322,34 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     cfg = args.config
     w = args.work_items or synth.FULL_WORK_ITEMS[cfg]
-    # weak scaling: the job is one world*w work-item trace; rank r owns the
-    # contiguous work-group shard synth.shard_range(cfg, world*w, r, world)
-    total_wi = world * w
+    config = bench_config(cfg, world, w, args.scaling)
+    # weak scaling: the job is one world*w work-item trace, strong scaling one w
+    # work-item trace; rank r owns the contiguous work-group shard
+    # synth.shard_range(cfg, total_wi, r, world) of it
+    total_wi = config["work_items"]
     first, count = synth.shard_range(cfg, total_wi, rank, world)
     tr = synth.device_trace(cfg, total_wi, first=first, count=count)
-    n_total = synth.n_events(cfg, total_wi)
+    n_total = config["events"]
     stream = torch.cuda.current_stream(dev)
-    res = _native.Result()
 
     n_streams = max(1, args.streams) if not sharded else 1
     if not sharded:
         # one engine context per CUDA stream; with several, concurrent host threads
         # each push whole trace -> report steps (the reference allows distinct
         # streams to run concurrently, pkg/README.md:192-193), so one stream's
-        # small kernels and host round trip overlap another stream's ingest
+        # small kernels and host round trip overlap another stream's ingest.
+        # Every lane reads its OWN copy of the trace (no cross-lane L2 reuse).
         info = trace_info(tr)
-        kptr = ctypes.c_void_p(tr.kind.data_ptr())
-        pptr = ctypes.c_void_p(tr.payload.data_ptr())
         lanes = []
         for i in range(n_streams):
             cs = stream if i == 0 else torch.cuda.Stream(dev)
+            ltr = tr if i == 0 else synth.device_trace(cfg, total_wi, first=first, count=count)
             lanes.append((_native.Context(local, flags=_native.OPT_NO_CONSERVATION | _native.OPT_TIMING), cs,
-                          _native.Result()))
+                          _native.Result(), ctypes.c_void_p(ltr.kind.data_ptr()),
+                          ctypes.c_void_p(ltr.payload.data_ptr()), ltr))
 
         def lane_step(i):
-            ctx, cs, r = lanes[i]
+            ctx, cs, r, kptr, pptr, _ = lanes[i]
             lib, sptr = ctx.lib, ctypes.c_void_p(cs.cuda_stream)
             ctx.check(lib.aiwc_reset(ctx.h))
             ctx.check(lib.aiwc_ingest(ctx.h, kptr, pptr, ctypes.byref(info), sptr))
@@ -440,31 +463,33 @@ def run_ours(args) -> None:
     traffic, traffic_src = ncu_traffic(cfg) if not sharded else (None, None)
 
     cpu = None
-    if rank == 0 and not sharded and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, w, args)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, total_wi, args)
     if rank == 0:
+        agg = ALG_BYTES_PER_EVENT * n_total / (ms_step / 1e3) / 1e9
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies", "data": "synthetic",
-            "config": {"workload": f"C{cfg} {synth.NAMES[cfg]}: {total_wi} work-items ({n_total} events), "
-                                   f"local {synth.LOCAL[cfg]}, {world} work-group shard(s)",
-                       "events_per_rank": count, "l2": "trace (9 B/event) larger than L2; no flush needed",
-                       "streams": n_streams,
-                       "parallelism": f"replica (N=1), {n_streams} concurrent trace streams" if not sharded else
-                                      f"work-group shards x{world}; NCCL all-reduce + address all-to-all"},
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "u8+u64 events, fp64 entropies",
+            "data": "synthetic", "config": config,
+            "lanes": {"events_per_rank": count, "streams": n_streams,
+                      "how": f"{n_streams} concurrent trace streams (engine ctx + CUDA stream + own copy of the "
+                             "trace each)" if not sharded else "one engine per rank; NCCL collectives"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
-                    "d2h_bytes_per_step": lanes[0][2].d2h_bytes if not sharded else backend.last_d2h, "ms_per_step": e2e_ms,
+                    "d2h_bytes_per_step": lanes[0][2].d2h_bytes if not sharded else backend.last_d2h,
+                    "ms_per_step": e2e_ms,
                     "h2d_gbs": 9 * count / (e2e_ms / 1e3) / 1e9, "bare_h2d_gbs": h2d_peak,
                     "link_frac": (9 * count / (e2e_ms / 1e3) / 1e9) / h2d_peak,
                     "path": "consume(ColumnarTrace on pinned host)+finalize" if not sharded else
                             "dist.sharded_report(CudaBackend, pinned host shard)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read+write)",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_unit": "bytes per launch (ncu dram read+write)",
                          "traffic_source": traffic_src, "alg_bytes": ALG_BYTES_PER_EVENT * count,
                          "kernel": "aiwc::ingest_kernel",
                          "peak_source": peak_src, "alg_bytes_per_event": ALG_BYTES_PER_EVENT,
-                         "step_alg_gbs": step_alg, "step_frac": step_alg / peak},
+                         "step_alg_gbs": step_alg, "step_frac": step_alg / peak,
+                         "aggregate_frac": agg / (world * peak)},
             "phases_ms": phase_med,
             "validate_ms": validate_ms,
             "gpu_launches": kernels[0],
@@ -490,27 +515,43 @@ def ncu_traffic(cfg: int):
         return None, None
 
 
-def cpu_baseline(cfg, w, args):
+def cpu_baseline(cfg, total_wi, args):
     """Oracle (C restatement of the reference path) on all host threads, on a
-    bounded prefix of the same trace, rank 0 only."""
-    import numpy as np
-
-    from oracle import oracle
+    bounded prefix of the same trace, rank 0 only (input from the numpy generator)."""
+    from oracle import oracle, synth_np
 
     try:
         oracle.build()
         threads = host_threads()
-        sample_wi, tr = reference_sample(cfg, w, args, threads)
-        kind, payload = tr.kind, tr.payload.view(np.uint64)
-        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes), threads=threads)
+        sample_wi, kind, payload = reference_sample(cfg, total_wi, args, threads)
+        run = lambda: oracle.run(kind, payload, kernel=synth_np.NAMES[cfg], invocation=0,  # noqa: E731
+                                 n_opcodes=len(synth_np.OPCODES[cfg]), threads=threads)
+        run()
         t0 = time.perf_counter()
-        oracle.run(kind, payload, kernel=tr.kernel_name, invocation=0, n_opcodes=len(tr.opcodes), threads=threads)
+        run()
         dt = time.perf_counter() - t0
         return {"value": kind.shape[0] / dt, "unit": UNIT, "cores": threads, "kind": "port",
-                "sample": f"first {sample_wi} work-items of C{cfg} ({kind.shape[0]} events), "
-                          f"oracle/aiwc_oracle_mt.c on {threads} threads"}
+                "sample": f"{'whole trace' if sample_wi == total_wi else f'first {sample_wi} work-items'} of C{cfg} "
+                          f"({kind.shape[0]} events), oracle/aiwc_oracle_mt.c on {threads} threads"}
     except Exception as exc:  # pragma: no cover
         return {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+
+def spawn_ranks(n: int) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with
+    one rank per GPU (127.0.0.1 rendezvous); NCCL prints its communicator lines."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execve(sys.executable, cmd, env)
 
 
 def main():
@@ -523,12 +564,15 @@ def main():
     ap.add_argument("--work-items", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sample-wi", type=int, default=1 << 21)
-    ap.add_argument("--ref-python-gen", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every rank a full-size shard (N-times larger trace); strong = one fixed trace")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=3,
                     help="N=1: engine contexts / CUDA streams with whole steps in flight concurrently")
     ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

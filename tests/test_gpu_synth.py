@@ -32,6 +32,18 @@ def test_device_generator_matches_python_twin(cfg):
     assert synth.n_events(cfg, w) == ref.n_events
 
 
+@pytest.mark.parametrize("cfg", [2, 3, 4, 5])
+def test_numpy_generator_matches_device_generator(cfg):
+    """oracle/synth_np.py (the reference arm's input) against the device generator."""
+    from oracle import synth_np
+
+    w = 1 << 14
+    dev = synth.device_trace(cfg, w)
+    kind, payload = synth_np.trace(cfg, w)
+    assert np.array_equal(dev.kind.cpu().numpy(), kind)
+    assert np.array_equal(dev.payload.cpu().numpy().view(np.uint64), payload)
+
+
 @pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
 def test_small_configs_match_oracle(cfg):
     tr = synth.device_trace(cfg, SMALL[cfg])
