@@ -328,7 +328,7 @@ static int encode_maps_uncached(aiwc_ctx* ctx, const uint8_t* kind, const uint64
   auto enc = get_encode();
   if (!enc) return fail(ctx, AIWC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {16, rows};
-  cuuint32_t box[2] = {16, (cuuint32_t)(TILE / 16)};
+  cuuint32_t box[2] = {16, (cuuint32_t)(WARP_TILE / 16)};  // one ingest warp tile per TMA box
   cuuint32_t estr[2] = {1, 1};
   cuuint64_t kstr[1] = {16};
   CUresult r = enc(km, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(kind), dims, kstr, box, estr,
@@ -583,8 +583,8 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   ctx->n_ranges = G;
   ctx->tiles_per_cta = tpc;
   const uint32_t pres_blocks = (tpc + PRES_TILES - 1) / PRES_TILES;
-  CK(grow(ctx->wpres, (size_t)G * pres_blocks * 4));
-  CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * pres_blocks * 4, s));
+  CK(grow(ctx->wpres, (size_t)G * P1_SUB * pres_blocks * 4));
+  CK(cudaMemsetAsync(ctx->wpres.p, 0, (size_t)G * P1_SUB * pres_blocks * 4, s));
 
   // ---- main ingest pass ----
   if (n) {
@@ -621,7 +621,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     ctx->mark(AIWC_PH_INGEST, 1, s);
     ctx->kernels += 1;
     if (ctx->n_instr) {  // first index of each width 1..16 (the columns are only ours until here)
-      launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G, pres_blocks, tpc, false,
+      launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G * P1_SUB, pres_blocks, tpc, WARP_TILE,
                          P<unsigned long long>(ctx->wfirst), s);
       ctx->kernels += 1;
     }

@@ -229,26 +229,28 @@ void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint
 // ---------------------------------------------------------------------------
 // main ingest pass
 // ---------------------------------------------------------------------------
-constexpr int BND_CAP = 256;  // segment closes buffered per tile (overflow is processed inline)
-constexpr uint32_t ACC_FLUSH_TILES = (65535 / EPT / PRES_TILES) * PRES_TILES;  // 16-bit fields take <= EPT per tile
 constexpr int NWARP = TPB / 32;
+constexpr int WT = 32 * EPT;       // events per warp tile (one 16-event row per lane)
+constexpr int WROWS = WT / 16;     // TMA box rows per warp tile
+constexpr int WCL_CAP = 64;        // segment closes buffered per warp tile (overflow is processed inline)
+constexpr uint32_t ACC_FLUSH_TILES = (65535 / EPT / PRES_TILES) * PRES_TILES;  // 16-bit fields take <= EPT per tile
+static_assert(TILE == NWARP * WT && P1_SUB == NWARP && WT == WARP_TILE,
+              "a CTA range is NWARP warp ranges (pass-1 sub-ranges) of the same tile count");
 
-// TMA stages (dynamic smem, 1024 B aligned for the 128 B swizzle)
+// TMA stages per warp (dynamic smem, 1024 B aligned for the 128 B swizzle):
+// payload boxes [NWARP][STAGES][WT] u64, then kind boxes, then the mbarriers
 struct StageSmem {
-  uint64_t pay[STAGES][TILE];  // payload rows, 16 B chunk c of row r stored at chunk c ^ (r & 7)
-  uint8_t kind[STAGES][TILE];
-  uint64_t bar[STAGES];
+  uint64_t pay[NWARP][STAGES][WT];  // 16 B chunk c of box row r stored at chunk c ^ (r & 7)
+  uint8_t kind[NWARP][STAGES][WT];
+  uint64_t bar[NWARP][STAGES];
 };
 
-// CTA-private accumulators and per-tile scratch (static smem: direct addressing)
+// CTA-private accumulators and per-warp scratch (static smem: direct addressing)
 struct LocalSmem {
-  uint16_t midx[NWARP][TILE / NWARP];  // per-warp memory-event list: tile position | write << 15
+  uint16_t midx[NWARP][WT];       // per-warp memory-event list: tile position | write << 15
   uint32_t itb_h[HBINS];
   uint32_t ipt_h[HBINS];
-  uint4 closes[BND_CAP];       // (segment length, local id, gseq | barrier << 31 | resumed << 30)
-  uint4 wtot[NWARP];           // per-warp inclusive totals of the packed scan values
-  uint32_t vpos[TPB];
-  uint32_t nc[5];
+  uint4 closes[NWARP][WCL_CAP];   // (segment length, local id, gseq | barrier << 31 | resumed << 30)
 };
 
 // 8x8 bit-matrix transpose: input byte i = event i (bit c = kind bit c);
@@ -276,6 +278,12 @@ __device__ __forceinline__ uint32_t nibble_planes(uint32_t b0, uint32_t b1, uint
   t = (y ^ (y >> 7)) & 0x00AA00AAu; y ^= t ^ (t << 7);
   p23 = __byte_perm(x, y, 0x7362);
   return __byte_perm(x, y, 0x5140);
+}
+
+// bit 4 of each byte of x (events 4q..4q+3) as a 4-bit mask: the multiply moves
+// bits 0, 8, 16, 24 to 21, 22, 23, 24 with no two partial products overlapping
+__device__ __forceinline__ uint32_t bit4_nibble(uint32_t x) {
+  return (((x >> 4) & 0x01010101u) * 0x00204081u >> 21) & 0xFu;
 }
 
 // Bin counts of 16 events from the 4 bit-planes of their values: bin v gets
@@ -329,14 +337,14 @@ __device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint
 }
 
 // add the per-thread packed bin counters (16-bit fields, bin 2i low / 2i + 1 high)
-// to the global opcode / width counters; warp-converged
+// to the global opcode / width counters; warp-converged.  Opcode bin v = opcode v,
+// width bin v = width v + 1.
 __device__ __forceinline__ void flush_counts(uint32_t (&oacc)[8], uint32_t (&wacc)[8], const IngestArgs& a, int lane,
                                              unsigned long long& flags) {
 #pragma unroll
   for (int v = 0; v < 16; ++v) {
     uint32_t co = (oacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
     uint32_t cw = (wacc[v >> 1] >> (16 * (v & 1))) & 0xFFFFu;
-    const uint32_t wv = v ? (uint32_t)v : 16u;  // width bin v holds width v, bin 0 width 16
     co = warp_sum(co);
     cw = warp_sum(cw);
     if (lane == 0) {
@@ -344,7 +352,7 @@ __device__ __forceinline__ void flush_counts(uint32_t (&oacc)[8], uint32_t (&wac
         atomicAdd(&a.opc_counts[v], (unsigned long long)co);
         if ((uint32_t)v >= a.n_opcodes) flags |= F_BAD_OPCODE;
       }
-      if (cw) atomicAdd(&a.width_count[wv], (unsigned long long)cw);
+      if (cw) atomicAdd(&a.width_count[v + 1], (unsigned long long)cw);
     }
   }
 #pragma unroll
@@ -355,6 +363,11 @@ __device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
   return pay[pos ^ (((pos >> 4) & 7u) << 1)];  // 128 B swizzle: chunk (j >> 1) ^ (row & 7)
 }
 
+// The ingest: every warp owns one contiguous warp range of the trace (pass 1's
+// sub-range c * P1_SUB + warp) and walks it in 512-event warp tiles through its
+// own 2-stage TMA ring -- no CTA barrier inside the loop.  Each lane holds one
+// 16-event row of the tile; a warp scan of packed class counts gives every lane
+// its exact carry-in; lane 31's end state is the next tile's carry-in.
 template <bool DENSE, bool STAGE>
 __global__ void __launch_bounds__(TPB, 2)
     ingest_kernel(const IngestArgs a, const __grid_constant__ CUtensorMap kmap,
@@ -369,37 +382,37 @@ __global__ void __launch_bounds__(TPB, 2)
   // small dense tables: per-CTA read / write counters after the TMA stages
   uint32_t* const stab = reinterpret_cast<uint32_t*>(smem_raw + pad + sizeof(StageSmem));
   const uint64_t n = a.n;
-  const uint64_t n_tiles_total = (n + TILE - 1) / TILE;
-  const uint64_t tile_begin = (uint64_t)blockIdx.x * a.tiles_per_cta;
-  if (tile_begin >= n_tiles_total) return;
-  const uint32_t my_tiles = (uint32_t)min((uint64_t)a.tiles_per_cta, n_tiles_total - tile_begin);
-  auto tile_of = [&](uint32_t it) -> uint64_t { return tile_begin + it; };
+  const uint64_t n_wtiles = (n + WT - 1) / WT;
+  const uint32_t gw = blockIdx.x * NWARP + warp;  // == pass 1 sub-range index
+  const uint64_t wt_begin = (uint64_t)gw * a.tiles_per_cta;
+  const uint32_t my_tiles = wt_begin < n_wtiles ? (uint32_t)min((uint64_t)a.tiles_per_cta, n_wtiles - wt_begin) : 0u;
   DevState* st = a.st;
+  uint64_t* const bars = S.bar[warp];
 
-  // ---- prologue: smem init + TMA ring fill ----
+  // ---- prologue: smem init + this warp's TMA ring fill ----
   for (int i = t; i < HBINS; i += TPB) { L.itb_h[i] = 0; L.ipt_h[i] = 0; }
   for (uint32_t i = t; i < 2 * a.smem_keys; i += TPB) stab[i] = 0;
   // shared-memory window of the dense table: [hot_lo, hot_lo + hot_n)
   const uint64_t hot_lo = a.hot_dev ? *a.hot_dev : a.hot_lo;
   const uint32_t hot_n = hot_lo == ~0ull ? 0u : a.smem_keys;
-  if (t == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&S.bar[s], 1);
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
     for (uint32_t it = 0; it < (uint32_t)STAGES && it < my_tiles; ++it) {
-      const uint64_t row0 = tile_of(it) * (TILE / 16);
+      const uint64_t row0 = (wt_begin + it) * WROWS;
       if (row0 < a.tma_rows) {
-        mbar_expect_tx(&S.bar[it], TILE * 9);
-        tma_load_2d(S.kind[it], &kmap, 0, (int)row0, &S.bar[it]);
-        tma_load_2d(S.pay[it], &pmap, 0, (int)row0, &S.bar[it]);
+        mbar_expect_tx(&bars[it], WT * 9);
+        tma_load_2d(S.kind[warp][it], &kmap, 0, (int)row0, &bars[it]);
+        tma_load_2d(S.pay[warp][it], &pmap, 0, (int)row0, &bars[it]);
       }
     }
   }
 
-  // ---- carry-in at the start of this CTA's range: combine the sub-ranges before it ----
+  // ---- carry-in at the start of this warp's range: combine the sub-ranges before it ----
   uint32_t cseg = 0, clid = 0, cbyres = 0, cgseq = 0, cgkey = 0;
   unsigned long long c_rd = 0, c_wr = 0, c_br = 0;
   {
-    const uint32_t c = blockIdx.x * P1_SUB;
+    const uint32_t c = blockIdx.x * P1_SUB;  // CTA-wide part: sub-ranges [0, c)
     long long jb = -1, lw = -1;
     uint64_t s_rd = 0, s_wr = 0, s_br = 0, s_wgb = 0;
     for (uint32_t j = t; j < c; j += TPB) {
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(TPB, 2)
       lw = max(lw, (long long)r.last_wgb);
       s_rd += r.n_rd; s_wr += r.n_wr; s_br += r.n_br; s_wgb += r.n_wgb;
     }
-    __shared__ unsigned long long red[TPB / 32][6];
+    __shared__ unsigned long long red[NWARP][6];
     s_rd = warp_sum(s_rd); s_wr = warp_sum(s_wr); s_br = warp_sum(s_br); s_wgb = warp_sum(s_wgb);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -421,7 +434,7 @@ __global__ void __launch_bounds__(TPB, 2)
     }
     __syncthreads();
     jb = -1; lw = -1; s_rd = s_wr = s_br = s_wgb = 0;
-    for (int w = 0; w < TPB / 32; ++w) {
+    for (int w = 0; w < NWARP; ++w) {
       s_rd += red[w][0]; s_wr += red[w][1]; s_br += red[w][2]; s_wgb += red[w][3];
       jb = max(jb, (long long)red[w][4]); lw = max(lw, (long long)red[w][5]);
     }
@@ -432,10 +445,21 @@ __global__ void __launch_bounds__(TPB, 2)
     if (lane == 0) red[warp][0] = s_in;
     __syncthreads();
     uint64_t after = 0;
-    for (int w = 0; w < TPB / 32; ++w) after += red[w][0];
+    for (int w = 0; w < NWARP; ++w) after += red[w][0];
+    long long lbpos = -1;
     if (jb >= 0) {
-      const long long lbpos = a.ranges[jb].last_bnd;
+      lbpos = a.ranges[jb].last_bnd;
       after += a.ranges[jb].instr_after;
+    }
+    // warp part: this CTA's sub-ranges before mine, in order
+    for (uint32_t j = c; j < c + (uint32_t)warp; ++j) {
+      const RangeSum& r = a.ranges[j];
+      if (r.last_bnd >= 0) { lbpos = r.last_bnd; after = r.instr_after; }
+      else after += r.n_instr;
+      if (r.last_wgb >= 0) lw = r.last_wgb;
+      s_rd += r.n_rd; s_wr += r.n_wr; s_br += r.n_br; s_wgb += r.n_wgb;
+    }
+    if (lbpos >= 0) {
       clid = (uint32_t)a.payload[lbpos];
       cbyres = a.kind[lbpos] == AIWC_K_WI_RESUME;
     }
@@ -447,47 +471,53 @@ __global__ void __launch_bounds__(TPB, 2)
   __syncthreads();
 
   uint32_t oacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // opcode bins 0..15, two 16-bit fields each
-  uint32_t wacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width bins (bin v = width v, bin 0 = 16)
+  uint32_t wacc[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width bins (bin v = width v + 1)
   uint32_t pres = 0;                                     // slow-path widths 1..16 seen in this presence block
   uint32_t wsnap[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // width counters at the block start
-  // widths 1..16 that occurred in presence block `blk` (PRES_TILES tile iterations) of this CTA
+  // widths 1..16 that occurred in presence block `blk` (PRES_TILES warp tiles) of this warp range
   auto record_presence = [&](uint32_t blk) {
     uint32_t bits = pres;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t d = wacc[i] ^ wsnap[i];
-      if (d & 0xFFFFu) bits |= 1u << ((2 * i ? 2 * i : 16) - 1);
-      if (d >> 16) bits |= 1u << (2 * i + 1 - 1);
+      if (d & 0xFFFFu) bits |= 1u << (2 * i);
+      if (d >> 16) bits |= 1u << (2 * i + 1);
       wsnap[i] = wacc[i];
     }
     bits = __reduce_or_sync(0xffffffffu, bits);
-    if (lane == 0 && bits) atomicOr(&a.width_presence[(uint64_t)blockIdx.x * a.pres_blocks + blk], bits);
+    if (lane == 0 && bits) a.width_presence[(uint64_t)gw * a.pres_blocks + blk] = bits;
     pres = 0;
   };
   unsigned long long itb_sum = 0, ipt_sum = 0, flags = 0, max_site = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   uint32_t n_wib = 0, n_bar = 0;  // WI_BEGIN / BARRIER events (metrics.py: work_items, barriers_hit)
+  const uint32_t sw = lane & 7, sw2 = sw << 1;
+  uint16_t* const midx = L.midx[warp];
+  uint4* const wclose = L.closes[warp];
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
-    const uint64_t tile_idx = tile_of(it);
-    const uint64_t tile0 = tile_idx * TILE;
-    const uint64_t row0 = tile0 / 16;
-    if (row0 < a.tma_rows) mbar_wait(&S.bar[s], (it / STAGES) & 1);
-    const uint64_t e0 = tile0 + 16ull * t;
+    const uint64_t wt = wt_begin + it;
+    const uint64_t tile0 = wt * WT;
+    const uint64_t row0 = wt * WROWS;
+    const uint64_t* const P = S.pay[warp][s];
+    uint8_t* const K = S.kind[warp][s];
+    if (row0 < a.tma_rows) mbar_wait(&bars[s], (it / STAGES) & 1);
+    const uint64_t e0 = tile0 + 16ull * lane;
     uint32_t w[4];
-    if (row0 + t < a.tma_rows) {
-      const uint4 v = *reinterpret_cast<const uint4*>(&S.kind[s][16 * t]);
+    if (row0 + lane < a.tma_rows) {
+      const uint4 v = *reinterpret_cast<const uint4*>(&K[16 * lane]);
       w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
     } else {
       // rows beyond the tensor maps (tail of the trace): direct loads, patch smem
       load_kind16(a.kind, e0, n, w);
-      *reinterpret_cast<uint4*>(&S.kind[s][16 * t]) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(&K[16 * lane]) = make_uint4(w[0], w[1], w[2], w[3]);
       for (int j = 0; j < 16; ++j) {
         const uint64_t e = e0 + j;
-        S.pay[s][t * 16 + ((((j >> 1) ^ (t & 7))) << 1) + (j & 1)] = e < n ? a.payload[e] : 0ull;
+        S.pay[warp][s][lane * 16 + ((((j >> 1) ^ sw)) << 1) + (j & 1)] = e < n ? a.payload[e] : 0ull;
       }
     }
+    if (row0 + WROWS > a.tma_rows) __syncwarp();  // patched rows are read by other lanes
     // ---- kind bit-planes of my 16 events: plane c bit j = bit c of kind byte j ----
     uint32_t ins16, rd16, wr16, br16, bnd16, p5, p6, p7;
     {
@@ -515,70 +545,56 @@ __global__ void __launch_bounds__(TPB, 2)
     const int lw = wgb16 ? 31 - __clz(wgb16) : -1;
     const uint32_t n_in = __popc(ins16);
     const uint32_t after = __popc(ins16 >> (lp + 1));
-    // ---- block scan of (instr | branch<<16), (read | write<<16), (wgb | close<<16), (lastpos | lastwgb<<16) ----
-    const uint32_t A = n_in | (__popc(br16) << 16), B = __popc(rd16) | (__popc(wr16) << 16);
-    const uint32_t C = __popc(wgb16) | (__popc(close16) << 16);
-    const uint32_t PQ = (lp >= 0 ? (uint32_t)(16 * t + lp + 1) : 0u) | ((lw >= 0 ? (uint32_t)(16 * t + lw + 1) : 0u) << 16);
-    uint32_t Ai = A, Bi = B, Ci = C, Mi = PQ;
+    // ---- warp scan of 10-bit fields (counts <= 512):
+    //      X = instr | branch << 10 | read << 20, Y = write | wgb << 10 | close << 20,
+    //      M = last boundary pos + 1 | last wg_begin pos + 1 << 16 (max) ----
+    const uint32_t n_rd = __popc(rd16), n_wr = __popc(wr16);
+    const uint32_t X = n_in | (__popc(br16) << 10) | (n_rd << 20);
+    const uint32_t Y = n_wr | (__popc(wgb16) << 10) | (__popc(close16) << 20);
+    const uint32_t PQ = (lp >= 0 ? (uint32_t)(16 * lane + lp + 1) : 0u) |
+                        ((lw >= 0 ? (uint32_t)(16 * lane + lw + 1) : 0u) << 16);
+    uint32_t Xi = X, Yi = Y, Mi = PQ;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t ua = __shfl_up_sync(0xffffffffu, Ai, o), ub = __shfl_up_sync(0xffffffffu, Bi, o);
-      const uint32_t uc = __shfl_up_sync(0xffffffffu, Ci, o), um = __shfl_up_sync(0xffffffffu, Mi, o);
-      if (lane >= o) { Ai += ua; Bi += ub; Ci += uc; Mi = __vmaxu2(Mi, um); }
+      const uint32_t ux = __shfl_up_sync(0xffffffffu, Xi, o), uy = __shfl_up_sync(0xffffffffu, Yi, o);
+      const uint32_t um = __shfl_up_sync(0xffffffffu, Mi, o);
+      if (lane >= o) { Xi += ux; Yi += uy; Mi = __vmaxu2(Mi, um); }
     }
-    if (lane == 31) L.wtot[warp] = make_uint4(Ai, Bi, Ci, Mi);
-    __syncthreads();
-    // exclusive prefix over earlier warps: lane q < 8 holds warp q's totals
-    uint4 wq = lane < TPB / 32 ? L.wtot[lane] : make_uint4(0u, 0u, 0u, 0u);
-    uint32_t pa = wq.x, pb = wq.y, pc = wq.z, pm = wq.w;
-    uint32_t TA = 0, TB = 0, TC = 0;
-#pragma unroll
-    for (int o = 1; o < TPB / 32; o <<= 1) {
-      const uint32_t ua = __shfl_up_sync(0xffffffffu, pa, o), ub = __shfl_up_sync(0xffffffffu, pb, o);
-      const uint32_t uc = __shfl_up_sync(0xffffffffu, pc, o), um = __shfl_up_sync(0xffffffffu, pm, o);
-      if (lane >= o) { pa += ua; pb += ub; pc += uc; pm = __vmaxu2(pm, um); }
-    }
-    TA = __shfl_sync(0xffffffffu, pa, TPB / 32 - 1);
-    TB = __shfl_sync(0xffffffffu, pb, TPB / 32 - 1);
-    TC = __shfl_sync(0xffffffffu, pc, TPB / 32 - 1);
-    const int src = warp > 0 ? warp - 1 : 0;
-    const uint32_t Ap = warp ? __shfl_sync(0xffffffffu, pa, src) : 0u;
-    const uint32_t Bp = warp ? __shfl_sync(0xffffffffu, pb, src) : 0u;
-    const uint32_t Cp = warp ? __shfl_sync(0xffffffffu, pc, src) : 0u;
-    const uint32_t Mp = warp ? __shfl_sync(0xffffffffu, pm, src) : 0u;
-    uint32_t Me = __shfl_up_sync(0xffffffffu, Mi, 1);
-    if (lane == 0) Me = 0;
-    const uint32_t Aex = Ap + Ai - A, Bex = Bp + Bi - B, Cex = Cp + Ci - C;
-    const uint32_t Mex = __vmaxu2(Mp, Me);
+    const uint32_t TX = __shfl_sync(0xffffffffu, Xi, 31), TY = __shfl_sync(0xffffffffu, Yi, 31);
+    uint32_t Mex = __shfl_up_sync(0xffffffffu, Mi, 1);
+    if (lane == 0) Mex = 0;
+    const uint32_t Xex = Xi - X, Yex = Yi - Y;
     const uint32_t Pex = Mex & 0xFFFFu, Qex = Mex >> 16;
-    const uint32_t ex_in = Aex & 0xFFFFu, ex_br = Aex >> 16, ex_rd = Bex & 0xFFFFu, ex_wr = Bex >> 16;
-    const uint32_t T_rd = TB & 0xFFFFu, T_wr = TB >> 16, T_br = TA >> 16, T_cl = TC >> 16;
-    L.vpos[t] = ex_in + n_in - after;  // instructions in the tile at positions <= my last boundary
-    __syncthreads();
-    // ---- carry-in for this thread ----
+    const uint32_t ex_in = Xex & 0x3FFu, ex_br = (Xex >> 10) & 0x3FFu, ex_rd = Xex >> 20;
+    const uint32_t ex_wr = Yex & 0x3FFu, ex_wgb = (Yex >> 10) & 0x3FFu, ex_cl = Yex >> 20;
+    const uint32_t T_br = (TX >> 10) & 0x3FFu, T_rd = TX >> 20, T_wr = TY & 0x3FFu, T_cl = TY >> 20;
+    // instructions in the tile at positions <= my last boundary, fetched from the boundary's lane
+    const uint32_t vpos = ex_in + n_in - after;
+    const uint32_t vsrc = __shfl_sync(0xffffffffu, vpos, Pex ? ((Pex - 1) >> 4) : 0u);
+    // ---- carry-in for this lane ----
     uint32_t seg_in, lid, byres;
     if (Pex) {
       const uint32_t pos = Pex - 1;
-      seg_in = ex_in - L.vpos[pos >> 4];
-      lid = (uint32_t)pay_at(S.pay[s], pos);
-      byres = S.kind[s][pos] == AIWC_K_WI_RESUME;
+      seg_in = ex_in - vsrc;
+      lid = (uint32_t)pay_at(P, pos);
+      byres = K[pos] == AIWC_K_WI_RESUME;
     } else {
       seg_in = cseg + ex_in; lid = clid; byres = cbyres;
     }
-    uint32_t gkey = Qex ? (uint32_t)pay_at(S.pay[s], Qex - 1) : cgkey;
-    uint32_t gseq = cgseq + (Cex & 0xFFFFu);
-    // ordered outputs go straight to their global slots (tile base + exclusive rank)
+    uint32_t gkey = Qex ? (uint32_t)pay_at(P, Qex - 1) : cgkey;
+    uint32_t gseq = cgseq + ex_wgb;
+    // ordered outputs go straight to their global slots (range offset + exclusive rank)
     uint64_t o_rd = c_rd + ex_rd, o_wr = c_wr + ex_wr;
     const uint64_t o_br = c_br + ex_br;
-    uint32_t o_cl = Cex >> 16;
+    uint32_t o_cl = ex_cl;
     // ---- fold my 16 events, one converged loop per event class ----
     // 128 B swizzle: event j of row r sits at u64 index 16 r + (j ^ ((r & 7) << 1))
-    const uint64_t* prow = &S.pay[s][t * 16];
-    const uint32_t sw = t & 7, sw2 = sw << 1;
+    const uint64_t* prow = &P[lane * 16];
 #define PAY(j) prow[(uint32_t)(j) ^ sw2]
     // instructions: opcode / width bins from bit-planes.  The fast bins take
-    // opcode < 16 and width 1..16; the low nibbles of those bytes are
-    // transposed into 4 planes each and bin v counts popc(minterm_v & fast).
+    // opcode < 16 and width 1..16: min(opcode, 16) and min(width - 1, 16) keep
+    // one byte each, bit 4 of those bytes flags the rest, and the low nibbles are
+    // transposed into 4 planes each; bin v counts popc(minterm_v & fast).
     uint32_t bad = 0;  // events outside the fast bins (meaningful for instructions only)
     uint32_t op[4], wp[4];
     {
@@ -587,18 +603,15 @@ __global__ void __launch_bounds__(TPB, 2)
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // chunk c = events 2c, 2c + 1
         const uint4 v = prow4[c ^ sw];
-        if (!(AIWC_ABL & 16)) {
-          if ((v.y | (v.x - 1u)) > 15u) bad |= 1u << (2 * c);
-          if ((v.w | (v.z - 1u)) > 15u) bad |= 2u << (2 * c);
-        }
-        lo2[c] = __byte_perm(v.x, v.z, 0x0040);  // width bytes of events 2c, 2c + 1
-        hi2[c] = __byte_perm(v.y, v.w, 0x0040);  // opcode bytes
+        lo2[c] = __byte_perm(min(v.x - 1u, 16u), min(v.z - 1u, 16u), 0x0040);  // width - 1 of events 2c, 2c + 1
+        hi2[c] = __byte_perm(min(v.y, 16u), min(v.w, 16u), 0x0040);            // opcode
       }
       uint32_t lw4[4], hw4[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         lw4[q] = __byte_perm(lo2[2 * q], lo2[2 * q + 1], 0x5410);
         hw4[q] = __byte_perm(hi2[2 * q], hi2[2 * q + 1], 0x5410);
+        if (!(AIWC_ABL & 16)) bad |= bit4_nibble(lw4[q] | hw4[q]) << (4 * q);
       }
       uint32_t o23, w23;
       const uint32_t o01 = nibble_planes(hw4[0], hw4[1], hw4[2], hw4[3], o23);
@@ -630,18 +643,15 @@ __global__ void __launch_bounds__(TPB, 2)
     if (DENSE && !(AIWC_ABL & 2)) {
       // my accesses go to the warp's list (pre-swizzled smem index | write << 15)
       // at my in-warp exclusive offset ...
-      const uint32_t bx = Bi - B;
-      uint32_t slot = (bx & 0xFFFFu) + (bx >> 16);
-      uint16_t* const midx = L.midx[warp];
-      const uint32_t rowb = 16u * t;
+      uint32_t slot = ex_rd + ex_wr;
+      const uint32_t rowb = 16u * lane;
       for (uint32_t m = rd16 | wr16; m; m &= m - 1) {
         const uint32_t j = __ffs(m) - 1;
         midx[slot++] = (uint16_t)((rowb | (j ^ sw2)) | (((wr16 >> j) & 1u) << 15));
       }
       __syncwarp();
       // ... and lane i folds accesses i, i + 32, ... of the warp in stream order
-      const uint32_t wt = L.wtot[warp].y, n_mem = (wt & 0xFFFFu) + (wt >> 16);
-      const uint64_t* const pay = S.pay[s];
+      const uint32_t n_mem = T_rd + T_wr;
       const uint64_t base = a.am.base, off_max = a.am.off_max;
       const uint32_t k = a.am.k, lmask = (uint32_t)a.am.low_mask, lconst = (uint32_t)a.am.low_const;
       uint32_t inval = 0;
@@ -650,10 +660,10 @@ __global__ void __launch_bounds__(TPB, 2)
         constexpr bool HOT = decltype(with_window)::value;
         if (a.dense32) {
           uint32_t* const tab = static_cast<uint32_t*>(a.dense);
-#pragma unroll 4  // several accesses per lane in flight (C2 ingest -2.5 %, C5 -4 %)
+#pragma unroll 4  // several accesses per lane in flight
           for (uint32_t i = lane; i < n_mem; i += 32) {
             const uint32_t e = midx[i];
-            const uint64_t off = pay[e & 0x0FFFu] - base;
+            const uint64_t off = P[e & 0x0FFFu] - base;
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
             if (v) {
@@ -669,10 +679,10 @@ __global__ void __launch_bounds__(TPB, 2)
           }
         } else {
           unsigned long long* const tab = static_cast<unsigned long long*>(a.dense);
-#pragma unroll 4  // several accesses per lane in flight (C2 ingest -2.5 %, C5 -4 %)
+#pragma unroll 4  // several accesses per lane in flight
           for (uint32_t i = lane; i < n_mem; i += 32) {
             const uint32_t e = midx[i];
-            const uint64_t off = pay[e & 0x0FFFu] - base;
+            const uint64_t off = P[e & 0x0FFFu] - base;
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
             if (v) {
@@ -697,7 +707,7 @@ __global__ void __launch_bounds__(TPB, 2)
       aand &= p; aor |= p;
     }
     // branches: ordered records site << 32 | group << 1 | taken; the group is the last
-    // wg_begin before the branch in my chunk, else my carry-in group
+    // wg_begin before the branch in my row, else my carry-in group
     if (STAGE) {
       for (uint32_t m = br16; m; m &= m - 1) {
         const uint32_t j = __ffs(m) - 1;
@@ -717,47 +727,50 @@ __global__ void __launch_bounds__(TPB, 2)
     int last_b = -1;  // my last boundary position so far
     for (uint32_t m = (AIWC_ABL & 8) ? 0u : rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
-      const uint32_t k = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
+      const uint32_t kk = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
-      if (k & 0x10) {
-        if (k & 0x20) {  // wi_begin / wi_resume opens a segment
-          lid = (uint32_t)p; byres = k >> 7;
-        } else {         // barrier / wi_end closes it: instructions since the open
+      if (kk & 0x10) {
+        if (kk & 0x20) {  // wi_begin / wi_resume opens a segment
+          lid = (uint32_t)p; byres = kk >> 7;
+        } else {          // barrier / wi_end closes it: instructions since the open
           const uint32_t cl = __popc(ins16 & ((1u << j) - 1u) & (0xFFFFFFFFu << (last_b + 1))) +
                               (last_b < 0 ? seg_in : 0u);
-          const uint32_t gz = (gseq & 0x3FFFFFFFu) | ((k & 0x80u) << 24) | (byres << 30);
+          const uint32_t gz = (gseq & 0x3FFFFFFFu) | ((kk & 0x80u) << 24) | (byres << 30);
           if (gseq >> 30) flags |= F_BAD_GROUP;
-          if (o_cl < (uint32_t)BND_CAP) L.closes[o_cl] = make_uint4(cl, lid, gz, 0u);
+          if (o_cl < (uint32_t)WCL_CAP) wclose[o_cl] = make_uint4(cl, lid, gz, 0u);
           else do_close(L, a, cl, lid, gz, itb_sum, ipt_sum, flags);
           ++o_cl;
         }
         last_b = (int)j;
-      } else if (k == AIWC_K_WG_BEGIN) {
+      } else if (kk == AIWC_K_WG_BEGIN) {
         ++gseq; gkey = (uint32_t)p;
-      } else if (k != AIWC_K_WG_END && k != AIWC_K_KERNEL_BEGIN && k != AIWC_K_KERNEL_END) {
+      } else if (kk != AIWC_K_WG_END && kk != AIWC_K_KERNEL_BEGIN && kk != AIWC_K_KERNEL_END) {
         flags |= F_BAD_KIND;
       }
     }
 #undef PAY
-    if (t == TPB - 1) {
-      L.nc[0] = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
-      L.nc[1] = lid; L.nc[2] = byres; L.nc[3] = gseq; L.nc[4] = gkey;
-    }
-    __syncthreads();
-    // ---- segment closes of the tile, all threads converged ----
-    for (uint32_t i = t; i < min(T_cl, (uint32_t)BND_CAP); i += TPB) {
-      const uint4 c = L.closes[i];
+    // ---- the next tile's carry-in: lane 31's end state ----
+    const uint32_t nseg = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
+    cseg = __shfl_sync(0xffffffffu, nseg, 31);
+    clid = __shfl_sync(0xffffffffu, lid, 31);
+    cbyres = __shfl_sync(0xffffffffu, byres, 31);
+    cgseq = __shfl_sync(0xffffffffu, gseq, 31);
+    cgkey = __shfl_sync(0xffffffffu, gkey, 31);
+    c_rd += T_rd; c_wr += T_wr; c_br += T_br;
+    __syncwarp();
+    // ---- segment closes of the tile, the warp's lanes converged ----
+    for (uint32_t i = lane; i < min(T_cl, (uint32_t)WCL_CAP); i += 32) {
+      const uint4 c = wclose[i];
       do_close(L, a, c.x, c.y, c.z, itb_sum, ipt_sum, flags);
     }
-    cseg = L.nc[0]; clid = L.nc[1]; cbyres = L.nc[2]; cgseq = L.nc[3]; cgkey = L.nc[4];
-    c_rd += T_rd; c_wr += T_wr; c_br += T_br;
-    // ---- refill this stage ----
-    if (t == 0 && it + STAGES < my_tiles) {
-      const uint64_t r2 = tile_of(it + STAGES) * (TILE / 16);
+    __syncwarp();
+    // ---- refill this stage (every lane is done with it) ----
+    if (lane == 0 && it + STAGES < my_tiles) {
+      const uint64_t r2 = (wt + STAGES) * WROWS;
       if (r2 < a.tma_rows) {
-        mbar_expect_tx(&S.bar[s], TILE * 9);
-        tma_load_2d(S.kind[s], &kmap, 0, (int)r2, &S.bar[s]);
-        tma_load_2d(S.pay[s], &pmap, 0, (int)r2, &S.bar[s]);
+        mbar_expect_tx(&bars[s], WT * 9);
+        tma_load_2d(S.kind[warp][s], &kmap, 0, (int)r2, &bars[s]);
+        tma_load_2d(S.pay[warp][s], &pmap, 0, (int)r2, &bars[s]);
       }
     }
     if ((it + 1) % PRES_TILES == 0) record_presence(it / PRES_TILES);
@@ -769,8 +782,10 @@ __global__ void __launch_bounds__(TPB, 2)
   }
 
   // ---- epilogue: flush CTA-private state ----
+  if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
+  flush_counts(oacc, wacc, a, lane, flags);
+  __syncthreads();
   if (DENSE && hot_n) {
-    __syncthreads();
     for (uint32_t i = t; i < hot_n; i += TPB) {
       const uint32_t r = stab[i], w = stab[hot_n + i];
       if (!(r | w)) continue;
@@ -784,8 +799,6 @@ __global__ void __launch_bounds__(TPB, 2)
       }
     }
   }
-  if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
-  flush_counts(oacc, wacc, a, lane, flags);
   for (int i = t; i < HBINS; i += TPB) {
     if (L.itb_h[i]) atomicAdd(&st->itb_hist[i], (unsigned long long)L.itb_h[i]);
     if (L.ipt_h[i]) atomicAdd(&st->ipt_hist[i], (unsigned long long)L.ipt_h[i]);

@@ -13,7 +13,8 @@ constexpr int TPB = 256;              // threads per ingest CTA
 constexpr int EPT = 16;               // events per thread per tile (one 16 B kind row)
 constexpr int TILE = TPB * EPT;       // 4096 events per tile
 constexpr int STAGES = 2;             // TMA ring depth (two CTAs per SM -> four tiles in flight)
-constexpr int P1_SUB = 8;             // pass-1 sub-ranges per ingest range
+constexpr int P1_SUB = 8;             // pass-1 sub-ranges per ingest range (= warp ranges per ingest CTA)
+constexpr int WARP_TILE = 32 * EPT;   // events per ingest warp tile (512)
 constexpr int CTAS_PER_SM = 2;        // ingest CTAs per SM (non-staging variant)
 constexpr int OBINS = 16;             // lane-private opcode bins (ids 0..15)
 constexpr int WBINS = 16;             // lane-private width bins (widths 1..16)
@@ -102,7 +103,7 @@ struct IngestArgs {
   unsigned long long* opc_counts;   // [n_opcodes]
   unsigned long long* width_count;  // [WIDTH_TABLE]
   unsigned long long* width_first;  // [WIDTH_TABLE] (widths > 16; 1..16 found by width_first_kernel)
-  uint32_t* width_presence;         // [n_ctas * pres_blocks]: widths 1..16 present (bit w - 1)
+  uint32_t* width_presence;         // [n_ctas * P1_SUB * pres_blocks]: widths 1..16 present per warp range (bit w - 1)
   uint32_t* itb_ovf;                // [n_bar + n_wie]
   uint32_t* ipt_ovf;                // [n_wie]
   unsigned long long* ipt_tab;      // [n_wgb * local_volume] or null
@@ -232,7 +233,7 @@ void launch_hot_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n,
                        unsigned long long* hot_out, cudaStream_t s);
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
-                        uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
+                        uint32_t n_ranges, uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
                         unsigned long long* width_first, cudaStream_t s);
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);

@@ -270,53 +270,37 @@ void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st,
 // width Counter in first-appearance order (metrics.py:136, :298-306)
 // ---------------------------------------------------------------------------
 // First event index of each width 1..16 counted by the ingest's bit-plane
-// bins.  The ingest records, per CTA and per block of PRES_TILES tile
-// iterations, which widths occurred; CTA w - 1 finds the earliest block holding
-// width w in stream order and scans its tiles in order up to the first hit.
-// Two layouts: contiguous ranges per CTA (two-pass ingest: blocks in (CTA,
-// block) order) or tiles dealt round-robin (one-pass ingest: block b of every
-// CTA together covers tiles [b * PRES_TILES * G, (b + 1) * PRES_TILES * G)).
+// bins.  The ingest records, per warp range and per block of PRES_TILES warp
+// tiles (`wt` events each), which widths occurred; CTA w - 1 finds the earliest
+// block holding width w in stream order (ranges are contiguous and in order, so
+// (range, block) order is stream order) and scans its events in order up to the
+// first hit.
 __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restrict__ kind,
                                                           const uint64_t* __restrict__ payload, uint64_t n,
-                                                          const uint32_t* __restrict__ presence, uint32_t G,
-                                                          uint32_t pres_blocks, uint32_t tpc, int interleaved,
+                                                          const uint32_t* __restrict__ presence, uint32_t n_ranges,
+                                                          uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
                                                           unsigned long long* width_first) {
   const uint32_t w = blockIdx.x + 1, bit = 1u << (w - 1);
   __shared__ unsigned long long s_unit, s_pos;
   if (threadIdx.x == 0) { s_unit = ~0ull; s_pos = ~0ull; }
   __syncthreads();
-  // earliest unit (stream order) whose presence mask holds w
-  for (uint64_t u = threadIdx.x; u < (uint64_t)G * pres_blocks; u += blockDim.x) {
-    if (!(presence[u] & bit)) continue;
-    const uint64_t c = u / pres_blocks, b = u % pres_blocks;
-    atomicMin(&s_unit, interleaved ? b * G + c : c * pres_blocks + b);
-  }
+  for (uint64_t u = threadIdx.x; u < (uint64_t)n_ranges * pres_blocks; u += blockDim.x)
+    if (presence[u] & bit) atomicMin(&s_unit, u);
   __syncthreads();
   if (s_unit == ~0ull) return;
-  const uint64_t n_tiles = (n + TILE - 1) / TILE;
-  // the candidate tiles, in stream order
-  uint64_t t_lo, t_hi;
-  if (interleaved) {
-    const uint64_t b = s_unit / G;
-    t_lo = b * PRES_TILES * G; t_hi = min(n_tiles, t_lo + (uint64_t)PRES_TILES * G);
-  } else {
-    const uint64_t c = s_unit / pres_blocks, b = s_unit % pres_blocks;
-    t_lo = c * tpc + b * PRES_TILES; t_hi = min(n_tiles, min(t_lo + PRES_TILES, (c + 1) * tpc));
-  }
-  for (uint64_t tile = t_lo; tile < t_hi; ++tile) {
-    if (interleaved) {  // skip tiles of CTAs whose block lacks the width
-      const uint64_t c = tile % G, b = tile / G / PRES_TILES;
-      if (!(presence[c * pres_blocks + b] & bit)) continue;
-    }
-    const uint64_t base = tile * TILE;
-    // all 32 loads of the tile in flight at once (one memory round trip)
+  const uint64_t r = s_unit / pres_blocks, b = s_unit % pres_blocks;
+  const uint64_t r_end = min(n, (r + 1) * tiles_per_range * (uint64_t)wt);
+  const uint64_t lo = r * tiles_per_range * (uint64_t)wt + b * PRES_TILES * (uint64_t)wt;
+  const uint64_t hi = min(r_end, lo + (uint64_t)PRES_TILES * wt);
+  for (uint64_t base = lo; base < hi; base += 16 * 256) {
+    // all 32 loads of the chunk in flight at once (one memory round trip)
     uint8_t k[16];
     uint32_t p[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const uint64_t e = base + (uint64_t)j * 256 + threadIdx.x;
-      k[j] = e < n ? kind[e] : 0;
-      p[j] = e < n ? (uint32_t)payload[e] : 0u;
+      k[j] = e < hi ? kind[e] : 0;
+      p[j] = e < hi ? (uint32_t)payload[e] : 0u;
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -332,10 +316,10 @@ __global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restr
 }
 
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
-                        uint32_t n_ctas, uint32_t pres_blocks, uint32_t tiles_per_cta, bool interleaved,
+                        uint32_t n_ranges, uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
                         unsigned long long* width_first, cudaStream_t s) {
-  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ctas, pres_blocks, tiles_per_cta,
-                                           interleaved ? 1 : 0, width_first);
+  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ranges, pres_blocks, tiles_per_range, wt,
+                                           width_first);
 }
 
 __global__ void width_list_kernel(const unsigned long long* __restrict__ count,
