@@ -444,8 +444,8 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     const uint64_t b0 = info->addr_min & ~1023ull, vary = info->addr_and ^ info->addr_or;
     const uint32_t k0 = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
     const uint64_t sk = (info->addr_max - b0) >> k0;
-    if (sk < (1ull << 40) && (sk + 1) * 4 <= ctx->opts.dense_budget_bytes && sk + 1 <= 4 * n + (1ull << 20)) {
-      const size_t tb = (size_t)(sk + 1) * 4;
+    if (sk + 1 < DENSE_MAX_KEYS && (sk + 2) * 4 <= ctx->opts.dense_budget_bytes && sk + 1 <= 4 * n + (1ull << 20)) {
+      const size_t tb = (size_t)(sk + 2) * 4;  // + the sentinel slot of invalid addresses
       if (ctx->dtab_clean >= tb && ctx->dtab.cap >= tb) {
         ctx->pre_zeroed = ctx->dtab_clean;  // cleared after the previous trace (join_ev)
       } else {
@@ -526,7 +526,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
       ctx->dense32 = M < E32_MAX_ACCESSES && (M <= am.n_keys || (hot_window && M <= 4 * am.n_keys));
       if (ctx->dense_entry == 32) ctx->dense32 = M < E32_MAX_ACCESSES && am.n_keys > SMEM_TABLE_KEYS;
       if (ctx->dense_entry == 64) ctx->dense32 = false;
-      const bool fits = span_keys < (1ull << 40) && am.n_keys * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
+      const bool fits = span_keys < DENSE_MAX_KEYS - 1 && (am.n_keys + 1) * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
                         am.n_keys <= 4 * M + (1ull << 20);
       // a shard keeps its addresses compacted: they are exchanged with the key owners
       ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
@@ -563,7 +563,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   CK(grow(ctx->br, std::max<uint64_t>(ctx->n_br, 1) * 8));
   if (M) {
     if (ctx->dense) {
-      const size_t tb = ctx->am.n_keys * (ctx->dense32 ? 4 : 8);
+      const size_t tb = (ctx->am.n_keys + 1) * (ctx->dense32 ? 4 : 8);  // + the sentinel slot
       size_t zeroed = ctx->pre_zeroed;
       if (!zeroed && clean_prev >= tb && ctx->dtab.cap >= tb) zeroed = clean_prev;  // cleared on aux (join_ev)
       if (zeroed) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));

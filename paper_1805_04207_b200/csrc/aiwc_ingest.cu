@@ -492,7 +492,6 @@ __global__ void __launch_bounds__(TPB, 2)
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   uint32_t n_wib = 0, n_bar = 0;  // WI_BEGIN / BARRIER events (metrics.py: work_items, barriers_hit)
   const uint32_t sw = lane & 7, sw2 = sw << 1;
-  uint16_t* const midx = L.midx[warp];
   uint4* const wclose = L.closes[warp];
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
@@ -546,31 +545,31 @@ __global__ void __launch_bounds__(TPB, 2)
     const uint32_t n_in = __popc(ins16);
     const uint32_t after = __popc(ins16 >> (lp + 1));
     // ---- warp scan of 10-bit fields (counts <= 512):
-    //      X = instr | branch << 10 | read << 20, Y = write | wgb << 10 | close << 20,
-    //      M = last boundary pos + 1 | last wg_begin pos + 1 << 16 (max) ----
+    //      X = instr | branch << 10 | read << 20, Y = write | wgb << 10 | close << 20 ----
     const uint32_t n_rd = __popc(rd16), n_wr = __popc(wr16);
     const uint32_t X = n_in | (__popc(br16) << 10) | (n_rd << 20);
     const uint32_t Y = n_wr | (__popc(wgb16) << 10) | (__popc(close16) << 20);
-    const uint32_t PQ = (lp >= 0 ? (uint32_t)(16 * lane + lp + 1) : 0u) |
-                        ((lw >= 0 ? (uint32_t)(16 * lane + lw + 1) : 0u) << 16);
-    uint32_t Xi = X, Yi = Y, Mi = PQ;
+    uint32_t Xi = X, Yi = Y;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t ux = __shfl_up_sync(0xffffffffu, Xi, o), uy = __shfl_up_sync(0xffffffffu, Yi, o);
-      const uint32_t um = __shfl_up_sync(0xffffffffu, Mi, o);
-      if (lane >= o) { Xi += ux; Yi += uy; Mi = __vmaxu2(Mi, um); }
+      if (lane >= o) { Xi += ux; Yi += uy; }
     }
     const uint32_t TX = __shfl_sync(0xffffffffu, Xi, 31), TY = __shfl_sync(0xffffffffu, Yi, 31);
-    uint32_t Mex = __shfl_up_sync(0xffffffffu, Mi, 1);
-    if (lane == 0) Mex = 0;
     const uint32_t Xex = Xi - X, Yex = Yi - Y;
-    const uint32_t Pex = Mex & 0xFFFFu, Qex = Mex >> 16;
     const uint32_t ex_in = Xex & 0x3FFu, ex_br = (Xex >> 10) & 0x3FFu, ex_rd = Xex >> 20;
     const uint32_t ex_wr = Yex & 0x3FFu, ex_wgb = (Yex >> 10) & 0x3FFu, ex_cl = Yex >> 20;
     const uint32_t T_br = (TX >> 10) & 0x3FFu, T_rd = TX >> 20, T_wr = TY & 0x3FFu, T_cl = TY >> 20;
-    // instructions in the tile at positions <= my last boundary, fetched from the boundary's lane
-    const uint32_t vpos = ex_in + n_in - after;
-    const uint32_t vsrc = __shfl_sync(0xffffffffu, vpos, Pex ? ((Pex - 1) >> 4) : 0u);
+    // the last boundary / wg_begin before my row: the nearest lower lane holding one (ballot),
+    // its position and (boundary) its count of instructions at positions <= it
+    const uint32_t below = (1u << lane) - 1u;
+    const uint32_t bl = __ballot_sync(0xffffffffu, bnd16 != 0) & below;
+    const uint32_t gl = __ballot_sync(0xffffffffu, wgb16 != 0) & below;
+    const uint32_t Lb = bl ? 31u - __clz(bl) : 0u, Lg = gl ? 31u - __clz(gl) : 0u;
+    const uint32_t bsrc = __shfl_sync(0xffffffffu, (uint32_t)(lp + 1) | ((ex_in + n_in - after) << 16), Lb);
+    const uint32_t gsrc = __shfl_sync(0xffffffffu, (uint32_t)(lw + 1), Lg);
+    const uint32_t Pex = bl ? 16u * Lb + (bsrc & 0xFFFFu) : 0u, Qex = gl ? 16u * Lg + gsrc : 0u;
+    const uint32_t vsrc = bsrc >> 16;
     // ---- carry-in for this lane ----
     uint32_t seg_in, lid, byres;
     if (Pex) {
@@ -643,6 +642,7 @@ __global__ void __launch_bounds__(TPB, 2)
     if (DENSE && !(AIWC_ABL & 2)) {
       // my accesses go to the warp's list (pre-swizzled smem index | write << 15)
       // at my in-warp exclusive offset ...
+      uint16_t* const midx = L.midx[warp];
       uint32_t slot = ex_rd + ex_wr;
       const uint32_t rowb = 16u * lane;
       for (uint32_t m = rd16 | wr16; m; m &= m - 1) {
@@ -650,7 +650,9 @@ __global__ void __launch_bounds__(TPB, 2)
         midx[slot++] = (uint16_t)((rowb | (j ^ sw2)) | (((wr16 >> j) & 1u) << 15));
       }
       __syncwarp();
-      // ... and lane i folds accesses i, i + 32, ... of the warp in stream order
+      // ... and lane i folds accesses i, i + 32, ... of the warp in stream order, so one
+      // RED instruction covers consecutive keys of streaming traces.  An address outside
+      // the declared statistics is counted into the sentinel slot n_keys (and flagged).
       const uint32_t n_mem = T_rd + T_wr;
       const uint64_t base = a.am.base, off_max = a.am.off_max;
       const uint32_t k = a.am.k, lmask = (uint32_t)a.am.low_mask, lconst = (uint32_t)a.am.low_const;
@@ -666,15 +668,13 @@ __global__ void __launch_bounds__(TPB, 2)
             const uint64_t off = P[e & 0x0FFFu] - base;
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
-            if (v) {
-              const uint64_t key = off >> k, rel = key - hot_lo;
-              if (HOT && rel < hot_n) {
-                atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
-              } else {
-                uint32_t* const q = tab + key;
-                atomicAdd(q, 1u);
-                if (!(AIWC_ABL & 4)) atomicOr(q, (e & 0x8000u) ? E32_WRITE : E32_READ);
-              }
+            const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
+            if (HOT && rel < hot_n) {
+              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+            } else {
+              uint32_t* const q = tab + key;
+              atomicAdd(q, 1u);
+              if (!(AIWC_ABL & 4)) atomicOr(q, E32_READ << (e >> 15));
             }
           }
         } else {
@@ -685,11 +685,9 @@ __global__ void __launch_bounds__(TPB, 2)
             const uint64_t off = P[e & 0x0FFFu] - base;
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
-            if (v) {
-              const uint64_t key = off >> k, rel = key - hot_lo;
-              if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
-              else atomicAdd(tab + key, (e & 0x8000u) ? (1ull << 32) : 1ull);
-            }
+            const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
+            if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+            else atomicAdd(tab + key, 1ull << (32 * (e >> 15)));
           }
         }
       };
@@ -788,7 +786,7 @@ __global__ void __launch_bounds__(TPB, 2)
   if (DENSE && hot_n) {
     for (uint32_t i = t; i < hot_n; i += TPB) {
       const uint32_t r = stab[i], w = stab[hot_n + i];
-      if (!(r | w)) continue;
+      if (!(r | w) || hot_lo + i >= a.am.n_keys) continue;  // (the sentinel key is not a table key)
       if (a.dense32) {
         uint32_t* const q = static_cast<uint32_t*>(a.dense) + hot_lo + i;
         atomicAdd(q, r + w);

@@ -28,6 +28,9 @@ constexpr uint64_t IPT_END_FLAG = 1ull << 63;
 // when the trace has fewer than 2^30 accesses, else u64 = reads | writes << 32
 constexpr uint32_t E32_COUNT = 0x3FFFFFFFu, E32_READ = 1u << 30, E32_WRITE = 1u << 31;
 constexpr uint64_t E32_MAX_ACCESSES = 1ull << 30;
+// dense-table keys travel as 31-bit list entries in the ingest; key n_keys is the
+// sentinel slot that addresses outside the declared statistics are counted into
+constexpr uint64_t DENSE_MAX_KEYS = (1ull << 31) - 1;
 
 // ---- kind-byte classes (include/aiwc_b200.h) -------------------------------
 __host__ __device__ constexpr bool is_instr(uint32_t k) { return k & 0x01; }
