@@ -252,9 +252,10 @@ def _timed(step, steps, stream, dev, world, local):
     return ms, wall, clk.summary()
 
 
-def _timed_lanes(lane_step, streams, steps, phases, kernels, stream, local):
+def _timed_lanes(lane_step, streams, steps, phases, kernels, stream, local, world=1, dev=None):
     """K steps split over len(streams) host threads (one engine context and CUDA
-    stream each), between CUDA events on `stream` that every lane stream joins."""
+    stream each), between CUDA events on `stream` that every lane stream joins;
+    barrier before, max over ranks after."""
     import torch
 
     from paper_1805_04207_b200 import _native
@@ -273,6 +274,10 @@ def _timed_lanes(lane_step, streams, steps, phases, kernels, stream, local):
             errs.append(e)
 
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -297,7 +302,14 @@ def _timed_lanes(lane_step, streams, steps, phases, kernels, stream, local):
             for i, p in enumerate(_native.PHASES):
                 phases[p].append(ph[i])
             kernels[0] += k
-    return start.elapsed_time(end), wall, clk.summary()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms, wall], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = (float(v) for v in t.tolist())
+    return ms, wall, clk.summary()
 
 
 def run_ours(args) -> None:
@@ -332,7 +344,7 @@ def run_ours(args) -> None:
     n_total = config["events"]
     stream = torch.cuda.current_stream(dev)
 
-    n_streams = max(1, args.streams) if not sharded else 1
+    n_streams = max(1, args.streams)
     if not sharded:
         # one engine context per CUDA stream; with several, concurrent host threads
         # each push whole trace -> report steps (the reference allows distinct
@@ -359,12 +371,33 @@ def run_ours(args) -> None:
         def step():
             return lane_step(0)
     else:
-        backend = D.CudaBackend(local, timing=True)
+        # one engine context, CUDA stream, NCCL communicator (process group) and copy of
+        # the shard per lane: the lanes' collectives run concurrently on their own
+        # communicators, like the single-GPU lanes' whole steps
+        # job mode: the engine runs every collective itself over its own NCCL
+        # communicator (aiwc_ctx_set_comm); AIWC_BENCH_PYDIST=1 drives the same
+        # exchange from Python instead (dist.sharded_result, one collective per call)
+        pydist = os.environ.get("AIWC_BENCH_PYDIST") == "1"
+        sh_lanes = []
+        for i in range(n_streams):
+            cs = stream if i == 0 else torch.cuda.Stream(dev)
+            ltr = tr if i == 0 else synth.device_trace(cfg, total_wi, first=first, count=count)
+            g = None if i == 0 else dist.new_group(list(range(world)))
+            eng = D.CudaBackend(local, timing=True) if pydist else D.NcclJob(local, group=g, timing=True)
+            sh_lanes.append((eng, cs, ltr, g))
+        backend = sh_lanes[0][0]
+
+        def lane_step(i):
+            eng, _, ltr, g = sh_lanes[i]
+            before = eng.launches
+            if pydist:
+                D.sharded_result(eng, ltr, first, group=g)
+            else:
+                eng.result(ltr, first)
+            return list(eng.last_phase_ms), eng.launches - before
 
         def step():
-            before = backend.launches
-            D.sharded_result(backend, tr, first)
-            return backend.last_phase_ms, backend.launches - before
+            return lane_step(0)
 
     phases = {p: [] for p in _native.PHASES}
     kernels = [0]
@@ -381,8 +414,9 @@ def run_ours(args) -> None:
         for i in range(1, n_streams):
             for _ in range(max(3, args.warmup)):
                 lane_step(i)
-        ms, _, clocks = _timed_lanes(lane_step, [c[1] for c in lanes], args.steps, {p: [] for p in phases}, kernels,
-                                     stream, local)
+        lane_streams = [c[1] for c in (lanes if not sharded else sh_lanes)]
+        ms, _, clocks = _timed_lanes(lane_step, lane_streams, args.steps, {p: [] for p in phases}, kernels,
+                                     stream, local, world, dev)
         # per-kernel (phase) times for the roofline come from a separate single-stream
         # run: overlapping streams stretch each kernel's event-to-event duration
         k_timed = kernels[0]
@@ -414,7 +448,7 @@ def run_ours(args) -> None:
     if args.no_e2e:
         if rank == 0:
             print(json.dumps({"ms_per_step": ms_step, "value": value, "phases_ms": phase_med,
-                              "validate_ms": validate_ms}), flush=True)
+                              "validate_ms": validate_ms, "shard_sections_ms": dict(D.LAST_PROFILE)}), flush=True)
         if sharded:
             dist.destroy_process_group()
         return
@@ -427,10 +461,13 @@ def run_ours(args) -> None:
     if not sharded:
         def e2e_step():
             return finalize(consume(host_tr, max_entries=1 << 62, device=local))
-    else:
+    elif pydist:
         def e2e_step():
             return D.sharded_report(backend, host_tr, first, tr.kernel_name, 0, tr.global_size, tr.local_size,
                                     tr.opcodes)
+    else:
+        def e2e_step():
+            return backend.report(host_tr, first, tr.kernel_name, 0, tr.global_size, tr.local_size, tr.opcodes)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     out = {}
     for _ in range(2):
@@ -474,14 +511,17 @@ def run_ours(args) -> None:
             "data": "synthetic", "config": config,
             "lanes": {"events_per_rank": count, "streams": n_streams,
                       "how": f"{n_streams} concurrent trace streams (engine ctx + CUDA stream + own copy of the "
-                             "trace each)" if not sharded else "one engine per rank; NCCL collectives"},
+                             "trace each)" if not sharded else
+                             f"{n_streams} concurrent shard streams per rank (engine ctx with its own NCCL "
+                             "communicator + CUDA stream + own copy of the shard each); collectives inside the engine; "
+                             "dense exchange of 1024-key chunks"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 9 * count,
                     "d2h_bytes_per_step": lanes[0][2].d2h_bytes if not sharded else backend.last_d2h,
                     "ms_per_step": e2e_ms,
                     "h2d_gbs": 9 * count / (e2e_ms / 1e3) / 1e9, "bare_h2d_gbs": h2d_peak,
                     "link_frac": (9 * count / (e2e_ms / 1e3) / 1e9) / h2d_peak,
                     "path": "consume(ColumnarTrace on pinned host)+finalize" if not sharded else
-                            "dist.sharded_report(CudaBackend, pinned host shard)"},
+                            "dist.NcclJob.report(pinned host shard): aiwc_ingest_host + aiwc_finalize in job mode"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_unit": "bytes per launch (ncu dram read+write)",

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define AIWC_ABI_VERSION 1
+#define AIWC_ABI_VERSION 2
 
 /* ---- columnar trace layout: one kind byte + one payload u64 per event ----
  * bit0 instr, bit1 read, bit2 write, bit3 branch, bit4 work-item boundary,
@@ -93,6 +93,9 @@ typedef struct {
    * when they differ). */
   uint64_t n_instr, n_reads, n_writes, n_branches, n_groups;
   uint32_t any_barrier_or_resume, reserved;
+  /* Event index of this trace's first event in the whole job (a work-group shard
+   * of a multi-GPU job: first-appearance order of widths spans the ranks); 0 else. */
+  uint64_t first_event;
 } aiwc_trace_info;
 
 typedef struct {
@@ -156,6 +159,18 @@ int  aiwc_finalize(aiwc_ctx *ctx, aiwc_result *out, void *stream);
 /* Details of the last non-zero return on ctx. */
 int  aiwc_last_error(const aiwc_ctx *ctx, aiwc_error *err);
 
+/* ---- multi-GPU job mode: NCCL inside the engine -------------
+ * Rank 0 makes an id with aiwc_nccl_unique_id (ncclUniqueId, 128 bytes), the
+ * caller broadcasts it, and every rank's ctx joins the job's communicator with
+ * aiwc_ctx_set_comm.  From then on aiwc_ingest takes this rank's work-group shard
+ * (info->first_event = its first event's index in the job) and aiwc_finalize
+ * returns the WHOLE job's result, identical on every rank: the address
+ * statistics all-gather, the dense chunk exchange (aiwc_shard_* below, NCCL
+ * send / recv) and the combine (one all-reduce of a packed u64 buffer, one
+ * all-gather of the variable lists) all run in the engine on `stream`.        */
+int  aiwc_nccl_unique_id(void *id_out);
+int  aiwc_ctx_set_comm(aiwc_ctx *ctx, const void *nccl_unique_id, int rank, int nranks);
+
 /* ---- multi-GPU (work-group shards) ----------------------------
  * A ctx created with AIWC_OPT_SHARD ingests one rank's work-group shard:
  * memory addresses stay compacted on the device and aiwc_finalize fills every
@@ -216,6 +231,41 @@ int  aiwc_partition_runs(aiwc_ctx *ctx, uint64_t base, uint32_t k, uint64_t keys
 int  aiwc_memory_partial_runs(aiwc_ctx *ctx, const uint64_t *runs_dev, uint64_t n_runs, uint32_t k,
                               uint64_t key_lo, uint64_t n_keys, uint64_t total_m, aiwc_memory_part *out,
                               void *stream);
+
+/* ---- multi-GPU dense exchange (aiwc_exchange.cu) ---------------------
+ * The per-rank work is the single-GPU ingest: every rank fills a dense table over
+ * the WHOLE job's key map, then only the 1024-key chunks several ranks touched
+ * travel, as runs of equal table entries, to one owner each.  On a shard ctx:
+ *   1. aiwc_shard_prepare  -- pass 1 of the shard; its address statistics and access count;
+ *   2. (caller) combine every rank's aiwc_shard_stats: min / max / and / or / sum,
+ *      budget = the smallest dense_budget_bytes;
+ *   3. aiwc_shard_ingest   -- ingest with the job's key map; *dense = 1 when the job's
+ *      span fits a dense table (every rank decides alike from the same inputs),
+ *      else the addresses stay compacted for aiwc_partition_* / aiwc_memory_partial*;
+ *   4. aiwc_finalize       -- every non-memory field of the shard;
+ *   5. aiwc_shard_chunks   -- device bitmap of the touched chunks (n_words u32);
+ *      (caller) all-gather the bitmaps into [nranks][n_words];
+ *   6. aiwc_shard_pack     -- runs of the touched chunks other ranks own, grouped by owner
+ *      (two u64 per run: key | length << 32, table entry); counts[o] = runs for owner o;
+ *      (caller) all-to-all of the runs;
+ *   7. aiwc_shard_owned    -- add the received runs, memory statistics of the owned chunks
+ *      with the job's access count; clears every chunk this rank wrote.
+ * Owner of a chunk: the only rank that touched it, else a hash of its index.       */
+typedef struct {
+  uint64_t addr_min, addr_max, addr_and, addr_or;  /* no accesses: ~0, 0, ~0, 0         */
+  uint64_t n_accesses;                             /* reads + writes                    */
+  uint64_t dense_budget_bytes;                     /* dense-table budget of the ctx     */
+  uint64_t n_branches;                             /* branch events of the shard        */
+} aiwc_shard_stats;
+
+int  aiwc_shard_prepare(aiwc_ctx *ctx, const uint8_t *kind_dev, const uint64_t *payload_dev,
+                        const aiwc_trace_info *info, aiwc_shard_stats *local, void *stream);
+int  aiwc_shard_ingest(aiwc_ctx *ctx, const aiwc_shard_stats *job, uint32_t *dense, void *stream);
+int  aiwc_shard_chunks(aiwc_ctx *ctx, uint32_t **bits_dev, uint64_t *n_words);
+int  aiwc_shard_pack(aiwc_ctx *ctx, const uint32_t *all_bits_dev, uint32_t rank, uint32_t nranks,
+                     uint64_t **runs_dev, uint64_t *counts, void *stream);
+int  aiwc_shard_owned(aiwc_ctx *ctx, const uint64_t *runs_dev, uint64_t n_runs, const uint32_t *all_bits_dev,
+                      uint32_t rank, uint32_t nranks, uint64_t total_m, aiwc_memory_part *out, void *stream);
 
 /* ---- stream validation (StreamChecker, trace.py:289-424) -------------------------
  * First violation of a columnar trace, decoded as ColumnarTrace.iter_events

@@ -35,7 +35,8 @@ class TraceInfo(ctypes.Structure):
                 ("addr_and", ctypes.c_uint64), ("addr_or", ctypes.c_uint64),
                 ("n_instr", ctypes.c_uint64), ("n_reads", ctypes.c_uint64), ("n_writes", ctypes.c_uint64),
                 ("n_branches", ctypes.c_uint64), ("n_groups", ctypes.c_uint64),
-                ("any_barrier_or_resume", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("any_barrier_or_resume", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("first_event", ctypes.c_uint64)]
 
 
 class Dist(ctypes.Structure):
@@ -83,6 +84,11 @@ class MemoryPart(ctypes.Structure):
                 ("big", u64p), ("kernels_launched", ctypes.c_uint32)]
 
 
+class ShardStats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("addr_min", "addr_max", "addr_and", "addr_or", "n_accesses",
+                                             "dense_budget_bytes", "n_branches")]
+
+
 class Violation(ctypes.Structure):
     _fields_ = [("event_index", ctypes.c_int64), ("rule", ctypes.c_char * 48), ("detail", ctypes.c_char * 256),
                 ("detail_code", ctypes.c_uint32), ("metric_kind", ctypes.c_uint32), ("group_key", ctypes.c_uint64),
@@ -122,7 +128,9 @@ SIM_SCHEDULE_FLAGS = {"auto": 0, "group": SIM_FORCE_GROUP, "sequential": SIM_FOR
 EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_reset", "aiwc_ingest",
            "aiwc_ingest_host", "aiwc_finalize", "aiwc_last_error", "aiwc_synth_size", "aiwc_synth_fill",
            "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial", "aiwc_validate",
-           "aiwc_sim_create", "aiwc_sim_destroy", "aiwc_sim_last_error", "aiwc_sim_plan", "aiwc_sim_emit")
+           "aiwc_sim_create", "aiwc_sim_destroy", "aiwc_sim_last_error", "aiwc_sim_plan", "aiwc_sim_emit",
+           "aiwc_partition_runs", "aiwc_memory_partial_runs", "aiwc_shard_prepare", "aiwc_shard_ingest",
+           "aiwc_shard_chunks", "aiwc_shard_pack", "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm")
 
 _lib = None
 _lock = threading.Lock()
@@ -161,6 +169,14 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_memory_partial.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                             ctypes.POINTER(MemoryPart), vp]
+        lib.aiwc_shard_prepare.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), ctypes.POINTER(ShardStats), vp]
+        lib.aiwc_shard_ingest.argtypes = [vp, ctypes.POINTER(ShardStats), ctypes.POINTER(ctypes.c_uint32), vp]
+        lib.aiwc_shard_chunks.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_uint64)]
+        lib.aiwc_shard_pack.argtypes = [vp, vp, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(vp), u64p, vp]
+        lib.aiwc_shard_owned.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint32, ctypes.c_uint32,
+                                         ctypes.c_uint64, ctypes.POINTER(MemoryPart), vp]
+        lib.aiwc_nccl_unique_id.argtypes = [vp]
+        lib.aiwc_ctx_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
         i64x3 = ctypes.c_int64 * 3
         lib.aiwc_validate.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), i64x3, i64x3, ctypes.POINTER(Violation), vp]
         lib.aiwc_sim_create.restype = vp
@@ -173,9 +189,11 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_sim_emit.argtypes = [vp, vp, vp, ctypes.c_uint64, vp]
         for name in ("aiwc_sim_plan", "aiwc_sim_emit", "aiwc_ctx_create", "aiwc_reset", "aiwc_ingest", "aiwc_ingest_host", "aiwc_finalize",
                      "aiwc_last_error", "aiwc_synth_fill", "aiwc_shard_tables_get", "aiwc_partition_addresses",
-                     "aiwc_memory_partial", "aiwc_validate"):
+                     "aiwc_memory_partial", "aiwc_validate", "aiwc_partition_runs", "aiwc_memory_partial_runs",
+                     "aiwc_shard_prepare", "aiwc_shard_ingest", "aiwc_shard_chunks", "aiwc_shard_pack",
+                     "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm"):
             getattr(lib, name).restype = ctypes.c_int
-        if lib.aiwc_abi_version() != 1:
+        if lib.aiwc_abi_version() != 2:
             raise DeviceError("libaiwc_b200.so ABI version mismatch")
         _lib = lib
         return lib
@@ -185,11 +203,11 @@ class Context:
     """One aiwc_ctx (one accumulator at a time) on one CUDA device."""
 
     def __init__(self, device: int = 0, *, entry_cap: int = 0, history_len: int = 16,
-                 flags: int = OPT_NO_CONSERVATION):
+                 flags: int = OPT_NO_CONSERVATION, dense_budget_bytes: int = 0):
         self.lib = load_library()
         self.device = device
         self.entry_cap = entry_cap
-        opts = Opts(history_len, flags, entry_cap, 0)
+        opts = Opts(history_len, flags, entry_cap, dense_budget_bytes)
         h = ctypes.c_void_p()
         rc = self.lib.aiwc_ctx_create(ctypes.byref(h), device, ctypes.byref(opts))
         self.h = h

@@ -2,6 +2,7 @@
 // ingest / finalize orchestration and the exact-integer host finishing
 // (coverage counts, order statistics) of pkg/src/aiwc/metrics.py:273-386.
 #include <cudaTypedefs.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -174,6 +175,28 @@ struct aiwc_ctx {
   size_t pre_zeroed = 0;
   size_t dtab_clean = 0, dtab_used = 0;  // bytes of the dense table cleared after the last finalize / used now
   bool one_pass = false;  // declared class totals: no round trip between pass 1 and the ingest
+  // an ingest between its two halves (ingest_begin -> ingest_finish; the shard path
+  // combines the ranks' address statistics in between)
+  struct Pending {
+    const uint8_t* kind = nullptr;
+    const uint64_t* payload = nullptr;
+    uint64_t rows = 0;
+    CUtensorMap km{}, pm{};
+    bool opc_big = false, with_stats = false;
+    size_t clean_prev = 0;
+    uint32_t G = 0, tpc = 0;
+  } pend;
+  // multi-GPU dense exchange: 1024-key chunks of the (global) table this rank touched
+  Buf chunk_bits, own_list;
+  uint64_t n_chunk_words = 0;
+  bool shard_dense = false;
+  // job mode (aiwc_ctx_set_comm): this ctx ingests one rank's shard and finalize
+  // returns the whole job's result; the collectives are NCCL calls on `comm`
+  ncclComm_t comm = nullptr;
+  uint32_t rank = 0, nranks = 1;
+  uint64_t job[7] = {};  // the job's aiwc_shard_stats (combined at ingest)
+  Buf nc_bits, nc_small, nc_send, nc_recv, nc_pack, nc_blob;
+  std::vector<uint64_t> job_itb_ovf, job_ipt_ovf;
   // last encoded TMA descriptors (re-used while the columns stay the same)
   const void* tm_kind = nullptr;
   const void* tm_payload = nullptr;
@@ -284,6 +307,10 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
   if (ctx->p1_ev) cudaEventDestroy(ctx->p1_ev);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  for (Buf* b : {&ctx->chunk_bits, &ctx->own_list, &ctx->nc_bits, &ctx->nc_small, &ctx->nc_send, &ctx->nc_recv,
+                 &ctx->nc_pack, &ctx->nc_blob})
+    if (b->p) cudaFree(b->p);
   if (ctx->hot_ev) cudaEventDestroy(ctx->hot_ev);
   delete ctx;
 }
@@ -391,8 +418,11 @@ static int region_compact(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* pa
   return AIWC_OK;
 }
 
-extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, const aiwc_trace_info* info,
-                           void* stream) {
+// First half of an ingest: argument checks, tensor maps, the dense-table pre-clear
+// (declared statistics), pass 1 and the class totals (a device->host round trip
+// unless the producer declared them).
+static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, const aiwc_trace_info* info,
+                        void* stream) {
   if (!ctx || !info) return AIWC_ERR_ARGUMENT;
   if (ctx->state != 0) return fail(ctx, AIWC_ERR_ARGUMENT, "ctx already holds a trace: call aiwc_reset first");
   const uint64_t n = info->n_events;
@@ -440,12 +470,14 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   // that size on the side stream (unless the previous finalize left it clean).
   // Bounded waste when the trace later takes another path: <= 4 keys / event + 2^20.
   ctx->pre_zeroed = 0;
-  if (n && !with_stats && info->addr_min <= info->addr_max && !(ctx->opts.flags & AIWC_OPT_SHARD)) {
+  const bool shard = ctx->opts.flags & AIWC_OPT_SHARD;
+  if (n && !with_stats && info->addr_min <= info->addr_max && !shard) {
     const uint64_t b0 = info->addr_min & ~1023ull, vary = info->addr_and ^ info->addr_or;
     const uint32_t k0 = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
     const uint64_t sk = (info->addr_max - b0) >> k0;
-    if (sk + 1 < DENSE_MAX_KEYS && (sk + 2) * 4 <= ctx->opts.dense_budget_bytes && sk + 1 <= 4 * n + (1ull << 20)) {
-      const size_t tb = (size_t)(sk + 2) * 4;  // + the sentinel slot of invalid addresses
+    if (sk + 1 < DENSE_MAX_KEYS && dense_alloc_keys(sk + 1) * 4 <= ctx->opts.dense_budget_bytes &&
+        sk + 1 <= 4 * n + (1ull << 20)) {
+      const size_t tb = (size_t)dense_alloc_keys(sk + 1) * 4;  // + the sentinel slot of invalid addresses
       if (ctx->dtab_clean >= tb && ctx->dtab.cap >= tb) {
         ctx->pre_zeroed = ctx->dtab_clean;  // cleared after the previous trace (join_ev)
       } else {
@@ -491,16 +523,31 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
     ctx->n_bres = tt[5];
   }
   ctx->n_events_seen = n;
+  ctx->pend.kind = kind; ctx->pend.payload = payload; ctx->pend.rows = rows;
+  ctx->pend.km = km; ctx->pend.pm = pm;
+  ctx->pend.opc_big = opc_big; ctx->pend.with_stats = with_stats; ctx->pend.clean_prev = clean_prev;
+  ctx->pend.G = G; ctx->pend.tpc = tpc;
+  return AIWC_OK;
+}
 
+// Second half: the memory path from address statistics (the trace's own, or in
+// the shard path the whole job's), buffers, the ingest kernel.
+static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t aand, uint64_t aor, uint64_t M,
+                         bool want_dense, void* stream) {
+  const aiwc_trace_info* info = &ctx->info;
+  const uint64_t n = info->n_events;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint8_t* kind = ctx->pend.kind;
+  const uint64_t* payload = ctx->pend.payload;
+  const uint64_t rows = ctx->pend.rows;
+  CUtensorMap km = ctx->pend.km, pm = ctx->pend.pm;
+  const bool opc_big = ctx->pend.opc_big;
+  const size_t clean_prev = ctx->pend.clean_prev;
+  const uint32_t G = ctx->pend.G, tpc = ctx->pend.tpc;
+  const bool shard = ctx->opts.flags & AIWC_OPT_SHARD;
+  DevState* st = P<DevState>(ctx->dev_state);
+  const uint64_t M_local = ctx->n_rd + ctx->n_wr;
   // ---- memory path decision ----
-  const uint64_t M = ctx->n_rd + ctx->n_wr;
-  uint64_t amin, amax, aand, aor;
-  if (with_stats) {
-    amin = ctx->h_state->addr_min; amax = ctx->h_state->addr_max;
-    aand = ctx->h_state->addr_and; aor = ctx->h_state->addr_or;
-  } else {
-    amin = info->addr_min; amax = info->addr_max; aand = info->addr_and; aor = info->addr_or;
-  }
   auto decide_memory = [&](uint64_t amin, uint64_t amax, uint64_t aand, uint64_t aor) {
     ctx->dense = false;
     ctx->dense32 = M < E32_MAX_ACCESSES;
@@ -526,17 +573,20 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
       ctx->dense32 = M < E32_MAX_ACCESSES && (M <= am.n_keys || (hot_window && M <= 4 * am.n_keys));
       if (ctx->dense_entry == 32) ctx->dense32 = M < E32_MAX_ACCESSES && am.n_keys > SMEM_TABLE_KEYS;
       if (ctx->dense_entry == 64) ctx->dense32 = false;
-      const bool fits = span_keys < DENSE_MAX_KEYS - 1 && (am.n_keys + 1) * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
+      const bool fits = span_keys < DENSE_MAX_KEYS - 1 &&
+                        dense_alloc_keys(am.n_keys) * (ctx->dense32 ? 4 : 8) <= ctx->opts.dense_budget_bytes &&
                         am.n_keys <= 4 * M + (1ull << 20);
-      // a shard keeps its addresses compacted: they are exchanged with the key owners
-      ctx->dense = fits && !(ctx->opts.flags & AIWC_OPT_SHARD);
+      // a shard either fills a dense table over the whole job's key map (the dense
+      // exchange) or keeps its addresses compacted for the owner exchange
+      ctx->dense = fits && (!shard || want_dense);
     }
   };
-  if (M && amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
+  if (M_local && amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
   decide_memory(amin, amax, aand, aor);
+  ctx->shard_dense = shard && ctx->dense;
   // a span too wide for the table: if the accesses sit in few 1 MB regions, squeeze
   // the regions together (exact for every memory statistic) and keep the dense path
-  if (M && n && !ctx->dense && !(ctx->opts.flags & AIWC_OPT_SHARD) && !ctx->region_off) {
+  if (M && n && !ctx->dense && !shard && !ctx->region_off) {
     const uint64_t* np = nullptr;
     unsigned long long rs[4];
     const int rc = region_compact(ctx, kind, payload, n, s, &np, rs);
@@ -563,7 +613,12 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   CK(grow(ctx->br, std::max<uint64_t>(ctx->n_br, 1) * 8));
   if (M) {
     if (ctx->dense) {
-      const size_t tb = (ctx->am.n_keys + 1) * (ctx->dense32 ? 4 : 8);  // + the sentinel slot
+      const size_t tb = dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8);  // + the sentinel slot
+      if (ctx->shard_dense) {  // bitmap of the 1024-key chunks this rank touches (the sentinel's included)
+        ctx->n_chunk_words = ((ctx->am.n_keys + 1 + 1023) / 1024 + 31) / 32;
+        CK(grow(ctx->chunk_bits, ctx->n_chunk_words * 4));
+        CK(cudaMemsetAsync(ctx->chunk_bits.p, 0, ctx->n_chunk_words * 4, s));
+      }
       size_t zeroed = ctx->pre_zeroed;
       if (!zeroed && clean_prev >= tb && ctx->dtab.cap >= tb) zeroed = clean_prev;  // cleared on aux (join_ev)
       if (zeroed) CK(cudaStreamWaitEvent(s, ctx->join_ev, 0));
@@ -616,6 +671,7 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
       ctx->kernels += 1;
     }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
+    a.chunk_bits = ctx->shard_dense ? P<uint32_t>(ctx->chunk_bits) : nullptr;
     ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, stage, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
@@ -629,6 +685,20 @@ extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* p
   ctx->mark(AIWC_PH_INGEST_TOTAL, 1, s);
   ctx->state = 1;
   return AIWC_OK;
+}
+
+static int job_ingest(aiwc_ctx* ctx, void* stream);
+
+extern "C" int aiwc_ingest(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload, const aiwc_trace_info* info,
+                           void* stream) {
+  int rc = ingest_begin(ctx, kind, payload, info, stream);
+  if (rc) return rc;
+  if (ctx->comm) return job_ingest(ctx, stream);
+  const bool own = ctx->pend.with_stats;  // pass 1 measured the statistics, else they were declared
+  const DevState& h = *ctx->h_state;
+  return ingest_finish(ctx, own ? h.addr_min : info->addr_min, own ? h.addr_max : info->addr_max,
+                       own ? h.addr_and : info->addr_and, own ? h.addr_or : info->addr_or, ctx->n_rd + ctx->n_wr,
+                       false, stream);
 }
 
 extern "C" int aiwc_ingest_host(aiwc_ctx* ctx, const uint8_t* kind_host, const uint64_t* payload_host,
@@ -707,7 +777,7 @@ static int fetch_sorted_u32(aiwc_ctx* ctx, Buf& src, uint64_t n, std::vector<uin
   return AIWC_OK;
 }
 
-extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
+static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   if (!ctx || !out) return AIWC_ERR_ARGUMENT;
   if (ctx->state != 1) return fail(ctx, AIWC_ERR_ARGUMENT, "finalize needs exactly one ingest since reset");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -953,7 +1023,7 @@ extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   else if (r.ipt.sum != r.total_instructions) bad = "accumulator inconsistent: IPT samples do not cover all instructions";
   else if (r.ipt.n != r.work_items) bad = "accumulator inconsistent: one IPT sample per work-item expected";
   if (bad && !(ctx->opts.flags & AIWC_OPT_NO_CONSERVATION)) return fail(ctx, AIWC_ERR_INCONSISTENT, bad);
-  if (ctx->opts.entry_cap && r.entries > ctx->opts.entry_cap) {
+  if (ctx->opts.entry_cap && r.entries > ctx->opts.entry_cap && !ctx->comm) {
     fail(ctx, AIWC_ERR_TOO_LARGE, "trace state exceeds the in-memory cap");
     ctx->err.entries = ctx->opts.entry_cap + 1;
     ctx->err.cap = ctx->opts.entry_cap;
@@ -1469,6 +1539,483 @@ extern "C" int aiwc_memory_partial(aiwc_ctx* ctx, const uint64_t* rd, uint64_t n
     launched += 1;
   }
   return owned_result(ctx, st, m, launched, out, s);
+}
+
+
+// ---------------------------------------------------------------------------
+// multi-GPU dense exchange (aiwc_exchange.cu)
+// ---------------------------------------------------------------------------
+extern "C" int aiwc_shard_prepare(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payload,
+                                  const aiwc_trace_info* info, aiwc_shard_stats* local, void* stream) {
+  if (!ctx || !info || !local) return AIWC_ERR_ARGUMENT;
+  if (!(ctx->opts.flags & AIWC_OPT_SHARD)) return fail(ctx, AIWC_ERR_ARGUMENT, "aiwc_shard_prepare needs a shard ctx");
+  const int rc = ingest_begin(ctx, kind, payload, info, stream);
+  if (rc) return rc;
+  const bool own = ctx->pend.with_stats;
+  const DevState& h = *ctx->h_state;
+  aiwc_shard_stats l{};
+  l.n_accesses = ctx->n_rd + ctx->n_wr;
+  if (l.n_accesses) {
+    l.addr_min = own ? h.addr_min : info->addr_min; l.addr_max = own ? h.addr_max : info->addr_max;
+    l.addr_and = own ? h.addr_and : info->addr_and; l.addr_or = own ? h.addr_or : info->addr_or;
+  } else {
+    l.addr_min = ~0ull; l.addr_max = 0; l.addr_and = ~0ull; l.addr_or = 0;
+  }
+  l.dense_budget_bytes = ctx->opts.dense_budget_bytes;
+  l.n_branches = ctx->n_br;
+  *local = l;
+  ctx->state = 3;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_shard_ingest(aiwc_ctx* ctx, const aiwc_shard_stats* job, uint32_t* dense, void* stream) {
+  if (!ctx || !job || !dense) return AIWC_ERR_ARGUMENT;
+  if (ctx->state != 3) return fail(ctx, AIWC_ERR_ARGUMENT, "aiwc_shard_ingest needs aiwc_shard_prepare first");
+  if (job->n_accesses < ctx->n_rd + ctx->n_wr || (job->n_accesses && job->addr_min > job->addr_max))
+    return fail(ctx, AIWC_ERR_ARGUMENT, "job statistics do not cover this shard");
+  const uint64_t budget = ctx->opts.dense_budget_bytes;
+  ctx->opts.dense_budget_bytes = std::min<uint64_t>(budget, job->dense_budget_bytes);  // every rank decides alike
+  const int rc = ingest_finish(ctx, job->addr_min, job->addr_max, job->addr_and, job->addr_or, job->n_accesses, true,
+                               stream);
+  ctx->opts.dense_budget_bytes = budget;
+  if (rc) return rc;
+  *dense = ctx->shard_dense ? 1u : 0u;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_shard_chunks(aiwc_ctx* ctx, uint32_t** bits, uint64_t* n_words) {
+  if (!ctx || !bits || !n_words) return AIWC_ERR_ARGUMENT;
+  if (!ctx->shard_dense || ctx->state != 2)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "chunk bitmap needs a dense shard ingest and aiwc_finalize");
+  *bits = P<uint32_t>(ctx->chunk_bits);
+  *n_words = ctx->n_chunk_words;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_shard_pack(aiwc_ctx* ctx, const uint32_t* all_bits, uint32_t rank, uint32_t nranks,
+                               uint64_t** runs_dev, uint64_t* counts, void* stream) {
+  if (!ctx || !all_bits || !runs_dev || !counts || nranks == 0 || rank >= nranks || nranks > (uint32_t)PA_MAXR)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad pack arguments");
+  if (!ctx->shard_dense || ctx->state != 2) return fail(ctx, AIWC_ERR_ARGUMENT, "pack needs a dense shard ingest");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->part_cursor, PA_MAXR * 8));
+  unsigned long long* cur = P<unsigned long long>(ctx->part_cursor);
+  CK(cudaMemsetAsync(cur, 0, PA_MAXR * 8, s));
+  const uint64_t words = ctx->n_chunk_words;
+  ctx->kernels += launch_pack(ctx->dtab.p, ctx->dense32, all_bits, words, rank, nranks, 0, cur, nullptr,
+                              (uint32_t)ctx->n_sms, s);
+  std::vector<unsigned long long> c(PA_MAXR, 0), off(PA_MAXR, 0);
+  CK(cudaMemcpyAsync(c.data(), cur, PA_MAXR * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  unsigned long long tot = 0;
+  for (uint32_t o = 0; o < nranks; ++o) { off[o] = tot; tot += c[o]; counts[o] = c[o]; }
+  CK(grow(ctx->part_entries, std::max<uint64_t>(tot, 1) * 16));
+  if (tot) {
+    CK(cudaMemcpyAsync(cur, off.data(), PA_MAXR * 8, cudaMemcpyHostToDevice, s));
+    ctx->kernels += launch_pack(ctx->dtab.p, ctx->dense32, all_bits, words, rank, nranks, 1, cur,
+                                P<uint64_t>(ctx->part_entries), (uint32_t)ctx->n_sms, s);
+  }
+  CK(cudaGetLastError());
+  *runs_dev = P<uint64_t>(ctx->part_entries);
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_shard_owned(aiwc_ctx* ctx, const uint64_t* runs, uint64_t n_runs, const uint32_t* all_bits,
+                                uint32_t rank, uint32_t nranks, uint64_t total_m, aiwc_memory_part* out, void* stream) {
+  if (!ctx || !out || !all_bits || (n_runs && !runs) || nranks == 0 || rank >= nranks)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad owned-statistics arguments");
+  if (!ctx->shard_dense || ctx->state != 2) return fail(ctx, AIWC_ERR_ARGUMENT, "owned statistics need a dense shard");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->mp_state, sizeof(DevState)));
+  DevState* st = P<DevState>(ctx->mp_state);
+  init_state_kernel<<<64, 256, 0, s>>>(st);
+  uint32_t launched = 1;
+  const uint64_t tm = std::max<uint64_t>(total_m, 1);
+  CK(grow(ctx->mp_ovf, (tm / CBINS + 2) * 8));
+  const uint64_t words = ctx->n_chunk_words;
+  const uint64_t n_keys = ctx->am.n_keys;
+  launched += launch_apply_runs(ctx->dtab.p, ctx->dense32, runs, n_runs, n_keys, all_bits, words, rank, nranks,
+                                &st->flags, (uint32_t)ctx->n_sms, s);
+  const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
+  launch_dense_stats(ctx->dtab.p, ctx->dense32, n_keys, ctx->am.k, tm, st, P<double>(ctx->partials), nct,
+                     P<uint64_t>(ctx->mp_ovf), s, all_bits, words, rank, nranks);
+  launch_entropy_finish(st, P<double>(ctx->partials), nct, tm, ctx->am.k, s);
+  // the table is clean again: zero what this rank wrote, reset its bitmap
+  launched += 2 + launch_clear_chunks(ctx->dtab.p, ctx->dense32, dense_alloc_keys(n_keys), all_bits, words, rank,
+                                      nranks, P<uint32_t>(ctx->chunk_bits), (uint32_t)ctx->n_sms, s);
+  ctx->dtab_clean = ctx->dtab.cap;
+  return owned_result(ctx, st, total_m, launched, out, s);
+}
+
+// ---------------------------------------------------------------------------
+// job mode: NCCL in the engine (aiwc_ctx_set_comm).  aiwc_ingest takes this
+// rank's work-group shard, aiwc_finalize returns the whole job's result on every
+// rank; every collective is an NCCL call on the caller's stream, with no Python
+// between them (SURVEY.md §8b aiwc_ctx_set_comm, §8e).
+// ---------------------------------------------------------------------------
+#define NC(call)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (call);                                                           \
+    if (r_ != ncclSuccess) {                                                            \
+      char m_[200];                                                                     \
+      snprintf(m_, sizeof m_, "%s: %s", #call, ncclGetErrorString(r_));                 \
+      return fail(ctx, AIWC_ERR_NCCL, m_);                                              \
+    }                                                                                   \
+  } while (0)
+
+extern "C" int aiwc_nccl_unique_id(void* id_out) {
+  if (!id_out) return AIWC_ERR_ARGUMENT;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return AIWC_ERR_NCCL;
+  memcpy(id_out, &id, sizeof id);
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_ctx_set_comm(aiwc_ctx* ctx, const void* id, int rank, int nranks) {
+  if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks || nranks > PA_MAXR)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "bad communicator arguments");
+  if (ctx->comm) return fail(ctx, AIWC_ERR_ARGUMENT, "ctx already has a communicator");
+  CK(cudaSetDevice(ctx->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  NC(ncclCommInitRank(&ctx->comm, nranks, uid, rank));
+  ctx->rank = (uint32_t)rank;
+  ctx->nranks = (uint32_t)nranks;
+  ctx->opts.flags |= AIWC_OPT_SHARD;  // memory statistics come from the job's exchange
+  return AIWC_OK;
+}
+
+// all-gather of n u64 per rank through device memory: out = [nranks][n] on the host
+static int job_allgather_u64(aiwc_ctx* ctx, const uint64_t* mine, size_t n, std::vector<uint64_t>& out,
+                             cudaStream_t s) {
+  const size_t R = ctx->nranks;
+  CK(grow(ctx->nc_small, (R + 1) * n * 8));
+  uint64_t* d = P<uint64_t>(ctx->nc_small);
+  CK(cudaMemcpyAsync(d + R * n, mine, n * 8, cudaMemcpyHostToDevice, s));
+  NC(ncclAllGather(d + R * n, d, n, ncclUint64, ctx->comm, s));
+  out.resize(R * n);
+  CK(cudaMemcpyAsync(out.data(), d, R * n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return AIWC_OK;
+}
+
+// second half of a job-mode ingest: the job's statistics from every rank's, then
+// the ingest with the job's key map (a dense table when it fits on every rank)
+static int job_ingest(aiwc_ctx* ctx, void* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const aiwc_trace_info* info = &ctx->info;
+  const bool own = ctx->pend.with_stats;
+  const DevState& h = *ctx->h_state;
+  uint64_t l[7];
+  l[4] = ctx->n_rd + ctx->n_wr;
+  if (l[4]) {
+    l[0] = own ? h.addr_min : info->addr_min; l[1] = own ? h.addr_max : info->addr_max;
+    l[2] = own ? h.addr_and : info->addr_and; l[3] = own ? h.addr_or : info->addr_or;
+  } else {
+    l[0] = ~0ull; l[1] = 0; l[2] = ~0ull; l[3] = 0;
+  }
+  l[5] = ctx->opts.dense_budget_bytes;
+  l[6] = ctx->n_br;
+  std::vector<uint64_t> all;
+  int rc = job_allgather_u64(ctx, l, 7, all, s);
+  if (rc) return rc;
+  uint64_t* j = ctx->job;
+  j[0] = ~0ull; j[1] = 0; j[2] = ~0ull; j[3] = 0; j[4] = 0; j[5] = ~0ull; j[6] = 0;
+  for (uint32_t r = 0; r < ctx->nranks; ++r) {
+    const uint64_t* x = &all[7 * r];
+    if (x[4]) { j[0] = std::min(j[0], x[0]); j[1] = std::max(j[1], x[1]); j[2] &= x[2]; j[3] |= x[3]; }
+    j[4] += x[4]; j[5] = std::min(j[5], x[5]); j[6] += x[6];
+  }
+  const uint64_t budget = ctx->opts.dense_budget_bytes;
+  ctx->opts.dense_budget_bytes = j[5];  // every rank decides alike
+  rc = ingest_finish(ctx, j[0], j[1], j[2], j[3], j[4], true, stream);
+  ctx->opts.dense_budget_bytes = budget;
+  return rc;
+}
+
+// runs / addresses to their owners: send counts[o] u64 words to rank o, receive
+// into ctx->nc_recv; *n_recv = words received (the counts matrix is all-gathered first)
+static int job_exchange(aiwc_ctx* ctx, const uint64_t* send, const uint64_t* counts, uint64_t* n_recv,
+                        cudaStream_t s) {
+  const uint32_t R = ctx->nranks, me = ctx->rank;
+  std::vector<uint64_t> m;
+  int rc = job_allgather_u64(ctx, counts, R, m, s);
+  if (rc) return rc;
+  uint64_t tot = 0;
+  for (uint32_t p = 0; p < R; ++p) tot += m[(size_t)p * R + me];
+  CK(grow(ctx->nc_recv, std::max<uint64_t>(tot, 1) * 8));
+  uint64_t* recv = P<uint64_t>(ctx->nc_recv);
+  NC(ncclGroupStart());
+  uint64_t so = 0, ro = 0;
+  for (uint32_t p = 0; p < R; ++p) {
+    const uint64_t sc = counts[p], rcnt = m[(size_t)p * R + me];
+    if (sc) NC(ncclSend(send + so, sc, ncclUint64, (int)p, ctx->comm, s));
+    if (rcnt) NC(ncclRecv(recv + ro, rcnt, ncclUint64, (int)p, ctx->comm, s));
+    so += sc; ro += rcnt;
+  }
+  NC(ncclGroupEnd());
+  *n_recv = tot;
+  return AIWC_OK;
+}
+
+static void merge_sorted(std::vector<uint64_t>& acc, const uint64_t* v, size_t n) {
+  const size_t a = acc.size();
+  acc.insert(acc.end(), v, v + n);
+  std::inplace_merge(acc.begin(), acc.begin() + (ptrdiff_t)a, acc.end());
+}
+
+static int finalize_job(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
+  aiwc_result loc{};
+  int rc = finalize_local(ctx, &loc, stream);
+  if (rc) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const uint32_t R = ctx->nranks, me = ctx->rank;
+  const uint64_t M = ctx->job[4];
+  const bool has_br = ctx->job[6] > 0;
+  // the shard's histograms (the owner statistics below reuse the host state block)
+  std::vector<uint64_t> itb_h(ctx->h_state->itb_hist, ctx->h_state->itb_hist + HBINS);
+  std::vector<uint64_t> ipt_h(ctx->h_state->ipt_hist, ctx->h_state->ipt_hist + HBINS);
+  const uint64_t itb_sum = loc.itb.sum, ipt_sum = loc.ipt.sum;
+
+  // ---- memory: the owners' statistics ----
+  aiwc_memory_part mp{};
+  std::vector<uint64_t> hist0(CBINS, 0), big;
+  if (M) {
+    if (ctx->shard_dense) {
+      const uint64_t words = ctx->n_chunk_words;
+      CK(grow(ctx->nc_bits, (size_t)R * words * 4));
+      NC(ncclAllGather(ctx->chunk_bits.p, ctx->nc_bits.p, words, ncclUint32, ctx->comm, s));
+      uint64_t* runs = nullptr;
+      std::vector<uint64_t> cnt(R);
+      if ((rc = aiwc_shard_pack(ctx, P<uint32_t>(ctx->nc_bits), me, R, &runs, cnt.data(), stream))) return rc;
+      for (auto& c : cnt) c *= 2;  // two words per run
+      uint64_t n_words = 0;
+      if ((rc = job_exchange(ctx, runs, cnt.data(), &n_words, s))) return rc;
+      if ((rc = aiwc_shard_owned(ctx, P<uint64_t>(ctx->nc_recv), n_words / 2, P<uint32_t>(ctx->nc_bits), me, R, M,
+                                 &mp, stream))) return rc;
+    } else {
+      // compacted addresses to key-range owners (ranges aligned to 1024 keys)
+      const uint64_t base = ctx->job[0] & ~1023ull, vary = ctx->job[2] ^ ctx->job[3];
+      const uint32_t k = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
+      const uint64_t n_keys = ((ctx->job[1] - base) >> k) + 1;
+      uint64_t kpr = (n_keys + R - 1) / R;
+      kpr = (kpr + 1023) / 1024 * 1024;
+      uint64_t *rd = nullptr, *wr = nullptr;
+      std::vector<uint64_t> c2(2 * R);
+      if ((rc = aiwc_partition_addresses(ctx, base, k, kpr, R, &rd, &wr, c2.data(), stream))) return rc;
+      // reads and writes travel in one exchange: [reads for o | writes for o] per owner
+      const uint64_t nr = ctx->n_rd, nw = ctx->n_wr;
+      CK(grow(ctx->nc_send, std::max<uint64_t>(nr + nw, 1) * 8));
+      std::vector<uint64_t> cnt(R);
+      uint64_t so = 0, ro = 0, wo = 0;
+      for (uint32_t o = 0; o < R; ++o) {
+        CK(cudaMemcpyAsync(P<uint64_t>(ctx->nc_send) + so, rd + ro, c2[o] * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(P<uint64_t>(ctx->nc_send) + so + c2[o], wr + wo, c2[R + o] * 8, cudaMemcpyDeviceToDevice, s));
+        cnt[o] = c2[o] + c2[R + o];
+        so += cnt[o]; ro += c2[o]; wo += c2[R + o];
+      }
+      // per-owner read counts travel too, so the owner can split what it receives
+      std::vector<uint64_t> rc_all;
+      if ((rc = job_allgather_u64(ctx, c2.data(), 2 * R, rc_all, s))) return rc;
+      uint64_t n_words = 0;
+      if ((rc = job_exchange(ctx, P<uint64_t>(ctx->nc_send), cnt.data(), &n_words, s))) return rc;
+      // regroup: reads of every sender first, then writes
+      const uint64_t* recv = P<uint64_t>(ctx->nc_recv);
+      uint64_t tr = 0, tw = 0;
+      for (uint32_t p = 0; p < R; ++p) { tr += rc_all[(size_t)p * 2 * R + me]; tw += rc_all[(size_t)p * 2 * R + R + me]; }
+      CK(grow(ctx->nc_pack, std::max<uint64_t>(tr + tw, 1) * 8));
+      uint64_t* rw = P<uint64_t>(ctx->nc_pack);
+      uint64_t off = 0, orr = 0, ow = tr;
+      for (uint32_t p = 0; p < R; ++p) {
+        const uint64_t a = rc_all[(size_t)p * 2 * R + me], b = rc_all[(size_t)p * 2 * R + R + me];
+        CK(cudaMemcpyAsync(rw + orr, recv + off, a * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(rw + ow, recv + off + a, b * 8, cudaMemcpyDeviceToDevice, s));
+        off += a + b; orr += a; ow += b;
+      }
+      const uint64_t lo = (uint64_t)me * kpr, n_owned = lo < n_keys ? std::min(kpr, n_keys - lo) : 0;
+      if ((rc = aiwc_memory_partial(ctx, rw, tr, rw + tr, tw, base, k, lo, n_owned, M, &mp, stream))) return rc;
+    }
+    hist0.assign(mp.cnt_hist0, mp.cnt_hist0 + CBINS);
+    big.assign(mp.big, mp.big + mp.n_big);
+  }
+
+  // ---- one packed all-reduce: every summable integer, plus each rank's list lengths
+  // in its own row of an [R][5] block (the sum hands every rank all lengths) ----
+  const uint32_t n_opc = loc.n_opcodes, tb = (uint32_t)ctx->branch_tab_host.size();
+  std::vector<uint64_t> pk;
+  pk.reserve(12 + n_opc + 3 * 1024 + 5 * R + (has_br ? tb : 0));
+  const uint64_t sc[12] = {loc.n_events, loc.total_instructions, loc.work_items, loc.barriers_hit, loc.total_reads,
+                           loc.total_writes, itb_sum, ipt_sum, loc.branch_executions, mp.unique_reads,
+                           mp.unique_writes, mp.footprint};
+  pk.insert(pk.end(), sc, sc + 12);
+  pk.insert(pk.end(), loc.opcode_counts, loc.opcode_counts + n_opc);
+  pk.insert(pk.end(), itb_h.begin(), itb_h.end());
+  pk.insert(pk.end(), ipt_h.begin(), ipt_h.end());
+  pk.insert(pk.end(), hist0.begin(), hist0.end());
+  const size_t lens_at = pk.size();
+  pk.resize(pk.size() + 5 * R, 0);
+  pk[lens_at + 5 * me + 0] = ctx->itb_ovf_sorted.size();
+  pk[lens_at + 5 * me + 1] = ctx->ipt_ovf_sorted.size();
+  pk[lens_at + 5 * me + 2] = big.size();
+  pk[lens_at + 5 * me + 3] = loc.n_widths;
+  pk[lens_at + 5 * me + 4] = loc.n_site_list;
+  if (has_br) pk.insert(pk.end(), ctx->branch_tab_host.begin(), ctx->branch_tab_host.end());
+  CK(grow(ctx->nc_pack, pk.size() * 8));
+  CK(cudaMemcpyAsync(ctx->nc_pack.p, pk.data(), pk.size() * 8, cudaMemcpyHostToDevice, s));
+  NC(ncclAllReduce(ctx->nc_pack.p, ctx->nc_pack.p, pk.size(), ncclUint64, ncclSum, ctx->comm, s));
+  CK(cudaMemcpyAsync(pk.data(), ctx->nc_pack.p, pk.size() * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+
+  // ---- one all-gather of the variable parts, padded to the longest ----
+  std::vector<uint64_t> blob;
+  double ls[NLEVELS];
+  for (int i = 0; i < NLEVELS; ++i) ls[i] = mp.level_sum[i];
+  blob.insert(blob.end(), reinterpret_cast<uint64_t*>(ls), reinterpret_cast<uint64_t*>(ls) + NLEVELS);
+  blob.insert(blob.end(), ctx->itb_ovf_sorted.begin(), ctx->itb_ovf_sorted.end());
+  blob.insert(blob.end(), ctx->ipt_ovf_sorted.begin(), ctx->ipt_ovf_sorted.end());
+  blob.insert(blob.end(), big.begin(), big.end());
+  for (uint32_t i = 0; i < loc.n_widths; ++i) {
+    blob.push_back(loc.width_values[i]); blob.push_back(loc.width_counts[i]);
+    blob.push_back(ctx->width_firsts[i] + ctx->info.first_event);  // job-wide first appearance
+  }
+  for (uint32_t i = 0; i < loc.n_site_list; ++i) { blob.push_back(loc.site_ids[i]); blob.push_back(loc.site_counts[i]); }
+  size_t width = 0;
+  for (uint32_t r = 0; r < R; ++r) {
+    const uint64_t* L = &pk[lens_at + 5 * r];
+    width = std::max<size_t>(width, NLEVELS + L[0] + L[1] + L[2] + 3 * L[3] + 2 * L[4]);
+  }
+  blob.resize(width, 0);
+  CK(grow(ctx->nc_blob, (size_t)(R + 1) * width * 8));
+  uint64_t* db = P<uint64_t>(ctx->nc_blob);
+  CK(cudaMemcpyAsync(db + (size_t)R * width, blob.data(), width * 8, cudaMemcpyHostToDevice, s));
+  NC(ncclAllGather(db + (size_t)R * width, db, width, ncclUint64, ctx->comm, s));
+  std::vector<uint64_t> all((size_t)R * width);
+  CK(cudaMemcpyAsync(all.data(), db, all.size() * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+
+  // ---- assemble the job's result (the rules of aiwc_finalize) ----
+  size_t o = 0;
+  auto take = [&](size_t n) { o += n; return &pk[o - n]; };
+  const uint64_t* S = take(12);
+  const uint64_t* opc = take(n_opc);
+  const uint64_t* ih = take(HBINS);
+  const uint64_t* ph = take(HBINS);
+  const uint64_t* h0 = take(CBINS);
+  take(5 * R);
+  const uint64_t* btab = has_br ? take(tb) : nullptr;
+  double lsum[NLEVELS] = {0};
+  std::vector<uint64_t> itb_o, ipt_o, big_all;
+  std::vector<std::pair<uint64_t, std::pair<uint64_t, uint64_t>>> wmap;  // width -> (count, first)
+  std::vector<std::pair<uint64_t, uint64_t>> smap;                       // (site, count)
+  for (uint32_t r = 0; r < R; ++r) {  // rank order: the fp64 level sums are deterministic
+    const uint64_t* L = &pk[lens_at + 5 * r];
+    const uint64_t* b = &all[(size_t)r * width];
+    const double* d = reinterpret_cast<const double*>(b);
+    for (int i = 0; i < NLEVELS; ++i) lsum[i] += d[i];
+    size_t q = NLEVELS;
+    merge_sorted(itb_o, b + q, L[0]); q += L[0];
+    merge_sorted(ipt_o, b + q, L[1]); q += L[1];
+    big_all.insert(big_all.end(), b + q, b + q + L[2]); q += L[2];
+    for (uint64_t i = 0; i < L[3]; ++i, q += 3) wmap.push_back({b[q], {b[q + 1], b[q + 2]}});
+    for (uint64_t i = 0; i < L[4]; ++i, q += 2) smap.push_back({b[q], b[q + 1]});
+  }
+  aiwc_result rj{};
+  rj.n_events = S[0]; rj.total_instructions = S[1]; rj.work_items = S[2]; rj.barriers_hit = S[3];
+  rj.total_reads = S[4]; rj.total_writes = S[5];
+  rj.branch_executions = S[8];
+  rj.unique_reads = S[9]; rj.unique_writes = S[10]; rj.footprint = S[11];
+  ctx->opc_counts.assign(opc, opc + n_opc);
+  {
+    std::vector<uint64_t> oc;
+    unsigned __int128 tot = 0;
+    for (uint32_t i = 0; i < n_opc; ++i) if (opc[i]) { oc.push_back(opc[i]); tot += opc[i]; }
+    std::sort(oc.begin(), oc.end(), std::greater<uint64_t>());
+    rj.opcode_coverage = coverage_from(oc, nullptr, 0, tot);
+  }
+  ctx->job_itb_ovf = itb_o; ctx->job_ipt_ovf = ipt_o;
+  std::vector<unsigned long long> ihv(ih, ih + HBINS), phv(ph, ph + HBINS), h0v(h0, h0 + CBINS);
+  order_stats(ihv.data(), itb_o, &rj.itb); rj.itb.sum = S[6];
+  order_stats(phv.data(), ipt_o, &rj.ipt); rj.ipt.sum = S[7];
+  std::sort(big_all.begin(), big_all.end(), std::greater<uint64_t>());
+  rj.footprint_90 = M ? coverage_from(big_all, h0v.data(), CBINS, M) : 0;
+  for (int i = 0; i < NLEVELS; ++i) {
+    const double v = M ? -lsum[i] : 0.0;
+    if (i == 0) rj.gmae = v; else rj.lmae[i - 1] = v;
+  }
+  // branch entropies from the job's pooled pattern table (entropy.py:123-132)
+  if (btab && rj.branch_executions) {
+    unsigned long long obs = 0;
+    double y = 0.0, l = 0.0;
+    for (uint32_t i = 0; i < tb; ++i) {
+      const uint64_t tot = btab[i] >> 32;
+      if (!tot) continue;
+      obs += tot;
+      const double dt = (double)tot, p = (double)(btab[i] & 0xFFFFFFFFull) / dt, q = 1.0 - p;
+      const double hh = -((p > 0 ? p * log2(p) : 0.0) + (q > 0 ? q * log2(q) : 0.0));
+      y += dt * hh;
+      l += dt * (p < q ? p : q);
+    }
+    rj.branch_observations = obs;
+    rj.yokota = obs ? y / (double)obs : 0.0;
+    rj.linear = obs ? l / (double)obs : 0.0;
+  }
+  rj.branch_excluded = rj.branch_executions - rj.branch_observations;
+  // sites ascending with summed executions; widths in first-appearance order
+  std::sort(smap.begin(), smap.end());
+  ctx->site_ids.clear(); ctx->site_counts.clear();
+  for (auto& sc2 : smap) {
+    if (!ctx->site_ids.empty() && ctx->site_ids.back() == sc2.first) ctx->site_counts.back() += sc2.second;
+    else { ctx->site_ids.push_back(sc2.first); ctx->site_counts.push_back(sc2.second); }
+  }
+  {
+    std::vector<uint64_t> scs(ctx->site_counts);
+    std::sort(scs.begin(), scs.end(), std::greater<uint64_t>());
+    rj.branch_90 = rj.branch_executions ? coverage_from(scs, nullptr, 0, rj.branch_executions) : 0;
+  }
+  rj.n_sites = ctx->site_ids.size();
+  std::sort(wmap.begin(), wmap.end());
+  std::vector<std::pair<uint64_t, std::pair<uint64_t, uint64_t>>> wm;  // (first, (width, count))
+  for (size_t i = 0; i < wmap.size();) {
+    uint64_t c = 0, f = ~0ull;
+    size_t e = i;
+    for (; e < wmap.size() && wmap[e].first == wmap[i].first; ++e) { c += wmap[e].second.first; f = std::min(f, wmap[e].second.second); }
+    wm.push_back({f, {wmap[i].first, c}});
+    i = e;
+  }
+  std::sort(wm.begin(), wm.end());
+  ctx->width_vals.clear(); ctx->width_counts.clear(); ctx->width_firsts.clear();
+  for (auto& w : wm) {
+    ctx->width_vals.push_back(w.second.first); ctx->width_counts.push_back(w.second.second);
+    ctx->width_firsts.push_back(w.first);
+  }
+  rj.entries = rj.unique_reads + rj.unique_writes + rj.branch_executions;
+  rj.n_opcodes = n_opc;
+  rj.opcode_counts = ctx->opc_counts.data();
+  rj.n_widths = (uint32_t)ctx->width_vals.size();
+  rj.width_values = ctx->width_vals.data();
+  rj.width_counts = ctx->width_counts.data();
+  rj.n_site_list = (uint32_t)ctx->site_ids.size();
+  rj.site_ids = ctx->site_ids.data();
+  rj.site_counts = ctx->site_counts.data();
+  rj.used_dense_table = ctx->shard_dense;
+  rj.kernels_launched = ctx->kernels;
+  rj.d2h_bytes = ctx->d2h;
+  for (int i = 0; i < AIWC_N_PHASES; ++i) rj.phase_ms[i] = loc.phase_ms[i];
+  *out = rj;
+  if (ctx->opts.entry_cap && rj.entries > ctx->opts.entry_cap) {
+    fail(ctx, AIWC_ERR_TOO_LARGE, "trace state exceeds the in-memory cap");
+    ctx->err.entries = ctx->opts.entry_cap + 1;
+    ctx->err.cap = ctx->opts.entry_cap;
+    return AIWC_ERR_TOO_LARGE;
+  }
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_finalize(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
+  if (ctx && ctx->comm) return finalize_job(ctx, out, stream);
+  return finalize_local(ctx, out, stream);
 }
 
 

@@ -96,7 +96,8 @@ template <typename E>
 __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__ tab,
                                                            uint64_t n_keys, int nlev, double m, DevState* st,
                                                            double* partials, uint32_t n_parts,
-                                                           unsigned long long* lvl0_ovf) {
+                                                           unsigned long long* lvl0_ovf, const uint32_t* own_bits,
+                                                           uint64_t own_words, uint32_t rank, uint32_t nranks) {
   extern __shared__ uint32_t hsm[];
   __shared__ DenseShared D;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -110,7 +111,10 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
 
   auto load = [&](uint64_t ch, E (&c)[K]) {
     const uint64_t k0 = ch * CHUNK + (uint64_t)t * K;
-    if (k0 + K <= n_keys) {
+    if (own_bits && !chunk_is_owned(own_bits, own_words, ch, rank, nranks)) {  // another rank's chunk: empty here
+#pragma unroll
+      for (int i = 0; i < K; ++i) c[i] = (E)0;
+    } else if (k0 + K <= n_keys) {
       const uint4* p = reinterpret_cast<const uint4*>(tab + k0);
       constexpr int V = K * (int)sizeof(E) / 16;
 #pragma unroll
@@ -269,19 +273,21 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
 }  // namespace
 
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
-                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s) {
+                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s,
+                        const uint32_t* own_bits, uint64_t own_words, uint32_t rank, uint32_t nranks) {
   const int nlev = k >= 10 ? 1 : 11 - (int)k;
   const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(lvl0_ovf);
   if (e32) {
     set_smem_once(dense_stats_kernel<uint32_t>, (int)smem);
     dense_stats_kernel<uint32_t><<<n_ctas, T, smem, s>>>(static_cast<const uint32_t*>(tab), n_keys, nlev,
-                                                         (double)total_m, st, partials, n_ctas, ovf);
+                                                         (double)total_m, st, partials, n_ctas, ovf,
+                                                         own_bits, own_words, rank, nranks);
   } else {
     set_smem_once(dense_stats_kernel<unsigned long long>, (int)smem);
     dense_stats_kernel<unsigned long long><<<n_ctas, T, smem, s>>>(static_cast<const unsigned long long*>(tab),
                                                                    n_keys, nlev, (double)total_m, st, partials,
-                                                                   n_ctas, ovf);
+                                                                   n_ctas, ovf, own_bits, own_words, rank, nranks);
   }
 }
 

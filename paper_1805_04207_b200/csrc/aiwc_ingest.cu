@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(TPB, 2)
   uint32_t n_wib = 0, n_bar = 0;  // WI_BEGIN / BARRIER events (metrics.py: work_items, barriers_hit)
   const uint32_t sw = lane & 7, sw2 = sw << 1;
   uint4* const wclose = L.closes[warp];
+  uint32_t last_ch = ~0u, last_ch2 = ~0u;  // shard: the last two chunks this lane marked
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -657,9 +658,27 @@ __global__ void __launch_bounds__(TPB, 2)
       const uint64_t base = a.am.base, off_max = a.am.off_max;
       const uint32_t k = a.am.k, lmask = (uint32_t)a.am.low_mask, lconst = (uint32_t)a.am.low_const;
       uint32_t inval = 0;
-      // the window check is compiled in only when a window exists (CTA-uniform branch)
-      auto fold = [&](auto with_window) {
+      // the window check and the shard's chunk marks are compiled in only when
+      // needed (CTA-uniform branches)
+      auto fold = [&](auto with_window, auto with_marks) {
         constexpr bool HOT = decltype(with_window)::value;
+        constexpr bool MARK = decltype(with_marks)::value;
+        // shard: bit (key >> 10) of the touched-chunk map -- checked only for a chunk
+        // neither of this lane's last two marks holds (they persist across tiles: reads
+        // and writes of streaming traces alternate between two chunks), and set only
+        // when not set yet (a plain load first: the map is small and L1 / L2 resident,
+        // same-word REDs are not)
+        auto mark = [&](uint64_t key) {
+          if (MARK) {
+            const uint32_t ch = (uint32_t)(key >> 10);
+            if (ch != last_ch && ch != last_ch2) {
+              last_ch2 = last_ch;
+              last_ch = ch;
+              const uint32_t bit = 1u << (ch & 31);
+              if (!(a.chunk_bits[ch >> 5] & bit)) atomicOr(&a.chunk_bits[ch >> 5], bit);
+            }
+          }
+        };
         if (a.dense32) {
           uint32_t* const tab = static_cast<uint32_t*>(a.dense);
 #pragma unroll 4  // several accesses per lane in flight
@@ -669,6 +688,7 @@ __global__ void __launch_bounds__(TPB, 2)
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
             const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
+            mark(key);
             if (HOT && rel < hot_n) {
               atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
             } else {
@@ -686,13 +706,19 @@ __global__ void __launch_bounds__(TPB, 2)
             const bool v = (off <= off_max) & (((uint32_t)off & lmask) == lconst);
             inval |= !v;
             const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
+            mark(key);
             if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
             else atomicAdd(tab + key, 1ull << (32 * (e >> 15)));
           }
         }
       };
-      if (hot_n) fold(std::true_type{});
-      else fold(std::false_type{});
+      if (a.chunk_bits) {
+        if (hot_n) fold(std::true_type{}, std::true_type{});
+        else fold(std::false_type{}, std::true_type{});
+      } else {
+        if (hot_n) fold(std::true_type{}, std::false_type{});
+        else fold(std::false_type{}, std::false_type{});
+      }
       if (inval) flags |= F_ADDR_HINT;
     }
     for (uint32_t m = DENSE ? 0u : (rd16 | wr16); m; m &= m - 1) {

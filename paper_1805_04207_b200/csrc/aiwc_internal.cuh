@@ -31,6 +31,32 @@ constexpr uint64_t E32_MAX_ACCESSES = 1ull << 30;
 // dense-table keys travel as 31-bit list entries in the ingest; key n_keys is the
 // sentinel slot that addresses outside the declared statistics are counted into
 constexpr uint64_t DENSE_MAX_KEYS = (1ull << 31) - 1;
+// table entries allocated for n_keys keys: + the sentinel slot, rounded up to whole
+// 1024-key chunks (the exchange unit of the multi-GPU dense path)
+__host__ __device__ constexpr uint64_t dense_alloc_keys(uint64_t n_keys) { return (n_keys + 1 + 1023) & ~1023ull; }
+
+// Multi-GPU dense exchange (aiwc_exchange.cu): all_bits holds every rank's bitmap of
+// touched 1024-key chunks ([nranks][words]).  A chunk touched by exactly one rank is
+// owned by it; any other chunk by a hash of its index.
+__device__ __forceinline__ uint32_t chunk_owner(const uint32_t* all_bits, uint64_t words, uint64_t c,
+                                                uint32_t nranks) {
+  const uint64_t w = c >> 5;
+  const uint32_t b = 1u << (c & 31);
+  uint32_t cnt = 0, who = 0;
+  for (uint32_t r = 0; r < nranks; ++r)
+    if (all_bits[(uint64_t)r * words + w] & b) { ++cnt; who = r; }
+  if (cnt == 1) return who;
+  uint32_t h = (uint32_t)c * 0x9E3779B1u ^ (uint32_t)(c >> 32);
+  h ^= h >> 15; h *= 0x85EBCA77u; h ^= h >> 13;
+  return h % nranks;
+}
+// owned by `rank` and touched by some rank (the chunks rank's statistics sweep)
+__device__ __forceinline__ bool chunk_is_owned(const uint32_t* all_bits, uint64_t words, uint64_t c, uint32_t rank,
+                                               uint32_t nranks) {
+  uint32_t any = 0;
+  for (uint32_t r = 0; r < nranks; ++r) any |= all_bits[(uint64_t)r * words + (c >> 5)];
+  return ((any >> (c & 31)) & 1u) && chunk_owner(all_bits, words, c, nranks) == rank;
+}
 
 // ---- kind-byte classes (include/aiwc_b200.h) -------------------------------
 __host__ __device__ constexpr bool is_instr(uint32_t k) { return k & 0x01; }
@@ -124,6 +150,7 @@ struct IngestArgs {
   uint64_t* rd_out;                 // compact mode
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
+  uint32_t* chunk_bits;             // shard dense exchange: bit c = this rank touched keys [1024 c, 1024 c + 1024)
 };
 
 // ---- stream validation (aiwc_validate.cu) ---------------------------------------
@@ -241,7 +268,17 @@ void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
-                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s);
+                        double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s,
+                        const uint32_t* own_bits = nullptr, uint64_t own_words = 0, uint32_t rank = 0,
+                        uint32_t nranks = 1);  // own_bits: only the chunks `rank` owns
+// multi-GPU dense exchange (aiwc_exchange.cu); return kernel counts
+int launch_pack(const void* tab, bool e32, const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
+                int pass, unsigned long long* cursor, uint64_t* out, uint32_t n_sms, cudaStream_t s);
+int launch_apply_runs(void* tab, bool e32, const uint64_t* runs, uint64_t n_runs, uint64_t n_keys,
+                      const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
+                      unsigned long long* flags, uint32_t n_sms, cudaStream_t s);
+int launch_clear_chunks(void* tab, bool e32, uint64_t n_keys, const uint32_t* all_bits, uint64_t words, uint32_t rank,
+                        uint32_t nranks, uint32_t* my_bits, uint32_t n_sms, cudaStream_t s);
 void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_parts, uint64_t total_m, uint32_t k,
                            cudaStream_t s);
 // sparse memory path; returns kernel count

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -193,6 +194,34 @@ def allreduce_stats(stats, group, device):
             int(np.bitwise_or.reduce(v[:, 3])))
 
 
+PROFILE = os.environ.get("AIWC_SHARD_PROFILE") == "1"  # section timings of sharded_result (synchronizing)
+LAST_PROFILE: dict = {}
+
+
+class _Sections:
+    """Wall-clock sections of one sharded_result with a device sync at each mark
+    (measurement only: AIWC_SHARD_PROFILE=1)."""
+
+    def __init__(self, device):
+        import time
+
+        self.t = time.perf_counter
+        self.device = device
+        self.last = self.t() if PROFILE else 0.0
+        LAST_PROFILE.clear()
+
+    def mark(self, name: str) -> None:
+        if not PROFILE:
+            return
+        import torch
+
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+        now = self.t()
+        LAST_PROFILE[name] = LAST_PROFILE.get(name, 0.0) + (now - self.last) * 1e3
+        self.last = now
+
+
 RUNS_TABLE_BUDGET = 16 << 30  # bytes of one owner's dense table in the run exchange
 LAST_EXCHANGE = None  # "runs" or "raw": the address exchange the last sharded_result used
 RUN_MIN_AVG = 32      # accesses per run below which the raw exchange is used
@@ -227,56 +256,105 @@ def comm_device(backend, group=None):
     return torch.device("cpu") if dist.get_backend(group) == "gloo" else backend.device
 
 
-def sharded_result(backend, shard, shard_offset: int, group=None):
-    """Every rank: exact whole-trace EngineResult from its work-group shard.
+def combine_stats(rows) -> tuple:
+    """The job's aiwc_shard_stats from every rank's: (min, max, and, or) over ranks
+    with accesses, the summed access count, the smallest dense-table budget, the
+    summed branch count."""
+    rows = [tuple(int(v) for v in r) for r in rows]
+    live = [r for r in rows if r[4]]
+    m = sum(r[4] for r in rows)
+    budget = min(r[5] for r in rows)
+    n_br = sum(r[6] for r in rows)
+    if not live:
+        return ((1 << 64) - 1, 0, (1 << 64) - 1, 0, 0, budget, n_br)
+    aand, aor = (1 << 64) - 1, 0
+    for r in live:
+        aand &= r[2]
+        aor |= r[3]
+    return (min(r[0] for r in live), max(r[1] for r in live), aand, aor, m, budget, n_br)
 
-    Collectives: one object all-gather of the small per-shard partials (counts,
-    opcode / ITB / IPT histograms, overflow and width / site lists, address
-    statistics), the 2^16 branch pattern table all-reduce only when the trace
-    has branches, the address exchange (run-count all-reduce + two all-to-alls),
-    and one object all-gather of the owners' memory partials."""
+
+def chunk_owner(all_bits: np.ndarray, c: int) -> int:
+    """Owner of 1024-key chunk c (aiwc_internal.cuh chunk_owner): the only rank that
+    touched it, else a hash of its index."""
+    nranks = all_bits.shape[0]
+    w, b = c >> 5, np.uint32(1 << (c & 31))
+    touched = [r for r in range(nranks) if int(all_bits[r, w]) & int(b)]
+    if len(touched) == 1:
+        return touched[0]
+    m32 = 0xFFFFFFFF
+    h = ((c * 0x9E3779B1) & m32) ^ ((c >> 32) & m32)
+    h ^= h >> 15
+    h = (h * 0x85EBCA77) & m32
+    h ^= h >> 13
+    return h % nranks
+
+
+def _all_gather_u64(vals: np.ndarray, group, device) -> np.ndarray:
+    """[world, len] of every rank's equal-length u64 vector (one all-gather)."""
+    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    mine = torch.from_numpy(np.ascontiguousarray(vals, dtype=np.uint64).view(np.int64).copy()).to(device)
+    out = torch.empty(world * mine.numel(), dtype=torch.int64, device=device)  # flat: gloo and NCCL alike
+    dist.all_gather_into_tensor(out, mine, group=group)
+    return out.cpu().numpy().view(np.uint64).reshape(world, -1)
+
+
+def sharded_result(backend, shard, shard_offset: int, group=None):
+    """Every rank: exact whole-trace EngineResult from its work-group shard.
+
+    1. pass 1 of the shard; one all-gather of every rank's address statistics and
+       access count fixes the job's key map;
+    2. the ingest fills a dense table over that key map (the single-GPU ingest) and
+       marks the 1024-key chunks it touched; one all-gather of the chunk bitmaps;
+    3. chunks several ranks touched travel to their owner as runs of equal table
+       entries (one all-to-all); the owner sweeps its chunks with the single-GPU
+       statistics kernel;
+    4. one device all-reduce of a packed u64 buffer (scalars, opcode / ITB / IPT /
+       count-of-counts histograms, the 2^H branch pattern table) and one all-gather
+       of the variable parts (overflow lists, width / site lists, fp64 level sums,
+       added in rank order).
+    A job whose key span does not fit a dense table keeps its addresses compacted
+    and exchanges them with key-range owners (runs or raw addresses)."""
+    import torch.distributed as dist
+
+    global LAST_EXCHANGE
+    world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     device = comm_device(backend, group)
-    sp: ShardPartial = backend.shard(shard, shard_offset)
-
-    # ---- small partials: one object all-gather, summed / merged on the host ----
-    scalars = [int(sp.n_events), int(sp.total_instructions), int(sp.work_items), int(sp.barriers_hit),
-               int(sp.total_reads), int(sp.total_writes), int(sp.itb_sum), int(sp.ipt_sum),
-               int(sp.branch_executions)]
-    parts = _gather_objects((scalars, sp.opcode_counts.astype(np.uint64), sp.itb_hist, sp.ipt_hist,
-                             sp.itb_ovf.tolist(), sp.ipt_ovf.tolist(), sp.widths, sp.sites, sp.addr_stats), group)
-    sc = [sum(p[0][i] for p in parts) for i in range(len(scalars))]
-    opcode_counts = [int(v) for v in np.sum([p[1] for p in parts], axis=0)]
-    itb_hist = np.sum([p[2] for p in parts], axis=0).astype(np.uint64)
-    ipt_hist = np.sum([p[3] for p in parts], axis=0).astype(np.uint64)
-    itb_ovf, ipt_ovf, widths, sites = _merge_lists([p[4:8] for p in parts])
-    n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec = sc
-    # ---- branch pattern tables (each (site, group) stream is whole on one rank) ----
-    if br_exec:
-        branch_table = _allreduce_i64(sp.branch_table.astype(np.uint64), dist.ReduceOp.SUM, group, device)
-    else:
-        branch_table = np.zeros(len(sp.branch_table), np.uint64)
-
-    # ---- addresses: global key map, owner exchange, owner partials ----
-    total_m = total_reads + total_writes
-    if total_m:
-        st = [p[8] for p in parts if p[8] is not None]
-        stats = (min(x[0] for x in st), max(x[1] for x in st), int(np.bitwise_and.reduce([np.uint64(x[2]) for x in st])),
-                 int(np.bitwise_or.reduce([np.uint64(x[3]) for x in st])))
-        km = key_map(stats, world)
+    sec = _Sections(getattr(backend, "device", device))
+    local = backend.prepare(shard, shard_offset)
+    sec.mark("prepare")
+    job = combine_stats(_all_gather_u64(np.array(local, np.uint64), group, device))
+    sec.mark("stats_allgather")
+    dense = backend.ingest(job)
+    sec.mark("ingest")
+    sp: ShardPartial = backend.finish()
+    sec.mark("finalize")
+    total_m = job[4]
+    if total_m and dense:
+        LAST_EXCHANGE = "dense"
+        bits = backend.chunk_bits()
+        all_bits = _all_gather_u32(bits, group, device)
+        sec.mark("bitmap_allgather")
+        runs, rcounts = backend.pack(all_bits, rank, world)
+        sec.mark("pack")
+        recv, n_words = exchange(runs, [2 * c for c in rcounts], group, device)
+        sec.mark("alltoall")
+        mp = backend.owned(recv, n_words // 2, all_bits, rank, world, total_m)
+        sec.mark("owned")
+    elif total_m:
+        km = key_map(job[:4], world)
         lo, n_owned = km.owned(rank)
         use_runs = False
         if hasattr(backend, "partition_runs") and runs_dense_ok(km, total_m):
             # pre-aggregation: runs of consecutive keys per owner; chosen (on every
-            # rank alike) when runs average >= RUN_MIN_AVG accesses (the owner
-            # applies one run per warp: short runs would idle its lanes)
+            # rank alike) when runs average >= RUN_MIN_AVG accesses
             runs, rcounts = backend.partition_runs(sp, km, world)
             tot = _allreduce_i64(np.array([sum(rcounts)], np.uint64), dist.ReduceOp.SUM, group, device)
             use_runs = RUN_MIN_AVG * int(tot[0]) <= total_m
-        global LAST_EXCHANGE
         LAST_EXCHANGE = "runs" if use_runs else "raw"
         if use_runs:
             recv, n_words = exchange(runs, [2 * c for c in rcounts], group, device)
@@ -288,21 +366,76 @@ def sharded_result(backend, shard, shard_offset: int, group=None):
             mp = backend.memory_partial(recv_r, n_r, recv_w, n_w, km, lo, n_owned, total_m)
     else:
         mp = MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(CBINS, np.uint64), np.zeros(0, np.uint64))
-    # ---- owners' partials: one object all-gather (level sums added in rank order) ----
-    mparts = _gather_objects((int(mp.unique_reads), int(mp.unique_writes), int(mp.footprint),
-                              np.asarray(mp.level_sum, dtype=np.float64), mp.cnt_hist0.astype(np.uint64),
-                              mp.big.astype(np.uint64)), group)
-    unique_r = sum(m[0] for m in mparts)
-    unique_w = sum(m[1] for m in mparts)
-    footprint = sum(m[2] for m in mparts)
+
+    # ---- one packed all-reduce: every summable integer (the 2^H branch pattern table
+    # only when the job has branches), plus every rank's list lengths in its own row
+    # of a [world, 5] block (zeros elsewhere), so the sum hands everyone all lengths ----
+    n_opc = len(sp.opcode_counts)
+    scalars = np.array([sp.n_events, sp.total_instructions, sp.work_items, sp.barriers_hit, sp.total_reads,
+                        sp.total_writes, sp.itb_sum, sp.ipt_sum, sp.branch_executions, mp.unique_reads,
+                        mp.unique_writes, mp.footprint], dtype=np.uint64)
+    lens = np.zeros((world, 5), np.uint64)
+    lens[rank] = (len(sp.itb_ovf), len(sp.ipt_ovf), len(mp.big), len(sp.widths), len(sp.sites))
+    has_br = job[6] > 0
+    packed = np.concatenate([scalars, np.asarray(sp.opcode_counts, np.uint64), np.asarray(sp.itb_hist, np.uint64),
+                             np.asarray(sp.ipt_hist, np.uint64), np.asarray(mp.cnt_hist0, np.uint64),
+                             lens.reshape(-1), np.asarray(sp.branch_table, np.uint64) if has_br else
+                             np.zeros(0, np.uint64)])
+    tot = _allreduce_i64(packed, dist.ReduceOp.SUM, group, device)
+    sec.mark("packed_allreduce")
+    o = 0
+
+    def take(n):
+        nonlocal o
+        o += n
+        return tot[o - n:o]
+
+    (n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec, unique_r,
+     unique_w, footprint) = (int(v) for v in take(len(scalars)))
+    opcode_counts = [int(v) for v in take(n_opc)]
+    itb_hist, ipt_hist, hist0 = take(HBINS).copy(), take(HBINS).copy(), take(CBINS).copy()
+    all_lens = take(5 * world).reshape(world, 5).astype(np.int64)
+    branch_table = take(len(sp.branch_table)).copy() if has_br else np.zeros(len(sp.branch_table), np.uint64)
+
+    # ---- one all-gather of the variable parts (blobs padded to the longest) ----
+    blob = np.concatenate([
+        np.asarray(mp.level_sum, np.float64).view(np.uint64),
+        np.asarray(sp.itb_ovf, np.uint64), np.asarray(sp.ipt_ovf, np.uint64), np.asarray(mp.big, np.uint64),
+        np.array([v for w in sp.widths for v in w], np.uint64),
+        np.array([v for it in sorted(sp.sites.items()) for v in it], np.uint64)])
     level_sum = np.zeros(11)
-    for m in mparts:
-        level_sum = level_sum + m[3]
-    hist0 = np.sum([m[4] for m in mparts], axis=0).astype(np.uint64)
-    big = np.sort(np.concatenate([m[5] for m in mparts]).astype(np.uint64))[::-1]
+    lists, bigs = [], []
+    width = int(max(11 + n[0] + n[1] + n[2] + 3 * n[3] + 2 * n[4] for n in all_lens))
+    padded = np.zeros(width, np.uint64)
+    padded[:blob.size] = blob
+    for r, b in enumerate(_all_gather_u64(padded, group, device)):
+        n_i, n_p, n_b, n_w, n_s = (int(v) for v in all_lens[r])
+        level_sum = level_sum + b[:11].view(np.float64)  # rank order: deterministic
+        q = 11
+        itb_o = b[q:q + n_i]; q += n_i
+        ipt_o = b[q:q + n_p]; q += n_p
+        bigs.append(b[q:q + n_b]); q += n_b
+        widths = [tuple(int(x) for x in b[q + 3 * i:q + 3 * i + 3]) for i in range(n_w)]; q += 3 * n_w
+        sites = {int(b[q + 2 * i]): int(b[q + 2 * i + 1]) for i in range(n_s)}
+        lists.append((itb_o.tolist(), ipt_o.tolist(), widths, sites))
+    itb_ovf, ipt_ovf, widths, sites = _merge_lists(lists)
+    big = np.sort(np.concatenate(bigs).astype(np.uint64))[::-1]
+    sec.mark("lists_allgather")
     return _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum,
                      br_exec, opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, branch_table, widths, sites,
                      unique_r, unique_w, footprint, hist0, big, level_sum)
+
+
+def _all_gather_u32(bits, group, device) -> object:
+    """[world, words] int32 tensor of every rank's chunk bitmap (on the collective device)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    mine = bits.to(device)
+    out = torch.empty(world * mine.numel(), dtype=mine.dtype, device=device)
+    dist.all_gather_into_tensor(out, mine.contiguous(), group=group)
+    return out.view(world, -1)
 
 
 def _assemble(n_events, total_instr, work_items, barriers, total_reads, total_writes, itb_sum, ipt_sum, br_exec,
@@ -437,6 +570,92 @@ def sharded_report(backend, shard, shard_offset: int, kernel_name: str, invocati
 
 
 # ---------------------------------------------------------------------------
+# job mode: NCCL inside the engine (aiwc_ctx_set_comm) -- the multi-GPU product path
+# ---------------------------------------------------------------------------
+class NcclJob:
+    """One engine context joined to the job's NCCL communicator.  torch.distributed
+    only bootstraps it (rank 0's ncclUniqueId is broadcast once); from then on
+    `result` is aiwc_ingest of this rank's shard + aiwc_finalize, and every
+    collective of the exchange and the combine runs inside the engine (no Python
+    between them).  One NcclJob per concurrent trace stream (its own communicator)."""
+
+    def __init__(self, device_index: int = 0, group=None, timing: bool = False, dense_budget_bytes: int = 0):
+        import torch.distributed as dist
+
+        from . import _native
+
+        self.device_index = device_index
+        flags = _native.OPT_NO_CONSERVATION | (_native.OPT_TIMING if timing else 0)
+        # dense_budget_bytes=1 (tests) forces the compacted-address exchange
+        self.ctx = _native.Context(device_index, flags=flags, dense_budget_bytes=dense_budget_bytes)
+        lib = self.ctx.lib
+        uid = (ctypes.c_uint8 * 128)()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        if rank == 0:
+            self.ctx.check(lib.aiwc_nccl_unique_id(uid))
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        import torch
+
+        torch.cuda.set_device(device_index)
+        self.ctx.check(lib.aiwc_ctx_set_comm(self.ctx.h, uid, rank, world))
+        self.rank, self.world = rank, world
+        self.last_phase_ms: list = []
+        self.last_d2h = 0
+        self.launches = 0
+
+    def result(self, shard, shard_offset: int):
+        """The whole job's EngineResult from this rank's work-group shard."""
+        from . import _native
+        from .metrics import _copy_result, _is_torch, trace_info
+
+        ctx = self.ctx
+        lib = ctx.lib
+        ctx.check(lib.aiwc_reset(ctx.h))
+        info = trace_info(shard)
+        info.first_event = shard_offset
+        kind, payload = shard.kind, shard.payload
+        if _is_torch(kind) and kind.is_cuda:
+            import torch
+
+            kind, payload = kind.contiguous(), payload.contiguous()
+            stream = torch.cuda.current_stream(kind.device).cuda_stream
+            ctx.check(lib.aiwc_ingest(ctx.h, ctypes.c_void_p(kind.data_ptr()), ctypes.c_void_p(payload.data_ptr()),
+                                      ctypes.byref(info), ctypes.c_void_p(stream)))
+        else:
+            if _is_torch(kind):
+                kind, payload = kind.numpy(), payload.numpy()
+            kind = np.ascontiguousarray(kind, dtype=np.uint8)
+            payload = np.ascontiguousarray(payload).view(np.uint64)
+            import torch
+
+            stream = torch.cuda.current_stream(self.device_index).cuda_stream
+            ctx.check(lib.aiwc_ingest_host(ctx.h, kind.ctypes.data_as(ctypes.c_void_p),
+                                           payload.ctypes.data_as(ctypes.c_void_p), ctypes.byref(info),
+                                           ctypes.c_void_p(stream)))
+        res = _native.Result()
+        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream)))
+        self.last_phase_ms = list(res.phase_ms)
+        self.last_d2h = res.d2h_bytes
+        self.launches += res.kernels_launched
+        return _copy_result(res)
+
+    def report(self, shard, shard_offset: int, kernel_name: str, invocation: int, global_size, local_size,
+               opcodes: list[str]):
+        """AiwcReport of the whole trace, identical on every rank."""
+        from .metrics import KernelAccumulator, finalize
+
+        res = self.result(shard, shard_offset)
+        acc = KernelAccumulator(kernel_name, [invocation], [(invocation, tuple(global_size), tuple(local_size))], res,
+                                list(opcodes))
+        return finalize(acc)
+
+    def close(self):
+        self.ctx.close()
+
+
+# ---------------------------------------------------------------------------
 # CUDA backend: the C ABI on this rank's GPU
 # ---------------------------------------------------------------------------
 class _CudaArray:
@@ -454,6 +673,7 @@ class CudaBackend:
 
     device_index: int = 0
     timing: bool = False
+    force_compact: bool = False  # tests: take the compacted-address exchange even when a dense table fits
     ctx: object = None
     last_phase_ms: list = field(default_factory=list)
     last_d2h: int = 0
@@ -473,22 +693,105 @@ class CudaBackend:
             self.ctx = _native.Context(self.device_index, flags=flags)
         return self.ctx
 
-    def shard(self, tr, shard_offset: int) -> ShardPartial:
+    # ---- the dense exchange (aiwc_shard_*) ----
+    def prepare(self, tr, shard_offset: int) -> tuple:
+        """Pass 1 of the shard (device columns; host columns are copied first): its
+        aiwc_shard_stats as six ints."""
+        import torch
+
         from . import _native
-        from .metrics import _copy_result, ingest_columns
+        from .metrics import _device_columns, trace_info
 
         ctx = self._ctx()
-        lib = ctx.lib
-        ctx.check(lib.aiwc_reset(ctx.h))
-        stream = ingest_columns(ctx, tr)
+        ctx.check(ctx.lib.aiwc_reset(ctx.h))
+        dtr = _device_columns(tr, self.device_index)
+        kind, payload = dtr.kind.contiguous(), dtr.payload.contiguous()
+        if kind.data_ptr() % 16:
+            kind = kind.clone()
+        if payload.data_ptr() % 16:
+            payload = payload.clone()
+        self._cols = (kind, payload)  # alive until the ingest has run
+        self._offset = shard_offset
+        self._stream = torch.cuda.current_stream(self.device).cuda_stream
+        out = _native.ShardStats()
+        info = trace_info(dtr)
+        ctx.check(ctx.lib.aiwc_shard_prepare(ctx.h, ctypes.c_void_p(kind.data_ptr()), ctypes.c_void_p(payload.data_ptr()),
+                                             ctypes.byref(info), ctypes.byref(out), ctypes.c_void_p(self._stream)))
+        return (out.addr_min, out.addr_max, out.addr_and, out.addr_or, out.n_accesses, out.dense_budget_bytes,
+                out.n_branches)
+
+    def ingest(self, job: tuple) -> bool:
+        from . import _native
+
+        ctx = self._ctx()
+        st = _native.ShardStats(*[int(v) for v in job[:5]], 0 if self.force_compact else int(job[5]), int(job[6]))
+        dense = ctypes.c_uint32(0)
+        ctx.check(ctx.lib.aiwc_shard_ingest(ctx.h, ctypes.byref(st), ctypes.byref(dense), ctypes.c_void_p(self._stream)))
+        return bool(dense.value)
+
+    def finish(self) -> ShardPartial:
+        from . import _native
+
+        ctx = self._ctx()
         res = _native.Result()
-        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
+        ctx.check(ctx.lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(self._stream)))
+        self._cols = None
+        return self._partial(res, self._offset)
+
+    def chunk_bits(self):
+        import torch
+
+        ctx = self._ctx()
+        p, n = ctypes.c_void_p(), ctypes.c_uint64()
+        ctx.check(ctx.lib.aiwc_shard_chunks(ctx.h, ctypes.byref(p), ctypes.byref(n)))
+        iface = {"shape": (max(int(n.value), 1),), "typestr": "<i4", "data": (p.value, False), "version": 3}
+        holder = type("_Bits", (), {"__cuda_array_interface__": iface})()
+        return torch.as_tensor(holder, device=self.device)[: int(n.value)]
+
+    def pack(self, all_bits, rank: int, nranks: int):
+        import torch
+
+        ctx = self._ctx()
+        all_bits = all_bits.to(self.device).contiguous()
+        counts = (ctypes.c_uint64 * nranks)()
+        rp = ctypes.c_void_p()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_shard_pack(ctx.h, ctypes.c_void_p(all_bits.data_ptr()), rank, nranks, ctypes.byref(rp),
+                                          counts, ctypes.c_void_p(stream)))
+        c = [int(x) for x in counts]
+        self.launches += 1 + int(sum(c) > 0)
+        runs = torch.as_tensor(_CudaArray(rp.value, max(2 * sum(c), 1)), device=self.device)
+        return runs, c
+
+    def owned(self, recv, n_runs: int, all_bits, rank: int, nranks: int, total_m: int) -> MemoryPartial:
+        import torch
+
+        from . import _native
+
+        ctx = self._ctx()
+        out = _native.MemoryPart()
+        recv = recv.to(self.device)
+        all_bits = all_bits.to(self.device).contiguous()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        ctx.check(ctx.lib.aiwc_shard_owned(ctx.h, ctypes.c_void_p(recv.data_ptr()), n_runs,
+                                           ctypes.c_void_p(all_bits.data_ptr()), rank, nranks, total_m,
+                                           ctypes.byref(out), ctypes.c_void_p(stream)))
+        self.launches += out.kernels_launched
+        big = np.ctypeslib.as_array(out.big, shape=(out.n_big,)).copy() if out.n_big else np.zeros(0, np.uint64)
+        return MemoryPartial(out.unique_reads, out.unique_writes, out.footprint, np.array(out.level_sum[:]),
+                             np.ctypeslib.as_array(out.cnt_hist0, shape=(CBINS,)).copy(), big)
+
+    def _partial(self, res, shard_offset: int) -> ShardPartial:
+        from . import _native
+        from .metrics import _copy_result
+
+        ctx = self._ctx()
         self.last_phase_ms = list(res.phase_ms)
         self.last_d2h = res.d2h_bytes
         self.launches += res.kernels_launched
         r = _copy_result(res)
         t = _native.ShardTables()
-        ctx.check(lib.aiwc_shard_tables_get(ctx.h, ctypes.byref(t)))
+        ctx.check(ctx.lib.aiwc_shard_tables_get(ctx.h, ctypes.byref(t)))
         arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint64)  # noqa: E731
         firsts = arr(t.width_first, len(r.widths))
         return ShardPartial(
@@ -502,6 +805,19 @@ class CudaBackend:
             sites=dict(r.sites), branch_executions=r.branch_executions,
             addr_stats=tuple(int(v) for v in t.addr_stats) if (r.total_reads + r.total_writes) else None,
         )
+
+    # ---- one ingest of a whole (sub)trace in shard mode: compacted addresses (chunked_result) ----
+    def shard(self, tr, shard_offset: int) -> ShardPartial:
+        from . import _native
+        from .metrics import ingest_columns
+
+        ctx = self._ctx()
+        lib = ctx.lib
+        ctx.check(lib.aiwc_reset(ctx.h))
+        stream = ingest_columns(ctx, tr)
+        res = _native.Result()
+        ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
+        return self._partial(res, shard_offset)
 
     def addresses(self, sp: ShardPartial):
         """Zero-copy device views of the last shard's compacted read / write addresses."""

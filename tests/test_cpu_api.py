@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     lib = _native.load_library()
     for name in sorted(declared):
         assert hasattr(lib, name), name
-    assert lib.aiwc_abi_version() == 1
+    assert lib.aiwc_abi_version() == 2
 
 
 def test_result_struct_matches_header_layout():

@@ -19,12 +19,97 @@ CASES = ["wavefront_big", "bfs_flags", "sweep4", "long_segments", "hot_address",
 
 
 class OracleBackend:
-    """Test double for dist.CudaBackend: the C oracle's accumulator + numpy."""
+    """Test double for dist.CudaBackend: the C oracle's accumulator + numpy.  The
+    dense exchange keeps a {key: (reads, writes)} table over the job's key map and
+    packs every key of a chunk owned elsewhere as a one-key run (runs need not be
+    maximal); force_compact takes the compacted-address exchange instead."""
 
     device = torch.device("cpu")
 
-    def __init__(self, n_opcodes):
+    def __init__(self, n_opcodes, force_compact=False):
         self.n_opcodes = n_opcodes
+        self.force_compact = force_compact
+
+    # ---- dense exchange ----
+    def prepare(self, tr, offset):
+        self.sp = self.shard(tr, offset)
+        m = self.sp.total_reads + self.sp.total_writes
+        st = self.sp.addr_stats or ((1 << 64) - 1, 0, (1 << 64) - 1, 0)
+        return (*st, m, 1 << 40, self.sp.branch_executions)
+
+    def ingest(self, job):
+        from paper_1805_04207_b200.dist import key_map
+
+        self.km = key_map(job[:4], 1)
+        m = job[4]
+        if self.force_compact or not m or self.km.n_keys > 4 * m + (1 << 20) or self.km.n_keys >= (1 << 31) - 2:
+            return False
+        rd_a, rd_c, wr_a, wr_c = self.sp.handle
+        tab = {}
+        for a, c, w in ((rd_a, rd_c, 0), (wr_a, wr_c, 1)):
+            for key, n in zip(((a - np.uint64(self.km.base)) >> np.uint64(self.km.k)).tolist(), c.tolist()):
+                r0, w0 = tab.get(key, (0, 0))
+                tab[key] = (r0 + (0 if w else n), w0 + (n if w else 0))
+        self.tab = tab
+        return True
+
+    def finish(self):
+        return self.sp
+
+    def chunk_bits(self):
+        words = ((self.km.n_keys + 1 + 1023) // 1024 + 31) // 32
+        bits = np.zeros(words, np.uint32)
+        for key in self.tab:
+            c = key >> 10
+            bits[c >> 5] |= np.uint32(1 << (c & 31))
+        return torch.from_numpy(bits.view(np.int32).copy())
+
+    def pack(self, all_bits, rank, nranks):
+        from paper_1805_04207_b200.dist import chunk_owner
+
+        ab = all_bits.numpy().view(np.uint32)
+        by_owner = [[] for _ in range(nranks)]
+        for key in sorted(self.tab):
+            o = chunk_owner(ab, key >> 10)
+            if o != rank:
+                r, w = self.tab[key]
+                by_owner[o].append((key | (1 << 32), r | (w << 32)))
+        flat = [v for lst in by_owner for run in lst for v in run]
+        arr = np.array(flat, dtype=np.uint64) if flat else np.zeros(1, np.uint64)
+        return torch.from_numpy(arr.view(np.int64).copy()), [len(lst) for lst in by_owner]
+
+    def owned(self, recv, n_runs, all_bits, rank, nranks, total_m):
+        from paper_1805_04207_b200.dist import chunk_owner
+
+        ab = all_bits.numpy().view(np.uint32)
+        tot = {k: v for k, v in self.tab.items() if chunk_owner(ab, k >> 10) == rank}
+        r = recv[: 2 * n_runs].numpy().view(np.uint64).reshape(-1, 2)
+        for w0, v in r.tolist():
+            key, n = w0 & 0xFFFFFFFF, w0 >> 32
+            assert chunk_owner(ab, key >> 10) == rank
+            for i in range(n):
+                r0, w_0 = tot.get(key + i, (0, 0))
+                tot[key + i] = (r0 + (v & 0xFFFFFFFF), w_0 + (v >> 32))
+        return self._partial_from_counts(tot, self.km, total_m)
+
+    def _partial_from_counts(self, tot, km, total_m):
+        from paper_1805_04207_b200.dist import CBINS, MemoryPartial
+
+        keys = np.array(sorted(tot), dtype=np.uint64)
+        rw = np.array([tot[int(k)] for k in keys], dtype=np.int64).reshape(-1, 2)
+        c = rw.sum(axis=1) if keys.size else np.zeros(0, np.int64)
+        sums = []
+        for lvl in range(11):
+            j = max(0, lvl - km.k)
+            if not keys.size:
+                sums.append(0.0)
+                continue
+            g = np.unique(keys >> np.uint64(j), return_inverse=True)[1]
+            p = np.bincount(g, weights=c) / total_m
+            sums.append(float((p * np.log2(p)).sum()))
+        return MemoryPartial(int((rw[:, 0] > 0).sum()) if keys.size else 0, int((rw[:, 1] > 0).sum()) if keys.size else 0,
+                             int(keys.size), np.array(sums), np.bincount(c[c < CBINS], minlength=CBINS).astype(np.uint64),
+                             c[c >= CBINS].astype(np.uint64))
 
     def shard(self, tr, offset):
         from oracle import oracle
@@ -159,9 +244,10 @@ def _worker(rank, world, port, names, q):
             lo, hi = cuts[rank], cuts[rank + 1]
             shard = ColumnarTrace(tr.kind[lo:hi], tr.payload[lo:hi], tr.kernel_name, tr.invocation, tr.global_size,
                                   tr.local_size, tr.opcodes, tr.extra_groups)
-            rep = D.sharded_report(OracleBackend(len(tr.opcodes)), shard, lo, tr.kernel_name, tr.invocation,
-                                   tr.global_size, tr.local_size, tr.opcodes)
-            q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
+            for compact in (False, True):
+                rep = D.sharded_report(OracleBackend(len(tr.opcodes), compact), shard, lo, tr.kernel_name,
+                                       tr.invocation, tr.global_size, tr.local_size, tr.opcodes)
+                q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
     finally:
         dist.destroy_process_group()
 
@@ -177,7 +263,7 @@ def test_sharded_reports_match_reference(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, CASES, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got = [q.get(timeout=240) for _ in range(world * len(CASES))]
+    got = [q.get(timeout=240) for _ in range(2 * world * len(CASES))]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -186,7 +272,7 @@ def test_sharded_reports_match_reference(world):
     for rank, name, rep, mode in got:
         assert_report_matches(rep, want[name])
         modes.add(mode)
-    assert {"runs", "raw"} <= modes  # both address exchanges were exercised
+    assert {"dense", "runs", "raw"} <= modes  # every address exchange was exercised
 
 
 def test_key_map_owner_ranges_are_block_aligned():

@@ -46,7 +46,7 @@ def _worker(rank, world, port, q):
     torch.cuda.set_device(0)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    backend = D.CudaBackend(0)
+    backends = (D.CudaBackend(0), D.CudaBackend(0, force_compact=True))
     try:
         by_name = {c["name"]: (c, t) for c, t in gc()}
         for name in GOLDEN:
@@ -58,15 +58,17 @@ def _worker(rank, world, port, q):
                                   torch.from_numpy(tr.payload[lo:hi].view(np.int64).copy()).cuda(),
                                   tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
                                   tr.extra_groups)
-            rep = D.sharded_report(backend, shard, lo, tr.kernel_name, tr.invocation, tr.global_size,
-                                   tr.local_size, tr.opcodes)
-            q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
+            for backend in backends:
+                rep = D.sharded_report(backend, shard, lo, tr.kernel_name, tr.invocation, tr.global_size,
+                                       tr.local_size, tr.opcodes)
+                q.put((rank, name, report_to_dict(rep), D.LAST_EXCHANGE))
         for cfg, w in SYNTH:
             first, count = synth.shard_range(cfg, w, rank, world)
             shard = synth.device_trace(cfg, w, first=first, count=count)
-            rep = D.sharded_report(backend, shard, first, shard.kernel_name, 0, shard.global_size,
-                                   shard.local_size, shard.opcodes)
-            q.put((rank, f"C{cfg}", report_to_dict(rep), D.LAST_EXCHANGE))
+            for backend in backends:
+                rep = D.sharded_report(backend, shard, first, shard.kernel_name, 0, shard.global_size,
+                                       shard.local_size, shard.opcodes)
+                q.put((rank, f"C{cfg}", report_to_dict(rep), D.LAST_EXCHANGE))
     finally:
         dist.destroy_process_group()
 
@@ -81,7 +83,7 @@ def test_sharded_cuda_backend_matches_whole_trace(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    n = world * (len(GOLDEN) + len(SYNTH))
+    n = 2 * world * (len(GOLDEN) + len(SYNTH))
     got = [q.get(timeout=300) for _ in range(n)]
     for p in procs:
         p.join(timeout=60)
@@ -93,4 +95,69 @@ def test_sharded_cuda_backend_matches_whole_trace(world):
     for rank, name, rep, mode in got:
         assert_report_matches(rep, want[name])
         modes.add(mode)
-    assert {"runs", "raw"} <= modes  # both address exchanges ran through the CUDA engine
+    assert {"dense", "runs", "raw"} <= modes  # every address exchange ran through the CUDA engine
+
+
+def _job_worker(port, q):
+    """World 1 over NCCL: the engine's job mode (aiwc_ctx_set_comm) end to end --
+    stats all-gather, dense chunk exchange or key-range owners, packed all-reduce,
+    list all-gather, the C++ combine."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch.distributed as dist
+
+    from conftest import golden_cases as gc
+    from paper_1805_04207_b200 import dist as D
+    from paper_1805_04207_b200 import report_to_dict, synth
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    torch.cuda.set_device(0)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    jobs = {"dense": D.NcclJob(0), "compact": D.NcclJob(0, dense_budget_bytes=1)}
+    try:
+        by_name = {c["name"]: (c, t) for c, t in gc()}
+        for name in GOLDEN:
+            c, tr = by_name[name]
+            shard = ColumnarTrace(torch.from_numpy(tr.kind.copy()).cuda(),
+                                  torch.from_numpy(tr.payload.view(np.int64).copy()).cuda(),
+                                  tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
+                                  tr.extra_groups)
+            for mode, job in jobs.items():
+                rep = job.report(shard, 0, tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes)
+                q.put((mode, name, report_to_dict(rep)))
+        for cfg, w in SYNTH:
+            shard = synth.device_trace(cfg, w)
+            for mode, job in jobs.items():
+                rep = job.report(shard, 0, shard.kernel_name, 0, shard.global_size, shard.local_size, shard.opcodes)
+                q.put((mode, f"C{cfg}", report_to_dict(rep)))
+        q.put(("done", "", {}))
+    finally:
+        for job in jobs.values():
+            job.close()
+        dist.destroy_process_group()
+
+
+def test_nccl_job_mode_matches_whole_trace():
+    from paper_1805_04207_b200 import consume, finalize, report_to_dict, synth
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_job_worker, args=(_free_port(), q))
+    p.start()
+    got = []
+    while True:
+        item = q.get(timeout=300)
+        if item[0] == "done":
+            break
+        got.append(item)
+    p.join(timeout=60)
+    assert p.exitcode == 0
+    want = {c["name"]: c["report"] for c, _ in golden_cases() if c["name"] in GOLDEN}
+    for cfg, w in SYNTH:
+        want[f"C{cfg}"] = report_to_dict(finalize(consume(synth.device_trace(cfg, w))))
+    assert len(got) == 2 * (len(GOLDEN) + len(SYNTH))
+    for mode, name, rep in got:
+        assert_report_matches(rep, want[name])
