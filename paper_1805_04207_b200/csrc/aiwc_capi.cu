@@ -97,16 +97,29 @@ __device__ __forceinline__ uint32_t reg_hash(uint64_t r) {
 __global__ void region_mark_kernel(const uint8_t* __restrict__ kind, const uint64_t* __restrict__ payload, uint64_t n,
                                    unsigned long long* keys, uint32_t* misc) {
   uint64_t last = REG_EMPTY;
+  uint32_t since_poll = 0;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    // once the table overflowed the answer is known (the sort path): stop early
+    if (++since_poll == 64) {
+      since_poll = 0;
+      if (*(volatile uint32_t*)&misc[1]) return;
+    }
     if (!is_mem(kind[i])) continue;
     const uint64_t r = payload[i] >> REG_SHIFT;
     if (r == last) continue;
     last = r;
     uint32_t h = reg_hash(r);
     for (uint32_t probe = 0;; ++probe, h = (h + 1) & (REG_SLOTS - 1)) {
-      if (probe == 64) { atomicOr(&misc[1], 1u); break; }
+      if (probe == 64) { atomicOr(&misc[1], 1u); return; }
+      // a plain load first: the region is usually present already (no CAS serialisation)
+      const unsigned long long cur = *(volatile unsigned long long*)&keys[h];
+      if (cur == r) break;
+      if (cur != REG_EMPTY) continue;
       const unsigned long long old = atomicCAS(&keys[h], REG_EMPTY, (unsigned long long)r);
-      if (old == REG_EMPTY) { if (atomicAdd(&misc[0], 1u) >= REG_MAX) atomicOr(&misc[1], 1u); break; }
+      if (old == REG_EMPTY) {
+        if (atomicAdd(&misc[0], 1u) >= REG_MAX) { atomicOr(&misc[1], 1u); return; }
+        break;
+      }
       if (old == r) break;
     }
   }
@@ -317,6 +330,11 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
 
 extern "C" int aiwc_reset(aiwc_ctx* ctx) {
   if (!ctx) return AIWC_ERR_ARGUMENT;
+  if (ctx->remap_pay.p) {  // a region-compacted column is per trace: do not keep ~8 B / event allocated
+    cudaSetDevice(ctx->device);
+    cudaFree(ctx->remap_pay.p);
+    ctx->remap_pay = Buf{};
+  }
   ctx->state = 0;
   ctx->err = aiwc_error{};
   return AIWC_OK;
@@ -401,6 +419,12 @@ static int region_compact(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* pa
   for (uint32_t i = 0; i < REG_SLOTS; ++i)
     if (hk[i] != REG_EMPTY) hv[i] = (uint32_t)(std::lower_bound(regs.begin(), regs.end(), hk[i]) - regs.begin());
   CK(cudaMemcpyAsync(ctx->reg_vals.p, hv.data(), REG_SLOTS * 4, cudaMemcpyHostToDevice, s));
+  // the remapped span (regions squeezed together) must then fit the dense rule, or
+  // the remap would be wasted: decide from the region count before writing anything
+  // (the remap keeps the low REG_SHIFT bits: min(k, REG_SHIFT) of them stay constant)
+  const uint64_t span_keys = ((uint64_t)regs.size() << REG_SHIFT) >> std::min<uint32_t>(ctx->am.k, REG_SHIFT);
+  const uint64_t M = ctx->n_rd + ctx->n_wr;
+  if (span_keys > 4 * M + (1ull << 20) || span_keys * 4 > ctx->opts.dense_budget_bytes) return AIWC_OK;
   if (grow(ctx->remap_pay, (n + 1) * 8) != cudaSuccess) {  // no room for the remapped column: sparse path
     cudaGetLastError();
     return AIWC_OK;
@@ -846,6 +870,14 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
                       h.p1_tot[3] == in.n_branches && h.p1_tot[4] == in.n_groups &&
                       (h.p1_tot[5] != 0) == (in.any_barrier_or_resume != 0);
     if (!same) return fail(ctx, AIWC_ERR_ARGUMENT, "declared class counts differ from the trace");
+  }
+  // compacted (sort-path) addresses: the ingest measured their statistics; a declared
+  // hint the keys were built from must cover them (the dense path checks per access)
+  if (!ctx->dense && ctx->info.has_addr_stats && ctx->n_rd + ctx->n_wr && h.addr_min <= h.addr_max) {
+    const AddrMap& am = ctx->am;
+    const bool ok = h.addr_min >= am.base && h.addr_max <= am.hi && ((h.addr_and ^ h.addr_or) & am.low_mask) == 0 &&
+                    ((h.addr_min - am.base) & am.low_mask) == am.low_const;
+    if (!ok) h.flags |= F_ADDR_HINT;
   }
   if (h.flags) {
     char m[160];

@@ -512,6 +512,34 @@ def chunk_cuts(kind, limit: int) -> list[int]:
     return cuts
 
 
+def _check_groups_unique_across(tr, cuts: list[int]) -> None:
+    """A (site, group) branch stream continues across work-groups that repeat the
+    group id (metrics.py:145-152 keys streams by group): split at a cut it would
+    become two streams.  Chunks that share a work-group id are refused."""
+    from .errors import UnsupportedTrace
+    from .trace import K_WG_BEGIN
+
+    if len(cuts) <= 2:
+        return
+    if type(tr.kind).__module__.startswith("torch"):
+        import torch
+
+        keys = []
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            k = tr.kind[lo:hi]
+            keys.append(torch.unique(tr.payload[lo:hi][k == K_WG_BEGIN]))
+        allk = torch.cat(keys)
+        repeated = int(torch.unique(allk).numel()) != int(allk.numel())
+    else:
+        kind, pay = np.asarray(tr.kind), np.asarray(tr.payload)
+        keys = [np.unique(pay[lo:hi][kind[lo:hi] == K_WG_BEGIN]) for lo, hi in zip(cuts[:-1], cuts[1:])]
+        allk = np.concatenate(keys)
+        repeated = np.unique(allk).size != allk.size
+    if repeated:
+        raise UnsupportedTrace("a work-group id repeats in more than one ingest chunk: its branch streams would split "
+                               "at the cut")
+
+
 def chunked_result(backend, tr, cuts: list[int]):
     """One trace larger than one ingest allows, on one GPU: each chunk (whole
     work-groups) is a shard pass; sums and lists combine as across ranks, and the
@@ -520,6 +548,7 @@ def chunked_result(backend, tr, cuts: list[int]):
 
     from .trace import ColumnarTrace
 
+    _check_groups_unique_across(tr, cuts)
     parts, rd, wr = [], [], []
     for lo, hi in zip(cuts[:-1], cuts[1:]):
         sub = ColumnarTrace(tr.kind[lo:hi], tr.payload[lo:hi], tr.kernel_name, tr.invocation, tr.global_size,

@@ -48,3 +48,19 @@ def test_synthetic_chunked_match_single_ingest(cfg, w, monkeypatch):
     monkeypatch.setenv("AIWC_MAX_INGEST_EVENTS", str(tr.n_events // 3))
     got = report_to_dict(finalize(consume(tr, max_entries=1 << 40)))
     assert_report_matches(got, want)
+
+
+def test_repeated_group_id_across_chunks_is_refused(monkeypatch):
+    """A work-group id that repeats on both sides of a cut would split its (site,
+    group) branch stream (metrics.py:145-152): refused, not silently wrong."""
+    from paper_1805_04207_b200 import UnsupportedTrace, consume, finalize, report_to_dict
+    from paper_1805_04207_b200.trace import K_WG_BEGIN
+
+    c, tr = next((c, t) for c, t in golden_cases() if c["name"] == "repeated_group_id")
+    starts = np.nonzero(tr.kind == K_WG_BEGIN)[0].tolist() + [tr.n_events]
+    longest = max(b - a for a, b in zip(starts[:-1], starts[1:]))
+    monkeypatch.setenv("AIWC_MAX_INGEST_EVENTS", str(longest + 2))
+    with pytest.raises(UnsupportedTrace, match="repeats"):
+        finalize(consume(tr, max_entries=1 << 40))
+    monkeypatch.delenv("AIWC_MAX_INGEST_EVENTS")
+    assert_report_matches(report_to_dict(finalize(consume(tr, max_entries=1 << 40))), c["report"])
