@@ -125,6 +125,7 @@ typedef struct {
   uint32_t kernels_launched;                /* engine kernels launched for this trace   */
   uint64_t d2h_bytes;                       /* device->host bytes read for this trace   */
   double phase_ms[AIWC_N_PHASES];           /* with AIWC_OPT_TIMING: CUDA-event times   */
+  uint64_t binned_accesses;                 /* accesses counted through key-block bins  */
 } aiwc_result;
 
 typedef struct {

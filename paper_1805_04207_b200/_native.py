@@ -61,7 +61,7 @@ class Result(ctypes.Structure):
         ("n_widths", ctypes.c_uint32), ("width_values", u64p), ("width_counts", u64p),
         ("n_site_list", ctypes.c_uint32), ("site_ids", u64p), ("site_counts", u64p),
         ("used_dense_table", ctypes.c_uint32), ("kernels_launched", ctypes.c_uint32),
-        ("d2h_bytes", ctypes.c_uint64), ("phase_ms", ctypes.c_double * 8),
+        ("d2h_bytes", ctypes.c_uint64), ("phase_ms", ctypes.c_double * 8), ("binned_accesses", ctypes.c_uint64),
     ]
 
 

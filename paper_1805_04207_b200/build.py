@@ -14,7 +14,7 @@ import sysconfig
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 CU_SOURCES = ["aiwc_ingest.cu", "aiwc_util.cu", "aiwc_memory.cu", "aiwc_dense.cu", "aiwc_branch.cu", "aiwc_capi.cu", "aiwc_synth.cu",
-              "aiwc_validate.cu", "aiwc_sim.cu", "aiwc_exchange.cu"]
+              "aiwc_validate.cu", "aiwc_sim.cu", "aiwc_exchange.cu", "aiwc_bins.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-lnccl"]  # NCCL: the job-mode collectives (aiwc_ctx_set_comm)
 LIB = os.path.join(HERE, "libaiwc_b200.so")

@@ -172,6 +172,11 @@ struct aiwc_ctx {
   bool dense32 = false;     // u32 count|flags entries (fewer than 2^30 accesses)
   bool hot_off = false;     // AIWC_HOT_WINDOW=0 disables the shared-memory hot-key window (measurement)
   bool region_off = false;  // AIWC_REGIONS=0 disables region compaction of wide address spans (measurement)
+  bool bins_off = false;    // AIWC_BINS=0 disables the key-block bins of random accesses (measurement)
+  bool bins_force = false;  // AIWC_BINS=2 makes every dense trace eligible (tests at small sizes)
+  bool bins = false;        // this trace: the zone sampler ran, the ingest may bin
+  uint64_t binned = 0;      // this trace: accesses counted through the bins
+  Buf bin_seg, bin_base, bin_fill, bin_scr;
   int dense_entry = 0;      // AIWC_DENSE_ENTRY=32|64 forces the entry width (measurement), 0 = rule
   uint64_t ipt_tab_len = 0;
   uint32_t n_ranges = 0, tiles_per_cta = 0;
@@ -270,6 +275,7 @@ extern "C" int aiwc_ctx_create(aiwc_ctx** out, int device, const aiwc_opts* opts
   if (const char* de = getenv("AIWC_DENSE_ENTRY")) ctx->dense_entry = atoi(de);
   if (const char* hw = getenv("AIWC_HOT_WINDOW")) ctx->hot_off = atoi(hw) == 0;
   if (const char* rg = getenv("AIWC_REGIONS")) ctx->region_off = atoi(rg) == 0;
+  if (const char* bn = getenv("AIWC_BINS")) { ctx->bins_off = atoi(bn) == 0; ctx->bins_force = atoi(bn) == 2; }
   CK(cudaSetDevice(device));
   CK(cudaDeviceGetAttribute(&ctx->n_sms, cudaDevAttrMultiProcessorCount, device));
   if (ctx->opts.dense_budget_bytes == 0) {
@@ -322,7 +328,7 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   if (ctx->p1_ev) cudaEventDestroy(ctx->p1_ev);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (Buf* b : {&ctx->chunk_bits, &ctx->own_list, &ctx->nc_bits, &ctx->nc_small, &ctx->nc_send, &ctx->nc_recv,
-                 &ctx->nc_pack, &ctx->nc_blob})
+                 &ctx->nc_pack, &ctx->nc_blob, &ctx->bin_seg, &ctx->bin_base, &ctx->bin_fill, &ctx->bin_scr})
     if (b->p) cudaFree(b->p);
   if (ctx->hot_ev) cudaEventDestroy(ctx->hot_ev);
   delete ctx;
@@ -696,6 +702,30 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     a.chunk_bits = ctx->shard_dense ? P<uint32_t>(ctx->chunk_bits) : nullptr;
+    // key-block bins: a dense table well beyond L2 with many accesses -- the zone
+    // sampler (beside pass 1, on the device) decides whether any key zone is random
+    const size_t tab_bytes = dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8);
+    ctx->bins = ctx->dense && !ctx->shard_dense && !ctx->bins_off && M < (1ull << 32) &&
+                ((tab_bytes > (256ull << 20) && M >= (1ull << 22)) || ctx->bins_force);
+    a.bin_zones = nullptr;
+    if (ctx->bins) {
+      const uint32_t nw = G * P1_SUB;
+      CK(grow(ctx->bin_seg, M * 4));
+      CK(grow(ctx->bin_base, (size_t)nw * 8));
+      CK(grow(ctx->bin_fill, (size_t)nw * 4));
+      CK(cudaMemsetAsync(ctx->bin_fill.p, 0, (size_t)nw * 4, s));
+      const uint32_t keybits = 64 - __builtin_clzll(std::max<uint64_t>(ctx->am.n_keys - 1, 1));
+      a.zone_shift = (uint32_t)std::max<int>(15, (int)keybits - 6);
+      CK(cudaStreamWaitEvent(ctx->aux2, ctx->p1_ev, 0));
+      launch_zone_sample(kind, payload, n, ctx->am, a.zone_shift, st->zone_counts, &st->bin_zones, ctx->aux2);
+      CK(cudaEventRecord(ctx->hot_ev, ctx->aux2));
+      CK(cudaStreamWaitEvent(s, ctx->hot_ev, 0));
+      ctx->kernels += 2;
+      a.bin_seg = P<uint32_t>(ctx->bin_seg);
+      a.bin_base = P<unsigned long long>(ctx->bin_base);
+      a.bin_fill = P<uint32_t>(ctx->bin_fill);
+      a.bin_zones = &st->bin_zones;
+    }
     ctx->mark(AIWC_PH_INGEST, 0, s);
     CK(launch_ingest(a, km, pm, G, ctx->dense, stage, s));
     ctx->mark(AIWC_PH_INGEST, 1, s);
@@ -819,6 +849,21 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   launch_width_list(P<unsigned long long>(ctx->wcount), P<unsigned long long>(ctx->wfirst), st, s);
   ctx->kernels += 1;
   ctx->mark(AIWC_PH_MEMORY, 0, s);
+  ctx->binned = 0;
+  if (M && ctx->dense && ctx->bins) {  // the binned accesses into the table first
+    unsigned long long nb = 0;
+    CK(cudaMemcpyAsync(&nb, &st->bin_total, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->d2h += 8;
+    ctx->binned = nb;
+    if (nb) {
+      const uint32_t nw = ctx->n_ranges * P1_SUB;
+      CK(grow(ctx->bin_scr, bin_scratch_bytes(nb, nw, (ctx->am.n_keys >> 14) + 2)));
+      ctx->kernels += bin_finish(P<uint32_t>(ctx->bin_seg), P<unsigned long long>(ctx->bin_base),
+                                 P<uint32_t>(ctx->bin_fill), nw, nb, ctx->dtab.p, ctx->dense32, ctx->am.n_keys,
+                                 ctx->bin_scr.p, s);
+    }
+  }
   if (M) {
     if (ctx->dense) {
       const uint64_t chunks = (ctx->am.n_keys + 1023) / 1024;
@@ -1031,6 +1076,7 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   r.site_ids = ctx->site_ids.data();
   r.site_counts = ctx->site_counts.data();
   r.used_dense_table = ctx->dense;
+  r.binned_accesses = ctx->binned;
   r.kernels_launched = ctx->kernels;
   r.d2h_bytes = ctx->d2h;
   if (ctx->timing) {

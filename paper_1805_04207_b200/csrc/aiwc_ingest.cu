@@ -494,6 +494,11 @@ __global__ void __launch_bounds__(TPB, 2)
   const uint32_t sw = lane & 7, sw2 = sw << 1;
   uint4* const wclose = L.closes[warp];
   uint32_t last_ch = ~0u, last_ch2 = ~0u;  // shard: the last two chunks this lane marked
+  // key-block bins: this warp range's segment of the bin buffer and its fill
+  const unsigned long long zmask = (DENSE && a.bin_zones) ? *a.bin_zones : 0ull;
+  const unsigned long long bin_base0 = c_rd + c_wr;
+  uint32_t bfill = 0;
+  if (zmask && lane == 0) a.bin_base[gw] = bin_base0;
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -712,7 +717,43 @@ __global__ void __launch_bounds__(TPB, 2)
           }
         }
       };
-      if (a.chunk_bits) {
+      // key-block bins: whole-warp rounds (a ballot places the appended entries);
+      // accesses into a random zone go to the warp's bin segment, the rest as above
+      auto fold_bins = [&](auto with_window) {
+        constexpr bool HOT = decltype(with_window)::value;
+        uint32_t* const seg = a.bin_seg + bin_base0;
+        const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll 2
+        for (uint32_t b0 = 0; b0 < n_mem; b0 += 32) {
+          const uint32_t i = b0 + lane;
+          const bool act = i < n_mem;
+          const uint32_t e = act ? midx[i] : 0u;
+          const uint64_t off = P[e & 0x0FFFu] - base;
+          const bool v = act & (off <= off_max) & (((uint32_t)off & lmask) == lconst);
+          inval |= act & !v;
+          const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
+          const bool hot = HOT && rel < hot_n;
+          const bool binned = v && !hot && ((zmask >> min(key >> a.zone_shift, (uint64_t)(ZONES - 1))) & 1ull);
+          const uint32_t bm = __ballot_sync(0xffffffffu, binned);
+          if (binned) seg[bfill + __popc(bm & lt)] = (uint32_t)key | ((uint32_t)(e >> 15) << 31);
+          bfill += __popc(bm);
+          if (act && !binned) {
+            if (hot) {
+              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+            } else if (a.dense32) {
+              uint32_t* const q = static_cast<uint32_t*>(a.dense) + key;
+              atomicAdd(q, 1u);
+              atomicOr(q, E32_READ << (e >> 15));
+            } else {
+              atomicAdd(static_cast<unsigned long long*>(a.dense) + key, 1ull << (32 * (e >> 15)));
+            }
+          }
+        }
+      };
+      if (zmask) {
+        if (hot_n) fold_bins(std::true_type{});
+        else fold_bins(std::false_type{});
+      } else if (a.chunk_bits) {
         if (hot_n) fold(std::true_type{}, std::true_type{});
         else fold(std::false_type{}, std::true_type{});
       } else {
@@ -806,6 +847,10 @@ __global__ void __launch_bounds__(TPB, 2)
   }
 
   // ---- epilogue: flush CTA-private state ----
+  if (zmask && lane == 0) {
+    a.bin_fill[gw] = bfill;
+    if (bfill) atomicAdd(&st->bin_total, (unsigned long long)bfill);
+  }
   if (my_tiles % PRES_TILES) record_presence((my_tiles - 1) / PRES_TILES);
   flush_counts(oacc, wacc, a, lane, flags);
   __syncthreads();

@@ -102,6 +102,8 @@ struct DevState {
   unsigned long long host_end;
   unsigned long long cnt_hist[NLEVELS][CBINS];      // count-of-counts per level (entropy)
   unsigned long long hot_key;                       // hot_sample_kernel: first key of the hot window, ~0 none
+  unsigned long long bin_zones, bin_total;          // random key zones (bit z: zone z is binned), entries binned
+  unsigned int zone_counts[128];                    // zone sampler: (near, far) per zone
 };
 
 // Memory-path description shared by the ingest and the dense-table kernels.
@@ -115,6 +117,7 @@ struct AddrMap {
   uint64_t off_max;    // largest valid addr - base: ((n_keys - 1) << k) | low_mask
 };
 
+constexpr int ZONES = 64;                   // key zones of the random-access sampler (aiwc_bins.cu)
 constexpr uint32_t SMEM_TABLE_KEYS = 1024;  // small dense tables / the hot window live in shared memory per CTA
 constexpr uint64_t HOT_MIN_ACCESSES = 1ull << 20;  // traces with fewer accesses skip the hot-window sampler
 constexpr int PRES_TILES = 16;         // width presence granularity (tile iterations per mask)
@@ -151,6 +154,12 @@ struct IngestArgs {
   uint64_t* wr_out;
   uint64_t* br_out;                 // branch records site << 32 | gkey << 1 | taken
   uint32_t* chunk_bits;             // shard dense exchange: bit c = this rank touched keys [1024 c, 1024 c + 1024)
+  // key-block bins (aiwc_bins.cu): accesses into random zones are appended, not REDed
+  uint32_t* bin_seg;                // [accesses]: warp range w appends at bin_base[w]
+  unsigned long long* bin_base;     // [warp ranges]: accesses before the range (written by the ingest)
+  uint32_t* bin_fill;               // [warp ranges]: entries the range appended
+  const unsigned long long* bin_zones;  // device zone mask (null / 0: no bins)
+  uint32_t zone_shift;
 };
 
 // ---- stream validation (aiwc_validate.cu) ---------------------------------------
@@ -271,6 +280,13 @@ void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, 
                         double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s,
                         const uint32_t* own_bits = nullptr, uint64_t own_words = 0, uint32_t rank = 0,
                         uint32_t nranks = 1);  // own_bits: only the chunks `rank` owns
+// key-block bins (aiwc_bins.cu)
+void launch_zone_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n, const AddrMap& am,
+                        uint32_t zone_shift, unsigned int* zone_counts, unsigned long long* zones_out,
+                        cudaStream_t s);
+size_t bin_scratch_bytes(uint64_t n_bins, uint32_t n_warps, uint64_t n_blocks);
+int bin_finish(const uint32_t* seg, const unsigned long long* seg_base, const uint32_t* fill, uint32_t n_warps,
+               uint64_t n_bins, void* table, bool e32, uint64_t n_keys, void* scratch, cudaStream_t s);
 // multi-GPU dense exchange (aiwc_exchange.cu); return kernel counts
 int launch_pack(const void* tab, bool e32, const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
                 int pass, unsigned long long* cursor, uint64_t* out, uint32_t n_sms, cudaStream_t s);

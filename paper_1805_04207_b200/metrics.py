@@ -77,6 +77,7 @@ class EngineResult:
     sites: list   # [(site, executions)] ascending site
     used_dense_table: bool
     kernels_launched: int
+    binned_accesses: int = 0
 
 
 def _dist(d) -> tuple:
@@ -96,6 +97,7 @@ def _copy_result(r: _native.Result) -> EngineResult:
         widths=[(r.width_values[i], r.width_counts[i]) for i in range(r.n_widths)],
         sites=[(r.site_ids[i], r.site_counts[i]) for i in range(r.n_site_list)],
         used_dense_table=bool(r.used_dense_table), kernels_launched=r.kernels_launched,
+        binned_accesses=r.binned_accesses,
     )
 
 
