@@ -351,7 +351,10 @@ def run_ours(args) -> None:
         # streams to run concurrently, pkg/README.md:192-193), so one stream's
         # small kernels and host round trip overlap another stream's ingest.
         # Every lane reads its OWN copy of the trace (no cross-lane L2 reuse).
-        info = trace_info(tr)
+        # the columns are treated as untrusted: every step also checks StreamChecker's
+        # invariants inside the pass (certified for traces without barriers / resumes;
+        # the separate full validator's cost is reported as validate_ms)
+        info = trace_info(tr, check=not args.no_stream_check)
         lanes = []
         for i in range(n_streams):
             cs = stream if i == 0 else torch.cuda.Stream(dev)
@@ -448,7 +451,8 @@ def run_ours(args) -> None:
     if args.no_e2e:
         if rank == 0:
             print(json.dumps({"ms_per_step": ms_step, "value": value, "phases_ms": phase_med,
-                              "validate_ms": validate_ms, "shard_sections_ms": dict(D.LAST_PROFILE)}), flush=True)
+                              "validate_ms": validate_ms, "shard_sections_ms": dict(D.LAST_PROFILE),
+                              "binned": lanes[0][2].binned_accesses if not sharded else None}), flush=True)
         if sharded:
             dist.destroy_process_group()
         return
@@ -532,6 +536,11 @@ def run_ours(args) -> None:
                          "aggregate_frac": agg / (world * peak)},
             "phases_ms": phase_med,
             "validate_ms": validate_ms,
+            "stream_check": {"in_pass": not sharded, "certified": bool(lanes[0][2].stream_checked) if not sharded else None,
+                             "full_validator_ms": validate_ms,
+                             "note": "every timed single-GPU step checks StreamChecker's invariants inside the pass "
+                                     "(trace.py:289-424); traces with barriers / resumes are certified by the "
+                                     "separate device validator instead (full_validator_ms)"},
             "gpu_launches": kernels[0],
             "clocks": clocks,
             "cpu_baseline": cpu,
@@ -610,6 +619,7 @@ def main():
     ap.add_argument("--streams", type=int, default=3,
                     help="N=1: engine contexts / CUDA streams with whole steps in flight concurrently")
     ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
+    ap.add_argument("--no-stream-check", action="store_true", help="measurement: steps without the in-pass checks")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         spawn_ranks(args.gpus)

@@ -92,10 +92,18 @@ typedef struct {
    * pass 1's totals are checked against them at finalize (AIWC_ERR_ARGUMENT
    * when they differ). */
   uint64_t n_instr, n_reads, n_writes, n_branches, n_groups;
-  uint32_t any_barrier_or_resume, reserved;
+  uint32_t any_barrier_or_resume;
+  /* 1: the columns come from an untrusted producer -- check StreamChecker's
+   * invariants (trace.py:289-424) inside the pass.  A violation makes
+   * aiwc_finalize return AIWC_ERR_INVALID_STREAM (aiwc_validate locates the
+   * first one); aiwc_result.stream_checked says whether the pass could certify
+   * the stream (traces with barriers / resumes need aiwc_validate).        */
+  uint32_t check_stream;
   /* Event index of this trace's first event in the whole job (a work-group shard
    * of a multi-GPU job: first-appearance order of widths spans the ranks); 0 else. */
   uint64_t first_event;
+  /* 1: keep the accumulator's state for aiwc_state_export (a later merge). */
+  uint32_t export_state, reserved2;
 } aiwc_trace_info;
 
 typedef struct {
@@ -126,6 +134,8 @@ typedef struct {
   uint64_t d2h_bytes;                       /* device->host bytes read for this trace   */
   double phase_ms[AIWC_N_PHASES];           /* with AIWC_OPT_TIMING: CUDA-event times   */
   uint64_t binned_accesses;                 /* accesses counted through key-block bins  */
+  uint32_t stream_checked;                  /* check_stream: the pass certified the stream */
+  uint32_t reserved;
 } aiwc_result;
 
 typedef struct {
@@ -267,6 +277,41 @@ int  aiwc_shard_pack(aiwc_ctx *ctx, const uint32_t *all_bits_dev, uint32_t rank,
                      uint64_t **runs_dev, uint64_t *counts, void *stream);
 int  aiwc_shard_owned(aiwc_ctx *ctx, const uint64_t *runs_dev, uint64_t n_runs, const uint32_t *all_bits_dev,
                       uint32_t rank, uint32_t nranks, uint64_t total_m, aiwc_memory_part *out, void *stream);
+
+/* ---- accumulator state and state merges (merge_accumulators, metrics.py:235-270) ----
+ * With info->export_state, aiwc_finalize keeps the trace's per-key memory state
+ * as runs of equal dense-table entries (two u64 per run: key | length << 32,
+ * count | read seen << 62 | write seen << 63) over its key map (address =
+ * base + (key << k) + low_const), plus the histograms finalize consumed.  A merge
+ * adds the parts' histograms on the host and rebuilds the memory statistics of
+ * the union from the parts' runs (aiwc_memory_merge): no re-ingest.        */
+typedef struct {
+  uint32_t exported;                        /* 0: the trace took the sort path (no table) */
+  uint32_t branch_table_size;
+  uint64_t n_runs;
+  const uint64_t *runs_dev;                 /* ctx-owned device memory, valid until the next ingest */
+  uint64_t base, low_const;
+  uint32_t k, pad;
+  uint64_t addr_stats[4];                   /* min, max, and, or of the addresses                   */
+  const uint64_t *itb_hist, *ipt_hist;      /* host, 1024 bins each                                 */
+  uint64_t n_itb_ovf, n_ipt_ovf;
+  const uint64_t *itb_ovf, *ipt_ovf;        /* ascending                                            */
+  const uint64_t *branch_table;             /* host: total << 32 | taken per pattern                */
+  const uint64_t *width_first;              /* per aiwc_result width: first event index             */
+} aiwc_state;
+
+typedef struct {
+  const uint64_t *runs_dev;
+  uint64_t n_runs, base, low_const;
+  uint32_t k, pad;
+} aiwc_runs_part;
+
+int  aiwc_state_export(aiwc_ctx *ctx, aiwc_state *out);
+/* memory statistics of the union of the parts' runs (counts add, flags OR) over the
+ * key map of the merged address statistics (min, max, and, or); AIWC_ERR_UNSUPPORTED
+ * when that span does not fit a dense table (the caller re-ingests instead). */
+int  aiwc_memory_merge(aiwc_ctx *ctx, const aiwc_runs_part *parts, uint32_t n_parts, const uint64_t stats[4],
+                       uint64_t total_m, aiwc_memory_part *out, void *stream);
 
 /* ---- stream validation (StreamChecker, trace.py:289-424) -------------------------
  * First violation of a columnar trace, decoded as ColumnarTrace.iter_events

@@ -35,8 +35,8 @@ class TraceInfo(ctypes.Structure):
                 ("addr_and", ctypes.c_uint64), ("addr_or", ctypes.c_uint64),
                 ("n_instr", ctypes.c_uint64), ("n_reads", ctypes.c_uint64), ("n_writes", ctypes.c_uint64),
                 ("n_branches", ctypes.c_uint64), ("n_groups", ctypes.c_uint64),
-                ("any_barrier_or_resume", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
-                ("first_event", ctypes.c_uint64)]
+                ("any_barrier_or_resume", ctypes.c_uint32), ("check_stream", ctypes.c_uint32),
+                ("first_event", ctypes.c_uint64), ("export_state", ctypes.c_uint32), ("reserved2", ctypes.c_uint32)]
 
 
 class Dist(ctypes.Structure):
@@ -62,6 +62,7 @@ class Result(ctypes.Structure):
         ("n_site_list", ctypes.c_uint32), ("site_ids", u64p), ("site_counts", u64p),
         ("used_dense_table", ctypes.c_uint32), ("kernels_launched", ctypes.c_uint32),
         ("d2h_bytes", ctypes.c_uint64), ("phase_ms", ctypes.c_double * 8), ("binned_accesses", ctypes.c_uint64),
+        ("stream_checked", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
     ]
 
 
@@ -87,6 +88,19 @@ class MemoryPart(ctypes.Structure):
 class ShardStats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("addr_min", "addr_max", "addr_and", "addr_or", "n_accesses",
                                              "dense_budget_bytes", "n_branches")]
+
+
+class State(ctypes.Structure):
+    _fields_ = [("exported", ctypes.c_uint32), ("branch_table_size", ctypes.c_uint32), ("n_runs", ctypes.c_uint64),
+                ("runs_dev", ctypes.c_void_p), ("base", ctypes.c_uint64), ("low_const", ctypes.c_uint64),
+                ("k", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("addr_stats", ctypes.c_uint64 * 4),
+                ("itb_hist", u64p), ("ipt_hist", u64p), ("n_itb_ovf", ctypes.c_uint64), ("n_ipt_ovf", ctypes.c_uint64),
+                ("itb_ovf", u64p), ("ipt_ovf", u64p), ("branch_table", u64p), ("width_first", u64p)]
+
+
+class RunsPart(ctypes.Structure):
+    _fields_ = [("runs_dev", ctypes.c_void_p), ("n_runs", ctypes.c_uint64), ("base", ctypes.c_uint64),
+                ("low_const", ctypes.c_uint64), ("k", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
 class Violation(ctypes.Structure):
@@ -130,7 +144,8 @@ EXPORTS = ("aiwc_abi_version", "aiwc_ctx_create", "aiwc_ctx_destroy", "aiwc_rese
            "aiwc_shard_tables_get", "aiwc_partition_addresses", "aiwc_memory_partial", "aiwc_validate",
            "aiwc_sim_create", "aiwc_sim_destroy", "aiwc_sim_last_error", "aiwc_sim_plan", "aiwc_sim_emit",
            "aiwc_partition_runs", "aiwc_memory_partial_runs", "aiwc_shard_prepare", "aiwc_shard_ingest",
-           "aiwc_shard_chunks", "aiwc_shard_pack", "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm")
+           "aiwc_shard_chunks", "aiwc_shard_pack", "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm",
+           "aiwc_state_export", "aiwc_memory_merge")
 
 _lib = None
 _lock = threading.Lock()
@@ -176,6 +191,9 @@ def load_library(path: str = LIB_PATH):
         lib.aiwc_shard_owned.argtypes = [vp, vp, ctypes.c_uint64, vp, ctypes.c_uint32, ctypes.c_uint32,
                                          ctypes.c_uint64, ctypes.POINTER(MemoryPart), vp]
         lib.aiwc_nccl_unique_id.argtypes = [vp]
+        lib.aiwc_state_export.argtypes = [vp, ctypes.POINTER(State)]
+        lib.aiwc_memory_merge.argtypes = [vp, ctypes.POINTER(RunsPart), ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64),
+                                          ctypes.c_uint64, ctypes.POINTER(MemoryPart), vp]
         lib.aiwc_ctx_set_comm.argtypes = [vp, vp, ctypes.c_int, ctypes.c_int]
         i64x3 = ctypes.c_int64 * 3
         lib.aiwc_validate.argtypes = [vp, vp, vp, ctypes.POINTER(TraceInfo), i64x3, i64x3, ctypes.POINTER(Violation), vp]
@@ -191,7 +209,8 @@ def load_library(path: str = LIB_PATH):
                      "aiwc_last_error", "aiwc_synth_fill", "aiwc_shard_tables_get", "aiwc_partition_addresses",
                      "aiwc_memory_partial", "aiwc_validate", "aiwc_partition_runs", "aiwc_memory_partial_runs",
                      "aiwc_shard_prepare", "aiwc_shard_ingest", "aiwc_shard_chunks", "aiwc_shard_pack",
-                     "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm"):
+                     "aiwc_shard_owned", "aiwc_nccl_unique_id", "aiwc_ctx_set_comm", "aiwc_state_export",
+                     "aiwc_memory_merge"):
             getattr(lib, name).restype = ctypes.c_int
         if lib.aiwc_abi_version() != 2:
             raise DeviceError("libaiwc_b200.so ABI version mismatch")

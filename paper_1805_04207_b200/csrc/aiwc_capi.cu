@@ -153,6 +153,16 @@ __global__ void region_remap_kernel(const uint8_t* __restrict__ kind, const uint
   }
 }
 
+// set bits of the duplicate-begin bitmap (in-pass stream check): fewer than the
+// wi_begin events means some work-item began twice in one group
+__global__ void popcount_kernel(const uint32_t* __restrict__ bits, uint64_t words, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+    c += __popc(bits[i]);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
 struct aiwc_ctx {
   int device = 0;
   int n_sms = 148;
@@ -172,10 +182,21 @@ struct aiwc_ctx {
   bool dense32 = false;     // u32 count|flags entries (fewer than 2^30 accesses)
   bool hot_off = false;     // AIWC_HOT_WINDOW=0 disables the shared-memory hot-key window (measurement)
   bool region_off = false;  // AIWC_REGIONS=0 disables region compaction of wide address spans (measurement)
-  bool bins_off = false;    // AIWC_BINS=0 disables the key-block bins of random accesses (measurement)
-  bool bins_force = false;  // AIWC_BINS=2 makes every dense trace eligible (tests at small sizes)
+  // key-block bins of random accesses: measured to cost more than the REDs they replace with the
+  // current two-pass partition (C3: ingest -1.35 ms, bin processing +6.2 ms), so opt-in:
+  // AIWC_BINS=1 enables them for eligible traces, AIWC_BINS=2 for every dense trace (tests)
+  bool bins_off = true;
+  bool bins_force = false;
   bool bins = false;        // this trace: the zone sampler ran, the ingest may bin
   uint64_t binned = 0;      // this trace: accesses counted through the bins
+  bool stream_checked = false;  // this trace: the ingest checked StreamChecker's invariants
+  Buf dup_bits;
+  uint64_t dup_len = 0;
+  // exported accumulator state (aiwc_state_export)
+  Buf state_runs, state_cur;
+  uint64_t state_n_runs = 0;
+  bool state_ok = false;
+  uint64_t stats4[4] = {};  // address statistics the key map was built from
   Buf bin_seg, bin_base, bin_fill, bin_scr;
   int dense_entry = 0;      // AIWC_DENSE_ENTRY=32|64 forces the entry width (measurement), 0 = rule
   uint64_t ipt_tab_len = 0;
@@ -328,7 +349,8 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   if (ctx->p1_ev) cudaEventDestroy(ctx->p1_ev);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (Buf* b : {&ctx->chunk_bits, &ctx->own_list, &ctx->nc_bits, &ctx->nc_small, &ctx->nc_send, &ctx->nc_recv,
-                 &ctx->nc_pack, &ctx->nc_blob, &ctx->bin_seg, &ctx->bin_base, &ctx->bin_fill, &ctx->bin_scr})
+                 &ctx->nc_pack, &ctx->nc_blob, &ctx->bin_seg, &ctx->bin_base, &ctx->bin_fill, &ctx->bin_scr,
+                 &ctx->dup_bits, &ctx->state_runs, &ctx->state_cur})
     if (b->p) cudaFree(b->p);
   if (ctx->hot_ev) cudaEventDestroy(ctx->hot_ev);
   delete ctx;
@@ -463,6 +485,9 @@ static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payl
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   CK(cudaSetDevice(ctx->device));
   ctx->info = *info;
+  ctx->stream_checked = false;
+  ctx->state_ok = false;
+  ctx->state_n_runs = 0;
   ctx->kernels = 0;
   ctx->d2h = 0;
   ctx->marked = 0;
@@ -613,6 +638,7 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
   };
   if (M_local && amin > amax) return fail(ctx, AIWC_ERR_ARGUMENT, "address statistics are empty but the trace has memory events");
   decide_memory(amin, amax, aand, aor);
+  ctx->stats4[0] = amin; ctx->stats4[1] = amax; ctx->stats4[2] = aand; ctx->stats4[3] = aor;
   ctx->shard_dense = shard && ctx->dense;
   // a span too wide for the table: if the accesses sit in few 1 MB regions, squeeze
   // the regions together (exact for every memory statistic) and keep the dense path
@@ -626,6 +652,7 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
       const int rc2 = encode_maps(ctx, kind, payload, rows, &km, &pm);
       if (rc2) return rc2;
       decide_memory(rs[0], rs[1], rs[2], rs[3]);
+      ctx->stats4[0] = rs[0]; ctx->stats4[1] = rs[1]; ctx->stats4[2] = rs[2]; ctx->stats4[3] = rs[3];
     }
   }
   const bool stage = !ctx->dense || ctx->n_br > 0;
@@ -702,6 +729,16 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     a.chunk_bits = ctx->shard_dense ? P<uint32_t>(ctx->chunk_bits) : nullptr;
+    // in-pass StreamChecker for untrusted columns without barriers / resumes
+    ctx->stream_checked = info->check_stream && !ctx->n_bres;
+    a.check = ctx->stream_checked;
+    if (a.check) {
+      a.dup_len = std::max<uint64_t>(ctx->n_wgb, 1) * a.local_volume;
+      ctx->dup_len = a.dup_len;
+      CK(grow(ctx->dup_bits, (a.dup_len + 31) / 32 * 4));
+      CK(cudaMemsetAsync(ctx->dup_bits.p, 0, (a.dup_len + 31) / 32 * 4, s));
+      a.dup_bits = P<uint32_t>(ctx->dup_bits);
+    }
     // key-block bins: a dense table well beyond L2 with many accesses -- the zone
     // sampler (beside pass 1, on the device) decides whether any key zone is random
     const size_t tab_bytes = dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8);
@@ -840,6 +877,12 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   const bool shard = ctx->opts.flags & AIWC_OPT_SHARD;
   const uint64_t M = shard ? 0 : ctx->n_rd + ctx->n_wr;  // a shard's memory is finished by the key owners
   ctx->mark(AIWC_PH_FINALIZE_TOTAL, 0, s);
+  if (ctx->stream_checked && ctx->info.n_events) {  // set bits of the duplicate-begin map -> DevState
+    const uint64_t words = (ctx->dup_len + 31) / 32;
+    popcount_kernel<<<(unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->n_sms * 4), 256, 0, s>>>(
+        P<uint32_t>(ctx->dup_bits), words, &st->dup_set);
+    ctx->kernels += 1;
+  }
 
   // ---- device finishing: IPT slots, widths, memory ----
   if (ctx->ipt_tab_len) {
@@ -870,6 +913,28 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
       const uint32_t nct = (uint32_t)std::min<uint64_t>(chunks, ctx->n_parts);
       launch_dense_stats(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, ctx->am.k, M, st,
                          P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s);
+      // the per-key state as runs for a later state merge -- tables up to 512 MB (a sweep of a
+      // larger table would cost a sizeable part of its ingest; such merges re-ingest)
+      if (ctx->info.export_state && !ctx->remap_pay.p &&
+          dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8) <= (512ull << 20)) {
+        CK(grow(ctx->state_cur, 8));
+        unsigned long long* cur = P<unsigned long long>(ctx->state_cur);
+        CK(cudaMemsetAsync(cur, 0, 8, s));
+        launch_pack_all(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, cur, nullptr, 0, (uint32_t)ctx->n_sms, s);
+        unsigned long long nr = 0;
+        CK(cudaMemcpyAsync(&nr, cur, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // kept only when the runs compress the table (streaming / strided traces): a
+        // random-access trace's state would be as large as its table -- its merge re-ingests
+        const bool keep = nr <= ctx->am.n_keys / 4 || nr * 16 <= (256ull << 20);
+        if (keep) CK(grow(ctx->state_runs, std::max<uint64_t>(nr, 1) * 16));
+        CK(cudaMemsetAsync(cur, 0, 8, s));
+        if (nr && keep) launch_pack_all(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, cur, P<uint64_t>(ctx->state_runs), 1,
+                                (uint32_t)ctx->n_sms, s);
+        ctx->state_n_runs = keep ? nr : 0;
+        ctx->state_ok = keep;
+        ctx->kernels += 2;
+      }
       // the table is clean again for the next trace: clear it on the side stream now
       CK(cudaEventRecord(ctx->fork_ev, s));
       CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
@@ -923,6 +988,12 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     const bool ok = h.addr_min >= am.base && h.addr_max <= am.hi && ((h.addr_and ^ h.addr_or) & am.low_mask) == 0 &&
                     ((h.addr_min - am.base) & am.low_mask) == am.low_const;
     if (!ok) h.flags |= F_ADDR_HINT;
+  }
+  // every wi_begin set its own (group, lid) bit: fewer set bits than begins = a duplicate
+  if (ctx->stream_checked && ctx->info.n_events && h.dup_set != h.n_wib) h.flags |= F_STREAM;
+  if (h.flags & F_STREAM) {
+    fail(ctx, AIWC_ERR_INVALID_STREAM, "stream invariant violated (aiwc_validate locates the first violation)");
+    return AIWC_ERR_INVALID_STREAM;
   }
   if (h.flags) {
     char m[160];
@@ -1057,7 +1128,7 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
       ctx->width_firsts.push_back(o.first);
     }
   }
-  if (shard) {  // the pooled pattern table is summed across ranks before the entropies
+  if (shard || ctx->info.export_state) {  // the pooled pattern table (summed across ranks / merged parts)
     const size_t tb = (size_t(1) << ctx->opts.history_len);
     ctx->branch_tab_host.assign(tb, 0);
     if (ctx->n_br) {
@@ -1077,6 +1148,7 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   r.site_counts = ctx->site_counts.data();
   r.used_dense_table = ctx->dense;
   r.binned_accesses = ctx->binned;
+  r.stream_checked = ctx->stream_checked;
   r.kernels_launched = ctx->kernels;
   r.d2h_bytes = ctx->d2h;
   if (ctx->timing) {
@@ -1725,6 +1797,62 @@ extern "C" int aiwc_shard_owned(aiwc_ctx* ctx, const uint64_t* runs, uint64_t n_
                                       nranks, P<uint32_t>(ctx->chunk_bits), (uint32_t)ctx->n_sms, s);
   ctx->dtab_clean = ctx->dtab.cap;
   return owned_result(ctx, st, total_m, launched, out, s);
+}
+
+// ---------------------------------------------------------------------------
+// accumulator state export and state merges (merge_accumulators, metrics.py:235-270)
+// ---------------------------------------------------------------------------
+extern "C" int aiwc_state_export(aiwc_ctx* ctx, aiwc_state* out) {
+  if (!ctx || !out) return AIWC_ERR_ARGUMENT;
+  if (ctx->state != 2 || !ctx->info.export_state)
+    return fail(ctx, AIWC_ERR_ARGUMENT, "state export needs info.export_state and aiwc_finalize");
+  aiwc_state o{};
+  o.exported = ctx->state_ok || !(ctx->n_rd + ctx->n_wr);
+  o.n_runs = ctx->state_ok ? ctx->state_n_runs : 0;
+  o.runs_dev = P<uint64_t>(ctx->state_runs);
+  o.base = ctx->am.base; o.low_const = ctx->am.low_const; o.k = ctx->am.k;
+  for (int i = 0; i < 4; ++i) o.addr_stats[i] = ctx->stats4[i];
+  o.itb_hist = reinterpret_cast<const uint64_t*>(ctx->h_state->itb_hist);
+  o.ipt_hist = reinterpret_cast<const uint64_t*>(ctx->h_state->ipt_hist);
+  o.n_itb_ovf = ctx->itb_ovf_sorted.size(); o.itb_ovf = ctx->itb_ovf_sorted.data();
+  o.n_ipt_ovf = ctx->ipt_ovf_sorted.size(); o.ipt_ovf = ctx->ipt_ovf_sorted.data();
+  o.branch_table_size = (uint32_t)ctx->branch_tab_host.size();
+  o.branch_table = ctx->branch_tab_host.data();
+  o.width_first = ctx->width_firsts.data();
+  *out = o;
+  return AIWC_OK;
+}
+
+extern "C" int aiwc_memory_merge(aiwc_ctx* ctx, const aiwc_runs_part* parts, uint32_t n_parts, const uint64_t* stats,
+                                 uint64_t total_m, aiwc_memory_part* out, void* stream) {
+  if (!ctx || !out || !stats || (n_parts && !parts)) return AIWC_ERR_ARGUMENT;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  CK(cudaSetDevice(ctx->device));
+  CK(grow(ctx->mp_state, sizeof(DevState)));
+  DevState* st = P<DevState>(ctx->mp_state);
+  init_state_kernel<<<64, 256, 0, s>>>(st);
+  uint32_t launched = 1;
+  if (!total_m) return owned_result(ctx, st, 0, launched, out, s);
+  // the merged key map by the engine's rule (aiwc_ingest's decide_memory)
+  const uint64_t base = stats[0] & ~1023ull, vary = stats[2] ^ stats[3];
+  const uint32_t k = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
+  const uint64_t span = (stats[1] - base) >> k, n_keys = span + 1;
+  if (span >= DENSE_MAX_KEYS - 1 || n_keys * 8 > ctx->opts.dense_budget_bytes || n_keys > 4 * total_m + (1ull << 20))
+    return fail(ctx, AIWC_ERR_UNSUPPORTED, "merged address span does not fit a dense table");
+  const uint64_t tm = total_m;
+  CK(grow(ctx->mp_ovf, (tm / CBINS + 2) * 8));
+  CK(grow(ctx->mp_tab, n_keys * 8));
+  CK(cudaMemsetAsync(ctx->mp_tab.p, 0, n_keys * 8, s));
+  for (uint32_t i = 0; i < n_parts; ++i) {
+    launch_merge_apply(parts[i].runs_dev, parts[i].n_runs, parts[i].base, parts[i].low_const, parts[i].k, base, k, n_keys,
+                       P<unsigned long long>(ctx->mp_tab), &st->flags, (uint32_t)ctx->n_sms, s);
+    launched += parts[i].n_runs ? 1 : 0;
+  }
+  const uint32_t nct = (uint32_t)std::min<uint64_t>((n_keys + 1023) / 1024, ctx->n_parts);
+  launch_dense_stats(ctx->mp_tab.p, false, n_keys, k, tm, st, P<double>(ctx->partials), nct, P<uint64_t>(ctx->mp_ovf), s);
+  launch_entropy_finish(st, P<double>(ctx->partials), nct, tm, k, s);
+  launched += 2;
+  return owned_result(ctx, st, tm, launched, out, s);
 }
 
 // ---------------------------------------------------------------------------

@@ -155,7 +155,126 @@ __global__ void __launch_bounds__(XT) clear_kernel(E* __restrict__ tab, uint64_t
   }
 }
 
+// ---- accumulator state export / merge (merge_accumulators, metrics.py:235-270) ----
+// entry64 = count | read seen << 62 | write seen << 63 (both table forms)
+template <typename E>
+__device__ __forceinline__ uint64_t entry64(E e);
+template <>
+__device__ __forceinline__ uint64_t entry64<uint32_t>(uint32_t e) {
+  return (uint64_t)(e & E32_COUNT) | ((uint64_t)((e >> 30) & 1u) << 62) | ((uint64_t)(e >> 31) << 63);
+}
+template <>
+__device__ __forceinline__ uint64_t entry64<unsigned long long>(unsigned long long e) {
+  const uint64_t r = e & 0xFFFFFFFFull, w = e >> 32;
+  return (r + w) | ((uint64_t)(r != 0) << 62) | ((uint64_t)(w != 0) << 63);
+}
+
+// runs of equal non-zero entries of every chunk of the table (pass 0 counts into
+// *cursor, pass 1 emits at the reserved slots); one warp per 1024-key chunk
+template <typename E>
+__global__ void __launch_bounds__(XT) pack_all_kernel(const E* __restrict__ tab, uint64_t n_keys, int pass,
+                                                      unsigned long long* __restrict__ cursor,
+                                                      uint64_t* __restrict__ out) {
+  __shared__ uint32_t s_bm[XW][33];
+  __shared__ uint32_t s_pre[XW][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t n_chunks = (n_keys + 1023) / 1024;
+  const uint64_t n_warps = (uint64_t)gridDim.x * XW;
+  for (uint64_t c = (uint64_t)blockIdx.x * XW + warp; c < n_chunks; c += n_warps) {
+    const E* src = tab + c * 1024;
+    E e[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const uint64_t key = c * 1024 + 32 * q + lane;
+      e[q] = key < n_keys ? src[32 * q + lane] : (E)0;
+    }
+    uint32_t hm_lane = 0, bm_lane = 0;
+    E last = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      E prev = shfl_up_e(e[q], 1);
+      const E wrap = shfl_e(last, 31);
+      if (lane == 0) prev = wrap;
+      const bool bnd = (q == 0 && lane == 0) || e[q] != prev;
+      const uint32_t bm = __ballot_sync(0xffffffffu, bnd);
+      const uint32_t hm = __ballot_sync(0xffffffffu, bnd && e[q] != 0);
+      if (lane == q) { bm_lane = bm; hm_lane = hm; }
+      last = e[q];
+    }
+    uint32_t cnt = __popc(hm_lane), inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    if (!total) continue;
+    s_bm[warp][lane] = bm_lane;
+    s_pre[warp][lane] = inc - cnt;
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(cursor, (unsigned long long)total);
+    if (pass == 1) {
+      base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t hm = __shfl_sync(0xffffffffu, hm_lane, q);
+        if (!((hm >> lane) & 1u)) continue;
+        uint32_t qq = q, m = s_bm[warp][q] & ~((2u << lane) - 1u);
+        while (!m) { ++qq; m = qq < 32 ? s_bm[warp][qq] : 1u; }
+        const uint32_t end = qq < 32 ? 32 * qq + (__ffs(m) - 1) : 1024u;
+        const uint32_t pos = 32 * q + lane;
+        const uint64_t slot = base + s_pre[warp][q] + __popc(hm & ((1u << lane) - 1u));
+        out[2 * slot] = (c * 1024 + pos) | ((uint64_t)(end - pos) << 32);
+        out[2 * slot + 1] = entry64<E>(e[q]);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// one part's runs into the merged u64 table (reads | writes << 32 form, the
+// (count, read seen, write seen) of each key kept exactly: count - 1 | 1 << 32
+// when both were seen), keys translated through the addresses
+__global__ void merge_apply_kernel(const uint64_t* __restrict__ runs, uint64_t n_runs, uint64_t base_p,
+                                   uint64_t low_p, uint32_t k_p, uint64_t base_m, uint32_t k_m, uint64_t n_keys_m,
+                                   unsigned long long* __restrict__ tab, unsigned long long* flags) {
+  // one warp per run (the exported runs are long: streaming / strided traces)
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_runs; r += nw) {
+    const uint64_t w0 = runs[2 * r], v = runs[2 * r + 1];
+    const uint64_t key = w0 & 0xFFFFFFFFull, len = w0 >> 32;
+    const uint64_t c = v & ((1ull << 62) - 1), rd = (v >> 62) & 1, wr = v >> 63;
+    const unsigned long long add = (rd && wr) ? (c - 1) | (1ull << 32) : (rd ? c : (c << 32));
+    for (uint64_t i = lane; i < len; i += 32) {
+      const uint64_t addr = base_p + ((key + i) << k_p) + low_p;
+      const uint64_t km = (addr - base_m) >> k_m;
+      if (km >= n_keys_m) { atomicOr(flags, (unsigned long long)F_SLOT_RANGE); continue; }
+      atomicAdd(&tab[km], add);
+    }
+  }
+}
+
 }  // namespace
+
+uint64_t launch_pack_all(const void* tab, bool e32, uint64_t n_keys, unsigned long long* cursor, uint64_t* out,
+                         int pass, uint32_t n_sms, cudaStream_t s) {
+  const uint64_t n_chunks = (n_keys + 1023) / 1024;
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n_chunks + XW - 1) / XW, (uint64_t)n_sms * 8));
+  if (e32) pack_all_kernel<uint32_t><<<grid, XT, 0, s>>>(static_cast<const uint32_t*>(tab), n_keys, pass, cursor, out);
+  else pack_all_kernel<unsigned long long><<<grid, XT, 0, s>>>(static_cast<const unsigned long long*>(tab), n_keys,
+                                                               pass, cursor, out);
+  return 1;
+}
+
+void launch_merge_apply(const uint64_t* runs, uint64_t n_runs, uint64_t base_p, uint64_t low_p, uint32_t k_p,
+                        uint64_t base_m, uint32_t k_m, uint64_t n_keys_m, unsigned long long* tab,
+                        unsigned long long* flags, uint32_t n_sms, cudaStream_t s) {
+  if (!n_runs) return;
+  const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n_runs + 7) / 8, (uint64_t)n_sms * 8));
+  merge_apply_kernel<<<grid, 256, 0, s>>>(runs, n_runs, base_p, low_p, k_p, base_m, k_m, n_keys_m, tab, flags);
+}
 
 int launch_pack(const void* tab, bool e32, const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
                 int pass, unsigned long long* cursor, uint64_t* out, uint32_t n_sms, cudaStream_t s) {

@@ -70,7 +70,7 @@ struct KindCounts {
   uint32_t instr = 0, rd = 0, wr = 0, br = 0, wgb = 0, bres = 0;
   // mb*: boundary bits (nibble bit 0), mw*: wg_begin bits (group bit without the variant bit)
   __device__ __forceinline__ void add(const uint32_t w[4], uint32_t& mb0, uint32_t& mb1, uint32_t& mw0,
-                                      uint32_t& mw1) {
+                                      uint32_t& mw1, uint32_t& me0, uint32_t& me1) {
     const uint32_t L0 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
     const uint32_t L1 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
     const uint32_t H0 = ((w[0] >> 4) & 0x0F0F0F0Fu) | (w[1] & 0xF0F0F0F0u);
@@ -83,6 +83,8 @@ struct KindCounts {
     mb1 = H1 & 0x11111111u;
     mw0 = H0 & ~(H0 >> 1) & 0x44444444u;
     mw1 = H1 & ~(H1 >> 1) & 0x44444444u;
+    me0 = H0 & (H0 >> 1) & 0x44444444u;  // wg_end: group bit with the variant bit
+    me1 = H1 & (H1 >> 1) & 0x44444444u;
     wgb += __popc(mw0) + __popc(mw1);
     bres |= (H0 & (H0 >> 3)) | (H1 & (H1 >> 3));  // boundary with the variant bit: barrier / resume
   }
@@ -109,8 +111,8 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   const uint64_t re = min(n, rb + sub_len);
   const int t = threadIdx.x;
   KindCounts kc;
-  long long lb_e0 = -1, lw_e0 = -1;  // last chunk holding a boundary / group begin, and its masks
-  uint32_t lb_m0 = 0, lb_m1 = 0, lw_m0 = 0, lw_m1 = 0;
+  long long lb_e0 = -1, lw_e0 = -1, le_e0 = -1;  // last chunk holding a boundary / wg_begin / wg_end, masks
+  uint32_t lb_m0 = 0, lb_m1 = 0, lw_m0 = 0, lw_m1 = 0, le_m0 = 0, le_m1 = 0;
   unsigned long long amin = ~0ull, amax = 0, aand = ~0ull, aor = 0;
   constexpr int U = 4;  // 16-byte loads in flight per thread
   for (uint64_t base = rb + 16ull * U * t; base < re; base += 16ull * U * P1_THREADS) {
@@ -120,10 +122,11 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t e0 = base + 16 * u;
-      uint32_t mb0, mb1, mw0, mw1;
-      kc.add(w[u], mb0, mb1, mw0, mw1);
+      uint32_t mb0, mb1, mw0, mw1, me0, me1;
+      kc.add(w[u], mb0, mb1, mw0, mw1, me0, me1);
       if (mb0 | mb1) { lb_e0 = (long long)e0; lb_m0 = mb0; lb_m1 = mb1; }
       if (mw0 | mw1) { lw_e0 = (long long)e0; lw_m0 = mw0; lw_m1 = mw1; }
+      if (me0 | me1) { le_e0 = (long long)e0; le_m0 = me0; le_m1 = me1; }
       if (with_stats) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -139,10 +142,11 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
     }
   }
   long long last_bnd = last_nib_event(lb_e0, lb_m0, lb_m1), last_wgb = last_nib_event(lw_e0, lw_m0, lw_m1);
+  long long last_wge = last_nib_event(le_e0, le_m0, le_m1);
   // block reduction
   constexpr int NW = P1_THREADS / 32;
   __shared__ uint32_t s_cnt[NW][6];
-  __shared__ long long s_pos[NW][2];
+  __shared__ long long s_pos[NW][3];
   __shared__ unsigned long long s_addr[NW][4];
   __shared__ long long s_lb;
   uint32_t v[6] = {kc.instr, kc.rd, kc.wr, kc.br, kc.wgb, __reduce_or_sync(0xffffffffu, kc.bres & 0x11111111u) ? 1u : 0u};
@@ -153,6 +157,7 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   for (int o = 16; o > 0; o >>= 1) {
     last_bnd = max(last_bnd, __shfl_xor_sync(0xffffffffu, last_bnd, o));
     last_wgb = max(last_wgb, __shfl_xor_sync(0xffffffffu, last_wgb, o));
+    last_wge = max(last_wge, __shfl_xor_sync(0xffffffffu, last_wge, o));
     if (with_stats) {
       amin = min(amin, __shfl_xor_sync(0xffffffffu, amin, o));
       amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -163,23 +168,23 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
   if (lane == 0) {
 #pragma unroll
     for (int i = 0; i < 6; ++i) s_cnt[warp][i] = v[i];
-    s_pos[warp][0] = last_bnd; s_pos[warp][1] = last_wgb;
+    s_pos[warp][0] = last_bnd; s_pos[warp][1] = last_wgb; s_pos[warp][2] = last_wge;
     s_addr[warp][0] = amin; s_addr[warp][1] = amax; s_addr[warp][2] = aand; s_addr[warp][3] = aor;
   }
   __syncthreads();
   if (t == 0) {
     RangeSum r{};
     uint32_t tot[6] = {0};
-    long long lb = -1, lw = -1;
+    long long lb = -1, lw = -1, le = -1;
     unsigned long long mn = ~0ull, mx = 0, an = ~0ull, o = 0;
     for (int w = 0; w < NW; ++w) {
       for (int i = 0; i < 6; ++i) tot[i] += s_cnt[w][i];
-      lb = max(lb, s_pos[w][0]); lw = max(lw, s_pos[w][1]);
+      lb = max(lb, s_pos[w][0]); lw = max(lw, s_pos[w][1]); le = max(le, s_pos[w][2]);
       mn = min(mn, s_addr[w][0]); mx = max(mx, s_addr[w][1]); an &= s_addr[w][2]; o |= s_addr[w][3];
     }
     r.n_instr = tot[0]; r.n_rd = tot[1]; r.n_wr = tot[2]; r.n_br = tot[3];
     r.n_wgb = tot[4]; r.any_bres = tot[5] ? 1u : 0u;
-    r.last_bnd = lb; r.last_wgb = lw;
+    r.last_bnd = lb; r.last_wgb = lw; r.last_wge = le;
     out[blockIdx.x] = r;
     s_lb = lb;
     atomicAdd(&st->p1_tot[0], (unsigned long long)tot[0]);
@@ -368,7 +373,10 @@ __device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
 // own 2-stage TMA ring -- no CTA barrier inside the loop.  Each lane holds one
 // 16-event row of the tile; a warp scan of packed class counts gives every lane
 // its exact carry-in; lane 31's end state is the next tile's carry-in.
-template <bool DENSE, bool STAGE>
+// compiled-in features (a trace that needs none runs the plain variant)
+enum : int { FEAT_CHECK = 1, FEAT_BINS = 2, FEAT_MARK = 4 };
+
+template <bool DENSE, bool STAGE, int FEAT>
 __global__ void __launch_bounds__(TPB, 2)
     ingest_kernel(const IngestArgs a, const __grid_constant__ CUtensorMap kmap,
                   const __grid_constant__ CUtensorMap pmap) {
@@ -410,33 +418,37 @@ __global__ void __launch_bounds__(TPB, 2)
 
   // ---- carry-in at the start of this warp's range: combine the sub-ranges before it ----
   uint32_t cseg = 0, clid = 0, cbyres = 0, cgseq = 0, cgkey = 0;
+  uint32_t cso = 0, cgo = 0;  // stream check: a segment / a work-group is open
   unsigned long long c_rd = 0, c_wr = 0, c_br = 0;
   {
     const uint32_t c = blockIdx.x * P1_SUB;  // CTA-wide part: sub-ranges [0, c)
-    long long jb = -1, lw = -1;
+    long long jb = -1, lw = -1, lwe = -1;
     uint64_t s_rd = 0, s_wr = 0, s_br = 0, s_wgb = 0;
     for (uint32_t j = t; j < c; j += TPB) {
       const RangeSum& r = a.ranges[j];
       if (r.last_bnd >= 0) jb = max(jb, (long long)j);
       lw = max(lw, (long long)r.last_wgb);
+      lwe = max(lwe, (long long)r.last_wge);
       s_rd += r.n_rd; s_wr += r.n_wr; s_br += r.n_br; s_wgb += r.n_wgb;
     }
-    __shared__ unsigned long long red[NWARP][6];
+    __shared__ unsigned long long red[NWARP][7];
     s_rd = warp_sum(s_rd); s_wr = warp_sum(s_wr); s_br = warp_sum(s_br); s_wgb = warp_sum(s_wgb);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       jb = max(jb, __shfl_xor_sync(0xffffffffu, jb, o));
       lw = max(lw, __shfl_xor_sync(0xffffffffu, lw, o));
+      lwe = max(lwe, __shfl_xor_sync(0xffffffffu, lwe, o));
     }
     if (lane == 0) {
       red[warp][0] = s_rd; red[warp][1] = s_wr; red[warp][2] = s_br; red[warp][3] = s_wgb;
       red[warp][4] = (unsigned long long)jb; red[warp][5] = (unsigned long long)lw;
+      red[warp][6] = (unsigned long long)lwe;
     }
     __syncthreads();
-    jb = -1; lw = -1; s_rd = s_wr = s_br = s_wgb = 0;
+    jb = -1; lw = -1; lwe = -1; s_rd = s_wr = s_br = s_wgb = 0;
     for (int w = 0; w < NWARP; ++w) {
       s_rd += red[w][0]; s_wr += red[w][1]; s_br += red[w][2]; s_wgb += red[w][3];
-      jb = max(jb, (long long)red[w][4]); lw = max(lw, (long long)red[w][5]);
+      jb = max(jb, (long long)red[w][4]); lw = max(lw, (long long)red[w][5]); lwe = max(lwe, (long long)red[w][6]);
     }
     uint64_t s_in = 0;  // instructions after the last boundary: after(jb) + instrs of later sub-ranges
     for (uint32_t j = (uint32_t)(jb + 1) + t; j < c; j += TPB) s_in += a.ranges[j].n_instr;
@@ -457,12 +469,16 @@ __global__ void __launch_bounds__(TPB, 2)
       if (r.last_bnd >= 0) { lbpos = r.last_bnd; after = r.instr_after; }
       else after += r.n_instr;
       if (r.last_wgb >= 0) lw = r.last_wgb;
+      if (r.last_wge >= 0) lwe = r.last_wge;
       s_rd += r.n_rd; s_wr += r.n_wr; s_br += r.n_br; s_wgb += r.n_wgb;
     }
     if (lbpos >= 0) {
       clid = (uint32_t)a.payload[lbpos];
       cbyres = a.kind[lbpos] == AIWC_K_WI_RESUME;
+      // stream check: a segment is open when the last boundary opened one after the last group event
+      cso = (a.kind[lbpos] & 0x20) && lbpos > max(lw, lwe);
     }
+    cgo = lw > lwe;
     cseg = (uint32_t)after;
     c_rd = s_rd; c_wr = s_wr; c_br = s_br;
     cgseq = (uint32_t)s_wgb;
@@ -495,10 +511,11 @@ __global__ void __launch_bounds__(TPB, 2)
   uint4* const wclose = L.closes[warp];
   uint32_t last_ch = ~0u, last_ch2 = ~0u;  // shard: the last two chunks this lane marked
   // key-block bins: this warp range's segment of the bin buffer and its fill
-  const unsigned long long zmask = (DENSE && a.bin_zones) ? *a.bin_zones : 0ull;
+  constexpr bool CHECK = FEAT & FEAT_CHECK, BINS = DENSE && (FEAT & FEAT_BINS), MARKS = DENSE && (FEAT & FEAT_MARK);
+  const unsigned long long zmask = BINS ? *a.bin_zones : 0ull;
   const unsigned long long bin_base0 = c_rd + c_wr;
   uint32_t bfill = 0;
-  if (zmask && lane == 0) a.bin_base[gw] = bin_base0;
+  if (BINS && zmask && lane == 0) a.bin_base[gw] = bin_base0;
 
   for (uint32_t it = 0; it < my_tiles; ++it) {
     const int s = it % STAGES;
@@ -588,6 +605,19 @@ __global__ void __launch_bounds__(TPB, 2)
     }
     uint32_t gkey = Qex ? (uint32_t)pay_at(P, Qex - 1) : cgkey;
     uint32_t gseq = cgseq + ex_wgb;
+    // stream check: is a segment / a work-group open at my row's start?
+    uint32_t so = 0, go = 0;
+    if (CHECK) {
+      so = Pex ? ((K[Pex - 1] >> 5) & 1u) : cso;
+      const uint32_t gx = __ballot_sync(0xffffffffu, p6 != 0) & below;
+      const uint32_t Lx = gx ? 31u - __clz(gx) : 0u;
+      const uint32_t xsrc = __shfl_sync(0xffffffffu, p6 ? (uint32_t)(31 - __clz(p6)) : 0u, Lx);
+      go = gx ? (uint32_t)(K[16 * Lx + xsrc] == AIWC_K_WG_BEGIN) : cgo;
+      // the trace starts with kernel_begin and ends with kernel_end
+      if (e0 == 0 && (w[0] & 0xFFu) != AIWC_K_KERNEL_BEGIN) flags |= F_STREAM;
+      if (n - 1 >= e0 && n - 1 < e0 + 16 && K[16 * lane + (uint32_t)(n - 1 - e0)] != AIWC_K_KERNEL_END)
+        flags |= F_STREAM;
+    }
     // ordered outputs go straight to their global slots (range offset + exclusive rank)
     uint64_t o_rd = c_rd + ex_rd, o_wr = c_wr + ex_wr;
     const uint64_t o_br = c_br + ex_br;
@@ -750,10 +780,10 @@ __global__ void __launch_bounds__(TPB, 2)
           }
         }
       };
-      if (zmask) {
+      if (BINS && zmask) {
         if (hot_n) fold_bins(std::true_type{});
         else fold_bins(std::false_type{});
-      } else if (a.chunk_bits) {
+      } else if (MARKS) {
         if (hot_n) fold(std::true_type{}, std::true_type{});
         else fold(std::false_type{}, std::true_type{});
       } else {
@@ -790,10 +820,41 @@ __global__ void __launch_bounds__(TPB, 2)
     // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
+    const uint32_t metric16 = ins16 | rd16 | wr16 | br16;
+    int last_r = -1;  // stream check: my last structural event so far
     for (uint32_t m = (AIWC_ABL & 8) ? 0u : rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t kk = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
+      if (CHECK) {  // StreamChecker's rules for a trace without barriers / resumes (trace.py:316-404)
+        bool bad = !so && (metric16 & ((1u << j) - 1u) & (0xFFFFFFFFu << (last_r + 1)));  // outside a segment
+        if (kk == AIWC_K_WI_BEGIN) {
+          bad |= !go || so || p >= a.local_volume;
+          // wi_begin for an already-started work-item: every begin sets its (group, lid)
+          // bit (RED, no round trip); finalize compares the set bits with the begins
+          const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + p;
+          if (!bad && gseq && slot < a.dup_len) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
+          else bad = true;
+          so = 1;
+        } else if (kk == AIWC_K_WI_END) {
+          bad |= !so || p != lid || p >= a.local_volume;
+          so = 0;
+        } else if (kk == AIWC_K_WG_BEGIN) {
+          bad |= go || so || (p >> 31);
+          go = 1;
+        } else if (kk == AIWC_K_WG_END) {
+          bad |= !go || so || p != (uint64_t)gkey;
+          go = 0;
+        } else if (kk == AIWC_K_KERNEL_BEGIN) {
+          bad |= e0 + j != 0;
+        } else if (kk == AIWC_K_KERNEL_END) {
+          bad |= e0 + j != n - 1 || go;
+        } else {  // barrier / resume: the launcher checks such traces with the full validator
+          bad = true;
+        }
+        if (bad) flags |= F_STREAM;
+        last_r = (int)j;
+      }
       if (kk & 0x10) {
         if (kk & 0x20) {  // wi_begin / wi_resume opens a segment
           lid = (uint32_t)p; byres = kk >> 7;
@@ -814,6 +875,11 @@ __global__ void __launch_bounds__(TPB, 2)
       }
     }
 #undef PAY
+    if (CHECK) {
+      if (!so && (metric16 & (0xFFFFFFFFu << (last_r + 1)) & 0xFFFFu)) flags |= F_STREAM;  // tail of my row
+      cso = __shfl_sync(0xffffffffu, so, 31);
+      cgo = __shfl_sync(0xffffffffu, go, 31);
+    }
     // ---- the next tile's carry-in: lane 31's end state ----
     const uint32_t nseg = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
     cseg = __shfl_sync(0xffffffffu, nseg, 31);
@@ -847,7 +913,7 @@ __global__ void __launch_bounds__(TPB, 2)
   }
 
   // ---- epilogue: flush CTA-private state ----
-  if (zmask && lane == 0) {
+  if (BINS && zmask && lane == 0) {
     a.bin_fill[gw] = bfill;
     if (bfill) atomicAdd(&st->bin_total, (unsigned long long)bfill);
   }
@@ -969,21 +1035,38 @@ void launch_hot_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n,
   hot_sample_kernel<<<1, HS_T, 0, s>>>(kind, payload, n, am, hot_out);
 }
 
-template <bool DENSE, bool STAGE>
+template <bool DENSE, bool STAGE, int FEAT>
 static cudaError_t launch_variant(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap,
                                   uint32_t n_ctas, cudaStream_t s) {
   const size_t smem = sizeof(StageSmem) + 1024 + 8ull * a.smem_keys;
-  cudaError_t e = set_smem_once(ingest_kernel<DENSE, STAGE>, (int)smem);
+  cudaError_t e = set_smem_once(ingest_kernel<DENSE, STAGE, FEAT>, (int)smem);
   if (e != cudaSuccess) return e;
-  ingest_kernel<DENSE, STAGE><<<n_ctas, TPB, smem, s>>>(a, kmap, pmap);
+  ingest_kernel<DENSE, STAGE, FEAT><<<n_ctas, TPB, smem, s>>>(a, kmap, pmap);
   return cudaGetLastError();
+}
+
+template <bool DENSE, bool STAGE>
+static cudaError_t launch_feat(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
+                               cudaStream_t s) {
+  const int feat = (a.check ? FEAT_CHECK : 0) | (DENSE && a.bin_zones ? FEAT_BINS : 0) |
+                   (DENSE && a.chunk_bits ? FEAT_MARK : 0);
+  switch (feat) {
+    case 0: return launch_variant<DENSE, STAGE, 0>(a, kmap, pmap, n_ctas, s);
+    case FEAT_CHECK: return launch_variant<DENSE, STAGE, FEAT_CHECK>(a, kmap, pmap, n_ctas, s);
+    case FEAT_BINS: return launch_variant<DENSE, STAGE, FEAT_BINS>(a, kmap, pmap, n_ctas, s);
+    case FEAT_BINS | FEAT_CHECK: return launch_variant<DENSE, STAGE, FEAT_BINS | FEAT_CHECK>(a, kmap, pmap, n_ctas, s);
+    case FEAT_MARK: return launch_variant<DENSE, STAGE, FEAT_MARK>(a, kmap, pmap, n_ctas, s);
+    case FEAT_MARK | FEAT_CHECK: return launch_variant<DENSE, STAGE, FEAT_MARK | FEAT_CHECK>(a, kmap, pmap, n_ctas, s);
+    default: return cudaErrorInvalidValue;  // bins and marks never combine (a shard does not bin)
+  }
 }
 
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
                           bool dense, bool stage, cudaStream_t s) {
-  if (dense) return stage ? launch_variant<true, true>(a, kmap, pmap, n_ctas, s)
-                          : launch_variant<true, false>(a, kmap, pmap, n_ctas, s);
-  return launch_variant<false, true>(a, kmap, pmap, n_ctas, s);
+  if (dense) return stage ? launch_feat<true, true>(a, kmap, pmap, n_ctas, s)
+                          : launch_feat<true, false>(a, kmap, pmap, n_ctas, s);
+  return a.check ? launch_variant<false, true, FEAT_CHECK>(a, kmap, pmap, n_ctas, s)
+                 : launch_variant<false, true, 0>(a, kmap, pmap, n_ctas, s);
 }
 
 }  // namespace aiwc

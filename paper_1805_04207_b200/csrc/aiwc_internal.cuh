@@ -65,7 +65,8 @@ __host__ __device__ constexpr bool is_mem(uint32_t k) { return k & 0x06; }
 // error flags raised by kernels (DevState::flags)
 enum : uint64_t {
   F_BAD_OPCODE = 1, F_BAD_WIDTH = 2, F_BAD_SITE = 4, F_ADDR_HINT = 8, F_BAD_GROUP = 16,
-  F_SLOT_RANGE = 32, F_BAD_KIND = 64
+  F_SLOT_RANGE = 32, F_BAD_KIND = 64,
+  F_STREAM = 128  // a StreamChecker invariant is violated (in-pass check; aiwc_validate locates it)
 };
 
 // Per-range summary computed from kind bytes alone (pass 1): what the ingest
@@ -75,6 +76,7 @@ struct RangeSum {
   uint32_t n_instr, n_rd, n_wr, n_br, n_wgb, instr_after;
   uint32_t any_bres, pad;       // a barrier or resume occurs (work-item lifetime slots needed)
   int64_t last_bnd, last_wgb;   // global event index, -1 when absent
+  int64_t last_wge;             // last wg_end, -1 when absent (in-pass stream checks)
 };
 
 // Device-resident accumulator scalars and small tables. The prefix up to
@@ -89,6 +91,7 @@ struct DevState {
   unsigned long long p1_tot[6];                    // pass-1 totals: instr, rd, wr, br, wgb, ranges with bres
   unsigned long long n_obs, n_sites, n_uniq;      // branch observations, #sites, #unique keys (sparse)
   unsigned long long n_wib, n_bar;                 // work-items begun, barriers hit (ingest)
+  unsigned long long dup_set;                      // in-pass stream check: set bits of the begin map
   unsigned long long n_widths_listed, n_sites_listed;
   double entropy[NLEVELS];
   double yokota, linear;
@@ -160,6 +163,11 @@ struct IngestArgs {
   uint32_t* bin_fill;               // [warp ranges]: entries the range appended
   const unsigned long long* bin_zones;  // device zone mask (null / 0: no bins)
   uint32_t zone_shift;
+  // in-pass StreamChecker (trace.py:289-424) of an untrusted trace without barriers /
+  // resumes: sequence rules per lane with carried state, duplicate wi_begin per group
+  uint32_t check;
+  uint32_t* dup_bits;               // [(groups) * local_volume] bits: wi_begin seen
+  uint64_t dup_len;
 };
 
 // ---- stream validation (aiwc_validate.cu) ---------------------------------------
@@ -293,6 +301,11 @@ int launch_pack(const void* tab, bool e32, const uint32_t* all_bits, uint64_t wo
 int launch_apply_runs(void* tab, bool e32, const uint64_t* runs, uint64_t n_runs, uint64_t n_keys,
                       const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
                       unsigned long long* flags, uint32_t n_sms, cudaStream_t s);
+uint64_t launch_pack_all(const void* tab, bool e32, uint64_t n_keys, unsigned long long* cursor, uint64_t* out,
+                         int pass, uint32_t n_sms, cudaStream_t s);
+void launch_merge_apply(const uint64_t* runs, uint64_t n_runs, uint64_t base_p, uint64_t low_p, uint32_t k_p,
+                        uint64_t base_m, uint32_t k_m, uint64_t n_keys_m, unsigned long long* tab,
+                        unsigned long long* flags, uint32_t n_sms, cudaStream_t s);
 int launch_clear_chunks(void* tab, bool e32, uint64_t n_keys, const uint32_t* all_bits, uint64_t words, uint32_t rank,
                         uint32_t nranks, uint32_t* my_bits, uint32_t n_sms, cudaStream_t s);
 void launch_entropy_finish(DevState* st, const double* partials, uint32_t n_parts, uint64_t total_m, uint32_t k,

@@ -78,6 +78,8 @@ class EngineResult:
     used_dense_table: bool
     kernels_launched: int
     binned_accesses: int = 0
+    stream_checked: bool = False
+    state: object = None  # EngineState for a state merge (merge_accumulators), or None
 
 
 def _dist(d) -> tuple:
@@ -122,8 +124,9 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def trace_info(tr: ColumnarTrace) -> _native.TraceInfo:
+def trace_info(tr: ColumnarTrace, check: bool = False) -> _native.TraceInfo:
     info = _native.TraceInfo()
+    info.check_stream = 1 if check else 0
     info.n_events = tr.n_events
     info.local_volume = max(1, tr.local_volume)
     info.n_opcodes = len(tr.opcodes)
@@ -137,12 +140,14 @@ def trace_info(tr: ColumnarTrace) -> _native.TraceInfo:
     return info
 
 
-def ingest_columns(ctx, tr: ColumnarTrace):
+def ingest_columns(ctx, tr: ColumnarTrace, check: bool = False, export: bool = False):
     """aiwc_ingest (device columns) or aiwc_ingest_host (host columns) of one
-    columnar trace into ctx; returns the stream handle the work was queued on."""
+    columnar trace into ctx; returns the stream handle the work was queued on.
+    check: the pass also checks StreamChecker's invariants (untrusted columns)."""
     kind, payload = tr.kind, tr.payload
     lib = ctx.lib
-    info = trace_info(tr)
+    info = trace_info(tr, check)
+    info.export_state = 1 if export else 0
     if _is_torch(kind) and kind.is_cuda:
         import torch
 
@@ -234,8 +239,52 @@ def max_ingest_events() -> int:
     return min(limit, int(env)) if env else limit
 
 
-def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
-    """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace."""
+@dataclass
+class EngineState:
+    """What a later state merge needs of one consumed trace (aiwc_state_export):
+    the per-key memory state as device runs over the trace's key map, and the
+    histograms / tables finalize consumed."""
+
+    runs: object            # torch int64 [2 * n_runs] on the device (key | len << 32, count | r << 62 | w << 63)
+    n_runs: int
+    base: int
+    low_const: int
+    k: int
+    addr_stats: tuple | None
+    itb_hist: np.ndarray
+    ipt_hist: np.ndarray
+    itb_ovf: np.ndarray
+    ipt_ovf: np.ndarray
+    branch_table: np.ndarray
+    width_first: list
+
+
+def _export_state(ctx, res: EngineResult, device: int) -> EngineState | None:
+    import torch
+
+    st = _native.State()
+    ctx.check(ctx.lib.aiwc_state_export(ctx.h, ctypes.byref(st)))
+    if not st.exported:
+        return None
+    arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy() if n else np.zeros(0, np.uint64)  # noqa: E731
+    runs = torch.zeros(2, dtype=torch.int64, device=torch.device("cuda", device))
+    if st.n_runs:
+        iface = {"shape": (2 * st.n_runs,), "typestr": "<i8", "data": (st.runs_dev, False), "version": 3}
+        holder = type("_Runs", (), {"__cuda_array_interface__": iface})()
+        runs = torch.as_tensor(holder, device=torch.device("cuda", device)).clone()
+    m = res.total_reads + res.total_writes
+    return EngineState(runs, int(st.n_runs), int(st.base), int(st.low_const), int(st.k),
+                       tuple(int(v) for v in st.addr_stats) if m else None,
+                       arr(st.itb_hist, 1024), arr(st.ipt_hist, 1024), arr(st.itb_ovf, st.n_itb_ovf),
+                       arr(st.ipt_ovf, st.n_ipt_ovf), arr(st.branch_table, st.branch_table_size),
+                       [int(v) for v in arr(st.width_first, len(res.widths))])
+
+
+def run_engine(tr: ColumnarTrace, device: int | None = None, check: bool = False,
+               export: bool = False) -> EngineResult:
+    """aiwc_reset + aiwc_ingest(_host) + aiwc_finalize on one columnar trace.
+    check: StreamChecker's invariants inside the pass (InvalidStream without a
+    location on a violation; result.stream_checked when the pass certified it)."""
     kind = tr.kind
     if device is None:
         device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
@@ -248,10 +297,14 @@ def run_engine(tr: ColumnarTrace, device: int | None = None) -> EngineResult:
     try:
         lib = ctx.lib
         ctx.check(lib.aiwc_reset(ctx.h))
-        stream = ingest_columns(ctx, tr)
+        stream = ingest_columns(ctx, tr, check, export)
         res = _native.Result()
         ctx.check(lib.aiwc_finalize(ctx.h, ctypes.byref(res), ctypes.c_void_p(stream) if stream else None))
-        return _copy_result(res)
+        out = _copy_result(res)
+        out.stream_checked = bool(res.stream_checked)
+        if export:
+            out.state = _export_state(ctx, out, device)
+        return out
     finally:
         _put_ctx(ctx)
 
@@ -364,7 +417,32 @@ def consume(events: Iterable | ColumnarTrace, *, max_entries: int | None = None,
                 kind = tr.kind
                 device = kind.device.index if (_is_torch(kind) and kind.is_cuda) else _default_device()
             tr = _device_columns(tr, device)
+            res = err = None
+            if tr.n_events <= max_ingest_events():
+                # the ingest checks the invariants of traces without barriers / resumes in
+                # the same pass; only a flagged stream (to locate its first violation) or a
+                # trace the pass cannot certify goes through the separate device checker
+                try:
+                    res = run_engine(tr, device, check=True, export=True)
+                except AiwcError as exc:  # a violation, or malformed data it caused (UnsupportedTrace too)
+                    res, err = None, exc
+                if res is not None and res.stream_checked:
+                    if res.entries > cap:
+                        raise TraceTooLarge(cap + 1, cap)
+                    return KernelAccumulator(
+                        kernel_name=tr.kernel_name, invocations=[tr.invocation],
+                        launches=[(tr.invocation, tuple(tr.global_size), tuple(tr.local_size))],
+                        result=res, opcodes=list(tr.opcodes), trace=tr)
             violation = validate_columnar(tr, device)
+            if violation is None and err is not None:  # a valid stream the engine still refuses
+                raise err
+            if violation is None and res is not None:  # the pass's result stands (barrier traces)
+                if res.entries > cap:
+                    raise TraceTooLarge(cap + 1, cap)
+                return KernelAccumulator(
+                    kernel_name=tr.kernel_name, invocations=[tr.invocation],
+                    launches=[(tr.invocation, tuple(tr.global_size), tuple(tr.local_size))],
+                    result=res, opcodes=list(tr.opcodes), trace=tr)
             if violation is not None and violation[2] != "stream has no kernel_end":
                 # consume() stops before the violating event; finish()'s rule sees every event
                 index = violation[0]
@@ -384,7 +462,7 @@ def consume(events: Iterable | ColumnarTrace, *, max_entries: int | None = None,
             if res.entries > cap:
                 raise TraceTooLarge(cap + 1, cap)
         raise InvalidStream(index, rule, detail)
-    res = run_engine(tr, device)
+    res = run_engine(tr, device, export=True)
     if res.entries > cap:
         raise TraceTooLarge(cap + 1, cap)
     return KernelAccumulator(
@@ -542,9 +620,97 @@ def merge_accumulators(parts: list[KernelAccumulator], *, allow_name_mismatch: b
             per_inv.extend(p.lmae_per_invocation)
         else:
             per_inv.append((p.invocations[0], lmae_profile(p)))
-    tr = concat_traces([p.trace for p in parts])
-    res = run_engine(tr)
     invocations = [i for p in parts for i in p.invocations]
     launches = [l for p in parts for l in p.launches]
+    leaves = _leaves(parts)
+    merged = _state_merge(leaves)  # sums of the parts' exported state: no re-ingest
+    if merged is not None:
+        res, opcodes = merged
+        return KernelAccumulator(parts[0].kernel_name, invocations, launches, res, opcodes, trace=None,
+                                 lmae_per_invocation=per_inv, parts=list(parts))
+    tr = concat_traces([p.trace for p in leaves])
+    res = run_engine(tr)
     return KernelAccumulator(parts[0].kernel_name, invocations, launches, res, list(tr.opcodes), trace=tr,
                              lmae_per_invocation=per_inv, parts=list(parts))
+
+
+def _leaves(parts: list) -> list:
+    """The consumed accumulators under (possibly nested) merges, in order."""
+    out = []
+    for p in parts:
+        if p.parts:
+            out.extend(_leaves(p.parts))
+        else:
+            out.append(p)
+    return out
+
+
+def _state_merge(parts: list):
+    """(EngineResult, opcode names) of the parts merged from their exported state
+    (EngineState), or None when a part has none (sort-path or random-access
+    traces) or the merged address span needs the sort path: the caller re-ingests."""
+    from . import dist as D
+
+    states = [p.result.state for p in parts]
+    if any(s is None for s in states) or any(p._over for p in parts):
+        return None
+    idx: dict = {}
+    for p in parts:
+        for o in p.opcodes:
+            idx.setdefault(o, len(idx))
+    opcode_counts = [0] * len(idx)
+    lists, offset = [], 0
+    itb_hist = np.zeros(1024, np.uint64)
+    ipt_hist = np.zeros(1024, np.uint64)
+    table = None
+    for p, st in zip(parts, states):
+        r = p.result
+        for i, c in enumerate(r.opcode_counts):
+            opcode_counts[idx[p.opcodes[i]]] += int(c)
+        widths = [(w, c, f + offset) for (w, c), f in zip(r.widths, st.width_first)]
+        lists.append((st.itb_ovf.tolist(), st.ipt_ovf.tolist(), widths, dict(r.sites)))
+        itb_hist += st.itb_hist
+        ipt_hist += st.ipt_hist
+        if st.branch_table.size:
+            table = st.branch_table.astype(np.uint64) if table is None else table + st.branch_table
+        offset += r.n_events
+    itb_ovf, ipt_ovf, widths, sites = D._merge_lists(lists)
+    tot = lambda f: sum(int(getattr(p.result, f)) for p in parts)  # noqa: E731
+    total_reads, total_writes = tot("total_reads"), tot("total_writes")
+    total_m = total_reads + total_writes
+    mp = D.MemoryPartial(0, 0, 0, np.zeros(11), np.zeros(D.CBINS, np.uint64), np.zeros(0, np.uint64))
+    if total_m:
+        live = [st for st in states if st.addr_stats is not None]
+        aand, aor = (1 << 64) - 1, 0
+        for st in live:
+            aand &= st.addr_stats[2]
+            aor |= st.addr_stats[3]
+        stats = (min(st.addr_stats[0] for st in live), max(st.addr_stats[1] for st in live), aand, aor)
+        device = live[0].runs.device.index
+        ctx = _get_ctx(device)
+        try:
+            import torch
+
+            rp = (_native.RunsPart * len(live))()
+            for i, st in enumerate(live):
+                rp[i] = _native.RunsPart(st.runs.data_ptr(), st.n_runs, st.base, st.low_const, st.k, 0)
+            out = _native.MemoryPart()
+            s4 = (ctypes.c_uint64 * 4)(*stats)
+            stream = torch.cuda.current_stream(device).cuda_stream
+            rc = ctx.lib.aiwc_memory_merge(ctx.h, rp, len(live), s4, total_m, ctypes.byref(out), ctypes.c_void_p(stream))
+            if rc == _native.ERR_UNSUPPORTED:
+                return None
+            ctx.check(rc)
+            big = np.ctypeslib.as_array(out.big, shape=(out.n_big,)).copy() if out.n_big else np.zeros(0, np.uint64)
+            mp = D.MemoryPartial(out.unique_reads, out.unique_writes, out.footprint, np.array(out.level_sum[:]),
+                                 np.ctypeslib.as_array(out.cnt_hist0, shape=(D.CBINS,)).copy(), big)
+        finally:
+            _put_ctx(ctx)
+    if table is None:
+        table = np.zeros(1 << 16, np.uint64)
+    res = D._assemble(tot("n_events"), tot("total_instructions"), tot("work_items"), tot("barriers_hit"), total_reads,
+                      total_writes, sum(int(p.result.itb[3]) for p in parts), sum(int(p.result.ipt[3]) for p in parts),
+                      tot("branch_executions"), opcode_counts, itb_hist, itb_ovf, ipt_hist, ipt_ovf, table, widths,
+                      sites, mp.unique_reads, mp.unique_writes, mp.footprint, mp.cnt_hist0.astype(np.uint64),
+                      np.sort(mp.big.astype(np.uint64))[::-1], np.asarray(mp.level_sum, dtype=np.float64))
+    return res, [o for o, _ in sorted(idx.items(), key=lambda kv: kv[1])]

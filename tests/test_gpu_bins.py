@@ -59,7 +59,7 @@ def test_binned_reports_match_unbinned_and_reference():
     for name in binned:
         binned[name].pop("__binned", None)
         plain[name].pop("__binned", None)
-    want = {c["name"]: c["report"] for c, _ in golden_cases()}
+    want = {c["name"]: c["report"] for c, _ in golden_cases() if "report" in c}
     for name, rep in binned.items():
         assert_report_matches(rep, plain[name])
         if name in want:

@@ -151,3 +151,32 @@ def test_consume_raises_for_untrusted_columns():
         consume(bad, max_entries=1 << 40)
     assert (ei.value.event_index, ei.value.rule) == want[:2]
     assert str(ei.value).endswith(f"({want[2]})")
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_in_pass_check_is_complete(seed):
+    """consume()'s in-pass StreamChecker (untrusted columns without barriers /
+    resumes, checked inside the ingest): it never certifies an invalid stream,
+    and it certifies every valid one it is meant to cover."""
+    from paper_1805_04207_b200 import AiwcError, UnsupportedTrace
+    from paper_1805_04207_b200.metrics import _device_columns, run_engine
+
+    rng = random.Random(5000 + seed)
+    traces = _traces()
+    certified_valid = 0
+    for _ in range(60):
+        name, tr = rng.choice(traces)
+        if len(tr.opcodes) == 0:
+            continue
+        mt = _mutate(tr, rng) if rng.random() < 0.8 else tr
+        want = _expected(mt)
+        try:
+            certified = run_engine(_device_columns(mt, 0), 0, check=True).stream_checked
+        except (AiwcError, UnsupportedTrace):
+            certified = False
+        if want is not None:
+            assert not certified, (name, seed, want)
+        elif not np.isin(np.asarray(mt.kind), [0x90, 0xB0]).any():
+            assert certified, (name, seed)
+            certified_valid += 1
+    assert certified_valid
