@@ -197,6 +197,7 @@ struct aiwc_ctx {
   uint64_t state_n_runs = 0;
   bool state_ok = false;
   uint64_t stats4[4] = {};  // address statistics the key map was built from
+  uint64_t state_cap = 0;
   Buf bin_seg, bin_base, bin_fill, bin_scr;
   int dense_entry = 0;      // AIWC_DENSE_ENTRY=32|64 forces the entry width (measurement), 0 = rule
   uint64_t ipt_tab_len = 0;
@@ -917,23 +918,16 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
       // larger table would cost a sizeable part of its ingest; such merges re-ingest)
       if (ctx->info.export_state && !ctx->remap_pay.p &&
           dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8) <= (512ull << 20)) {
-        CK(grow(ctx->state_cur, 8));
-        unsigned long long* cur = P<unsigned long long>(ctx->state_cur);
-        CK(cudaMemsetAsync(cur, 0, 8, s));
-        launch_pack_all(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, cur, nullptr, 0, (uint32_t)ctx->n_sms, s);
-        unsigned long long nr = 0;
-        CK(cudaMemcpyAsync(&nr, cur, 8, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        // kept only when the runs compress the table (streaming / strided traces): a
-        // random-access trace's state would be as large as its table -- its merge re-ingests
-        const bool keep = nr <= ctx->am.n_keys / 4 || nr * 16 <= (256ull << 20);
-        if (keep) CK(grow(ctx->state_runs, std::max<uint64_t>(nr, 1) * 16));
-        CK(cudaMemsetAsync(cur, 0, 8, s));
-        if (nr && keep) launch_pack_all(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, cur, P<uint64_t>(ctx->state_runs), 1,
-                                (uint32_t)ctx->n_sms, s);
-        ctx->state_n_runs = keep ? nr : 0;
-        ctx->state_ok = keep;
-        ctx->kernels += 2;
+        // one pass, no round trip: runs are claimed chunk by chunk into a buffer of a
+        // quarter run per key (runs that do not compress the table that much -- random
+        // accesses -- overflow it and the state is dropped: such merges re-ingest)
+        const uint64_t cap = std::max<uint64_t>(1ull << 16, ctx->am.n_keys / 4);
+        CK(grow(ctx->state_runs, cap * 16));
+        launch_pack_all(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, &st->state_runs_n, P<uint64_t>(ctx->state_runs), 1,
+                        (uint32_t)ctx->n_sms, s, cap);
+        ctx->state_cap = cap;
+        ctx->state_ok = true;  // confirmed against the claimed count after the state read below
+        ctx->kernels += 1;
       }
       // the table is clean again for the next trace: clear it on the side stream now
       CK(cudaEventRecord(ctx->fork_ev, s));
@@ -988,6 +982,10 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     const bool ok = h.addr_min >= am.base && h.addr_max <= am.hi && ((h.addr_and ^ h.addr_or) & am.low_mask) == 0 &&
                     ((h.addr_min - am.base) & am.low_mask) == am.low_const;
     if (!ok) h.flags |= F_ADDR_HINT;
+  }
+  if (ctx->state_ok) {  // the exported runs fit their buffer?
+    ctx->state_n_runs = h.state_runs_n;
+    ctx->state_ok = h.state_runs_n <= ctx->state_cap;
   }
   // every wi_begin set its own (group, lid) bit: fewer set bits than begins = a duplicate
   if (ctx->stream_checked && ctx->info.n_events && h.dup_set != h.n_wib) h.flags |= F_STREAM;

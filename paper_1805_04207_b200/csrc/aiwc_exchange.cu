@@ -174,7 +174,7 @@ __device__ __forceinline__ uint64_t entry64<unsigned long long>(unsigned long lo
 template <typename E>
 __global__ void __launch_bounds__(XT) pack_all_kernel(const E* __restrict__ tab, uint64_t n_keys, int pass,
                                                       unsigned long long* __restrict__ cursor,
-                                                      uint64_t* __restrict__ out) {
+                                                      uint64_t* __restrict__ out, uint64_t cap) {
   __shared__ uint32_t s_bm[XW][33];
   __shared__ uint32_t s_pre[XW][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(XT) pack_all_kernel(const E* __restrict__ tab,
     __syncwarp();
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(cursor, (unsigned long long)total);
-    if (pass == 1) {
-      base = __shfl_sync(0xffffffffu, base, 0);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (pass == 1 && base + total <= cap) {  // (runs in chunk-claim order: a merge does not care)
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
         const uint32_t hm = __shfl_sync(0xffffffffu, hm_lane, q);
@@ -259,12 +259,13 @@ __global__ void merge_apply_kernel(const uint64_t* __restrict__ runs, uint64_t n
 }  // namespace
 
 uint64_t launch_pack_all(const void* tab, bool e32, uint64_t n_keys, unsigned long long* cursor, uint64_t* out,
-                         int pass, uint32_t n_sms, cudaStream_t s) {
+                         int pass, uint32_t n_sms, cudaStream_t s, uint64_t cap) {
   const uint64_t n_chunks = (n_keys + 1023) / 1024;
   const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n_chunks + XW - 1) / XW, (uint64_t)n_sms * 8));
-  if (e32) pack_all_kernel<uint32_t><<<grid, XT, 0, s>>>(static_cast<const uint32_t*>(tab), n_keys, pass, cursor, out);
+  if (e32) pack_all_kernel<uint32_t><<<grid, XT, 0, s>>>(static_cast<const uint32_t*>(tab), n_keys, pass, cursor, out,
+                                                         cap);
   else pack_all_kernel<unsigned long long><<<grid, XT, 0, s>>>(static_cast<const unsigned long long*>(tab), n_keys,
-                                                               pass, cursor, out);
+                                                               pass, cursor, out, cap);
   return 1;
 }
 

@@ -605,18 +605,47 @@ __global__ void __launch_bounds__(TPB, 2)
     }
     uint32_t gkey = Qex ? (uint32_t)pay_at(P, Qex - 1) : cgkey;
     uint32_t gseq = cgseq + ex_wgb;
-    // stream check: is a segment / a work-group open at my row's start?
+    // ---- stream check, bit-parallel over my row (no per-event branches) ----
+    // Segment events (opens / closes) and group events (wg_begin / wg_end) must each
+    // alternate; given that, the open / closed state at every position is a parity:
+    // the carried state XOR the boundaries up to it.  The state at my row's start is the
+    // tile's carried state XOR the parity of all lower lanes' boundaries (one ballot).
     uint32_t so = 0, go = 0;
     if (CHECK) {
-      so = Pex ? ((K[Pex - 1] >> 5) & 1u) : cso;
-      const uint32_t gx = __ballot_sync(0xffffffffu, p6 != 0) & below;
-      const uint32_t Lx = gx ? 31u - __clz(gx) : 0u;
-      const uint32_t xsrc = __shfl_sync(0xffffffffu, p6 ? (uint32_t)(31 - __clz(p6)) : 0u, Lx);
-      go = gx ? (uint32_t)(K[16 * Lx + xsrc] == AIWC_K_WG_BEGIN) : cgo;
+      const uint32_t ko = bnd16 & p5 & ~p7;                      // wi_begin (wi_resume is not covered)
+      const uint32_t kc = bnd16 & ~p5;                           // wi_end / barrier
+      const uint32_t gb = wgb16, ge = p6 & p7;                   // wg_begin, wg_end
+      const uint32_t kb = p5 & ~bnd16 & ~p6 & ~p7, ke = p5 & ~bnd16 & ~p6 & p7;  // kernel begin / end
+      const uint32_t X = bnd16, G = gb | ge;
+      so = cso ^ (__popc(__ballot_sync(0xffffffffu, __popc(X) & 1u) & below) & 1u);
+      go = cgo ^ (__popc(__ballot_sync(0xffffffffu, __popc(G) & 1u) & below) & 1u);
+      // inclusive / exclusive prefix parities (bit j: boundaries at positions <= j / < j)
+      uint32_t px = X, pg = G;
+      px ^= px << 1; px ^= px << 2; px ^= px << 4; px ^= px << 8;
+      pg ^= pg << 1; pg ^= pg << 2; pg ^= pg << 4; pg ^= pg << 8;
+      const uint32_t seg_in = ((so ? 0xFFFFu : 0u) ^ px) & 0xFFFFu;          // segment open after position j
+      const uint32_t seg_before = seg_in ^ X;                                 // ... before position j
+      const uint32_t grp_in = ((go ? 0xFFFFu : 0u) ^ pg) & 0xFFFFu, grp_before = grp_in ^ G;
+      const uint32_t metric16 = ins16 | rd16 | wr16 | br16;
+      const uint32_t bad =
+          (metric16 & ~seg_in) |                  // metric event outside a segment
+          (ko & seg_before) | (kc & ~seg_before) |  // segments alternate: open when closed, close when open
+          (X & ~grp_before) |                     // work-item events inside a work-group only
+          (gb & grp_before) | (ge & ~grp_before) |  // groups alternate
+          (G & seg_before) |                      // no group event inside a segment
+          (bnd16 & p7 & ~kc) |                    // wi_resume: the full validator's case
+          (kb & ~(e0 == 0 ? 1u : 0u)) |           // kernel_begin is event 0 ...
+          (ke & ~((n - 1 >= e0 && n - 1 < e0 + 16) ? (1u << (uint32_t)(n - 1 - e0)) : 0u)) |  // ... kernel_end the last
+          (ke & grp_before);                      // ... with no work-group open
+      if (bad) flags |= F_STREAM;
       // the trace starts with kernel_begin and ends with kernel_end
-      if (e0 == 0 && (w[0] & 0xFFu) != AIWC_K_KERNEL_BEGIN) flags |= F_STREAM;
-      if (n - 1 >= e0 && n - 1 < e0 + 16 && K[16 * lane + (uint32_t)(n - 1 - e0)] != AIWC_K_KERNEL_END)
-        flags |= F_STREAM;
+      if (e0 == 0 && !(kb & 1u)) flags |= F_STREAM;
+      if (n - 1 >= e0 && n - 1 < e0 + 16 && !((ke >> (uint32_t)(n - 1 - e0)) & 1u)) flags |= F_STREAM;
+      // the next tile's carried state
+      const uint32_t all_x = __popc(__ballot_sync(0xffffffffu, __popc(X) & 1u)) & 1u;
+      const uint32_t all_g = __popc(__ballot_sync(0xffffffffu, __popc(G) & 1u)) & 1u;
+      cso ^= all_x;
+      cgo ^= all_g;
     }
     // ordered outputs go straight to their global slots (range offset + exclusive rank)
     uint64_t o_rd = c_rd + ex_rd, o_wr = c_wr + ex_wr;
@@ -820,40 +849,26 @@ __global__ void __launch_bounds__(TPB, 2)
     // rare events in stream order: segment opens / closes, groups
     const uint64_t klo = (uint64_t)w[0] | ((uint64_t)w[1] << 32), khi = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     int last_b = -1;  // my last boundary position so far
-    const uint32_t metric16 = ins16 | rd16 | wr16 | br16;
-    int last_r = -1;  // stream check: my last structural event so far
     for (uint32_t m = (AIWC_ABL & 8) ? 0u : rare16; m; m &= m - 1) {
       const uint32_t j = __ffs(m) - 1;
       const uint32_t kk = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
-      if (CHECK) {  // StreamChecker's rules for a trace without barriers / resumes (trace.py:316-404)
-        bool bad = !so && (metric16 & ((1u << j) - 1u) & (0xFFFFFFFFu << (last_r + 1)));  // outside a segment
+      if (CHECK) {  // the payload rules (the sequence rules were checked on the masks above)
+        bool bad = false;
         if (kk == AIWC_K_WI_BEGIN) {
-          bad |= !go || so || p >= a.local_volume;
           // wi_begin for an already-started work-item: every begin sets its (group, lid)
           // bit (RED, no round trip); finalize compares the set bits with the begins
           const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + p;
-          if (!bad && gseq && slot < a.dup_len) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
-          else bad = true;
-          so = 1;
+          bad = p >= a.local_volume || !gseq || slot >= a.dup_len;
+          if (!bad) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
         } else if (kk == AIWC_K_WI_END) {
-          bad |= !so || p != lid || p >= a.local_volume;
-          so = 0;
+          bad = p != lid || p >= a.local_volume;
         } else if (kk == AIWC_K_WG_BEGIN) {
-          bad |= go || so || (p >> 31);
-          go = 1;
+          bad = (p >> 31) != 0;
         } else if (kk == AIWC_K_WG_END) {
-          bad |= !go || so || p != (uint64_t)gkey;
-          go = 0;
-        } else if (kk == AIWC_K_KERNEL_BEGIN) {
-          bad |= e0 + j != 0;
-        } else if (kk == AIWC_K_KERNEL_END) {
-          bad |= e0 + j != n - 1 || go;
-        } else {  // barrier / resume: the launcher checks such traces with the full validator
-          bad = true;
+          bad = p != (uint64_t)gkey;
         }
         if (bad) flags |= F_STREAM;
-        last_r = (int)j;
       }
       if (kk & 0x10) {
         if (kk & 0x20) {  // wi_begin / wi_resume opens a segment
@@ -875,11 +890,6 @@ __global__ void __launch_bounds__(TPB, 2)
       }
     }
 #undef PAY
-    if (CHECK) {
-      if (!so && (metric16 & (0xFFFFFFFFu << (last_r + 1)) & 0xFFFFu)) flags |= F_STREAM;  // tail of my row
-      cso = __shfl_sync(0xffffffffu, so, 31);
-      cgo = __shfl_sync(0xffffffffu, go, 31);
-    }
     // ---- the next tile's carry-in: lane 31's end state ----
     const uint32_t nseg = __popc(ins16 >> (last_b + 1)) + (last_b < 0 ? seg_in : 0u);
     cseg = __shfl_sync(0xffffffffu, nseg, 31);

@@ -92,6 +92,7 @@ struct DevState {
   unsigned long long n_obs, n_sites, n_uniq;      // branch observations, #sites, #unique keys (sparse)
   unsigned long long n_wib, n_bar;                 // work-items begun, barriers hit (ingest)
   unsigned long long dup_set;                      // in-pass stream check: set bits of the begin map
+  unsigned long long state_runs_n;                 // state export: runs claimed (kept when <= capacity)
   unsigned long long n_widths_listed, n_sites_listed;
   double entropy[NLEVELS];
   double yokota, linear;
@@ -302,7 +303,7 @@ int launch_apply_runs(void* tab, bool e32, const uint64_t* runs, uint64_t n_runs
                       const uint32_t* all_bits, uint64_t words, uint32_t rank, uint32_t nranks,
                       unsigned long long* flags, uint32_t n_sms, cudaStream_t s);
 uint64_t launch_pack_all(const void* tab, bool e32, uint64_t n_keys, unsigned long long* cursor, uint64_t* out,
-                         int pass, uint32_t n_sms, cudaStream_t s);
+                         int pass, uint32_t n_sms, cudaStream_t s, uint64_t cap = ~0ull);
 void launch_merge_apply(const uint64_t* runs, uint64_t n_runs, uint64_t base_p, uint64_t low_p, uint32_t k_p,
                         uint64_t base_m, uint32_t k_m, uint64_t n_keys_m, unsigned long long* tab,
                         unsigned long long* flags, uint32_t n_sms, cudaStream_t s);

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <tuple>
@@ -852,6 +853,267 @@ PyObject* py_encode_lines(PyObject*, PyObject* args) {
   return finish(w, pending ? 2 : rc, last_line, pending);
 }
 
+// ---- encode_lines_fast: the canonical lines of an .aiwctrace file on all host threads ----
+// Every line after the header must be a canonical, decodable event line (no
+// comments, no other forms) and pass the per-event checks that the columnar
+// layout cannot carry (id arithmetic, a work-item's group = the open group);
+// then chunks of lines are parsed in parallel into columns with chunk-local
+// opcode / out-of-grid group dictionaries, merged in first-appearance order.
+// The stream invariants are NOT checked here: the columns are handed to the
+// engine as untrusted (the in-pass check / device validator).  Returns None
+// whenever the sequential walker must decide (its errors are exact).
+struct FastChunk {
+  std::vector<uint8_t> kind;
+  std::vector<uint64_t> pay;
+  std::unordered_map<std::string, uint32_t> opc;
+  std::vector<std::string> opc_order;
+  std::unordered_map<V3, uint32_t, V3Hash> extra;
+  std::vector<V3> extra_order;
+  bool failed = false;
+  bool has_gb = false, pre = false, pre_mismatch = false;
+  V3 last_gb{}, pre_g{};
+  uint64_t amin = ~0ull, amax = 0, aand = ~0ull, aor = 0, n_mem = 0;
+  uint64_t c_instr = 0, c_rd = 0, c_wr = 0, c_br = 0, c_wgb = 0, c_bres = 0;
+};
+
+constexpr uint64_t EXTRA_TAG = 1ull << 63;  // chunk-local out-of-grid group key, remapped at the merge
+
+void parse_chunk(const char* b, const char* e, const V3& lsz, const V3& grid, FastChunk* out) {
+  FastChunk& ch = *out;
+  auto gkey = [&](const V3& g) -> uint64_t {
+    bool in = true;
+    for (int d = 0; d < 3; ++d) in = in && g.v[d] < grid.v[d];
+    if (in) return (uint64_t)(g.v[0] + grid.v[0] * (g.v[1] + grid.v[1] * g.v[2]));
+    auto it = ch.extra.find(g);
+    if (it != ch.extra.end()) return EXTRA_TAG | it->second;
+    const uint32_t k = (uint32_t)ch.extra_order.size();
+    ch.extra.emplace(g, k);
+    ch.extra_order.push_back(g);
+    return EXTRA_TAG | k;
+  };
+  const char* p = b;
+  while (p < e) {
+    const char* nl = static_cast<const char*>(memchr(p, '\n', (size_t)(e - p)));
+    const char* le = nl ? nl : e;
+    Cur c{p, le};
+    p = nl ? nl + 1 : e;
+    if (!c.lit("{\"ev\":\"")) { ch.failed = true; return; }
+    if (c.lit("instr\",\"opcode\":")) {
+      const char* s; size_t n; uint64_t width;
+      if (!c.str(&s, &n) || !c.lit(",\"width\":") || !c.uint(&width) || !c.end() || width == 0 || width >= (1ull << 32)) {
+        ch.failed = true; return;
+      }
+      for (size_t k = 0; k < n; ++k) if ((unsigned char)s[k] >= 0x80) { ch.failed = true; return; }
+      std::string key(s, n);
+      auto it = ch.opc.find(key);
+      uint32_t id;
+      if (it == ch.opc.end()) {
+        id = (uint32_t)ch.opc_order.size();
+        ch.opc.emplace(key, id);
+        ch.opc_order.push_back(std::move(key));
+      } else {
+        id = it->second;
+      }
+      ch.kind.push_back(AIWC_K_INSTR); ch.pay.push_back(((uint64_t)id << 32) | width);
+      ++ch.c_instr;
+    } else if (c.lit("mem\",\"op\":\"")) {
+      uint8_t k;
+      if (c.lit("load\"")) k = AIWC_K_LOAD;
+      else if (c.lit("store\"")) k = AIWC_K_STORE;
+      else if (c.lit("atomic_load\"")) k = AIWC_K_ATOMIC_LOAD;
+      else if (c.lit("atomic_store\"")) k = AIWC_K_ATOMIC_STORE;
+      else { ch.failed = true; return; }
+      uint64_t addr;
+      if (!c.lit(",\"addr\":") || !c.uint(&addr) || !c.end()) { ch.failed = true; return; }
+      ch.kind.push_back(k); ch.pay.push_back(addr);
+      ch.amin = std::min(ch.amin, addr); ch.amax = std::max(ch.amax, addr); ch.aand &= addr; ch.aor |= addr;
+      ++ch.n_mem;
+      if (k & 0x02) ++ch.c_rd; else ++ch.c_wr;
+    } else if (c.lit("branch\",\"site\":")) {
+      uint64_t site; int taken;
+      if (!c.uint(&site) || site >= (1ull << 32) || !c.lit(",\"taken\":")) { ch.failed = true; return; }
+      if (c.lit("true")) taken = 1;
+      else if (c.lit("false")) taken = 0;
+      else { ch.failed = true; return; }
+      if (!c.end()) { ch.failed = true; return; }
+      ch.kind.push_back(AIWC_K_BRANCH); ch.pay.push_back((site << 1) | (uint64_t)taken);
+      ++ch.c_br;
+    } else if (c.lit("barrier\"")) {
+      if (!c.end()) { ch.failed = true; return; }
+      ch.kind.push_back(AIWC_K_BARRIER); ch.pay.push_back(0);
+      ch.c_bres = 1;
+    } else if (c.lit("kernel_end\"")) {
+      if (!c.end()) { ch.failed = true; return; }
+      ch.kind.push_back(AIWC_K_KERNEL_END); ch.pay.push_back(0);
+    } else if (c.lit("wg_")) {
+      bool begin;
+      if (c.lit("begin\",\"group\":")) begin = true;
+      else if (c.lit("end\",\"group\":")) begin = false;
+      else { ch.failed = true; return; }
+      V3 g;
+      if (!c.v3(&g) || !c.end()) { ch.failed = true; return; }
+      ch.kind.push_back(begin ? AIWC_K_WG_BEGIN : AIWC_K_WG_END); ch.pay.push_back(gkey(g));
+      if (begin) { ch.has_gb = true; ch.last_gb = g; ++ch.c_wgb; }
+    } else {
+      uint8_t k;
+      if (c.lit("wi_begin\"")) k = AIWC_K_WI_BEGIN;
+      else if (c.lit("wi_resume\"")) k = AIWC_K_WI_RESUME;
+      else if (c.lit("wi_end\"")) k = AIWC_K_WI_END;
+      else { ch.failed = true; return; }  // kernel_begin in the body, unknown events: the walker decides
+      V3 gid, lid, g;
+      if (!c.lit(",\"global\":") || !c.v3(&gid) || !c.lit(",\"local\":") || !c.v3(&lid) || !c.lit(",\"group\":") ||
+          !c.v3(&g) || !c.end()) {
+        ch.failed = true; return;
+      }
+      for (int d = 0; d < 3; ++d)  // wi.id_arithmetic (trace.py:406-418): the columns keep only the local id
+        if (lid.v[d] >= lsz.v[d] || gid.v[d] != g.v[d] * lsz.v[d] + lid.v[d]) { ch.failed = true; return; }
+      // the work-item's group must be the open group: the last wg_begin (in an earlier chunk: checked at the merge)
+      if (ch.has_gb) {
+        if (!(g == ch.last_gb)) { ch.failed = true; return; }
+      } else if (!ch.pre) {
+        ch.pre = true; ch.pre_g = g;
+      } else if (!(g == ch.pre_g)) {
+        ch.pre_mismatch = true;
+      }
+      ch.kind.push_back(k); ch.pay.push_back((uint64_t)(lid.v[0] + lsz.v[0] * (lid.v[1] + lsz.v[1] * lid.v[2])));
+      if (k == AIWC_K_WI_RESUME) ch.c_bres = 1;
+    }
+  }
+}
+
+PyObject* py_encode_lines_fast(PyObject*, PyObject* args) {
+  Py_buffer buf;
+  int threads;
+  if (!PyArg_ParseTuple(args, "y*i", &buf, &threads)) return nullptr;
+  const char* b = static_cast<const char*>(buf.buf);
+  const char* end = b + buf.len;
+  auto none = [&]() { PyBuffer_Release(&buf); Py_RETURN_NONE; };
+  if (buf.len == 0) return none();
+  // the header: a canonical kernel_begin on line 1
+  const char* nl = static_cast<const char*>(memchr(b, '\n', (size_t)(end - b)));
+  if (!nl) return none();
+  Walker w;
+  OpDict d;
+  w.opc_dict = PyDict_New();
+  w.opc_list = PyList_New(0);
+  Rec hr;
+  PyObject* tmp[2] = {nullptr, nullptr};
+  const int got = parse_canonical(w, d, b, nl, &hr, tmp);
+  auto bail = [&]() -> PyObject* {
+    Py_XDECREF(tmp[0]); Py_XDECREF(tmp[1]);
+    Py_XDECREF(w.opc_dict); Py_XDECREF(w.opc_list);
+    PyBuffer_Release(&buf);
+    Py_RETURN_NONE;
+  };
+  if (got != 1 || hr.c != E_KB) { PyErr_Clear(); return bail(); }
+  V3 lsz = hr.lsz, grid;
+  for (int dd = 0; dd < 3; ++dd) grid.v[dd] = (hr.gsz.v[dd] + lsz.v[dd] - 1) / lsz.v[dd];
+  if ((uint64_t)(grid.v[0] * grid.v[1] * grid.v[2]) >= (1ull << 31) || (uint64_t)(lsz.v[0] * lsz.v[1] * lsz.v[2]) >= (1ull << 31))
+    return bail();
+  // chunks of whole lines
+  const char* body = nl + 1;
+  const int T = std::max(1, std::min(threads, 64));
+  std::vector<const char*> cuts{body};
+  for (int t = 1; t < T; ++t) {
+    const char* q = body + (end - body) * t / T;
+    if (q <= cuts.back()) continue;
+    const char* n2 = static_cast<const char*>(memchr(q, '\n', (size_t)(end - q)));
+    if (!n2) break;
+    if (n2 + 1 > cuts.back() && n2 + 1 < end) cuts.push_back(n2 + 1);
+  }
+  cuts.push_back(end);
+  const size_t C = cuts.size() - 1;
+  std::vector<FastChunk> ch(C);
+  Py_BEGIN_ALLOW_THREADS
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < C; ++i) th.emplace_back(parse_chunk, cuts[i], cuts[i + 1], std::cref(lsz), std::cref(grid), &ch[i]);
+  for (auto& t : th) t.join();
+  Py_END_ALLOW_THREADS
+  // a trailing newline leaves an empty last line: the reference's iterator skips nothing else
+  bool fail = false;
+  bool have_gb = false;
+  V3 open_g{};
+  for (size_t i = 0; i < C && !fail; ++i) {
+    fail = ch[i].failed || ch[i].pre_mismatch || (ch[i].pre && (!have_gb || !(ch[i].pre_g == open_g)));
+    if (ch[i].has_gb) { have_gb = true; open_g = ch[i].last_gb; }
+  }
+  if (fail) return bail();
+  // dictionaries in first-appearance order, then the remap of each chunk
+  std::unordered_map<std::string, uint64_t>& gop = d.str_ids;
+  std::vector<std::vector<uint64_t>> omap(C), xmap(C);
+  std::unordered_map<V3, uint64_t, V3Hash> gx;
+  std::vector<V3> gx_order;
+  const uint64_t n_grid = (uint64_t)(grid.v[0] * grid.v[1] * grid.v[2]);
+  for (size_t i = 0; i < C; ++i) {
+    for (auto& o : ch[i].opc_order) {
+      uint64_t id;
+      if (opcode_id_str(w, d, o.data(), o.size(), &id) < 0) { PyErr_Clear(); return bail(); }
+      omap[i].push_back(id);
+    }
+    for (auto& g : ch[i].extra_order) {
+      auto it = gx.find(g);
+      if (it == gx.end()) { it = gx.emplace(g, n_grid + gx_order.size()).first; gx_order.push_back(g); }
+      xmap[i].push_back(it->second);
+    }
+  }
+  (void)gop;
+  std::vector<size_t> off(C + 1, 1);
+  for (size_t i = 0; i < C; ++i) off[i + 1] = off[i] + ch[i].kind.size();
+  const size_t N = off[C];
+  PyObject* kinds = PyBytes_FromStringAndSize(nullptr, (Py_ssize_t)N);
+  PyObject* pays = PyBytes_FromStringAndSize(nullptr, (Py_ssize_t)(N * 8));
+  if (!kinds || !pays) { Py_XDECREF(kinds); Py_XDECREF(pays); return bail(); }
+  uint8_t* K = reinterpret_cast<uint8_t*>(PyBytes_AS_STRING(kinds));
+  uint64_t* P = reinterpret_cast<uint64_t*>(PyBytes_AS_STRING(pays));
+  K[0] = AIWC_K_KERNEL_BEGIN; P[0] = 0;
+  Py_BEGIN_ALLOW_THREADS
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < C; ++i)
+    th.emplace_back([&, i]() {
+      const FastChunk& c = ch[i];
+      uint8_t* k = K + off[i];
+      uint64_t* q = P + off[i];
+      memcpy(k, c.kind.data(), c.kind.size());
+      for (size_t j = 0; j < c.kind.size(); ++j) {
+        uint64_t v = c.pay[j];
+        if (c.kind[j] == AIWC_K_INSTR) v = (omap[i][v >> 32] << 32) | (v & 0xFFFFFFFFull);
+        else if ((c.kind[j] & 0x40) && (v & EXTRA_TAG)) v = xmap[i][v & 0xFFFFFFFFull];
+        q[j] = v;
+      }
+    });
+  for (auto& t : th) t.join();
+  Py_END_ALLOW_THREADS
+  uint64_t amin = ~0ull, amax = 0, aand = ~0ull, aor = 0, n_mem = 0, cnt[6] = {0, 0, 0, 0, 0, 0};
+  for (auto& c : ch) {
+    if (c.n_mem) { amin = std::min(amin, c.amin); amax = std::max(amax, c.amax); aand &= c.aand; aor |= c.aor; }
+    n_mem += c.n_mem;
+    cnt[0] += c.c_instr; cnt[1] += c.c_rd; cnt[2] += c.c_wr; cnt[3] += c.c_br; cnt[4] += c.c_wgb;
+    cnt[5] |= c.c_bres;
+  }
+  PyObject* extras = PyList_New((Py_ssize_t)gx_order.size());
+  for (size_t k = 0; k < gx_order.size(); ++k)
+    PyList_SET_ITEM(extras, k, Py_BuildValue("(LLL)", gx_order[k].v[0], gx_order[k].v[1], gx_order[k].v[2]));
+  PyObject* stats = Py_None;
+  Py_INCREF(Py_None);
+  if (n_mem) {
+    Py_DECREF(Py_None);
+    stats = Py_BuildValue("(KKKK)", (unsigned long long)amin, (unsigned long long)amax, (unsigned long long)aand,
+                          (unsigned long long)aor);
+  }
+  PyObject* counts = Py_BuildValue("(KKKKKK)", (unsigned long long)cnt[0], (unsigned long long)cnt[1],
+                                   (unsigned long long)cnt[2], (unsigned long long)cnt[3], (unsigned long long)cnt[4],
+                                   (unsigned long long)cnt[5]);
+  PyObject* out = Py_BuildValue("{s:N,s:N,s:O,s:O,s:(LLL),s:(LLL),s:O,s:N,s:N,s:N,s:L}", "kind", kinds, "payload",
+                                pays, "kernel_name", hr.name, "invocation", hr.inv, "global_size", hr.gsz.v[0],
+                                hr.gsz.v[1], hr.gsz.v[2], "local_size", lsz.v[0], lsz.v[1], lsz.v[2], "opcodes",
+                                w.opc_list, "extra_groups", extras, "addr_stats", stats, "counts", counts, "lines",
+                                (long long)N);
+  Py_XDECREF(tmp[0]); Py_XDECREF(tmp[1]);
+  Py_XDECREF(w.opc_dict); Py_XDECREF(w.opc_list);
+  PyBuffer_Release(&buf);
+  return out;
+}
+
 PyObject* py_init(PyObject*, PyObject* args) {
   PyObject* cls;
   if (!PyArg_ParseTuple(args, "O", &cls)) return nullptr;
@@ -866,6 +1128,8 @@ PyMethodDef methods[] = {
     {"encode_lines", py_encode_lines, METH_VARARGS,
      "encode_lines(data, decode_event) -> the same for the lines of an .aiwctrace file"},
     {"validate", py_validate, METH_VARARGS, "validate(iterable) -> [(event_index, rule, detail)] (every violation)"},
+    {"encode_lines_fast", py_encode_lines_fast, METH_VARARGS,
+     "encode_lines_fast(data, threads) -> columns of an all-canonical .aiwctrace file (unchecked stream) or None"},
     {"init", py_init, METH_VARARGS, "init(UnsupportedTrace class)"},
     {nullptr, nullptr, 0, nullptr}};
 

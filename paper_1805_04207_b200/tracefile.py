@@ -16,6 +16,7 @@ would raise them (cli.py:130-152).
 from __future__ import annotations
 
 import json
+import os
 from typing import IO, Iterable, Iterator
 
 import numpy as np
@@ -225,6 +226,26 @@ def load_trace(path: str) -> tuple[ColumnarTrace | None, tuple | None, BaseExcep
     return tr, out["violation"], err, out["last_line"]
 
 
+def fast_trace(path: str, threads: int | None = None) -> ColumnarTrace | None:
+    """An all-canonical `.aiwctrace` file parsed on all host threads into untrusted
+    columns (the engine checks the stream invariants on the device), or None when
+    the file needs the sequential walker (comments, other line forms, '\r', or a
+    per-event error the columns cannot carry)."""
+    from .walker import _walker
+
+    with open(path, "rb") as fp:
+        data = fp.read()
+    if b"\r" in data:
+        return None
+    out = _walker().encode_lines_fast(data, threads or max(1, os.cpu_count() or 1))
+    if out is None:
+        return None
+    return ColumnarTrace(np.frombuffer(out["kind"], dtype=np.uint8), np.frombuffer(out["payload"], dtype=np.uint64),
+                         out["kernel_name"], out["invocation"], tuple(out["global_size"]), tuple(out["local_size"]),
+                         list(out["opcodes"]), [tuple(g) for g in out["extra_groups"]], out["addr_stats"],
+                         validated=False, class_counts=tuple(out["counts"]))
+
+
 def consume_file(path: str, *, max_entries: int | None = None, device: int | None = None):
     """``consume(iter_trace(open(path)))`` without per-event Python objects.
 
@@ -234,9 +255,17 @@ def consume_file(path: str, *, max_entries: int | None = None, device: int | Non
     violation (cli.py:130-152 adds the line number to the latter's message;
     it is returned here as ``exc.line_no``).
     """
-    from .metrics import KernelAccumulator, default_entry_cap, run_engine
+    from .metrics import KernelAccumulator, consume, default_entry_cap, run_engine
 
     cap = default_entry_cap() if max_entries is None else max_entries
+    fast = fast_trace(path)
+    if fast is not None:
+        # canonical files: parsed in parallel, checked on the device; an invalid stream is
+        # re-read by the sequential walker, whose exception carries the line number
+        try:
+            return consume(fast, max_entries=cap, device=device)
+        except InvalidStream:
+            pass
     tr, violation, err, last_line = load_trace(path)
     if violation is not None or err is not None:
         if tr is not None and tr.n_events:

@@ -172,3 +172,40 @@ def test_consume_file_cap_before_malformed_line(tmp_path):
         consume_file(str(path), max_entries=3)
     with pytest.raises(MalformedEvent):
         consume_file(str(path), max_entries=100)
+
+
+@pytest.mark.parametrize("name", ["wavefront_big", "bfs_flags", "random31337_4", "offgrid_groups", "branch_streams_per_group"])
+def test_fast_parallel_parse_matches_walker(name, tmp_path):
+    """encode_lines_fast (all host threads, chunk-local dictionaries merged in
+    first-appearance order) gives the sequential walker's columns exactly."""
+    from paper_1805_04207_b200.tracefile import encode_event, fast_trace, load_trace
+
+    c, tr = {c["name"]: (c, t) for c, t in golden_cases() if t is not None}[name]
+    path = tmp_path / "f.aiwctrace"
+    _write(path, [encode_event(e) for e in _events(tr)])
+    want, violation, err, _ = load_trace(str(path))
+    assert violation is None and err is None
+    for threads in (1, 3, 16):
+        got = fast_trace(str(path), threads)
+        assert got is not None and not got.validated
+        assert np.array_equal(np.asarray(got.kind), np.asarray(want.kind))
+        assert np.array_equal(np.asarray(got.payload).view(np.uint64), np.asarray(want.payload).view(np.uint64))
+        assert got.opcodes == want.opcodes and got.extra_groups == want.extra_groups
+        assert got.addr_stats == want.addr_stats and got.class_counts == want.class_counts
+
+
+def test_fast_parse_declines_what_the_walker_must_decide(tmp_path):
+    from paper_1805_04207_b200.tracefile import fast_trace
+
+    head = ['{"ev":"kernel_begin","kernel":"k","invocation":0,"global_size":[2,1,1],"local_size":[2,1,1]}',
+            '{"ev":"wg_begin","group":[0,0,0]}']
+    cases = {
+        "comment": head + ["# c", '{"ev":"kernel_end"}'],
+        "bad_id": head + ['{"ev":"wi_begin","global":[1,0,0],"local":[0,0,0],"group":[0,0,0]}'],
+        "other_group": head + ['{"ev":"wi_begin","global":[2,0,0],"local":[0,0,0],"group":[1,0,0]}'],
+        "noncanonical": head + ['{"ev": "kernel_end"}'],
+    }
+    for name, lines in cases.items():
+        path = tmp_path / f"{name}.aiwctrace"
+        _write(path, lines)
+        assert fast_trace(str(path), 4) is None, name
