@@ -124,6 +124,117 @@ __global__ void shift_copy_kernel(const uint64_t* __restrict__ src, uint64_t n, 
     dst[i] = src[i] >> sh;
 }
 
+// ---------------------------------------------------------------------------
+// every level >= 1 in ONE sweep over the sorted unique keys (sparse path)
+// ---------------------------------------------------------------------------
+// Level j groups keys by key >> j; the groups of every level lie inside one group
+// of the top level (key >> (nlev - 1)), so each warp takes whole top-level groups
+// (its nominal range moved forward to a top-level boundary) and walks them 32
+// keys at a time: per level, a head flag (key >> j differs from the previous
+// key's), a segmented warp scan of the counts, and every group that ends inside
+// the tile goes to that level's count-of-counts histogram (or, >= CBINS, its fp64
+// term); the group still open at the tile's end carries to the next tile.
+constexpr int LV_T = 256, LV_W = LV_T / 32;
+
+__global__ void __launch_bounds__(LV_T) levels_kernel(const uint64_t* __restrict__ key,
+                                                      const unsigned long long* __restrict__ cr,
+                                                      const unsigned long long* __restrict__ cw, uint64_t n,
+                                                      int nlev, double m, DevState* st, double* partials,
+                                                      uint32_t n_parts) {
+  extern __shared__ uint32_t lh[];  // [nlev - 1][CBINS]
+  __shared__ double red[LV_W][NLEVELS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < (nlev - 1) * CBINS; i += LV_T) lh[i] = 0;
+  __syncthreads();
+  const int top = nlev - 1;
+  const uint64_t W = (uint64_t)gridDim.x * LV_W, gw = (uint64_t)blockIdx.x * LV_W + warp;
+  // a top-level boundary at or after position p (n if none)
+  auto boundary = [&](uint64_t p) -> uint64_t {
+    if (p == 0 || p >= n) return p >= n ? n : 0;
+    for (uint64_t q = p; q < n; q += 32) {
+      const uint64_t i = q + lane;
+      const bool h = i < n && (key[i] >> top) != (key[i - 1] >> top);
+      const uint32_t b = __ballot_sync(0xffffffffu, h);
+      if (b) return q + (__ffs(b) - 1);
+    }
+    return n;
+  };
+  const uint64_t lo = boundary(n * gw / W), hi = boundary(n * (gw + 1) / W);
+  double part[NLEVELS];
+#pragma unroll
+  for (int j = 0; j < NLEVELS; ++j) part[j] = 0.0;
+  unsigned long long csum[NLEVELS];   // open group's sum carried from the previous tile (per level)
+  uint64_t ckey = 0;                  // previous tile's last key
+#pragma unroll
+  for (int j = 0; j < NLEVELS; ++j) csum[j] = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint64_t t0 = lo; t0 < hi; t0 += 32) {
+    const uint64_t i = t0 + lane;
+    const bool act = i < hi;
+    const uint64_t kk = act ? key[i] : 0ull;
+    const unsigned long long c = act ? cr[i] + cw[i] : 0ull;
+    uint64_t pk = __shfl_up_sync(0xffffffffu, kk, 1);
+    if (lane == 0) pk = ckey;
+    const uint32_t nact = __ballot_sync(0xffffffffu, act);
+    const int last = 31 - __clz(nact);
+#pragma unroll
+    for (int j = 1; j < NLEVELS; ++j) {
+      if (j >= nlev) break;
+      const bool head = act && ((kk >> j) != (pk >> j) || (i == lo));
+      const uint32_t hm = __ballot_sync(0xffffffffu, head);
+      // a head at the tile's first key closes the group carried from the previous tile
+      if (lane == 0 && t0 != lo && (hm & 1u)) {
+        const unsigned long long g = csum[j];
+        if (g < (unsigned long long)CBINS) atomicAdd(&lh[(j - 1) * CBINS + (uint32_t)g], 1u);
+        else part[j] += plogp(g, m);
+      }
+      // segmented inclusive scan: sum over my segment up to me
+      unsigned long long v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+        // add when no head in (lane - o, lane]
+        const uint32_t win = (lane >= o) ? (((1u << lane) << 1) - (1u << (lane - o + 1))) : 0u;
+        if (lane >= o && !(hm & win)) v += u;
+      }
+      // the tile's first segment continues the carried group (no head before me)
+      if (!(hm & (lt | (1u << lane)))) v += csum[j];
+      // my group ends here when the next position is a head, or past the tile (flushed next tile / at the end)
+      const bool next_head = (hm >> (lane + 1)) & 1u;
+      const bool ends = act && lane < last && next_head;
+      if (ends) {
+        if (v < (unsigned long long)CBINS) atomicAdd(&lh[(j - 1) * CBINS + (uint32_t)v], 1u);
+        else part[j] += plogp(v, m);
+      }
+      csum[j] = __shfl_sync(0xffffffffu, v, last);
+    }
+    ckey = __shfl_sync(0xffffffffu, kk, last);
+  }
+  // the groups open at the warp range's end are complete (ranges end on top-level boundaries)
+  if (lo < hi && lane == 0) {
+    for (int j = 1; j < nlev; ++j) {
+      const unsigned long long v = csum[j];
+      if (v < (unsigned long long)CBINS) atomicAdd(&lh[(j - 1) * CBINS + (uint32_t)v], 1u);
+      else part[j] += plogp(v, m);
+    }
+  }
+#pragma unroll
+  for (int j = 1; j < NLEVELS; ++j) {
+    double x = part[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) red[warp][j] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 1 && threadIdx.x < nlev) {
+    double x = 0.0;
+    for (int w = 0; w < LV_W; ++w) x += red[w][threadIdx.x];
+    partials[threadIdx.x * n_parts + blockIdx.x] = x;
+  }
+  for (int i = threadIdx.x; i < (nlev - 1) * CBINS; i += LV_T)
+    if (lh[i]) atomicAdd(&st->cnt_hist[1 + i / CBINS][i % CBINS], (unsigned long long)lh[i]);
+}
+
 static int bitwidth(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
 static void set_u64(unsigned long long* dst, unsigned long long v, cudaStream_t s) {
@@ -161,8 +272,15 @@ int sparse_memory_stats(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, u
     U = rle_reduce(keys, nullptr, m, 1, RLE_RW, lkey[1], ur, uw, rscr, s, &kernels);
     count_stats_kernel<<<n_parts, DS_T, 0, s>>>(ur, uw, U, 0, dm, st, partials, n_parts, ovf);
     ++kernels;
-    rle_reduce(keys, nullptr, m, 1, RLE_ONES, lkey[0], lcnt[0], nullptr, rscr, s, &kernels);  // merged counts
     nlev = am.k >= 10 ? 1 : 11 - (int)am.k;
+    set_u64(&st->footprint, U, s);
+    if (nlev > 1) {  // every other level in one sweep over the unique keys
+      const size_t smem = (size_t)(nlev - 1) * CBINS * 4;
+      set_smem_once(levels_kernel, (int)smem);
+      levels_kernel<<<n_parts, LV_T, smem, s>>>(lkey[1], ur, uw, U, nlev, dm, st, partials, n_parts);
+      ++kernels;
+    }
+    return kernels;
   } else {
     // all 64 key bits significant: untagged sorts (reads, writes, all) of raw addresses
     cudaMemcpyAsync(keys, rd, n_rd * 8, cudaMemcpyDeviceToDevice, s);
