@@ -716,7 +716,8 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     a.dense32 = ctx->dense32;
     a.smem_keys = 0; a.hot_lo = 0; a.hot_dev = nullptr;
     if (ctx->dense && !ctx->dense32 && ctx->am.n_keys <= SMEM_TABLE_KEYS) {
-      a.smem_keys = (uint32_t)ctx->am.n_keys;  // the whole (small) table per CTA
+      a.smem_keys = SMEM_TABLE_KEYS;  // the whole (small) table per CTA: a full window (the bank swizzle
+                                      // permutes inside 1024 keys; keys >= n_keys are never flushed)
     } else if (ctx->dense && ctx->am.n_keys > SMEM_TABLE_KEYS && M >= HOT_MIN_ACCESSES && !ctx->hot_off) {
       // a 1024-key window holding many accesses (shared scratch, lookup tables) is
       // counted per CTA in shared memory: its keys would otherwise serialise in L2

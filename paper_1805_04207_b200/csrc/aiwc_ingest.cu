@@ -364,6 +364,11 @@ __device__ __forceinline__ void flush_counts(uint32_t (&oacc)[8], uint32_t (&wac
   for (int i = 0; i < 8; ++i) { oacc[i] = 0; wacc[i] = 0; }
 }
 
+// shared-memory slot of hot-window key `rel`: the low 5 bits XOR the next 5 (an
+// involution inside every 1024 keys), so strided key patterns -- a scratch indexed
+// by 4 * lid + i -- spread over all 32 banks instead of 8
+__device__ __forceinline__ uint32_t hot_swz(uint32_t rel) { return rel ^ ((rel >> 5) & 31u); }
+
 __device__ __forceinline__ uint64_t pay_at(const uint64_t* pay, uint32_t pos) {
   return pay[pos ^ (((pos >> 4) & 7u) << 1)];  // 128 B swizzle: chunk (j >> 1) ^ (row & 7)
 }
@@ -637,7 +642,7 @@ __global__ void __launch_bounds__(TPB, 2)
           (kb & ~(e0 == 0 ? 1u : 0u)) |           // kernel_begin is event 0 ...
           (ke & ~((n - 1 >= e0 && n - 1 < e0 + 16) ? (1u << (uint32_t)(n - 1 - e0)) : 0u)) |  // ... kernel_end the last
           (ke & grp_before);                      // ... with no work-group open
-      if (bad) flags |= F_STREAM;
+      if (bad && !(AIWC_ABL & 32)) flags |= F_STREAM;
       // the trace starts with kernel_begin and ends with kernel_end
       if (e0 == 0 && !(kb & 1u)) flags |= F_STREAM;
       if (n - 1 >= e0 && n - 1 < e0 + 16 && !((ke >> (uint32_t)(n - 1 - e0)) & 1u)) flags |= F_STREAM;
@@ -754,7 +759,7 @@ __global__ void __launch_bounds__(TPB, 2)
             const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
             mark(key);
             if (HOT && rel < hot_n) {
-              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + hot_swz((uint32_t)rel)], 1u);
             } else {
               uint32_t* const q = tab + key;
               atomicAdd(q, 1u);
@@ -771,7 +776,7 @@ __global__ void __launch_bounds__(TPB, 2)
             inval |= !v;
             const uint64_t key = v ? off >> k : a.am.n_keys, rel = key - hot_lo;
             mark(key);
-            if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+            if (HOT && rel < hot_n) atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + hot_swz((uint32_t)rel)], 1u);
             else atomicAdd(tab + key, 1ull << (32 * (e >> 15)));
           }
         }
@@ -798,7 +803,7 @@ __global__ void __launch_bounds__(TPB, 2)
           bfill += __popc(bm);
           if (act && !binned) {
             if (hot) {
-              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + (uint32_t)rel], 1u);
+              atomicAdd(&stab[((e >> 15) ? hot_n : 0u) + hot_swz((uint32_t)rel)], 1u);
             } else if (a.dense32) {
               uint32_t* const q = static_cast<uint32_t*>(a.dense) + key;
               atomicAdd(q, 1u);
@@ -853,14 +858,14 @@ __global__ void __launch_bounds__(TPB, 2)
       const uint32_t j = __ffs(m) - 1;
       const uint32_t kk = (uint32_t)((j < 8 ? klo >> (8 * j) : khi >> (8 * (j - 8))) & 0xFFu);
       const uint64_t p = PAY(j);
-      if (CHECK) {  // the payload rules (the sequence rules were checked on the masks above)
+      if (CHECK && !(AIWC_ABL & 64)) {  // the payload rules (the sequence rules were checked on the masks above)
         bool bad = false;
         if (kk == AIWC_K_WI_BEGIN) {
           // wi_begin for an already-started work-item: every begin sets its (group, lid)
           // bit (RED, no round trip); finalize compares the set bits with the begins
           const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + p;
           bad = p >= a.local_volume || !gseq || slot >= a.dup_len;
-          if (!bad) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
+          if (!bad && !(AIWC_ABL & 128)) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
         } else if (kk == AIWC_K_WI_END) {
           bad = p != lid || p >= a.local_volume;
         } else if (kk == AIWC_K_WG_BEGIN) {
@@ -932,7 +937,7 @@ __global__ void __launch_bounds__(TPB, 2)
   __syncthreads();
   if (DENSE && hot_n) {
     for (uint32_t i = t; i < hot_n; i += TPB) {
-      const uint32_t r = stab[i], w = stab[hot_n + i];
+      const uint32_t r = stab[hot_swz(i)], w = stab[hot_n + hot_swz(i)];
       if (!(r | w) || hot_lo + i >= a.am.n_keys) continue;  // (the sentinel key is not a table key)
       if (a.dense32) {
         uint32_t* const q = static_cast<uint32_t*>(a.dense) + hot_lo + i;
