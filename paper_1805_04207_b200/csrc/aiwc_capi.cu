@@ -950,6 +950,13 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     }
   }
   ctx->mark(AIWC_PH_MEMORY, 1, s);
+  // branch walk phase 1 before the read-back: its site-table overflow flag comes back with it
+  if (ctx->n_br) {
+    CK(grow(ctx->branch_scr, branch_scratch_bytes(ctx->n_br)));
+    ctx->mark(AIWC_PH_BRANCH, 0, s);
+    ctx->kernels += branch_walk_prepare(P<uint64_t>(ctx->br), ctx->n_br, ctx->opts.history_len, st,
+                                        ctx->branch_scr.p, s);
+  }
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(ctx->h_state, st, offsetof(DevState, host_end), cudaMemcpyDeviceToHost, s));
   ctx->d2h += offsetof(DevState, host_end);
@@ -958,9 +965,8 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   // ---- branches ----
   if (ctx->n_br) {
     const uint32_t site_bits = (uint32_t)bitwidth64(ctx->h_state->max_site);
-    CK(grow(ctx->branch_scr, branch_scratch_bytes(ctx->n_br)));
-    ctx->mark(AIWC_PH_BRANCH, 0, s);
-    ctx->kernels += branch_stats(P<uint64_t>(ctx->br), ctx->n_br, site_bits, ctx->opts.history_len, st,
+    ctx->kernels += branch_stats(P<uint64_t>(ctx->br), ctx->n_br, site_bits, ctx->opts.history_len,
+                                 ctx->h_state->bw_overflow == 0, st,
                                  P<unsigned long long>(ctx->branch_tab), ctx->branch_scr.p, ctx->branch_scr.cap, s);
     ctx->mark(AIWC_PH_BRANCH, 1, s);
     CK(cudaGetLastError());

@@ -93,6 +93,7 @@ struct DevState {
   unsigned long long n_wib, n_bar;                 // work-items begun, barriers hit (ingest)
   unsigned long long dup_set;                      // in-pass stream check: set bits of the begin map
   unsigned long long state_runs_n;                 // state export: runs claimed (kept when <= capacity)
+  unsigned long long bw_overflow;                  // branch walk: more sites than its table (sort path instead)
   unsigned long long n_widths_listed, n_sites_listed;
   double entropy[NLEVELS];
   double yokota, linear;
@@ -317,9 +318,13 @@ int sparse_memory_stats(const uint64_t* rd, uint64_t n_rd, const uint64_t* wr, u
                         void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t sparse_scratch_bytes(uint64_t m);
 // branch path; returns kernel count
-int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t history_len, DevState* st,
+int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t history_len, bool walk, DevState* st,
                  unsigned long long* tables, void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t branch_scratch_bytes(uint64_t n);
+// phase 1 of the sort-free branch walk (launched before finalize's state read-back;
+// sets st->bw_overflow when the sites do not fit its table)
+int branch_walk_prepare(const uint64_t* recs, uint64_t n, uint32_t history_len, DevState* st, void* scratch,
+                        cudaStream_t s);
 size_t branch_site_list_offset(uint64_t n);
 // utilities
 void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,

@@ -138,7 +138,12 @@ __global__ void __launch_bounds__(RS_T) radix_hist_kernel(const uint64_t* __rest
   for (int d = threadIdx.x; d < 256; d += RS_T) hist[(uint64_t)d * nb + blockIdx.x] = h[d];
 }
 
-__global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __restrict__ keys,
+static bool scatter_direct() {
+  static const bool v = [] { const char* e = getenv("AIWC_SCATTER"); return e && atoi(e) == 0; }();
+  return v;
+}
+// Direct scatter (passes of <= 6 bits; AIWC_SCATTER=0 forces it for A/B)
+__global__ void __launch_bounds__(RS_T) radix_scatter_direct_kernel(const uint64_t* __restrict__ keys,
                                                              uint64_t* __restrict__ out, uint64_t n, int shift,
                                                              uint32_t mask, const uint32_t* __restrict__ offs,
                                                              uint32_t nb) {
@@ -185,6 +190,82 @@ __global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __r
   }
 }
 
+// Stable scatter of one 4096-key tile: ranks by match.any (keys in j-major / lane-minor
+// order, the tile's key order), then the tile is first sorted by digit in shared memory
+// and written out digit run by digit run, so the global stores are contiguous per digit
+// (a direct scatter writes each warp's 32 keys to up to 32 buckets).
+__global__ void __launch_bounds__(RS_T) radix_scatter_kernel(const uint64_t* __restrict__ keys,
+                                                             uint64_t* __restrict__ out, uint64_t n, int shift,
+                                                             uint32_t mask, const uint32_t* __restrict__ offs,
+                                                             uint32_t nb) {
+  __shared__ uint32_t cnt[RS_W][256];
+  __shared__ uint32_t dstart[256];   // tile-local start of each digit (digit-major order)
+  __shared__ uint32_t gbase[256];    // the digit's global position for this tile
+  __shared__ uint64_t stage[RS_TILE];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_W * 256; i += RS_T) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t tile0 = (uint64_t)blockIdx.x * RS_TILE;
+  const uint64_t base = tile0 + (uint64_t)warp * 32 * RS_I;
+  uint64_t k[RS_I];
+  uint32_t d[RS_I];
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {  // all loads in flight before the first atomic
+    const uint64_t i = base + 32 * j + lane;
+    k[j] = i < n ? __ldcs(keys + i) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {
+    const uint64_t i = base + 32 * j + lane;
+    d[j] = i < n ? ((uint32_t)(k[j] >> shift) & mask) : 256u;
+    if (i < n) atomicAdd(&cnt[warp][d[j]], 1u);
+  }
+  __syncthreads();
+  // per digit (thread = digit; RS_T == 256): tile-local start = exclusive scan of the
+  // tile totals over digits; each warp's running offset; the tile's global base
+  static_assert(RS_T == 256, "one thread per digit");
+  __shared__ uint32_t wsum[RS_W];
+  {
+    const int dg = threadIdx.x;
+    uint32_t tot = 0;
+    for (int w = 0; w < RS_W; ++w) tot += cnt[w][dg];
+    uint32_t inc = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    gbase[dg] = offs[(uint64_t)dg * nb + blockIdx.x];
+    __syncthreads();
+    uint32_t start = inc - tot;
+    for (int w = 0; w < warp; ++w) start += wsum[w];
+    dstart[dg] = start;
+    for (int w = 0; w < RS_W; ++w) {  // running offsets per warp, over the counts
+      const uint32_t c = cnt[w][dg];
+      cnt[w][dg] = start;
+      start += c;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < RS_I; ++j) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, d[j]);
+    if (d[j] < 256u) stage[cnt[warp][d[j]] + __popc(peers & lt)] = k[j];
+    __syncwarp();
+    if (d[j] < 256u && (peers & lt) == 0) cnt[warp][d[j]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  const uint32_t m = n > tile0 ? (uint32_t)(n - tile0 < RS_TILE ? n - tile0 : RS_TILE) : 0u;
+  for (uint32_t p = threadIdx.x; p < m; p += RS_T) {
+    const uint64_t key = stage[p];
+    const uint32_t dg = (uint32_t)(key >> shift) & mask;
+    out[gbase[dg] + (p - dstart[dg])] = key;
+  }
+}
+
 // stable sort of keys by bits [bit_lo, bit_hi); returns the buffer holding the
 // result (keys or tmp: odd digit counts end in tmp, no copy back)
 uint64_t* radix_sort_u64_any(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int bit_hi, uint32_t* hist_scratch,
@@ -200,7 +281,12 @@ uint64_t* radix_sort_u64_any(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_
     const uint32_t mask = (1u << bits) - 1u;
     radix_hist_kernel<<<nb, RS_T, 0, s>>>(src, n, b, mask, hist, nb);
     scan_exclusive_u32(hist, 256ull * nb, scan_tmp, nullptr, s, kernels);
-    radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    // few digits: a warp's 32 keys land in few buckets and the direct scatter is
+    // already near-contiguous; many digits: stage the tile sorted in shared memory
+    if (bits <= 6 || scatter_direct())
+      radix_scatter_direct_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    else
+      radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
     if (kernels) *kernels += 2;
     uint64_t* x = src; src = dst; dst = x;
   }
@@ -220,7 +306,12 @@ void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t n, int bit_lo, int b
     const uint32_t mask = (1u << bits) - 1u;
     radix_hist_kernel<<<nb, RS_T, 0, s>>>(src, n, b, mask, hist, nb);
     scan_exclusive_u32(hist, 256ull * nb, scan_tmp, nullptr, s, kernels);
-    radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    // few digits: a warp's 32 keys land in few buckets and the direct scatter is
+    // already near-contiguous; many digits: stage the tile sorted in shared memory
+    if (bits <= 6 || scatter_direct())
+      radix_scatter_direct_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
+    else
+      radix_scatter_kernel<<<nb, RS_T, 0, s>>>(src, dst, n, b, mask, hist, nb);
     if (kernels) *kernels += 2;
     uint64_t* x = src; src = dst; dst = x;
   }
