@@ -38,7 +38,7 @@ namespace aiwc {
 constexpr int PC_T = 1024;                // threads per counting block (one block per SM: loads in flight)
 constexpr int PC_PER = 32;                // records per thread per step
 constexpr int PC_HALO = 16;               // warm-up window (>= history_len)
-constexpr int PC_PART_BITS = 14;          // patterns per partition: 2^14 (128 KB of counters)
+constexpr int PC_PART_BITS = 15;          // patterns per partition: 2^15 (128 KB of 16-bit counter pairs)
 constexpr int PC_CHUNK_ALIGN = 16;
 
 __device__ __forceinline__ void stage_one(uint64_t i, uint64_t r, uint64_t prev, uint8_t* __restrict__ bits,
@@ -126,18 +126,21 @@ __global__ void __launch_bounds__(256) pattern_walk_kernel(const uint8_t* __rest
   }
 }
 
-// Counts the observations of one 2^14-pattern partition in one chunk of codes,
-// entirely in shared memory, and writes the partition to the chunk's partial table.
+// Counts the observations of one 2^15-pattern partition in one chunk of codes,
+// entirely in shared memory, and writes the partition to the chunk's partial
+// table.  One 32-bit word per pattern holds two 16-bit counters (not taken,
+// taken); the add that carries a counter across 0x8000 takes 0x8000 back out
+// and moves it to the global overflow table (1024 threads cannot push a
+// counter from 0x8000 past 0xFFFF before that subtraction lands).
 __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __restrict__ code, uint64_t n,
                                                              uint32_t H, uint32_t n_parts, uint64_t chunk_len,
-                                                             unsigned long long* __restrict__ partials) {
-  extern __shared__ uint32_t cnt[];  // [2][part_size]: not taken, taken (one atomic per observation)
+                                                             unsigned long long* __restrict__ partials,
+                                                             unsigned long long* __restrict__ ovf) {
+  extern __shared__ uint32_t cnt[];  // [part_size]: taken << 16 | not taken
   const uint32_t part = blockIdx.x % n_parts, chunk = blockIdx.x / n_parts;
   const uint32_t part_size = (1u << H) / n_parts;
   const uint32_t shift = 31 - __clz(part_size) + 1;  // code >> shift = partition
-  uint32_t* nt = cnt;
-  uint32_t* tk = cnt + part_size;
-  for (uint32_t i = threadIdx.x; i < 2 * part_size; i += PC_T) cnt[i] = 0;
+  for (uint32_t i = threadIdx.x; i < part_size; i += PC_T) cnt[i] = 0;
   __syncthreads();
   const uint64_t c0 = (uint64_t)chunk * chunk_len, c1 = min(n, c0 + chunk_len);
   // coalesced 16-byte loads, eight in flight per thread; equal neighbours inside a
@@ -145,8 +148,12 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   // pattern for long stretches and would serialise on one bin)
   auto add = [&](uint32_t c, uint32_t k) {
     if (c != NO_OBS && (c >> shift) == part) {
-      const uint32_t slot = (c >> 1) & (part_size - 1);
-      atomicAdd(((c & 1) ? tk : nt) + slot, k);
+      const uint32_t slot = (c >> 1) & (part_size - 1), sh = (c & 1) ? 16 : 0;
+      const uint32_t old = (atomicAdd(cnt + slot, k << sh) >> sh) & 0xFFFFu;
+      if (old < 0x8000u && old + k >= 0x8000u) {
+        atomicSub(cnt + slot, 0x8000u << sh);
+        atomicAdd(ovf + (c >> 1), (0x8000ull << 32) | ((c & 1) ? 0x8000ull : 0ull));
+      }
     }
   };
   auto count4 = [&](const uint4 q) {
@@ -169,16 +176,18 @@ __global__ void __launch_bounds__(PC_T) pattern_count_kernel(const uint32_t* __r
   for (uint64_t i = max(v1, v0) + threadIdx.x; i < c1; i += PC_T) add(code[i], 1);
   __syncthreads();
   unsigned long long* out = partials + (uint64_t)chunk * (1u << H) + (uint64_t)part * part_size;
-  for (uint32_t i = threadIdx.x; i < part_size; i += PC_T)
-    out[i] = ((unsigned long long)(nt[i] + tk[i]) << 32) | tk[i];
+  for (uint32_t i = threadIdx.x; i < part_size; i += PC_T) {
+    const uint32_t w = cnt[i], nt = w & 0xFFFFu, tk = w >> 16;
+    out[i] = ((unsigned long long)(nt + tk) << 32) | tk;
+  }
 }
 
 // tab[p] = sum over chunks of the partial tables
 __global__ void pattern_reduce_kernel(const unsigned long long* __restrict__ partials, uint32_t chunks, uint32_t size,
-                                      unsigned long long* __restrict__ tab) {
+                                      const unsigned long long* __restrict__ ovf, unsigned long long* __restrict__ tab) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= size) return;
-  unsigned long long v = 0;
+  unsigned long long v = ovf[p];
   for (uint32_t c = 0; c < chunks; ++c) v += partials[(uint64_t)c * size + p];
   tab[p] = v;
 }
@@ -684,7 +693,8 @@ static uint32_t n_chunks_for(uint64_t n, uint32_t parts) {
 }
 
 // [sort tmp (8n) = observation codes (4n) + stage bytes (n)][partial tables][radix histograms][site list]
-static uint64_t partial_bytes(uint64_t n) { return (uint64_t)n_chunks_for(n, 4) * (1ull << 16) * 8; }
+// per-chunk partial tables (H <= 16: at most 2 partitions) + the overflow table
+static uint64_t partial_bytes(uint64_t n) { return ((uint64_t)n_chunks_for(n, 2) + 1) * (1ull << 16) * 8; }
 static uint64_t branch_tmp_bytes(uint64_t n) { return ((8 * n + 15) & ~15ull) + partial_bytes(n); }
 
 size_t branch_site_list_offset(uint64_t n) {
@@ -792,10 +802,12 @@ int branch_stats(uint64_t* recs, uint64_t n, uint32_t site_bits, uint32_t histor
     kernels += 2;
   }
   const uint64_t chunk_len = ((n + chunks - 1) / chunks + PC_CHUNK_ALIGN - 1) / PC_CHUNK_ALIGN * PC_CHUNK_ALIGN;
-  const size_t smem = 2 * (size_t)(size / parts) * sizeof(uint32_t);
+  const size_t smem = (size_t)(size / parts) * sizeof(uint32_t);
+  unsigned long long* ovf = partials + (uint64_t)chunks * size;
+  cudaMemsetAsync(ovf, 0, (size_t)size * 8, s);
   set_smem_once(pattern_count_kernel, (int)smem);
-  pattern_count_kernel<<<chunks * parts, PC_T, smem, s>>>(code, n, H, parts, chunk_len, partials);
-  pattern_reduce_kernel<<<(size + 255) / 256, 256, 0, s>>>(partials, chunks, size, tables);
+  pattern_count_kernel<<<chunks * parts, PC_T, smem, s>>>(code, n, H, parts, chunk_len, partials, ovf);
+  pattern_reduce_kernel<<<(size + 255) / 256, 256, 0, s>>>(partials, chunks, size, ovf, tables);
   // the per-chunk partial tables are consumed: their space holds the finish partials
   double* fin = reinterpret_cast<double*>(partials);
   const uint32_t fb = std::min<uint32_t>(BF_BLOCKS, (size + BF_T - 1) / BF_T);
