@@ -771,8 +771,8 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     ctx->kernels += 1;
     if (ctx->n_instr) {  // first index of each width 1..16 (the columns are only ours until here)
       launch_width_first(kind, payload, n, P<uint32_t>(ctx->wpres), G * P1_SUB, pres_blocks, tpc, WARP_TILE,
-                         P<unsigned long long>(ctx->wfirst), s);
-      ctx->kernels += 1;
+                         P<unsigned long long>(ctx->wfirst), st, s);
+      ctx->kernels += 2;
     }
   }
   ctx->mark(AIWC_PH_INGEST_TOTAL, 1, s);

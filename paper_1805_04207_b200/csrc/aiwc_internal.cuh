@@ -109,6 +109,7 @@ struct DevState {
   unsigned long long hot_key;                       // hot_sample_kernel: first key of the hot window, ~0 none
   unsigned long long bin_zones, bin_total;          // random key zones (bit z: zone z is binned), entries binned
   unsigned int zone_counts[128];                    // zone sampler: (near, far) per zone
+  unsigned long long width_unit[WBINS];             // first presence unit of widths 1..16 (launch_width_first)
 };
 
 // Memory-path description shared by the ingest and the dense-table kernels.
@@ -283,7 +284,7 @@ void launch_hot_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n,
 void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st, uint32_t* ipt_ovf, cudaStream_t s);
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
                         uint32_t n_ranges, uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
-                        unsigned long long* width_first, cudaStream_t s);
+                        unsigned long long* width_first, DevState* st, cudaStream_t s);
 void launch_width_list(const unsigned long long* count, const unsigned long long* first, DevState* st,
                        cudaStream_t s);
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,

@@ -393,51 +393,67 @@ void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st,
 // block holding width w in stream order (ranges are contiguous and in order, so
 // (range, block) order is stream order) and scans its events in order up to the
 // first hit.
-__global__ void __launch_bounds__(256) width_first_kernel(const uint8_t* __restrict__ kind,
-                                                          const uint64_t* __restrict__ payload, uint64_t n,
-                                                          const uint32_t* __restrict__ presence, uint32_t n_ranges,
-                                                          uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
-                                                          unsigned long long* width_first) {
-  const uint32_t w = blockIdx.x + 1, bit = 1u << (w - 1);
-  __shared__ unsigned long long s_unit, s_pos;
-  if (threadIdx.x == 0) { s_unit = ~0ull; s_pos = ~0ull; }
+// First index of each width 1..16 (first-appearance order of simd widths,
+// reference Counter insertion order).  The ingest pass left one presence word per
+// (range, unit of PRES_TILES tiles) with bit w-1 set when width w occurs there.
+// width_unit_kernel: the first unit holding each width (all presence words read
+// in parallel); width_pos_kernel: one block per (width, tile of that unit) finds
+// the first matching instruction.
+__global__ void __launch_bounds__(256) width_unit_kernel(const uint32_t* __restrict__ presence, uint64_t n_units,
+                                                         unsigned long long* __restrict__ unit_first) {
+  __shared__ unsigned long long s_min[WBINS];
+  if (threadIdx.x < WBINS) s_min[threadIdx.x] = ~0ull;
   __syncthreads();
-  for (uint64_t u = threadIdx.x; u < (uint64_t)n_ranges * pres_blocks; u += blockDim.x)
-    if (presence[u] & bit) atomicMin(&s_unit, u);
+  uint32_t seen = 0;  // widths this thread has already reported (units ascend per thread)
+  for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n_units;
+       u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t pw = presence[u];
+    for (uint32_t m = pw & ~seen & ((1u << WBINS) - 1u); m; m &= m - 1) atomicMin(&s_min[__ffs(m) - 1], u);
+    seen |= pw;
+  }
   __syncthreads();
-  if (s_unit == ~0ull) return;
-  const uint64_t r = s_unit / pres_blocks, b = s_unit % pres_blocks;
+  if (threadIdx.x < WBINS && s_min[threadIdx.x] != ~0ull) atomicMin(&unit_first[threadIdx.x], s_min[threadIdx.x]);
+}
+
+__global__ void __launch_bounds__(256) width_pos_kernel(const uint8_t* __restrict__ kind,
+                                                        const uint64_t* __restrict__ payload, uint64_t n,
+                                                        const unsigned long long* __restrict__ unit_first,
+                                                        uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
+                                                        unsigned long long* width_first) {
+  const uint32_t w = blockIdx.x / PRES_TILES + 1, t = blockIdx.x % PRES_TILES;
+  const unsigned long long u = unit_first[w - 1];
+  if (u == ~0ull) return;
+  const uint64_t r = u / pres_blocks, b = u % pres_blocks;
   const uint64_t r_end = min(n, (r + 1) * tiles_per_range * (uint64_t)wt);
-  const uint64_t lo = r * tiles_per_range * (uint64_t)wt + b * PRES_TILES * (uint64_t)wt;
-  const uint64_t hi = min(r_end, lo + (uint64_t)PRES_TILES * wt);
+  const uint64_t lo = r * tiles_per_range * (uint64_t)wt + (b * PRES_TILES + t) * (uint64_t)wt;
+  const uint64_t hi = min(r_end, lo + wt);
+  unsigned long long best = ~0ull;
   for (uint64_t base = lo; base < hi; base += 16 * 256) {
-    // all 32 loads of the chunk in flight at once (one memory round trip)
     uint8_t k[16];
     uint32_t p[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < 16; ++j) {  // all 32 loads in flight
       const uint64_t e = base + (uint64_t)j * 256 + threadIdx.x;
       k[j] = e < hi ? kind[e] : 0;
       p[j] = e < hi ? (uint32_t)payload[e] : 0u;
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (k[j] == AIWC_K_INSTR && p[j] == w) {
-        atomicMin(&s_pos, base + (uint64_t)j * 256 + threadIdx.x);
-        break;
-      }
-    }
-    __syncthreads();
-    if (s_pos != ~0ull) break;
+    for (int j = 0; j < 16; ++j)
+      if (k[j] == AIWC_K_INSTR && p[j] == w) best = min(best, (unsigned long long)(base + (uint64_t)j * 256 + threadIdx.x));
+    if (__syncthreads_or(best != ~0ull)) break;
   }
-  if (threadIdx.x == 0 && s_pos != ~0ull) atomicMin(&width_first[w], s_pos);
+  if (best != ~0ull) atomicMin(&width_first[w], best);
 }
 
 void launch_width_first(const uint8_t* kind, const uint64_t* payload, uint64_t n, const uint32_t* presence,
                         uint32_t n_ranges, uint32_t pres_blocks, uint32_t tiles_per_range, uint32_t wt,
-                        unsigned long long* width_first, cudaStream_t s) {
-  width_first_kernel<<<WBINS, 256, 0, s>>>(kind, payload, n, presence, n_ranges, pres_blocks, tiles_per_range, wt,
-                                           width_first);
+                        unsigned long long* width_first, DevState* st, cudaStream_t s) {
+  const uint64_t n_units = (uint64_t)n_ranges * pres_blocks;
+  cudaMemsetAsync(st->width_unit, 0xFF, sizeof(st->width_unit), s);
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((n_units + 1023) / 1024, 148 * 4));
+  width_unit_kernel<<<g, 256, 0, s>>>(presence, n_units, st->width_unit);
+  width_pos_kernel<<<WBINS * PRES_TILES, 256, 0, s>>>(kind, payload, n, st->width_unit, pres_blocks, tiles_per_range,
+                                                      wt, width_first);
 }
 
 __global__ void width_list_kernel(const unsigned long long* __restrict__ count,
