@@ -352,8 +352,8 @@ def run_ours(args) -> None:
         # small kernels and host round trip overlap another stream's ingest.
         # Every lane reads its OWN copy of the trace (no cross-lane L2 reuse).
         # the columns are treated as untrusted: every step also checks StreamChecker's
-        # invariants inside the pass (certified for traces without barriers / resumes;
-        # the separate full validator's cost is reported as validate_ms)
+        # invariants inside the pass (barrier / resume traces included; the separate
+        # full validator -- which only locates a violation -- is reported as validate_ms)
         info = trace_info(tr, check=not args.no_stream_check)
         lanes = []
         for i in range(n_streams):
@@ -539,8 +539,8 @@ def run_ours(args) -> None:
             "stream_check": {"in_pass": not sharded, "certified": bool(lanes[0][2].stream_checked) if not sharded else None,
                              "full_validator_ms": validate_ms,
                              "note": "every timed single-GPU step checks StreamChecker's invariants inside the pass "
-                                     "(trace.py:289-424); traces with barriers / resumes are certified by the "
-                                     "separate device validator instead (full_validator_ms)"},
+                                     "(trace.py:289-424), barrier / resume rules included; the separate device "
+                                     "validator (full_validator_ms) only locates a violation"},
             "gpu_launches": kernels[0],
             "clocks": clocks,
             "cpu_baseline": cpu,

@@ -163,6 +163,37 @@ __global__ void popcount_kernel(const uint32_t* __restrict__ bits, uint64_t word
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// the per-work-item rules of traces with barriers / resumes (trace.py:355-404), one
+// warp per group: every work-item that closed a segment opened its first one with
+// wi_begin, closed its last with wi_end, ended once, and all hit the same number of
+// barriers (three words per slot, written at each close by the ingest)
+__global__ void wi_rules_kernel(const unsigned long long* __restrict__ rules, uint64_t n_groups, uint32_t lv,
+                                DevState* st) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t w0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  bool bad = false;
+  for (uint64_t g = w0; g < n_groups; g += nw) {
+    uint32_t bmin = ~0u, bmax = 0;
+    for (uint32_t i = lane; i < lv; i += 32) {
+      const unsigned long long* w = rules + 3 * (g * lv + i);
+      const unsigned long long first = w[0];
+      if (first == 0) continue;  // no segment of this work-item in this group
+      const unsigned long long last = w[1], k = w[2];
+      bad |= (~first & 1ull) || !(last & 1ull) || (k >> 32) != 1ull;
+      bmin = min(bmin, (uint32_t)k);
+      bmax = max(bmax, (uint32_t)k);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      bmin = min(bmin, __shfl_xor_sync(0xffffffffu, bmin, o));
+      bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+    }
+    bad |= bmin != ~0u && bmin != bmax;  // barrier.divergence
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&st->flags, (unsigned long long)F_STREAM);
+}
+
 struct aiwc_ctx {
   int device = 0;
   int n_sms = 148;
@@ -190,8 +221,9 @@ struct aiwc_ctx {
   bool bins = false;        // this trace: the zone sampler ran, the ingest may bin
   uint64_t binned = 0;      // this trace: accesses counted through the bins
   bool stream_checked = false;  // this trace: the ingest checked StreamChecker's invariants
-  Buf dup_bits;
+  Buf dup_bits, wi_rules;
   uint64_t dup_len = 0;
+  bool wi_rules_on = false;
   // exported accumulator state (aiwc_state_export)
   Buf state_runs, state_cur;
   uint64_t state_n_runs = 0;
@@ -351,7 +383,7 @@ extern "C" void aiwc_ctx_destroy(aiwc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   for (Buf* b : {&ctx->chunk_bits, &ctx->own_list, &ctx->nc_bits, &ctx->nc_small, &ctx->nc_send, &ctx->nc_recv,
                  &ctx->nc_pack, &ctx->nc_blob, &ctx->bin_seg, &ctx->bin_base, &ctx->bin_fill, &ctx->bin_scr,
-                 &ctx->dup_bits, &ctx->state_runs, &ctx->state_cur})
+                 &ctx->dup_bits, &ctx->wi_rules, &ctx->state_runs, &ctx->state_cur})
     if (b->p) cudaFree(b->p);
   if (ctx->hot_ev) cudaEventDestroy(ctx->hot_ev);
   delete ctx;
@@ -731,15 +763,23 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     }
     a.rd_out = P<uint64_t>(ctx->rd); a.wr_out = P<uint64_t>(ctx->wr); a.br_out = P<uint64_t>(ctx->br);
     a.chunk_bits = ctx->shard_dense ? P<uint32_t>(ctx->chunk_bits) : nullptr;
-    // in-pass StreamChecker for untrusted columns without barriers / resumes
-    ctx->stream_checked = info->check_stream && !ctx->n_bres;
+    // in-pass StreamChecker for untrusted columns; with barriers / resumes the
+    // per-work-item order rules take three words per (group, lid) slot
+    ctx->stream_checked = info->check_stream;
     a.check = ctx->stream_checked;
+    ctx->wi_rules_on = false;
     if (a.check) {
       a.dup_len = std::max<uint64_t>(ctx->n_wgb, 1) * a.local_volume;
       ctx->dup_len = a.dup_len;
       CK(grow(ctx->dup_bits, (a.dup_len + 31) / 32 * 4));
       CK(cudaMemsetAsync(ctx->dup_bits.p, 0, (a.dup_len + 31) / 32 * 4, s));
       a.dup_bits = P<uint32_t>(ctx->dup_bits);
+      if (ctx->n_bres) {
+        CK(grow(ctx->wi_rules, a.dup_len * 24));
+        CK(cudaMemsetAsync(ctx->wi_rules.p, 0, a.dup_len * 24, s));
+        a.wi_rules = P<unsigned long long>(ctx->wi_rules);
+        ctx->wi_rules_on = true;
+      }
     }
     // key-block bins: a dense table well beyond L2 with many accesses -- the zone
     // sampler (beside pass 1, on the device) decides whether any key zone is random
@@ -884,6 +924,13 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     popcount_kernel<<<(unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)ctx->n_sms * 4), 256, 0, s>>>(
         P<uint32_t>(ctx->dup_bits), words, &st->dup_set);
     ctx->kernels += 1;
+    if (ctx->wi_rules_on) {
+      const uint32_t lv = std::max<uint32_t>(ctx->info.local_volume, 1);
+      const uint64_t groups = ctx->dup_len / lv;
+      wi_rules_kernel<<<(unsigned)std::max<uint64_t>(1, std::min<uint64_t>((groups + 7) / 8, (uint64_t)ctx->n_sms * 8)),
+                        256, 0, s>>>(P<unsigned long long>(ctx->wi_rules), groups, lv, st);
+      ctx->kernels += 1;
+    }
   }
 
   // ---- device finishing: IPT slots, widths, memory ----

@@ -321,10 +321,21 @@ __device__ __forceinline__ void bin_counts(uint32_t (&acc)[8], const uint32_t (&
 // non-empty); IPT either straight to the histogram (work-item never crossed a
 // barrier) or accumulated in the work-item's lifetime slot.
 __device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint32_t seg, uint32_t lid, uint32_t gz,
-                                         unsigned long long& itb_sum, unsigned long long& ipt_sum,
+                                         uint64_t pos, unsigned long long& itb_sum, unsigned long long& ipt_sum,
                                          unsigned long long& flags) {
   const bool bar = gz >> 31, byres = (gz >> 30) & 1u;
   const uint32_t gseq = gz & 0x3FFFFFFFu;
+  if (a.wi_rules && !(AIWC_ABL & 256)) {  // per-work-item order (stream check of barrier / resume traces)
+    const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + lid;
+    if (gseq == 0 || slot >= a.dup_len) {
+      flags |= F_STREAM;
+    } else {
+      unsigned long long* const w = a.wi_rules + 3 * slot;
+      atomicMax(w, ~((pos << 1) | (byres ? 1ull : 0ull)));     // the first segment: opened by wi_begin
+      atomicMax(w + 1, ((pos + 1) << 1) | (bar ? 0ull : 1ull));  // the last: closed by wi_end
+      atomicAdd(w + 2, bar ? 1ull : (1ull << 32));               // barriers | ends << 32
+    }
+  }
   if (bar || seg) {
     if (seg < (uint32_t)HBINS) atomicAdd(&L.itb_h[seg], 1u);
     else a.itb_ovf[atomicAdd(&a.st->itb_ovf_n, 1ull)] = seg;
@@ -617,7 +628,8 @@ __global__ void __launch_bounds__(TPB, 2)
     // tile's carried state XOR the parity of all lower lanes' boundaries (one ballot).
     uint32_t so = 0, go = 0;
     if (CHECK) {
-      const uint32_t ko = bnd16 & p5 & ~p7;                      // wi_begin (wi_resume is not covered)
+      // segment opens: wi_begin, and wi_resume when the per-work-item rules run (a.wi_open)
+      const uint32_t ko = bnd16 & p5 & (a.wi_rules ? 0xFFFFu : ~p7);
       const uint32_t kc = bnd16 & ~p5;                           // wi_end / barrier
       const uint32_t gb = wgb16, ge = p6 & p7;                   // wg_begin, wg_end
       const uint32_t kb = p5 & ~bnd16 & ~p6 & ~p7, ke = p5 & ~bnd16 & ~p6 & p7;  // kernel begin / end
@@ -638,7 +650,7 @@ __global__ void __launch_bounds__(TPB, 2)
           (X & ~grp_before) |                     // work-item events inside a work-group only
           (gb & grp_before) | (ge & ~grp_before) |  // groups alternate
           (G & seg_before) |                      // no group event inside a segment
-          (bnd16 & p7 & ~kc) |                    // wi_resume: the full validator's case
+          (a.wi_rules ? 0u : bnd16 & p7 & ~kc) |  // wi_resume without the per-work-item rules: the full validator's case
           (kb & ~(e0 == 0 ? 1u : 0u)) |           // kernel_begin is event 0 ...
           (ke & ~((n - 1 >= e0 && n - 1 < e0 + 16) ? (1u << (uint32_t)(n - 1 - e0)) : 0u)) |  // ... kernel_end the last
           (ke & grp_before);                      // ... with no work-group open
@@ -868,6 +880,8 @@ __global__ void __launch_bounds__(TPB, 2)
           if (!bad && !(AIWC_ABL & 128)) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
         } else if (kk == AIWC_K_WI_END) {
           bad = p != lid || p >= a.local_volume;
+        } else if (kk == AIWC_K_WI_RESUME) {
+          bad = p >= a.local_volume;
         } else if (kk == AIWC_K_WG_BEGIN) {
           bad = (p >> 31) != 0;
         } else if (kk == AIWC_K_WG_END) {
@@ -883,8 +897,8 @@ __global__ void __launch_bounds__(TPB, 2)
                               (last_b < 0 ? seg_in : 0u);
           const uint32_t gz = (gseq & 0x3FFFFFFFu) | ((kk & 0x80u) << 24) | (byres << 30);
           if (gseq >> 30) flags |= F_BAD_GROUP;
-          if (o_cl < (uint32_t)WCL_CAP) wclose[o_cl] = make_uint4(cl, lid, gz, 0u);
-          else do_close(L, a, cl, lid, gz, itb_sum, ipt_sum, flags);
+          if (o_cl < (uint32_t)WCL_CAP) wclose[o_cl] = make_uint4(cl, lid, gz, 16u * lane + j);
+          else do_close(L, a, cl, lid, gz, e0 + j, itb_sum, ipt_sum, flags);
           ++o_cl;
         }
         last_b = (int)j;
@@ -907,7 +921,7 @@ __global__ void __launch_bounds__(TPB, 2)
     // ---- segment closes of the tile, the warp's lanes converged ----
     for (uint32_t i = lane; i < min(T_cl, (uint32_t)WCL_CAP); i += 32) {
       const uint4 c = wclose[i];
-      do_close(L, a, c.x, c.y, c.z, itb_sum, ipt_sum, flags);
+      do_close(L, a, c.x, c.y, c.z, tile0 + c.w, itb_sum, ipt_sum, flags);
     }
     __syncwarp();
     // ---- refill this stage (every lane is done with it) ----

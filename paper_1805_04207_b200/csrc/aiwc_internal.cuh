@@ -171,6 +171,10 @@ struct IngestArgs {
   uint32_t check;
   uint32_t* dup_bits;               // [(groups) * local_volume] bits: wi_begin seen
   uint64_t dup_len;
+  // traces with barriers / resumes: three words per (group, lid) slot, updated at
+  // each segment close (null otherwise): ~min(pos << 1 | opened by resume),
+  // max((pos + 1) << 1 | closed by end), barriers | ends << 32
+  unsigned long long* wi_rules;
 };
 
 // ---- stream validation (aiwc_validate.cu) ---------------------------------------

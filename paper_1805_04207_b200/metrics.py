@@ -419,9 +419,10 @@ def consume(events: Iterable | ColumnarTrace, *, max_entries: int | None = None,
             tr = _device_columns(tr, device)
             res = err = None
             if tr.n_events <= max_ingest_events():
-                # the ingest checks the invariants of traces without barriers / resumes in
-                # the same pass; only a flagged stream (to locate its first violation) or a
-                # trace the pass cannot certify goes through the separate device checker
+                # the ingest checks StreamChecker's invariants in the same pass (barrier /
+                # resume traces: per-work-item order words, aiwc_capi.cu wi_rules_kernel);
+                # only a flagged stream goes through the separate device checker, which
+                # locates its first violation
                 try:
                     res = run_engine(tr, device, check=True, export=True)
                 except AiwcError as exc:  # a violation, or malformed data it caused (UnsupportedTrace too)

@@ -155,9 +155,8 @@ def test_consume_raises_for_untrusted_columns():
 
 @pytest.mark.parametrize("seed", range(25))
 def test_in_pass_check_is_complete(seed):
-    """consume()'s in-pass StreamChecker (untrusted columns without barriers /
-    resumes, checked inside the ingest): it never certifies an invalid stream,
-    and it certifies every valid one it is meant to cover."""
+    """consume()'s in-pass StreamChecker (untrusted columns, checked inside the
+    ingest): it never certifies an invalid stream and certifies every valid one."""
     from paper_1805_04207_b200 import AiwcError, UnsupportedTrace
     from paper_1805_04207_b200.metrics import _device_columns, run_engine
 
@@ -176,7 +175,69 @@ def test_in_pass_check_is_complete(seed):
             certified = False
         if want is not None:
             assert not certified, (name, seed, want)
-        elif not np.isin(np.asarray(mt.kind), [0x90, 0xB0]).any():
+        else:
             assert certified, (name, seed)
             certified_valid += 1
     assert certified_valid
+
+
+def _mutate_bres(tr, rng):
+    """One targeted change to the barrier / resume structure."""
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    k = np.array(tr.kind, dtype=np.uint8).copy()
+    p = np.array(tr.payload, dtype=np.uint64).copy()
+    bar, res = np.flatnonzero(k == 0x90), np.flatnonzero(k == 0xB0)
+    lv = int(np.prod(tr.local_size))
+    op = rng.choice(["drop_bar", "drop_res", "dup_bar", "res_lid", "swap_res", "bar_to_end", "end_to_bar"])
+    if op == "drop_bar" and bar.size:
+        i = rng.choice(bar.tolist()); k, p = np.delete(k, i), np.delete(p, i)
+    elif op == "drop_res" and res.size:  # with its segment up to the next close
+        i = rng.choice(res.tolist())
+        j = i + 1
+        while j < len(k) and k[j] not in (0x90, 0x10):
+            j += 1
+        k, p = np.delete(k, range(i, j + 1)), np.delete(p, range(i, j + 1))
+    elif op == "dup_bar" and bar.size:
+        i = rng.choice(bar.tolist()); k, p = np.insert(k, i, k[i]), np.insert(p, i, p[i])
+    elif op == "res_lid" and res.size:
+        i = rng.choice(res.tolist()); p[i] = np.uint64(rng.randrange(lv + 1))
+    elif op == "swap_res" and res.size > 1:
+        a, b = rng.sample(res.tolist(), 2); p[[a, b]] = p[[b, a]]
+    elif op == "bar_to_end" and bar.size:  # the closing barrier becomes the work-item's end
+        i = rng.choice(bar.tolist())
+        j = i - 1
+        while j >= 0 and k[j] not in (0x30, 0xB0):
+            j -= 1
+        if j >= 0:
+            k[i], p[i] = 0x10, p[j]
+    elif op == "end_to_bar":
+        e = np.flatnonzero(k == 0x10)
+        if e.size:
+            i = rng.choice(e.tolist()); k[i], p[i] = 0x90, 0
+    return ColumnarTrace(k, p, tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
+                         tr.extra_groups)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_in_pass_check_barrier_rules(seed):
+    """Barrier / resume traces: the per-work-item rules inside the pass (begin first,
+    end last, one end, equal barrier counts) against the checker restatement."""
+    from paper_1805_04207_b200 import AiwcError, UnsupportedTrace
+    from paper_1805_04207_b200.metrics import _device_columns, run_engine
+
+    rng = random.Random(9000 + seed)
+    traces = [(n, t) for n, t in _traces() if len(t.opcodes) and np.isin(np.asarray(t.kind), [0x90, 0xB0]).any()]
+    assert traces
+    seen = {True: 0, False: 0}
+    for _ in range(40):
+        name, tr = rng.choice(traces)
+        mt = _mutate_bres(tr, rng) if rng.random() < 0.85 else tr
+        want = _expected(mt)
+        try:
+            certified = run_engine(_device_columns(mt, 0), 0, check=True).stream_checked
+        except (AiwcError, UnsupportedTrace):
+            certified = False
+        assert certified == (want is None), (name, seed, want)
+        seen[want is None] += 1
+    assert seen[True] and seen[False]
