@@ -96,8 +96,9 @@ typedef struct {
   /* 1: the columns come from an untrusted producer -- check StreamChecker's
    * invariants (trace.py:289-424) inside the pass.  A violation makes
    * aiwc_finalize return AIWC_ERR_INVALID_STREAM (aiwc_validate locates the
-   * first one); aiwc_result.stream_checked says whether the pass could certify
-   * the stream (traces with barriers / resumes need aiwc_validate).        */
+   * first one); aiwc_result.stream_checked says the pass certified the stream
+   * (barrier / resume traces included: per-work-item order words, +24 B per
+   * (group, local id) slot of device scratch).                              */
   uint32_t check_stream;
   /* Event index of this trace's first event in the whole job (a work-group shard
    * of a multi-GPU job: first-appearance order of widths spans the ranks); 0 else. */
