@@ -387,15 +387,10 @@ void launch_ipt_table(const unsigned long long* tab, uint64_t len, DevState* st,
 // ---------------------------------------------------------------------------
 // width Counter in first-appearance order (metrics.py:136, :298-306)
 // ---------------------------------------------------------------------------
-// First event index of each width 1..16 counted by the ingest's bit-plane
-// bins.  The ingest records, per warp range and per block of PRES_TILES warp
-// tiles (`wt` events each), which widths occurred; CTA w - 1 finds the earliest
-// block holding width w in stream order (ranges are contiguous and in order, so
-// (range, block) order is stream order) and scans its events in order up to the
-// first hit.
 // First index of each width 1..16 (first-appearance order of simd widths,
 // reference Counter insertion order).  The ingest pass left one presence word per
-// (range, unit of PRES_TILES tiles) with bit w-1 set when width w occurs there.
+// (range, unit of PRES_TILES tiles) with bit w-1 set when width w occurs there
+// (ranges are contiguous and in order, so (range, unit) order is stream order).
 // width_unit_kernel: the first unit holding each width (all presence words read
 // in parallel); width_pos_kernel: one block per (width, tile of that unit) finds
 // the first matching instruction.

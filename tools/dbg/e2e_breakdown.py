@@ -27,8 +27,11 @@ def t(f, k=5):
 
 bare, _ = t(lambda: (dk.copy_(hk, non_blocking=True), dp.copy_(hp, non_blocking=True)))
 dev, _ = t(lambda: finalize(consume(tr, max_entries=1 << 62)))
+ut = ColumnarTrace(tr.kind, tr.payload, tr.kernel_name, 0, tr.global_size, tr.local_size, tr.opcodes, [], tr.addr_stats)
+devu, _ = t(lambda: finalize(consume(ut, max_entries=1 << 62)))
+h2d_sync, _ = t(lambda: (hk.to("cuda"), hp.to("cuda")))
 cons, acc = t(lambda: consume(ht, max_entries=1 << 62))
 fin, _ = t(lambda: finalize(acc))
 full, _ = t(lambda: finalize(consume(ht, max_entries=1 << 62)))
-print(f"bare H2D {bare:.3f} ms | device-resident consume+finalize {dev:.3f} | host consume {cons:.3f} | "
-      f"finalize {fin:.3f} | host consume+finalize {full:.3f} ms")
+print(f"bare H2D {bare:.3f} ms | .to() H2D {h2d_sync:.3f} | device-resident consume+finalize {dev:.3f} "
+      f"(untrusted {devu:.3f}) | host consume {cons:.3f} | finalize {fin:.3f} | host consume+finalize {full:.3f} ms")
