@@ -26,7 +26,10 @@ from .trace import (
     Violation, WorkGroupBegin, WorkGroupEnd, WorkItemBegin, WorkItemEnd, WorkItemId, WorkItemResume, validate_stream,
 )
 from .entropy import BranchStats, branch_entropy, coverage_count, local_entropy, shannon_entropy
-from .tracefile import consume_file, decode_event, encode_event, iter_trace, load_trace, read_trace, write_trace
+from .tracefile import (
+    consume_file, decode_event, encode_event, iter_trace, load_trace, read_columnar, read_trace, write_columnar,
+    write_trace,
+)
 from .ir import KernelProgram, parse_kernel
 from .sim import NDRangeConfig, assign_bases, simulate, simulate_events, simulate_trace
 
@@ -35,7 +38,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BranchStats", "ValidationReport", "Violation", "branch_entropy", "consume_file", "coverage_count",
     "decode_event", "encode_event", "iter_trace", "load_trace", "local_entropy", "read_trace", "shannon_entropy",
-    "validate_stream", "write_trace",
+    "validate_stream", "write_trace", "read_columnar", "write_columnar",
     "AiwcError", "AiwcReport", "Barrier", "Branch", "ColumnarTrace", "DerivedMetrics", "DeviceError", "DistStats",
     "EmptyHistogram", "EmptySample", "IncompatibleReports", "Instruction", "InvalidSkip", "InvalidStream",
     "KernelAccumulator", "KernelBegin", "KernelEnd", "MalformedEvent", "Memory", "NoBranches", "SchemaError",

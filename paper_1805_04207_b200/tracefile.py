@@ -11,6 +11,12 @@ whitespace and the rejection rules and messages stay the reference's -- and
 the stream is validated on the way like ``consume``'s StreamChecker.  Errors
 come out in stream order as the reference's lazy ``consume(iter_trace(fp))``
 would raise them (cli.py:130-152).
+
+``write_columnar`` / ``read_columnar`` are the binary columnar on-disk form the
+survey pairs with the parser: the two columns as they sit in device memory
+behind a small JSON header, memory-mapped on load (no parsing; the columns are
+untrusted and the engine checks the stream invariants inside its pass).
+``consume_file`` recognises them by their magic.
 """
 
 from __future__ import annotations
@@ -246,6 +252,72 @@ def fast_trace(path: str, threads: int | None = None) -> ColumnarTrace | None:
                          validated=False, class_counts=tuple(out["counts"]))
 
 
+COLUMNAR_MAGIC = b"AIWCCOL1"
+_COL_ALIGN = 64
+
+
+def write_columnar(tr: ColumnarTrace, path: str) -> None:
+    """The binary columnar file of one trace: magic, u64 header length, a JSON
+    header (launch, opcode dictionary, extra groups, declared statistics), then the
+    kind bytes and the little-endian u64 payloads, each 64-byte aligned."""
+    t = tr.to_numpy()
+    kind = np.ascontiguousarray(t.kind, dtype=np.uint8)
+    payload = np.ascontiguousarray(t.payload).view(np.uint64)
+    if kind.shape != payload.shape:
+        raise ValueError("kind and payload columns differ in length")
+    head = json.dumps({"n_events": int(kind.shape[0]), "kernel_name": t.kernel_name, "invocation": int(t.invocation),
+                       "global_size": [int(x) for x in t.global_size], "local_size": [int(x) for x in t.local_size],
+                       "opcodes": list(t.opcodes), "extra_groups": [[int(x) for x in g] for g in t.extra_groups],
+                       "addr_stats": [int(x) for x in t.addr_stats] if t.addr_stats is not None else None,
+                       "class_counts": [int(x) for x in t.class_counts] if t.class_counts is not None else None},
+                      separators=(",", ":")).encode("utf-8")
+
+    def pad(n: int) -> bytes:
+        return b"\0" * ((-n) % _COL_ALIGN)
+
+    with open(path, "wb") as fp:
+        pre = COLUMNAR_MAGIC + len(head).to_bytes(8, "little") + head
+        fp.write(pre + pad(len(pre)))
+        fp.write(kind.tobytes())
+        fp.write(pad(kind.nbytes))
+        fp.write(payload.astype("<u8", copy=False).tobytes())
+
+
+def is_columnar_file(path: str) -> bool:
+    with open(path, "rb") as fp:
+        return fp.read(len(COLUMNAR_MAGIC)) == COLUMNAR_MAGIC
+
+
+def read_columnar(path: str) -> ColumnarTrace:
+    """A binary columnar file as an untrusted ColumnarTrace over memory-mapped columns
+    (copy-on-write maps: the file is never written)."""
+    size = os.path.getsize(path)
+    with open(path, "rb") as fp:
+        pre = fp.read(len(COLUMNAR_MAGIC) + 8)
+        if len(pre) < len(COLUMNAR_MAGIC) + 8 or pre[:len(COLUMNAR_MAGIC)] != COLUMNAR_MAGIC:
+            raise ValueError(f"{path}: not a columnar trace file")
+        hlen = int.from_bytes(pre[len(COLUMNAR_MAGIC):], "little")
+        if hlen > size:
+            raise ValueError(f"{path}: truncated columnar header")
+        try:
+            h = json.loads(fp.read(hlen).decode("utf-8"))
+        except (UnicodeDecodeError, json.JSONDecodeError) as exc:
+            raise ValueError(f"{path}: bad columnar header ({exc})") from None
+    n = int(h["n_events"])
+    k_off = len(pre) + hlen
+    k_off += (-k_off) % _COL_ALIGN
+    p_off = k_off + n
+    p_off += (-p_off) % _COL_ALIGN
+    if n < 0 or p_off + 8 * n > size:
+        raise ValueError(f"{path}: truncated columnar file ({size} bytes, {n} events declared)")
+    kind = np.memmap(path, dtype=np.uint8, mode="c", offset=k_off, shape=(n,)) if n else np.zeros(0, np.uint8)
+    payload = np.memmap(path, dtype="<u8", mode="c", offset=p_off, shape=(n,)) if n else np.zeros(0, np.uint64)
+    return ColumnarTrace(kind, payload, h["kernel_name"], int(h["invocation"]), tuple(h["global_size"]),
+                         tuple(h["local_size"]), list(h["opcodes"]), [tuple(g) for g in h["extra_groups"]],
+                         tuple(h["addr_stats"]) if h.get("addr_stats") is not None else None, validated=False,
+                         class_counts=tuple(h["class_counts"]) if h.get("class_counts") is not None else None)
+
+
 def consume_file(path: str, *, max_entries: int | None = None, device: int | None = None):
     """``consume(iter_trace(open(path)))`` without per-event Python objects.
 
@@ -258,6 +330,8 @@ def consume_file(path: str, *, max_entries: int | None = None, device: int | Non
     from .metrics import KernelAccumulator, consume, default_entry_cap, run_engine
 
     cap = default_entry_cap() if max_entries is None else max_entries
+    if is_columnar_file(path):  # binary columns: no parsing, checked inside the engine's pass
+        return consume(read_columnar(path), max_entries=cap, device=device)
     fast = fast_trace(path)
     if fast is not None:
         # canonical files: parsed in parallel, checked on the device; an invalid stream is

@@ -209,3 +209,67 @@ def test_fast_parse_declines_what_the_walker_must_decide(tmp_path):
         path = tmp_path / f"{name}.aiwctrace"
         _write(path, lines)
         assert fast_trace(str(path), 4) is None, name
+
+
+@pytest.mark.parametrize("name", ["wavefront_big", "bfs_flags", "offgrid_groups", "branch_streams_per_group", "single_item_no_barriers"])
+def test_columnar_file_round_trip(name, tmp_path):
+    """write_columnar / read_columnar: the columns and the launch metadata come back
+    exactly, memory-mapped and untrusted."""
+    from paper_1805_04207_b200.tracefile import is_columnar_file, read_columnar, write_columnar
+
+    cases = {c["name"]: t for c, t in golden_cases() if t is not None}
+    if name not in cases:
+        pytest.skip(f"no golden trace {name}")
+    tr = cases[name]
+    path = str(tmp_path / "t.aiwcc")
+    write_columnar(tr, path)
+    assert is_columnar_file(path) and os.path.getsize(path) % 8 == 0
+    got = read_columnar(path)
+    assert not got.validated
+    assert np.array_equal(np.asarray(got.kind), np.asarray(tr.kind))
+    assert np.array_equal(np.asarray(got.payload).view(np.uint64), np.asarray(tr.payload).view(np.uint64))
+    assert (got.kernel_name, got.invocation, tuple(got.global_size), tuple(got.local_size)) == \
+        (tr.kernel_name, tr.invocation, tuple(tr.global_size), tuple(tr.local_size))
+    assert got.opcodes == list(tr.opcodes) and got.extra_groups == [tuple(g) for g in tr.extra_groups]
+    assert got.addr_stats == (tuple(tr.addr_stats) if tr.addr_stats is not None else None)
+
+
+def test_columnar_file_rejects_damage(tmp_path):
+    from paper_1805_04207_b200.tracefile import read_columnar, write_columnar
+
+    tr = next(t for c, t in golden_cases() if t is not None and t.n_events > 100)
+    path = tmp_path / "t.aiwcc"
+    write_columnar(tr, str(path))
+    data = path.read_bytes()
+    (tmp_path / "short.aiwcc").write_bytes(data[:-9])
+    with pytest.raises(ValueError, match="truncated"):
+        read_columnar(str(tmp_path / "short.aiwcc"))
+    (tmp_path / "magic.aiwcc").write_bytes(b"X" + data[1:])
+    with pytest.raises(ValueError, match="not a columnar"):
+        read_columnar(str(tmp_path / "magic.aiwcc"))
+    (tmp_path / "head.aiwcc").write_bytes(data[:16] + b"X" + data[17:])
+    with pytest.raises(ValueError, match="bad columnar header"):
+        read_columnar(str(tmp_path / "head.aiwcc"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["wavefront_big", "bfs_flags", "random31337_4", "branch_streams_per_group"])
+def test_consume_columnar_file_matches_reference(name, tmp_path):
+    """consume_file on the binary columnar form: the reference's report; a damaged
+    stream inside a columnar file raises InvalidStream (the engine checks it)."""
+    from paper_1805_04207_b200 import InvalidStream, finalize, report_to_dict
+    from paper_1805_04207_b200.tracefile import consume_file, write_columnar
+    from paper_1805_04207_b200.trace import ColumnarTrace
+
+    c, tr = {c["name"]: (c, t) for c, t in golden_cases() if t is not None}[name]
+    path = str(tmp_path / "t.aiwcc")
+    write_columnar(tr, path)
+    rep = report_to_dict(finalize(consume_file(path, max_entries=1 << 40)))
+    assert_report_matches(rep, {k: v for k, v in c["report"].items() if k not in DERIVED})
+    k = np.array(tr.kind, dtype=np.uint8).copy()
+    k[-1] = 0x40  # kernel_end -> wg_begin
+    bad = ColumnarTrace(k, tr.payload, tr.kernel_name, tr.invocation, tr.global_size, tr.local_size, tr.opcodes,
+                        tr.extra_groups)
+    write_columnar(bad, path)
+    with pytest.raises(InvalidStream):
+        consume_file(path, max_entries=1 << 40)
