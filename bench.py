@@ -344,7 +344,7 @@ def run_ours(args) -> None:
     n_total = config["events"]
     stream = torch.cuda.current_stream(dev)
 
-    n_streams = max(1, args.streams)
+    n_streams = max(1, args.streams if args.streams is not None else (3 if world == 1 else 1))
     if not sharded:
         # one engine context per CUDA stream; with several, concurrent host threads
         # each push whole trace -> report steps (the reference allows distinct
@@ -616,8 +616,9 @@ def main():
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N>1: weak = every rank a full-size shard (N-times larger trace); strong = one fixed trace")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=3,
-                    help="N=1: engine contexts / CUDA streams with whole steps in flight concurrently")
+    ap.add_argument("--streams", type=int, default=None,
+                    help="engine contexts / CUDA streams with whole steps in flight concurrently (default 3 at "
+                         "N=1; 1 at N>1, where each would add an NCCL communicator driven from its own thread)")
     ap.add_argument("--no-e2e", action="store_true", help="device-resident timing only (profiling runs)")
     ap.add_argument("--no-stream-check", action="store_true", help="measurement: steps without the in-pass checks")
     args = ap.parse_args()
