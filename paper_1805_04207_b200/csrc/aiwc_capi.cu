@@ -1042,7 +1042,9 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     ctx->state_ok = h.state_runs_n <= ctx->state_cap;
   }
   // every wi_begin set its own (group, lid) bit: fewer set bits than begins = a duplicate
+#if !defined(AIWC_ABL) || !(AIWC_ABL & 128)  // (measurement builds without the duplicate-begin REDs)
   if (ctx->stream_checked && ctx->info.n_events && h.dup_set != h.n_wib) h.flags |= F_STREAM;
+#endif
   if (h.flags & F_STREAM) {
     fail(ctx, AIWC_ERR_INVALID_STREAM, "stream invariant violated (aiwc_validate locates the first violation)");
     return AIWC_ERR_INVALID_STREAM;
