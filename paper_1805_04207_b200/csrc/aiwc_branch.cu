@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(BT_T, 3) bw_pass_kernel(const uint64_t* __rest
             if ((fl & F_PREFIX) && kk < H) {
               const uint32_t d = atomicAdd(&sm.ndef, 1u);
               if (d < (uint32_t)BW_DEF_CAP) mydef[d] = bw_def(t0 + p, s, kk, hist, t);
+              else overflow = true;  // (cannot happen: < H prefix records per site) -> the sort path
             } else if (kk >= H) {
               out[q] = (hist << 1) | t;
             }
