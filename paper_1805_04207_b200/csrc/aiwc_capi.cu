@@ -960,12 +960,20 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
     if (ctx->dense) {
       const uint64_t chunks = (ctx->am.n_keys + 1023) / 1024;
       const uint32_t nct = (uint32_t)std::min<uint64_t>(chunks, ctx->n_parts);
-      launch_dense_stats(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, ctx->am.k, M, st,
-                         P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s);
       // the per-key state as runs for a later state merge -- tables up to 512 MB (a sweep of a
       // larger table would cost a sizeable part of its ingest; such merges re-ingest)
-      if (ctx->info.export_state && !ctx->remap_pay.p &&
-          dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8) <= (512ull << 20)) {
+      const bool export_runs = ctx->info.export_state && !ctx->remap_pay.p &&
+                               dense_alloc_keys(ctx->am.n_keys) * (ctx->dense32 ? 4 : 8) <= (512ull << 20);
+      // Without a later reader, tables of >= 1 GiB are zeroed by the statistics pass as it
+      // reads them (C3: step 12.04 -> 11.64 ms): a separate clear of that size competes
+      // with the next trace's memory-bound ingest.  Smaller tables keep the side-stream
+      // clear, which hides behind compute-bound passes (C2: fused 0.988 vs 0.969 ms).
+      const size_t tab_bytes = (size_t)ctx->am.n_keys * (ctx->dense32 ? 4 : 8);
+      const bool clear_in_stats = !export_runs && tab_bytes >= (1ull << 30);
+      launch_dense_stats(ctx->dtab.p, ctx->dense32, ctx->am.n_keys, ctx->am.k, M, st,
+                         P<double>(ctx->partials), nct, P<uint64_t>(ctx->lvl0_ovf), s, nullptr, 0, 0, 1,
+                         clear_in_stats);
+      if (export_runs) {
         // one pass, no round trip: runs are claimed chunk by chunk into a buffer of a
         // quarter run per key (runs that do not compress the table that much -- random
         // accesses -- overflow it and the state is dropped: such merges re-ingest)
@@ -977,11 +985,19 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
         ctx->state_ok = true;  // confirmed against the claimed count after the state read below
         ctx->kernels += 1;
       }
-      // the table is clean again for the next trace: clear it on the side stream now
-      CK(cudaEventRecord(ctx->fork_ev, s));
-      CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
-      CK(cudaMemsetAsync(ctx->dtab.p, 0, ctx->dtab_used, ctx->aux));
-      CK(cudaEventRecord(ctx->join_ev, ctx->aux));
+      // the table is clean again for the next trace: zeroed by the statistics pass up to
+      // n_keys (the words after it -- the sentinel slot, allocation padding -- here), or
+      // cleared on the side stream now
+      if (clear_in_stats) {
+        if (ctx->dtab_used > tab_bytes)
+          CK(cudaMemsetAsync(reinterpret_cast<uint8_t*>(ctx->dtab.p) + tab_bytes, 0, ctx->dtab_used - tab_bytes, s));
+        CK(cudaEventRecord(ctx->join_ev, s));
+      } else {
+        CK(cudaEventRecord(ctx->fork_ev, s));
+        CK(cudaStreamWaitEvent(ctx->aux, ctx->fork_ev, 0));
+        CK(cudaMemsetAsync(ctx->dtab.p, 0, ctx->dtab_used, ctx->aux));
+        CK(cudaEventRecord(ctx->join_ev, ctx->aux));
+      }
       ctx->dtab_clean = ctx->dtab_used;
       launch_entropy_finish(st, P<double>(ctx->partials), nct, M, ctx->am.k, s);
       ctx->kernels += 2;

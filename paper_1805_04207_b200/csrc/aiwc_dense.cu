@@ -92,8 +92,10 @@ __device__ __forceinline__ void decode<unsigned long long>(unsigned long long e,
   c = lo + hi; r = lo != 0; w = hi != 0;
 }
 
-template <typename E>
-__global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__ tab,
+// CLEAR: the table is zeroed as it is read (each thread stores zeros over the words
+// it just loaded), so the next trace finds it clean without a separate memset pass
+template <typename E, bool CLEAR>
+__global__ void __launch_bounds__(T, 4) dense_stats_kernel(E* tab,
                                                            uint64_t n_keys, int nlev, double m, DevState* st,
                                                            double* partials, uint32_t n_parts,
                                                            unsigned long long* lvl0_ovf, const uint32_t* own_bits,
@@ -125,6 +127,22 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
     } else {
 #pragma unroll
       for (int i = 0; i < K; ++i) c[i] = (k0 + i < n_keys) ? tab[k0 + i] : (E)0;
+    }
+  };
+
+  // CLEAR: zeros over a chunk's words once the fold consumed them (stores issued right
+  // after the loads would wait for them and serialise the loads in flight)
+  auto clear_chunk = [&](uint64_t ch) {
+    if (!CLEAR) return;
+    const uint64_t k0 = ch * CHUNK + (uint64_t)t * K;
+    if (k0 + K <= n_keys) {
+      uint4* p = reinterpret_cast<uint4*>(tab + k0);
+      constexpr int V = K * (int)sizeof(E) / 16;
+#pragma unroll
+      for (int q = 0; q < V; ++q) __stcs(p + q, make_uint4(0u, 0u, 0u, 0u));
+    } else {
+      for (int i = 0; i < K; ++i)
+        if (k0 + i < n_keys) tab[k0 + i] = (E)0;
     }
   };
 
@@ -243,7 +261,8 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
     if (ch + 2 * g < n_chunks) load(ch + 2 * g, n0);
     if (ch + 3 * g < n_chunks) load(ch + 3 * g, n1);
     fold(c0);
-    if (ch + g < n_chunks) fold(c1);
+    clear_chunk(ch);
+    if (ch + g < n_chunks) { fold(c1); clear_chunk(ch + g); }
 #pragma unroll
     for (int i = 0; i < K; ++i) { c0[i] = n0[i]; c1[i] = n1[i]; }
   }
@@ -272,23 +291,35 @@ __global__ void __launch_bounds__(T, 4) dense_stats_kernel(const E* __restrict__
 
 }  // namespace
 
+template <typename E>
+static void dense_stats_launch(void* tab, bool clear, uint32_t n_ctas, size_t smem, cudaStream_t s, uint64_t n_keys,
+                               int nlev, double m, DevState* st, double* partials, unsigned long long* ovf,
+                               const uint32_t* own_bits, uint64_t own_words, uint32_t rank, uint32_t nranks) {
+  E* t = static_cast<E*>(tab);
+  if (clear) {
+    set_smem_once(dense_stats_kernel<E, true>, (int)smem);
+    dense_stats_kernel<E, true><<<n_ctas, T, smem, s>>>(t, n_keys, nlev, m, st, partials, n_ctas, ovf, own_bits,
+                                                        own_words, rank, nranks);
+  } else {
+    set_smem_once(dense_stats_kernel<E, false>, (int)smem);
+    dense_stats_kernel<E, false><<<n_ctas, T, smem, s>>>(t, n_keys, nlev, m, st, partials, n_ctas, ovf, own_bits,
+                                                         own_words, rank, nranks);
+  }
+}
+
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
                         double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s,
-                        const uint32_t* own_bits, uint64_t own_words, uint32_t rank, uint32_t nranks) {
+                        const uint32_t* own_bits, uint64_t own_words, uint32_t rank, uint32_t nranks, bool clear) {
   const int nlev = k >= 10 ? 1 : 11 - (int)k;
   const size_t smem = (size_t)nlev * CBINS * sizeof(uint32_t);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(lvl0_ovf);
-  if (e32) {
-    set_smem_once(dense_stats_kernel<uint32_t>, (int)smem);
-    dense_stats_kernel<uint32_t><<<n_ctas, T, smem, s>>>(static_cast<const uint32_t*>(tab), n_keys, nlev,
-                                                         (double)total_m, st, partials, n_ctas, ovf,
-                                                         own_bits, own_words, rank, nranks);
-  } else {
-    set_smem_once(dense_stats_kernel<unsigned long long>, (int)smem);
-    dense_stats_kernel<unsigned long long><<<n_ctas, T, smem, s>>>(static_cast<const unsigned long long*>(tab),
-                                                                   n_keys, nlev, (double)total_m, st, partials,
-                                                                   n_ctas, ovf, own_bits, own_words, rank, nranks);
-  }
+  void* t = const_cast<void*>(tab);
+  if (e32)
+    dense_stats_launch<uint32_t>(t, clear && !own_bits, n_ctas, smem, s, n_keys, nlev, (double)total_m, st, partials,
+                                 ovf, own_bits, own_words, rank, nranks);
+  else
+    dense_stats_launch<unsigned long long>(t, clear && !own_bits, n_ctas, smem, s, n_keys, nlev, (double)total_m, st,
+                                           partials, ovf, own_bits, own_words, rank, nranks);
 }
 
 }  // namespace aiwc

@@ -294,7 +294,8 @@ void launch_width_list(const unsigned long long* count, const unsigned long long
 void launch_dense_stats(const void* tab, bool e32, uint64_t n_keys, uint32_t k, uint64_t total_m, DevState* st,
                         double* partials, uint32_t n_ctas, uint64_t* lvl0_ovf, cudaStream_t s,
                         const uint32_t* own_bits = nullptr, uint64_t own_words = 0, uint32_t rank = 0,
-                        uint32_t nranks = 1);  // own_bits: only the chunks `rank` owns
+                        uint32_t nranks = 1,   // own_bits: only the chunks `rank` owns
+                        bool clear = false);   // zero the table while reading it (not with own_bits)
 // key-block bins (aiwc_bins.cu)
 void launch_zone_sample(const uint8_t* kind, const uint64_t* payload, uint64_t n, const AddrMap& am,
                         uint32_t zone_shift, unsigned int* zone_counts, unsigned long long* zones_out,
