@@ -325,6 +325,14 @@ __device__ __forceinline__ void do_close(LocalSmem& L, const IngestArgs& a, uint
                                          unsigned long long& flags) {
   const bool bar = gz >> 31, byres = (gz >> 30) & 1u;
   const uint32_t gseq = gz & 0x3FFFFFFFu;
+  if (a.dup_bits) {
+    // in-pass check, per segment: the opener's local id inside the group, and for a
+    // wi_begin-opened segment its (group, lid) bit (RED, no round trip); finalize
+    // compares the set bits with the begins
+    const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + lid;
+    if (lid >= a.local_volume || !gseq || slot >= a.dup_len) flags |= F_STREAM;
+    else if (!byres && !(AIWC_ABL & 128)) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
+  }
   if (a.wi_rules && !(AIWC_ABL & 256)) {  // per-work-item order (stream check of barrier / resume traces)
     const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + lid;
     if (gseq == 0 || slot >= a.dup_len) {
@@ -872,16 +880,10 @@ __global__ void __launch_bounds__(TPB, 2)
       const uint64_t p = PAY(j);
       if (CHECK && !(AIWC_ABL & 64)) {  // the payload rules (the sequence rules were checked on the masks above)
         bool bad = false;
-        if (kk == AIWC_K_WI_BEGIN) {
-          // wi_begin for an already-started work-item: every begin sets its (group, lid)
-          // bit (RED, no round trip); finalize compares the set bits with the begins
-          const uint64_t slot = (uint64_t)(gseq - 1) * a.local_volume + p;
-          bad = p >= a.local_volume || !gseq || slot >= a.dup_len;
-          if (!bad && !(AIWC_ABL & 128)) atomicOr(&a.dup_bits[slot >> 5], 1u << (slot & 31));
-        } else if (kk == AIWC_K_WI_END) {
-          bad = p != lid || p >= a.local_volume;
-        } else if (kk == AIWC_K_WI_RESUME) {
-          bad = p >= a.local_volume;
+        // (an opener's local id range and a wi_begin's duplicate-begin bit are handled at
+        // the segment's close, do_close: the masks flag a segment never closed in its group)
+        if (kk == AIWC_K_WI_END) {
+          bad = p != lid;
         } else if (kk == AIWC_K_WG_BEGIN) {
           bad = (p >> 31) != 0;
         } else if (kk == AIWC_K_WG_END) {
