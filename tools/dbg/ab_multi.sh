@@ -10,7 +10,7 @@ for c in $CFGS; do
       env $envs timeout 300 python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline --streams 1 2>&1 | \
         python -c "import json,sys
 try:
-  d=json.loads(sys.stdin.readline()); print(round(d['ms_per_step'],4), round(d['phases_ms']['ingest'],4))
+  d=json.loads(sys.stdin.readline()); print(round(d['ms_per_step'],4), round(d['phases_ms']['ingest'],4), round(d['phases_ms']['pass1'],4))
 except Exception as e: print('ERR', e)" >> $OUT
     done
   done
