@@ -255,6 +255,7 @@ struct aiwc_ctx {
     uint64_t rows = 0;
     CUtensorMap km{}, pm{};
     bool opc_big = false, with_stats = false;
+    bool light = false;  // pass 1 ran light (a dense table, no branches predicted from the declaration)
     size_t clean_prev = 0;
     uint32_t G = 0, tpc = 0;
   } pend;
@@ -559,6 +560,7 @@ static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payl
   // Bounded waste when the trace later takes another path: <= 4 keys / event + 2^20.
   ctx->pre_zeroed = 0;
   const bool shard = ctx->opts.flags & AIWC_OPT_SHARD;
+  bool light = false;
   if (n && !with_stats && info->addr_min <= info->addr_max && !shard) {
     const uint64_t b0 = info->addr_min & ~1023ull, vary = info->addr_and ^ info->addr_or;
     const uint32_t k0 = vary ? std::min<uint32_t>((uint32_t)__builtin_ctzll(vary), 32u) : 0u;
@@ -566,6 +568,11 @@ static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payl
     if (sk + 1 < DENSE_MAX_KEYS && dense_alloc_keys(sk + 1) * 4 <= ctx->opts.dense_budget_bytes &&
         sk + 1 <= 4 * n + (1ull << 20)) {
       const size_t tb = (size_t)dense_alloc_keys(sk + 1) * 4;  // + the sentinel slot of invalid addresses
+      // a dense table and no branches: nothing is staged, so pass 1 need not count
+      // instructions or branches (finalize checks the declared instruction total against
+      // the opcode counts; a wrong prediction re-runs the full pass 1 in ingest_finish)
+      light = declared && info->n_branches == 0 && ctx->bins_off && info->n_reads + info->n_writes > 0 &&
+              info->n_opcodes <= (uint32_t)MAX_SMALL_LIST;  // (instructions: checked from the opcode counts)
       if (ctx->dtab_clean >= tb && ctx->dtab.cap >= tb) {
         ctx->pre_zeroed = ctx->dtab_clean;  // cleared after the previous trace (join_ev)
       } else {
@@ -590,7 +597,7 @@ static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payl
   if (n) {
     CK(cudaEventRecord(ctx->p1_ev, s));  // the columns (and DevState init) are ready here
     ctx->mark(AIWC_PH_PASS1, 0, s);
-    launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s);
+    launch_pass1(kind, payload, n, G, tpc, with_stats, P<RangeSum>(ctx->ranges), st, s, light);
     ctx->mark(AIWC_PH_PASS1, 1, s);
     ctx->kernels += 1;
     CK(cudaGetLastError());
@@ -614,7 +621,7 @@ static int ingest_begin(aiwc_ctx* ctx, const uint8_t* kind, const uint64_t* payl
   ctx->pend.kind = kind; ctx->pend.payload = payload; ctx->pend.rows = rows;
   ctx->pend.km = km; ctx->pend.pm = pm;
   ctx->pend.opc_big = opc_big; ctx->pend.with_stats = with_stats; ctx->pend.clean_prev = clean_prev;
-  ctx->pend.G = G; ctx->pend.tpc = tpc;
+  ctx->pend.G = G; ctx->pend.tpc = tpc; ctx->pend.light = light;
   return AIWC_OK;
 }
 
@@ -689,6 +696,12 @@ static int ingest_finish(aiwc_ctx* ctx, uint64_t amin, uint64_t amax, uint64_t a
     }
   }
   const bool stage = !ctx->dense || ctx->n_br > 0;
+  if (ctx->pend.light && (stage || shard)) {  // the light pass 1 was mispredicted: the staging needs its counts
+    CK(cudaMemsetAsync(st->p1_tot, 0, sizeof(st->p1_tot), s));
+    launch_pass1(kind, payload, n, G, tpc, ctx->pend.with_stats, P<RangeSum>(ctx->ranges), st, s, false);
+    ctx->kernels += 1;
+    ctx->pend.light = false;
+  }
 
   // ---- buffers ----
   // an ITB / IPT sample >= HBINS spans >= HBINS distinct instructions: that bounds both overflow lists
@@ -1040,7 +1053,12 @@ static int finalize_local(aiwc_ctx* ctx, aiwc_result* out, void* stream) {
   DevState& h = *ctx->h_state;
   if (ctx->one_pass) {  // the declared class totals against what the pass counted
     const aiwc_trace_info& in = ctx->info;
-    const bool same = h.p1_tot[0] == in.n_instr && h.p1_tot[1] == in.n_reads && h.p1_tot[2] == in.n_writes &&
+    unsigned long long n_in = h.p1_tot[0];
+    if (ctx->pend.light) {  // light pass 1: every instruction event landed in an opcode counter
+      n_in = 0;
+      for (uint32_t i = 0; i < in.n_opcodes; ++i) n_in += h.opc_small[i];
+    }
+    const bool same = n_in == in.n_instr && h.p1_tot[1] == in.n_reads && h.p1_tot[2] == in.n_writes &&
                       h.p1_tot[3] == in.n_branches && h.p1_tot[4] == in.n_groups &&
                       (h.p1_tot[5] != 0) == (in.any_barrier_or_resume != 0);
     if (!same) return fail(ctx, AIWC_ERR_ARGUMENT, "declared class counts differ from the trace");

@@ -69,16 +69,19 @@ __device__ __forceinline__ void load_kind16(const uint8_t* kind, uint64_t e0, ui
 struct KindCounts {
   uint32_t instr = 0, rd = 0, wr = 0, br = 0, wgb = 0, bres = 0;
   // mb*: boundary bits (nibble bit 0), mw*: wg_begin bits (group bit without the variant bit)
+  template <bool LIGHT>
   __device__ __forceinline__ void add(const uint32_t w[4], uint32_t& mb0, uint32_t& mb1, uint32_t& mw0,
                                       uint32_t& mw1, uint32_t& me0, uint32_t& me1) {
     const uint32_t L0 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
     const uint32_t L1 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
     const uint32_t H0 = ((w[0] >> 4) & 0x0F0F0F0Fu) | (w[1] & 0xF0F0F0F0u);
     const uint32_t H1 = ((w[2] >> 4) & 0x0F0F0F0Fu) | (w[3] & 0xF0F0F0F0u);
-    instr += __popc(L0 & 0x11111111u) + __popc(L1 & 0x11111111u);
     rd += __popc(L0 & 0x22222222u) + __popc(L1 & 0x22222222u);
     wr += __popc(L0 & 0x44444444u) + __popc(L1 & 0x44444444u);
-    br += __popc(L0 & 0x88888888u) + __popc(L1 & 0x88888888u);
+    if (!LIGHT) {  // (light: instructions are checked from the opcode counts, branches must be absent)
+      instr += __popc(L0 & 0x11111111u) + __popc(L1 & 0x11111111u);
+      br += __popc(L0 & 0x88888888u) + __popc(L1 & 0x88888888u);
+    }
     mb0 = H0 & 0x11111111u;
     mb1 = H1 & 0x11111111u;
     mw0 = H0 & ~(H0 >> 1) & 0x44444444u;
@@ -100,6 +103,12 @@ __device__ __forceinline__ long long last_nib_event(long long e0, uint32_t m0, u
   return -1;
 }
 
+// LIGHT (declared totals, a dense table, no branches: nothing is staged): no
+// instruction or branch counts -- finalize checks the declared instruction total
+// against the opcode counts, and a branch makes the unstaged ingest fail
+// (F_BAD_KIND); the carries use instr_after, which is the whole sub-range's
+// instruction count when it holds no boundary.
+template <bool LIGHT>
 __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __restrict__ kind,
                                                            const uint64_t* __restrict__ payload, uint64_t n,
                                                            uint32_t tiles_per_cta, bool with_stats,
@@ -123,7 +132,7 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
     for (int u = 0; u < U; ++u) {
       const uint64_t e0 = base + 16 * u;
       uint32_t mb0, mb1, mw0, mw1, me0, me1;
-      kc.add(w[u], mb0, mb1, mw0, mw1, me0, me1);
+      kc.add<LIGHT>(w[u], mb0, mb1, mw0, mw1, me0, me1);
       if (mb0 | mb1) { lb_e0 = (long long)e0; lb_m0 = mb0; lb_m1 = mb1; }
       if (mw0 | mw1) { lw_e0 = (long long)e0; lw_m0 = mw0; lw_m1 = mw1; }
       if (me0 | me1) { le_e0 = (long long)e0; le_m0 = me0; le_m1 = me1; }
@@ -227,8 +236,11 @@ __global__ void __launch_bounds__(P1_THREADS) pass1_kernel(const uint8_t* __rest
 }
 
 void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t n_ranges, uint32_t tiles_per_cta,
-                  bool with_stats, RangeSum* out, DevState* st, cudaStream_t s) {
-  pass1_kernel<<<n_ranges * P1_SUB, P1_THREADS, 0, s>>>(kind, payload, n, tiles_per_cta, with_stats, out, st);
+                  bool with_stats, RangeSum* out, DevState* st, cudaStream_t s, bool light) {
+  if (light)
+    pass1_kernel<true><<<n_ranges * P1_SUB, P1_THREADS, 0, s>>>(kind, payload, n, tiles_per_cta, with_stats, out, st);
+  else
+    pass1_kernel<false><<<n_ranges * P1_SUB, P1_THREADS, 0, s>>>(kind, payload, n, tiles_per_cta, with_stats, out, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -475,7 +487,8 @@ __global__ void __launch_bounds__(TPB, 2)
       jb = max(jb, (long long)red[w][4]); lw = max(lw, (long long)red[w][5]); lwe = max(lwe, (long long)red[w][6]);
     }
     uint64_t s_in = 0;  // instructions after the last boundary: after(jb) + instrs of later sub-ranges
-    for (uint32_t j = (uint32_t)(jb + 1) + t; j < c; j += TPB) s_in += a.ranges[j].n_instr;
+    // (instr_after = all of a sub-range's instructions when it holds no boundary)
+    for (uint32_t j = (uint32_t)(jb + 1) + t; j < c; j += TPB) s_in += a.ranges[j].instr_after;
     s_in = warp_sum(s_in);
     __syncthreads();
     if (lane == 0) red[warp][0] = s_in;
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(TPB, 2)
     for (uint32_t j = c; j < c + (uint32_t)warp; ++j) {
       const RangeSum& r = a.ranges[j];
       if (r.last_bnd >= 0) { lbpos = r.last_bnd; after = r.instr_after; }
-      else after += r.n_instr;
+      else after += r.instr_after;
       if (r.last_wgb >= 0) lw = r.last_wgb;
       if (r.last_wge >= 0) lwe = r.last_wge;
       s_rd += r.n_rd; s_wr += r.n_wr; s_br += r.n_br; s_wgb += r.n_wgb;

@@ -278,7 +278,8 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 // ---- host-side launchers (defined in the .cu files) -------------------------
 void launch_pass1(const uint8_t* kind, const uint64_t* payload, uint64_t n, uint32_t n_ranges,
-                  uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s);
+                  uint32_t tiles_per_cta, bool with_stats, RangeSum* out, DevState* st, cudaStream_t s,
+                  bool light = false);
 cudaError_t launch_ingest(const IngestArgs& a, const CUtensorMap& kmap, const CUtensorMap& pmap, uint32_t n_ctas,
                           bool dense, bool stage, cudaStream_t s);  // smem grows by 8 * a.smem_keys
 // hot-key window: samples memory events, writes the most frequent 1024-key block of the
