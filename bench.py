@@ -452,7 +452,8 @@ def run_ours(args) -> None:
     unchecked_ingest_ms = None
     if not sharded and not args.no_stream_check:
         uinfo = trace_info(tr, check=False)
-        uctx, ucs, ur, ukptr, upptr, _ = lanes[0]
+        uctx, ucs, _, ukptr, upptr, _ = lanes[0]
+        ur = _native.Result()  # (lane 0's own result keeps the checked step's certification)
         ui = _native.PHASES.index("ingest")
         u_ph = []
 

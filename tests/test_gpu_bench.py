@@ -35,6 +35,9 @@ def test_bench_contract_and_sharded_path_agree():
         assert key in single, key
     assert single["value"] > 0 and single["e2e"]["value"] > 0 and single["gpu_launches"] > 0
     assert single["roofline"]["bound"] == "hbm" and 0 < single["roofline"]["frac"] < 1
+    # the timed steps checked the stream inside the pass and certified it
+    assert single["stream_check"]["in_pass"] and single["stream_check"]["certified"] is True
+    assert single["roofline"]["frac"] <= single["roofline"]["frac_without_stream_check"] < 1
     e2e = single["e2e"]
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["bare_h2d_gbs"] > 0 and 0 < e2e["link_frac"] < 1.2
     sharded = _line([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
